@@ -1,0 +1,196 @@
+"""Oracle steps O5 (pre-communication reordering) and O7 (post-communication
+reordering) for AllReduce, ReduceScatter and All-to-All.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md:385-386: "the reordered output is first reshaped into a column of tiles
+(row major) before communication.  For the inter-tile data contiguity, the tile
+indices are reordered based on their execution order".
+
+  AR: unit = tile.  Tile at execution position p goes to slot p
+      (reading R2: slot = execution position), each slot BM*BN
+      contiguous elements, row-major inside the slot.
+      Layout "rowband" (H11a): when the order is a row-major raster and
+      every group boundary falls on a whole tile-row, the slot layout is replaced
+      by the identity (the buffer IS row-major C); each group is then a
+      contiguous row band.  Both layouts are valid AR reorderings.
+  RS: unit = subtile of h = BM/n rows.  Inside group j (positions
+      [ps, pe), G = pe - ps), chunk k (the part ReduceScatter delivers to rank k)
+      holds the k-th subtile of every tile of the group, tiles in execution
+      order:  buf[ps*BM*BN + k*G*h*BN + q*h*BN + a'*BN + b]
+                 = Y[i*BM + k*h + a', j*BN + b],   q = p - ps.
+  A2A: unit = subtoken (one row of one tile, BN elements).  One
+      memory pool per destination rank; subtokens are appended in execution
+      order (p ascending, then row inside the tile ascending).  Group j's
+      subtokens form one contiguous range of every pool.
+
+Pins (tests/test_oracle_reorder.py): post(pre(X)) == X bit-exactly
+("the output in (d) is the same as (a)"); every element lands in
+exactly one buffer position (bijection); group ranges contiguous and ordered
+(monotonicity); RS: each row complete on exactly one rank;
+SURVEY g5/g6/g7 worked cases and SPEC.md:145's gathered row order
+[0,1,4,5,2,3,6,7].
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .plan import OracleError, Plan
+
+
+# =========================================================== AllReduce
+def ar_rowband_ok(plan: Plan) -> bool:
+    """Identity layout is valid iff the order is the row-major raster and every
+    group starts on a tile-row boundary (so each group is a row band of C)."""
+    if not np.array_equal(plan.order, np.arange(plan.ntiles)):
+        return False
+    return all(lo % plan.Nt == 0 for lo, _ in plan.ranges)
+
+
+def group_elem_ranges(plan: Plan) -> list[tuple[int, int]]:
+    """Element range [lo, hi) of each group in the AR / RS send buffer."""
+    t = plan.BM * plan.BN
+    return [(lo * t, hi * t) for lo, hi in plan.ranges]
+
+
+def ar_pre(Y: np.ndarray, plan: Plan, layout: str = "slot") -> np.ndarray:
+    """O5 for AllReduce: Y [M, N] -> flat buffer of M*N elements."""
+    BM, BN = plan.BM, plan.BN
+    if layout == "rowband":
+        if not ar_rowband_ok(plan):
+            raise OracleError("rowband layout needs a raster order and tile-row group boundaries")
+        return Y.reshape(-1).copy()
+    buf = np.empty(plan.M * plan.N, dtype=Y.dtype)
+    for p in range(plan.ntiles):
+        i, j = plan.tile_of_position(p)
+        buf[p * BM * BN:(p + 1) * BM * BN] = Y[i * BM:(i + 1) * BM, j * BN:(j + 1) * BN].reshape(-1)
+    return buf
+
+
+def ar_post(buf: np.ndarray, plan: Plan, layout: str = "slot") -> np.ndarray:
+    """O7 for AllReduce: the inverse of ar_pre."""
+    BM, BN = plan.BM, plan.BN
+    if layout == "rowband":
+        return buf.reshape(plan.M, plan.N).copy()
+    Y = np.empty((plan.M, plan.N), dtype=buf.dtype)
+    for p in range(plan.ntiles):
+        i, j = plan.tile_of_position(p)
+        Y[i * BM:(i + 1) * BM, j * BN:(j + 1) * BN] = buf[p * BM * BN:(p + 1) * BM * BN].reshape(BM, BN)
+    return Y
+
+
+# =========================================================== ReduceScatter
+def rs_subtile_rows(plan: Plan, n: int) -> int:
+    if plan.BM % n:
+        raise OracleError(f"tile_m={plan.BM} not divisible by world size {n}")
+    return plan.BM // n
+
+
+def rs_pre(Y: np.ndarray, plan: Plan, n: int) -> np.ndarray:
+    """O5 for ReduceScatter (formula in the module header)."""
+    BM, BN = plan.BM, plan.BN
+    h = rs_subtile_rows(plan, n)
+    buf = np.empty(plan.M * plan.N, dtype=Y.dtype)
+    for ps, pe in plan.ranges:
+        G = pe - ps
+        for p in range(ps, pe):
+            q = p - ps
+            i, j = plan.tile_of_position(p)
+            for k in range(n):
+                off = ps * BM * BN + k * G * h * BN + q * h * BN
+                sub = Y[i * BM + k * h:i * BM + (k + 1) * h, j * BN:(j + 1) * BN]
+                buf[off:off + h * BN] = sub.reshape(-1)
+    return buf
+
+
+def rs_chunk(buf: np.ndarray, plan: Plan, n: int, group: int, k: int) -> np.ndarray:
+    """Chunk k of group `group`: what ReduceScatter on the group range delivers to rank k."""
+    BM, BN = plan.BM, plan.BN
+    h = rs_subtile_rows(plan, n)
+    ps, pe = plan.ranges[group]
+    G = pe - ps
+    off = ps * BM * BN + k * G * h * BN
+    return buf[off:off + G * h * BN]
+
+
+def rs_local_to_global_row(l: int, BM: int, h: int, k: int) -> int:
+    """Rank k's local output row l holds global row floor(l/h)*BM + k*h + (l mod h)
+    (block-cyclic rows R_k, SURVEY.md §8(b) output contract)."""
+    return (l // h) * BM + k * h + (l % h)
+
+
+def rs_post(recv: np.ndarray, plan: Plan, n: int) -> np.ndarray:
+    """O7 for ReduceScatter on one rank: the received buffer (group chunks
+    concatenated in group order, each G*h*BN elements) -> local [M/n, N] rows
+    in block-cyclic order (local row i*h + a' <- tile-row i, subtile row a')."""
+    BM, BN = plan.BM, plan.BN
+    h = rs_subtile_rows(plan, n)
+    out = np.empty((plan.M // n, plan.N), dtype=recv.dtype)
+    for ps, pe in plan.ranges:
+        for p in range(ps, pe):
+            q = p - ps
+            i, j = plan.tile_of_position(p)
+            off = ps * h * BN + q * h * BN
+            out[i * h:(i + 1) * h, j * BN:(j + 1) * BN] = recv[off:off + h * BN].reshape(h, BN)
+    return out
+
+
+# =========================================================== All-to-All
+class A2ASend:
+    """Per-source pools: pools[d] is an array [cnt_d, BN]; meta[d] the list of
+    (row, tile_col) of each subtoken; ranges[d][j] = (start, end) subtoken range
+    of group j in pool d."""
+
+    def __init__(self, n: int, P: int):
+        self.pools = [[] for _ in range(n)]
+        self.meta = [[] for _ in range(n)]
+        self.ranges = [[None] * P for _ in range(n)]
+
+
+def a2a_pre(Y: np.ndarray, plan: Plan, row_dst, n: int) -> A2ASend:
+    """O5 for All-to-All (module header)."""
+    BM, BN = plan.BM, plan.BN
+    row_dst = np.asarray(row_dst).reshape(-1)
+    if row_dst.size != plan.M:
+        raise OracleError("row_dst must give a destination for every output row")
+    if row_dst.size and (row_dst.min() < 0 or row_dst.max() >= n):
+        raise OracleError("row_dst out of range")
+    P = len(plan.ranges)
+    s = A2ASend(n, P)
+    for gj, (ps, pe) in enumerate(plan.ranges):
+        start = [len(s.pools[d]) for d in range(n)]
+        for p in range(ps, pe):
+            i, j = plan.tile_of_position(p)
+            for a in range(BM):
+                row = i * BM + a
+                d = int(row_dst[row])
+                s.pools[d].append(Y[row, j * BN:(j + 1) * BN].copy())
+                s.meta[d].append((row, j))
+        for d in range(n):
+            s.ranges[d][gj] = (start[d], len(s.pools[d]))
+    for d in range(n):
+        s.pools[d] = (np.array(s.pools[d]).reshape(-1, BN) if s.pools[d]
+                      else np.zeros((0, BN), dtype=Y.dtype))
+    return s
+
+
+def a2a_post(recv_parts, sources_meta, sources_row_dst, me: int, N: int, BN: int) -> np.ndarray:
+    """O7 for All-to-All on rank `me`.
+
+    recv_parts: list over (group j, source s) in receive order of
+    (s, subtoken_array) as produced by collectives.alltoall.
+    sources_meta[s]: the (row, tile_col) list of pool s->me (source order).
+    Output: rows grouped by source ascending; within a source, ascending
+    source row (standard all-to-all-v order)."""
+    n = len(sources_row_dst)
+    rows_to_me = [np.flatnonzero(np.asarray(sources_row_dst[s]) == me) for s in range(n)]
+    base = np.concatenate([[0], np.cumsum([len(r) for r in rows_to_me])]).astype(np.int64)
+    rank_of = [{int(r): idx for idx, r in enumerate(rows_to_me[s])} for s in range(n)]
+    out = np.zeros((int(base[-1]), N))
+    consumed = [0] * n
+    for s, chunk in recv_parts:
+        for v in chunk:
+            row, j = sources_meta[s][consumed[s]]
+            consumed[s] += 1
+            out[base[s] + rank_of[s][row], j * BN:(j + 1) * BN] = v
+    return out

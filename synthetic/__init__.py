@@ -1,0 +1,145 @@
+"""Seeded synthetic input generators shared by the tests, the bench and smoke().
+
+This module holds NONE of the method's arithmetic (no tiling, no reordering, no
+GEMM, no collective).  It only draws seeded random inputs with the shapes and
+value distributions of the paper's workloads ("we use randomly
+generated inputs").  Both the CPU oracle (`oracle/`)
+and the CUDA path consume what it returns; neither imports the other.
+
+All matrices are returned as CPU `torch.bfloat16` tensors (row-major,
+contiguous).  A is [M, K_loc] (activations, K-major); Bt is [N, K_loc] (the
+nn.Linear weight layout, K-major), so C = A @ Bt^T.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import torch
+
+__all__ = [
+    "rank_seed",
+    "cell_seed",
+    "normal_bf16",
+    "exact_int_A",
+    "exact_int_B",
+    "float_inputs",
+    "exact_inputs",
+    "random_order",
+    "random_partition",
+    "moe_routing",
+    "random_row_dst",
+]
+
+
+def rank_seed(base: int, tp: int, rank: int) -> int:
+    """Seed recipe of SURVEY.md §8(d): seed = base + 100*TP + rank."""
+    return int(base) + 100 * int(tp) + int(rank)
+
+
+def cell_seed(*parts) -> int:
+    """Deterministic seed from a tuple of cell parameters (sweep cells)."""
+    h = hashlib.sha256(repr(tuple(parts)).encode()).digest()
+    return int.from_bytes(h[:4], "little")
+
+
+def _gen(seed: int) -> torch.Generator:
+    g = torch.Generator()
+    g.manual_seed(int(seed) & 0x7FFFFFFFFFFFFFFF)
+    return g
+
+
+def normal_bf16(shape, std: float, seed: int) -> torch.Tensor:
+    """N(0, std^2) draws rounded to bf16 (torch's own fp32->bf16 conversion)."""
+    x = torch.randn(*shape, generator=_gen(seed), dtype=torch.float32)
+    if std != 1.0:
+        x = x * std
+    return x.to(torch.bfloat16).contiguous()
+
+
+def exact_int_A(M: int, K: int, seed: int, nnz_per_row: int) -> torch.Tensor:
+    """Exact-integer regime: entries in {-1,0,1}, at most
+    `nnz_per_row` nonzeros per row.  The caller picks nnz_per_row so that the
+    nonzeros per output row summed over all ranks stay <= 256, which keeps
+    every partial sum an integer of magnitude <= 256 (exact in bf16 and fp32)."""
+    g = _gen(seed)
+    nnz = max(0, min(int(nnz_per_row), K))
+    A = torch.zeros(M, K, dtype=torch.float32)
+    if nnz > 0 and M > 0:
+        # random column subset per row + random signs
+        keys = torch.rand(M, K, generator=g)
+        cols = keys.argsort(dim=1)[:, :nnz]
+        signs = torch.randint(0, 2, (M, nnz), generator=g).float() * 2 - 1
+        # allow some zeros inside the support too
+        keep = (torch.rand(M, nnz, generator=g) < 0.9).float()
+        A.scatter_(1, cols, signs * keep)
+    return A.to(torch.bfloat16).contiguous()
+
+
+def exact_int_B(N: int, K: int, seed: int) -> torch.Tensor:
+    """Dense {-1,0,1} weights for the exact-integer regime."""
+    g = _gen(seed)
+    B = torch.randint(-1, 2, (N, K), generator=g).float()
+    return B.to(torch.bfloat16).contiguous()
+
+
+def float_inputs(M: int, N: int, K: int, seed: int):
+    """Float regime of SURVEY.md §8(d): A ~ N(0,1) (activations), Bt ~ N(0,0.02^2)
+    (weights), both bf16."""
+    A = normal_bf16((M, K), 1.0, seed * 2 + 1)
+    Bt = normal_bf16((N, K), 0.02, seed * 2 + 2)
+    return A, Bt
+
+
+def exact_inputs(M: int, N: int, K: int, seed: int, nnz_per_row: int):
+    A = exact_int_A(M, K, seed * 2 + 1, nnz_per_row)
+    Bt = exact_int_B(N, K, seed * 2 + 2)
+    return A, Bt
+
+
+def random_order(ntiles: int, seed: int) -> np.ndarray:
+    """A random explicit tile execution order (a permutation), int32."""
+    rng = np.random.default_rng(seed)
+    return rng.permutation(ntiles).astype(np.int32)
+
+
+def random_partition(T: int, seed: int) -> list[int]:
+    """A random composition of T (random communicate/not decision after each
+    wave but the last)."""
+    rng = np.random.default_rng(seed)
+    cuts = [w for w in range(1, T) if rng.random() < 0.5]
+    bounds = [0] + cuts + [T]
+    return [bounds[i + 1] - bounds[i] for i in range(len(bounds) - 1)]
+
+
+def random_row_dst(M: int, n: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, n, size=M).astype(np.int32)
+
+
+def moe_routing(tokens: int, n_experts: int, topk: int, n_ranks: int, seed: int):
+    """Mixtral-style top-k routing (BASELINE.json configs[3]; SURVEY.md ambiguity 20).
+
+    `tokens` tokens are spread evenly over `n_ranks` source ranks (token t lives
+    on rank t // (tokens // n_ranks)).  Router logits ~ N(0,1) from `seed`;
+    each token picks its top-k experts.  Experts are placed one per rank
+    (expert e on rank e % n_ranks).
+
+    Returns a list, per expert rank e, of the int32 array `row_dst` giving the
+    source rank of each row that expert computes; rows are sorted by source
+    rank (then token id), as the dispatch All-to-All would deliver them."""
+    g = _gen(seed)
+    logits = torch.randn(tokens, n_experts, generator=g)
+    top = logits.topk(topk, dim=1).indices.numpy()
+    per_rank = tokens // n_ranks
+    out = []
+    for r in range(n_ranks):
+        experts_here = [e for e in range(n_experts) if e % n_ranks == r]
+        rows = []
+        for t in range(tokens):
+            for e in experts_here:
+                if e in top[t]:
+                    rows.append((t // per_rank, t))
+        rows.sort()
+        out.append(np.array([s for s, _ in rows], dtype=np.int32))
+    return out

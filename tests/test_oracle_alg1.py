@@ -1,0 +1,93 @@
+"""Pins for the Alg. 1 oracle and the design space."""
+import json
+import os
+
+import pytest
+
+from oracle import alg1
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "alg1.json")))
+
+
+def _compositions(T):
+    """Independent enumeration: all tuples of positive ints summing to T."""
+    if T == 0:
+        return [()]
+    return [(first,) + rest for first in range(1, T + 1) for rest in _compositions(T - first)]
+
+
+@pytest.mark.parametrize("T", range(1, 11))
+def test_space_is_all_compositions(T):
+    c = alg1.candidates(T)
+    assert len(c) == 2 ** (T - 1) == len(set(c))
+    assert sorted(c) == sorted(_compositions(T))
+
+
+def test_space_paper_examples():
+    for case in GOLD["space"]:
+        space = alg1.candidates(case["T"])
+        if "unpruned" in case:
+            assert len(space) == case["unpruned"]
+        for m in case.get("members", []):
+            assert tuple(m) in space
+
+
+@pytest.mark.parametrize("T", range(1, 12))
+def test_pruned_space(T):
+    got = alg1.pruned_candidates(T, 2, 4)
+    want = [c for c in _compositions(T) if (T == 1 or (c[0] <= 2 and c[-1] <= 4))]
+    assert sorted(got) == sorted(want)
+    # O(2^(T-2)) bound of PAPER.md:446
+    assert len(got) <= max(1, 2 ** (T - 2)) * 2 * 4
+
+
+@pytest.mark.parametrize("case", GOLD["traces"], ids=lambda c: c["id"])
+def test_hand_traces(case):
+    T, dur, S, tiles = case["T"], case["duration_us"], case["S"], case["tiles"]
+    per = case["per_wave_comm_us"]
+
+    def lat(nbytes):  # 1 byte per tile, linear comm
+        return per * nbytes / S
+
+    for k, want in case["expect"].items():
+        part = tuple(int(x) for x in k.split(","))
+        sizes = alg1.group_bytes(part, S, tiles, 1)
+        assert alg1.predict(part, dur, T, sizes, lat) == pytest.approx(want)
+
+
+def test_single_group_is_gemm_plus_full_comm():
+    curve = [(2 ** 16, 10.0), (2 ** 20, 100.0), (2 ** 26, 400.0)]
+    for T in range(1, 9):
+        sizes = alg1.group_bytes((T,), 64, 64 * T, 65536)
+        full = alg1.interp_latency_us(curve, 64 * T * 65536)
+        assert alg1.predict((T,), 100.0, T, sizes, lambda b: alg1.interp_latency_us(curve, b)) == pytest.approx(100.0 + full)
+
+
+def test_comm_bound_finest_meets_bound():
+    """Linear comm, comm-bound: the all-ones partition attains the PAPER.md:622 bound."""
+    T, dur, per = 6, 30.0, 20.0
+    sizes = alg1.group_bytes((1,) * T, 1, T, 1)
+    t = alg1.predict((1,) * T, dur, T, sizes, lambda b: per * b)
+    assert t == pytest.approx(alg1.perfect_overlap_bound(dur, T, per * T, per))
+
+
+def test_interp_log_linear():
+    curve = [(1024, 10.0), (4096, 30.0)]
+    assert alg1.interp_bandwidth(curve, 1024) == 10.0
+    assert alg1.interp_bandwidth(curve, 2048) == pytest.approx(20.0)   # geometric midpoint
+    assert alg1.interp_bandwidth(curve, 100) == 10.0                   # clamp
+    assert alg1.interp_bandwidth(curve, 1 << 30) == 30.0
+
+
+def test_search_tie_break_and_knee():
+    # infinite bandwidth -> every partition predicts dur; tie -> single group
+    best, t = alg1.search(5, 50.0, lambda G: alg1.group_bytes(G, 1, 5, 1), lambda b: 0.0, prune=False)
+    assert best == (5,) and t == pytest.approx(50.0)
+    # pruned (|G1| <= 2): fewest groups, then lexicographically smallest
+    best, t = alg1.search(5, 50.0, lambda G: alg1.group_bytes(G, 1, 5, 1), lambda b: 0.0)
+    assert best == (1, 4) and t == pytest.approx(50.0)
+    # a curve with a knee: tiny messages are slow -> not the all-ones partition
+    curve = [(2 ** 10, 1.0), (2 ** 22, 1.0), (2 ** 24, 200.0), (2 ** 28, 400.0)]
+    lat = lambda b: alg1.interp_latency_us(curve, b)
+    best, _ = alg1.search(8, 400.0, lambda G: alg1.group_bytes(G, 64, 512, 65536), lat)
+    assert best != (1,) * 8

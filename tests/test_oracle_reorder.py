@@ -1,0 +1,156 @@
+"""Pins for oracle steps O5/O7 (pre/post-communication reordering) and O9."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synthetic
+from oracle import collectives as oc
+from oracle import pipeline as opl
+from oracle import plan as op
+from oracle import reorder as orr
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reorder.json")))
+
+
+def _rand_plan(rng, BMs=(1, 2, 4), n=1):
+    BM = int(rng.choice(BMs)) * n
+    BN = int(rng.integers(1, 4))
+    Mt, Nt = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    ntiles = Mt * Nt
+    S = int(rng.integers(1, ntiles + 1))
+    T = op.num_waves(ntiles, S)
+    part = synthetic.random_partition(T, int(rng.integers(1 << 30)))
+    order = synthetic.random_order(ntiles, int(rng.integers(1 << 30)))
+    return op.make_plan(Mt * BM, Nt * BN, BM, BN, S, part, order=order)
+
+
+def test_ar_roundtrip_and_bijection():
+    """post(pre(X)) == X bit-exactly; pre is a bijection."""
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        pl = _rand_plan(rng)
+        X = rng.standard_normal((pl.M, pl.N))
+        buf = orr.ar_pre(X, pl)
+        assert np.array_equal(orr.ar_post(buf, pl), X)
+        idx = orr.ar_pre(np.arange(pl.M * pl.N, dtype=float).reshape(pl.M, pl.N), pl)
+        assert np.array_equal(np.sort(idx), np.arange(pl.M * pl.N))
+
+
+def test_ar_group_contiguity_and_monotonicity():
+    """Every element of group j sits inside group j's range, ranges ordered
+    (SPEC.md:150-152)."""
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        pl = _rand_plan(rng)
+        idx = orr.ar_pre(np.arange(pl.M * pl.N, dtype=float).reshape(pl.M, pl.N), pl).astype(int)
+        gop = op.group_of_position(pl.partition, pl.S, pl.ntiles)
+        pos_of_tile = {int(t): p for p, t in enumerate(pl.order)}
+        for (lo, hi), j in zip(orr.group_elem_ranges(pl), range(len(pl.ranges))):
+            for e in idx[lo:hi]:
+                r, c = divmod(int(e), pl.N)
+                t = (r // pl.BM) * pl.Nt + c // pl.BN
+                assert gop[pos_of_tile[t]] == j
+        starts = [lo for lo, _ in orr.group_elem_ranges(pl)]
+        assert starts == sorted(starts)
+
+
+def test_ar_rowband_is_identity_layout():
+    pl = op.make_plan(8, 6, 2, 2, 6, [1, 1], swizzle=1)   # 4x3 tiles, waves of 2 tile-rows
+    X = np.arange(48.0).reshape(8, 6)
+    assert orr.ar_rowband_ok(pl)
+    assert np.array_equal(orr.ar_pre(X, pl, "rowband"), X.reshape(-1))
+    bad = op.make_plan(8, 6, 2, 2, 4, [1, 1, 1], swizzle=1)  # group boundary mid tile-row
+    assert not orr.ar_rowband_ok(bad)
+    with pytest.raises(op.OracleError):
+        orr.ar_pre(X, bad, "rowband")
+
+
+def test_rs_worked_example_g6():
+    c = GOLD["rs"][0]
+    pl = op.make_plan(c["M"], c["N"], c["BM"], c["BN"], c["S"], c["partition"])
+    Y = np.repeat(np.arange(c["M"], dtype=float)[:, None], c["N"], axis=1)  # value = row id
+    buf = orr.rs_pre(Y, pl, c["n"])
+    assert buf.reshape(-1, c["N"])[:, 0].astype(int).tolist() == c["buffer_rows"]
+    for k in range(c["n"]):
+        chunk = orr.rs_chunk(buf, pl, c["n"], 0, k)
+        assert chunk.reshape(-1, c["N"])[:, 0].astype(int).tolist() == c["rank_rows"][k]
+        assert opl.rs_rows_of_rank(c["M"], c["BM"], c["n"], k).tolist() == c["rank_rows"][k]
+
+
+def test_row_exchange_spec_example():
+    c = GOLD["rs"][1]
+    gathered = np.array(c["gathered"], dtype=float)[:, None]
+    assert opl.row_exchange(gathered, c["BM"], c["n"])[:, 0].astype(int).tolist() == list(range(c["M"]))
+
+
+def test_rs_rows_complete_on_one_rank():
+    """after RS each row resides entirely on one GPU."""
+    rng = np.random.default_rng(2)
+    for n in (1, 2, 3, 4):
+        for _ in range(40):
+            pl = _rand_plan(rng, n=n)
+            M, N = pl.M, pl.N
+            Y = (np.arange(M)[:, None] * 1000 + np.arange(N)[None, :]).astype(float)
+            bufs = [orr.rs_pre(Y, pl, n) for _ in range(n)]
+            recv = oc.reduce_scatter_groups(bufs, orr.group_elem_ranges(pl))
+            covered = np.zeros(M, int)
+            for k in range(n):
+                out = orr.rs_post(recv[k], pl, n)
+                for l in range(M // n):
+                    g = orr.rs_local_to_global_row(l, pl.BM, pl.BM // n, k)
+                    assert np.array_equal(out[l], n * Y[g])
+                    covered[g] += 1
+            assert (covered == 1).all()
+
+
+def test_rs_pre_inverse():
+    """O9 for RS with n = 1 (identity collective): post(pre(X)) == X."""
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        pl = _rand_plan(rng)
+        X = rng.standard_normal((pl.M, pl.N))
+        buf = orr.rs_pre(X, pl, 1)
+        assert np.array_equal(orr.rs_post(buf, pl, 1), X)
+        idx = orr.rs_pre(np.arange(pl.M * pl.N, dtype=float).reshape(pl.M, pl.N), pl, 1)
+        assert np.array_equal(np.sort(idx), np.arange(pl.M * pl.N))
+
+
+def test_rs_indivisible_rejected():
+    pl = op.make_plan(6, 2, 3, 2, 1, None)
+    with pytest.raises(op.OracleError):
+        orr.rs_pre(np.zeros((6, 2)), pl, 2)
+
+
+def test_a2a_worked_example_g7():
+    c = GOLD["a2a"][0]
+    pl = op.make_plan(c["M"], c["N"], c["BM"], c["BN"], c["S"], c["partition"])
+    Y = np.arange(c["M"] * c["N"], dtype=float).reshape(c["M"], c["N"])
+    s = orr.a2a_pre(Y, pl, c["row_dst"], c["n"])
+    for d in range(c["n"]):
+        assert [list(m) for m in s.meta[d]] == c["pool_meta"][d]
+        assert [list(r) for r in s.ranges[d]] == c["pool_ranges"][d]
+        for (row, j), v in zip(s.meta[d], s.pools[d]):
+            assert np.array_equal(v, Y[row, j * c["BN"]:(j + 1) * c["BN"]])
+    assert np.flatnonzero(np.array(c["row_dst"]) == 0).tolist() == c["rank0_rows_from_self"]
+
+
+def test_a2a_identity_routing_roundtrip():
+    """A2A with every row routed to the only rank is a permutation + inverse."""
+    rng = np.random.default_rng(4)
+    for _ in range(60):
+        pl = _rand_plan(rng)
+        X = rng.standard_normal((pl.M, pl.N))
+        s = orr.a2a_pre(X, pl, np.zeros(pl.M, int), 1)
+        recv = oc.alltoall_groups([s], len(pl.ranges))
+        out = orr.a2a_post(recv[0], [s.meta[0]], [np.zeros(pl.M, int)], 0, pl.N, pl.BN)
+        assert np.array_equal(out, X)
+
+
+def test_a2a_errors():
+    pl = op.make_plan(4, 4, 2, 2, 2, None)
+    with pytest.raises(op.OracleError):
+        orr.a2a_pre(np.zeros((4, 4)), pl, [0, 1, 2], 2)
+    with pytest.raises(op.OracleError):
+        orr.a2a_pre(np.zeros((4, 4)), pl, [0, 1, 2, 0], 2)
