@@ -1,0 +1,224 @@
+/*
+ * flashoverlap.h — C ABI of the B200-native FlashOverlap hot path
+ * (arXiv 2504.19519, "Efficient and Adaptable Overlapping for Computation and
+ * Communication via Signaling and Reordering").
+ *
+ * The library runs ONE tensor-parallel GEMM  C = A · Btᵀ as a
+ * single persistent tcgen05 kernel whose epilogue stores every finished tile
+ * into a pre-communication-reordered buffer and bumps a per-wave-group counter
+ * (signaling; reordering).  A
+ * communication stream waits on each counter (cuStreamWaitValue32, no SM
+ * spent) and issues a plain NCCL AllReduce / ReduceScatter / All-to-All on the
+ * group's contiguous range.  A post-communication reorder
+ * kernel restores row-major order, optionally fused with residual-add and
+ * RMSNorm.  Alg. 1 is exposed as
+ * fo_tune_search / fo_tune_predict.
+ *
+ * Conventions
+ *  - Matrices are bf16, row-major, contiguous.  A is [m, k] (K-major); Bt is
+ *    [n, k] (the nn.Linear weight layout, K-major); C is [m, n].
+ *  - "device" pointers are CUDA device addresses on the context's device.
+ *    "host" pointers are ordinary CPU memory, read during the call only
+ *    (the library copies what it keeps).
+ *  - Streams are passed as void* (a cudaStream_t); NULL is the legacy stream.
+ *  - Tiles: tile id t = i*nt + j (tile-row i, tile-column j).  Execution
+ *    position p in [0, tiles): the persistent kernel runs the tile
+ *    tile_order[p] as the p-th unit; worker w of S runs positions w, w+S, ...
+ *    so position p belongs to wave floor(p/S) and to the wave
+ *    group containing that wave.
+ *  - Every function returns fo_status; nothing is thrown across the ABI.
+ *    On a non-OK status fo_last_error() returns a thread-local message.
+ *
+ * Ownership: the caller owns A, Bt, out, residual, gamma and every buffer it
+ * passes; they must stay valid until the stream reaches the end of the op.
+ * The library owns contexts (NCCL communicator, streams, events) and plans
+ * (device tables, the communication buffer, the counting table); the
+ * matching *_destroy releases them.
+ */
+#ifndef FLASHOVERLAP_H_
+#define FLASHOVERLAP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FO_OK = 0,
+  FO_ERR_INVALID_ARG = 1, /* non-permutation order, sum(group_waves) != T, zero group, row_dst out of range, NULL */
+  FO_ERR_SHAPE = 2,       /* m % tile_m, n % tile_n, k % 64, tile_m % world (RS) */
+  FO_ERR_UNSUPPORTED = 3, /* tile shape not compiled, layout not applicable, no sm_100 device */
+  FO_ERR_CUDA = 4,
+  FO_ERR_NCCL = 5,
+  FO_ERR_OOM = 6,
+  FO_ERR_TIMEOUT = 7,
+  FO_ERR_STATE = 8        /* plan used with a mismatched context, etc. */
+} fo_status;
+
+/* Which collective follows the GEMM. */
+typedef enum {
+  FO_ALLREDUCE = 0,     /* TP row-parallel linear; every rank gets sum_r C_r           */
+  FO_REDUCESCATTER = 1, /* TP + sequence parallel; rank k gets rows R_k of sum_r C_r    */
+  FO_ALLTOALL = 2,      /* EP combine; row g of C goes to rank row_dst[g]               */
+  FO_NOCOMM = 3         /* plain GEMM writing row-major C (sequential baseline, tuner)  */
+} fo_coll;
+
+/* AllReduce buffer layout (H11a). */
+typedef enum {
+  FO_LAYOUT_SLOT = 0,    /* paper: tile at position p -> contiguous slot p (tile_m*tile_n elems, row-major) */
+  FO_LAYOUT_ROWBAND = 1, /* identity: raster order + tile-row group boundaries -> each group is a row band of C;
+                            the epilogue writes C in place and both reorders are the identity */
+  FO_LAYOUT_AUTO = 2     /* ROWBAND when legal, else SLOT */
+} fo_ar_layout;
+
+/* Elementwise op fused into the post-communication reorder (R12). */
+typedef enum {
+  FO_POST_NONE = 0,
+  FO_POST_ADD = 1,          /* out = x + residual                                   */
+  FO_POST_ADD_RMSNORM = 2   /* y = x + residual; out = y / sqrt(mean(y^2) + eps) * gamma */
+} fo_post;
+
+typedef struct fo_ctx_s* fo_ctx;
+typedef struct fo_plan_s* fo_plan;
+
+/* One rank's view of the overlapped layer.  All pointers are HOST pointers,
+ * read during fo_plan_create only. */
+typedef struct {
+  int32_t coll;          /* fo_coll */
+  int32_t ar_layout;     /* fo_ar_layout (AllReduce only) */
+  int64_t m, n, k;       /* this rank's GEMM: A [m,k], Bt [n,k], C [m,n]; k = K/world for TP */
+  int32_t tile_m;        /* 128 (cta_group::1) or 256 (cta_group::2 pair) */
+  int32_t tile_n;        /* 64, 128 or 256 */
+  int32_t workers;       /* S >= 1 = concurrent tile workers = wave width (grid of the persistent GEMM) */
+  const int32_t* tile_order; /* [tiles] permutation of tile ids, or NULL => default swizzle */
+  int32_t swizzle;       /* default order: row-panels of `swizzle` tile-rows, column-major inside (R1) */
+  int32_t num_groups;    /* P */
+  const int32_t* group_waves; /* [P] wave counts, sum == T = ceil(tiles / S); NULL => one group */
+  const int32_t* row_dst;     /* All-to-All: [m] destination rank of each output row */
+  int32_t post;          /* fo_post */
+  float eps;             /* RMSNorm epsilon */
+} fo_plan_desc;
+
+typedef struct {
+  int32_t rank, world;
+  int32_t mt, nt, tiles;
+  int32_t workers;       /* S actually used */
+  int32_t waves;         /* T */
+  int32_t num_groups;    /* P */
+  int32_t ar_layout;     /* resolved layout (AllReduce) */
+  int32_t rs_subtile_rows; /* h = tile_m / world (ReduceScatter) */
+  int64_t send_elems;    /* elements of the pre-reordered send buffer */
+  int64_t recv_elems;    /* elements of the receive buffer (AR: == send) */
+  int64_t out_rows, out_cols; /* shape of `out` expected by fo_run */
+} fo_plan_info;
+
+/* ---------------------------------------------------------------- library */
+const char* fo_last_error(void);
+const char* fo_version(void);
+/* Number of SMs of `device` (0 if no device); for choosing workers. */
+fo_status fo_device_sm_count(int32_t device, int32_t* sm_count);
+
+/* ---------------------------------------------------------------- plan (host only, no GPU needed) */
+/* Build the host-side plan of rank `rank` in a `world`-rank group.
+ * peers: All-to-All only — peers[s] is rank s's descriptor (peers[rank] may be
+ * `self`); every rank must use the same number of groups P.  The caller
+ * gathers the peer descriptors (e.g. torch.distributed all_gather_object);
+ * this is the "census" of the A2A receive layout.  Ignored
+ * (may be NULL) for AllReduce / ReduceScatter / no-comm.
+ * No CUDA call is made; device state is created lazily by the first run. */
+fo_status fo_plan_create(const fo_plan_desc* self, int32_t rank, int32_t world,
+                         const fo_plan_desc* const* peers, fo_plan* out);
+fo_status fo_plan_destroy(fo_plan plan);
+fo_status fo_plan_get_info(fo_plan plan, fo_plan_info* info);
+/* Group j: execution positions [pos_begin, pos_end) and send-buffer element
+ * range [elem_begin, elem_end) (AR / RS; for A2A the element range spans the
+ * group's part of pool 0..world-1 and is informational). */
+fo_status fo_plan_group(fo_plan plan, int32_t j, int32_t* pos_begin, int32_t* pos_end,
+                        int64_t* elem_begin, int64_t* elem_end);
+/* Parity exports (host arrays, caller-allocated):
+ *  order[tiles]                 execution order (tile id at position p)
+ *  send_map[m*n]                send-buffer element index of C[r][c] (index r*n + c)
+ *  recv_map[out_rows*out_cols]  receive-buffer element index read for out[r][c]
+ *  a2a_send_cnt[P*world], a2a_recv_cnt[P*world]  subtokens per (group, peer) */
+fo_status fo_plan_export_order(fo_plan plan, int32_t* order);
+fo_status fo_plan_export_send_map(fo_plan plan, int64_t* send_map);
+fo_status fo_plan_export_recv_map(fo_plan plan, int64_t* recv_map);
+fo_status fo_plan_export_a2a_counts(fo_plan plan, int64_t* a2a_send_cnt, int64_t* a2a_recv_cnt);
+
+/* ---------------------------------------------------------------- context (one per process / GPU) */
+/* NCCL unique id (128 bytes) made on one rank and broadcast by the caller. */
+fo_status fo_get_unique_id(uint8_t uid[128]);
+/* Create the library's NCCL communicator (rank of world) on `device` plus a
+ * highest-priority communication stream.  nccl_max_ctas > 0
+ * caps NCCL's CTAs (ncclConfig_t.maxCTAs) so they fit the SMs the persistent
+ * GEMM leaves free; 0 = NCCL default.  Collective over the ranks. */
+fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128],
+                        int32_t nccl_max_ctas, fo_ctx* out);
+fo_status fo_ctx_destroy(fo_ctx ctx);
+
+/* ---------------------------------------------------------------- the overlapped op */
+/* Overlapped GEMM + collective (+ post-reorder, + fused elementwise), stream
+ * ordered on `stream` and host-asynchronous.  Collective: every rank calls it
+ * with matching plans in the same order.  A plan must not run concurrently
+ * with itself.
+ *   A [m,k], Bt [n,k]: device bf16.
+ *   out: device bf16 [info.out_rows, info.out_cols]:
+ *     AR  -> [m, n] row-major, identical on every rank;
+ *     RS  -> [m/world, n]: local row l = global row floor(l/h)*tile_m + rank*h + l%h (h = tile_m/world);
+ *     A2A -> [sum_s cnt(s->rank), n]: rows grouped by source rank ascending, then source row ascending;
+ *     NOCOMM -> [m, n].
+ *   residual (FO_POST_ADD*): device bf16, same shape as out; gamma (RMSNorm): device bf16 [n].
+ * Internals: counters reset, GEMM on the caller stream, per group a
+ * stream-side wait (counter >= |G_j|) then the NCCL call on the comm stream,
+ * post-reorder, join back to `stream`. */
+fo_status fo_run(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
+                 const void* residual, const void* gamma, void* stream);
+/* Non-overlapped baseline: the SAME GEMM kernel writing row-major C, then ONE
+ * full-size NCCL call (AR in place; RS standard contiguous rows; A2A with
+ * row_dst sorted ascending), then the fused elementwise op as its own pass. */
+fo_status fo_run_sequential(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
+                            const void* residual, const void* gamma, void* stream);
+
+/* ---------------------------------------------------------------- stages (tests, single GPU, no NCCL) */
+/* Run only the GEMM with this plan's pre-reorder epilogue into a caller
+ * device buffer `send` of info.send_elems bf16 (the counting table is bumped
+ * as in fo_run).  Lets one GPU exercise every rank's epilogue of a
+ * multi-rank plan. */
+fo_status fo_gemm_stage(fo_plan plan, const void* A, const void* Bt, void* send, void* stream);
+/* As fo_gemm_stage, and also write %globaltimer (ns) into the device array
+ * tile_ts[tiles] at the moment each execution position signals (wave
+ * pattern evidence, the analogue of PAPER.md:230 fig:wave). */
+fo_status fo_gemm_stage_timed(fo_plan plan, const void* A, const void* Bt, void* send,
+                              unsigned long long* tile_ts, void* stream);
+/* Run only the post-communication reorder (+ fused op) from a caller device
+ * receive buffer of info.recv_elems bf16. */
+fo_status fo_post_stage(fo_plan plan, const void* recv, void* out, const void* residual,
+                        const void* gamma, void* stream);
+/* Copy the plan's P counters to host (synchronises the device). */
+fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
+/* Number of kernels the library launched since load (for gpu_launches). */
+int64_t fo_kernel_launch_count(void);
+
+/* ---------------------------------------------------------------- tuner (Alg. 1, host only) */
+/* Predicted latency (us) of partition `groups[0..P)`:
+ *   duration_us  GEMM duration at wave width S; T = ceil(tiles/S)
+ *   tile_bytes   message bytes per tile (tile_m*tile_n*2)
+ *   curve        npts samples (bytes, GB/s), bytes strictly increasing;
+ *                linear interpolation in log2(bytes), clamped (R15). */
+fo_status fo_tune_predict(const int32_t* groups, int32_t P, double duration_us, int32_t tiles,
+                          int32_t S, double tile_bytes, const double* curve_bytes,
+                          const double* curve_gbps, int32_t npts, double* predicted_us);
+/* Alg. 1 search over the candidates with |G_1| <= s1 and |G_P| <= sp (prune
+ * != 0) or all 2^(T-1) (prune == 0).  Ties: fewer groups, then
+ * lexicographically smaller (R16).  out_groups must hold T entries. */
+fo_status fo_tune_search(double duration_us, int32_t tiles, int32_t S, double tile_bytes,
+                         const double* curve_bytes, const double* curve_gbps, int32_t npts,
+                         int32_t s1, int32_t sp, int32_t prune, int32_t* out_groups,
+                         int32_t* out_num_groups, double* predicted_us);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHOVERLAP_H_ */

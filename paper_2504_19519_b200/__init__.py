@@ -1,0 +1,245 @@
+"""paper_2504_19519_b200 — B200-native FlashOverlap hot path (arXiv 2504.19519).
+
+Thin Python layer over include/flashoverlap.h.  It only marshals arguments
+(torch tensors -> device pointers, numpy arrays -> host pointers); every step
+of the overlapped GEMM + collective runs in libflashoverlap.so.  PyTorch is
+used for device memory, streams and process groups only.
+
+    plan = Plan(coll="allreduce", m=M, n=N, k=K_loc, tile_n=256, workers=S,
+                group_waves=[2, 2], rank=r, world=n)
+    ctx  = Context.create(device, rank, world, uid)           # NCCL comm + comm stream
+    run(ctx, plan, A, Bt, out)                                # overlapped
+    run_sequential(ctx, plan, A, Bt, out)                     # GEMM -> one NCCL call
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import COLL, LAYOUT, POST, FOError, check, load
+
+__all__ = ["Plan", "Context", "run", "run_sequential", "gemm_stage", "gemm_stage_timed", "post_stage",
+           "unique_id", "tune_search", "tune_predict", "kernel_launch_count", "FOError", "load",
+           "device_sm_count"]
+
+
+def _i32(a) -> Optional[np.ndarray]:
+    if a is None:
+        return None
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+
+
+def _p32(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+@dataclass
+class PlanSpec:
+    coll: str = "allreduce"
+    m: int = 0
+    n: int = 0
+    k: int = 0
+    tile_m: int = 128
+    tile_n: int = 256
+    workers: int = 148
+    tile_order: Optional[Sequence[int]] = None
+    swizzle: int = 1
+    group_waves: Optional[Sequence[int]] = None
+    row_dst: Optional[Sequence[int]] = None
+    post: str = "none"
+    eps: float = 1e-5
+    ar_layout: str = "auto"
+    _keep: list = field(default_factory=list, repr=False)
+
+    def to_c(self) -> _lib.PlanDescC:
+        order, gw, rd = _i32(self.tile_order), _i32(self.group_waves), _i32(self.row_dst)
+        self._keep = [order, gw, rd]
+        d = _lib.PlanDescC()
+        d.coll = COLL[self.coll]
+        d.ar_layout = LAYOUT[self.ar_layout]
+        d.m, d.n, d.k = int(self.m), int(self.n), int(self.k)
+        d.tile_m, d.tile_n, d.workers = int(self.tile_m), int(self.tile_n), int(self.workers)
+        d.tile_order = _p32(order)
+        d.swizzle = int(self.swizzle)
+        d.num_groups = 0 if gw is None else int(gw.size)
+        d.group_waves = _p32(gw)
+        d.row_dst = _p32(rd)
+        d.post = POST[self.post]
+        d.eps = float(self.eps)
+        return d
+
+
+class Plan:
+    """Host plan of one rank (fo_plan_create).  `peers` (All-to-All only): the
+    PlanSpec of every rank, gathered by the caller (see dist.gather_specs)."""
+
+    def __init__(self, rank: int = 0, world: int = 1, peers: Optional[Sequence[PlanSpec]] = None, **kw):
+        lib = load()
+        self.spec = PlanSpec(**kw)
+        self.rank, self.world = rank, world
+        d = self.spec.to_c()
+        peer_arr = None
+        keep = []
+        if peers is not None:
+            cs = []
+            for s in peers:
+                s = s if isinstance(s, PlanSpec) else PlanSpec(**s)
+                c = s.to_c()
+                keep.append(s)
+                cs.append(C.pointer(c))
+                keep.append(c)
+            peer_arr = (C.POINTER(_lib.PlanDescC) * world)(*cs)
+        h = C.c_void_p()
+        check(lib.fo_plan_create(C.byref(d), rank, world, peer_arr, C.byref(h)))
+        self._h = h
+        info = _lib.PlanInfoC()
+        check(lib.fo_plan_get_info(h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in info._fields_}
+
+    @property
+    def handle(self):
+        return self._h
+
+    def group(self, j: int):
+        pb, pe, eb, ee = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+        check(load().fo_plan_group(self._h, j, C.byref(pb), C.byref(pe), C.byref(eb), C.byref(ee)))
+        return pb.value, pe.value, eb.value, ee.value
+
+    def export_order(self) -> np.ndarray:
+        o = np.empty(self.info["tiles"], np.int32)
+        check(load().fo_plan_export_order(self._h, o.ctypes.data_as(C.POINTER(C.c_int32))))
+        return o
+
+    def export_send_map(self) -> np.ndarray:
+        m = np.empty(self.spec.m * self.spec.n, np.int64)
+        check(load().fo_plan_export_send_map(self._h, m.ctypes.data_as(C.POINTER(C.c_int64))))
+        return m
+
+    def export_recv_map(self) -> np.ndarray:
+        m = np.empty(self.info["out_rows"] * self.info["out_cols"], np.int64)
+        check(load().fo_plan_export_recv_map(self._h, m.ctypes.data_as(C.POINTER(C.c_int64))))
+        return m
+
+    def export_a2a_counts(self):
+        n = self.info["num_groups"] * self.world
+        s, r = np.empty(n, np.int64), np.empty(n, np.int64)
+        check(load().fo_plan_export_a2a_counts(self._h, s.ctypes.data_as(C.POINTER(C.c_int64)),
+                                               r.ctypes.data_as(C.POINTER(C.c_int64))))
+        return s.reshape(-1, self.world), r.reshape(-1, self.world)
+
+    def read_counters(self) -> np.ndarray:
+        c = np.empty(self.info["num_groups"], np.uint32)
+        check(load().fo_plan_read_counters(self._h, c.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return c
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            load().fo_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(load().fo_get_unique_id(buf))
+    return bytes(buf)
+
+
+class Context:
+    """Library-owned NCCL communicator + highest-priority comm stream."""
+
+    def __init__(self, handle, device, rank, world):
+        self._h, self.device, self.rank, self.world = handle, device, rank, world
+
+    @classmethod
+    def create(cls, device: int, rank: int, world: int, uid: bytes, nccl_max_ctas: int = 0) -> "Context":
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(load().fo_ctx_create(device, rank, world, buf, nccl_max_ctas, C.byref(h)))
+        return cls(h, device, rank, world)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            check(load().fo_ctx_destroy(self._h))
+            self._h = C.c_void_p()
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+
+
+def run(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=None):
+    check(load().fo_run(ctx._h, plan.handle, _ptr(A), _ptr(Bt), _ptr(out), _ptr(residual), _ptr(gamma),
+                        _stream(stream)))
+
+
+def run_sequential(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=None):
+    check(load().fo_run_sequential(ctx._h, plan.handle, _ptr(A), _ptr(Bt), _ptr(out), _ptr(residual),
+                                   _ptr(gamma), _stream(stream)))
+
+
+def gemm_stage(plan: Plan, A, Bt, send, stream=None):
+    check(load().fo_gemm_stage(plan.handle, _ptr(A), _ptr(Bt), _ptr(send), _stream(stream)))
+
+
+def gemm_stage_timed(plan: Plan, A, Bt, send, tile_ts, stream=None):
+    check(load().fo_gemm_stage_timed(plan.handle, _ptr(A), _ptr(Bt), _ptr(send), _ptr(tile_ts), _stream(stream)))
+
+
+def post_stage(plan: Plan, recv, out, residual=None, gamma=None, stream=None):
+    check(load().fo_post_stage(plan.handle, _ptr(recv), _ptr(out), _ptr(residual), _ptr(gamma), _stream(stream)))
+
+
+def kernel_launch_count() -> int:
+    return int(load().fo_kernel_launch_count())
+
+
+def device_sm_count(device: int = 0) -> int:
+    n = C.c_int32()
+    check(load().fo_device_sm_count(device, C.byref(n)))
+    return n.value
+
+
+def _curve(curve):
+    b = np.ascontiguousarray([float(x) for x, _ in curve], np.float64)
+    g = np.ascontiguousarray([float(y) for _, y in curve], np.float64)
+    return b, g
+
+
+def tune_predict(groups, duration_us, tiles, S, tile_bytes, curve) -> float:
+    g = _i32(groups)
+    b, bw = _curve(curve)
+    out = C.c_double()
+    check(load().fo_tune_predict(_p32(g), int(g.size), float(duration_us), int(tiles), int(S), float(tile_bytes),
+                                 b.ctypes.data_as(C.POINTER(C.c_double)), bw.ctypes.data_as(C.POINTER(C.c_double)),
+                                 int(b.size), C.byref(out)))
+    return out.value
+
+
+def tune_search(duration_us, tiles, S, tile_bytes, curve, s1=2, sp=4, prune=True):
+    T = (tiles + S - 1) // S
+    b, bw = _curve(curve)
+    groups = np.zeros(max(T, 1), np.int32)
+    P = C.c_int32()
+    pred = C.c_double()
+    check(load().fo_tune_search(float(duration_us), int(tiles), int(S), float(tile_bytes),
+                                b.ctypes.data_as(C.POINTER(C.c_double)), bw.ctypes.data_as(C.POINTER(C.c_double)),
+                                int(b.size), int(s1), int(sp), int(bool(prune)), _p32(groups), C.byref(P),
+                                C.byref(pred)))
+    return tuple(int(x) for x in groups[:P.value]), pred.value

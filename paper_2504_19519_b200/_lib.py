@@ -1,0 +1,110 @@
+"""ctypes binding of include/flashoverlap.h (argument marshalling only).
+
+Every step of the hot path runs in libflashoverlap.so (the sm_100a kernels,
+the stream waits and the NCCL calls).  If the library is missing this module
+raises: there is no Python / CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libflashoverlap.so")
+
+FO_OK, FO_ERR_INVALID_ARG, FO_ERR_SHAPE, FO_ERR_UNSUPPORTED, FO_ERR_CUDA, FO_ERR_NCCL, FO_ERR_OOM, \
+    FO_ERR_TIMEOUT, FO_ERR_STATE = range(9)
+STATUS_NAMES = ["OK", "INVALID_ARG", "SHAPE", "UNSUPPORTED", "CUDA", "NCCL", "OOM", "TIMEOUT", "STATE"]
+
+COLL = {"allreduce": 0, "reducescatter": 1, "alltoall": 2, "nocomm": 3}
+LAYOUT = {"slot": 0, "rowband": 1, "auto": 2}
+POST = {"none": 0, "add": 1, "add_rmsnorm": 2}
+
+
+class FOError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"FO_ERR_{name}: {msg}")
+
+
+class PlanDescC(C.Structure):
+    _fields_ = [
+        ("coll", C.c_int32), ("ar_layout", C.c_int32),
+        ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
+        ("tile_m", C.c_int32), ("tile_n", C.c_int32), ("workers", C.c_int32),
+        ("tile_order", C.POINTER(C.c_int32)), ("swizzle", C.c_int32),
+        ("num_groups", C.c_int32), ("group_waves", C.POINTER(C.c_int32)),
+        ("row_dst", C.POINTER(C.c_int32)),
+        ("post", C.c_int32), ("eps", C.c_float),
+    ]
+
+
+class PlanInfoC(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32), ("world", C.c_int32),
+        ("mt", C.c_int32), ("nt", C.c_int32), ("tiles", C.c_int32),
+        ("workers", C.c_int32), ("waves", C.c_int32), ("num_groups", C.c_int32),
+        ("ar_layout", C.c_int32), ("rs_subtile_rows", C.c_int32),
+        ("send_elems", C.c_int64), ("recv_elems", C.c_int64),
+        ("out_rows", C.c_int64), ("out_cols", C.c_int64),
+    ]
+
+
+# (name, restype, argtypes) for every symbol include/flashoverlap.h declares
+_P = C.c_void_p
+_SIGS = [
+    ("fo_last_error", C.c_char_p, []),
+    ("fo_version", C.c_char_p, []),
+    ("fo_device_sm_count", C.c_int, [C.c_int32, C.POINTER(C.c_int32)]),
+    ("fo_plan_create", C.c_int, [C.POINTER(PlanDescC), C.c_int32, C.c_int32, C.POINTER(C.POINTER(PlanDescC)),
+                                 C.POINTER(_P)]),
+    ("fo_plan_destroy", C.c_int, [_P]),
+    ("fo_plan_get_info", C.c_int, [_P, C.POINTER(PlanInfoC)]),
+    ("fo_plan_group", C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("fo_plan_export_order", C.c_int, [_P, C.POINTER(C.c_int32)]),
+    ("fo_plan_export_send_map", C.c_int, [_P, C.POINTER(C.c_int64)]),
+    ("fo_plan_export_recv_map", C.c_int, [_P, C.POINTER(C.c_int64)]),
+    ("fo_plan_export_a2a_counts", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("fo_get_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("fo_ctx_create", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32,
+                                C.POINTER(_P)]),
+    ("fo_ctx_destroy", C.c_int, [_P]),
+    ("fo_run", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    ("fo_run_sequential", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    ("fo_gemm_stage", C.c_int, [_P, _P, _P, _P, _P]),
+    ("fo_gemm_stage_timed", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("fo_post_stage", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("fo_plan_read_counters", C.c_int, [_P, C.POINTER(C.c_uint32)]),
+    ("fo_kernel_launch_count", C.c_int64, []),
+    ("fo_tune_predict", C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_double,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double)]),
+    ("fo_tune_search", C.c_int, [C.c_double, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+]
+SYMBOLS = [s[0] for s in _SIGS]
+
+_lib = None
+
+
+def load():
+    """Load libflashoverlap.so (built in-tree by build.py) and bind its symbols."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in _SIGS:
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status != FO_OK:
+        raise FOError(status, load().fo_last_error().decode(errors="replace"))

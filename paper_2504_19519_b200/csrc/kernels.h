@@ -1,0 +1,60 @@
+// Launch interface of the sm_100a kernels (host <-> device structs).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fo {
+
+// Epilogue store mode = the pre-communication reordering.
+enum EpiMode : int {
+  EPI_ROWMAJOR = 0,  // C row-major with row stride ldc (no-comm, AR ROWBAND)
+  EPI_SLOT = 1,      // AR: tile at position p -> slot p (BM*BN contiguous, row-major)
+  EPI_RS = 2,        // RS: subtile k of the tile -> chunk k of its group
+  EPI_A2A = 3        // A2A: row a of the tile -> its destination pool slot
+};
+
+struct GemmArgs {
+  const void* A;      // [M, K] bf16 row-major
+  const void* Bt;     // [N, K] bf16 row-major
+  void* dst;          // bf16 destination (C or the send buffer)
+  int64_t M, N, K;
+  int BM, BN;
+  int Mt, Nt, tiles;
+  int workers;        // grid size S
+  int mode;           // EpiMode
+  int64_t ldc;        // EPI_ROWMAJOR row stride
+  const int32_t* order;        // [tiles] device
+  const int32_t* group_of_pos; // [tiles] device
+  const int32_t* gpos;         // [P+1] device
+  const int32_t* row_slot;     // [tiles*BM] device (A2A)
+  uint32_t* counters;          // [P] device, may be null
+  int h;                       // RS subtile rows
+  unsigned long long* tile_ts; // optional [tiles] device: %globaltimer at signal
+};
+
+enum PostMode : int { POSTMAP_IDENTITY = 0, POSTMAP_SLOT = 1, POSTMAP_RS = 2, POSTMAP_A2A = 3 };
+
+struct PostArgs {
+  int map;                 // PostMode
+  int op;                  // fo_post
+  const void* src;         // receive buffer (bf16)
+  void* out;               // [rows, N] bf16
+  const void* residual;    // [rows, N] bf16 or null
+  const void* gamma;       // [N] bf16 or null
+  int64_t rows, N;
+  int BM, BN, Nt, h;
+  const int32_t* pos_of_tile;  // device
+  const int32_t* src_row;      // device (A2A)
+  float eps;
+};
+
+// Returns a cudaError_t-compatible code (0 = success).
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream);
+cudaError_t launch_post(const PostArgs& a, cudaStream_t stream);
+bool gemm_shape_supported(int BM, int BN);
+void count_launch();
+int64_t launch_count();
+
+}  // namespace fo

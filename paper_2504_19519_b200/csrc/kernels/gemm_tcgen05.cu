@@ -1,0 +1,416 @@
+// Persistent warp-specialised tcgen05 bf16 GEMM for sm_100a whose epilogue
+// performs FlashOverlap's pre-communication reordering and group signaling.
+//
+//   C[M,N] = A[M,K] · Bt[N,K]^T,   bf16 in, fp32 accumulate (TMEM), bf16 out.
+//
+// Method: the main loop is an unmodified GEMM (PAPER.md:241-242,
+// 394 "involving only the epilogue without interrupting the main loop"); the
+// epilogue stores each finished tile straight into the reordered send buffer
+// and then atomically adds 1 to the counter of the tile's
+// wave group ("The j-th number in the counting table is
+// atomically added by 1 when a tile in G_j is finished").
+//
+// B200 design:
+//  - grid = S persistent CTAs (S = wave width); CTA w runs execution positions
+//    w, w+S, w+2S, ...  so position p is in wave floor(p/S) by construction.
+//  - warp 0: TMA producer (128B-swizzled K-major boxes, mbarrier ring of ST
+//    stages); warp 1: single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//    accumulating in TMEM; warp 2: TMEM allocator; warps 4-7: epilogue.
+//  - two TMEM accumulator stages so the epilogue of tile i overlaps the main
+//    loop of tile i+1.
+//  - epilogue: tcgen05.ld (32 lanes x 32 cols) -> bf16 RNE -> per-warp smem
+//    staging -> coalesced 16-byte stores to the mode's destination rows; a
+//    named barrier over the 4 epilogue warps, then ONE red.release.gpu add on
+//    the group counter (release orders all the tile's stores before it).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+
+#include "../kernels.h"
+
+namespace fo {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;                      // 64 bf16 = 128 B = one swizzle row
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int EPI_COLS = 64;                // columns staged per epilogue chunk
+constexpr int EPI_PITCH = EPI_COLS * 2 + 16;  // padded row pitch (bank-conflict free)
+constexpr int EPI_WARP_BYTES = 32 * EPI_PITCH;
+constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
+constexpr int NUM_THREADS = 256;
+
+template <int BN>
+struct Cfg {
+  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128) ? 6 : 8;
+  static constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulator stages
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+  static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM alloc power of 2");
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row core groups
+// 1024 B apart (SBO), LBO unused for swizzled K-major (=1), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N>>3, M>>4.
+template <int N>
+__device__ __forceinline__ constexpr uint32_t idesc_bf16() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+#define FO_R8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : FO_R8(0), FO_R8(8), FO_R8(16), FO_R8(24)
+      : "r"(taddr));
+}
+#undef FO_R8
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Destination of row `a` (0..BM-1) of the tile at position `pos` = (ti, tj).
+__device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, int ti, int tj, int a, int BN) {
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.dst);
+  switch (p.mode) {
+    case EPI_ROWMAJOR:
+      return base + ((int64_t)ti * BM + a) * p.ldc + (int64_t)tj * BN;
+    case EPI_SLOT:  // slot pos, row-major
+      return base + ((int64_t)pos * BM + a) * BN;
+    case EPI_RS: {  // subtile k = a / h goes to chunk k of the group
+      const int g = p.group_of_pos[pos];
+      const int ps = p.gpos[g], G = p.gpos[g + 1] - ps;
+      const int k = a / p.h, a2 = a - k * p.h;
+      return base + ((int64_t)ps * BM + (int64_t)k * G * p.h + (int64_t)(pos - ps) * p.h + a2) * BN;
+    }
+    default:  // EPI_A2A: row -> slot in its destination pool
+      return base + (int64_t)p.row_slot[(int64_t)pos * BM + a] * BN;
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    fo_gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const GemmArgs p) {
+  using C = Cfg<BN>;
+  constexpr int ST = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                   // ST x 16 KB
+  uint8_t* sB = smem + ST * A_STAGE_BYTES;              // ST x BN*128 B
+  uint8_t* sEpi = smem + ST * C::STAGE_BYTES;           // 4 warps x 32 rows x pitch
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int KB = (int)(p.K / BK);
+
+  if (warp == 0) {
+    // ======================= TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pos = blockIdx.x; pos < p.tiles; pos += gridDim.x) {
+        const int t = p.order[pos];
+        const int ti = t / p.Nt, tj = t - ti * p.Nt;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, ti * BM, &full[stage]);
+          tma_load_2d(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, tj * BN, &full[stage]);
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16<BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int pos = blockIdx.x; pos < p.tiles; pos += gridDim.x) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = sw128_desc(smem_u32(sA + stage * A_STAGE_BYTES));
+          const uint64_t bdesc = sw128_desc(smem_u32(sB + stage * C::B_STAGE_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // +32 bytes along K inside the 128-byte swizzle row = +2 in the >>4 address field
+            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ======================= epilogue: reorder-store + signal
+    const int q = warp - 4;  // TMEM lane quarter: warp (4+q) may access lanes 32q..32q+31
+    uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int pos = blockIdx.x; pos < p.tiles; pos += gridDim.x) {
+      const int t = p.order[pos];
+      const int ti = t / p.Nt, tj = t - ti * p.Nt;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN / EPI_COLS; ++c) {
+        uint32_t v[64];
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * EPI_COLS);
+        tmem_ld32(taddr, v);
+        tmem_ld32(taddr + 32, v + 32);
+        tmem_wait_ld();
+        if (c == BN / EPI_COLS - 1) {
+          // accumulator fully read: hand the TMEM stage back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        // stage row `lane` (this thread's TMEM lane) as bf16
+        uint4* srow = reinterpret_cast<uint4*>(stg + lane * EPI_PITCH);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          uint4 w;
+          w.x = pack_bf16(v[8 * x + 0], v[8 * x + 1]);
+          w.y = pack_bf16(v[8 * x + 2], v[8 * x + 3]);
+          w.z = pack_bf16(v[8 * x + 4], v[8 * x + 5]);
+          w.w = pack_bf16(v[8 * x + 6], v[8 * x + 7]);
+          srow[x] = w;
+        }
+        __syncwarp();
+        // coalesced copy-out: each instruction moves 4 rows x 128 B
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + (lane >> 3);
+          const int ch = lane & 7;
+          const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + ch * 16);
+          __nv_bfloat16* d = row_dst(p, pos, ti, tj, q * 32 + r, BN) + c * EPI_COLS + ch * 8;
+          *reinterpret_cast<uint4*>(d) = w;
+        }
+        __syncwarp();
+      }
+      // all 128 epilogue threads finished this tile's stores -> one release add
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (q == 0 && lane == 0) {
+        if (p.counters) red_release_add(&p.counters[p.group_of_pos[pos]], 1u);
+        if (p.tile_ts) p.tile_ts[pos] = globaltimer();
+      }
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D K-major bf16 map over [rows, K] with a [box_rows, 64] box, 128B swizzle.
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(K * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+cudaError_t launch_bn(const GemmArgs& a, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fo_gemm_tcgen05_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, a.A, a.M, a.K, BM) || !make_map(&mB, a.Bt, a.N, a.K, BN)) return cudaErrorInvalidValue;
+  fo_gemm_tcgen05_kernel<BN><<<a.workers, NUM_THREADS, C::SMEM_BYTES, stream>>>(mA, mB, a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+std::atomic<int64_t> g_launches{0};
+
+}  // namespace
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+bool gemm_shape_supported(int bm, int bn) { return bm == BM && (bn == 64 || bn == 128 || bn == 256); }
+
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
+  if (a.BM != BM) return cudaErrorInvalidValue;
+  switch (a.BN) {
+    case 64: return launch_bn<64>(a, stream);
+    case 128: return launch_bn<128>(a, stream);
+    case 256: return launch_bn<256>(a, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace fo

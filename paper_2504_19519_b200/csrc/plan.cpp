@@ -1,0 +1,294 @@
+// Host-side plan construction: see plan.h.  Every map here is checked
+// element-by-element against oracle/ by tests/test_plan_parity.py.
+#include "plan.h"
+
+#include <algorithm>
+#include <numeric>
+
+namespace fo {
+
+std::vector<int32_t> default_order(int Mt, int Nt, int s) {
+  // DESIGN.md R1: row-panels of s tile-rows, panels top to
+  // bottom, inside a panel column by column with the tile-row index fastest.
+  std::vector<int32_t> o;
+  o.reserve((size_t)Mt * Nt);
+  for (int p0 = 0; p0 < Mt; p0 += s)
+    for (int j = 0; j < Nt; ++j)
+      for (int i = p0; i < std::min(p0 + s, Mt); ++i) o.push_back(i * Nt + j);
+  return o;
+}
+
+static void check_tile_shape(int BM, int BN) {
+  if (BM != 128 && BM != 256) fail(FO_ERR_UNSUPPORTED, "tile_m=%d not compiled (128 or 256)", BM);
+  if (BN != 64 && BN != 128 && BN != 256) fail(FO_ERR_UNSUPPORTED, "tile_n=%d not compiled (64/128/256)", BN);
+}
+
+struct Grid {
+  int Mt, Nt, tiles, T, P;
+  std::vector<int32_t> order, gpos, waves;
+};
+
+// O1-O3 for one descriptor (shared by self and A2A peers).
+static Grid make_grid(const fo_plan_desc& d, int world) {
+  if (d.m <= 0 || d.n <= 0 || d.k <= 0) fail(FO_ERR_SHAPE, "m, n, k must be positive");
+  check_tile_shape(d.tile_m, d.tile_n);
+  if (d.m % d.tile_m || d.n % d.tile_n)
+    fail(FO_ERR_SHAPE, "shape %lldx%lld not divisible by tile %dx%d", (long long)d.m, (long long)d.n,
+         d.tile_m, d.tile_n);
+  if (d.k % 64) fail(FO_ERR_SHAPE, "k=%lld must be a multiple of 64", (long long)d.k);
+  if (d.workers < 1) fail(FO_ERR_INVALID_ARG, "workers (wave width S) must be >= 1");
+  Grid g;
+  g.Mt = (int)(d.m / d.tile_m);
+  g.Nt = (int)(d.n / d.tile_n);
+  g.tiles = g.Mt * g.Nt;
+  if (d.tile_order) {
+    g.order.assign(d.tile_order, d.tile_order + g.tiles);
+    std::vector<char> seen(g.tiles, 0);
+    for (int32_t t : g.order) {
+      if (t < 0 || t >= g.tiles || seen[t]) fail(FO_ERR_INVALID_ARG, "tile_order is not a permutation");
+      seen[t] = 1;
+    }
+  } else {
+    if (d.swizzle < 1) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 1");
+    g.order = default_order(g.Mt, g.Nt, d.swizzle);
+  }
+  // T = ceil(tiles / S) (Alg. 1 line 3)
+  g.T = (g.tiles + d.workers - 1) / d.workers;
+  if (d.group_waves && d.num_groups > 0) {
+    g.waves.assign(d.group_waves, d.group_waves + d.num_groups);
+  } else {
+    g.waves.assign(1, g.T);
+  }
+  g.P = (int)g.waves.size();
+  long sum = 0;
+  for (int w : g.waves) {
+    if (w < 1) fail(FO_ERR_INVALID_ARG, "group of %d waves (must be >= 1)", w);
+    sum += w;
+  }
+  if (sum != g.T) fail(FO_ERR_INVALID_ARG, "group_waves sum to %ld but T=%d", sum, g.T);
+  // group j = positions [S*W_{j-1}, min(S*W_j, tiles))
+  g.gpos.assign(g.P + 1, 0);
+  long W = 0;
+  for (int j = 0; j < g.P; ++j) {
+    W += g.waves[j];
+    g.gpos[j + 1] = (int32_t)std::min<long>((long)d.workers * W, g.tiles);
+  }
+  (void)world;
+  return g;
+}
+
+// A2A send side of one source: pools per destination, subtokens
+// appended in execution order (position p, then row a).  Returns, per
+// destination d and group j, the (row, tile-col) list of that pool range.
+struct A2ASide {
+  std::vector<int64_t> cnt;    // [P*world]
+  std::vector<int64_t> start;  // [P*world] start within pool d
+  std::vector<int64_t> total;  // [world]
+};
+
+static A2ASide a2a_census(const fo_plan_desc& d, const Grid& g, int world) {
+  A2ASide a;
+  a.cnt.assign((size_t)g.P * world, 0);
+  a.start.assign((size_t)g.P * world, 0);
+  a.total.assign(world, 0);
+  for (int j = 0; j < g.P; ++j) {
+    for (int dd = 0; dd < world; ++dd) a.start[(size_t)j * world + dd] = a.total[dd];
+    for (int p = g.gpos[j]; p < g.gpos[j + 1]; ++p) {
+      int i = g.order[p] / g.Nt;
+      for (int r = 0; r < d.tile_m; ++r) {
+        int dst = d.row_dst[(int64_t)i * d.tile_m + r];
+        a.cnt[(size_t)j * world + dst]++;
+        a.total[dst]++;
+      }
+    }
+  }
+  return a;
+}
+
+PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_desc* const* peers,
+                    int /*sm_count*/) {
+  if (world < 1 || rank < 0 || rank >= world) fail(FO_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
+  if (d.coll < FO_ALLREDUCE || d.coll > FO_NOCOMM) fail(FO_ERR_INVALID_ARG, "unknown coll %d", d.coll);
+  if (d.post < FO_POST_NONE || d.post > FO_POST_ADD_RMSNORM) fail(FO_ERR_INVALID_ARG, "unknown post %d", d.post);
+  Grid g = make_grid(d, world);
+
+  PlanHost p;
+  p.coll = d.coll;
+  p.M = d.m; p.N = d.n; p.K = d.k;
+  p.BM = d.tile_m; p.BN = d.tile_n;
+  p.S = d.workers;
+  p.post = d.post;
+  p.eps = d.eps;
+  p.rank = rank; p.world = world;
+  p.Mt = g.Mt; p.Nt = g.Nt; p.tiles = g.tiles; p.T = g.T; p.P = g.P;
+  p.order = g.order;
+  p.group_waves = g.waves;
+  p.gpos = g.gpos;
+  p.pos_of_tile.assign(p.tiles, 0);
+  for (int q = 0; q < p.tiles; ++q) p.pos_of_tile[p.order[q]] = q;
+  p.group_of_pos.assign(p.tiles, 0);
+  for (int j = 0; j < p.P; ++j)
+    for (int q = p.gpos[j]; q < p.gpos[j + 1]; ++q) p.group_of_pos[q] = j;
+
+  const int64_t MN = p.M * p.N;
+  switch (p.coll) {
+    case FO_NOCOMM:
+      p.layout = FO_LAYOUT_ROWBAND;
+      p.out_rows = p.M;
+      p.send_elems = p.recv_elems = MN;
+      break;
+    case FO_ALLREDUCE: {
+      // ROWBAND (H11a) is legal iff the order is the raster and every
+      // group begins on a tile-row boundary: each group is then a row band of C.
+      bool raster = true;
+      for (int q = 0; q < p.tiles; ++q) raster = raster && (p.order[q] == q);
+      bool rows = true;
+      for (int j = 0; j < p.P; ++j) rows = rows && (p.gpos[j] % p.Nt == 0);
+      bool ok = raster && rows;
+      if (d.ar_layout == FO_LAYOUT_ROWBAND && !ok)
+        fail(FO_ERR_UNSUPPORTED, "ROWBAND layout needs a raster order and tile-row group boundaries");
+      p.layout = (d.ar_layout == FO_LAYOUT_SLOT) ? FO_LAYOUT_SLOT
+                 : ok                           ? FO_LAYOUT_ROWBAND
+                                                : FO_LAYOUT_SLOT;
+      p.out_rows = p.M;
+      p.send_elems = p.recv_elems = MN;
+      break;
+    }
+    case FO_REDUCESCATTER:
+      // subtile of h = BM/n rows (R7)
+      if (p.BM % world) fail(FO_ERR_SHAPE, "tile_m=%d not divisible by world=%d", p.BM, world);
+      p.h = p.BM / world;
+      p.out_rows = p.M / world;
+      p.send_elems = MN;
+      p.recv_elems = MN / world;
+      break;
+    case FO_ALLTOALL: {
+      if (!d.row_dst) fail(FO_ERR_INVALID_ARG, "All-to-All needs row_dst");
+      for (int64_t r = 0; r < p.M; ++r)
+        if (d.row_dst[r] < 0 || d.row_dst[r] >= world) fail(FO_ERR_INVALID_ARG, "row_dst[%lld] out of range", (long long)r);
+      p.row_dst.assign(d.row_dst, d.row_dst + p.M);
+      // ---- send side (self)
+      A2ASide me = a2a_census(d, g, world);
+      p.send_cnt = me.cnt;
+      p.send_start = me.start;
+      p.pool_base.assign(world + 1, 0);
+      for (int dd = 0; dd < world; ++dd) p.pool_base[dd + 1] = p.pool_base[dd] + me.total[dd];
+      p.send_elems = p.pool_base[world] * p.BN;
+      p.row_slot.assign((size_t)p.tiles * p.BM, -1);
+      {
+        std::vector<int64_t> fill(world, 0);
+        for (int q = 0; q < p.tiles; ++q) {
+          int i = p.order[q] / p.Nt;
+          for (int r = 0; r < p.BM; ++r) {
+            int dst = p.row_dst[(int64_t)i * p.BM + r];
+            p.row_slot[(size_t)q * p.BM + r] = (int32_t)(p.pool_base[dst] + fill[dst]++);
+          }
+        }
+      }
+      // ---- receive side: needs every source's descriptor (the census exchange)
+      if (!peers) fail(FO_ERR_INVALID_ARG, "All-to-All needs the peers' descriptors");
+      std::vector<Grid> pg(world);
+      for (int s = 0; s < world; ++s) {
+        const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
+        if (!ps) fail(FO_ERR_INVALID_ARG, "peer %d descriptor missing", s);
+        if (ps->n != d.n || ps->tile_n != d.tile_n || ps->tile_m != d.tile_m)
+          fail(FO_ERR_INVALID_ARG, "peer %d: n / tile shape differ", s);
+        if (!ps->row_dst) fail(FO_ERR_INVALID_ARG, "peer %d: row_dst missing", s);
+        pg[s] = make_grid(*ps, world);
+        if (pg[s].P != p.P) fail(FO_ERR_INVALID_ARG, "peer %d has %d groups, self %d", s, pg[s].P, p.P);
+      }
+      // output rows: sources ascending, then source rows ascending (all-to-all-v order)
+      p.src_base.assign(world + 1, 0);
+      std::vector<std::vector<int32_t>> rank_of_row(world);
+      for (int s = 0; s < world; ++s) {
+        const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
+        rank_of_row[s].assign(ps->m, -1);
+        int64_t c = 0;
+        for (int64_t r = 0; r < ps->m; ++r)
+          if (ps->row_dst[r] == rank) rank_of_row[s][r] = (int32_t)c++;
+        p.src_base[s + 1] = p.src_base[s] + c;
+      }
+      p.out_rows = p.src_base[world];
+      // receive layout [group j][source s] (R9)
+      p.recv_cnt.assign((size_t)p.P * world, 0);
+      p.recv_off.assign((size_t)p.P * world, 0);
+      std::vector<A2ASide> sides(world);
+      for (int s = 0; s < world; ++s) {
+        const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
+        sides[s] = a2a_census(*ps, pg[s], world);
+      }
+      int64_t off = 0;
+      for (int j = 0; j < p.P; ++j)
+        for (int s = 0; s < world; ++s) {
+          p.recv_off[(size_t)j * world + s] = off;
+          p.recv_cnt[(size_t)j * world + s] = sides[s].cnt[(size_t)j * world + rank];
+          off += sides[s].cnt[(size_t)j * world + rank];
+        }
+      p.recv_elems = off * p.BN;
+      p.src_row.assign((size_t)p.out_rows * p.Nt, -1);
+      for (int s = 0; s < world; ++s) {
+        const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
+        const Grid& gs = pg[s];
+        for (int j = 0; j < gs.P; ++j) {
+          int64_t idx = p.recv_off[(size_t)j * world + s];
+          for (int q = gs.gpos[j]; q < gs.gpos[j + 1]; ++q) {
+            int i = gs.order[q] / gs.Nt, jc = gs.order[q] % gs.Nt;
+            for (int r = 0; r < ps->tile_m; ++r) {
+              int64_t row = (int64_t)i * ps->tile_m + r;
+              if (ps->row_dst[row] != rank) continue;
+              int64_t orow = p.src_base[s] + rank_of_row[s][row];
+              p.src_row[(size_t)orow * p.Nt + jc] = (int32_t)idx++;
+            }
+          }
+        }
+      }
+      break;
+    }
+  }
+  if (p.coll != FO_ALLREDUCE) p.layout = (p.coll == FO_NOCOMM) ? FO_LAYOUT_ROWBAND : FO_LAYOUT_SLOT;
+  return p;
+}
+
+int64_t PlanHost::send_index(int64_t r, int64_t c) const {
+  const int i = (int)(r / BM), a = (int)(r % BM), jc = (int)(c / BN), b = (int)(c % BN);
+  const int q = pos_of_tile[i * Nt + jc];
+  switch (coll) {
+    case FO_NOCOMM:
+      return r * N + c;
+    case FO_ALLREDUCE:
+      if (layout == FO_LAYOUT_ROWBAND) return r * N + c;
+      return ((int64_t)q * BM + a) * BN + b;  // slot q, row-major
+    case FO_REDUCESCATTER: {
+      const int j = group_of_pos[q];
+      const int ps = gpos[j], G = gpos[j + 1] - gpos[j];
+      const int k = a / h, a2 = a % h;
+      return (int64_t)ps * BM * BN + (int64_t)k * G * h * BN + (int64_t)(q - ps) * h * BN + (int64_t)a2 * BN + b;
+    }
+    case FO_ALLTOALL:
+      return (int64_t)row_slot[(size_t)q * BM + a] * BN + b;
+  }
+  return -1;
+}
+
+int64_t PlanHost::recv_index(int64_t r, int64_t c) const {
+  const int jc = (int)(c / BN), b = (int)(c % BN);
+  switch (coll) {
+    case FO_NOCOMM:
+      return r * N + c;
+    case FO_ALLREDUCE: {
+      if (layout == FO_LAYOUT_ROWBAND) return r * N + c;
+      const int q = pos_of_tile[(r / BM) * Nt + jc];
+      return ((int64_t)q * BM + r % BM) * BN + b;
+    }
+    case FO_REDUCESCATTER: {
+      // local row l = i*h + a'  <-  receive row q*h + a' (group chunks in order)
+      const int q = pos_of_tile[(r / h) * Nt + jc];
+      return ((int64_t)q * h + r % h) * BN + b;
+    }
+    case FO_ALLTOALL:
+      return (int64_t)src_row[(size_t)r * Nt + jc] * BN + b;
+  }
+  return -1;
+}
+
+}  // namespace fo

@@ -1,0 +1,456 @@
+// Runtime: NCCL context, device plan state, and the overlapped op
+// (PAPER.md:297 fig:framework, PAPER.md:555 two-stream orchestration).
+//
+// fo_run on the caller stream `s`:
+//   1. reset the P group counters (counting table)
+//   2. fork: record E0 on s; the comm stream waits on E0
+//   3. s: persistent tcgen05 GEMM with the reorder+signal epilogue
+//   4. comm stream, for each group j: cuStreamWaitValue32(counter_j >= |G_j|)
+//      (a front-end wait, no SM spent — replaces the paper's spinning signal
+//      kernel) then the NCCL call on group j's contiguous range
+//   5. comm stream: post-communication reorder (+ fused add / RMSNorm)
+//   6. join: record E1 on the comm stream; s waits on E1
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "kernels.h"
+#include "runtime.h"
+
+struct fo_ctx_s {
+  int device = 0;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+};
+
+namespace fo {
+
+#define FO_CUDA(x)                                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess) fail(FO_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define FO_NCCL(x)                                                                          \
+  do {                                                                                      \
+    ncclResult_t r_ = (x);                                                                  \
+    if (r_ != ncclSuccess) fail(FO_ERR_NCCL, "%s: %s (%s:%d)", #x, ncclGetErrorString(r_), __FILE__, __LINE__); \
+  } while (0)
+
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static WaitValue32Fn wait_value_fn() {
+  static WaitValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitValue32Fn>(ptr);
+  });
+  return fn;
+}
+
+template <class T>
+static T* upload(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* d = nullptr;
+  FO_CUDA(cudaMalloc(&d, sizeof(T) * v.size()));
+  FO_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return d;
+}
+
+void release_device(fo_plan_s* p) {
+  if (p->device < 0) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(p->device);
+  for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
+                    (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
+                    p->d_rowmajor})
+    if (ptr) cudaFree(ptr);
+  cudaSetDevice(cur);
+  p->device = -1;
+}
+
+static void ensure_device(fo_plan_s* p) {
+  int dev = 0;
+  FO_CUDA(cudaGetDevice(&dev));
+  if (p->device == dev) return;
+  if (p->device >= 0) fail(FO_ERR_STATE, "plan bound to device %d, used on %d", p->device, dev);
+  const PlanHost& h = p->host;
+  if (!gemm_shape_supported(h.BM, h.BN))
+    fail(FO_ERR_UNSUPPORTED, "tile %dx%d not compiled into this build", h.BM, h.BN);
+  int major = 0, minor = 0;
+  FO_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  FO_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (major != 10 || minor != 0) fail(FO_ERR_UNSUPPORTED, "sm_%d%d device; this build targets sm_100a", major, minor);
+  p->device = dev;
+  p->d_order = upload(h.order);
+  p->d_pos_of_tile = upload(h.pos_of_tile);
+  p->d_group_of_pos = upload(h.group_of_pos);
+  p->d_gpos = upload(h.gpos);
+  p->d_row_slot = upload(h.row_slot);
+  p->d_src_row = upload(h.src_row);
+  FO_CUDA(cudaMalloc(&p->d_counters, sizeof(uint32_t) * h.P));
+  FO_CUDA(cudaMemset(p->d_counters, 0, sizeof(uint32_t) * h.P));
+  const bool need_send = !(h.coll == FO_NOCOMM || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND));
+  if (need_send && h.send_elems) FO_CUDA(cudaMalloc(&p->d_send, 2 * h.send_elems));
+  if ((h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && h.recv_elems)
+    FO_CUDA(cudaMalloc(&p->d_recv, 2 * h.recv_elems));
+}
+
+static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst, int mode, bool signal) {
+  const PlanHost& h = p->host;
+  GemmArgs a{};
+  a.A = A;
+  a.Bt = Bt;
+  a.dst = dst;
+  a.M = h.M;
+  a.N = h.N;
+  a.K = h.K;
+  a.BM = h.BM;
+  a.BN = h.BN;
+  a.Mt = h.Mt;
+  a.Nt = h.Nt;
+  a.tiles = h.tiles;
+  a.workers = h.S;
+  a.mode = mode;
+  a.ldc = h.N;
+  a.order = p->d_order;
+  a.group_of_pos = p->d_group_of_pos;
+  a.gpos = p->d_gpos;
+  a.row_slot = p->d_row_slot;
+  a.counters = signal ? p->d_counters : nullptr;
+  a.h = h.h;
+  a.tile_ts = nullptr;
+  return a;
+}
+
+// Epilogue mode + destination of the overlapped GEMM for this plan.
+static int epi_mode(const PlanHost& h) {
+  switch (h.coll) {
+    case FO_ALLREDUCE: return h.layout == FO_LAYOUT_ROWBAND ? EPI_ROWMAJOR : EPI_SLOT;
+    case FO_REDUCESCATTER: return EPI_RS;
+    case FO_ALLTOALL: return EPI_A2A;
+    default: return EPI_ROWMAJOR;
+  }
+}
+
+static void run_gemm(fo_plan_s* p, const void* A, const void* Bt, void* dst, int mode, bool signal,
+                     cudaStream_t s, unsigned long long* tile_ts = nullptr) {
+  if (!A || !Bt || !dst) fail(FO_ERR_INVALID_ARG, "null device pointer");
+  GemmArgs a = gemm_args(p, A, Bt, dst, mode, signal);
+  a.tile_ts = tile_ts;
+  FO_CUDA(launch_gemm(a, s));
+}
+
+static void run_post(fo_plan_s* p, int map, const void* src, void* out, const void* residual, const void* gamma,
+                     cudaStream_t s) {
+  const PlanHost& h = p->host;
+  if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
+  if (h.post == FO_POST_ADD_RMSNORM && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
+  PostArgs a{};
+  a.map = map;
+  a.op = h.post;
+  a.src = src;
+  a.out = out;
+  a.residual = residual;
+  a.gamma = gamma;
+  a.rows = h.out_rows;
+  a.N = h.N;
+  a.BM = h.BM;
+  a.BN = h.BN;
+  a.Nt = h.Nt;
+  a.h = h.h;
+  a.pos_of_tile = p->d_pos_of_tile;
+  a.src_row = p->d_src_row;
+  a.eps = h.eps;
+  FO_CUDA(launch_post(a, s));
+}
+
+static int post_map(const PlanHost& h) {
+  switch (h.coll) {
+    case FO_ALLREDUCE: return h.layout == FO_LAYOUT_ROWBAND ? POSTMAP_IDENTITY : POSTMAP_SLOT;
+    case FO_REDUCESCATTER: return POSTMAP_RS;
+    case FO_ALLTOALL: return POSTMAP_A2A;
+    default: return POSTMAP_IDENTITY;
+  }
+}
+
+static ncclDataType_t bf16() { return ncclBfloat16; }
+
+// The collective of group j, on the comm stream ("Once the j-th
+// number reaches |G_j|, the communication of G_j starts").
+static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* ar_base) {
+  const PlanHost& h = p->host;
+  cudaStream_t cs = c->comm_stream;
+  char* send = reinterpret_cast<char*>(p->d_send);
+  char* recv = reinterpret_cast<char*>(p->d_recv);
+  switch (h.coll) {
+    case FO_ALLREDUCE: {
+      char* base = reinterpret_cast<char*>(ar_base) + 2 * h.group_elem_begin(j);
+      const size_t count = (size_t)(h.group_elem_end(j) - h.group_elem_begin(j));
+      FO_NCCL(ncclAllReduce(base, base, count, bf16(), ncclSum, c->comm, cs));
+      break;
+    }
+    case FO_REDUCESCATTER: {
+      const int64_t b = h.group_elem_begin(j), e = h.group_elem_end(j);
+      FO_NCCL(ncclReduceScatter(send + 2 * b, recv + 2 * (b / h.world), (size_t)((e - b) / h.world), bf16(),
+                                ncclSum, c->comm, cs));
+      break;
+    }
+    case FO_ALLTOALL: {
+      const int W = h.world;
+      // self part: a device copy (no NCCL needed)
+      {
+        const int64_t cnt = h.send_cnt[(size_t)j * W + h.rank];
+        if (cnt) {
+          const int64_t so = (h.pool_base[h.rank] + h.send_start[(size_t)j * W + h.rank]) * h.BN;
+          const int64_t ro = h.recv_off[(size_t)j * W + h.rank] * h.BN;
+          FO_CUDA(cudaMemcpyAsync(recv + 2 * ro, send + 2 * so, 2 * cnt * h.BN, cudaMemcpyDeviceToDevice, cs));
+        }
+      }
+      FO_NCCL(ncclGroupStart());
+      for (int d = 0; d < W; ++d) {
+        if (d == h.rank) continue;
+        const int64_t sc = h.send_cnt[(size_t)j * W + d];
+        if (sc) {
+          const int64_t so = (h.pool_base[d] + h.send_start[(size_t)j * W + d]) * h.BN;
+          FO_NCCL(ncclSend(send + 2 * so, (size_t)(sc * h.BN), bf16(), d, c->comm, cs));
+        }
+        const int64_t rc = h.recv_cnt[(size_t)j * W + d];
+        if (rc) {
+          const int64_t ro = h.recv_off[(size_t)j * W + d] * h.BN;
+          FO_NCCL(ncclRecv(recv + 2 * ro, (size_t)(rc * h.BN), bf16(), d, c->comm, cs));
+        }
+      }
+      FO_NCCL(ncclGroupEnd());
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+}  // namespace fo
+
+using namespace fo;
+
+extern "C" {
+
+fo_status fo_device_sm_count(int32_t device, int32_t* sm_count) {
+  return guard([&] {
+    if (!sm_count) fail(FO_ERR_INVALID_ARG, "null argument");
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) n = 0;
+    *sm_count = n;
+  });
+}
+
+fo_status fo_get_unique_id(uint8_t uid[128]) {
+  return guard([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    FO_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(uid, &id, 128);
+  });
+}
+
+fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128], int32_t nccl_max_ctas,
+                        fo_ctx* out) {
+  return guard([&] {
+    if (!uid || !out || world < 1 || rank < 0 || rank >= world) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    FO_CUDA(cudaSetDevice(device));
+    auto* c = new fo_ctx_s();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    try {
+      ncclUniqueId id;
+      std::memcpy(&id, uid, 128);
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.blocking = 1;
+      if (nccl_max_ctas > 0) {
+        cfg.maxCTAs = nccl_max_ctas;
+        cfg.minCTAs = 1;
+      }
+      FO_NCCL(ncclCommInitRankConfig(&c->comm, world, id, rank, &cfg));
+      int lo = 0, hi = 0;
+      FO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      // highest priority for the communication stream
+      FO_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+      FO_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      FO_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    } catch (...) {
+      if (c->comm) ncclCommDestroy(c->comm);
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+fo_status fo_ctx_destroy(fo_ctx c) {
+  return guard([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    delete c;
+  });
+}
+
+fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
+                 const void* gamma, void* stream) {
+  return guard([&] {
+    if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    const PlanHost& h = p->host;
+    if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
+    ensure_device(p);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    WaitValue32Fn wait = wait_value_fn();
+    if (!wait) fail(FO_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
+    const bool rowband = (h.coll == FO_NOCOMM) || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND);
+    void* gemm_dst = rowband ? out : p->d_send;
+    // 1. counting table reset (every run starts from zero)
+    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * h.P, s));
+    // 2. fork
+    FO_CUDA(cudaEventRecord(c->ev_fork, s));
+    FO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+    // 3. GEMM with reorder + signal epilogue
+    run_gemm(p, A, Bt, gemm_dst, epi_mode(h), true, s);
+    // 4. per-group wait + collective
+    if (h.coll != FO_NOCOMM) {
+      for (int j = 0; j < h.P; ++j) {
+        CUresult r = wait(reinterpret_cast<CUstream>(c->comm_stream),
+                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), (cuuint32_t)h.group_tiles(j),
+                          CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        group_collective(c, p, j, gemm_dst);
+      }
+    } else {
+      // no communication: the comm stream only has to see the GEMM finish
+      for (int j = 0; j < h.P; ++j) {
+        CUresult r = wait(reinterpret_cast<CUstream>(c->comm_stream),
+                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), (cuuint32_t)h.group_tiles(j),
+                          CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      }
+    }
+    // 5. post-communication reorder (+ fused op)
+    const int map = post_map(h);
+    if (map != POSTMAP_IDENTITY || h.post != FO_POST_NONE) {
+      const void* src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : p->d_recv);
+      run_post(p, map, src, out, residual, gamma, c->comm_stream);
+    }
+    // 6. join
+    FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
+    FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  });
+}
+
+fo_status fo_run_sequential(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
+                            const void* gamma, void* stream) {
+  return guard([&] {
+    if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    const PlanHost& h = p->host;
+    if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
+    ensure_device(p);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t MN = h.M * h.N;
+    switch (h.coll) {
+      case FO_NOCOMM:
+      case FO_ALLREDUCE:
+        run_gemm(p, A, Bt, out, EPI_ROWMAJOR, false, s);
+        if (h.coll == FO_ALLREDUCE) FO_NCCL(ncclAllReduce(out, out, (size_t)MN, bf16(), ncclSum, c->comm, s));
+        break;
+      case FO_REDUCESCATTER: {
+        if (!p->d_rowmajor) FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * MN));
+        run_gemm(p, A, Bt, p->d_rowmajor, EPI_ROWMAJOR, false, s);
+        FO_NCCL(ncclReduceScatter(p->d_rowmajor, out, (size_t)(MN / h.world), bf16(), ncclSum, c->comm, s));
+        break;
+      }
+      case FO_ALLTOALL: {
+        for (int64_t r = 1; r < h.M; ++r)
+          if (h.row_dst[r] < h.row_dst[r - 1]) fail(FO_ERR_UNSUPPORTED, "sequential A2A needs row_dst sorted");
+        if (!p->d_rowmajor) FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * MN));
+        run_gemm(p, A, Bt, p->d_rowmajor, EPI_ROWMAJOR, false, s);
+        char* src = reinterpret_cast<char*>(p->d_rowmajor);
+        char* dst = reinterpret_cast<char*>(out);
+        std::vector<int64_t> rows_to(h.world, 0);
+        for (int64_t r = 0; r < h.M; ++r) rows_to[h.row_dst[r]]++;
+        FO_NCCL(ncclGroupStart());
+        int64_t soff = 0;
+        for (int d = 0; d < h.world; ++d) {
+          const int64_t rc = h.src_base[d + 1] - h.src_base[d];
+          if (d == h.rank) {
+            if (rows_to[d])
+              FO_CUDA(cudaMemcpyAsync(dst + 2 * h.src_base[d] * h.N, src + 2 * soff * h.N, 2 * rows_to[d] * h.N,
+                                      cudaMemcpyDeviceToDevice, s));
+          } else {
+            if (rows_to[d]) FO_NCCL(ncclSend(src + 2 * soff * h.N, (size_t)(rows_to[d] * h.N), bf16(), d, c->comm, s));
+            if (rc) FO_NCCL(ncclRecv(dst + 2 * h.src_base[d] * h.N, (size_t)(rc * h.N), bf16(), d, c->comm, s));
+          }
+          soff += rows_to[d];
+        }
+        FO_NCCL(ncclGroupEnd());
+        break;
+      }
+    }
+    if (h.post != FO_POST_NONE) run_post(p, POSTMAP_IDENTITY, out, out, residual, gamma, s);
+  });
+}
+
+fo_status fo_gemm_stage(fo_plan p, const void* A, const void* Bt, void* send, void* stream) {
+  return guard([&] {
+    if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
+    ensure_device(p);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->host.P, s));
+    run_gemm(p, A, Bt, send, epi_mode(p->host), true, s);
+  });
+}
+
+fo_status fo_gemm_stage_timed(fo_plan p, const void* A, const void* Bt, void* send, unsigned long long* tile_ts,
+                              void* stream) {
+  return guard([&] {
+    if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
+    ensure_device(p);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->host.P, s));
+    run_gemm(p, A, Bt, send, epi_mode(p->host), true, s, tile_ts);
+  });
+}
+
+fo_status fo_post_stage(fo_plan p, const void* recv, void* out, const void* residual, const void* gamma,
+                        void* stream) {
+  return guard([&] {
+    if (!p || !recv || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    ensure_device(p);
+    run_post(p, post_map(p->host), recv, out, residual, gamma, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+fo_status fo_plan_read_counters(fo_plan p, uint32_t* counters) {
+  return guard([&] {
+    if (!p || !counters) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (p->device < 0) fail(FO_ERR_STATE, "plan has no device state yet");
+    FO_CUDA(cudaDeviceSynchronize());
+    FO_CUDA(cudaMemcpy(counters, p->d_counters, sizeof(uint32_t) * p->host.P, cudaMemcpyDeviceToHost));
+  });
+}
+
+int64_t fo_kernel_launch_count(void) { return launch_count(); }
+
+}  // extern "C"

@@ -1,0 +1,26 @@
+// Runtime objects behind the opaque C handles.
+#pragma once
+
+#include <cstdint>
+
+#include "plan.h"
+
+struct fo_plan_s {
+  fo::PlanHost host;
+  // ---- device state (created lazily on first device use)
+  int device = -1;
+  int32_t* d_order = nullptr;
+  int32_t* d_pos_of_tile = nullptr;
+  int32_t* d_group_of_pos = nullptr;
+  int32_t* d_gpos = nullptr;
+  int32_t* d_row_slot = nullptr;
+  int32_t* d_src_row = nullptr;
+  uint32_t* d_counters = nullptr;
+  void* d_send = nullptr;  // pre-reordered send buffer (bf16), library-owned
+  void* d_recv = nullptr;  // receive buffer (RS / A2A)
+  void* d_rowmajor = nullptr;  // sequential baseline scratch (RS / A2A row-major C)
+};
+
+namespace fo {
+void release_device(fo_plan_s* p);
+}

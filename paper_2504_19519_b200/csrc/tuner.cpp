@@ -1,0 +1,123 @@
+// Alg. 1 "Grouping tuning algorithm": latency predictor
+// and pruned predictive search over wave-group partitions.  Host only.
+//
+// Readings: R13 the first group's predecessor has 0 comm latency;
+// R14 duration is measured at the actual wave width S, T = ceil(tiles/S);
+// R15 bandwidth is linear in log2(bytes) between samples, clamped; R16 ties go
+// to fewer groups, then the lexicographically smaller partition.
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "common.h"
+
+namespace fo {
+
+struct Curve {
+  std::vector<double> lx, bw;
+  double latency_us(double bytes) const {
+    if (bytes <= 0) return 0.0;
+    const double x = std::log2(bytes);
+    double b;
+    if (x <= lx.front()) b = bw.front();
+    else if (x >= lx.back()) b = bw.back();
+    else {
+      size_t k = 0;
+      while (!(lx[k] <= x && x <= lx[k + 1])) ++k;
+      const double f = (x - lx[k]) / (lx[k + 1] - lx[k]);
+      b = bw[k] + f * (bw[k + 1] - bw[k]);
+    }
+    return bytes / (b * 1e9) * 1e6;
+  }
+};
+
+static Curve make_curve(const double* bytes, const double* gbps, int n) {
+  if (n < 1 || !bytes || !gbps) fail(FO_ERR_INVALID_ARG, "empty bandwidth curve");
+  Curve c;
+  for (int i = 0; i < n; ++i) {
+    if (bytes[i] <= 0 || gbps[i] <= 0) fail(FO_ERR_INVALID_ARG, "curve point %d not positive", i);
+    if (i && bytes[i] <= bytes[i - 1]) fail(FO_ERR_INVALID_ARG, "curve sizes must increase");
+    c.lx.push_back(std::log2(bytes[i]));
+    c.bw.push_back(gbps[i]);
+  }
+  return c;
+}
+
+// Lines 10-22 of Alg. 1 for one candidate.
+static double predict(const std::vector<int>& G, double duration, int T, int tiles, int S, double tile_bytes,
+                      const Curve& c) {
+  auto size_of = [&](int i) {  // get_data_size(G_i): tiles of group i x bytes per tile
+    long W0 = 0;
+    for (int q = 0; q < i; ++q) W0 += G[q];
+    const long lo = (long)S * W0, hi = std::min<long>((long)S * (W0 + G[i]), tiles);
+    return (double)(hi - lo) * tile_bytes;
+  };
+  double acc_p = 0.0, acc_m = 0.0;
+  for (size_t i = 0; i < G.size(); ++i) {
+    const double t_m = i ? c.latency_us(size_of((int)i - 1)) : 0.0;
+    const double t_p = duration / T * G[i];
+    acc_m = std::max(acc_p, acc_m) + t_m;
+    acc_p = acc_p + t_p;
+  }
+  return std::max(acc_p, acc_m) + c.latency_us(size_of((int)G.size() - 1));
+}
+
+}  // namespace fo
+
+using namespace fo;
+
+extern "C" fo_status fo_tune_predict(const int32_t* groups, int32_t P, double duration_us, int32_t tiles,
+                                     int32_t S, double tile_bytes, const double* curve_bytes,
+                                     const double* curve_gbps, int32_t npts, double* predicted_us) {
+  return guard([&] {
+    if (!groups || P < 1 || !predicted_us || S < 1 || tiles < 1) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    const int T = (tiles + S - 1) / S;
+    std::vector<int> G(groups, groups + P);
+    long sum = 0;
+    for (int g : G) {
+      if (g < 1) fail(FO_ERR_INVALID_ARG, "zero-size group");
+      sum += g;
+    }
+    if (sum != T) fail(FO_ERR_INVALID_ARG, "groups sum to %ld, T=%d", sum, T);
+    *predicted_us = predict(G, duration_us, T, tiles, S, tile_bytes, make_curve(curve_bytes, curve_gbps, npts));
+  });
+}
+
+extern "C" fo_status fo_tune_search(double duration_us, int32_t tiles, int32_t S, double tile_bytes,
+                                    const double* curve_bytes, const double* curve_gbps, int32_t npts,
+                                    int32_t s1, int32_t sp, int32_t prune, int32_t* out_groups,
+                                    int32_t* out_num_groups, double* predicted_us) {
+  return guard([&] {
+    if (!out_groups || !out_num_groups || !predicted_us || S < 1 || tiles < 1) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    const int T = (tiles + S - 1) / S;
+    if (T > 30) fail(FO_ERR_UNSUPPORTED, "T=%d too large to enumerate", T);
+    const Curve c = make_curve(curve_bytes, curve_gbps, npts);
+    std::vector<int> best;
+    double best_t = std::numeric_limits<double>::infinity();
+    std::vector<int> G;
+    // line 7: the binary communicate/not decision after each wave but the last
+    for (uint32_t mask = 0; mask < (1u << (T - 1)); ++mask) {
+      G.clear();
+      int run = 0;
+      for (int w = 0; w < T; ++w) {
+        ++run;
+        if (w == T - 1 || ((mask >> w) & 1u)) {
+          G.push_back(run);
+          run = 0;
+        }
+      }
+      if (prune && T > 1 && (G.front() > s1 || G.back() > sp)) continue;
+      const double t = predict(G, duration_us, T, tiles, S, tile_bytes, c);
+      bool better = best.empty() || t < best_t ||
+                    (t == best_t && (G.size() < best.size() || (G.size() == best.size() && G < best)));
+      if (better) {
+        best = G;
+        best_t = t;
+      }
+    }
+    if (best.empty()) fail(FO_ERR_INVALID_ARG, "pruning left no candidate");
+    for (size_t i = 0; i < best.size(); ++i) out_groups[i] = best[i];
+    *out_num_groups = (int32_t)best.size();
+    *predicted_us = best_t;
+  });
+}

@@ -1,0 +1,275 @@
+"""GPU parity: the sm_100a kernels through the C ABI vs the CPU oracle.
+
+Exact-integer regime -> bit-exact buffers and outputs;
+float regime -> max |g - o| / max(|o|, rms(o)) <= 1e-2 (north_star tolerance).
+Multi-rank plans are exercised on ONE GPU through the stage entry points:
+fo_gemm_stage (GEMM + pre-reorder epilogue + counters) is compared with the
+oracle's send buffer, and fo_post_stage is fed the oracle's receive buffer (what
+NCCL delivers) and compared with the oracle's output.  fo_run itself (streams,
+stream waits, NCCL) is exercised at world = 1.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synthetic
+from oracle import collectives as oc
+from oracle import numerics as onum
+from oracle import pipeline as opl
+from oracle import plan as op
+from oracle import post as opost
+from oracle import reorder as orr
+
+pytestmark = pytest.mark.gpu
+
+fo = pytest.importorskip("paper_2504_19519_b200")
+TOL = 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    fo.load()
+    torch.cuda.set_device(0)
+    yield
+
+
+@pytest.fixture(scope="module")
+def ctx1():
+    c = fo.Context.create(0, 0, 1, fo.unique_id())
+    yield c
+    c.close()
+
+
+def _dev_bf16(x):
+    if isinstance(x, torch.Tensor):
+        return x.to(torch.bfloat16).cuda().contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).cuda()
+
+
+def _host(t):
+    return t.double().cpu().numpy()
+
+
+def _rel_err(g, o):
+    g, o = np.asarray(g, np.float64), np.asarray(o, np.float64)
+    rms = np.sqrt(np.mean(o * o)) if o.size else 1.0
+    return float(np.max(np.abs(g - o) / np.maximum(np.abs(o), rms))) if o.size else 0.0
+
+
+def _counters_ok(plan, oplan):
+    assert plan.read_counters().tolist() == op.group_thresholds(oplan.partition, oplan.S, oplan.ntiles)
+
+
+# ------------------------------------------------------------------ plain GEMM
+@pytest.mark.parametrize("BN", [64, 128, 256])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (384, 512, 320), (256, 768, 1024)])
+def test_gemm_rowmajor_exact(BN, shape):
+    M, N, K = shape
+    if N % BN:
+        pytest.skip("N % BN")
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=M + N + K, nnz_per_row=256)
+    tiles = (M // 128) * (N // BN)
+    S = max(1, min(tiles, 7))
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=2)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, _dev_bf16(A), _dev_bf16(Bt), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(out), onum.gemm(A, Bt))
+    _counters_ok(plan, op.make_plan(M, N, 128, BN, S, None, swizzle=2))
+
+
+@pytest.mark.parametrize("BN", [128, 256])
+def test_gemm_float_regime(BN):
+    M, N, K = 512, 512, 2048
+    A, Bt = synthetic.float_inputs(M, N, K, seed=11)
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_n=BN, workers=5)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, _dev_bf16(A), _dev_bf16(Bt), out)
+    torch.cuda.synchronize()
+    assert _rel_err(_host(out), onum.gemm(A, Bt)) <= TOL
+
+
+# ------------------------------------------------------------------ multi-rank stages on one GPU
+def _rank_inputs(n, M, N, K, seed, exact=True):
+    As, Bts = [], []
+    for r in range(n):
+        if exact:
+            A, Bt = synthetic.exact_inputs(M, N, K, seed=synthetic.rank_seed(seed, n, r), nnz_per_row=max(1, 256 // n))
+        else:
+            A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.rank_seed(seed, n, r))
+        As.append(A)
+        Bts.append(Bt)
+    return As, Bts
+
+
+CASES = [
+    # M, N, K, BN, S, groups, swizzle
+    (512, 512, 128, 128, 3, None, 2),
+    (384, 768, 192, 256, 2, None, 1),
+    (640, 256, 64, 64, 4, None, 3),
+]
+
+
+def _groups(tiles, S, seed):
+    return synthetic.random_partition(op.num_waves(tiles, S), seed)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("case", range(len(CASES)))
+@pytest.mark.parametrize("layout", ["slot", "auto"])
+def test_allreduce_stages_exact(n, case, layout):
+    M, N, K, BN, S, _, swz = CASES[case]
+    tiles = (M // 128) * (N // BN)
+    groups = _groups(tiles, S, case + 10 * n)
+    order = synthetic.random_order(tiles, case) if (case == 1 and layout == "slot") else None
+    As, Bts = _rank_inputs(n, M, N, K, 100 + case)
+    oplan = op.make_plan(M, N, 128, BN, S, groups, order=order, swizzle=swz)
+    plans = [fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_n=BN, workers=S, tile_order=order, swizzle=swz,
+                     group_waves=groups, ar_layout=layout, rank=r, world=n) for r in range(n)]
+    lay = "rowband" if plans[0].info["ar_layout"] == 1 else "slot"
+    ores = opl.run_allreduce(As, Bts, oplan, layout=lay)
+    for r in range(n):
+        send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plans[r], _dev_bf16(As[r]), _dev_bf16(Bts[r]), send)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(send), ores["send"][r]), f"rank {r} send buffer"
+        _counters_ok(plans[r], oplan)
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plans[r], _dev_bf16(ores["recv"][r]), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(out), opl.plain_allreduce(As, Bts)[r])
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_reducescatter_stages_exact(n, case):
+    M, N, K, BN, S, _, swz = CASES[case]
+    tiles = (M // 128) * (N // BN)
+    groups = _groups(tiles, S, case + 20 * n)
+    As, Bts = _rank_inputs(n, M, N, K, 200 + case)
+    oplan = op.make_plan(M, N, 128, BN, S, groups, swizzle=swz)
+    ores = opl.run_reducescatter(As, Bts, oplan)
+    plain = opl.plain_reducescatter(As, Bts, 128)
+    for r in range(n):
+        plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=swz, group_waves=groups,
+                       rank=r, world=n)
+        send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, _dev_bf16(As[r]), _dev_bf16(Bts[r]), send)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(send), ores["send"][r]), f"rank {r} send buffer"
+        _counters_ok(plan, oplan)
+        out = torch.empty(M // n, N, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plan, _dev_bf16(ores["recv"][r]), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(out), plain[r])
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_alltoall_stages_exact(n):
+    rng = np.random.default_rng(n)
+    N, K, BN, P = 512, 128, 128, 2
+    specs, oplans, As, Bts, rds = [], [], [], [], []
+    for s in range(n):
+        Mt = int(rng.integers(2, 5))
+        M = Mt * 128
+        tiles = Mt * (N // BN)
+        S = int(rng.integers(1, tiles // P + 1))
+        T = op.num_waves(tiles, S)
+        part = [1] * (P - 1) + [T - (P - 1)]
+        rd = synthetic.random_row_dst(M, n, 1000 + s)
+        A, Bt = synthetic.exact_inputs(M, N, K, seed=300 + s, nnz_per_row=64)
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=2, group_waves=part,
+                          row_dst=rd))
+        oplans.append(op.make_plan(M, N, 128, BN, S, part, swizzle=2))
+        As.append(A), Bts.append(Bt), rds.append(rd)
+    ores = opl.run_alltoall(As, Bts, oplans, rds)
+    plain = opl.plain_alltoall(As, Bts, rds)
+    for me in range(n):
+        plan = fo.Plan(rank=me, world=n, peers=specs, **specs[me])
+        send = torch.empty(plan.info["send_elems"], dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, _dev_bf16(As[me]), _dev_bf16(Bts[me]), send)
+        torch.cuda.synchronize()
+        flat = np.concatenate([ores["send"][me].pools[d].reshape(-1) for d in range(n)])
+        assert np.array_equal(_host(send), flat)
+        _counters_ok(plan, oplans[me])
+        recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][me]]) if ores["recv"][me] else np.zeros(0)
+        out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plan, _dev_bf16(recv), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(out), plain[me])
+
+
+# ------------------------------------------------------------------ fused elementwise (float regime)
+@pytest.mark.parametrize("post", ["add", "add_rmsnorm"])
+def test_post_fused_ops(post):
+    M, N, K, BN, S = 512, 1024, 256, 256, 3
+    tiles = (M // 128) * (N // BN)
+    groups = _groups(tiles, S, 7)
+    A, Bt = synthetic.float_inputs(M, N, K, seed=3)
+    res = synthetic.normal_bf16((M, N), 1.0, 99)
+    gamma = synthetic.normal_bf16((N,), 1.0, 98)
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=2, group_waves=groups,
+                   ar_layout="slot", post=post, eps=1e-5)
+    oplan = op.make_plan(M, N, 128, BN, S, groups, swizzle=2)
+    ores = opl.run_allreduce([A], [Bt], oplan, model_bf16=True)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.post_stage(plan, _dev_bf16(ores["recv"][0]), out, _dev_bf16(res), _dev_bf16(gamma))
+    torch.cuda.synchronize()
+    x = ores["out"][0]
+    want = opost.add(x, onum.to_f64(res)) if post == "add" else opost.add_rmsnorm(x, onum.to_f64(res), onum.to_f64(gamma), 1e-5)
+    assert _rel_err(_host(out), want) <= TOL
+
+
+# ------------------------------------------------------------------ full path with NCCL (world = 1)
+@pytest.mark.parametrize("coll", ["allreduce", "reducescatter", "alltoall", "nocomm"])
+@pytest.mark.parametrize("post", ["none", "add_rmsnorm"])
+def test_fo_run_world1(ctx1, coll, post):
+    M, N, K, BN, S = 512, 512, 256, 128, 5
+    tiles = (M // 128) * (N // BN)
+    groups = _groups(tiles, S, 3)
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=5, nnz_per_row=200)
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=2, group_waves=groups, post=post)
+    if coll == "alltoall":
+        kw["row_dst"] = np.zeros(M, np.int32)
+        plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
+    else:
+        plan = fo.Plan(**kw)
+    res = synthetic.normal_bf16((M, N), 1.0, 1)
+    gamma = synthetic.normal_bf16((N,), 1.0, 2)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    args = (_dev_bf16(res), _dev_bf16(gamma)) if post != "none" else (None, None)
+    Ad, Bd = _dev_bf16(A), _dev_bf16(Bt)
+    for _ in range(3):  # repeated runs: counters reset each time
+        fo.run(ctx1, plan, Ad, Bd, out, *args)
+    torch.cuda.synchronize()
+    C = onum.gemm(A, Bt)
+    if post == "none":
+        assert np.array_equal(_host(out), C)
+    else:
+        want = opost.add_rmsnorm(C, onum.to_f64(res), onum.to_f64(gamma), 1e-5)
+        assert _rel_err(_host(out), want) <= TOL
+    out2 = torch.empty_like(out)
+    if coll != "alltoall" or True:
+        fo.run_sequential(ctx1, plan, Ad, Bd, out2, *args)
+        torch.cuda.synchronize()
+        if post == "none":
+            assert np.array_equal(_host(out2), C)
+
+
+def test_tile_timestamps_follow_waves():
+    """Per-tile %globaltimer: every tile of wave w+1 signals after the first
+    tile of wave w (wave pattern; X1 analogue)."""
+    M, N, K, BN = 2048, 2048, 4096, 256
+    S = 16
+    A, Bt = synthetic.float_inputs(M, N, K, seed=1)
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_n=BN, workers=S)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    ts = torch.zeros(plan.info["tiles"], dtype=torch.int64, device="cuda")
+    fo.gemm_stage_timed(plan, _dev_bf16(A), _dev_bf16(Bt), out, ts)
+    torch.cuda.synchronize()
+    t = ts.cpu().numpy().astype(np.int64)
+    waves = t.reshape(-1, S)
+    assert (waves[1:].min(axis=1) > waves[:-1].min(axis=1)).all()

@@ -1,0 +1,201 @@
+"""C-ABI library (host part) vs the oracle: bit-exact index maps, group
+ranges, A2A census, Alg. 1 — all on CPU, no GPU needed.
+
+Also checks that libflashoverlap.so loads and exports every symbol declared in
+include/flashoverlap.h."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synthetic
+from oracle import alg1
+from oracle import collectives as oc
+from oracle import plan as op
+from oracle import reorder as orr
+
+fo = pytest.importorskip("paper_2504_19519_b200")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    fo.load()
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "flashoverlap.h")).read()
+    declared = set(re.findall(r"^\s*(?:fo_status|const char\*|int64_t)\s+(fo_[a-z0-9_]+)\s*\(", hdr, re.M))
+    lib = fo.load()
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared but not exported"
+    from paper_2504_19519_b200 import _lib
+    assert declared == set(_lib.SYMBOLS)
+
+
+def _oracle_send_map(Y_idx_buf):
+    inv = np.empty(Y_idx_buf.size, np.int64)
+    inv[Y_idx_buf.astype(np.int64)] = np.arange(Y_idx_buf.size)
+    return inv
+
+
+def _rand_case(rng, coll, world, BN_choices=(64, 128, 256)):
+    BM = 128
+    BN = int(rng.choice(BN_choices))
+    Mt, Nt = int(rng.integers(1, 5)), int(rng.integers(1, 4))
+    tiles = Mt * Nt
+    S = int(rng.integers(1, tiles + 1))
+    T = op.num_waves(tiles, S)
+    part = synthetic.random_partition(T, int(rng.integers(1 << 30)))
+    use_order = rng.random() < 0.5
+    order = synthetic.random_order(tiles, int(rng.integers(1 << 30))) if use_order else None
+    swz = int(rng.integers(1, 4))
+    return dict(M=Mt * BM, N=Nt * BN, BM=BM, BN=BN, S=S, part=part, order=order, swz=swz)
+
+
+def _fo_plan(c, coll, rank=0, world=1, layout="auto", row_dst=None, peers=None):
+    return fo.Plan(coll=coll, m=c["M"], n=c["N"], k=64, tile_m=c["BM"], tile_n=c["BN"], workers=c["S"],
+                   tile_order=c["order"], swizzle=c["swz"], group_waves=c["part"], ar_layout=layout,
+                   row_dst=row_dst, rank=rank, world=world, peers=peers)
+
+
+def _op_plan(c):
+    return op.make_plan(c["M"], c["N"], c["BM"], c["BN"], c["S"], c["part"], order=c["order"], swizzle=c["swz"])
+
+
+@pytest.mark.parametrize("layout", ["slot", "auto"])
+def test_allreduce_maps(layout):
+    rng = np.random.default_rng(10)
+    for _ in range(40):
+        c = _rand_case(rng, "allreduce", 1)
+        pl = _fo_plan(c, "allreduce", layout=layout)
+        o = _op_plan(c)
+        assert pl.export_order().tolist() == o.order.tolist()
+        lay = "rowband" if pl.info["ar_layout"] == 1 else "slot"
+        if layout == "auto":
+            assert (lay == "rowband") == orr.ar_rowband_ok(o)
+        Y = np.arange(c["M"] * c["N"], dtype=float).reshape(c["M"], c["N"])
+        buf = orr.ar_pre(Y, o, lay)
+        assert np.array_equal(pl.export_send_map(), _oracle_send_map(buf))
+        post = orr.ar_post(np.arange(c["M"] * c["N"], dtype=float), o, lay)
+        assert np.array_equal(pl.export_recv_map(), post.reshape(-1).astype(np.int64))
+        for j, ((lo, hi), (elo, ehi)) in enumerate(zip(o.ranges, orr.group_elem_ranges(o))):
+            assert pl.group(j) == (lo, hi, elo, ehi)
+        assert pl.info["waves"] == o.T and pl.info["tiles"] == o.ntiles
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_reducescatter_maps(world):
+    rng = np.random.default_rng(20 + world)
+    for _ in range(25):
+        c = _rand_case(rng, "reducescatter", world)
+        o = _op_plan(c)
+        for rank in range(world):
+            pl = _fo_plan(c, "reducescatter", rank=rank, world=world)
+            Y = np.arange(c["M"] * c["N"], dtype=float).reshape(c["M"], c["N"])
+            buf = orr.rs_pre(Y, o, world)
+            assert np.array_equal(pl.export_send_map(), _oracle_send_map(buf))
+            n_recv = c["M"] * c["N"] // world
+            post = orr.rs_post(np.arange(n_recv, dtype=float), o, world)
+            assert np.array_equal(pl.export_recv_map(), post.reshape(-1).astype(np.int64))
+            assert pl.info["rs_subtile_rows"] == c["BM"] // world
+            assert pl.info["out_rows"] == c["M"] // world
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_alltoall_maps_and_census(world):
+    rng = np.random.default_rng(30 + world)
+    for case in range(12):
+        BN = int(rng.choice([64, 128]))
+        Nt = int(rng.integers(1, 3))
+        N = Nt * BN
+        P = int(rng.integers(1, 3))
+        specs, oplans, row_dsts = [], [], []
+        for s in range(world):
+            Mt = int(rng.integers(max(1, P), 4))
+            tiles = Mt * Nt
+            # choose S so that T >= P
+            S = int(rng.integers(1, max(1, tiles // P) + 1))
+            T = op.num_waves(tiles, S)
+            part = [1] * (P - 1) + [T - (P - 1)]
+            order = synthetic.random_order(tiles, int(rng.integers(1 << 30))) if rng.random() < 0.5 else None
+            rd = synthetic.random_row_dst(Mt * 128, world, int(rng.integers(1 << 30)))
+            specs.append(dict(coll="alltoall", m=Mt * 128, n=N, k=64, tile_m=128, tile_n=BN, workers=S,
+                              tile_order=order, swizzle=1, group_waves=part, row_dst=rd))
+            oplans.append(op.make_plan(Mt * 128, N, 128, BN, S, part, order=order, swizzle=1))
+            row_dsts.append(rd)
+        sends = [orr.a2a_pre(np.arange(oplans[s].M * N, dtype=float).reshape(-1, N), oplans[s], row_dsts[s], world)
+                 for s in range(world)]
+        recv = oc.alltoall_groups(sends, P)
+        for me in range(world):
+            pl = fo.Plan(rank=me, world=world, peers=specs, **specs[me])
+            # send map: pools concatenated by destination
+            flat = np.concatenate([sends[me].pools[d].reshape(-1) for d in range(world)])
+            assert np.array_equal(pl.export_send_map(), _oracle_send_map(flat))
+            sc, rc = pl.export_a2a_counts()
+            for j in range(P):
+                for d in range(world):
+                    a, b = sends[me].ranges[d][j]
+                    assert sc[j, d] == b - a
+                    a, b = sends[d].ranges[me][j]
+                    assert rc[j, d] == b - a
+            # recv map: receive layout [group][source]
+            parts, idx = [], 0
+            for s, chunk in recv[me]:
+                parts.append((s, np.arange(idx * BN, (idx + len(chunk)) * BN, dtype=float).reshape(-1, BN)))
+                idx += len(chunk)
+            post = orr.a2a_post(parts, [sends[s].meta[me] for s in range(world)], row_dsts, me, N, BN)
+            assert pl.info["out_rows"] == post.shape[0]
+            assert np.array_equal(pl.export_recv_map(), post.reshape(-1).astype(np.int64))
+
+
+def test_error_contract():
+    base = dict(coll="allreduce", m=256, n=256, k=64, tile_m=128, tile_n=128, workers=2)
+    with pytest.raises(fo.FOError, match="SHAPE"):
+        fo.Plan(**{**base, "m": 200})
+    with pytest.raises(fo.FOError, match="SHAPE"):
+        fo.Plan(**{**base, "k": 100})
+    with pytest.raises(fo.FOError, match="INVALID_ARG"):
+        fo.Plan(**{**base, "tile_order": [0, 0, 1, 2]})
+    with pytest.raises(fo.FOError, match="INVALID_ARG"):
+        fo.Plan(**{**base, "group_waves": [1]})          # T = 2
+    with pytest.raises(fo.FOError, match="INVALID_ARG"):
+        fo.Plan(**{**base, "group_waves": [0, 2]})
+    with pytest.raises(fo.FOError, match="UNSUPPORTED"):
+        fo.Plan(**{**base, "tile_n": 96})
+    with pytest.raises(fo.FOError, match="SHAPE"):
+        fo.Plan(**{**base, "coll": "reducescatter", "tile_m": 128}, rank=0, world=3)
+    with pytest.raises(fo.FOError, match="INVALID_ARG"):
+        fo.Plan(**{**base, "coll": "alltoall", "row_dst": [0] * 255 + [2]}, rank=0, world=2,
+                peers=[{**base, "coll": "alltoall", "row_dst": [0] * 256}] * 2)
+    with pytest.raises(fo.FOError, match="UNSUPPORTED"):
+        fo.Plan(**{**base, "ar_layout": "rowband", "swizzle": 2})
+
+
+def test_tuner_matches_oracle():
+    rng = np.random.default_rng(5)
+    for _ in range(60):
+        S = int(rng.integers(1, 80))
+        tiles = int(rng.integers(1, 10 * S + 1))
+        T = op.num_waves(tiles, S)
+        if T > 12:
+            continue
+        tile_bytes = float(rng.choice([8192, 65536, 131072]))
+        xs = sorted(set(int(2 ** x) for x in rng.uniform(10, 30, size=6)))
+        curve = [(x, float(rng.uniform(1, 700))) for x in xs]
+        dur = float(rng.uniform(5, 500))
+        lat = lambda b: alg1.interp_latency_us(curve, b)
+        sizes_of = lambda G: alg1.group_bytes(G, S, tiles, tile_bytes)
+        for prune in (True, False):
+            want, want_t = alg1.search(T, dur, sizes_of, lat, prune=prune)
+            got, got_t = fo.tune_search(dur, tiles, S, tile_bytes, curve, prune=prune)
+            assert got == want
+            assert got_t == pytest.approx(want_t, rel=1e-12)
+        G = tuple(synthetic.random_partition(T, int(rng.integers(1 << 20))))
+        assert fo.tune_predict(G, dur, tiles, S, tile_bytes, curve) == pytest.approx(
+            alg1.predict(G, dur, T, sizes_of(G), lat), rel=1e-12)
