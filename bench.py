@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the overlapped GEMM + collective layer (BASELINE.json metric):
+overlapped GEMM+AllReduce us per layer, speedup vs the same GEMM followed by a
+non-overlapped NCCL call, and % of roofline.
+
+Workload (BASELINE.json configs[1]): Llama-3-8B row-parallel down-proj,
+M=4096 tokens, N=4096, K=14336/TP, bf16, AllReduce at TP = --gpus.
+At --gpus 1 this is TP=1 (K=14336, the AllReduce is a 1-rank NCCL call).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fo|reference]
+
+One JSON line on rank 0.  Timing: W untimed warm-up steps, then K steps, each
+bracketed by (barrier,) an L2 flush (256 MiB write, outside the timed span) and
+CUDA events on the launching stream; per-step device time, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+M_TOK, N_HID, K_FFN = 4096, 4096, 14336
+BM, BN = 128, 256
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fo", choices=["fo", "reference"])
+    ap.add_argument("--comm-sms", type=int, default=None, help="SMs left free for NCCL (default 0 at N=1, 20 else)")
+    ap.add_argument("--groups", default=None, help="explicit wave-group partition, e.g. 1,1,2 (default: Alg. 1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle sample")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def workload(n):
+    K = K_FFN // n
+    return dict(workload=f"llama3-8b-down-proj-allreduce-tp{n}", M=M_TOK, N=N_HID, K_loc=K, K=K_FFN, tp=n,
+                collective="allreduce", tile=f"{BM}x{BN}", dtype="bf16")
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if num(r[0])]
+        mx = [num(r[1]) for r in self.rows if num(r[1])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_sample(wl, n, target_s):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload:
+    the full pipeline (n fp64 rank GEMMs -> AR pre-reorder -> explicit per-group
+    AllReduce -> post-reorder) for `rows` output rows of every rank; scaled to
+    the full M.  Returns (us per full layer, description, threads)."""
+    import torch
+
+    import synthetic
+    from oracle import pipeline as opl
+    from oracle import plan as op
+
+    M, N, K = wl["M"], wl["N"], wl["K_loc"]
+
+    def run(rows):
+        As, Bts = [], []
+        for r in range(n):
+            A, Bt = synthetic.float_inputs(rows, N, K, seed=synthetic.rank_seed(20000, n, r))
+            As.append(A)
+            Bts.append(Bt)
+        tiles = (rows // BM) * (N // BN)
+        pl = op.make_plan(rows, N, BM, BN, min(tiles, 148), None)
+        t0 = time.perf_counter()
+        opl.run_allreduce(As, Bts, pl)
+        return time.perf_counter() - t0
+
+    t1 = run(BM)
+    rows = int(min(M, max(BM, BM * round(target_s / max(t1, 1e-3)))))
+    rows = max(BM, (rows // BM) * BM)
+    t = run(rows) if rows != BM else t1
+    us = t * 1e6 * (M / rows)
+    threads = torch.get_num_threads()
+    try:
+        import numpy.__config__  # noqa: F401
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count()
+    desc = (f"oracle run_allreduce on {rows} of {M} rows x all {N} cols, K={K}, {n} simulated rank(s): "
+            f"{t:.2f} s, scaled x{M / rows:.1f} to the full layer")
+    return us, desc, cores or threads
+
+
+# --------------------------------------------------------------------------- reference arm
+def reference_arm(args, wl, rank, world):
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    per = max(0.5, min(10.0, 120.0 / max(1, K + W)))
+    times, desc, cores = [], "", 1
+    for i in range(W + K):
+        us, desc, cores = cpu_oracle_sample(wl, world, per)
+        if i >= W:
+            times.append(us)
+    v = statistics.mean(times)
+    line = {"impl": "reference", "metric": "overlapped GEMM+AllReduce us per layer", "value": round(v, 1),
+            "unit": "us", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(v / 1e3, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective")},
+            "cpu_baseline": {"value": round(v, 1), "unit": "us", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": round(v, 1), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    wl = workload(world)
+    if args.impl == "reference":
+        return reference_arm(args, wl, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_19519_b200 as fo
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peak_src = load_peaks()
+    sms = fo.device_sm_count(local)
+    comm_sms = args.comm_sms if args.comm_sms is not None else (0 if world == 1 else 20)
+    S = sms - comm_sms
+    M, N, K = wl["M"], wl["N"], wl["K_loc"]
+    tiles = (M // BM) * (N // BN)
+    T = (tiles + S - 1) // S
+
+    # ---- inputs (synthetic, seeded; SURVEY §8(d) recipe), resident in HBM
+    import synthetic
+    A_h, B_h = synthetic.float_inputs(M, N, K, seed=synthetic.rank_seed(20000, world, rank))
+    A = A_h.cuda()
+    Bt = B_h.cuda()
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    # ---- NCCL context of the library (unique id broadcast over the process group)
+    if world > 1:
+        obj = [fo.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    else:
+        uid = fo.unique_id()
+    ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=comm_sms if world > 1 else 0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def timed(fn, steps, warm):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e) * 1e3)
+        mean = statistics.mean(ts)
+        if world > 1:
+            t = torch.tensor([mean], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            mean = t.item()
+        return mean, ts
+
+    # ---- offline stage of Alg. 1 (untimed): GEMM duration at S, NCCL AR curve
+    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S)
+    gemm_us, _ = timed(lambda: fo.gemm_stage(gplan, A, Bt, out), 5, 2)
+    if world > 1:
+        curve = []
+        for sz in [1 << s for s in range(18, 27)]:
+            buf = torch.empty(sz // 2, dtype=torch.bfloat16, device="cuda")
+            t, _ = timed(lambda: dist.all_reduce(buf), 5, 2)
+            curve.append((sz, sz / (t * 1e-6) / 1e9))
+    else:
+        curve = [(1 << 10, 1e6), (1 << 30, 1e6)]  # 1 rank: the collective moves no bytes
+    if args.groups:
+        groups = tuple(int(x) for x in args.groups.split(","))
+        pred = fo.tune_predict(groups, gemm_us, tiles, S, BM * BN * 2, curve)
+    else:
+        groups, pred = fo.tune_search(gemm_us, tiles, S, BM * BN * 2, curve)
+
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=list(groups),
+                   ar_layout="auto", rank=rank, world=world)
+
+    # ---- full-size spot check (N=1: sampled rows vs an fp64 torch CPU product; not the oracle)
+    fo.run(ctx, plan, A, Bt, out)
+    torch.cuda.synchronize()
+    spot = None
+    if world == 1:
+        rows = torch.randperm(M, generator=torch.Generator().manual_seed(0))[:8]
+        ref = A_h[rows].double() @ B_h.double().t()
+        got = out[rows.cuda()].double().cpu()
+        rms = ref.pow(2).mean().sqrt()
+        spot = {"rows": 8, "max_rel_err": float(((got - ref).abs() / torch.maximum(ref.abs(), rms)).max())}
+
+    # ---- timed: overlapped, sequential, GEMM kernel alone
+    launches0 = fo.kernel_launch_count()
+    with ClockSampler(local) as clk:
+        ov_us, ov_all = timed(lambda: fo.run(ctx, plan, A, Bt, out), args.steps, args.warmup)
+    launches = (fo.kernel_launch_count() - launches0) * args.steps // (args.steps + args.warmup)
+    seq_us, _ = timed(lambda: fo.run_sequential(ctx, plan, A, Bt, out), args.steps, args.warmup)
+    gk_us, _ = timed(lambda: fo.gemm_stage(gplan, A, Bt, out), args.steps, args.warmup)
+
+    # ---- e2e through the public API with host (pinned) buffers
+    A_pin, B_pin = A_h.pin_memory(), B_h.pin_memory()
+    out_pin = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        A.copy_(A_pin, non_blocking=True)
+        Bt.copy_(B_pin, non_blocking=True)
+        fo.run(ctx, plan, A, Bt, out)
+        out_pin.copy_(out, non_blocking=True)
+
+    e2e_us, _ = timed(e2e_step, max(3, args.steps // 2), 2)
+
+    flops = 2.0 * M * N * K
+    achieved = flops / (gk_us * 1e-6) / 1e12
+    peak = peaks["bf16_tflops"]
+    nvlink_gbs = 770.0
+    bus = 2.0 * (world - 1) / world * M * N * 2
+    layer_roof_us = max(flops / (peak * 1e12) * 1e6, bus / (nvlink_gbs * 1e9) * 1e6)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
+        traffic = tr.get(f"{M}x{N}x{K}/{BM}x{BN}/S{S}")
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            us, desc, cores = cpu_oracle_sample(wl, world, args.cpu_seconds)
+            cpu = {"value": round(us, 1), "unit": "us", "cores": cores, "kind": "oracle", "sample": desc}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "us", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "overlapped GEMM+AllReduce us per layer",
+            "value": round(ov_us, 2), "unit": "us", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ov_us / 1e3, 4), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) weights)",
+            "config": {**{k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective", "tile")},
+                       "workers": S, "comm_sms": comm_sms, "waves": T, "groups": list(groups),
+                       "ar_layout": "rowband" if plan.info["ar_layout"] == 1 else "slot",
+                       "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"tp{world}"},
+            "speedup_vs_sequential": round(seq_us / ov_us, 4), "sequential_us": round(seq_us, 2),
+            "tflops": round(world * flops / (ov_us * 1e-6) / 1e12, 1),
+            "layer_roofline_us": round(layer_roof_us, 2), "frac_of_layer_roofline": round(layer_roof_us / ov_us, 4),
+            "alg1_predicted_us": round(pred, 2), "spot_check": spot,
+            "roofline": {"bound": "tensor", "kernel": "fo_gemm_tcgen05_kernel<256>", "achieved": round(achieved, 1),
+                         "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed alone per step)",
+                         "kernel_us": round(gk_us, 2), "flops_per_launch": flops},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_us, 1), "unit": "us",
+                    "h2d_bytes_per_step": int((M * K + N * K) * 2), "d2h_bytes_per_step": int(M * N * 2)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,72 @@
+"""Summarise ncu artefacts into profiles/ (dev tool, runs on the CPU box).
+
+    python tools/ncu_summary.py rep  gpurun_out/x.ncu-rep  > profiles/rNN_x.txt
+    python tools/ncu_summary.py launches gpurun_out/launches.csv > profiles/rNN_launches.txt
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum",
+    "sm__cycles_elapsed.avg.per_second",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "launch__registers_per_thread",
+    "launch__grid_size",
+    "launch__block_size",
+    "launch__shared_mem_per_block_dynamic",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
+]
+
+
+def rep(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        print("no data")
+        return
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:
+        d = dict(zip(hdr, vals))
+        print(f"kernel: {d.get('Kernel Name', '?')[:120]}")
+        for k in KEYS:
+            for h, u, v in zip(hdr, units, vals):
+                if h == k or h.endswith("." + k) or h.endswith(k):
+                    print(f"  {k:75s} {v:>16s} {u}")
+                    break
+        print()
+
+
+def launches(path):
+    lines = open(path).read().splitlines()
+    start = [i for i, l in enumerate(lines) if l.startswith('"ID"')][0]
+    rows = list(csv.reader(lines[start:]))
+    idx = {h: i for i, h in enumerate(rows[0])}
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        if r[idx["Metric Name"]] != "gpu__time_duration.sum":
+            continue
+        v = float(r[idx["Metric Value"]].replace(",", ""))
+        u = r[idx["Metric Unit"]]
+        v = v * 1e3 if u == "us" else v * 1e6 if u == "ms" else v
+        k = r[idx["Kernel Name"]][:100]
+        agg[k][0] += 1
+        agg[k][1] += v
+    tot = sum(v for _, v in agg.values())
+    print(f"{'launches':>8} {'total_us':>10} {'avg_us':>9} {'share':>6}  kernel")
+    for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{n:8d} {v / 1e3:10.1f} {v / 1e3 / n:9.2f} {100 * v / tot:5.1f}%  {k}")
+
+
+if __name__ == "__main__":
+    {"rep": rep, "launches": launches}[sys.argv[1]](sys.argv[2])
