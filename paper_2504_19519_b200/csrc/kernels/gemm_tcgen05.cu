@@ -34,7 +34,7 @@
 namespace fo {
 namespace {
 
-constexpr int BM = 128;
+constexpr int BM = 128;                     // rows per CTA (a CTA pair covers 256)
 constexpr int BK = 64;                      // 64 bf16 = 128 B = one swizzle row
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int EPI_COLS = 64;                // columns staged per epilogue chunk
@@ -43,11 +43,17 @@ constexpr int EPI_WARP_BYTES = 32 * EPI_PITCH;
 constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
 constexpr int NUM_THREADS = 256;
 
-template <int BN>
+// CG = CTA group size: 1 -> tile 128 x BN on one SM; 2 -> tile 256 x BN on a
+// CTA pair (tcgen05 cta_group::2): each CTA stages its 128 rows of A and
+// BN/2 rows of B, the leader issues M=256 MMAs, each CTA's TMEM holds its
+// 128 accumulator rows.
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int B_ROWS = BN / CG;                 // B rows staged per CTA
+  static constexpr int B_STAGE_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128) ? 6 : 8;
+  static constexpr int BUDGET = 232448 - 1024 - EPI_BYTES - 256;
+  static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulator stages
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
@@ -95,6 +101,37 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// shared::cluster address of the same object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// 2-SM TMA: data lands in this CTA's smem, the transaction bytes are counted
+// on the leader CTA's mbarrier (cluster address).
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, int x, int y, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -111,22 +148,42 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 }
 
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N>>3, M>>4.
-template <int N>
+template <int M, int N>
 __device__ __forceinline__ constexpr uint32_t idesc_bf16() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+template <int CG>
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
 }
 
+// MMA completion -> mbarrier arrive; for a pair, multicast to the barrier at
+// the same offset in both CTAs.
+template <int CG>
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+  }
 }
 
 #define FO_R8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
@@ -157,35 +214,39 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Destination of row `a` (0..BM-1) of the tile at position `pos` = (ti, tj).
-__device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, int ti, int tj, int a, int BN) {
+// Destination of row `a` (0..TM-1) of the TM x BN tile at position `pos` = (ti, tj).
+template <int TM, int BN>
+__device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, int ti, int tj, int a) {
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.dst);
   switch (p.mode) {
     case EPI_ROWMAJOR:
-      return base + ((int64_t)ti * BM + a) * p.ldc + (int64_t)tj * BN;
+      return base + ((int64_t)ti * TM + a) * p.ldc + (int64_t)tj * BN;
     case EPI_SLOT:  // slot pos, row-major
-      return base + ((int64_t)pos * BM + a) * BN;
+      return base + ((int64_t)pos * TM + a) * BN;
     case EPI_RS: {  // subtile k = a / h goes to chunk k of the group
       const int g = p.group_of_pos[pos];
       const int ps = p.gpos[g], G = p.gpos[g + 1] - ps;
       const int k = a / p.h, a2 = a - k * p.h;
-      return base + ((int64_t)ps * BM + (int64_t)k * G * p.h + (int64_t)(pos - ps) * p.h + a2) * BN;
+      return base + ((int64_t)ps * TM + (int64_t)k * G * p.h + (int64_t)(pos - ps) * p.h + a2) * BN;
     }
     default:  // EPI_A2A: row -> slot in its destination pool
-      return base + (int64_t)p.row_slot[(int64_t)pos * BM + a] * BN;
+      return base + (int64_t)p.row_slot[(int64_t)pos * TM + a] * BN;
   }
 }
 
-template <int BN>
+// One persistent worker = one CTA (CG=1) or one CTA pair (CG=2).  Worker w of
+// S = gridDim.x/CG runs positions w, w+S, ... (wave floor(p/S)).
+template <int BN, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     fo_gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const GemmArgs p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   constexpr int ST = C::STAGES;
+  constexpr int TM = BM * CG;  // tile rows
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                   // ST x 16 KB
-  uint8_t* sB = smem + ST * A_STAGE_BYTES;              // ST x BN*128 B
+  uint8_t* sB = smem + ST * A_STAGE_BYTES;              // ST x (BN/CG)*128 B
   uint8_t* sEpi = smem + ST * C::STAGE_BYTES;           // 4 warps x 32 rows x pitch
   uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + EPI_BYTES);
   uint64_t* empty = full + ST;
@@ -195,6 +256,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = (CG == 1) ? 0u : cluster_rank();
+  const bool leader = (crank == 0);
+  const int worker = blockIdx.x / CG;
+  const int nworkers = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -207,35 +272,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[s], 4 * CG);  // one arrive per epilogue warp of each CTA of the group
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"((uint32_t)C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int KB = (int)(p.K / BK);
 
   if (warp == 0) {
-    // ======================= TMA producer
+    // ======================= TMA producer (every CTA loads its own A rows and B rows)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int pos = blockIdx.x; pos < p.tiles; pos += gridDim.x) {
+      for (int pos = worker; pos < p.tiles; pos += nworkers) {
         const int t = p.order[pos];
         const int ti = t / p.Nt, tj = t - ti * p.Nt;
+        const int arow = ti * TM + (int)crank * BM;
+        const int brow = tj * BN + (int)crank * C::B_ROWS;
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, ti * BM, &full[stage]);
-          tma_load_2d(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, tj * BN, &full[stage]);
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, arow, &full[stage]);
+            tma_load_2d(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, brow, &full[stage]);
+          } else {
+            // both CTAs' bytes are counted on the leader's full barrier
+            if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
+            const uint32_t bar = mapa_shared(&full[stage], 0);
+            tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, arow, bar);
+            tma_load_2d_2sm(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, brow, bar);
+          }
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
@@ -244,14 +326,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer (one thread)
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16<BN>();
+    // ======================= MMA issuer (one thread of the leader CTA)
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_bf16<TM, BN>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int pos = blockIdx.x; pos < p.tiles; pos += gridDim.x) {
+      for (int pos = worker; pos < p.tiles; pos += nworkers) {
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -263,15 +345,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 bytes along K inside the 128-byte swizzle row = +2 in the >>4 address field
-            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16<CG>(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
+          umma_commit<CG>(&empty[stage]);  // frees the smem stage (in both CTAs) when these MMAs retire
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        umma_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue(s)
         if (++acc == 2) {
           acc = 0;
           aphase ^= 1;
@@ -279,12 +361,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ======================= epilogue: reorder-store + signal
+    // ======================= epilogue: reorder-store + signal (this CTA's 128 rows)
     const int q = warp - 4;  // TMEM lane quarter: warp (4+q) may access lanes 32q..32q+31
     uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
+    const uint32_t tempty_leader0 = (CG == 1) ? 0u : mapa_shared(&tempty[0], 0);
     int acc = 0;
     uint32_t aphase = 0;
-    for (int pos = blockIdx.x; pos < p.tiles; pos += gridDim.x) {
+    for (int pos = worker; pos < p.tiles; pos += nworkers) {
       const int t = p.order[pos];
       const int ti = t / p.Nt, tj = t - ti * p.Nt;
       mbar_wait(&tfull[acc], aphase);
@@ -300,7 +383,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // accumulator fully read: hand the TMEM stage back to the MMA warp
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+            else mbar_arrive_cluster(tempty_leader0 + 8u * acc);
+          }
         }
         // stage row `lane` (this thread's TMEM lane) as bf16
         uint4* srow = reinterpret_cast<uint4*>(stg + lane * EPI_PITCH);
@@ -320,16 +406,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int r = it * 4 + (lane >> 3);
           const int ch = lane & 7;
           const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + ch * 16);
-          __nv_bfloat16* d = row_dst(p, pos, ti, tj, q * 32 + r, BN) + c * EPI_COLS + ch * 8;
+          __nv_bfloat16* d = row_dst<TM, BN>(p, pos, ti, tj, (int)crank * BM + q * 32 + r) + c * EPI_COLS + ch * 8;
           *reinterpret_cast<uint4*>(d) = w;
         }
         __syncwarp();
       }
-      // all 128 epilogue threads finished this tile's stores -> one release add
+      // all 128 epilogue threads of this CTA finished their stores -> one
+      // release add (a pair signals twice per tile: counters count half tiles)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (q == 0 && lane == 0) {
         if (p.counters) red_release_add(&p.counters[p.group_of_pos[pos]], 1u);
-        if (p.tile_ts) p.tile_ts[pos] = globaltimer();
+        if (p.tile_ts && leader) p.tile_ts[pos] = globaltimer();
       }
       if (++acc == 2) {
         acc = 0;
@@ -338,12 +425,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)C::TMEM_COLS)
-                 : "memory");
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -377,20 +469,33 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
-cudaError_t launch_bn(const GemmArgs& a, cudaStream_t stream) {
-  using C = Cfg<BN>;
+template <int BN, int CG>
+cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
+  using C = Cfg<BN, CG>;
   static bool attr_set = false;
+  auto kern = fo_gemm_tcgen05_kernel<BN, CG>;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fo_gemm_tcgen05_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   CUtensorMap mA, mB;
-  if (!make_map(&mA, a.A, a.M, a.K, BM) || !make_map(&mB, a.Bt, a.N, a.K, BN)) return cudaErrorInvalidValue;
-  fo_gemm_tcgen05_kernel<BN><<<a.workers, NUM_THREADS, C::SMEM_BYTES, stream>>>(mA, mB, a);
+  if (!make_map(&mA, a.A, a.M, a.K, BM) || !make_map(&mB, a.Bt, a.N, a.K, C::B_ROWS)) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.workers * CG);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mB, a);
   count_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -401,16 +506,25 @@ std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
-bool gemm_shape_supported(int bm, int bn) { return bm == BM && (bn == 64 || bn == 128 || bn == 256); }
+bool gemm_shape_supported(int bm, int bn) {
+  return (bm == 128 || bm == 256) && (bn == 64 || bn == 128 || bn == 256);
+}
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
-  if (a.BM != BM) return cudaErrorInvalidValue;
-  switch (a.BN) {
-    case 64: return launch_bn<64>(a, stream);
-    case 128: return launch_bn<128>(a, stream);
-    case 256: return launch_bn<256>(a, stream);
-    default: return cudaErrorInvalidValue;
+  if (a.BM == 128) {
+    switch (a.BN) {
+      case 64: return launch_cfg<64, 1>(a, stream);
+      case 128: return launch_cfg<128, 1>(a, stream);
+      case 256: return launch_cfg<256, 1>(a, stream);
+    }
+  } else if (a.BM == 256) {
+    switch (a.BN) {
+      case 64: return launch_cfg<64, 2>(a, stream);
+      case 128: return launch_cfg<128, 2>(a, stream);
+      case 256: return launch_cfg<256, 2>(a, stream);
+    }
   }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace fo

@@ -88,6 +88,11 @@ static void ensure_device(fo_plan_s* p) {
   const PlanHost& h = p->host;
   if (!gemm_shape_supported(h.BM, h.BN))
     fail(FO_ERR_UNSUPPORTED, "tile %dx%d not compiled into this build", h.BM, h.BN);
+  int sms = 0;
+  FO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (h.S * (h.BM / 128) > sms)
+    fail(FO_ERR_INVALID_ARG, "workers=%d x %d CTAs exceeds the %d SMs (waves would not be resident)", h.S,
+         h.BM / 128, sms);
   int major = 0, minor = 0;
   FO_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
   FO_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
@@ -184,6 +189,10 @@ static int post_map(const PlanHost& h) {
     default: return POSTMAP_IDENTITY;
   }
 }
+
+// Each CTA signals once per tile it finishes; a 256-row tile is finished by a
+// CTA pair, so group j completes at |G_j| * tile_m/128 signals.
+static cuuint32_t signal_target(const PlanHost& h, int j) { return (cuuint32_t)(h.group_tiles(j) * (h.BM / 128)); }
 
 static ncclDataType_t bf16() { return ncclBfloat16; }
 
@@ -334,7 +343,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     if (h.coll != FO_NOCOMM) {
       for (int j = 0; j < h.P; ++j) {
         CUresult r = wait(reinterpret_cast<CUstream>(c->comm_stream),
-                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), (cuuint32_t)h.group_tiles(j),
+                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), signal_target(h, j),
                           CU_STREAM_WAIT_VALUE_GEQ);
         if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
         group_collective(c, p, j, gemm_dst);
@@ -343,7 +352,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
       // no communication: the comm stream only has to see the GEMM finish
       for (int j = 0; j < h.P; ++j) {
         CUresult r = wait(reinterpret_cast<CUstream>(c->comm_stream),
-                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), (cuuint32_t)h.group_tiles(j),
+                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), signal_target(h, j),
                           CU_STREAM_WAIT_VALUE_GEQ);
         if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
       }

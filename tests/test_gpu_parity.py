@@ -60,32 +60,37 @@ def _rel_err(g, o):
 
 
 def _counters_ok(plan, oplan):
-    assert plan.read_counters().tolist() == op.group_thresholds(oplan.partition, oplan.S, oplan.ntiles)
+    # each CTA signals once per tile it finishes; a 256-row tile is finished by a CTA pair
+    mult = oplan.BM // 128
+    want = [mult * t for t in op.group_thresholds(oplan.partition, oplan.S, oplan.ntiles)]
+    assert plan.read_counters().tolist() == want
 
 
 # ------------------------------------------------------------------ plain GEMM
+@pytest.mark.parametrize("BM", [128, 256])
 @pytest.mark.parametrize("BN", [64, 128, 256])
-@pytest.mark.parametrize("shape", [(128, 256, 64), (384, 512, 320), (256, 768, 1024)])
-def test_gemm_rowmajor_exact(BN, shape):
+@pytest.mark.parametrize("shape", [(256, 256, 64), (768, 512, 320), (512, 768, 1024)])
+def test_gemm_rowmajor_exact(BM, BN, shape):
     M, N, K = shape
-    if N % BN:
-        pytest.skip("N % BN")
+    if N % BN or M % BM:
+        pytest.skip("shape not divisible")
     A, Bt = synthetic.exact_inputs(M, N, K, seed=M + N + K, nnz_per_row=256)
-    tiles = (M // 128) * (N // BN)
+    tiles = (M // BM) * (N // BN)
     S = max(1, min(tiles, 7))
-    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=2)
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2)
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     fo.gemm_stage(plan, _dev_bf16(A), _dev_bf16(Bt), out)
     torch.cuda.synchronize()
     assert np.array_equal(_host(out), onum.gemm(A, Bt))
-    _counters_ok(plan, op.make_plan(M, N, 128, BN, S, None, swizzle=2))
+    _counters_ok(plan, op.make_plan(M, N, BM, BN, S, None, swizzle=2))
 
 
+@pytest.mark.parametrize("BM", [128, 256])
 @pytest.mark.parametrize("BN", [128, 256])
-def test_gemm_float_regime(BN):
+def test_gemm_float_regime(BM, BN):
     M, N, K = 512, 512, 2048
     A, Bt = synthetic.float_inputs(M, N, K, seed=11)
-    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_n=BN, workers=5)
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=3)
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     fo.gemm_stage(plan, _dev_bf16(A), _dev_bf16(Bt), out)
     torch.cuda.synchronize()
@@ -106,10 +111,12 @@ def _rank_inputs(n, M, N, K, seed, exact=True):
 
 
 CASES = [
-    # M, N, K, BN, S, groups, swizzle
-    (512, 512, 128, 128, 3, None, 2),
-    (384, 768, 192, 256, 2, None, 1),
-    (640, 256, 64, 64, 4, None, 3),
+    # M, N, K, BN, S, BM, swizzle
+    (512, 512, 128, 128, 3, 128, 2),
+    (384, 768, 192, 256, 2, 128, 1),
+    (640, 256, 64, 64, 4, 128, 3),
+    (768, 512, 128, 256, 2, 256, 2),
+    (512, 768, 192, 128, 3, 256, 1),
 ]
 
 
@@ -121,13 +128,13 @@ def _groups(tiles, S, seed):
 @pytest.mark.parametrize("case", range(len(CASES)))
 @pytest.mark.parametrize("layout", ["slot", "auto"])
 def test_allreduce_stages_exact(n, case, layout):
-    M, N, K, BN, S, _, swz = CASES[case]
-    tiles = (M // 128) * (N // BN)
+    M, N, K, BN, S, BM, swz = CASES[case]
+    tiles = (M // BM) * (N // BN)
     groups = _groups(tiles, S, case + 10 * n)
-    order = synthetic.random_order(tiles, case) if (case == 1 and layout == "slot") else None
+    order = synthetic.random_order(tiles, case) if (case in (1, 4) and layout == "slot") else None
     As, Bts = _rank_inputs(n, M, N, K, 100 + case)
-    oplan = op.make_plan(M, N, 128, BN, S, groups, order=order, swizzle=swz)
-    plans = [fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_n=BN, workers=S, tile_order=order, swizzle=swz,
+    oplan = op.make_plan(M, N, BM, BN, S, groups, order=order, swizzle=swz)
+    plans = [fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=order, swizzle=swz,
                      group_waves=groups, ar_layout=layout, rank=r, world=n) for r in range(n)]
     lay = "rowband" if plans[0].info["ar_layout"] == 1 else "slot"
     ores = opl.run_allreduce(As, Bts, oplan, layout=lay)
@@ -146,15 +153,15 @@ def test_allreduce_stages_exact(n, case, layout):
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
 @pytest.mark.parametrize("case", range(len(CASES)))
 def test_reducescatter_stages_exact(n, case):
-    M, N, K, BN, S, _, swz = CASES[case]
-    tiles = (M // 128) * (N // BN)
+    M, N, K, BN, S, BM, swz = CASES[case]
+    tiles = (M // BM) * (N // BN)
     groups = _groups(tiles, S, case + 20 * n)
     As, Bts = _rank_inputs(n, M, N, K, 200 + case)
-    oplan = op.make_plan(M, N, 128, BN, S, groups, swizzle=swz)
+    oplan = op.make_plan(M, N, BM, BN, S, groups, swizzle=swz)
     ores = opl.run_reducescatter(As, Bts, oplan)
-    plain = opl.plain_reducescatter(As, Bts, 128)
+    plain = opl.plain_reducescatter(As, Bts, BM)
     for r in range(n):
-        plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=swz, group_waves=groups,
+        plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=swz, group_waves=groups,
                        rank=r, world=n)
         send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
         fo.gemm_stage(plan, _dev_bf16(As[r]), _dev_bf16(Bts[r]), send)
@@ -167,23 +174,24 @@ def test_reducescatter_stages_exact(n, case):
         assert np.array_equal(_host(out), plain[r])
 
 
+@pytest.mark.parametrize("BM", [128, 256])
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
-def test_alltoall_stages_exact(n):
+def test_alltoall_stages_exact(n, BM):
     rng = np.random.default_rng(n)
     N, K, BN, P = 512, 128, 128, 2
     specs, oplans, As, Bts, rds = [], [], [], [], []
     for s in range(n):
         Mt = int(rng.integers(2, 5))
-        M = Mt * 128
+        M = Mt * BM
         tiles = Mt * (N // BN)
         S = int(rng.integers(1, tiles // P + 1))
         T = op.num_waves(tiles, S)
         part = [1] * (P - 1) + [T - (P - 1)]
         rd = synthetic.random_row_dst(M, n, 1000 + s)
         A, Bt = synthetic.exact_inputs(M, N, K, seed=300 + s, nnz_per_row=64)
-        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=2, group_waves=part,
-                          row_dst=rd))
-        oplans.append(op.make_plan(M, N, 128, BN, S, part, swizzle=2))
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2,
+                          group_waves=part, row_dst=rd))
+        oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=2))
         As.append(A), Bts.append(Bt), rds.append(rd)
     ores = opl.run_alltoall(As, Bts, oplans, rds)
     plain = opl.plain_alltoall(As, Bts, rds)
@@ -224,14 +232,15 @@ def test_post_fused_ops(post):
 
 
 # ------------------------------------------------------------------ full path with NCCL (world = 1)
+@pytest.mark.parametrize("BM", [128, 256])
 @pytest.mark.parametrize("coll", ["allreduce", "reducescatter", "alltoall", "nocomm"])
 @pytest.mark.parametrize("post", ["none", "add_rmsnorm"])
-def test_fo_run_world1(ctx1, coll, post):
-    M, N, K, BN, S = 512, 512, 256, 128, 5
-    tiles = (M // 128) * (N // BN)
+def test_fo_run_world1(ctx1, coll, post, BM):
+    M, N, K, BN, S = 1024, 512, 256, 128, 5
+    tiles = (M // BM) * (N // BN)
     groups = _groups(tiles, S, 3)
     A, Bt = synthetic.exact_inputs(M, N, K, seed=5, nnz_per_row=200)
-    kw = dict(coll=coll, m=M, n=N, k=K, tile_n=BN, workers=S, swizzle=2, group_waves=groups, post=post)
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2, group_waves=groups, post=post)
     if coll == "alltoall":
         kw["row_dst"] = np.zeros(M, np.int32)
         plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
@@ -259,13 +268,14 @@ def test_fo_run_world1(ctx1, coll, post):
             assert np.array_equal(_host(out2), C)
 
 
-def test_tile_timestamps_follow_waves():
+@pytest.mark.parametrize("BM", [128, 256])
+def test_tile_timestamps_follow_waves(BM):
     """Per-tile %globaltimer: every tile of wave w+1 signals after the first
     tile of wave w (wave pattern; X1 analogue)."""
     M, N, K, BN = 2048, 2048, 4096, 256
     S = 16
     A, Bt = synthetic.float_inputs(M, N, K, seed=1)
-    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_n=BN, workers=S)
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S)
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     ts = torch.zeros(plan.info["tiles"], dtype=torch.int64, device="cuda")
     fo.gemm_stage_timed(plan, _dev_bf16(A), _dev_bf16(Bt), out, ts)

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--shapes", default="4096x4096x14336,4096x4096x7168,4096x4096x3584,4096x4096x1792,8192x8192x1024")
     ap.add_argument("--bn", default="128,256")
     ap.add_argument("--s", default="148,144,132")
+    ap.add_argument("--bm", default="128,256")
     args = ap.parse_args()
     sms = fo.device_sm_count(0)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -45,13 +46,15 @@ def main():
         t = timeit(lambda: torch.matmul(A, B.t(), out=C), flush=flush)
         print(f"{sh} cublas {t:8.1f} us {fl / t / 1e6:7.1f} TF", flush=True)
         ref = C.float().clone()
-        for bn in map(int, args.bn.split(",")):
-            for S in map(int, args.s.split(",")):
-                S = min(S, sms)
-                plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_n=bn, workers=S)
-                t = timeit(lambda: fo.gemm_stage(plan, A, B, C), flush=flush)
-                err = (C.float() - ref).abs().max().item()
-                print(f"{sh} fo BN={bn} S={S} {t:8.1f} us {fl / t / 1e6:7.1f} TF  maxdiff {err:.3g}", flush=True)
+        for bm in map(int, args.bm.split(",")):
+            for bn in map(int, args.bn.split(",")):
+                for S in map(int, args.s.split(",")):
+                    S = min(S, sms) // (bm // 128)
+                    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=bm, tile_n=bn, workers=S)
+                    t = timeit(lambda: fo.gemm_stage(plan, A, B, C), flush=flush)
+                    err = (C.float() - ref).abs().max().item()
+                    print(f"{sh} fo BM={bm} BN={bn} S={S} {t:8.1f} us {fl / t / 1e6:7.1f} TF  maxdiff {err:.3g}",
+                          flush=True)
 
 
 if __name__ == "__main__":
