@@ -30,16 +30,17 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 M_TOK, N_HID, K_FFN = 4096, 4096, 14336
-BM, BN = 128, 256
+BM, BN = 256, 256   # tcgen05 cta_group::2 tile (CTA pair)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fo", choices=["fo", "reference"])
-    ap.add_argument("--comm-sms", type=int, default=None, help="SMs left free for NCCL (default 0 at N=1, 20 else)")
+    ap.add_argument("--workers", type=int, default=None,
+                    help="S = concurrent tile workers (CTA pairs); default: fewest workers with the same wave count as all SMs")
     ap.add_argument("--groups", default=None, help="explicit wave-group partition, e.g. 1,1,2 (default: Alg. 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle sample")
@@ -61,34 +62,31 @@ def workload(n):
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    """nvidia-smi sampling (to a file, 50 ms period) of SM clocks and throttle
+    reasons while the timed region runs."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device, self.rows, self.proc = device, [], None
+        import tempfile
+        self.device, self.proc = device, None
+        self.path = tempfile.mktemp(prefix="fo_clocks_", suffix=".csv")
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -96,20 +94,31 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+
         def num(x):
             try:
                 return float(x)
             except ValueError:
                 return None
-        sm = [num(r[0]) for r in self.rows if num(r[0])]
-        mx = [num(r[1]) for r in self.rows if num(r[1])]
+        sm = [num(r[0]) for r in rows if num(r[0])]
+        mx = [num(r[1]) for r in rows if num(r[1])]
+        pw = [num(r[2]) for r in rows if num(r[2])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
         load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
 
 
 # --------------------------------------------------------------------------- CPU oracle baseline
@@ -197,10 +206,17 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peak_src = load_peaks()
     sms = fo.device_sm_count(local)
-    comm_sms = args.comm_sms if args.comm_sms is not None else (0 if world == 1 else 20)
-    S = sms - comm_sms
     M, N, K = wl["M"], wl["N"], wl["K_loc"]
     tiles = (M // BM) * (N // BN)
+    cg = BM // 128
+    if args.workers:
+        S = args.workers
+    else:
+        # waves are quantised: keep T of the full-GPU grid, use the fewest workers
+        # achieving it; the SMs this frees are left to NCCL (R18)
+        T_full = -(-tiles // (sms // cg))
+        S = -(-tiles // T_full)
+    comm_sms = sms - cg * S
     T = (tiles + S - 1) // S
 
     # ---- inputs (synthetic, seeded; SURVEY §8(d) recipe), resident in HBM
@@ -218,7 +234,7 @@ def main():
         uid = obj[0]
     else:
         uid = fo.unique_id()
-    ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=comm_sms if world > 1 else 0)
+    ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
 
     def barrier():
         if world > 1:
@@ -278,12 +294,12 @@ def main():
         spot = {"rows": 8, "max_rel_err": float(((got - ref).abs() / torch.maximum(ref.abs(), rms)).max())}
 
     # ---- timed: overlapped, sequential, GEMM kernel alone
-    launches0 = fo.kernel_launch_count()
     with ClockSampler(local) as clk:
+        launches0 = fo.kernel_launch_count()
         ov_us, ov_all = timed(lambda: fo.run(ctx, plan, A, Bt, out), args.steps, args.warmup)
-    launches = (fo.kernel_launch_count() - launches0) * args.steps // (args.steps + args.warmup)
-    seq_us, _ = timed(lambda: fo.run_sequential(ctx, plan, A, Bt, out), args.steps, args.warmup)
-    gk_us, _ = timed(lambda: fo.gemm_stage(gplan, A, Bt, out), args.steps, args.warmup)
+        launches = (fo.kernel_launch_count() - launches0) * args.steps // (args.steps + args.warmup)
+        seq_us, _ = timed(lambda: fo.run_sequential(ctx, plan, A, Bt, out), args.steps, args.warmup)
+        gk_us, _ = timed(lambda: fo.gemm_stage(gplan, A, Bt, out), args.steps, args.warmup)
 
     # ---- e2e through the public API with host (pinned) buffers
     A_pin, B_pin = A_h.pin_memory(), B_h.pin_memory()
@@ -332,7 +348,7 @@ def main():
             "tflops": round(world * flops / (ov_us * 1e-6) / 1e12, 1),
             "layer_roofline_us": round(layer_roof_us, 2), "frac_of_layer_roofline": round(layer_roof_us / ov_us, 4),
             "alg1_predicted_us": round(pred, 2), "spot_check": spot,
-            "roofline": {"bound": "tensor", "kernel": "fo_gemm_tcgen05_kernel<256>", "achieved": round(achieved, 1),
+            "roofline": {"bound": "tensor", "kernel": f"fo_gemm_tcgen05_kernel<{BN},{cg}>", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed alone per step)",
                          "kernel_us": round(gk_us, 2), "flops_per_launch": flops},
