@@ -21,21 +21,44 @@
 namespace fo {
 namespace {
 
-__device__ __forceinline__ int64_t src_offset(const PostArgs& p, int64_t r, int64_t col) {
-  const int jc = (int)(col / p.BN), b = (int)(col - (int64_t)jc * p.BN);
-  switch (p.map) {
-    case POSTMAP_IDENTITY:
-      return r * p.N + col;
-    case POSTMAP_SLOT:
-      return ((int64_t)p.pos_of_tile[(r / p.BM) * p.Nt + jc] * p.BM + r % p.BM) * p.BN + b;
-    case POSTMAP_RS:
-      return ((int64_t)p.pos_of_tile[(r / p.h) * p.Nt + jc] * p.h + r % p.h) * p.BN + b;
-    default:
-      return (int64_t)p.src_row[r * p.Nt + jc] * p.BN + b;
+// Per-row source description: chunk c of row r (columns 8c..8c+7, tile-column
+// jc = 8c >> log2(BN)) starts at element  tbl[jc] * tscale + roff + (8c & (BN-1)).
+struct RowSrc {
+  const int32_t* tbl;  // per tile-column table row (pos_of_tile / src_row), or null for identity
+  int64_t tscale;      // elements per table unit
+  int64_t roff;        // element offset of this row inside the unit
+};
+
+template <int MAP>
+__device__ __forceinline__ RowSrc row_src(const PostArgs& p, int64_t r) {
+  RowSrc s;
+  if (MAP == POSTMAP_IDENTITY) {
+    s.tbl = nullptr;
+    s.tscale = 0;
+    s.roff = r * p.N;
+  } else if (MAP == POSTMAP_SLOT) {  // slot of tile (r/BM, jc), row r%BM
+    s.tbl = p.pos_of_tile + (r / p.BM) * p.Nt;
+    s.tscale = (int64_t)p.BM * p.BN;
+    s.roff = (r % p.BM) * p.BN;
+  } else if (MAP == POSTMAP_RS) {    // receive row q*h + r%h
+    s.tbl = p.pos_of_tile + (r / p.h) * p.Nt;
+    s.tscale = (int64_t)p.h * p.BN;
+    s.roff = (r % p.h) * p.BN;
+  } else {                           // A2A subtoken
+    s.tbl = p.src_row + r * p.Nt;
+    s.tscale = p.BN;
+    s.roff = 0;
   }
+  return s;
 }
 
-__device__ __forceinline__ uint4 ldg16(const void* ptr) {
+template <int MAP>
+__device__ __forceinline__ int64_t chunk_src(const RowSrc& s, int64_t col, int lbn, int bn_mask) {
+  if (MAP == POSTMAP_IDENTITY) return s.roff + col;
+  return (int64_t)__ldg(s.tbl + (col >> lbn)) * s.tscale + s.roff + (col & bn_mask);
+}
+
+__device__ __forceinline__ uint4 ld_stream(const void* ptr) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -43,8 +66,12 @@ __device__ __forceinline__ uint4 ldg16(const void* ptr) {
   return v;
 }
 
-__device__ __forceinline__ uint4 ldg16_coherent(const void* ptr) {
-  return *reinterpret_cast<const uint4*>(ptr);
+__device__ __forceinline__ uint4 ld_coherent(const void* ptr) { return *reinterpret_cast<const uint4*>(ptr); }
+
+__device__ __forceinline__ void st_stream(void* ptr, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
 __device__ __forceinline__ void unpack8(const uint4& v, float* f) {
@@ -68,22 +95,30 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
   return v;
 }
 
-template <int OP>
-__global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p) {
+constexpr int UNROLL = 4;
+
+// One warp per output row; lane l handles chunks l, l+32, ... (16 B each).
+template <int MAP, int OP>
+__global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p, int lbn) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t chunks = p.N / 8;
-  const char* src = reinterpret_cast<const char*>(p.src);
-  char* out = reinterpret_cast<char*>(p.out);
-  const char* res = reinterpret_cast<const char*>(p.residual);
+  const int64_t chunks = p.N >> 3;
+  const int bn_mask = p.BN - 1;
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(p.residual);
+  const bool inplace = (p.src == p.out);
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.rows; r += warps) {
+    const RowSrc rs = row_src<MAP>(p, r);
+    __nv_bfloat16* orow = out + r * p.N;
+    const __nv_bfloat16* rrow = res ? res + r * p.N : nullptr;
     if (OP == FO_POST_ADD_RMSNORM) {
       // pass 1: sum of squares of y = x + residual (fp32)
       float ss = 0.f;
       for (int64_t c = lane; c < chunks; c += 32) {
         float x[8], y[8];
-        unpack8(ldg16_coherent(src + 2 * src_offset(p, r, 8 * c)), x);
-        unpack8(ldg16(res + 2 * (r * p.N + 8 * c)), y);
+        unpack8(ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask)), x);
+        unpack8(ld_stream(rrow + 8 * c), y);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float t = x[i] + y[i];
@@ -93,31 +128,53 @@ __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p) 
 #pragma unroll
       for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       const float rstd = rsqrtf(ss / (float)p.N + p.eps);
-      const char* gam = reinterpret_cast<const char*>(p.gamma);
-      // pass 2 (re-read hits L2): out = y * rstd * gamma
+      const __nv_bfloat16* gam = reinterpret_cast<const __nv_bfloat16*>(p.gamma);
+      // pass 2 (the re-read hits L2): out = y * rstd * gamma
       for (int64_t c = lane; c < chunks; c += 32) {
         float x[8], y[8], g[8];
-        unpack8(ldg16_coherent(src + 2 * src_offset(p, r, 8 * c)), x);
-        unpack8(ldg16(res + 2 * (r * p.N + 8 * c)), y);
-        unpack8(ldg16(gam + 2 * (8 * c)), g);
+        unpack8(ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask)), x);
+        unpack8(ld_coherent(rrow + 8 * c), y);
+        unpack8(ld_coherent(gam + 8 * c), g);
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = (x[i] + y[i]) * rstd * g[i];
-        *reinterpret_cast<uint4*>(out + 2 * (r * p.N + 8 * c)) = pack8(x);
+        st_stream(orow + 8 * c, pack8(x));
       }
     } else {
-#pragma unroll 4
-      for (int64_t c = lane; c < chunks; c += 32) {
-        const char* sp = src + 2 * src_offset(p, r, 8 * c);
-        uint4 v = (p.src == p.out) ? ldg16_coherent(sp) : ldg16(sp);
+      int64_t c = lane;
+      // batches of UNROLL independent 16-byte loads in flight per lane
+      for (; c + 32 * (UNROLL - 1) < chunks; c += 32 * UNROLL) {
+        uint4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const __nv_bfloat16* sp = src + chunk_src<MAP>(rs, 8 * (c + 32 * u), lbn, bn_mask);
+          v[u] = inplace ? ld_coherent(sp) : ld_stream(sp);
+        }
+        if (OP == FO_POST_ADD) {
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            float x[8], y[8];
+            unpack8(v[u], x);
+            unpack8(ld_stream(rrow + 8 * (c + 32 * u)), y);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] += y[i];
+            v[u] = pack8(x);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) st_stream(orow + 8 * (c + 32 * u), v[u]);
+      }
+      for (; c < chunks; c += 32) {
+        const __nv_bfloat16* sp = src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask);
+        uint4 v = inplace ? ld_coherent(sp) : ld_stream(sp);
         if (OP == FO_POST_ADD) {
           float x[8], y[8];
           unpack8(v, x);
-          unpack8(ldg16(res + 2 * (r * p.N + 8 * c)), y);
+          unpack8(ld_stream(rrow + 8 * c), y);
 #pragma unroll
           for (int i = 0; i < 8; ++i) x[i] += y[i];
           v = pack8(x);
         }
-        *reinterpret_cast<uint4*>(out + 2 * (r * p.N + 8 * c)) = v;
+        st_stream(orow + 8 * c, v);
       }
     }
   }
@@ -125,26 +182,40 @@ __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p) 
 
 int g_num_sms = 0;
 
+template <int MAP>
+cudaError_t launch_map(const PostArgs& a, int grid, int lbn, cudaStream_t stream) {
+  switch (a.op) {
+    case FO_POST_ADD: fo_post_reorder_kernel<MAP, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
+    case FO_POST_ADD_RMSNORM: fo_post_reorder_kernel<MAP, FO_POST_ADD_RMSNORM><<<grid, 256, 0, stream>>>(a, lbn); break;
+    default: fo_post_reorder_kernel<MAP, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_post(const PostArgs& a, cudaStream_t stream) {
   if (a.rows <= 0) return cudaSuccess;
-  if (a.N % 8) return cudaErrorInvalidValue;
+  if (a.N % 8 || (a.BN & (a.BN - 1))) return cudaErrorInvalidValue;
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (!g_num_sms) g_num_sms = 148;
   }
+  int lbn = 0;
+  while ((1 << lbn) < a.BN) ++lbn;
   const int64_t blocks_needed = (a.rows + 7) / 8;  // 8 warps (rows) per block
   const int grid = (int)std::min<int64_t>(blocks_needed, (int64_t)g_num_sms * 8);
-  switch (a.op) {
-    case FO_POST_ADD: fo_post_reorder_kernel<FO_POST_ADD><<<grid, 256, 0, stream>>>(a); break;
-    case FO_POST_ADD_RMSNORM: fo_post_reorder_kernel<FO_POST_ADD_RMSNORM><<<grid, 256, 0, stream>>>(a); break;
-    default: fo_post_reorder_kernel<FO_POST_NONE><<<grid, 256, 0, stream>>>(a); break;
+  cudaError_t e;
+  switch (a.map) {
+    case POSTMAP_SLOT: e = launch_map<POSTMAP_SLOT>(a, grid, lbn, stream); break;
+    case POSTMAP_RS: e = launch_map<POSTMAP_RS>(a, grid, lbn, stream); break;
+    case POSTMAP_A2A: e = launch_map<POSTMAP_A2A>(a, grid, lbn, stream); break;
+    default: e = launch_map<POSTMAP_IDENTITY>(a, grid, lbn, stream); break;
   }
   count_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace fo

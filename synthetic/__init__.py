@@ -28,6 +28,7 @@ __all__ = [
     "random_order",
     "random_partition",
     "moe_routing",
+    "balanced_moe_row_dst",
     "random_row_dst",
 ]
 
@@ -43,15 +44,17 @@ def cell_seed(*parts) -> int:
     return int.from_bytes(h[:4], "little")
 
 
-def _gen(seed: int) -> torch.Generator:
-    g = torch.Generator()
+def _gen(seed: int, device="cpu") -> torch.Generator:
+    g = torch.Generator(device=device)
     g.manual_seed(int(seed) & 0x7FFFFFFFFFFFFFFF)
     return g
 
 
-def normal_bf16(shape, std: float, seed: int) -> torch.Tensor:
-    """N(0, std^2) draws rounded to bf16 (torch's own fp32->bf16 conversion)."""
-    x = torch.randn(*shape, generator=_gen(seed), dtype=torch.float32)
+def normal_bf16(shape, std: float, seed: int, device="cpu") -> torch.Tensor:
+    """N(0, std^2) draws rounded to bf16 (torch's own fp32->bf16 conversion).
+    device="cuda" draws with the CUDA generator (a different, equally seeded
+    stream) for full-size inputs; callers copy what the oracle needs to CPU."""
+    x = torch.randn(*shape, generator=_gen(seed, device), dtype=torch.float32, device=device)
     if std != 1.0:
         x = x * std
     return x.to(torch.bfloat16).contiguous()
@@ -83,12 +86,18 @@ def exact_int_B(N: int, K: int, seed: int) -> torch.Tensor:
     return B.to(torch.bfloat16).contiguous()
 
 
-def float_inputs(M: int, N: int, K: int, seed: int):
+def float_inputs(M: int, N: int, K: int, seed: int, device="cpu"):
     """Float regime of SURVEY.md §8(d): A ~ N(0,1) (activations), Bt ~ N(0,0.02^2)
     (weights), both bf16."""
-    A = normal_bf16((M, K), 1.0, seed * 2 + 1)
-    Bt = normal_bf16((N, K), 0.02, seed * 2 + 2)
+    A = normal_bf16((M, K), 1.0, seed * 2 + 1, device)
+    Bt = normal_bf16((N, K), 0.02, seed * 2 + 2, device)
     return A, Bt
+
+
+def balanced_moe_row_dst(rows_per_src: int, n_ranks: int) -> np.ndarray:
+    """Exact-balanced EP routing (SURVEY.md §8(d) C4 variant): an expert rank
+    holds rows_per_src rows from every source rank, sorted by source."""
+    return np.repeat(np.arange(n_ranks, dtype=np.int32), rows_per_src)
 
 
 def exact_inputs(M: int, N: int, K: int, seed: int, nnz_per_row: int):
@@ -143,3 +152,12 @@ def moe_routing(tokens: int, n_experts: int, topk: int, n_ranks: int, seed: int)
         rows.sort()
         out.append(np.array([s for s, _ in rows], dtype=np.int32))
     return out
+
+
+def pad_row_dst(row_dst, multiple: int, own_rank: int) -> np.ndarray:
+    """Pad an expert's routed rows to a multiple of the GEMM tile height, as MoE
+    expert kernels pad token counts; padding rows (zero activations) stay on the
+    expert's own rank and are appended after the routed rows."""
+    row_dst = np.asarray(row_dst, np.int32)
+    pad = (-len(row_dst)) % multiple
+    return np.concatenate([row_dst, np.full(pad, own_rank, np.int32)])
