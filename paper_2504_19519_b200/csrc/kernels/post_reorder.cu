@@ -96,74 +96,54 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
 }
 
 constexpr int UNROLL = 4;
+constexpr int SEG_CHUNKS = 32 * UNROLL;  // 16-byte chunks per work unit (2 KB)
 
-// One warp per output row; lane l handles chunks l, l+32, ... (16 B each).
+// Copy / residual-add: work unit = (row, 2 KB segment) so that outputs with
+// few rows (RS: M/n rows) still fill every SM.  One warp per unit; lane l
+// moves chunks l, l+32, l+64, l+96 with UNROLL independent loads in flight.
 template <int MAP, int OP>
 __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p, int lbn) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t chunks = p.N >> 3;
+  const int64_t upr = (chunks + SEG_CHUNKS - 1) / SEG_CHUNKS;  // units per row
+  const int64_t units = p.rows * upr;
   const int bn_mask = p.BN - 1;
   const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
   const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(p.residual);
   const bool inplace = (p.src == p.out);
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.rows; r += warps) {
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units; u += warps) {
+    const int64_t r = u / upr;
+    const int64_t c0 = (u - r * upr) * SEG_CHUNKS;
     const RowSrc rs = row_src<MAP>(p, r);
     __nv_bfloat16* orow = out + r * p.N;
     const __nv_bfloat16* rrow = res ? res + r * p.N : nullptr;
-    if (OP == FO_POST_ADD_RMSNORM) {
-      // pass 1: sum of squares of y = x + residual (fp32)
-      float ss = 0.f;
-      for (int64_t c = lane; c < chunks; c += 32) {
-        float x[8], y[8];
-        unpack8(ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask)), x);
-        unpack8(ld_stream(rrow + 8 * c), y);
+    if (c0 + SEG_CHUNKS <= chunks) {
+      uint4 v[UNROLL];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float t = x[i] + y[i];
-          ss += t * t;
+      for (int k = 0; k < UNROLL; ++k) {
+        const __nv_bfloat16* sp = src + chunk_src<MAP>(rs, 8 * (c0 + lane + 32 * k), lbn, bn_mask);
+        v[k] = inplace ? ld_coherent(sp) : ld_stream(sp);
+      }
+      if (OP == FO_POST_ADD) {
+        uint4 w[UNROLL];
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) w[k] = ld_stream(rrow + 8 * (c0 + lane + 32 * k));
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) {
+          float x[8], y[8];
+          unpack8(v[k], x);
+          unpack8(w[k], y);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] += y[i];
+          v[k] = pack8(x);
         }
       }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      const float rstd = rsqrtf(ss / (float)p.N + p.eps);
-      const __nv_bfloat16* gam = reinterpret_cast<const __nv_bfloat16*>(p.gamma);
-      // pass 2 (the re-read hits L2): out = y * rstd * gamma
-      for (int64_t c = lane; c < chunks; c += 32) {
-        float x[8], y[8], g[8];
-        unpack8(ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask)), x);
-        unpack8(ld_coherent(rrow + 8 * c), y);
-        unpack8(ld_coherent(gam + 8 * c), g);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = (x[i] + y[i]) * rstd * g[i];
-        st_stream(orow + 8 * c, pack8(x));
-      }
+      for (int k = 0; k < UNROLL; ++k) st_stream(orow + 8 * (c0 + lane + 32 * k), v[k]);
     } else {
-      int64_t c = lane;
-      // batches of UNROLL independent 16-byte loads in flight per lane
-      for (; c + 32 * (UNROLL - 1) < chunks; c += 32 * UNROLL) {
-        uint4 v[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          const __nv_bfloat16* sp = src + chunk_src<MAP>(rs, 8 * (c + 32 * u), lbn, bn_mask);
-          v[u] = inplace ? ld_coherent(sp) : ld_stream(sp);
-        }
-        if (OP == FO_POST_ADD) {
-#pragma unroll
-          for (int u = 0; u < UNROLL; ++u) {
-            float x[8], y[8];
-            unpack8(v[u], x);
-            unpack8(ld_stream(rrow + 8 * (c + 32 * u)), y);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] += y[i];
-            v[u] = pack8(x);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) st_stream(orow + 8 * (c + 32 * u), v[u]);
-      }
-      for (; c < chunks; c += 32) {
+      for (int64_t c = c0 + lane; c < chunks; c += 32) {
         const __nv_bfloat16* sp = src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask);
         uint4 v = inplace ? ld_coherent(sp) : ld_stream(sp);
         if (OP == FO_POST_ADD) {
@@ -180,15 +160,128 @@ __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p, 
   }
 }
 
+// Residual add + RMSNorm: one 256-thread block per row, the whole row held in
+// registers (MAXC chunks of 8 per thread, N <= 2048*MAXC), single pass over HBM:
+// read x (through the map) and residual once, write out once.
+template <int MAP, int MAXC>
+__global__ void __launch_bounds__(256) fo_post_rmsnorm_kernel(const PostArgs p, int lbn) {
+  __shared__ float red[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t chunks = p.N >> 3;
+  const int bn_mask = p.BN - 1;
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  const __nv_bfloat16* gam = reinterpret_cast<const __nv_bfloat16*>(p.gamma);
+  for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const RowSrc rs = row_src<MAP>(p, r);
+    const __nv_bfloat16* rrow = reinterpret_cast<const __nv_bfloat16*>(p.residual) + r * p.N;
+    __nv_bfloat16* orow = out + r * p.N;
+    uint4 xv[MAXC], rv[MAXC];
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int64_t c = tid + 256 * i;
+      if (c < chunks) {
+        xv[i] = ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask));
+        rv[i] = ld_stream(rrow + 8 * c);
+      }
+    }
+    float y[MAXC][8];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int64_t c = tid + 256 * i;
+      if (c < chunks) {
+        float x[8], q[8];
+        unpack8(xv[i], x);
+        unpack8(rv[i], q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          y[i][k] = x[k] + q[k];
+          ss += y[i][k] * y[i][k];
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    __syncthreads();  // red[] reused by the next row
+    const float rstd = rsqrtf(tot / (float)p.N + p.eps);
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int64_t c = tid + 256 * i;
+      if (c < chunks) {
+        float g[8];
+        unpack8(ld_coherent(gam + 8 * c), g);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) y[i][k] = y[i][k] * rstd * g[k];
+        st_stream(orow + 8 * c, pack8(y[i]));
+      }
+    }
+  }
+}
+
+// Fallback for very wide rows (N > 16384): warp per row, two passes (the
+// second read hits L2).
+template <int MAP>
+__global__ void __launch_bounds__(256) fo_post_rmsnorm_wide_kernel(const PostArgs p, int lbn) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t chunks = p.N >> 3;
+  const int bn_mask = p.BN - 1;
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  const __nv_bfloat16* gam = reinterpret_cast<const __nv_bfloat16*>(p.gamma);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.rows; r += warps) {
+    const RowSrc rs = row_src<MAP>(p, r);
+    const __nv_bfloat16* rrow = reinterpret_cast<const __nv_bfloat16*>(p.residual) + r * p.N;
+    float ss = 0.f;
+    for (int64_t c = lane; c < chunks; c += 32) {
+      float x[8], y[8];
+      unpack8(ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask)), x);
+      unpack8(ld_coherent(rrow + 8 * c), y);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += (x[i] + y[i]) * (x[i] + y[i]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float rstd = rsqrtf(ss / (float)p.N + p.eps);
+    for (int64_t c = lane; c < chunks; c += 32) {
+      float x[8], y[8], g[8];
+      unpack8(ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask)), x);
+      unpack8(ld_coherent(rrow + 8 * c), y);
+      unpack8(ld_coherent(gam + 8 * c), g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = (x[i] + y[i]) * rstd * g[i];
+      st_stream(out + r * p.N + 8 * c, pack8(x));
+    }
+  }
+}
+
 int g_num_sms = 0;
 
 template <int MAP>
-cudaError_t launch_map(const PostArgs& a, int grid, int lbn, cudaStream_t stream) {
-  switch (a.op) {
-    case FO_POST_ADD: fo_post_reorder_kernel<MAP, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
-    case FO_POST_ADD_RMSNORM: fo_post_reorder_kernel<MAP, FO_POST_ADD_RMSNORM><<<grid, 256, 0, stream>>>(a, lbn); break;
-    default: fo_post_reorder_kernel<MAP, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
+cudaError_t launch_map(const PostArgs& a, int lbn, cudaStream_t stream) {
+  const int64_t chunks = a.N / 8;
+  if (a.op == FO_POST_ADD_RMSNORM) {
+    const int grid = (int)std::min<int64_t>(a.rows, (int64_t)g_num_sms * 8);
+    if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 1><<<grid, 256, 0, stream>>>(a, lbn);
+    else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 2><<<grid, 256, 0, stream>>>(a, lbn);
+    else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 4><<<grid, 256, 0, stream>>>(a, lbn);
+    else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8><<<grid, 256, 0, stream>>>(a, lbn);
+    else {
+      const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)g_num_sms * 8);
+      fo_post_rmsnorm_wide_kernel<MAP><<<g2, 256, 0, stream>>>(a, lbn);
+    }
+    return cudaGetLastError();
   }
+  const int64_t units = a.rows * ((chunks + SEG_CHUNKS - 1) / SEG_CHUNKS);
+  const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)g_num_sms * 16);
+  if (a.op == FO_POST_ADD) fo_post_reorder_kernel<MAP, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn);
+  else fo_post_reorder_kernel<MAP, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn);
   return cudaGetLastError();
 }
 
@@ -205,14 +298,12 @@ cudaError_t launch_post(const PostArgs& a, cudaStream_t stream) {
   }
   int lbn = 0;
   while ((1 << lbn) < a.BN) ++lbn;
-  const int64_t blocks_needed = (a.rows + 7) / 8;  // 8 warps (rows) per block
-  const int grid = (int)std::min<int64_t>(blocks_needed, (int64_t)g_num_sms * 8);
   cudaError_t e;
   switch (a.map) {
-    case POSTMAP_SLOT: e = launch_map<POSTMAP_SLOT>(a, grid, lbn, stream); break;
-    case POSTMAP_RS: e = launch_map<POSTMAP_RS>(a, grid, lbn, stream); break;
-    case POSTMAP_A2A: e = launch_map<POSTMAP_A2A>(a, grid, lbn, stream); break;
-    default: e = launch_map<POSTMAP_IDENTITY>(a, grid, lbn, stream); break;
+    case POSTMAP_SLOT: e = launch_map<POSTMAP_SLOT>(a, lbn, stream); break;
+    case POSTMAP_RS: e = launch_map<POSTMAP_RS>(a, lbn, stream); break;
+    case POSTMAP_A2A: e = launch_map<POSTMAP_A2A>(a, lbn, stream); break;
+    default: e = launch_map<POSTMAP_IDENTITY>(a, lbn, stream); break;
   }
   count_launch();
   return e;
