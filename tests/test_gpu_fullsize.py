@@ -146,13 +146,14 @@ def test_c4_ep8_alltoall(routing):
     else:
         rds = [synthetic.pad_row_dst(rd, BM, e) for e, rd in enumerate(synthetic.moe_routing(4096, 8, 2, n, 40000))]
     P = 2
+    BNe = 128  # 1024 rows x 4096 cols -> 128 tiles of 256x128 -> T = 2 at S = 64
     specs = []
     for e in range(n):
         M = len(rds[e])
-        tiles = (M // BM) * (N // BN)
+        tiles = (M // BM) * (N // BNe)
         Se = min(S, tiles)
         T = -(-tiles // Se)
-        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=Se,
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BNe, workers=Se,
                           group_waves=[1, T - 1] if T > 1 else [1], row_dst=rds[e]))
     if any(len(s["group_waves"]) != P for s in specs):
         pytest.skip("an expert got a single wave")
@@ -175,7 +176,7 @@ def test_c4_ep8_alltoall(routing):
                 pool_base = int(sc.sum(axis=0)[:d].sum())
                 start = int(sc[:j, d].sum())
                 cnt = int(sc[j, d])
-                parts.append(sends[s][(pool_base + start) * BN:(pool_base + start + cnt) * BN])
+                parts.append(sends[s][(pool_base + start) * BNe:(pool_base + start + cnt) * BNe])
         recv = torch.cat(parts)
         assert recv.numel() == plans[d].info["recv_elems"]
         out = torch.empty(plans[d].info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
