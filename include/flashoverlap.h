@@ -198,6 +198,21 @@ fo_status fo_post_stage(fo_plan plan, const void* recv, void* out, const void* r
                         const void* gamma, void* stream);
 /* Copy the plan's P counters to host (synchronises the device). */
 fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
+/* Debug / evidence hooks (tests, tools; never needed for correct use):
+ *  tile_ts  device uint64[tiles] or NULL: fo_run records %globaltimer (ns)
+ *           when each execution position signals (PAPER.md:230 fig:wave);
+ *  group_ts device uint64[2P] or NULL: fo_run records %globaltimer on the
+ *           comm stream right after group j's wait is released (2j) and after
+ *           its collective + per-group post-reorder (2j+1) — causality and
+ *           overlap evidence;
+ *  group_post -1 auto (default), 0 off, 1 on: run the post-communication
+ *           reorder per group right after its collective (only for non-identity
+ *           maps with op none/add; RMSNorm always runs once at the end). */
+fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned long long* group_ts,
+                            int32_t group_post);
+/* Fill the library-owned send/receive buffers of the plan with a bf16 bit
+ * pattern on `stream` (poison for the memory-ordering stress test). */
+fo_status fo_plan_fill_buffers(fo_plan plan, uint16_t pattern, void* stream);
 /* Number of kernels the library launched since load (for gpu_launches). */
 int64_t fo_kernel_launch_count(void);
 

@@ -136,6 +136,14 @@ class Plan:
         check(load().fo_plan_read_counters(self._h, c.ctypes.data_as(C.POINTER(C.c_uint32))))
         return c
 
+    def set_debug(self, tile_ts=None, group_ts=None, group_post: int = -1):
+        """Evidence hooks: device int64 tensors for tile / group timestamps; group_post -1/0/1."""
+        self._dbg = (tile_ts, group_ts)  # keep alive
+        check(load().fo_plan_set_debug(self._h, _ptr(tile_ts), _ptr(group_ts), int(group_post)))
+
+    def fill_buffers(self, pattern: int, stream=None):
+        check(load().fo_plan_fill_buffers(self._h, int(pattern) & 0xFFFF, _stream(stream)))
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             load().fo_plan_destroy(self._h)

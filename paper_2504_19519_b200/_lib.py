@@ -78,6 +78,8 @@ _SIGS = [
     ("fo_post_stage", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("fo_plan_read_counters", C.c_int, [_P, C.POINTER(C.c_uint32)]),
     ("fo_kernel_launch_count", C.c_int64, []),
+    ("fo_plan_set_debug", C.c_int, [_P, _P, _P, C.c_int32]),
+    ("fo_plan_fill_buffers", C.c_int, [_P, C.c_uint16, _P]),
     ("fo_tune_predict", C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_double,
                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double)]),
     ("fo_tune_search", C.c_int, [C.c_double, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_double),

@@ -50,9 +50,31 @@ struct PostArgs {
   float eps;
 };
 
+// Post-reorder of ONE wave group's data right after its collective (DESIGN.md
+// H11b): AR-slot / RS move whole per-position blocks of R rows x BN
+// (R = BM for AR, h for RS) from src + p*R*BN to out tile (i, jc); A2A moves
+// the group's received subtokens [sub_begin, sub_end) through recv_dst.
+struct GroupPostArgs {
+  int map;                 // POSTMAP_SLOT / POSTMAP_RS / POSTMAP_A2A
+  int op;                  // FO_POST_NONE or FO_POST_ADD
+  const void* src;
+  void* out;
+  const void* residual;
+  int64_t N;
+  int BN, Nt, R;
+  int pos_begin, pos_end;          // positions of the group (SLOT / RS)
+  const int32_t* order;            // device
+  int64_t sub_begin, sub_end;      // received subtokens of the group (A2A)
+  const int32_t* recv_dst;         // device
+  int grid_cap;                    // max blocks (0 = default)
+};
+
 // Returns a cudaError_t-compatible code (0 = success).
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream);
 cudaError_t launch_post(const PostArgs& a, cudaStream_t stream);
+cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream);
+cudaError_t launch_timestamp(unsigned long long* dst, cudaStream_t stream);
+cudaError_t launch_fill_u16(void* dst, int64_t count, uint16_t value, cudaStream_t stream);
 bool gemm_shape_supported(int BM, int BN);
 void count_launch();
 int64_t launch_count();

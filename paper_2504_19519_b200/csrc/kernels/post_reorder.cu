@@ -261,6 +261,65 @@ __global__ void __launch_bounds__(256) fo_post_rmsnorm_wide_kernel(const PostArg
   }
 }
 
+// Per-group post-reorder.  Unit = one warp x 32 chunks (512 B) of the group's
+// contiguous received data; reads are fully contiguous, each 16-byte chunk is
+// written to its row of the output tile.
+template <int MAP, int OP>
+__global__ void __launch_bounds__(256) fo_post_group_kernel(const GroupPostArgs p, int lbn) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int cpr = p.BN >> 3;  // chunks per BN-wide row segment
+  int64_t c_begin, c_end;
+  if (MAP == POSTMAP_A2A) {
+    c_begin = p.sub_begin * cpr;
+    c_end = p.sub_end * cpr;
+  } else {
+    c_begin = (int64_t)p.pos_begin * p.R * cpr;
+    c_end = (int64_t)p.pos_end * p.R * cpr;
+  }
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(p.residual);
+  for (int64_t c = c_begin + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32 + lane; c < c_end;
+       c += warps * 32) {
+    int64_t dst;
+    const int64_t seg = c / cpr;               // BN-wide row segment index in the receive buffer
+    const int b = (int)(c - seg * cpr) * 8;
+    if (MAP == POSTMAP_A2A) {
+      const int32_t d = __ldg(p.recv_dst + seg);
+      const int64_t orow = d / p.Nt;
+      dst = orow * p.N + (int64_t)(d - orow * p.Nt) * p.BN + b;
+    } else {
+      const int64_t pos = seg / p.R;
+      const int a = (int)(seg - pos * p.R);
+      const int t = __ldg(p.order + pos);
+      const int ti = t / p.Nt, tj = t - ti * p.Nt;
+      dst = ((int64_t)ti * p.R + a) * p.N + (int64_t)tj * p.BN + b;
+    }
+    uint4 v = ld_stream(src + 8 * c);
+    if (OP == FO_POST_ADD) {
+      float x[8], y[8];
+      unpack8(v, x);
+      unpack8(ld_stream(res + dst), y);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] += y[i];
+      v = pack8(x);
+    }
+    st_stream(out + dst, v);
+  }
+}
+
+__global__ void fo_timestamp_kernel(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
+__global__ void fo_fill_u16_kernel(uint16_t* dst, int64_t n, uint16_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
 int g_num_sms = 0;
 
 template <int MAP>
@@ -286,6 +345,43 @@ cudaError_t launch_map(const PostArgs& a, int lbn, cudaStream_t stream) {
 }
 
 }  // namespace
+
+cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream) {
+  if (a.BN & (a.BN - 1)) return cudaErrorInvalidValue;
+  int lbn = 0;
+  while ((1 << lbn) < a.BN) ++lbn;
+  const int64_t cpr = a.BN / 8;
+  const int64_t chunks = (a.map == POSTMAP_A2A) ? (a.sub_end - a.sub_begin) * cpr
+                                                 : (int64_t)(a.pos_end - a.pos_begin) * a.R * cpr;
+  if (chunks <= 0) return cudaSuccess;
+  const int cap = a.grid_cap > 0 ? a.grid_cap : 148 * 4;
+  const int grid = (int)std::min<int64_t>((chunks + 255) / 256, cap);
+  switch (a.map * 4 + a.op) {
+    case POSTMAP_SLOT * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_SLOT, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
+    case POSTMAP_SLOT * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_SLOT, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
+    case POSTMAP_RS * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_RS, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
+    case POSTMAP_RS * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_RS, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
+    case POSTMAP_A2A * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_A2A, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
+    case POSTMAP_A2A * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_A2A, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_timestamp(unsigned long long* dst, cudaStream_t stream) {
+  fo_timestamp_kernel<<<1, 1, 0, stream>>>(dst);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_u16(void* dst, int64_t count, uint16_t value, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 8);
+  fo_fill_u16_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<uint16_t*>(dst), count, value);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_post(const PostArgs& a, cudaStream_t stream) {
   if (a.rows <= 0) return cudaSuccess;

@@ -226,6 +226,7 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
         }
       p.recv_elems = off * p.BN;
       p.src_row.assign((size_t)p.out_rows * p.Nt, -1);
+      p.recv_dst.assign((size_t)off, -1);
       for (int s = 0; s < world; ++s) {
         const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
         const Grid& gs = pg[s];
@@ -237,6 +238,7 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
               int64_t row = (int64_t)i * ps->tile_m + r;
               if (ps->row_dst[row] != rank) continue;
               int64_t orow = p.src_base[s] + rank_of_row[s][row];
+              p.recv_dst[(size_t)idx] = (int32_t)(orow * p.Nt + jc);
               p.src_row[(size_t)orow * p.Nt + jc] = (int32_t)idx++;
             }
           }

@@ -42,6 +42,7 @@ struct PlanHost {
   std::vector<int64_t> recv_cnt;         // [P*world] subtokens of group j from source s
   std::vector<int64_t> recv_off;         // [P*world] receive-buffer subtoken offset, layout [group][source]
   std::vector<int32_t> src_row;          // [out_rows*Nt] receive-buffer subtoken index for out row r, col block j
+  std::vector<int32_t> recv_dst;         // [recv subtokens] out_row*Nt + col block of each received subtoken
   std::vector<int64_t> src_base;         // [world+1] first output row of each source
 
   int64_t out_rows = 0;

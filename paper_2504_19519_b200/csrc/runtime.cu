@@ -74,7 +74,7 @@ void release_device(fo_plan_s* p) {
   cudaSetDevice(p->device);
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
-                    p->d_rowmajor})
+                    p->d_rowmajor, (void*)p->d_recv_dst})
     if (ptr) cudaFree(ptr);
   cudaSetDevice(cur);
   p->device = -1;
@@ -104,6 +104,7 @@ static void ensure_device(fo_plan_s* p) {
   p->d_gpos = upload(h.gpos);
   p->d_row_slot = upload(h.row_slot);
   p->d_src_row = upload(h.src_row);
+  p->d_recv_dst = upload(h.recv_dst);
   FO_CUDA(cudaMalloc(&p->d_counters, sizeof(uint32_t) * h.P));
   FO_CUDA(cudaMemset(p->d_counters, 0, sizeof(uint32_t) * h.P));
   const bool need_send = !(h.coll == FO_NOCOMM || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND));
@@ -195,6 +196,42 @@ static int post_map(const PlanHost& h) {
 static cuuint32_t signal_target(const PlanHost& h, int j) { return (cuuint32_t)(h.group_tiles(j) * (h.BM / 128)); }
 
 static ncclDataType_t bf16() { return ncclBfloat16; }
+
+// Per-group post-reorder (H11b) applies to the non-identity maps
+// when the fused op is elementwise per element (none / residual add); RMSNorm
+// needs whole rows and runs once after the last group.
+static bool use_group_post(const fo_plan_s* p) {
+  const PlanHost& h = p->host;
+  if (p->group_post == 0) return false;
+  const int map = post_map(h);
+  return map != POSTMAP_IDENTITY && (h.post == FO_POST_NONE || h.post == FO_POST_ADD);
+}
+
+static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, const void* residual, cudaStream_t s) {
+  const PlanHost& h = p->host;
+  if (h.post == FO_POST_ADD && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
+  GroupPostArgs a{};
+  a.map = post_map(h);
+  a.op = h.post;
+  a.src = src;
+  a.out = out;
+  a.residual = residual;
+  a.N = h.N;
+  a.BN = h.BN;
+  a.Nt = h.Nt;
+  a.R = (h.coll == FO_REDUCESCATTER) ? h.h : h.BM;
+  a.pos_begin = h.gpos[j];
+  a.pos_end = h.gpos[j + 1];
+  a.order = p->d_order;
+  if (h.coll == FO_ALLTOALL) {
+    const int W = h.world;
+    a.sub_begin = h.recv_off[(size_t)j * W];
+    a.sub_end = (j + 1 < h.P) ? h.recv_off[(size_t)(j + 1) * W] : h.recv_elems / h.BN;
+  }
+  a.recv_dst = p->d_recv_dst;
+  a.grid_cap = 296;
+  FO_CUDA(launch_group_post(a, s));
+}
 
 // The collective of group j, on the comm stream ("Once the j-th
 // number reaches |G_j|, the communication of G_j starts").
@@ -338,15 +375,20 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     FO_CUDA(cudaEventRecord(c->ev_fork, s));
     FO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
     // 3. GEMM with reorder + signal epilogue
-    run_gemm(p, A, Bt, gemm_dst, epi_mode(h), true, s);
-    // 4. per-group wait + collective
+    run_gemm(p, A, Bt, gemm_dst, epi_mode(h), true, s, p->trace_tile_ts);
+    const bool gpost = use_group_post(p);
+    const void* post_src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : p->d_recv);
+    // 4. per-group wait + collective (+ per-group post-reorder)
     if (h.coll != FO_NOCOMM) {
       for (int j = 0; j < h.P; ++j) {
         CUresult r = wait(reinterpret_cast<CUstream>(c->comm_stream),
                           reinterpret_cast<CUdeviceptr>(p->d_counters + j), signal_target(h, j),
                           CU_STREAM_WAIT_VALUE_GEQ);
         if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j, c->comm_stream));
         group_collective(c, p, j, gemm_dst);
+        if (gpost) run_group_post(p, j, post_src, out, residual, c->comm_stream);
+        if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j + 1, c->comm_stream));
       }
     } else {
       // no communication: the comm stream only has to see the GEMM finish
@@ -357,12 +399,10 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
         if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
       }
     }
-    // 5. post-communication reorder (+ fused op)
+    // 5. post-communication reorder (+ fused op) when not done per group
     const int map = post_map(h);
-    if (map != POSTMAP_IDENTITY || h.post != FO_POST_NONE) {
-      const void* src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : p->d_recv);
-      run_post(p, map, src, out, residual, gamma, c->comm_stream);
-    }
+    if (!gpost && (map != POSTMAP_IDENTITY || h.post != FO_POST_NONE))
+      run_post(p, map, post_src, out, residual, gamma, c->comm_stream);
     // 6. join
     FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
     FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
@@ -461,5 +501,26 @@ fo_status fo_plan_read_counters(fo_plan p, uint32_t* counters) {
 }
 
 int64_t fo_kernel_launch_count(void) { return launch_count(); }
+
+fo_status fo_plan_set_debug(fo_plan p, unsigned long long* tile_ts, unsigned long long* group_ts,
+                            int32_t group_post) {
+  return guard([&] {
+    if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
+    if (group_post < -1 || group_post > 1) fail(FO_ERR_INVALID_ARG, "group_post must be -1, 0 or 1");
+    p->trace_tile_ts = tile_ts;
+    p->trace_group_ts = group_ts;
+    p->group_post = group_post;
+  });
+}
+
+fo_status fo_plan_fill_buffers(fo_plan p, uint16_t pattern, void* stream) {
+  return guard([&] {
+    if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
+    ensure_device(p);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (p->d_send) FO_CUDA(launch_fill_u16(p->d_send, p->host.send_elems, pattern, s));
+    if (p->d_recv) FO_CUDA(launch_fill_u16(p->d_recv, p->host.recv_elems, pattern, s));
+  });
+}
 
 }  // extern "C"

@@ -19,6 +19,11 @@ struct fo_plan_s {
   void* d_send = nullptr;  // pre-reordered send buffer (bf16), library-owned
   void* d_recv = nullptr;  // receive buffer (RS / A2A)
   void* d_rowmajor = nullptr;  // sequential baseline scratch (RS / A2A row-major C)
+  int32_t* d_recv_dst = nullptr;  // A2A received subtoken -> output position
+  // ---- debug / evidence hooks (fo_plan_set_debug)
+  unsigned long long* trace_tile_ts = nullptr;   // device [tiles]
+  unsigned long long* trace_group_ts = nullptr;  // device [2P]: wait released, group done
+  int group_post = -1;                            // -1 auto, 0 off, 1 on
 };
 
 namespace fo {

@@ -1,0 +1,117 @@
+"""Evidence that the signaling chain is correct and overlapped (world = 1,
+real fo_run with stream waits + NCCL):
+
+* causality: the comm stream's wait for group j is released only after every
+  tile of group j signalled (%globaltimer of the release >= the last tile of
+  the group) — PAPER.md:368 "Once the j-th number reaches |G_j|, the
+  communication of G_j starts";
+* overlap: group 0's wait is released (and its per-group post-reorder done)
+  while the GEMM still computes later waves;
+* memory ordering under stress: the library's send/receive
+  buffers are poisoned with NaN before every run and inputs alternate between
+  two data sets; any collective or post-reorder reading a group before its
+  tiles' stores are visible would leak NaN or stale values into the output;
+* per-group post-reorder (H11b) == one post-reorder after the last group.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synthetic
+
+pytestmark = pytest.mark.gpu
+fo = pytest.importorskip("paper_2504_19519_b200")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    c = fo.Context.create(0, 0, 1, fo.unique_id())
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("coll", ["allreduce", "reducescatter"])
+def test_causality_and_overlap(ctx, coll):
+    M, N, K, S = 4096, 4096, 7168, 64
+    groups = [1, 1, 1, 1]
+    A, Bt = synthetic.float_inputs(M, N, K, seed=3, device="cuda")
+    plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=2, group_waves=groups,
+                   ar_layout="slot")
+    tiles = plan.info["tiles"]
+    tile_ts = torch.zeros(tiles, dtype=torch.int64, device="cuda")
+    group_ts = torch.zeros(2 * len(groups), dtype=torch.int64, device="cuda")
+    plan.set_debug(tile_ts, group_ts)
+    out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+    for _ in range(3):
+        fo.run(ctx, plan, A, Bt, out)
+    torch.cuda.synchronize()
+    t = tile_ts.cpu().numpy()
+    g = group_ts.cpu().numpy()
+    gemm_end = t.max()
+    for j in range(len(groups)):
+        lo, hi, _, _ = plan.group(j)
+        assert g[2 * j] >= t[lo:hi].max(), f"group {j} released before its last tile signalled"
+        assert g[2 * j + 1] >= g[2 * j]
+    assert g[0] < gemm_end, "group 0's communication did not start before the GEMM finished"
+    assert g[1] < gemm_end, "group 0's collective + post-reorder did not finish inside the GEMM"
+
+
+@pytest.mark.parametrize("coll", ["allreduce", "reducescatter", "alltoall"])
+def test_memory_ordering_stress(ctx, coll):
+    M, N, K, S = 2048, 2048, 1024, 16
+    groups = [1, 1, 1, 1]  # 64 tiles of 256x256, 16 pairs -> 4 waves
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=2, group_waves=groups,
+              ar_layout="slot")
+    if coll == "alltoall":
+        kw["row_dst"] = np.zeros(M, np.int32)
+        plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
+    else:
+        plan = fo.Plan(**kw)
+    inputs = [synthetic.float_inputs(M, N, K, seed=s, device="cuda") for s in (11, 12)]
+    want = []
+    for A, Bt in inputs:
+        o = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+        fo.run_sequential(ctx, plan, A, Bt, o)
+        want.append(o)
+    torch.cuda.synchronize()
+    out = torch.empty_like(want[0])
+    bad = 0
+    for it in range(300):
+        A, Bt = inputs[it % 2]
+        plan.fill_buffers(0x7FC0)  # bf16 NaN
+        out.fill_(float("nan"))
+        fo.run(ctx, plan, A, Bt, out)
+        if not torch.equal(out, want[it % 2]):
+            bad += 1
+    torch.cuda.synchronize()
+    assert bad == 0, f"{bad} of 300 overlapped runs read data before it was complete"
+
+
+@pytest.mark.parametrize("coll,post", [("allreduce", "none"), ("allreduce", "add"), ("reducescatter", "add"),
+                                       ("alltoall", "none")])
+def test_group_post_equals_single_post(ctx, coll, post):
+    M, N, K, S = 2048, 1024, 512, 8
+    tiles = (M // 256) * (N // 128)
+    T = -(-tiles // S)
+    groups = synthetic.random_partition(T, 4)
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=128, workers=S, swizzle=3, group_waves=groups,
+              ar_layout="slot", post=post)
+    if coll == "alltoall":
+        kw["row_dst"] = np.zeros(M, np.int32)
+        mk = lambda: fo.Plan(rank=0, world=1, peers=[kw], **kw)
+    else:
+        mk = lambda: fo.Plan(**kw)
+    p_on, p_off = mk(), mk()
+    p_off.set_debug(group_post=0)
+    A, Bt = synthetic.float_inputs(M, N, K, seed=9, device="cuda")
+    res = synthetic.normal_bf16((p_on.info["out_rows"], N), 1.0, 5, device="cuda")
+    o1 = torch.empty(p_on.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    fo.run(ctx, p_on, A, Bt, o1, res if post != "none" else None)
+    fo.run(ctx, p_off, A, Bt, o2, res if post != "none" else None)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
