@@ -210,6 +210,13 @@ fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
  *           maps with op none/add; RMSNorm always runs once at the end). */
 fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned long long* group_ts,
                             int32_t group_post);
+/* Plan options (run-time knobs; defaults shown):
+ *  FO_OPT_GROUP_POST  -1 auto | 0 off | 1 on — as group_post above
+ *  FO_OPT_WAIT_KERNEL  0 — trigger = cuStreamWaitValue32 (front-end wait, no SM)
+ *                      1 — trigger = the paper's signaling kernel:
+ *                          a 1-warp kernel spinning on an acquire load */
+typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1 } fo_option;
+fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */
 fo_status fo_plan_fill_buffers(fo_plan plan, uint16_t pattern, void* stream);

@@ -74,6 +74,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream);
 cudaError_t launch_post(const PostArgs& a, cudaStream_t stream);
 cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream);
 cudaError_t launch_timestamp(unsigned long long* dst, cudaStream_t stream);
+cudaError_t launch_wait(const uint32_t* counter, uint32_t target, cudaStream_t stream);
 cudaError_t launch_fill_u16(void* dst, int64_t count, uint16_t value, cudaStream_t stream);
 bool gemm_shape_supported(int BM, int BN);
 void count_launch();

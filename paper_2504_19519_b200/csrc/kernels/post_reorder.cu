@@ -315,6 +315,20 @@ __global__ void fo_timestamp_kernel(unsigned long long* dst) {
   *dst = t;
 }
 
+// The paper's signaling kernel: spin until the group counter
+// reaches its target (cyclic comparison, like CU_STREAM_WAIT_VALUE_GEQ), with
+// acquire semantics so the following stream work sees the group's data.
+__global__ void fo_wait_kernel(const uint32_t* ctr, uint32_t target) {
+  if (threadIdx.x == 0) {
+    uint32_t v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if ((int32_t)(v - target) >= 0) break;
+      __nanosleep(64);
+    }
+  }
+}
+
 __global__ void fo_fill_u16_kernel(uint16_t* dst, int64_t n, uint16_t v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = v;
@@ -371,6 +385,12 @@ cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream) {
 
 cudaError_t launch_timestamp(unsigned long long* dst, cudaStream_t stream) {
   fo_timestamp_kernel<<<1, 1, 0, stream>>>(dst);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait(const uint32_t* counter, uint32_t target, cudaStream_t stream) {
+  fo_wait_kernel<<<1, 32, 0, stream>>>(counter, target);
   count_launch();
   return cudaGetLastError();
 }

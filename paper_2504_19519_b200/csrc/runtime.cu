@@ -197,6 +197,20 @@ static cuuint32_t signal_target(const PlanHost& h, int j) { return (cuuint32_t)(
 
 static ncclDataType_t bf16() { return ncclBfloat16; }
 
+// Trigger: block the comm stream until group j's counter
+// reaches its target — a front-end stream wait (no SM) or the paper's
+// signaling kernel (a 1-warp spin on an acquire load).
+static void stream_wait(fo_plan_s* p, WaitValue32Fn wait, cudaStream_t cs, int j) {
+  const cuuint32_t target = signal_target(p->host, j);
+  if (p->wait_kernel) {
+    FO_CUDA(launch_wait(p->d_counters + j, target, cs));
+    return;
+  }
+  CUresult r = wait(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(p->d_counters + j), target,
+                    CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+}
+
 // Per-group post-reorder (H11b) applies to the non-identity maps
 // when the fused op is elementwise per element (none / residual add); RMSNorm
 // needs whole rows and runs once after the last group.
@@ -381,10 +395,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     // 4. per-group wait + collective (+ per-group post-reorder)
     if (h.coll != FO_NOCOMM) {
       for (int j = 0; j < h.P; ++j) {
-        CUresult r = wait(reinterpret_cast<CUstream>(c->comm_stream),
-                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), signal_target(h, j),
-                          CU_STREAM_WAIT_VALUE_GEQ);
-        if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        stream_wait(p, wait, c->comm_stream, j);
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j, c->comm_stream));
         group_collective(c, p, j, gemm_dst);
         if (gpost) run_group_post(p, j, post_src, out, residual, c->comm_stream);
@@ -393,10 +404,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     } else {
       // no communication: the comm stream only has to see the GEMM finish
       for (int j = 0; j < h.P; ++j) {
-        CUresult r = wait(reinterpret_cast<CUstream>(c->comm_stream),
-                          reinterpret_cast<CUdeviceptr>(p->d_counters + j), signal_target(h, j),
-                          CU_STREAM_WAIT_VALUE_GEQ);
-        if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        stream_wait(p, wait, c->comm_stream, j);
       }
     }
     // 5. post-communication reorder (+ fused op) when not done per group
@@ -510,6 +518,24 @@ fo_status fo_plan_set_debug(fo_plan p, unsigned long long* tile_ts, unsigned lon
     p->trace_tile_ts = tile_ts;
     p->trace_group_ts = group_ts;
     p->group_post = group_post;
+  });
+}
+
+fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
+  return guard([&] {
+    if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
+    switch (option) {
+      case FO_OPT_GROUP_POST:
+        if (value < -1 || value > 1) fail(FO_ERR_INVALID_ARG, "group_post must be -1, 0 or 1");
+        p->group_post = (int)value;
+        break;
+      case FO_OPT_WAIT_KERNEL:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "wait_kernel must be 0 or 1");
+        p->wait_kernel = (int)value;
+        break;
+      default:
+        fail(FO_ERR_INVALID_ARG, "unknown option %d", option);
+    }
   });
 }
 

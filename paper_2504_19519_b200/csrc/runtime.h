@@ -24,6 +24,7 @@ struct fo_plan_s {
   unsigned long long* trace_tile_ts = nullptr;   // device [tiles]
   unsigned long long* trace_group_ts = nullptr;  // device [2P]: wait released, group done
   int group_post = -1;                            // -1 auto, 0 off, 1 on
+  int wait_kernel = 0;                            // 0 cuStreamWaitValue32, 1 spin-wait kernel
 };
 
 namespace fo {
