@@ -141,6 +141,10 @@ class Plan:
         self._dbg = (tile_ts, group_ts)  # keep alive
         check(load().fo_plan_set_debug(self._h, _ptr(tile_ts), _ptr(group_ts), int(group_post)))
 
+    def set_option(self, name: str, value: int):
+        """Run-time knobs: group_post (-1/0/1), wait_kernel (0 stream wait, 1 spin kernel)."""
+        check(load().fo_plan_set_option(self._h, _lib.OPTION[name], int(value)))
+
     def fill_buffers(self, pattern: int, stream=None):
         check(load().fo_plan_fill_buffers(self._h, int(pattern) & 0xFFFF, _stream(stream)))
 

@@ -19,6 +19,7 @@ STATUS_NAMES = ["OK", "INVALID_ARG", "SHAPE", "UNSUPPORTED", "CUDA", "NCCL", "OO
 COLL = {"allreduce": 0, "reducescatter": 1, "alltoall": 2, "nocomm": 3}
 LAYOUT = {"slot": 0, "rowband": 1, "auto": 2}
 POST = {"none": 0, "add": 1, "add_rmsnorm": 2}
+OPTION = {"group_post": 0, "wait_kernel": 1}
 
 
 class FOError(RuntimeError):
@@ -80,6 +81,7 @@ _SIGS = [
     ("fo_kernel_launch_count", C.c_int64, []),
     ("fo_plan_set_debug", C.c_int, [_P, _P, _P, C.c_int32]),
     ("fo_plan_fill_buffers", C.c_int, [_P, C.c_uint16, _P]),
+    ("fo_plan_set_option", C.c_int, [_P, C.c_int32, C.c_int64]),
     ("fo_tune_predict", C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_double,
                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double)]),
     ("fo_tune_search", C.c_int, [C.c_double, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_double),

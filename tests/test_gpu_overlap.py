@@ -34,13 +34,15 @@ def ctx():
     c.close()
 
 
+@pytest.mark.parametrize("wait_kernel", [0, 1])
 @pytest.mark.parametrize("coll", ["allreduce", "reducescatter"])
-def test_causality_and_overlap(ctx, coll):
+def test_causality_and_overlap(ctx, coll, wait_kernel):
     M, N, K, S = 4096, 4096, 7168, 64
     groups = [1, 1, 1, 1]
     A, Bt = synthetic.float_inputs(M, N, K, seed=3, device="cuda")
     plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=2, group_waves=groups,
                    ar_layout="slot")
+    plan.set_option("wait_kernel", wait_kernel)
     tiles = plan.info["tiles"]
     tile_ts = torch.zeros(tiles, dtype=torch.int64, device="cuda")
     group_ts = torch.zeros(2 * len(groups), dtype=torch.int64, device="cuda")
@@ -60,8 +62,9 @@ def test_causality_and_overlap(ctx, coll):
     assert g[1] < gemm_end, "group 0's collective + post-reorder did not finish inside the GEMM"
 
 
+@pytest.mark.parametrize("wait_kernel", [0, 1])
 @pytest.mark.parametrize("coll", ["allreduce", "reducescatter", "alltoall"])
-def test_memory_ordering_stress(ctx, coll):
+def test_memory_ordering_stress(ctx, coll, wait_kernel):
     M, N, K, S = 2048, 2048, 1024, 16
     groups = [1, 1, 1, 1]  # 64 tiles of 256x256, 16 pairs -> 4 waves
     kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=2, group_waves=groups,
@@ -71,6 +74,7 @@ def test_memory_ordering_stress(ctx, coll):
         plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
     else:
         plan = fo.Plan(**kw)
+    plan.set_option("wait_kernel", wait_kernel)
     inputs = [synthetic.float_inputs(M, N, K, seed=s, device="cuda") for s in (11, 12)]
     want = []
     for A, Bt in inputs:

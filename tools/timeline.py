@@ -17,14 +17,15 @@ import synthetic  # noqa: E402
 from tools.gemm_probe import timeit  # noqa: E402
 
 
-def one(ctx, coll, M, N, K, BN, S, groups, layout="slot", flush=None):
-    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=BN, workers=S, swizzle=2, group_waves=groups,
-              ar_layout=layout)
+def one(ctx, coll, M, N, K, BN, S, groups, layout="slot", flush=None, wait_kernel=0):
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=BN, workers=S, swizzle=1 if layout == "rowband" else 2,
+              group_waves=groups, ar_layout=layout)
     if coll == "alltoall":
         kw["row_dst"] = np.zeros(M, np.int32)
         plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
     else:
         plan = fo.Plan(**kw)
+    plan.set_option("wait_kernel", wait_kernel)
     A, Bt = synthetic.float_inputs(M, N, K, seed=1, device="cuda")
     out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
     t_ov = timeit(lambda: fo.run(ctx, plan, A, Bt, out), flush=flush)
@@ -37,7 +38,8 @@ def one(ctx, coll, M, N, K, BN, S, groups, layout="slot", flush=None):
     torch.cuda.synchronize()
     t, g = tile_ts.cpu().numpy(), group_ts.cpu().numpy()
     t0 = t.min()
-    print(f"\n{coll} {M}x{N}x{K} tile 256x{BN} S={S} groups={groups} layout={plan.info['ar_layout']}: "
+    print(f"\n{coll} {M}x{N}x{K} tile 256x{BN} S={S} groups={groups} layout={plan.info['ar_layout']} "
+          f"trigger={'spin-kernel' if wait_kernel else 'stream-wait'}: "
           f"fo_run {t_ov:.1f} us, sequential {t_seq:.1f} us, speedup {t_seq / t_ov:.3f}")
     print(f"  GEMM: first tile signal 0.0 us, last tile signal {(t.max() - t0) / 1e3:.1f} us")
     for j in range(len(groups)):
@@ -52,10 +54,11 @@ def main():
     torch.cuda.set_device(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 1, 1, 1], "slot", flush)
-    one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 2, 1], "rowband", flush)
-    one(ctx, "reducescatter", 8192, 8192, 1024, 256, 64, [2, 4, 6, 4], "auto", flush)
-    one(ctx, "alltoall", 1024, 4096, 14336, 128, 64, [1, 1], "auto", flush)
+    for wk in (0, 1):
+        one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 1, 1, 1], "slot", flush, wk)
+        one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 2, 1], "rowband", flush, wk)
+        one(ctx, "reducescatter", 8192, 8192, 1024, 256, 64, [2, 4, 6, 4], "auto", flush, wk)
+        one(ctx, "alltoall", 1024, 4096, 14336, 128, 64, [1, 1], "auto", flush, wk)
     ctx.close()
 
 
