@@ -175,6 +175,14 @@ fo_status fo_ctx_destroy(fo_ctx ctx);
  * post-reorder, join back to `stream`. */
 fo_status fo_run(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
                  const void* residual, const void* gamma, void* stream);
+/* fo_run with HOST buffers (same shapes as fo_run): stream-ordered
+ * host->device copies of A, Bt (+ residual, gamma) into library-owned device
+ * staging, the overlapped op, and the device->host copy of `out`, all on
+ * `stream` (host-asynchronous when the host buffers are page-locked; the
+ * caller synchronises the stream before reading `out`).  This is the
+ * end-to-end entry point bench.py's `e2e` number is measured through. */
+fo_status fo_run_host(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
+                      const void* residual, const void* gamma, void* stream);
 /* Non-overlapped baseline: the SAME GEMM kernel writing row-major C, then ONE
  * full-size NCCL call (AR in place; RS standard contiguous rows; A2A with
  * row_dst sorted ascending), then the fused elementwise op as its own pass. */

@@ -74,7 +74,7 @@ void release_device(fo_plan_s* p) {
   cudaSetDevice(p->device);
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
-                    p->d_rowmajor, (void*)p->d_recv_dst})
+                    p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma})
     if (ptr) cudaFree(ptr);
   cudaSetDevice(cur);
   p->device = -1;
@@ -414,6 +414,31 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     // 6. join
     FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
     FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  });
+}
+
+fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
+                      const void* gamma, void* stream) {
+  return guard([&] {
+    if (!c || !p || !A || !Bt || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    ensure_device(p);
+    const PlanHost& h = p->host;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t a_bytes = 2 * (size_t)(h.M * h.K), b_bytes = 2 * (size_t)(h.N * h.K);
+    const size_t o_bytes = 2 * (size_t)(h.out_rows * h.N);
+    if (!p->h_A) FO_CUDA(cudaMalloc(&p->h_A, a_bytes));
+    if (!p->h_Bt) FO_CUDA(cudaMalloc(&p->h_Bt, b_bytes));
+    if (!p->h_out) FO_CUDA(cudaMalloc(&p->h_out, o_bytes));
+    if (residual && !p->h_res) FO_CUDA(cudaMalloc(&p->h_res, o_bytes));
+    if (gamma && !p->h_gamma) FO_CUDA(cudaMalloc(&p->h_gamma, 2 * (size_t)h.N));
+    FO_CUDA(cudaMemcpyAsync(p->h_A, A, a_bytes, cudaMemcpyHostToDevice, s));
+    FO_CUDA(cudaMemcpyAsync(p->h_Bt, Bt, b_bytes, cudaMemcpyHostToDevice, s));
+    if (residual) FO_CUDA(cudaMemcpyAsync(p->h_res, residual, o_bytes, cudaMemcpyHostToDevice, s));
+    if (gamma) FO_CUDA(cudaMemcpyAsync(p->h_gamma, gamma, 2 * (size_t)h.N, cudaMemcpyHostToDevice, s));
+    fo_status st = fo_run(c, p, p->h_A, p->h_Bt, p->h_out, residual ? p->h_res : nullptr,
+                          gamma ? p->h_gamma : nullptr, stream);
+    if (st != FO_OK) throw Error(st, fo_last_error());
+    FO_CUDA(cudaMemcpyAsync(out, p->h_out, o_bytes, cudaMemcpyDeviceToHost, s));
   });
 }
 

@@ -20,6 +20,12 @@ struct fo_plan_s {
   void* d_recv = nullptr;  // receive buffer (RS / A2A)
   void* d_rowmajor = nullptr;  // sequential baseline scratch (RS / A2A row-major C)
   int32_t* d_recv_dst = nullptr;  // A2A received subtoken -> output position
+  // ---- device staging for fo_run_host (lazily allocated)
+  void* h_A = nullptr;
+  void* h_Bt = nullptr;
+  void* h_out = nullptr;
+  void* h_res = nullptr;
+  void* h_gamma = nullptr;
   // ---- debug / evidence hooks (fo_plan_set_debug)
   unsigned long long* trace_tile_ts = nullptr;   // device [tiles]
   unsigned long long* trace_group_ts = nullptr;  // device [2P]: wait released, group done
