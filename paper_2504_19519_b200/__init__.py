@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib
 from ._lib import COLL, LAYOUT, POST, FOError, check, load
 
-__all__ = ["Plan", "Context", "run", "run_sequential", "gemm_stage", "gemm_stage_timed", "post_stage",
+__all__ = ["Plan", "Context", "run", "run_host", "run_sequential", "gemm_stage", "gemm_stage_timed", "post_stage",
            "unique_id", "tune_search", "tune_predict", "kernel_launch_count", "FOError", "load",
            "device_sm_count"]
 
@@ -199,6 +199,12 @@ def _stream(stream):
 def run(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=None):
     check(load().fo_run(ctx._h, plan.handle, _ptr(A), _ptr(Bt), _ptr(out), _ptr(residual), _ptr(gamma),
                         _stream(stream)))
+
+
+def run_host(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=None):
+    """fo_run_host: A, Bt, out (and residual, gamma) are CPU tensors (pin them for async copies)."""
+    check(load().fo_run_host(ctx._h, plan.handle, _ptr(A), _ptr(Bt), _ptr(out), _ptr(residual), _ptr(gamma),
+                             _stream(stream)))
 
 
 def run_sequential(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=None):

@@ -74,6 +74,7 @@ _SIGS = [
     ("fo_ctx_destroy", C.c_int, [_P]),
     ("fo_run", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_sequential", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    ("fo_run_host", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_gemm_stage", C.c_int, [_P, _P, _P, _P, _P]),
     ("fo_gemm_stage_timed", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("fo_post_stage", C.c_int, [_P, _P, _P, _P, _P, _P]),

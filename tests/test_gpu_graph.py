@@ -59,3 +59,26 @@ def test_graph_capture_replay(coll, layout):
         torch.cuda.synchronize()
         assert torch.equal(out, want[it % 3])
     ctx.close()
+
+
+def test_run_host_matches_device_run():
+    """fo_run_host (host buffers, copies inside the call) == fo_run."""
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    M, N, K = 1024, 1024, 512
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=8, group_waves=[1, 1],
+                   ar_layout="slot", swizzle=2, post="add_rmsnorm")
+    A, Bt = synthetic.float_inputs(M, N, K, seed=4)
+    res = synthetic.normal_bf16((M, N), 1.0, 6)
+    gam = synthetic.normal_bf16((N,), 1.0, 7)
+    out_h = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    fo.run_host(ctx, plan, A.pin_memory(), Bt.pin_memory(), out_h, res.pin_memory(), gam.pin_memory())
+    torch.cuda.synchronize()
+    out_d = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, A.cuda(), Bt.cuda(), out_d, res.cuda(), gam.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, out_d.cpu())
+    ctx.close()
