@@ -1,0 +1,56 @@
+"""configs[4] shape sweep at N=1 (the heatmap analogue):
+M in {1k,2k,4k,8k,16k} x N=K in {4k,8k,16k}.  Per cell: our GEMM kernel
+(CTA-pair 256x256, wave-quantisation-aware S) vs cuBLAS (torch.matmul), the
+overlapped fo_run (AllReduce, world 1) vs fo_run_sequential, and the GEMM's
+fraction of the measured bf16 peak.  Dev tool; prints a table."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2504_19519_b200 as fo  # noqa: E402
+import synthetic  # noqa: E402
+from tools.gemm_probe import timeit  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def main():
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+    torch.cuda.set_device(0)
+    sms = fo.device_sm_count(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    print(f"{'M':>6} {'N=K':>6} {'tiles':>5} {'S':>3} {'T':>3} {'cublas_TF':>9} {'fo_TF':>7} {'frac':>5} "
+          f"{'fo_run_us':>9} {'seq_us':>8} {'speedup':>7}")
+    for M in (1024, 2048, 4096, 8192, 16384):
+        for NK in (4096, 8192, 16384):
+            N = K = NK
+            A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.cell_seed(M, N, K), device="cuda")
+            C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+            fl = 2.0 * M * N * K
+            t_cb = timeit(lambda: torch.matmul(A, Bt.t(), out=C), iters=10, flush=flush)
+            tiles = (M // 256) * (N // 256)
+            T_full = -(-tiles // (sms // 2))
+            S = -(-tiles // T_full)
+            T = -(-tiles // S)
+            gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S)
+            t_fo = timeit(lambda: fo.gemm_stage(gplan, A, Bt, C), iters=10, flush=flush)
+            groups = fo.tune_search(t_fo, tiles, S, 256 * 256 * 2, [(1 << 10, 1e6), (1 << 30, 1e6)])[0]
+            plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
+                           group_waves=list(groups))
+            t_ov = timeit(lambda: fo.run(ctx, plan, A, Bt, C), iters=10, flush=flush)
+            t_sq = timeit(lambda: fo.run_sequential(ctx, plan, A, Bt, C), iters=10, flush=flush)
+            tf = fl / t_fo / 1e6
+            print(f"{M:6d} {NK:6d} {tiles:5d} {S:3d} {T:3d} {fl / t_cb / 1e6:9.1f} {tf:7.1f} {tf / peak:5.2f} "
+                  f"{t_ov:9.1f} {t_sq:8.1f} {t_sq / t_ov:7.3f}", flush=True)
+            del A, Bt, C
+            torch.cuda.empty_cache()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
