@@ -37,7 +37,7 @@ def run_allreduce(As, Bts, plan: Plan, layout="slot", model_bf16=False):
     n = len(As)
     Ys = [_Y(As[r], Bts[r], model_bf16) for r in range(n)]
     bufs = [reorder.ar_pre(Ys[r], plan, layout) for r in range(n)]
-    red = collectives.allreduce_groups(bufs, reorder.group_elem_ranges(plan))
+    red = collectives.allreduce_groups(bufs, reorder.group_elem_ranges(plan, layout))
     outs = [reorder.ar_post(red[r], plan, layout) for r in range(n)]
     return {"Y": Ys, "send": bufs, "recv": red, "out": outs}
 

@@ -10,10 +10,12 @@ indices are reordered based on their execution order".
   AR: unit = tile.  Tile at execution position p goes to slot p
       (reading R2: slot = execution position), each slot BM*BN
       contiguous elements, row-major inside the slot.
-      Layout "rowband" (H11a): when the order is a row-major raster and
-      every group boundary falls on a whole tile-row, the slot layout is replaced
-      by the identity (the buffer IS row-major C); each group is then a
-      contiguous row band.  Both layouts are valid AR reorderings.
+      Layout "rowband" (H11a): when the tiles of every group are
+      exactly the complete tile-rows of one contiguous band [r0, r1) (any
+      execution order inside the group), the slot layout is replaced by the
+      identity (the buffer IS row-major C) and group j communicates its row
+      band [r0*BM*N, r1*BM*N).  Both layouts are valid AR reorderings
+      (only a consistent order across GPUs is required).
   RS: unit = subtile of h = BM/n rows.  Inside group j (positions
       [ps, pe), G = pe - ps), chunk k (the part ReduceScatter delivers to rank k)
       holds the k-th subtile of every tile of the group, tiles in execution
@@ -39,16 +41,30 @@ from .plan import OracleError, Plan
 
 
 # =========================================================== AllReduce
+def rowband_of_group(plan: Plan, lo: int, hi: int):
+    """(r0, r1) if the tiles at positions [lo, hi) are exactly the complete
+    tile-rows r0..r1-1, else None."""
+    tiles = sorted(int(t) for t in plan.order[lo:hi])
+    if not tiles or len(tiles) % plan.Nt:
+        return None
+    r0 = tiles[0] // plan.Nt
+    r1 = r0 + len(tiles) // plan.Nt
+    if tiles != list(range(r0 * plan.Nt, r1 * plan.Nt)):
+        return None
+    return r0, r1
+
+
 def ar_rowband_ok(plan: Plan) -> bool:
-    """Identity layout is valid iff the order is the row-major raster and every
-    group starts on a tile-row boundary (so each group is a row band of C)."""
-    if not np.array_equal(plan.order, np.arange(plan.ntiles)):
-        return False
-    return all(lo % plan.Nt == 0 for lo, _ in plan.ranges)
+    """Identity layout is valid iff every group's tiles form one band of
+    complete, contiguous tile-rows (so each group is a row band of C)."""
+    return all(rowband_of_group(plan, lo, hi) is not None for lo, hi in plan.ranges)
 
 
-def group_elem_ranges(plan: Plan) -> list[tuple[int, int]]:
+def group_elem_ranges(plan: Plan, layout: str = "slot") -> list[tuple[int, int]]:
     """Element range [lo, hi) of each group in the AR / RS send buffer."""
+    if layout == "rowband":
+        band = [rowband_of_group(plan, lo, hi) for lo, hi in plan.ranges]
+        return [(r0 * plan.BM * plan.N, r1 * plan.BM * plan.N) for r0, r1 in band]
     t = plan.BM * plan.BN
     return [(lo * t, hi * t) for lo, hi in plan.ranges]
 
@@ -58,7 +74,7 @@ def ar_pre(Y: np.ndarray, plan: Plan, layout: str = "slot") -> np.ndarray:
     BM, BN = plan.BM, plan.BN
     if layout == "rowband":
         if not ar_rowband_ok(plan):
-            raise OracleError("rowband layout needs a raster order and tile-row group boundaries")
+            raise OracleError("rowband layout needs every group to be a band of complete tile-rows")
         return Y.reshape(-1).copy()
     buf = np.empty(plan.M * plan.N, dtype=Y.dtype)
     for p in range(plan.ntiles):

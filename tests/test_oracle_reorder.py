@@ -61,10 +61,41 @@ def test_ar_rowband_is_identity_layout():
     X = np.arange(48.0).reshape(8, 6)
     assert orr.ar_rowband_ok(pl)
     assert np.array_equal(orr.ar_pre(X, pl, "rowband"), X.reshape(-1))
+    assert orr.group_elem_ranges(pl, "rowband") == [(0, 24), (24, 48)]
     bad = op.make_plan(8, 6, 2, 2, 4, [1, 1, 1], swizzle=1)  # group boundary mid tile-row
     assert not orr.ar_rowband_ok(bad)
     with pytest.raises(op.OracleError):
         orr.ar_pre(X, bad, "rowband")
+    # swizzled order whose groups are whole row-panels: still a row band per group
+    sw = op.make_plan(8, 6, 2, 2, 6, [1, 1], swizzle=2)   # panel of 2 tile-rows = 6 tiles = 1 wave
+    assert orr.ar_rowband_ok(sw)
+    # a group made of two non-adjacent tile-rows is not a band
+    nb = op.make_plan(8, 6, 2, 2, 6, [1, 1], order=[0, 1, 2, 6, 7, 8, 3, 4, 5, 9, 10, 11])
+    assert not orr.ar_rowband_ok(nb)
+
+
+def test_ar_rowband_roundtrip_random_bands():
+    """Rowband AR pipeline == plain definition for random band partitions with
+    random within-band orders and bands in arbitrary order."""
+    from oracle import pipeline as opl
+    rng = np.random.default_rng(9)
+    for _ in range(50):
+        Mt, Nt, BM, BN = int(rng.integers(1, 6)), int(rng.integers(1, 4)), 2, 2
+        S = Nt * int(rng.integers(1, 3))          # wave = whole tile-rows
+        rows_per_wave = S // Nt
+        T = -(-Mt // rows_per_wave)
+        part = synthetic.random_partition(T, int(rng.integers(1 << 20)))
+        # assign bands to groups in a random order of bands
+        band_rows = list(range(Mt))
+        order = []
+        for r in band_rows:
+            order += list(rng.permutation(np.arange(r * Nt, (r + 1) * Nt)))
+        pl = op.make_plan(Mt * BM, Nt * BN, BM, BN, S, part, order=order)
+        assert orr.ar_rowband_ok(pl)
+        As = [rng.integers(-3, 4, size=(Mt * BM, 3)).astype(float) for _ in range(2)]
+        Bts = [rng.integers(-3, 4, size=(Nt * BN, 3)).astype(float) for _ in range(2)]
+        res = opl.run_allreduce(As, Bts, pl, layout="rowband")
+        assert np.array_equal(res["out"][0], opl.plain_allreduce(As, Bts)[0])
 
 
 def test_rs_worked_example_g6():
