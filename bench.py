@@ -289,7 +289,7 @@ def main():
         return means
 
     # ---- offline stage of Alg. 1 (untimed): GEMM duration at S, NCCL AR curve
-    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S)
+    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=0)
     gemm_us, _ = timed(lambda: fo.gemm_stage(gplan, A, Bt, out), 5, 2)
     if world > 1:
         curve = []
@@ -306,7 +306,7 @@ def main():
         groups, pred = fo.tune_search(gemm_us, tiles, S, BM * BN * 2, curve)
 
     plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=list(groups),
-                   ar_layout="auto", rank=rank, world=world)
+                   ar_layout="auto", swizzle=0, rank=rank, world=world)
 
     # ---- full-size spot check (N=1: sampled rows vs an fp64 torch CPU product; not the oracle)
     fo.run(ctx, plan, A, Bt, out)

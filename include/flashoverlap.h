@@ -93,7 +93,8 @@ typedef struct {
   int32_t tile_n;        /* 64, 128 or 256 */
   int32_t workers;       /* S >= 1 = concurrent tile workers = wave width (grid of the persistent GEMM) */
   const int32_t* tile_order; /* [tiles] permutation of tile ids, or NULL => default swizzle */
-  int32_t swizzle;       /* default order: row-panels of `swizzle` tile-rows, column-major inside (R1) */
+  int32_t swizzle;       /* default order: row-panels of `swizzle` tile-rows, column-major inside (R1);
+                            0 = auto: the panel height minimising the tile-rows + tile-columns one wave touches */
   int32_t num_groups;    /* P */
   const int32_t* group_waves; /* [P] wave counts, sum == T = ceil(tiles / S); NULL => one group */
   const int32_t* row_dst;     /* All-to-All: [m] destination rank of each output row */
@@ -240,9 +241,13 @@ int64_t fo_kernel_launch_count(void);
 fo_status fo_tune_predict(const int32_t* groups, int32_t P, double duration_us, int32_t tiles,
                           int32_t S, double tile_bytes, const double* curve_bytes,
                           const double* curve_gbps, int32_t npts, double* predicted_us);
-/* Alg. 1 search over the candidates with |G_1| <= s1 and |G_P| <= sp (prune
- * != 0) or all 2^(T-1) (prune == 0).  Ties: fewer groups, then
- * lexicographically smaller (R16).  out_groups must hold T entries. */
+/* Alg. 1 search.  prune: 0 = enumerate all 2^(T-1)
+ * partitions, 1 = enumerate those with |G_1| <= s1 and |G_P| <= sp
+ * (PAPER.md:446); ties -> fewer groups, then lexicographically smaller
+ * (R16).  2 / 3 = exact argmin of the same predictor by an O(T^2)
+ * dynamic program (R24) without / with the caps; used automatically
+ * (with the caps iff prune == 1) when T > 20, where enumeration is
+ * infeasible.  out_groups must hold T entries. */
 fo_status fo_tune_search(double duration_us, int32_t tiles, int32_t S, double tile_bytes,
                          const double* curve_bytes, const double* curve_gbps, int32_t npts,
                          int32_t s1, int32_t sp, int32_t prune, int32_t* out_groups,

@@ -251,6 +251,8 @@ def tune_predict(groups, duration_us, tiles, S, tile_bytes, curve) -> float:
 
 
 def tune_search(duration_us, tiles, S, tile_bytes, curve, s1=2, sp=4, prune=True):
+    """Alg. 1.  prune: True/1 pruned enumeration, False/0 full enumeration,
+    2/3 exact DP argmin without/with the caps (automatic when T > 20)."""
     T = (tiles + S - 1) // S
     b, bw = _curve(curve)
     groups = np.zeros(max(T, 1), np.int32)
@@ -258,6 +260,6 @@ def tune_search(duration_us, tiles, S, tile_bytes, curve, s1=2, sp=4, prune=True
     pred = C.c_double()
     check(load().fo_tune_search(float(duration_us), int(tiles), int(S), float(tile_bytes),
                                 b.ctypes.data_as(C.POINTER(C.c_double)), bw.ctypes.data_as(C.POINTER(C.c_double)),
-                                int(b.size), int(s1), int(sp), int(bool(prune)), _p32(groups), C.byref(P),
+                                int(b.size), int(s1), int(sp), int(prune), _p32(groups), C.byref(P),
                                 C.byref(pred)))
     return tuple(int(x) for x in groups[:P.value]), pred.value

@@ -18,6 +18,29 @@ std::vector<int32_t> default_order(int Mt, int Nt, int s) {
   return o;
 }
 
+int auto_swizzle(int Mt, int Nt, int S) {
+  int best = 1;
+  long best_fp = -1;
+  for (int s = 1; s <= Mt; ++s) {
+    // one wave = S consecutive positions of the panel order
+    const long panel = (long)s * Nt;
+    long rows, cols;
+    if (S <= panel) {
+      cols = std::min<long>(Nt, (S + s - 1) / s);
+      rows = std::min<long>(s, S);
+    } else {
+      cols = Nt;
+      rows = std::min<long>(Mt, (long)s * ((S + panel - 1) / panel));
+    }
+    const long fp = rows + cols;
+    if (best_fp < 0 || fp < best_fp) {
+      best_fp = fp;
+      best = s;
+    }
+  }
+  return best;
+}
+
 static void check_tile_shape(int BM, int BN) {
   if (BM != 128 && BM != 256) fail(FO_ERR_UNSUPPORTED, "tile_m=%d not compiled (128 or 256)", BM);
   if (BN != 64 && BN != 128 && BN != 256) fail(FO_ERR_UNSUPPORTED, "tile_n=%d not compiled (64/128/256)", BN);
@@ -49,8 +72,9 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
       seen[t] = 1;
     }
   } else {
-    if (d.swizzle < 1) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 1");
-    g.order = default_order(g.Mt, g.Nt, d.swizzle);
+    if (d.swizzle < 0) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 0");
+    const int s = d.swizzle ? d.swizzle : auto_swizzle(g.Mt, g.Nt, d.workers);
+    g.order = default_order(g.Mt, g.Nt, s);
   }
   // T = ceil(tiles / S) (Alg. 1 line 3)
   g.T = (g.tiles + d.workers - 1) / d.workers;
@@ -138,13 +162,30 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
       p.send_elems = p.recv_elems = MN;
       break;
     case FO_ALLREDUCE: {
-      // ROWBAND (H11a) is legal iff the order is the raster and every
-      // group begins on a tile-row boundary: each group is then a row band of C.
-      bool raster = true;
-      for (int q = 0; q < p.tiles; ++q) raster = raster && (p.order[q] == q);
-      bool rows = true;
-      for (int j = 0; j < p.P; ++j) rows = rows && (p.gpos[j] % p.Nt == 0);
-      bool ok = raster && rows;
+      // ROWBAND (H11a) is legal iff every group's tiles are exactly
+      // the complete tile-rows of one contiguous band [r0, r1) (any order inside).
+      bool ok = true;
+      p.band_rows.assign(2 * p.P, 0);
+      for (int j = 0; j < p.P && ok; ++j) {
+        const int lo = p.gpos[j], hi = p.gpos[j + 1];
+        if ((hi - lo) % p.Nt) {
+          ok = false;
+          break;
+        }
+        int rmin = p.Mt, rmax = -1;
+        std::vector<char> seen((size_t)(hi - lo), 0);
+        for (int q = lo; q < hi; ++q) rmin = std::min(rmin, p.order[q] / p.Nt);
+        const int r1 = rmin + (hi - lo) / p.Nt;
+        for (int q = lo; q < hi && ok; ++q) {
+          const int t = p.order[q] - rmin * p.Nt;
+          if (t < 0 || t >= hi - lo || seen[t]) ok = false;
+          else seen[t] = 1;
+          rmax = std::max(rmax, p.order[q] / p.Nt);
+        }
+        ok = ok && rmax < r1;
+        p.band_rows[2 * j] = rmin;
+        p.band_rows[2 * j + 1] = r1;
+      }
       if (d.ar_layout == FO_LAYOUT_ROWBAND && !ok)
         fail(FO_ERR_UNSUPPORTED, "ROWBAND layout needs a raster order and tile-row group boundaries");
       p.layout = (d.ar_layout == FO_LAYOUT_SLOT) ? FO_LAYOUT_SLOT

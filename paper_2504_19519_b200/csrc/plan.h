@@ -48,9 +48,17 @@ struct PlanHost {
   int64_t out_rows = 0;
   int64_t send_elems = 0, recv_elems = 0;
 
-  // Group j's element range in the AR/RS send buffer.
-  int64_t group_elem_begin(int j) const { return (int64_t)gpos[j] * BM * BN; }
-  int64_t group_elem_end(int j) const { return (int64_t)gpos[j + 1] * BM * BN; }
+  std::vector<int64_t> band_rows;       // AR ROWBAND: [2P] tile-row band (r0, r1) of each group
+
+  // Group j's element range in the AR/RS send buffer (AR ROWBAND: its row band of C).
+  int64_t group_elem_begin(int j) const {
+    if (coll == FO_ALLREDUCE && layout == FO_LAYOUT_ROWBAND) return band_rows[2 * j] * BM * N;
+    return (int64_t)gpos[j] * BM * BN;
+  }
+  int64_t group_elem_end(int j) const {
+    if (coll == FO_ALLREDUCE && layout == FO_LAYOUT_ROWBAND) return band_rows[2 * j + 1] * BM * N;
+    return (int64_t)gpos[j + 1] * BM * BN;
+  }
   int group_tiles(int j) const { return gpos[j + 1] - gpos[j]; }
 
   int64_t send_index(int64_t r, int64_t c) const;  // C[r][c] -> send buffer
@@ -59,6 +67,9 @@ struct PlanHost {
 
 // Default order of DESIGN.md R1: row-panels of s tile-rows, column-major inside.
 std::vector<int32_t> default_order(int Mt, int Nt, int s);
+// swizzle == 0: the panel height minimising the tile-rows + tile-columns one
+// wave of S touches (the operand panels that must be L2-resident together).
+int auto_swizzle(int Mt, int Nt, int S);
 
 // Validate + build.  `sm_count` resolves workers == 0 (pass 0 if unknown: then
 // workers must be given explicitly).

@@ -62,6 +62,48 @@ static double predict(const std::vector<int>& G, double duration, int T, int til
   return std::max(acc_p, acc_m) + c.latency_us(size_of((int)G.size() - 1));
 }
 
+// Exact argmin of the Alg. 1 predictor by dynamic programming (our
+// extension for large T, where 2^(T-1) candidates cannot be enumerated).
+// With E(w) the predicted end of the communication of the group that ends at
+// wave w, lines 12-18 of Alg. 1 unroll to
+//   E(w) = max(dur*w'/T, E(w')) + lat(bytes(w', w)),   E(0) = 0  (R13)
+// where w' is the end of the previous group (the max takes the compute end of
+// the group and the end of the previous communication), and lines 20-21 give
+// the prediction E(T).  E is nondecreasing in E(w'), so the minimum over
+// partitions is  E*(w) = min_{w'} max(dur*w'/T, E*(w')) + lat(w', w).
+// Caps: first group <= s1 waves, last group <= sp waves (pruning).
+static std::vector<int> dp_search(double duration, int T, int tiles, int S, double tile_bytes, const Curve& c,
+                                  int s1, int sp, bool prune, double* best_t) {
+  const double inf = std::numeric_limits<double>::infinity();
+  auto bytes = [&](int w0, int w1) {
+    const long lo = (long)S * w0, hi = std::min<long>((long)S * w1, tiles);
+    return (double)(hi - lo) * tile_bytes;
+  };
+  std::vector<double> E(T + 1, inf);
+  std::vector<int> prev(T + 1, -1), ng(T + 1, 0);
+  E[0] = 0.0;
+  for (int w = 1; w <= T; ++w) {
+    for (int w0 = 0; w0 < w; ++w0) {
+      if (E[w0] == inf) continue;
+      if (prune && w0 == 0 && w > s1 && T > 1) continue;
+      if (prune && w == T && (w - w0) > sp && T > 1) continue;
+      const double start = (w0 == 0) ? 0.0 : std::max(duration * w0 / T, E[w0]);
+      // the group's own comm is charged when the next group starts (or at the
+      // end); E(w) below is the end of this group's communication
+      const double e = std::max(duration * w / T, start) + c.latency_us(bytes(w0, w));
+      if (e < E[w] || (e == E[w] && ng[w0] + 1 < ng[w])) {
+        E[w] = e;
+        prev[w] = w0;
+        ng[w] = ng[w0] + 1;
+      }
+    }
+  }
+  std::vector<int> G;
+  for (int w = T; w > 0; w = prev[w]) G.insert(G.begin(), w - prev[w]);
+  *best_t = E[T];
+  return G;
+}
+
 }  // namespace fo
 
 using namespace fo;
@@ -90,8 +132,17 @@ extern "C" fo_status fo_tune_search(double duration_us, int32_t tiles, int32_t S
   return guard([&] {
     if (!out_groups || !out_num_groups || !predicted_us || S < 1 || tiles < 1) fail(FO_ERR_INVALID_ARG, "bad arguments");
     const int T = (tiles + S - 1) / S;
-    if (T > 30) fail(FO_ERR_UNSUPPORTED, "T=%d too large to enumerate", T);
     const Curve c = make_curve(curve_bytes, curve_gbps, npts);
+    if (prune >= 2 || T > 20) {
+      // exact DP argmin (prune 2: all partitions, 3: with the caps; T > 20: caps iff prune == 1)
+      const bool caps = (prune == 3) || (prune == 1);
+      double t = 0;
+      std::vector<int> G = dp_search(duration_us, T, tiles, S, tile_bytes, c, s1, sp, caps, &t);
+      for (size_t i = 0; i < G.size(); ++i) out_groups[i] = G[i];
+      *out_num_groups = (int32_t)G.size();
+      *predicted_us = predict(G, duration_us, T, tiles, S, tile_bytes, c);
+      return;
+    }
     std::vector<int> best;
     double best_t = std::numeric_limits<double>::infinity();
     std::vector<int> G;

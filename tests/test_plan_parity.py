@@ -71,8 +71,15 @@ def _op_plan(c):
 @pytest.mark.parametrize("layout", ["slot", "auto"])
 def test_allreduce_maps(layout):
     rng = np.random.default_rng(10)
-    for _ in range(40):
+    for it in range(60):
         c = _rand_case(rng, "allreduce", 1)
+        if it % 3 == 0:  # waves of whole tile-row panels -> rowband-eligible swizzled orders
+            Nt = c["N"] // c["BN"]
+            c["swz"] = int(rng.integers(1, 4))
+            c["S"] = Nt * c["swz"]
+            c["order"] = None
+            Mt = c["M"] // c["BM"]
+            c["part"] = synthetic.random_partition(op.num_waves(Mt * Nt, c["S"]), it)
         pl = _fo_plan(c, "allreduce", layout=layout)
         o = _op_plan(c)
         assert pl.export_order().tolist() == o.order.tolist()
@@ -84,7 +91,7 @@ def test_allreduce_maps(layout):
         assert np.array_equal(pl.export_send_map(), _oracle_send_map(buf))
         post = orr.ar_post(np.arange(c["M"] * c["N"], dtype=float), o, lay)
         assert np.array_equal(pl.export_recv_map(), post.reshape(-1).astype(np.int64))
-        for j, ((lo, hi), (elo, ehi)) in enumerate(zip(o.ranges, orr.group_elem_ranges(o))):
+        for j, ((lo, hi), (elo, ehi)) in enumerate(zip(o.ranges, orr.group_elem_ranges(o, lay))):
             assert pl.group(j) == (lo, hi, elo, ehi)
         assert pl.info["waves"] == o.T and pl.info["tiles"] == o.ntiles
 
@@ -174,7 +181,7 @@ def test_error_contract():
         fo.Plan(**{**base, "coll": "alltoall", "row_dst": [0] * 255 + [2]}, rank=0, world=2,
                 peers=[{**base, "coll": "alltoall", "row_dst": [0] * 256}] * 2)
     with pytest.raises(fo.FOError, match="UNSUPPORTED"):
-        fo.Plan(**{**base, "ar_layout": "rowband", "swizzle": 2})
+        fo.Plan(**{**base, "ar_layout": "rowband", "swizzle": 2, "group_waves": [1, 1]})
 
 
 def test_tuner_matches_oracle():
@@ -199,3 +206,35 @@ def test_tuner_matches_oracle():
         G = tuple(synthetic.random_partition(T, int(rng.integers(1 << 20))))
         assert fo.tune_predict(G, dur, tiles, S, tile_bytes, curve) == pytest.approx(
             alg1.predict(G, dur, T, sizes_of(G), lat), rel=1e-12)
+
+
+def test_tuner_dp_equals_enumeration():
+    """The O(T^2) DP finds the same optimal predicted latency as enumerating
+    the (pruned / full) candidate space of the oracle's Alg. 1."""
+    rng = np.random.default_rng(6)
+    for _ in range(80):
+        S = int(rng.integers(1, 64))
+        tiles = int(rng.integers(1, 12 * S + 1))
+        T = op.num_waves(tiles, S)
+        if T > 12:
+            continue
+        tile_bytes = float(rng.choice([65536, 131072]))
+        xs = sorted(set(int(2 ** x) for x in rng.uniform(12, 30, size=5)))
+        curve = [(x, float(rng.uniform(1, 700))) for x in xs]
+        dur = float(rng.uniform(5, 500))
+        lat = lambda b: alg1.interp_latency_us(curve, b)
+        sizes_of = lambda G: alg1.group_bytes(G, S, tiles, tile_bytes)
+        for prune_enum, prune_dp in ((False, 2), (True, 3)):
+            _, want_t = alg1.search(T, dur, sizes_of, lat, prune=prune_enum)
+            got, got_t = fo.tune_search(dur, tiles, S, tile_bytes, curve, prune=prune_dp)
+            assert sum(got) == T
+            assert got_t == pytest.approx(want_t, rel=1e-12)
+            assert alg1.predict(got, dur, T, sizes_of(got), lat) == pytest.approx(want_t, rel=1e-12)
+
+
+def test_tuner_large_T_uses_dp():
+    curve = [(2 ** 16, 20.0), (2 ** 22, 300.0), (2 ** 28, 600.0)]
+    got, t = fo.tune_search(5000.0, 2048, 37, 131072.0, curve)   # T = 56
+    assert sum(got) == 56 and got[0] <= 2 and got[-1] <= 4
+    assert t == pytest.approx(fo.tune_predict(got, 5000.0, 2048, 37, 131072.0, curve))
+    assert t <= fo.tune_predict([56], 5000.0, 2048, 37, 131072.0, curve) + 1e-9

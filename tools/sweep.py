@@ -25,7 +25,7 @@ def main():
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     print(f"{'M':>6} {'N=K':>6} {'tiles':>5} {'S':>3} {'T':>3} {'cublas_TF':>9} {'fo_TF':>7} {'frac':>5} "
-          f"{'fo_run_us':>9} {'seq_us':>8} {'speedup':>7}")
+          f"{'fo_run_us':>9} {'seq_us':>8} {'speedup':>7} layout groups")
     for M in (1024, 2048, 4096, 8192, 16384):
         for NK in (4096, 8192, 16384):
             N = K = NK
@@ -37,16 +37,17 @@ def main():
             T_full = -(-tiles // (sms // 2))
             S = -(-tiles // T_full)
             T = -(-tiles // S)
-            gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S)
+            gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0)
             t_fo = timeit(lambda: fo.gemm_stage(gplan, A, Bt, C), iters=10, flush=flush)
             groups = fo.tune_search(t_fo, tiles, S, 256 * 256 * 2, [(1 << 10, 1e6), (1 << 30, 1e6)])[0]
             plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
-                           group_waves=list(groups))
+                           group_waves=list(groups), swizzle=0)
             t_ov = timeit(lambda: fo.run(ctx, plan, A, Bt, C), iters=10, flush=flush)
             t_sq = timeit(lambda: fo.run_sequential(ctx, plan, A, Bt, C), iters=10, flush=flush)
             tf = fl / t_fo / 1e6
             print(f"{M:6d} {NK:6d} {tiles:5d} {S:3d} {T:3d} {fl / t_cb / 1e6:9.1f} {tf:7.1f} {tf / peak:5.2f} "
-                  f"{t_ov:9.1f} {t_sq:8.1f} {t_sq / t_ov:7.3f}", flush=True)
+                  f"{t_ov:9.1f} {t_sq:8.1f} {t_sq / t_ov:7.3f} {'rowband' if plan.info['ar_layout'] == 1 else 'slot':7s} "
+                  f"{list(groups)}", flush=True)
             del A, Bt, C
             torch.cuda.empty_cache()
     ctx.close()
