@@ -223,8 +223,13 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *  FO_OPT_GROUP_POST  -1 auto | 0 off | 1 on — as group_post above
  *  FO_OPT_WAIT_KERNEL  0 — trigger = cuStreamWaitValue32 (front-end wait, no SM)
  *                      1 — trigger = the paper's signaling kernel:
- *                          a 1-warp kernel spinning on an acquire load */
-typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1 } fo_option;
+ *                          a 1-warp kernel spinning on an acquire load
+ *  FO_OPT_TAIL_SPLIT   0 — off; f >= 2 — the R tiles of the last partial wave are
+ *                      split into f K-slices run by otherwise idle workers of that
+ *                      wave (needs R*f <= S); the slice-0 owner adds the fp32
+ *                      partials in its epilogue and signals as usual; -1 — auto
+ *                      (f = min(4, S/R) when 2R <= S).  Set before the first run. */
+typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

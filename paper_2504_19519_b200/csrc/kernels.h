@@ -32,6 +32,12 @@ struct GemmArgs {
   uint32_t* counters;          // [P] device, may be null
   int h;                       // RS subtile rows
   unsigned long long* tile_ts; // optional [tiles] device: %globaltimer at signal
+  // ---- tail split (split-K of the last partial wave across idle workers)
+  int units;                   // work units: tail_pos + (tiles - tail_pos) * split
+  int tail_pos;                // first execution position of the split tail (= tiles: no split)
+  int split;                   // K slices per tail tile (1 = no split)
+  float* workspace;            // fp32 partials [(tiles - tail_pos) * (split - 1)][TM][BN]
+  uint32_t* flags;             // [(tiles - tail_pos) * CG] partial-ready counts (reset with the counters)
 };
 
 enum PostMode : int { POSTMAP_IDENTITY = 0, POSTMAP_SLOT = 1, POSTMAP_RS = 2, POSTMAP_A2A = 3 };

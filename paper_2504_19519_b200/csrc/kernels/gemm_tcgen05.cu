@@ -214,6 +214,37 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Work unit u -> execution position, K-slice and k-block range.  Units below
+// tail_pos are whole tiles (unit = position); the tail's tiles are split into
+// `split` K-slices taken by consecutive units (so by different workers of the
+// last wave).
+struct Unit {
+  int pos, slice, kb0, kb1;
+};
+
+__device__ __forceinline__ Unit decode_unit(const GemmArgs& p, int u, int KB) {
+  Unit r;
+  if (u < p.tail_pos) {
+    r.pos = u;
+    r.slice = 0;
+    r.kb0 = 0;
+    r.kb1 = KB;
+  } else {
+    const int v = u - p.tail_pos;
+    r.pos = p.tail_pos + v / p.split;
+    r.slice = v % p.split;
+    r.kb0 = r.slice * KB / p.split;
+    r.kb1 = (r.slice + 1) * KB / p.split;
+  }
+  return r;
+}
+
 // Destination of row `a` (0..TM-1) of the TM x BN tile at position `pos` = (ti, tj).
 template <int TM, int BN>
 __device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, int ti, int tj, int a) {
@@ -300,12 +331,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int pos = worker; pos < p.tiles; pos += nworkers) {
-        const int t = p.order[pos];
+      for (int u = worker; u < p.units; u += nworkers) {
+        const Unit un = decode_unit(p, u, KB);
+        const int t = p.order[un.pos];
         const int ti = t / p.Nt, tj = t - ti * p.Nt;
         const int arow = ti * TM + (int)crank * BM;
         const int brow = tj * BN + (int)crank * C::B_ROWS;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -333,11 +365,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int pos = worker; pos < p.tiles; pos += nworkers) {
+      for (int u = worker; u < p.units; u += nworkers) {
+        const Unit un = decode_unit(p, u, KB);
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = sw128_desc(smem_u32(sA + stage * A_STAGE_BYTES));
@@ -345,7 +378,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 bytes along K inside the 128-byte swizzle row = +2 in the >>4 address field
-            umma_bf16<CG>(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16<CG>(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit<CG>(&empty[stage]);  // frees the smem stage (in both CTAs) when these MMAs retire
           if (++stage == ST) {
@@ -367,11 +400,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader0 = (CG == 1) ? 0u : mapa_shared(&tempty[0], 0);
     int acc = 0;
     uint32_t aphase = 0;
-    for (int pos = worker; pos < p.tiles; pos += nworkers) {
+    for (int u = worker; u < p.units; u += nworkers) {
+      const Unit un = decode_unit(p, u, KB);
+      const int pos = un.pos;
       const int t = p.order[pos];
       const int ti = t / p.Nt, tj = t - ti * p.Nt;
+      const bool tail = (pos >= p.tail_pos) && p.split > 1;
+      const int tt = pos - p.tail_pos;  // tail tile index
+      const int row = (int)crank * BM + q * 32 + lane;  // this thread's accumulator row in the tile
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
+      if (tail && un.slice == 0) {
+        // owner of a split tile: wait until the other K-slices' partials of
+        // this CTA's rows are published (acquire), then fold them in below
+        if (q == 0 && lane == 0) {
+          const uint32_t* f = p.flags + tt * CG + crank;
+          while (ld_acquire(f) < (uint32_t)(p.split - 1)) __nanosleep(32);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / EPI_COLS; ++c) {
         uint32_t v[64];
@@ -386,6 +433,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) {
             if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
             else mbar_arrive_cluster(tempty_leader0 + 8u * acc);
+          }
+        }
+        if (tail) {
+          if (un.slice > 0) {
+            // K-slice producer: publish fp32 partials of this thread's row
+            float4* w = reinterpret_cast<float4*>(
+                p.workspace + (((int64_t)tt * (p.split - 1) + (un.slice - 1)) * TM + row) * BN + c * EPI_COLS);
+#pragma unroll
+            for (int x = 0; x < 16; ++x)
+              w[x] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                 __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
+            continue;
+          }
+          for (int sl = 1; sl < p.split; ++sl) {
+            const float4* w = reinterpret_cast<const float4*>(
+                p.workspace + (((int64_t)tt * (p.split - 1) + (sl - 1)) * TM + row) * BN + c * EPI_COLS);
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+              const float4 f = w[x];
+              v[4 * x] = __float_as_uint(__uint_as_float(v[4 * x]) + f.x);
+              v[4 * x + 1] = __float_as_uint(__uint_as_float(v[4 * x + 1]) + f.y);
+              v[4 * x + 2] = __float_as_uint(__uint_as_float(v[4 * x + 2]) + f.z);
+              v[4 * x + 3] = __float_as_uint(__uint_as_float(v[4 * x + 3]) + f.w);
+            }
           }
         }
         // stage row `lane` (this thread's TMEM lane) as bf16
@@ -410,6 +481,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           *reinterpret_cast<uint4*>(d) = w;
         }
         __syncwarp();
+      }
+      if (tail && un.slice > 0) {
+        // partials of this CTA's rows stored -> one release increment of the tile's flag
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) red_release_add(p.flags + tt * CG + crank, 1u);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+        continue;
       }
       // all 128 epilogue threads of this CTA finished their stores -> one
       // release add (a pair signals twice per tile: counters count half tiles)

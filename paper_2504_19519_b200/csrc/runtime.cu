@@ -74,7 +74,8 @@ void release_device(fo_plan_s* p) {
   cudaSetDevice(p->device);
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
-                    p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma})
+                    p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma,
+                    (void*)p->d_ws})
     if (ptr) cudaFree(ptr);
   cudaSetDevice(cur);
   p->device = -1;
@@ -105,8 +106,26 @@ static void ensure_device(fo_plan_s* p) {
   p->d_row_slot = upload(h.row_slot);
   p->d_src_row = upload(h.src_row);
   p->d_recv_dst = upload(h.recv_dst);
-  FO_CUDA(cudaMalloc(&p->d_counters, sizeof(uint32_t) * h.P));
-  FO_CUDA(cudaMemset(p->d_counters, 0, sizeof(uint32_t) * h.P));
+  // ---- tail split: the R tiles of the last partial wave split into f K-slices
+  // taken by otherwise idle workers of that wave (R*f <= S, f <= k-blocks)
+  {
+    const int KB = (int)(h.K / 64);
+    const int R = h.tiles - (h.T - 1) * h.S;
+    int f = p->tail_split_req;
+    if (f < 0) f = (R > 0 && 2 * R <= h.S) ? std::min(4, h.S / R) : 1;
+    if (f > 1 && (R * f > h.S || f > KB))
+      fail(FO_ERR_INVALID_ARG, "tail split %d: %d tail tiles x %d slices exceed S=%d or k-blocks=%d", f, R, f, h.S, KB);
+    p->split = (f > 1) ? f : 1;
+    p->tail_pos = (p->split > 1) ? (h.T - 1) * h.S : h.tiles;
+    p->units = p->tail_pos + (h.tiles - p->tail_pos) * p->split;
+    const int cg = h.BM / 128;
+    p->ctr_words = h.P + ((p->split > 1) ? R * cg : 0);
+    if (p->split > 1)
+      FO_CUDA(cudaMalloc(&p->d_ws, sizeof(float) * (size_t)R * (p->split - 1) * h.BM * h.BN));
+  }
+  FO_CUDA(cudaMalloc(&p->d_counters, sizeof(uint32_t) * p->ctr_words));
+  FO_CUDA(cudaMemset(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words));
+  p->d_flags = p->d_counters + h.P;
   const bool need_send = !(h.coll == FO_NOCOMM || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND));
   if (need_send && h.send_elems) FO_CUDA(cudaMalloc(&p->d_send, 2 * h.send_elems));
   if ((h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && h.recv_elems)
@@ -137,6 +156,11 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   a.counters = signal ? p->d_counters : nullptr;
   a.h = h.h;
   a.tile_ts = nullptr;
+  a.units = p->units;
+  a.tail_pos = p->tail_pos;
+  a.split = p->split;
+  a.workspace = p->d_ws;
+  a.flags = p->d_flags;
   return a;
 }
 
@@ -384,7 +408,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     const bool rowband = (h.coll == FO_NOCOMM) || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND);
     void* gemm_dst = rowband ? out : p->d_send;
     // 1. counting table reset (every run starts from zero)
-    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * h.P, s));
+    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
     // 2. fork
     FO_CUDA(cudaEventRecord(c->ev_fork, s));
     FO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
@@ -451,6 +475,7 @@ fo_status fo_run_sequential(fo_ctx c, fo_plan p, const void* A, const void* Bt, 
     ensure_device(p);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int64_t MN = h.M * h.N;
+    if (p->split > 1) FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
     switch (h.coll) {
       case FO_NOCOMM:
       case FO_ALLREDUCE:
@@ -499,7 +524,7 @@ fo_status fo_gemm_stage(fo_plan p, const void* A, const void* Bt, void* send, vo
     if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
     ensure_device(p);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->host.P, s));
+    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
     run_gemm(p, A, Bt, send, epi_mode(p->host), true, s);
   });
 }
@@ -510,7 +535,7 @@ fo_status fo_gemm_stage_timed(fo_plan p, const void* A, const void* Bt, void* se
     if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
     ensure_device(p);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->host.P, s));
+    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
     run_gemm(p, A, Bt, send, epi_mode(p->host), true, s, tile_ts);
   });
 }
@@ -553,6 +578,11 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_GROUP_POST:
         if (value < -1 || value > 1) fail(FO_ERR_INVALID_ARG, "group_post must be -1, 0 or 1");
         p->group_post = (int)value;
+        break;
+      case FO_OPT_TAIL_SPLIT:
+        if (value < -1 || value > 16) fail(FO_ERR_INVALID_ARG, "tail_split must be -1..16");
+        if (p->device >= 0) fail(FO_ERR_STATE, "tail_split must be set before the plan's first run");
+        p->tail_split_req = (int)value;
         break;
       case FO_OPT_WAIT_KERNEL:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "wait_kernel must be 0 or 1");

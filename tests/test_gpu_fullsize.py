@@ -187,3 +187,25 @@ def test_c4_ep8_alltoall(routing):
         sample = _sample(len(src_rows), 16, 7 + d)
         want = np.stack([onum.gemm(As[s][[r]].cpu(), Bts[s].cpu())[0] for s, r in (src_rows[i] for i in sample)])
         _check_rows(out[torch.from_numpy(sample).cuda()], want)
+
+
+def test_c2_bench_config_tp1_tail_split():
+    """configs[1] at TP=1 with all 74 CTA pairs and the last partial wave split
+    along K (the N=1 bench launch configuration)."""
+    M, N, K = 4096, 4096, 14336
+    A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.rank_seed(20000, 1, 0))
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=74, group_waves=[1, 2, 1],
+                   swizzle=0)
+    plan.set_option("tail_split", -1)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, A.cuda(), Bt.cuda(), out)
+    torch.cuda.synchronize()
+    rows = _sample(M, 24, 5)
+    _check_rows(out[torch.from_numpy(rows).cuda()], onum.gemm(A[rows], Bt))
+    # the tail tiles (last wave positions) in particular
+    order = plan.export_order()
+    tail_tiles = order[3 * 74:]
+    trows = np.unique((tail_tiles // 16) * 256 + 17)
+    _check_rows(out[torch.from_numpy(trows).cuda()], onum.gemm(A[trows], Bt))
+    ctx.close()

@@ -283,3 +283,43 @@ def test_tile_timestamps_follow_waves(BM):
     t = ts.cpu().numpy().astype(np.int64)
     waves = t.reshape(-1, S)
     assert (waves[1:].min(axis=1) > waves[:-1].min(axis=1)).all()
+
+
+# ------------------------------------------------------------------ tail split (split-K of the last wave)
+@pytest.mark.parametrize("BM,BN,M,N,K,S,split", [
+    (256, 256, 1024, 1024, 512, 12, -1),    # 16 tiles, T=2, R=4 -> f=3
+    (256, 128, 768, 1024, 256, 10, 2),      # 24 tiles, T=3, R=4 -> f=2
+    (128, 256, 512, 1024, 1024, 14, 4),     # 16 tiles, T=2, R=2 -> f=4
+    (256, 256, 2048, 2048, 2048, 28, -1),   # 64 tiles, T=3, R=8 -> f=3
+])
+def test_tail_split_exact(ctx1, BM, BN, M, N, K, S, split):
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=77, nnz_per_row=256)
+    C = onum.gemm(A, Bt)
+    for coll in ("nocomm", "allreduce"):
+        plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2, ar_layout="slot")
+        plan.set_option("tail_split", split)
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        Ad, Bd = _dev_bf16(A), _dev_bf16(Bt)
+        for _ in range(3):  # flags must reset between runs
+            out.zero_()
+            if coll == "nocomm":
+                fo.gemm_stage(plan, Ad, Bd, out)
+            else:
+                fo.run(ctx1, plan, Ad, Bd, out)
+            torch.cuda.synchronize()
+            assert np.array_equal(_host(out), C)
+        _counters_ok(plan, op.make_plan(M, N, BM, BN, S, None, swizzle=2))
+        for _ in range(2):
+            out.zero_()
+            fo.run_sequential(ctx1, plan, Ad, Bd, out)
+            torch.cuda.synchronize()
+            assert np.array_equal(_host(out), C)
+
+
+def test_tail_split_rejects_oversubscription():
+    plan = fo.Plan(coll="nocomm", m=1024, n=1024, k=128, tile_m=256, tile_n=256, workers=4)  # T=4, R=4
+    plan.set_option("tail_split", 2)   # 4 tail tiles x 2 > S = 4
+    A = torch.zeros(1024, 128, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty(1024, 1024, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(fo.FOError, match="INVALID_ARG"):
+        fo.gemm_stage(plan, A, A[:1024], out)
