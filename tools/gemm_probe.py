@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--s", default="148,144,132")
     ap.add_argument("--bm", default="128,256")
     ap.add_argument("--swizzle", type=int, default=0)
+    ap.add_argument("--split", default="0")
     args = ap.parse_args()
     sms = fo.device_sm_count(0)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -50,13 +51,19 @@ def main():
         for bm in map(int, args.bm.split(",")):
             for bn in map(int, args.bn.split(",")):
                 for S in map(int, args.s.split(",")):
+                  for split in map(int, args.split.split(",")):
                     S = min(S, sms) // (bm // 128)
                     plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=bm, tile_n=bn, workers=S,
                                    swizzle=args.swizzle)
-                    t = timeit(lambda: fo.gemm_stage(plan, A, B, C), flush=flush)
+                    try:
+                        plan.set_option("tail_split", split)
+                        t = timeit(lambda: fo.gemm_stage(plan, A, B, C), flush=flush)
+                    except fo.FOError as e:
+                        print(f"{sh} BM={bm} BN={bn} S={S} split={split}: {e}")
+                        continue
                     err = (C.float() - ref).abs().max().item()
-                    print(f"{sh} fo BM={bm} BN={bn} S={S} {t:8.1f} us {fl / t / 1e6:7.1f} TF  maxdiff {err:.3g}",
-                          flush=True)
+                    print(f"{sh} fo BM={bm} BN={bn} S={S} split={split} {t:8.1f} us {fl / t / 1e6:7.1f} TF  "
+                          f"maxdiff {err:.3g}", flush=True)
 
 
 if __name__ == "__main__":
