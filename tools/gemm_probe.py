@@ -51,18 +51,18 @@ def main():
         for bm in map(int, args.bm.split(",")):
             for bn in map(int, args.bn.split(",")):
                 for S in map(int, args.s.split(",")):
+                  Sw = min(S, sms) // (bm // 128)
                   for split in map(int, args.split.split(",")):
-                    S = min(S, sms) // (bm // 128)
-                    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=bm, tile_n=bn, workers=S,
+                    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=bm, tile_n=bn, workers=Sw,
                                    swizzle=args.swizzle)
                     try:
                         plan.set_option("tail_split", split)
                         t = timeit(lambda: fo.gemm_stage(plan, A, B, C), flush=flush)
                     except fo.FOError as e:
-                        print(f"{sh} BM={bm} BN={bn} S={S} split={split}: {e}")
+                        print(f"{sh} BM={bm} BN={bn} S={Sw} split={split}: {e}")
                         continue
                     err = (C.float() - ref).abs().max().item()
-                    print(f"{sh} fo BM={bm} BN={bn} S={S} split={split} {t:8.1f} us {fl / t / 1e6:7.1f} TF  "
+                    print(f"{sh} fo BM={bm} BN={bn} S={Sw} split={split} {t:8.1f} us {fl / t / 1e6:7.1f} TF  "
                           f"maxdiff {err:.3g}", flush=True)
 
 
