@@ -190,6 +190,17 @@ fo_status fo_run_host(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, v
 fo_status fo_run_sequential(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
                             const void* residual, const void* gamma, void* stream);
 
+/* RS follow-on (NEXT f2): AllGather of every rank's local RS
+ * output `local` [m/world, n] (block-cyclic rows R_k, device bf16) into
+ * `out` [m, n].  row_exchange != 0: the rank-major gather is permuted back to
+ * the standard row order by a kernel that also applies the plan's elementwise
+ * op (residual / gamma as in fo_run, now [m, n] / [n]); row_exchange == 0:
+ * gathered rows stay rank-major ("if the row order has no impact on
+ * subsequent processing, the exchange step can be safely eliminated").
+ * Collective; `plan` must be the ReduceScatter plan that produced `local`. */
+fo_status fo_run_allgather(fo_ctx ctx, fo_plan plan, const void* local, void* out, const void* residual,
+                           const void* gamma, int32_t row_exchange, void* stream);
+
 /* ---------------------------------------------------------------- stages (tests, single GPU, no NCCL) */
 /* Run only the GEMM with this plan's pre-reorder epilogue into a caller
  * device buffer `send` of info.send_elems bf16 (the counting table is bumped
@@ -205,6 +216,10 @@ fo_status fo_gemm_stage_timed(fo_plan plan, const void* A, const void* Bt, void*
  * receive buffer of info.recv_elems bf16. */
 fo_status fo_post_stage(fo_plan plan, const void* recv, void* out, const void* residual,
                         const void* gamma, void* stream);
+/* The row exchange alone, from a caller-provided rank-major gathered buffer
+ * [m, n] (what ncclAllGather of the ranks' RS outputs delivers). */
+fo_status fo_rowexchange_stage(fo_plan plan, const void* gathered, void* out, const void* residual,
+                               const void* gamma, void* stream);
 /* Copy the plan's P counters to host (synchronises the device). */
 fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
 /* Debug / evidence hooks (tests, tools; never needed for correct use):

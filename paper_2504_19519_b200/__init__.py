@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib
 from ._lib import COLL, LAYOUT, POST, FOError, check, load
 
-__all__ = ["Plan", "Context", "run", "run_host", "run_sequential", "gemm_stage", "gemm_stage_timed", "post_stage",
+__all__ = ["Plan", "Context", "run", "run_host", "run_allgather", "rowexchange_stage", "run_sequential", "gemm_stage", "gemm_stage_timed", "post_stage",
            "unique_id", "tune_search", "tune_predict", "kernel_launch_count", "FOError", "load",
            "device_sm_count"]
 
@@ -205,6 +205,17 @@ def run_host(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, st
     """fo_run_host: A, Bt, out (and residual, gamma) are CPU tensors (pin them for async copies)."""
     check(load().fo_run_host(ctx._h, plan.handle, _ptr(A), _ptr(Bt), _ptr(out), _ptr(residual), _ptr(gamma),
                              _stream(stream)))
+
+
+def run_allgather(ctx: Context, plan: Plan, local, out, residual=None, gamma=None, row_exchange=True, stream=None):
+    """RS follow-on: AllGather of the RS outputs (+ row exchange fused with the elementwise op)."""
+    check(load().fo_run_allgather(ctx._h, plan.handle, _ptr(local), _ptr(out), _ptr(residual), _ptr(gamma),
+                                  int(bool(row_exchange)), _stream(stream)))
+
+
+def rowexchange_stage(plan: Plan, gathered, out, residual=None, gamma=None, stream=None):
+    check(load().fo_rowexchange_stage(plan.handle, _ptr(gathered), _ptr(out), _ptr(residual), _ptr(gamma),
+                                      _stream(stream)))
 
 
 def run_sequential(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=None):

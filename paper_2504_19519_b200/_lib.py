@@ -75,6 +75,8 @@ _SIGS = [
     ("fo_run", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_sequential", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_host", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    ("fo_run_allgather", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_int32, _P]),
+    ("fo_rowexchange_stage", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("fo_gemm_stage", C.c_int, [_P, _P, _P, _P, _P]),
     ("fo_gemm_stage_timed", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("fo_post_stage", C.c_int, [_P, _P, _P, _P, _P, _P]),

@@ -40,7 +40,13 @@ struct GemmArgs {
   uint32_t* flags;             // [(tiles - tail_pos) * CG] partial-ready counts (reset with the counters)
 };
 
-enum PostMode : int { POSTMAP_IDENTITY = 0, POSTMAP_SLOT = 1, POSTMAP_RS = 2, POSTMAP_A2A = 3 };
+enum PostMode : int {
+  POSTMAP_IDENTITY = 0,
+  POSTMAP_SLOT = 1,
+  POSTMAP_RS = 2,
+  POSTMAP_A2A = 3,
+  POSTMAP_ROWX = 4  // RS follow-on: rank-major AllGather of block-cyclic rows -> standard row order
+};
 
 struct PostArgs {
   int map;                 // PostMode

@@ -36,6 +36,14 @@ __device__ __forceinline__ RowSrc row_src(const PostArgs& p, int64_t r) {
     s.tbl = nullptr;
     s.tscale = 0;
     s.roff = r * p.N;
+  } else if (MAP == POSTMAP_ROWX) {
+    // PAPER.md:390 row exchange: global row r = (l/h)*BM + k*h + l%h came from
+    // rank k's local row l, i.e. row k*(M/n) + l of the rank-major gather
+    const int64_t n = p.BM / p.h, rows_per_rank = p.rows / n;
+    const int64_t k = (r % p.BM) / p.h, l = (r / p.BM) * p.h + r % p.h;
+    s.tbl = nullptr;
+    s.tscale = 0;
+    s.roff = (k * rows_per_rank + l) * p.N;
   } else if (MAP == POSTMAP_SLOT) {  // slot of tile (r/BM, jc), row r%BM
     s.tbl = p.pos_of_tile + (r / p.BM) * p.Nt;
     s.tscale = (int64_t)p.BM * p.BN;
@@ -54,7 +62,7 @@ __device__ __forceinline__ RowSrc row_src(const PostArgs& p, int64_t r) {
 
 template <int MAP>
 __device__ __forceinline__ int64_t chunk_src(const RowSrc& s, int64_t col, int lbn, int bn_mask) {
-  if (MAP == POSTMAP_IDENTITY) return s.roff + col;
+  if (MAP == POSTMAP_IDENTITY || MAP == POSTMAP_ROWX) return s.roff + col;
   return (int64_t)__ldg(s.tbl + (col >> lbn)) * s.tscale + s.roff + (col & bn_mask);
 }
 
@@ -419,6 +427,7 @@ cudaError_t launch_post(const PostArgs& a, cudaStream_t stream) {
     case POSTMAP_SLOT: e = launch_map<POSTMAP_SLOT>(a, lbn, stream); break;
     case POSTMAP_RS: e = launch_map<POSTMAP_RS>(a, lbn, stream); break;
     case POSTMAP_A2A: e = launch_map<POSTMAP_A2A>(a, lbn, stream); break;
+    case POSTMAP_ROWX: e = launch_map<POSTMAP_ROWX>(a, lbn, stream); break;
     default: e = launch_map<POSTMAP_IDENTITY>(a, lbn, stream); break;
   }
   count_launch();

@@ -519,6 +519,79 @@ fo_status fo_run_sequential(fo_ctx c, fo_plan p, const void* A, const void* Bt, 
   });
 }
 
+// ---- RS follow-on (NEXT f2): AllGather of the block-cyclic
+// local outputs, then the row exchange (fused with the plan's elementwise op)
+static void run_rowexchange(fo_plan_s* p, const void* gathered, void* out, const void* residual, const void* gamma,
+                            cudaStream_t s) {
+  const PlanHost& h = p->host;
+  PostArgs a{};
+  a.map = POSTMAP_ROWX;
+  a.op = h.post;
+  a.src = gathered;
+  a.out = out;
+  a.residual = residual;
+  a.gamma = gamma;
+  a.rows = h.M;
+  a.N = h.N;
+  a.BM = h.BM;
+  a.BN = h.BN;
+  a.Nt = h.Nt;
+  a.h = h.h;
+  a.eps = h.eps;
+  if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
+  if (h.post == FO_POST_ADD_RMSNORM && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
+  FO_CUDA(launch_post(a, s));
+}
+
+fo_status fo_rowexchange_stage(fo_plan p, const void* gathered, void* out, const void* residual, const void* gamma,
+                               void* stream) {
+  return guard([&] {
+    if (!p || !gathered || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (p->host.coll != FO_REDUCESCATTER) fail(FO_ERR_INVALID_ARG, "row exchange follows a ReduceScatter plan");
+    ensure_device(p);
+    run_rowexchange(p, gathered, out, residual, gamma, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+fo_status fo_run_allgather(fo_ctx c, fo_plan p, const void* local, void* out, const void* residual,
+                           const void* gamma, int32_t row_exchange, void* stream) {
+  return guard([&] {
+    if (!c || !p || !local || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    const PlanHost& h = p->host;
+    if (h.coll != FO_REDUCESCATTER) fail(FO_ERR_INVALID_ARG, "AllGather follow-on needs a ReduceScatter plan");
+    if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
+    ensure_device(p);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t local_elems = (size_t)(h.out_rows * h.N);
+    if (!row_exchange) {
+      // row order not needed downstream: gather straight into out
+      FO_NCCL(ncclAllGather(local, out, local_elems, bf16(), c->comm, s));
+      if (h.post != FO_POST_NONE) {
+        PostArgs a{};
+        a.map = POSTMAP_IDENTITY;
+        a.op = h.post;
+        a.src = out;
+        a.out = out;
+        a.residual = residual;
+        a.gamma = gamma;
+        a.rows = h.M;
+        a.N = h.N;
+        a.BM = h.BM;
+        a.BN = h.BN;
+        a.Nt = h.Nt;
+        a.h = h.h;
+        a.eps = h.eps;
+        if (!residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
+        FO_CUDA(launch_post(a, s));
+      }
+      return;
+    }
+    if (!p->d_rowmajor) FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * (size_t)(h.M * h.N)));
+    FO_NCCL(ncclAllGather(local, p->d_rowmajor, local_elems, bf16(), c->comm, s));
+    run_rowexchange(p, p->d_rowmajor, out, residual, gamma, s);
+  });
+}
+
 fo_status fo_gemm_stage(fo_plan p, const void* A, const void* Bt, void* send, void* stream) {
   return guard([&] {
     if (!p) fail(FO_ERR_INVALID_ARG, "null plan");

@@ -323,3 +323,47 @@ def test_tail_split_rejects_oversubscription():
     out = torch.empty(1024, 1024, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(fo.FOError, match="INVALID_ARG"):
         fo.gemm_stage(plan, A, A[:1024], out)
+
+
+# ------------------------------------------------------------------ RS follow-on: AllGather + row exchange (f2)
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("post", ["none", "add_rmsnorm"])
+def test_rs_allgather_rowexchange(n, post):
+    """RS -> (elementwise) -> AllGather -> row exchange == AllReduce
+    (PAPER.md:390); the rank-major gather is emulated, the row exchange (fused
+    with the elementwise op) runs on the GPU."""
+    M, N, K, BN, S, BM = 1024, 512, 128, 128, 5, 256
+    tiles = (M // BM) * (N // BN)
+    groups = _groups(tiles, S, 31 + n)
+    As, Bts = _rank_inputs(n, M, N, K, 500)
+    oplan = op.make_plan(M, N, BM, BN, S, groups, swizzle=2)
+    rs = opl.run_reducescatter(As, Bts, oplan)
+    gathered = np.concatenate(rs["out"], axis=0)          # rank-major AllGather
+    plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2,
+                   group_waves=groups, rank=0, world=n, post=post)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    res = synthetic.normal_bf16((M, N), 1.0, 8)
+    gam = synthetic.normal_bf16((N,), 1.0, 9)
+    extra = (_dev_bf16(res), _dev_bf16(gam)) if post != "none" else (None, None)
+    fo.rowexchange_stage(plan, _dev_bf16(gathered), out, *extra)
+    torch.cuda.synchronize()
+    C = opl.plain_allreduce(As, Bts)[0]
+    assert np.array_equal(opl.row_exchange(gathered, BM, n), C)
+    if post == "none":
+        assert np.array_equal(_host(out), C)
+    else:
+        want = opost.add_rmsnorm(C, onum.to_f64(res), onum.to_f64(gam), 1e-5)
+        assert _rel_err(_host(out), want) <= TOL
+
+
+def test_run_allgather_world1(ctx1):
+    M, N, K = 512, 512, 128
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=3, nnz_per_row=100)
+    plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=3, swizzle=2)
+    local = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx1, plan, _dev_bf16(A), _dev_bf16(Bt), local)
+    full = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    for rx in (True, False):
+        fo.run_allgather(ctx1, plan, local, full, row_exchange=rx)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(full), onum.gemm(A, Bt))
