@@ -273,6 +273,19 @@ fo_status fo_tune_search(double duration_us, int32_t tiles, int32_t S, double ti
                          int32_t s1, int32_t sp, int32_t prune, int32_t* out_groups,
                          int32_t* out_num_groups, double* predicted_us);
 
+/* A2A imbalance extension of Alg. 1 (NEXT f3; R26):
+ * `ranks` GPUs share one partition of T waves; durations[r] is rank r's GEMM
+ * duration, wave_bytes[r*T + w] the A2A bytes rank r sends in wave w.  The
+ * accumulated latencies are maxed across GPUs after every step. */
+fo_status fo_tune_predict_multi(const int32_t* groups, int32_t P, int32_t ranks, int32_t T,
+                                const double* durations, const double* wave_bytes,
+                                const double* curve_bytes, const double* curve_gbps, int32_t npts,
+                                double* predicted_us);
+fo_status fo_tune_search_multi(int32_t ranks, int32_t T, const double* durations, const double* wave_bytes,
+                               const double* curve_bytes, const double* curve_gbps, int32_t npts,
+                               int32_t s1, int32_t sp, int32_t prune, int32_t* out_groups,
+                               int32_t* out_num_groups, double* predicted_us);
+
 #ifdef __cplusplus
 }
 #endif

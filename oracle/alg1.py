@@ -115,3 +115,47 @@ def perfect_overlap_bound(duration_us: float, T: int, comm_full_us: float, comm_
     if duration_us >= comm_full_us:
         return duration_us + comm_last_wave_us
     return duration_us / T + comm_full_us
+
+
+# ------------------------------------------------------------------ A2A imbalance extension
+def predict_multi(partition, durations, wave_bytes, comm_latency) -> float:
+    """"the prediction algorithm is extended by taking the maximum
+    across all GPUs for the accumulated latencies (t_p^acc and t_m^acc)".
+
+    Reading R26: every rank r runs the same wave partition over T
+    waves (experts padded to a common tile count), with its own GEMM duration
+    durations[r] and its own A2A bytes per wave wave_bytes[r][w].  Alg. 1's
+    loop runs per rank from the shared (maxed) accumulators, and after every
+    step each accumulator is the maximum over the ranks."""
+    R = len(durations)
+    T = len(wave_bytes[0])
+    bounds, W = [], 0
+    for g in partition:
+        bounds.append((W, W + g))
+        W += g
+    if W != T:
+        raise ValueError("partition does not cover the T waves")
+
+    def t_m(r, i):  # comm latency of group i on rank r
+        lo, hi = bounds[i]
+        return comm_latency(sum(wave_bytes[r][lo:hi]))
+
+    t_acc_p = [0.0] * R
+    t_acc_m = 0.0
+    for i, g in enumerate(partition):
+        p_max = max(t_acc_p)
+        t_acc_m = max(max(p_max, t_acc_m) + (t_m(r, i - 1) if i > 0 else 0.0) for r in range(R))
+        t_acc_p = [t_acc_p[r] + durations[r] / T * g for r in range(R)]
+    p_max = max(t_acc_p)
+    return max(max(p_max, t_acc_m) + t_m(r, len(partition) - 1) for r in range(R))
+
+
+def search_multi(T, durations, wave_bytes, comm_latency, S1=2, SP=4, prune=True):
+    """Argmin of predict_multi over the (pruned) candidates; tie-break R16."""
+    cands = pruned_candidates(T, S1, SP) if prune else candidates(T)
+    best, best_t = None, math.inf
+    for G in cands:
+        t = predict_multi(G, durations, wave_bytes, comm_latency)
+        if best is None or (t, len(G), G) < (best_t, len(best), best):
+            best, best_t = G, t
+    return best, best_t

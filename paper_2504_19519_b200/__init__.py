@@ -274,3 +274,37 @@ def tune_search(duration_us, tiles, S, tile_bytes, curve, s1=2, sp=4, prune=True
                                 int(b.size), int(s1), int(sp), int(prune), _p32(groups), C.byref(P),
                                 C.byref(pred)))
     return tuple(int(x) for x in groups[:P.value]), pred.value
+
+
+def _d(a):
+    a = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))
+    return a, a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def tune_predict_multi(groups, durations, wave_bytes, curve) -> float:
+    """A2A imbalance extension: wave_bytes is [ranks][T]."""
+    g = _i32(groups)
+    wb = np.asarray(wave_bytes, np.float64)
+    dur, pd = _d(durations)
+    wbf, pw = _d(wb)
+    b, bw = _curve(curve)
+    out = C.c_double()
+    check(load().fo_tune_predict_multi(_p32(g), int(g.size), int(wb.shape[0]), int(wb.shape[1]), pd, pw,
+                                       b.ctypes.data_as(C.POINTER(C.c_double)),
+                                       bw.ctypes.data_as(C.POINTER(C.c_double)), int(b.size), C.byref(out)))
+    return out.value
+
+
+def tune_search_multi(durations, wave_bytes, curve, s1=2, sp=4, prune=True):
+    wb = np.asarray(wave_bytes, np.float64)
+    T = int(wb.shape[1])
+    dur, pd = _d(durations)
+    wbf, pw = _d(wb)
+    b, bw = _curve(curve)
+    groups = np.zeros(T, np.int32)
+    P = C.c_int32()
+    pred = C.c_double()
+    check(load().fo_tune_search_multi(int(wb.shape[0]), T, pd, pw, b.ctypes.data_as(C.POINTER(C.c_double)),
+                                      bw.ctypes.data_as(C.POINTER(C.c_double)), int(b.size), int(s1), int(sp),
+                                      int(prune), _p32(groups), C.byref(P), C.byref(pred)))
+    return tuple(int(x) for x in groups[:P.value]), pred.value

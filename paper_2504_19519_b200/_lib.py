@@ -90,6 +90,13 @@ _SIGS = [
     ("fo_tune_search", C.c_int, [C.c_double, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_double),
                                  C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                  C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+    ("fo_tune_predict_multi", C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32,
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double)]),
+    ("fo_tune_search_multi", C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32, C.c_int32,
+                                       C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_double)]),
 ]
 SYMBOLS = [s[0] for s in _SIGS]
 

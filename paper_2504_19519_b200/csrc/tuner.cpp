@@ -6,6 +6,8 @@
 // R15 bandwidth is linear in log2(bytes) between samples, clamped; R16 ties go
 // to fewer groups, then the lexicographically smaller partition.
 #include <cmath>
+#include <functional>
+#include <memory>
 #include <limits>
 #include <vector>
 
@@ -104,9 +106,132 @@ static std::vector<int> dp_search(double duration, int T, int tiles, int S, doub
   return G;
 }
 
+// ---- generic form: group latency lat(w0, w1) of the group covering waves [w0, w1)
+using GroupLat = std::function<double(int, int)>;
+
+static double predict_g(const std::vector<int>& G, double duration, int T, const GroupLat& lat) {
+  double acc_p = 0.0, acc_m = 0.0;
+  int W = 0, Wprev = 0;
+  for (size_t i = 0; i < G.size(); ++i) {
+    const double t_m = i ? lat(Wprev, W) : 0.0;
+    acc_m = std::max(acc_p, acc_m) + t_m;
+    acc_p += duration / T * G[i];
+    Wprev = W;
+    W += G[i];
+  }
+  return std::max(acc_p, acc_m) + lat(Wprev, W);
+}
+
+static std::vector<int> dp_g(double duration, int T, const GroupLat& lat, int s1, int sp, bool caps, double* best) {
+  const double inf = std::numeric_limits<double>::infinity();
+  std::vector<double> E(T + 1, inf);
+  std::vector<int> prev(T + 1, -1), ng(T + 1, 0);
+  E[0] = 0.0;
+  for (int w = 1; w <= T; ++w)
+    for (int w0 = 0; w0 < w; ++w0) {
+      if (E[w0] == inf) continue;
+      if (caps && T > 1 && ((w0 == 0 && w > s1) || (w == T && w - w0 > sp))) continue;
+      const double e = std::max(duration * w / T, E[w0]) + lat(w0, w);
+      if (e < E[w] || (e == E[w] && ng[w0] + 1 < ng[w])) {
+        E[w] = e;
+        prev[w] = w0;
+        ng[w] = ng[w0] + 1;
+      }
+    }
+  std::vector<int> G;
+  for (int w = T; w > 0; w = prev[w]) G.insert(G.begin(), w - prev[w]);
+  *best = E[T];
+  return G;
+}
+
+static std::vector<int> enum_g(double duration, int T, const GroupLat& lat, int s1, int sp, bool prune, double* best_t) {
+  std::vector<int> best, G;
+  *best_t = std::numeric_limits<double>::infinity();
+  for (uint32_t mask = 0; mask < (1u << (T - 1)); ++mask) {
+    G.clear();
+    int run = 0;
+    for (int w = 0; w < T; ++w) {
+      ++run;
+      if (w == T - 1 || ((mask >> w) & 1u)) {
+        G.push_back(run);
+        run = 0;
+      }
+    }
+    if (prune && T > 1 && (G.front() > s1 || G.back() > sp)) continue;
+    const double t = predict_g(G, duration, T, lat);
+    if (best.empty() || t < *best_t || (t == *best_t && (G.size() < best.size() || (G.size() == best.size() && G < best)))) {
+      best = G;
+      *best_t = t;
+    }
+  }
+  return best;
+}
+
+// A2A imbalance extension (R26): all ranks share the
+// wave partition; the accumulated compute is the maximum over ranks (=
+// max duration) and a group's communication lasts as long as the slowest
+// rank's message: lat(w0, w1) = max_r latency(sum of rank r's bytes of waves [w0, w1)).
+static GroupLat multi_lat(int ranks, int T, const double* wave_bytes, const Curve* c) {
+  auto prefix = std::make_shared<std::vector<double>>((size_t)ranks * (T + 1), 0.0);
+  for (int r = 0; r < ranks; ++r)
+    for (int w = 0; w < T; ++w)
+      (*prefix)[(size_t)r * (T + 1) + w + 1] = (*prefix)[(size_t)r * (T + 1) + w] + wave_bytes[(size_t)r * T + w];
+  return [prefix, ranks, T, c](int w0, int w1) {
+    double m = 0.0;
+    for (int r = 0; r < ranks; ++r) {
+      const double b = (*prefix)[(size_t)r * (T + 1) + w1] - (*prefix)[(size_t)r * (T + 1) + w0];
+      m = std::max(m, c->latency_us(b));
+    }
+    return m;
+  };
+}
+
 }  // namespace fo
 
 using namespace fo;
+
+extern "C" fo_status fo_tune_predict_multi(const int32_t* groups, int32_t P, int32_t ranks, int32_t T,
+                                           const double* durations, const double* wave_bytes,
+                                           const double* curve_bytes, const double* curve_gbps, int32_t npts,
+                                           double* predicted_us) {
+  return guard([&] {
+    if (!groups || P < 1 || ranks < 1 || T < 1 || !durations || !wave_bytes || !predicted_us)
+      fail(FO_ERR_INVALID_ARG, "bad arguments");
+    std::vector<int> G(groups, groups + P);
+    long sum = 0;
+    for (int g : G) {
+      if (g < 1) fail(FO_ERR_INVALID_ARG, "zero-size group");
+      sum += g;
+    }
+    if (sum != T) fail(FO_ERR_INVALID_ARG, "groups sum to %ld, T=%d", sum, T);
+    const Curve c = make_curve(curve_bytes, curve_gbps, npts);
+    double dmax = 0.0;
+    for (int r = 0; r < ranks; ++r) dmax = std::max(dmax, durations[r]);
+    *predicted_us = predict_g(G, dmax, T, multi_lat(ranks, T, wave_bytes, &c));
+  });
+}
+
+extern "C" fo_status fo_tune_search_multi(int32_t ranks, int32_t T, const double* durations, const double* wave_bytes,
+                                          const double* curve_bytes, const double* curve_gbps, int32_t npts,
+                                          int32_t s1, int32_t sp, int32_t prune, int32_t* out_groups,
+                                          int32_t* out_num_groups, double* predicted_us) {
+  return guard([&] {
+    if (ranks < 1 || T < 1 || !durations || !wave_bytes || !out_groups || !out_num_groups || !predicted_us)
+      fail(FO_ERR_INVALID_ARG, "bad arguments");
+    const Curve c = make_curve(curve_bytes, curve_gbps, npts);
+    double dmax = 0.0;
+    for (int r = 0; r < ranks; ++r) dmax = std::max(dmax, durations[r]);
+    const GroupLat lat = multi_lat(ranks, T, wave_bytes, &c);
+    double t = 0.0;
+    std::vector<int> G = (prune >= 2 || T > 20)
+                             ? dp_g(dmax, T, lat, s1, sp, prune == 1 || prune == 3, &t)
+                             : enum_g(dmax, T, lat, s1, sp, prune != 0, &t);
+    if (G.empty()) fail(FO_ERR_INVALID_ARG, "pruning left no candidate");
+    for (size_t i = 0; i < G.size(); ++i) out_groups[i] = G[i];
+    *out_num_groups = (int32_t)G.size();
+    *predicted_us = predict_g(G, dmax, T, lat);
+  });
+}
 
 extern "C" fo_status fo_tune_predict(const int32_t* groups, int32_t P, double duration_us, int32_t tiles,
                                      int32_t S, double tile_bytes, const double* curve_bytes,

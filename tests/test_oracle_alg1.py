@@ -91,3 +91,29 @@ def test_search_tie_break_and_knee():
     lat = lambda b: alg1.interp_latency_us(curve, b)
     best, _ = alg1.search(8, 400.0, lambda G: alg1.group_bytes(G, 64, 512, 65536), lat)
     assert best != (1,) * 8
+
+
+def test_multi_balanced_equals_scalar():
+    """balanced A2A routing -> the per-GPU-max prediction equals
+    the scalar prediction."""
+    curve = [(2 ** 12, 5.0), (2 ** 20, 100.0), (2 ** 26, 400.0)]
+    lat = lambda b: alg1.interp_latency_us(curve, b)
+    for T in range(1, 7):
+        wb = [3 * 2 ** 19] * T
+        for G in alg1.candidates(T):
+            single = alg1.predict(G, 120.0, T, [sum(wb[:g]) for g in G], lat)
+            multi = alg1.predict_multi(G, [120.0] * 4, [wb] * 4, lat)
+            assert multi == pytest.approx(single)
+
+
+def test_multi_hand_trace_and_monotone():
+    # two ranks, T = 2, partition (1, 1); linear comm 1 us per byte unit
+    lat = lambda b: float(b)
+    # rank 0: dur 10, bytes per wave (4, 4); rank 1: dur 20, bytes (1, 9)
+    # i=1: t_acc_m = 0; t_acc_p = (5, 10)
+    # i=2: p_max = 10; t_acc_m = max(10, 0) + max(4, 1) = 14; t_acc_p = (10, 20)
+    # end: max(20, 14) + max(4, 9) = 29
+    assert alg1.predict_multi((1, 1), [10.0, 20.0], [[4, 4], [1, 9]], lat) == pytest.approx(29.0)
+    # a slower rank never lowers the prediction
+    base = alg1.predict_multi((1, 1), [10.0, 10.0], [[4, 4], [4, 4]], lat)
+    assert alg1.predict_multi((1, 1), [10.0, 30.0], [[4, 4], [4, 4]], lat) >= base

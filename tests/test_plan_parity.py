@@ -238,3 +238,29 @@ def test_tuner_large_T_uses_dp():
     assert sum(got) == 56 and got[0] <= 2 and got[-1] <= 4
     assert t == pytest.approx(fo.tune_predict(got, 5000.0, 2048, 37, 131072.0, curve))
     assert t <= fo.tune_predict([56], 5000.0, 2048, 37, 131072.0, curve) + 1e-9
+
+
+def test_tuner_multi_matches_oracle():
+    """A2A imbalance extension vs the oracle's predict_multi /
+    search_multi; DP (prune 2/3) attains the enumeration's optimum."""
+    rng = np.random.default_rng(12)
+    for _ in range(40):
+        R, T = int(rng.integers(1, 5)), int(rng.integers(1, 10))
+        durs = rng.uniform(10, 300, size=R)
+        wb = rng.uniform(1e5, 3e7, size=(R, T))
+        xs = sorted(set(int(2 ** x) for x in rng.uniform(14, 28, size=5)))
+        curve = [(x, float(rng.uniform(5, 600))) for x in xs]
+        lat = lambda b: alg1.interp_latency_us(curve, b)
+        G = tuple(synthetic.random_partition(T, int(rng.integers(1 << 20))))
+        assert fo.tune_predict_multi(G, durs, wb, curve) == pytest.approx(
+            alg1.predict_multi(G, list(durs), wb.tolist(), lat), rel=1e-12)
+        for prune, dp in ((True, 3), (False, 2)):
+            want, want_t = alg1.search_multi(T, list(durs), wb.tolist(), lat, prune=prune)
+            got, got_t = fo.tune_search_multi(durs, wb, curve, prune=prune)
+            # exact ties in the model (e.g. compute-bound: only the last group
+            # matters) may be broken differently by rounding; the optimum value
+            # and the chosen partition's oracle prediction must agree
+            assert got_t == pytest.approx(want_t, rel=1e-12)
+            assert alg1.predict_multi(got, list(durs), wb.tolist(), lat) == pytest.approx(want_t, rel=1e-12)
+            _, dp_t = fo.tune_search_multi(durs, wb, curve, prune=dp)
+            assert dp_t == pytest.approx(want_t, rel=1e-12)
