@@ -1,0 +1,183 @@
+"""Offline tuner driver (Alg. 1) and the pre-searched plan
+cache with nearest-neighbour reuse for unseen sizes (NEXT f1).
+
+Offline stage:
+  (1) computation - the GEMM duration of our persistent kernel at wave width S
+      (measured with CUDA events, L2 flushed), T = ceil(tiles / S);
+  (2) communication - the (bytes, GB/s) curve of the collective, sampled at
+      log-spaced sizes on the process group's NCCL (world 1: no exchange);
+  (3) resource contention - S = SMs left after `comm_sms` (Alg. 1 line 3).
+Online stage: fo_tune_search (C++, enumeration or the exact DP, R24).
+
+The cache is a JSON file keyed "MxNxK/coll/g<world>"; a miss reuses the
+nearest cached shape when its distance |dlog2 M| + |dlog2 N| + |dlog2 K| is at
+most 1.5 (SPEC.md:339 idea), else tunes and stores.
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+from dataclasses import asdict, dataclass, field
+from typing import Callable, Optional
+
+from . import Plan, device_sm_count, gemm_stage, tune_search
+
+TILE_M, TILE_N = 256, 256
+
+
+@dataclass
+class TunedPlan:
+    M: int
+    N: int
+    K: int
+    coll: str
+    world: int
+    tile_m: int
+    tile_n: int
+    workers: int
+    swizzle: int
+    groups: list
+    predicted_us: float
+    gemm_us: float
+    curve: list = field(default_factory=list)
+    source: str = "tuned"  # "tuned" | "neighbour:<key>"
+
+    def spec(self) -> dict:
+        return dict(coll=self.coll, m=self.M, n=self.N, k=self.K, tile_m=self.tile_m, tile_n=self.tile_n,
+                    workers=self.workers, swizzle=self.swizzle, group_waves=list(self.groups))
+
+
+def key_of(M, N, K, coll, world) -> str:
+    return f"{M}x{N}x{K}/{coll}/g{world}"
+
+
+def default_workers(tiles: int, sms: int, cg: int = 2) -> int:
+    """Fewest workers with the wave count of the full GPU (the freed SMs are left to NCCL)."""
+    t_full = -(-tiles // max(1, sms // cg))
+    return -(-tiles // t_full)
+
+
+def measure_gemm_us(M, N, K, workers, swizzle=0, tile_m=TILE_M, tile_n=TILE_N, iters=10) -> float:
+    """Offline stage (1): our GEMM's duration at wave width S (CUDA events, L2 flushed)."""
+    import torch
+
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    Bt = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    plan = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=workers, swizzle=swizzle)
+    for _ in range(3):
+        gemm_stage(plan, A, Bt, C)
+    tot = 0.0
+    for _ in range(iters):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        gemm_stage(plan, A, Bt, C)
+        e.record()
+        torch.cuda.synchronize()
+        tot += s.elapsed_time(e) * 1e3
+    return tot / iters
+
+
+def sample_curve(coll: str, group=None, sizes=None, iters=5) -> list:
+    """Offline stage (2): NCCL bandwidth vs message size on the process group
+    (torch.distributed's NCCL, the same library the hot path calls).  World 1
+    has no exchange: a flat, very high curve."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return [(1 << 10, 1e6), (1 << 30, 1e6)]
+    n = dist.get_world_size(group)
+    sizes = sizes or [1 << s for s in range(16, 28)]
+    out = []
+    for sz in sizes:
+        x = torch.empty(sz // 2, dtype=torch.bfloat16, device="cuda")
+        y = torch.empty(sz // 2 // n, dtype=torch.bfloat16, device="cuda")
+
+        def op():
+            if coll == "reducescatter":
+                dist.reduce_scatter_tensor(y, x, group=group)
+            else:
+                dist.all_reduce(x, group=group)
+
+        for _ in range(2):
+            op()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            op()
+        e.record()
+        torch.cuda.synchronize()
+        t_us = s.elapsed_time(e) * 1e3 / iters
+        out.append((sz, sz / (t_us * 1e-6) / 1e9))
+    return out
+
+
+def tune(M, N, K, coll="allreduce", world=1, comm_sms=None, group=None, swizzle=0, device=0) -> TunedPlan:
+    """Run the offline + online stages of Alg. 1 for one layer shape."""
+    sms = device_sm_count(device)
+    tiles = (M // TILE_M) * (N // TILE_N)
+    S = default_workers(tiles, sms) if comm_sms is None else (sms - comm_sms) // 2
+    dur = measure_gemm_us(M, N, K, S, swizzle)
+    curve = sample_curve(coll, group)
+    groups, pred = tune_search(dur, tiles, S, TILE_M * TILE_N * 2, curve)
+    return TunedPlan(M, N, K, coll, world, TILE_M, TILE_N, S, swizzle, list(groups), pred, dur, curve)
+
+
+def distance(a, b) -> float:
+    return sum(abs(math.log2(x) - math.log2(y)) for x, y in zip(a, b))
+
+
+class PlanCache:
+    """Pre-searched plans for representative sizes + nearest-neighbour reuse
+    ("pre-search for representative GEMM sizes, and apply
+    nearest-neighbor matching for unseen cases during execution")."""
+
+    def __init__(self, path: Optional[str] = None, threshold: float = 1.5):
+        self.path, self.threshold = path, threshold
+        self.entries: dict = {}
+        if path and os.path.exists(path):
+            with open(path) as f:
+                self.entries = json.load(f)
+
+    def save(self):
+        if self.path:
+            with open(self.path, "w") as f:
+                json.dump(self.entries, f, indent=1, sort_keys=True)
+
+    def put(self, tp: TunedPlan):
+        self.entries[key_of(tp.M, tp.N, tp.K, tp.coll, tp.world)] = asdict(tp)
+
+    def nearest(self, M, N, K, coll, world):
+        best, best_d = None, math.inf
+        for k, e in self.entries.items():
+            if e["coll"] != coll or e["world"] != world:
+                continue
+            d = distance((M, N, K), (e["M"], e["N"], e["K"]))
+            if d < best_d or (d == best_d and best is not None and k < best[0]):
+                best, best_d = (k, e), d
+        return best, best_d
+
+    def lookup_or_tune(self, M, N, K, coll="allreduce", world=1,
+                       tuner: Callable[..., TunedPlan] = tune, **kw) -> TunedPlan:
+        k = key_of(M, N, K, coll, world)
+        if k in self.entries:
+            return TunedPlan(**self.entries[k])
+        near, d = self.nearest(M, N, K, coll, world)
+        if near is not None and d <= self.threshold:
+            e = dict(near[1])
+            tp = TunedPlan(**e)
+            # reuse the neighbour's choices (workers, swizzle, groups) if they fit this shape
+            tiles = (M // tp.tile_m) * (N // tp.tile_n)
+            T = -(-tiles // tp.workers)
+            if sum(tp.groups) == T:
+                return TunedPlan(M, N, K, coll, world, tp.tile_m, tp.tile_n, tp.workers, tp.swizzle, tp.groups,
+                                 tp.predicted_us, tp.gemm_us, tp.curve, f"neighbour:{near[0]}")
+        tp = tuner(M, N, K, coll=coll, world=world, **kw)
+        self.put(tp)
+        self.save()
+        return tp

@@ -1,0 +1,58 @@
+"""Plan cache with nearest-neighbour reuse (SPEC.md:339-341
+examples) — host logic, CPU only (the tuner itself is injected)."""
+import pytest
+
+from paper_2504_19519_b200 import tuner
+
+
+def fake_tuner(calls):
+    def t(M, N, K, coll="allreduce", world=1, **kw):
+        calls.append((M, N, K))
+        tiles = (M // 256) * (N // 256)
+        S = tuner.default_workers(tiles, 148)
+        T = -(-tiles // S)
+        groups = [1] * (T - 1) + [1] if T > 1 else [1]
+        return tuner.TunedPlan(M, N, K, coll, world, 256, 256, S, 0, groups, 1.0, 1.0, [], "tuned")
+    return t
+
+
+def test_empty_cache_tunes_and_stores(tmp_path):
+    calls = []
+    c = tuner.PlanCache(str(tmp_path / "plans.json"))
+    tp = c.lookup_or_tune(4096, 4096, 1792, tuner=fake_tuner(calls))
+    assert tp.source == "tuned" and calls == [(4096, 4096, 1792)]
+    c2 = tuner.PlanCache(str(tmp_path / "plans.json"))   # persisted
+    assert tuner.key_of(4096, 4096, 1792, "allreduce", 1) in c2.entries
+
+
+def test_exact_hit(tmp_path):
+    calls = []
+    c = tuner.PlanCache(str(tmp_path / "p.json"))
+    c.lookup_or_tune(4096, 4096, 1792, tuner=fake_tuner(calls))
+    tp = c.lookup_or_tune(4096, 4096, 1792, tuner=fake_tuner(calls))
+    assert len(calls) == 1 and tp.source == "tuned"
+
+
+def test_neighbour_within_threshold_reused():
+    calls = []
+    c = tuner.PlanCache(None)
+    c.lookup_or_tune(4096, 4096, 1792, tuner=fake_tuner(calls))
+    # (4096, 4096, 3584): distance 1 -> reuse (same tile grid, same T)
+    tp = c.lookup_or_tune(4096, 4096, 3584, tuner=fake_tuner(calls))
+    assert len(calls) == 1 and tp.source.startswith("neighbour:")
+    # far away (distance 4): tune
+    c.lookup_or_tune(16384, 16384, 7168, tuner=fake_tuner(calls))
+    assert len(calls) == 2
+
+
+def test_neighbour_with_incompatible_waves_is_retuned():
+    calls = []
+    c = tuner.PlanCache(None)
+    c.lookup_or_tune(4096, 4096, 1792, tuner=fake_tuner(calls))
+    # M doubled (distance 1) -> twice the tiles, different T -> cannot reuse the partition
+    tp = c.lookup_or_tune(8192, 4096, 1792, tuner=fake_tuner(calls))
+    assert len(calls) == 2 and tp.source == "tuned"
+
+
+def test_distance():
+    assert tuner.distance((4096, 4096, 4096), (8192, 4096, 2048)) == pytest.approx(2.0)
