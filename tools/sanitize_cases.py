@@ -1,0 +1,66 @@
+"""Small runs of every device path for compute-sanitizer (memcheck / racecheck
+/ synccheck): GEMM (CTA and CTA-pair, tail split), every epilogue mode,
+fo_run at world 1 for AR/RS/A2A (+ fused RMSNorm), per-group post, row
+exchange.  Dev tool; exits non-zero on a numerical mismatch."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2504_19519_b200 as fo  # noqa: E402
+import synthetic  # noqa: E402
+
+
+def main():
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    M, N, K = 512, 512, 256
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=1, nnz_per_row=100)
+    Ad, Bd = A.cuda(), Bt.cuda()
+    C = (A.double() @ Bt.double().t()).to(torch.bfloat16).cuda()
+    res = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    gam = torch.ones(N, dtype=torch.bfloat16, device="cuda")
+    bad = 0
+    for BM in (128, 256):
+        for coll in ("nocomm", "allreduce", "reducescatter", "alltoall"):
+            for post in ("none", "add"):
+                kw = dict(coll=coll, m=M, n=N, k=K, tile_m=BM, tile_n=128, workers=3, swizzle=2,
+                          ar_layout="slot", post=post)
+                if coll == "alltoall":
+                    kw["row_dst"] = np.zeros(M, np.int32)
+                    plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
+                else:
+                    plan = fo.Plan(**kw)
+                out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+                fo.run(ctx, plan, Ad, Bd, out, res if post != "none" else None)
+                torch.cuda.synchronize()
+                if not torch.equal(out, C):
+                    print("mismatch", BM, coll, post)
+                    bad += 1
+    # tail split
+    plan = fo.Plan(coll="nocomm", m=1024, n=1024, k=256, tile_m=256, tile_n=256, workers=12, swizzle=2)
+    plan.set_option("tail_split", -1)
+    A2, B2 = synthetic.exact_inputs(1024, 1024, 256, seed=2, nnz_per_row=100)
+    out = torch.empty(1024, 1024, dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, A2.cuda(), B2.cuda(), out)
+    torch.cuda.synchronize()
+    if not torch.equal(out.cpu(), (A2.double() @ B2.double().t()).to(torch.bfloat16)):
+        print("mismatch tail split")
+        bad += 1
+    # fused RMSNorm + row exchange
+    plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=3, post="add_rmsnorm")
+    local = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, Ad, Bd, local, res, gam)
+    full = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run_allgather(ctx, plan, local, full, res, gam)
+    torch.cuda.synchronize()
+    ctx.close()
+    print("sanitize cases done, mismatches:", bad)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
