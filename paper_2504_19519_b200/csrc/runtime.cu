@@ -26,7 +26,9 @@ struct fo_ctx_s {
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t post_stream = nullptr;  // per-group post-reorder, chained to each group's collective
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_post_join = nullptr;
+  std::vector<cudaEvent_t> ev_group;   // one per wave group (grown on demand)
 };
 
 namespace fo {
@@ -371,8 +373,10 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
       FO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       // highest priority for the communication stream
       FO_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+      FO_CUDA(cudaStreamCreateWithPriority(&c->post_stream, cudaStreamNonBlocking, hi));
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+      FO_CUDA(cudaEventCreateWithFlags(&c->ev_post_join, cudaEventDisableTiming));
     } catch (...) {
       if (c->comm) ncclCommDestroy(c->comm);
       delete c;
@@ -388,9 +392,13 @@ fo_status fo_ctx_destroy(fo_ctx c) {
     cudaSetDevice(c->device);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->post_stream) cudaStreamSynchronize(c->post_stream);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->post_stream) cudaStreamDestroy(c->post_stream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_post_join) cudaEventDestroy(c->ev_post_join);
+    for (cudaEvent_t e : c->ev_group) cudaEventDestroy(e);
     delete c;
   });
 }
@@ -416,14 +424,27 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     run_gemm(p, A, Bt, gemm_dst, epi_mode(h), true, s, p->trace_tile_ts);
     const bool gpost = use_group_post(p);
     const void* post_src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : p->d_recv);
-    // 4. per-group wait + collective (+ per-group post-reorder)
+    // 4. per-group wait + collective; the per-group post-reorder runs on the
+    //    post stream, chained to its group's collective by an event, so the
+    //    next group's collective never queues behind a reorder
+    while ((int)c->ev_group.size() < h.P) {
+      cudaEvent_t e;
+      FO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->ev_group.push_back(e);
+    }
     if (h.coll != FO_NOCOMM) {
       for (int j = 0; j < h.P; ++j) {
         stream_wait(p, wait, c->comm_stream, j);
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j, c->comm_stream));
         group_collective(c, p, j, gemm_dst);
-        if (gpost) run_group_post(p, j, post_src, out, residual, c->comm_stream);
-        if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j + 1, c->comm_stream));
+        cudaStream_t ps = c->comm_stream;
+        if (gpost) {
+          FO_CUDA(cudaEventRecord(c->ev_group[j], c->comm_stream));
+          FO_CUDA(cudaStreamWaitEvent(c->post_stream, c->ev_group[j], 0));
+          ps = c->post_stream;
+          run_group_post(p, j, post_src, out, residual, ps);
+        }
+        if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j + 1, ps));
       }
     } else {
       // no communication: the comm stream only has to see the GEMM finish
@@ -438,6 +459,10 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     // 6. join
     FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
     FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+    if (gpost && h.coll != FO_NOCOMM) {
+      FO_CUDA(cudaEventRecord(c->ev_post_join, c->post_stream));
+      FO_CUDA(cudaStreamWaitEvent(s, c->ev_post_join, 0));
+    }
   });
 }
 
