@@ -291,14 +291,9 @@ def main():
     # ---- offline stage of Alg. 1 (untimed): GEMM duration at S, NCCL AR curve
     gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=0)
     gemm_us, _ = timed(lambda: fo.gemm_stage(gplan, A, Bt, out), 5, 2)
-    if world > 1:
-        curve = []
-        for sz in [1 << s for s in range(18, 27)]:
-            buf = torch.empty(sz // 2, dtype=torch.bfloat16, device="cuda")
-            t, _ = timed(lambda: dist.all_reduce(buf), 5, 2)
-            curve.append((sz, sz / (t * 1e-6) / 1e9))
-    else:
-        curve = [(1 << 10, 1e6), (1 << 30, 1e6)]  # 1 rank: the collective moves no bytes
+    # NCCL curve on the library's own communicator (CTA cap included); at one
+    # rank this is the fixed per-call cost of the degenerate collective
+    curve = ctx.sample_curve("allreduce", [1 << s for s in range(18, 27)], iters=5)
     if args.groups:
         groups = tuple(int(x) for x in args.groups.split(","))
         pred = fo.tune_predict(groups, gemm_us, tiles, S, BM * BN * 2, curve)

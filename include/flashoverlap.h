@@ -159,6 +159,13 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
                         int32_t nccl_max_ctas, fo_ctx* out);
 fo_status fo_ctx_destroy(fo_ctx ctx);
 
+/* Offline stage of the tuner ("the bandwidth curve is sampled
+ * with multiple dense points"): average latency of one `coll` (AllReduce in
+ * place, ReduceScatter, or equal-split All-to-All) of `bytes` total message
+ * bytes on the context's own communicator and comm stream (its CTA cap
+ * included).  Collective; synchronises the host (tuning only). */
+fo_status fo_ctx_time_collective(fo_ctx ctx, int32_t coll, int64_t bytes, int32_t iters, double* avg_us);
+
 /* ---------------------------------------------------------------- the overlapped op */
 /* Overlapped GEMM + collective (+ post-reorder, + fused elementwise), stream
  * ordered on `stream` and host-asynchronous.  Collective: every rank calls it

@@ -179,6 +179,17 @@ class Context:
         check(load().fo_ctx_create(device, rank, world, buf, nccl_max_ctas, C.byref(h)))
         return cls(h, device, rank, world)
 
+    def time_collective(self, coll: str, nbytes: int, iters: int = 5) -> float:
+        """Average us of one collective of `nbytes` on this context's communicator (tuning)."""
+        out = C.c_double()
+        check(load().fo_ctx_time_collective(self._h, COLL[coll], int(nbytes), int(iters), C.byref(out)))
+        return out.value
+
+    def sample_curve(self, coll: str, sizes=None, iters: int = 5):
+        """(bytes, GB/s) samples of `coll` on this communicator (Alg. 1 line 5)."""
+        sizes = sizes or [1 << s for s in range(16, 28)]
+        return [(sz, sz / (self.time_collective(coll, sz, iters) * 1e-6) / 1e9) for sz in sizes]
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             check(load().fo_ctx_destroy(self._h))

@@ -72,6 +72,7 @@ _SIGS = [
     ("fo_ctx_create", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32,
                                 C.POINTER(_P)]),
     ("fo_ctx_destroy", C.c_int, [_P]),
+    ("fo_ctx_time_collective", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double)]),
     ("fo_run", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_sequential", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_host", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),

@@ -658,6 +658,58 @@ fo_status fo_plan_read_counters(fo_plan p, uint32_t* counters) {
 
 int64_t fo_kernel_launch_count(void) { return launch_count(); }
 
+fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t iters, double* avg_us) {
+  return guard([&] {
+    if (!c || !avg_us || bytes <= 0 || iters < 1) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    FO_CUDA(cudaSetDevice(c->device));
+    const int W = c->world;
+    const size_t count = (size_t)(bytes / 2 / W) * W;  // bf16 elements, divisible by world
+    if (count == 0) fail(FO_ERR_INVALID_ARG, "message too small");
+    void *a = nullptr, *b = nullptr;
+    FO_CUDA(cudaMalloc(&a, 2 * count));
+    FO_CUDA(cudaMalloc(&b, 2 * count));
+    FO_CUDA(cudaMemset(a, 0, 2 * count));
+    cudaStream_t cs = c->comm_stream;
+    auto once = [&] {
+      switch (coll) {
+        case FO_ALLREDUCE:
+          FO_NCCL(ncclAllReduce(a, a, count, bf16(), ncclSum, c->comm, cs));
+          break;
+        case FO_REDUCESCATTER:
+          FO_NCCL(ncclReduceScatter(a, b, count / W, bf16(), ncclSum, c->comm, cs));
+          break;
+        case FO_ALLTOALL: {
+          const size_t per = count / W;
+          FO_NCCL(ncclGroupStart());
+          for (int d = 0; d < W; ++d) {
+            FO_NCCL(ncclSend(reinterpret_cast<char*>(a) + 2 * per * d, per, bf16(), d, c->comm, cs));
+            FO_NCCL(ncclRecv(reinterpret_cast<char*>(b) + 2 * per * d, per, bf16(), d, c->comm, cs));
+          }
+          FO_NCCL(ncclGroupEnd());
+          break;
+        }
+        default:
+          fail(FO_ERR_INVALID_ARG, "unknown collective %d", coll);
+      }
+    };
+    cudaEvent_t e0, e1;
+    FO_CUDA(cudaEventCreate(&e0));
+    FO_CUDA(cudaEventCreate(&e1));
+    for (int i = 0; i < 2; ++i) once();
+    FO_CUDA(cudaEventRecord(e0, cs));
+    for (int i = 0; i < iters; ++i) once();
+    FO_CUDA(cudaEventRecord(e1, cs));
+    FO_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FO_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *avg_us = 1e3 * ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(a);
+    cudaFree(b);
+  });
+}
+
 fo_status fo_plan_set_debug(fo_plan p, unsigned long long* tile_ts, unsigned long long* group_ts,
                             int32_t group_post) {
   return guard([&] {

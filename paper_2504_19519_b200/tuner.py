@@ -81,13 +81,16 @@ def measure_gemm_us(M, N, K, workers, swizzle=0, tile_m=TILE_M, tile_n=TILE_N, i
     return tot / iters
 
 
-def sample_curve(coll: str, group=None, sizes=None, iters=5) -> list:
-    """Offline stage (2): NCCL bandwidth vs message size on the process group
-    (torch.distributed's NCCL, the same library the hot path calls).  World 1
-    has no exchange: a flat, very high curve."""
+def sample_curve(coll: str, group=None, sizes=None, iters=5, ctx=None) -> list:
+    """Offline stage (2): NCCL bandwidth vs message size.  With `ctx`, on the
+    library's own communicator and comm stream (its CTA cap included — what the
+    hot path will see); else on the torch.distributed group.  World 1 without a
+    context has no exchange: a flat, very high curve."""
     import torch
     import torch.distributed as dist
 
+    if ctx is not None:
+        return ctx.sample_curve(coll, sizes, iters)
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return [(1 << 10, 1e6), (1 << 30, 1e6)]
     n = dist.get_world_size(group)
@@ -117,13 +120,13 @@ def sample_curve(coll: str, group=None, sizes=None, iters=5) -> list:
     return out
 
 
-def tune(M, N, K, coll="allreduce", world=1, comm_sms=None, group=None, swizzle=0, device=0) -> TunedPlan:
+def tune(M, N, K, coll="allreduce", world=1, comm_sms=None, group=None, swizzle=0, device=0, ctx=None) -> TunedPlan:
     """Run the offline + online stages of Alg. 1 for one layer shape."""
     sms = device_sm_count(device)
     tiles = (M // TILE_M) * (N // TILE_N)
     S = default_workers(tiles, sms) if comm_sms is None else (sms - comm_sms) // 2
     dur = measure_gemm_us(M, N, K, S, swizzle)
-    curve = sample_curve(coll, group)
+    curve = sample_curve(coll, group, ctx=ctx)
     groups, pred = tune_search(dur, tiles, S, TILE_M * TILE_N * 2, curve)
     return TunedPlan(M, N, K, coll, world, TILE_M, TILE_N, S, swizzle, list(groups), pred, dur, curve)
 

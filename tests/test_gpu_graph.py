@@ -82,3 +82,17 @@ def test_run_host_matches_device_run():
     torch.cuda.synchronize()
     assert torch.equal(out_h, out_d.cpu())
     ctx.close()
+
+
+def test_time_collective_world1():
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    for coll in ("allreduce", "reducescatter", "alltoall"):
+        us = ctx.time_collective(coll, 1 << 20, iters=3)
+        assert 0.0 < us < 1e4
+    curve = ctx.sample_curve("allreduce", [1 << 16, 1 << 20], iters=2)
+    assert len(curve) == 2 and all(b > 0 for _, b in curve)
+    ctx.close()
