@@ -302,6 +302,8 @@ def main():
 
     plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=list(groups),
                    ar_layout="auto", swizzle=0, rank=rank, world=world)
+    # the GEMM-only timing uses exactly the overlapped plan's execution order
+    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=plan.export_order())
 
     # ---- full-size spot check (N=1: sampled rows vs an fp64 torch CPU product; not the oracle)
     fo.run(ctx, plan, A, Bt, out)

@@ -18,27 +18,52 @@ std::vector<int32_t> default_order(int Mt, int Nt, int s) {
   return o;
 }
 
+static long wave_footprint(int Mt, int Nt, int S, int s) {
+  // tile-rows + tile-columns touched by one wave of S consecutive positions
+  const long panel = (long)s * Nt;
+  long rows, cols;
+  if (S <= panel) {
+    cols = std::min<long>(Nt, (S + s - 1) / s);
+    rows = std::min<long>(s, S);
+  } else {
+    cols = Nt;
+    rows = std::min<long>(Mt, (long)s * ((S + panel - 1) / panel));
+  }
+  return rows + cols;
+}
+
 int auto_swizzle(int Mt, int Nt, int S) {
   int best = 1;
   long best_fp = -1;
   for (int s = 1; s <= Mt; ++s) {
-    // one wave = S consecutive positions of the panel order
-    const long panel = (long)s * Nt;
-    long rows, cols;
-    if (S <= panel) {
-      cols = std::min<long>(Nt, (S + s - 1) / s);
-      rows = std::min<long>(s, S);
-    } else {
-      cols = Nt;
-      rows = std::min<long>(Mt, (long)s * ((S + panel - 1) / panel));
-    }
-    const long fp = rows + cols;
+    const long fp = wave_footprint(Mt, Nt, S, s);
     if (best_fp < 0 || fp < best_fp) {
       best_fp = fp;
       best = s;
     }
   }
   return best;
+}
+
+// AllReduce: prefer panel heights whose panels end exactly on the group
+// boundaries (every group is then a band of whole tile-rows -> ROWBAND layout,
+// no reorder at all) unless the unconstrained footprint is much smaller.
+static int auto_swizzle_ar(int Mt, int Nt, int S, const std::vector<int32_t>& gpos) {
+  const int any = auto_swizzle(Mt, Nt, S);
+  int band = -1;
+  long band_fp = -1;
+  for (int s = 1; s <= Mt; ++s) {
+    bool ok = true;
+    for (size_t j = 1; j + 1 < gpos.size() && ok; ++j) ok = (gpos[j] % ((long)s * Nt) == 0);
+    if (!ok) continue;
+    const long fp = wave_footprint(Mt, Nt, S, s);
+    if (band < 0 || fp < band_fp) {
+      band = s;
+      band_fp = fp;
+    }
+  }
+  if (band > 0 && 4 * band_fp <= 5 * wave_footprint(Mt, Nt, S, any)) return band;
+  return any;
 }
 
 static void check_tile_shape(int BM, int BN) {
@@ -64,18 +89,6 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
   g.Mt = (int)(d.m / d.tile_m);
   g.Nt = (int)(d.n / d.tile_n);
   g.tiles = g.Mt * g.Nt;
-  if (d.tile_order) {
-    g.order.assign(d.tile_order, d.tile_order + g.tiles);
-    std::vector<char> seen(g.tiles, 0);
-    for (int32_t t : g.order) {
-      if (t < 0 || t >= g.tiles || seen[t]) fail(FO_ERR_INVALID_ARG, "tile_order is not a permutation");
-      seen[t] = 1;
-    }
-  } else {
-    if (d.swizzle < 0) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 0");
-    const int s = d.swizzle ? d.swizzle : auto_swizzle(g.Mt, g.Nt, d.workers);
-    g.order = default_order(g.Mt, g.Nt, s);
-  }
   // T = ceil(tiles / S) (Alg. 1 line 3)
   g.T = (g.tiles + d.workers - 1) / d.workers;
   if (d.group_waves && d.num_groups > 0) {
@@ -96,6 +109,21 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
   for (int j = 0; j < g.P; ++j) {
     W += g.waves[j];
     g.gpos[j + 1] = (int32_t)std::min<long>((long)d.workers * W, g.tiles);
+  }
+  if (d.tile_order) {
+    g.order.assign(d.tile_order, d.tile_order + g.tiles);
+    std::vector<char> seen(g.tiles, 0);
+    for (int32_t t : g.order) {
+      if (t < 0 || t >= g.tiles || seen[t]) fail(FO_ERR_INVALID_ARG, "tile_order is not a permutation");
+      seen[t] = 1;
+    }
+  } else {
+    if (d.swizzle < 0) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 0");
+    int s = d.swizzle;
+    if (s == 0)
+      s = (d.coll == FO_ALLREDUCE && d.ar_layout != FO_LAYOUT_SLOT) ? auto_swizzle_ar(g.Mt, g.Nt, d.workers, g.gpos)
+                                                                     : auto_swizzle(g.Mt, g.Nt, d.workers);
+    g.order = default_order(g.Mt, g.Nt, s);
   }
   (void)world;
   return g;
