@@ -373,7 +373,9 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
       FO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       // highest priority for the communication stream
       FO_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
-      FO_CUDA(cudaStreamCreateWithPriority(&c->post_stream, cudaStreamNonBlocking, hi));
+      // post-reorder one step below the collectives (pending NCCL CTAs are
+      // scheduled first), still above default-priority work
+      FO_CUDA(cudaStreamCreateWithPriority(&c->post_stream, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_post_join, cudaEventDisableTiming));
