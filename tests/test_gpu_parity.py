@@ -367,3 +367,55 @@ def test_run_allgather_world1(ctx1):
         fo.run_allgather(ctx1, plan, local, full, row_exchange=rx)
         torch.cuda.synchronize()
         assert np.array_equal(_host(full), onum.gemm(A, Bt))
+
+
+# ------------------------------------------------------------------ tag runs
+def _tag_inputs(M, N, code_rows):
+    """K=64 GEMM with one nonzero k-column: C[r, c] = code[r] (code_rows) or code[c]."""
+    K = 64
+    A = torch.zeros(M, K)
+    Bt = torch.zeros(N, K)
+    if code_rows is not None:
+        A[:, 0] = torch.as_tensor(code_rows, dtype=torch.float32)
+        Bt[:, 0] = 1.0
+    return A.to(torch.bfloat16), Bt.to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("coll,n", [("allreduce", 1), ("reducescatter", 4), ("alltoall", 3)])
+def test_tag_runs_decode_every_element(coll, n):
+    """Four K=64 GEMMs whose outputs are (row mod 256, row div 256, col mod 256,
+    col div 256) - all integers <= 255, exact in bf16 - decode the source
+    coordinate of every send-buffer element through the real epilogue; it must
+    equal the plan's (oracle-verified) send map."""
+    M, N, BM, BN, S = 1024, 768, 256, 128, 5
+    tiles = (M // BM) * (N // BN)
+    groups = _groups(tiles, S, 3)
+    kw = dict(coll=coll, m=M, n=N, k=64, tile_m=BM, tile_n=BN, workers=S, swizzle=2, group_waves=groups,
+              ar_layout="slot")
+    if coll == "alltoall":
+        kw["row_dst"] = synthetic.random_row_dst(M, n, 5)
+        plan = fo.Plan(rank=0, world=n, peers=[kw] * n, **kw)
+    else:
+        plan = fo.Plan(rank=0, world=n, **kw)
+    send_elems = plan.info["send_elems"]
+    rows = np.arange(M)
+    cols = np.arange(N)
+    codes = []
+    for vec, on_rows in ((rows % 256, True), (rows // 256, True), (cols % 256, False), (cols // 256, False)):
+        if on_rows:
+            A, Bt = _tag_inputs(M, N, vec)
+        else:
+            A, Bt = _tag_inputs(N, M, vec)      # C^T trick: swap roles, then transpose the operands
+            A, Bt = torch.zeros(M, 64, dtype=torch.bfloat16), torch.zeros(N, 64, dtype=torch.bfloat16)
+            A[:, 0] = 1.0
+            Bt[:, 0] = torch.as_tensor(vec, dtype=torch.bfloat16)
+        send = torch.empty(send_elems, dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, A.cuda(), Bt.cuda(), send)
+        torch.cuda.synchronize()
+        codes.append(send.float().cpu().numpy().astype(np.int64))
+    r = codes[0] + 256 * codes[1]
+    c = codes[2] + 256 * codes[3]
+    decoded = r * N + c                          # flat source index of every send element
+    want = np.empty(send_elems, np.int64)
+    want[plan.export_send_map()] = np.arange(M * N)
+    assert np.array_equal(decoded, want)
