@@ -370,14 +370,16 @@ def test_run_allgather_world1(ctx1):
 
 
 # ------------------------------------------------------------------ tag runs
-def _tag_inputs(M, N, code_rows):
-    """K=64 GEMM with one nonzero k-column: C[r, c] = code[r] (code_rows) or code[c]."""
-    K = 64
-    A = torch.zeros(M, K)
-    Bt = torch.zeros(N, K)
-    if code_rows is not None:
-        A[:, 0] = torch.as_tensor(code_rows, dtype=torch.float32)
+def _tag_inputs(M, N, code, on_rows):
+    """K=64 GEMM with one nonzero k-column: C[r, c] = code[r] (on_rows) or code[c]."""
+    A = torch.zeros(M, 64)
+    Bt = torch.zeros(N, 64)
+    if on_rows:
+        A[:, 0] = torch.as_tensor(code, dtype=torch.float32)
         Bt[:, 0] = 1.0
+    else:
+        A[:, 0] = 1.0
+        Bt[:, 0] = torch.as_tensor(code, dtype=torch.float32)
     return A.to(torch.bfloat16), Bt.to(torch.bfloat16)
 
 
@@ -402,13 +404,7 @@ def test_tag_runs_decode_every_element(coll, n):
     cols = np.arange(N)
     codes = []
     for vec, on_rows in ((rows % 256, True), (rows // 256, True), (cols % 256, False), (cols // 256, False)):
-        if on_rows:
-            A, Bt = _tag_inputs(M, N, vec)
-        else:
-            A, Bt = _tag_inputs(N, M, vec)      # C^T trick: swap roles, then transpose the operands
-            A, Bt = torch.zeros(M, 64, dtype=torch.bfloat16), torch.zeros(N, 64, dtype=torch.bfloat16)
-            A[:, 0] = 1.0
-            Bt[:, 0] = torch.as_tensor(vec, dtype=torch.bfloat16)
+        A, Bt = _tag_inputs(M, N, vec, on_rows)
         send = torch.empty(send_elems, dtype=torch.bfloat16, device="cuda")
         fo.gemm_stage(plan, A.cuda(), Bt.cuda(), send)
         torch.cuda.synchronize()
