@@ -100,6 +100,10 @@ typedef struct {
   const int32_t* row_dst;     /* All-to-All: [m] destination rank of each output row */
   int32_t post;          /* fo_post */
   float eps;             /* RMSNorm epsilon */
+  int32_t a_mn_major;    /* 0: A is [m, k] row-major (K-major); 1: A is stored [k, m] row-major (M-major),
+                            e.g. dY of a weight-gradient GEMM dW = dY^T X (NEXT f4) */
+  int32_t b_mn_major;    /* 0: Bt is [n, k] row-major (K-major); 1: stored [k, n] row-major (N-major), e.g. X.
+                            MN-major operands need tile_n >= 128 */
 } fo_plan_desc;
 
 typedef struct {

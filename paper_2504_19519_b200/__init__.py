@@ -53,6 +53,8 @@ class PlanSpec:
     post: str = "none"
     eps: float = 1e-5
     ar_layout: str = "auto"
+    a_mn_major: int = 0   # 1: A given as [k, m] row-major (dY of dW = dY^T X)
+    b_mn_major: int = 0   # 1: Bt given as [k, n] row-major (X of dW = dY^T X)
     _keep: list = field(default_factory=list, repr=False)
 
     def to_c(self) -> _lib.PlanDescC:
@@ -70,6 +72,8 @@ class PlanSpec:
         d.row_dst = _p32(rd)
         d.post = POST[self.post]
         d.eps = float(self.eps)
+        d.a_mn_major = int(self.a_mn_major)
+        d.b_mn_major = int(self.b_mn_major)
         return d
 
 

@@ -38,6 +38,7 @@ class PlanDescC(C.Structure):
         ("num_groups", C.c_int32), ("group_waves", C.POINTER(C.c_int32)),
         ("row_dst", C.POINTER(C.c_int32)),
         ("post", C.c_int32), ("eps", C.c_float),
+        ("a_mn_major", C.c_int32), ("b_mn_major", C.c_int32),
     ]
 
 

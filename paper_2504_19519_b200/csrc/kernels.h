@@ -16,8 +16,9 @@ enum EpiMode : int {
 };
 
 struct GemmArgs {
-  const void* A;      // [M, K] bf16 row-major
-  const void* Bt;     // [N, K] bf16 row-major
+  const void* A;      // [M, K] bf16 row-major (K-major) or [K, M] (mn_major bit 0)
+  const void* Bt;     // [N, K] bf16 row-major (K-major) or [K, N] (mn_major bit 1)
+  int mn_major;       // bit 0: A is M-major, bit 1: Bt is N-major
   void* dst;          // bf16 destination (C or the send buffer)
   int64_t M, N, K;
   int BM, BN;

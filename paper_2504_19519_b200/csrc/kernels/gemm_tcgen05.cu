@@ -147,10 +147,26 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N>>3, M>>4.
-template <int M, int N>
+// UMMA descriptor for an MN-major operand staged as 64x64 TMA boxes (64
+// MN-elements = one 128-byte swizzled row per k): 8-k-row core groups are
+// 1024 B apart (SBO), consecutive 64-element MN chunks (boxes) 8192 B apart
+// (LBO); a K=16 step advances 2 core groups = 2048 B.
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(8192 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, N>>3, M>>4; MJ bit 0 /
+// bit 1 = A / B is MN-major (else K-major).
+template <int M, int N, int MJ>
 __device__ __forceinline__ constexpr uint32_t idesc_bf16() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MJ & 1) << 15) | ((uint32_t)((MJ >> 1) & 1) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 template <int CG>
@@ -267,13 +283,16 @@ __device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, in
 
 // One persistent worker = one CTA (CG=1) or one CTA pair (CG=2).  Worker w of
 // S = gridDim.x/CG runs positions w, w+S, ... (wave floor(p/S)).
-template <int BN, int CG>
+// MJ: operand majorness (bit 0: A is [K, M] M-major, bit 1: Bt is [K, N]
+// N-major — the weight-gradient dW = dY^T X layout); 0 = both K-major.
+template <int BN, int CG, int MJ>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     fo_gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const GemmArgs p) {
   using C = Cfg<BN, CG>;
   constexpr int ST = C::STAGES;
   constexpr int TM = BM * CG;  // tile rows
+  static_assert(!(MJ & 2) || (C::B_ROWS % 64 == 0), "MN-major B needs 64-row chunks");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                   // ST x 16 KB
@@ -339,17 +358,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int brow = tj * BN + (int)crank * C::B_ROWS;
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if constexpr (CG == 1) {
-            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, arow, &full[stage]);
-            tma_load_2d(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, brow, &full[stage]);
-          } else {
-            // both CTAs' bytes are counted on the leader's full barrier
-            if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
-            const uint32_t bar = mapa_shared(&full[stage], 0);
-            tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, arow, bar);
-            tma_load_2d_2sm(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, brow, bar);
-          }
+          // K-major operand: one box [rows, 64 k]; MN-major operand: 64x64
+          // boxes [64 k, 64 mn], one per 64-row chunk, 8 KB apart
+          auto load = [&](void* dst, const CUtensorMap* map, int rows0, int nrows) {
+            const bool mn = (map == &tmA) ? (MJ & 1) : (MJ & 2);
+            if (!mn) {
+              if constexpr (CG == 1) tma_load_2d(dst, map, kb * BK, rows0, &full[stage]);
+              else tma_load_2d_2sm(dst, map, kb * BK, rows0, mapa_shared(&full[stage], 0));
+            } else {
+              for (int h = 0; h < nrows / 64; ++h) {
+                uint8_t* d = reinterpret_cast<uint8_t*>(dst) + h * 8192;
+                if constexpr (CG == 1) tma_load_2d(d, map, rows0 + 64 * h, kb * BK, &full[stage]);
+                else tma_load_2d_2sm(d, map, rows0 + 64 * h, kb * BK, mapa_shared(&full[stage], 0));
+              }
+            }
+          };
+          // a pair's two CTAs' bytes are all counted on the leader's full barrier
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
+          load(sA + stage * A_STAGE_BYTES, &tmA, arow, BM);
+          load(sB + stage * C::B_STAGE_BYTES, &tmB, brow, C::B_ROWS);
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
@@ -360,7 +387,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     // ======================= MMA issuer (one thread of the leader CTA)
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = idesc_bf16<TM, BN>();
+      constexpr uint32_t idesc = idesc_bf16<TM, BN, MJ>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -373,12 +400,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t adesc = sw128_desc(smem_u32(sA + stage * A_STAGE_BYTES));
-          const uint64_t bdesc = sw128_desc(smem_u32(sB + stage * C::B_STAGE_BYTES));
+          const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t sb = smem_u32(sB + stage * C::B_STAGE_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            // +32 bytes along K inside the 128-byte swizzle row = +2 in the >>4 address field
-            umma_bf16<CG>(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
+            // K-major: +32 bytes along K inside the 128-byte swizzle row (+2 in the
+            // >>4 address field); MN-major: +2 core groups of 8 k-rows (+2048 B)
+            const uint64_t adesc = (MJ & 1) ? sw128_mn_desc(sa + 2048 * k) : sw128_desc(sa) + 2 * k;
+            const uint64_t bdesc = (MJ & 2) ? sw128_mn_desc(sb + 2048 * k) : sw128_desc(sb) + 2 * k;
+            umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit<CG>(&empty[stage]);  // frees the smem stage (in both CTAs) when these MMAs retire
           if (++stage == ST) {
@@ -537,31 +567,40 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// 2-D K-major bf16 map over [rows, K] with a [box_rows, 64] box, 128B swizzle.
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box_rows) {
+// 2-D bf16 map with 128B swizzle.  K-major operand [rows, K]: box [box_rows, 64 k].
+// MN-major operand stored [K, rows]: box [64 k, 64 rows].
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box_rows, bool mn_major) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(K * 2)};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  if (mn_major) {
+    dims[0] = (cuuint64_t)rows;
+    dims[1] = (cuuint64_t)K;
+    strides[0] = (cuuint64_t)(rows * 2);
+    box[0] = 64;
+    box[1] = (cuuint32_t)BK;
+  }
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int MJ>
 cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
   using C = Cfg<BN, CG>;
   static bool attr_set = false;
-  auto kern = fo_gemm_tcgen05_kernel<BN, CG>;
+  auto kern = fo_gemm_tcgen05_kernel<BN, CG, MJ>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   CUtensorMap mA, mB;
-  if (!make_map(&mA, a.A, a.M, a.K, BM) || !make_map(&mB, a.Bt, a.N, a.K, C::B_ROWS)) return cudaErrorInvalidValue;
+  if (!make_map(&mA, a.A, a.M, a.K, BM, MJ & 1) || !make_map(&mB, a.Bt, a.N, a.K, C::B_ROWS, MJ & 2))
+    return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.workers * CG);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -591,18 +630,30 @@ bool gemm_shape_supported(int bm, int bn) {
   return (bm == 128 || bm == 256) && (bn == 64 || bn == 128 || bn == 256);
 }
 
+template <int BN, int CG>
+cudaError_t launch_mj(const GemmArgs& a, cudaStream_t stream) {
+  switch (a.mn_major) {
+    case 0: return launch_cfg<BN, CG, 0>(a, stream);
+    case 1: return launch_cfg<BN, CG, 1>(a, stream);
+    case 2: return launch_cfg<BN, CG, 2>(a, stream);
+    case 3: return launch_cfg<BN, CG, 3>(a, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
+  if (a.mn_major && a.BN == 64) return cudaErrorInvalidValue;  // MN-major needs >= 64-row B chunks per CTA
   if (a.BM == 128) {
     switch (a.BN) {
-      case 64: return launch_cfg<64, 1>(a, stream);
-      case 128: return launch_cfg<128, 1>(a, stream);
-      case 256: return launch_cfg<256, 1>(a, stream);
+      case 64: return launch_cfg<64, 1, 0>(a, stream);
+      case 128: return launch_mj<128, 1>(a, stream);
+      case 256: return launch_mj<256, 1>(a, stream);
     }
   } else if (a.BM == 256) {
     switch (a.BN) {
-      case 64: return launch_cfg<64, 2>(a, stream);
-      case 128: return launch_cfg<128, 2>(a, stream);
-      case 256: return launch_cfg<256, 2>(a, stream);
+      case 64: return launch_cfg<64, 2, 0>(a, stream);
+      case 128: return launch_mj<128, 2>(a, stream);
+      case 256: return launch_mj<256, 2>(a, stream);
     }
   }
   return cudaErrorInvalidValue;

@@ -172,6 +172,10 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
   p.post = d.post;
   p.eps = d.eps;
   p.rank = rank; p.world = world;
+  if (d.a_mn_major < 0 || d.a_mn_major > 1 || d.b_mn_major < 0 || d.b_mn_major > 1)
+    fail(FO_ERR_INVALID_ARG, "a_mn_major / b_mn_major must be 0 or 1");
+  p.mn_major = (d.a_mn_major ? 1 : 0) | (d.b_mn_major ? 2 : 0);
+  if (p.mn_major && p.BN < 128) fail(FO_ERR_UNSUPPORTED, "MN-major operands need tile_n >= 128");
   p.Mt = g.Mt; p.Nt = g.Nt; p.tiles = g.tiles; p.T = g.T; p.P = g.P;
   p.order = g.order;
   p.group_waves = g.waves;

@@ -23,6 +23,7 @@ struct PlanHost {
   int post = FO_POST_NONE;
   float eps = 1e-5f;
   int rank = 0, world = 1;
+  int mn_major = 0;             // bit 0: A M-major, bit 1: Bt N-major
 
   // ---- O1-O3
   int Mt = 0, Nt = 0, tiles = 0, T = 0, P = 0;

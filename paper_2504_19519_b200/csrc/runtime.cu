@@ -139,6 +139,7 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   GemmArgs a{};
   a.A = A;
   a.Bt = Bt;
+  a.mn_major = h.mn_major;
   a.dst = dst;
   a.M = h.M;
   a.N = h.N;

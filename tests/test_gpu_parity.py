@@ -415,3 +415,60 @@ def test_tag_runs_decode_every_element(coll, n):
     want = np.empty(send_elems, np.int64)
     want[plan.export_send_map()] = np.arange(M * N)
     assert np.array_equal(decoded, want)
+
+
+# ------------------------------------------------------------------ MN-major operands (weight-gradient GEMMs, NEXT f4)
+@pytest.mark.parametrize("mj", [1, 2, 3])
+@pytest.mark.parametrize("BM,BN", [(128, 128), (128, 256), (256, 128), (256, 256)])
+def test_gemm_mn_major_exact(mj, BM, BN):
+    M, N, K = 768, 768, 320
+    if M % BM or N % BN:
+        pytest.skip("shape")
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=40 + mj, nnz_per_row=256)
+    a_st = A.t().contiguous() if mj & 1 else A       # [K, M] when M-major
+    b_st = Bt.t().contiguous() if mj & 2 else Bt     # [K, N] when N-major
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=5, swizzle=2,
+                   a_mn_major=mj & 1, b_mn_major=(mj >> 1) & 1)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, _dev_bf16(a_st), _dev_bf16(b_st), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(out), onum.gemm(A, Bt))
+
+
+@pytest.mark.parametrize("coll", ["allreduce", "reducescatter"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_weight_gradient_dp_fsdp(coll, n):
+    """NEXT f4: data-parallel gradient AllReduce / FSDP
+    ReduceScatter after the weight-gradient GEMM dW_r = dY_r^T X_r, with dY_r
+    [tokens, out] and X_r [tokens, in] used in place (M- / N-major operands).
+    Every rank's GEMM + pre-reorder runs on the GPU; the collective is emulated;
+    the result is compared with sum_r dY_r^T X_r (exact-integer regime)."""
+    T_tok, OUT, IN, BM, BN, S = 512, 512, 768, 256, 128, 4
+    tiles = (OUT // BM) * (IN // BN)
+    groups = _groups(tiles, S, 9)
+    dYs, Xs = [], []
+    for r in range(n):
+        # dY_r^T plays A ([out, tokens] logical), X_r^T plays Bt ([in, tokens] logical)
+        A_log, Bt_log = synthetic.exact_inputs(OUT, IN, T_tok, seed=600 + r, nnz_per_row=max(1, 256 // n))
+        dYs.append(A_log.t().contiguous())    # dY_r stored [tokens, out]
+        Xs.append(Bt_log.t().contiguous())    # X_r stored [tokens, in]
+    oplan = op.make_plan(OUT, IN, BM, BN, S, groups, swizzle=2)
+    logical_A = [d.t() for d in dYs]
+    logical_Bt = [x.t() for x in Xs]
+    if coll == "allreduce":
+        ores = opl.run_allreduce(logical_A, logical_Bt, oplan)
+        plain = opl.plain_allreduce(logical_A, logical_Bt)
+    else:
+        ores = opl.run_reducescatter(logical_A, logical_Bt, oplan)
+        plain = opl.plain_reducescatter(logical_A, logical_Bt, BM)
+    for r in range(n):
+        plan = fo.Plan(coll=coll, m=OUT, n=IN, k=T_tok, tile_m=BM, tile_n=BN, workers=S, swizzle=2,
+                       group_waves=groups, ar_layout="slot", rank=r, world=n, a_mn_major=1, b_mn_major=1)
+        send = torch.empty(plan.info["send_elems"], dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, _dev_bf16(dYs[r]), _dev_bf16(Xs[r]), send)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(send), ores["send"][r])
+        out = torch.empty(plan.info["out_rows"], IN, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plan, _dev_bf16(ores["recv"][r]), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(out), plain[r])
