@@ -591,12 +591,15 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box
 template <int BN, int CG, int MJ>
 cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
   using C = Cfg<BN, CG>;
-  static bool attr_set = false;
+  static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
   auto kern = fo_gemm_tcgen05_kernel<BN, CG, MJ>;
-  if (!attr_set) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.fetch_or(bit);
   }
   CUtensorMap mA, mB;
   if (!make_map(&mA, a.A, a.M, a.K, BM, MJ & 1) || !make_map(&mB, a.Bt, a.N, a.K, C::B_ROWS, MJ & 2))

@@ -342,25 +342,35 @@ __global__ void fo_fill_u16_kernel(uint16_t* dst, int64_t n, uint16_t v) {
     dst[i] = v;
 }
 
-int g_num_sms = 0;
+int num_sms() {
+  static int cache[64] = {0};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = cache[dev & 63];
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (!n) n = 148;
+  }
+  return n;
+}
 
 template <int MAP>
 cudaError_t launch_map(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int64_t chunks = a.N / 8;
   if (a.op == FO_POST_ADD_RMSNORM) {
-    const int grid = (int)std::min<int64_t>(a.rows, (int64_t)g_num_sms * 8);
+    const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 8);
     if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 1><<<grid, 256, 0, stream>>>(a, lbn);
     else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 2><<<grid, 256, 0, stream>>>(a, lbn);
     else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 4><<<grid, 256, 0, stream>>>(a, lbn);
     else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8><<<grid, 256, 0, stream>>>(a, lbn);
     else {
-      const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)g_num_sms * 8);
+      const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)num_sms() * 8);
       fo_post_rmsnorm_wide_kernel<MAP><<<g2, 256, 0, stream>>>(a, lbn);
     }
     return cudaGetLastError();
   }
   const int64_t units = a.rows * ((chunks + SEG_CHUNKS - 1) / SEG_CHUNKS);
-  const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)g_num_sms * 16);
+  const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)num_sms() * 16);
   if (a.op == FO_POST_ADD) fo_post_reorder_kernel<MAP, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn);
   else fo_post_reorder_kernel<MAP, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn);
   return cudaGetLastError();
@@ -376,7 +386,7 @@ cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream) {
   const int64_t chunks = (a.map == POSTMAP_A2A) ? (a.sub_end - a.sub_begin) * cpr
                                                  : (int64_t)(a.pos_end - a.pos_begin) * a.R * cpr;
   if (chunks <= 0) return cudaSuccess;
-  const int cap = a.grid_cap > 0 ? a.grid_cap : 148 * 4;
+  const int cap = a.grid_cap > 0 ? a.grid_cap : num_sms() * 4;
   const int grid = (int)std::min<int64_t>((chunks + 255) / 256, cap);
   switch (a.map * 4 + a.op) {
     case POSTMAP_SLOT * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_SLOT, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
@@ -405,7 +415,7 @@ cudaError_t launch_wait(const uint32_t* counter, uint32_t target, cudaStream_t s
 
 cudaError_t launch_fill_u16(void* dst, int64_t count, uint16_t value, cudaStream_t stream) {
   if (count <= 0) return cudaSuccess;
-  const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 8);
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 8);
   fo_fill_u16_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<uint16_t*>(dst), count, value);
   count_launch();
   return cudaGetLastError();
@@ -414,12 +424,6 @@ cudaError_t launch_fill_u16(void* dst, int64_t count, uint16_t value, cudaStream
 cudaError_t launch_post(const PostArgs& a, cudaStream_t stream) {
   if (a.rows <= 0) return cudaSuccess;
   if (a.N % 8 || (a.BN & (a.BN - 1))) return cudaErrorInvalidValue;
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (!g_num_sms) g_num_sms = 148;
-  }
   int lbn = 0;
   while ((1 << lbn) < a.BN) ++lbn;
   cudaError_t e;

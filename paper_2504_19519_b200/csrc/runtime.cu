@@ -270,7 +270,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
     a.sub_end = (j + 1 < h.P) ? h.recv_off[(size_t)(j + 1) * W] : h.recv_elems / h.BN;
   }
   a.recv_dst = p->d_recv_dst;
-  a.grid_cap = 296;
+  a.grid_cap = 0;  // default: 4 blocks per SM
   FO_CUDA(launch_group_post(a, s));
 }
 
