@@ -472,3 +472,58 @@ def test_weight_gradient_dp_fsdp(coll, n):
         fo.post_stage(plan, _dev_bf16(ores["recv"][r]), out)
         torch.cuda.synchronize()
         assert np.array_equal(_host(out), plain[r])
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("BM,BN,M,N,K,S", [
+    (128, 64, 128, 64, 64, 1),      # one tile, one k-block, one worker
+    (256, 256, 256, 256, 64, 1),    # one pair tile
+    (128, 128, 512, 256, 64, 16),   # more workers than tiles (idle workers)
+    (256, 128, 512, 512, 128, 1),   # a single worker runs every position (T = tiles)
+])
+def test_gemm_edge_shapes(ctx1, BM, BN, M, N, K, S):
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=M + K, nnz_per_row=64)
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, ar_layout="slot")
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx1, plan, _dev_bf16(A), _dev_bf16(Bt), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(out), onum.gemm(A, Bt))
+
+
+def test_rs_one_row_subtiles():
+    """RS with world == tile_m: subtiles of a single row (h = 1)."""
+    n, M, N, K, BM, BN, S = 128, 256, 128, 64, 128, 128, 1
+    As, Bts = _rank_inputs(1, M, N, K, 77)
+    oplan = op.make_plan(M, N, BM, BN, S, None)
+    Y = onum.gemm(As[0], Bts[0])
+    buf = orr.rs_pre(Y, oplan, n)
+    plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, rank=5, world=n)
+    send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, _dev_bf16(As[0]), _dev_bf16(Bts[0]), send)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(send), buf)
+
+
+def test_alltoall_rank_receiving_nothing():
+    """Rank 1 gets no rows from anyone; rank 0 gets everything (zero counts are legal)."""
+    n, N, K, BM, BN = 2, 256, 64, 128, 128
+    specs, As, Bts, oplans, rds = [], [], [], [], []
+    for s in range(n):
+        M = 256 * (s + 1)
+        rd = np.zeros(M, np.int32)
+        A, Bt = synthetic.exact_inputs(M, N, K, seed=90 + s, nnz_per_row=64)
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=2, group_waves=[1, (M // BM * 2 + 1) // 2 - 1], row_dst=rd))
+        oplans.append(op.make_plan(M, N, BM, BN, 2, specs[-1]["group_waves"]))
+        As.append(A), Bts.append(Bt), rds.append(rd)
+    ores = opl.run_alltoall(As, Bts, oplans, rds)
+    for me in range(n):
+        plan = fo.Plan(rank=me, world=n, peers=specs, **specs[me])
+        assert plan.info["out_rows"] == (sum(s["m"] for s in specs) if me == 0 else 0)
+        recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][me]])
+        if me == 1:
+            assert recv.size == 0 and plan.info["recv_elems"] == 0
+            continue
+        out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plan, _dev_bf16(recv), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(out), opl.plain_alltoall(As, Bts, rds)[me])
