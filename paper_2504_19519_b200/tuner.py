@@ -184,3 +184,39 @@ class PlanCache:
         self.put(tp)
         self.save()
         return tp
+
+
+def a2a_wave_bytes(specs: list, elem_bytes: int = 2):
+    """Per-rank, per-wave bytes each rank sends off-rank in an All-to-All plan
+    set (the census of PAPER.md:392, one plan per wave): [ranks][T]."""
+    import numpy as np
+
+    from . import Plan
+
+    n = len(specs)
+    out = []
+    Ts = set()
+    for r, sp in enumerate(specs):
+        tiles = (sp["m"] // sp["tile_m"]) * (sp["n"] // sp["tile_n"])
+        T = -(-tiles // sp["workers"])
+        Ts.add(T)
+        per_wave = [dict(s, group_waves=[1] * (-(-(s["m"] // s["tile_m"]) * (s["n"] // s["tile_n"]) // s["workers"])))
+                    for s in specs]
+        plan = Plan(rank=r, world=n, peers=per_wave, **per_wave[r])
+        sc, _ = plan.export_a2a_counts()          # [T, n] subtokens per (wave, destination)
+        sc = sc.astype(np.float64)
+        sc[:, r] = 0.0                            # the self part is a local copy
+        out.append((sc.sum(axis=1) * sp["tile_n"] * elem_bytes).tolist())
+    if len(Ts) != 1:
+        raise ValueError("imbalance-aware search needs a common wave count (pad experts to a common tile count)")
+    return out
+
+
+def tune_alltoall(specs: list, durations: list, curve: list, s1=2, sp=4, prune=True):
+    """A2A imbalance extension of Alg. 1 (R26): one
+    common partition for all expert ranks from their GEMM durations and their
+    per-wave send bytes."""
+    from . import tune_search_multi
+
+    wb = a2a_wave_bytes(specs)
+    return tune_search_multi(durations, wb, curve, s1=s1, sp=sp, prune=prune)

@@ -527,3 +527,30 @@ def test_alltoall_rank_receiving_nothing():
         fo.post_stage(plan, _dev_bf16(recv), out)
         torch.cuda.synchronize()
         assert np.array_equal(_host(out), opl.plain_alltoall(As, Bts, rds)[me])
+
+
+@pytest.mark.parametrize("n", [1, 4])
+def test_rowband_with_swizzled_panels(ctx1, n):
+    """ROWBAND layout with a non-raster order: panels of 2 tile-rows visited
+    column-major, one panel per wave, so every group is a band of whole
+    tile-rows and the epilogue writes row-major C in place (H11a)."""
+    M, N, K, BM, BN, S = 1024, 512, 128, 128, 128, 8    # Mt=8, Nt=4, panel = 2 rows = 8 tiles = S
+    groups = [1, 2, 1]
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2,
+                   group_waves=groups, ar_layout="rowband", rank=0, world=n)
+    assert plan.info["ar_layout"] == 1
+    assert plan.export_order()[:4].tolist() == [0, 4, 1, 5]
+    As, Bts = _rank_inputs(n, M, N, K, 123)
+    oplan = op.make_plan(M, N, BM, BN, S, groups, swizzle=2)
+    ores = opl.run_allreduce(As, Bts, oplan, layout="rowband")
+    send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, _dev_bf16(As[0]), _dev_bf16(Bts[0]), send)
+    torch.cuda.synchronize()
+    assert np.array_equal(_host(send), ores["send"][0])
+    for j in range(len(groups)):
+        assert plan.group(j)[2:] == orr.group_elem_ranges(oplan, "rowband")[j]
+    if n == 1:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        fo.run(ctx1, plan, _dev_bf16(As[0]), _dev_bf16(Bts[0]), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(out), opl.plain_allreduce(As, Bts)[0])

@@ -56,3 +56,31 @@ def test_neighbour_with_incompatible_waves_is_retuned():
 
 def test_distance():
     assert tuner.distance((4096, 4096, 4096), (8192, 4096, 2048)) == pytest.approx(2.0)
+
+
+def test_tune_alltoall_imbalanced_census():
+    """A2A imbalance extension: per-wave send bytes come from the plan census;
+    a rank with more off-rank traffic / a slower GEMM dominates the prediction."""
+    import numpy as np
+
+    from oracle import alg1
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    n, N = 2, 256
+    rng = np.random.default_rng(0)
+    specs = []
+    for r in range(n):
+        rd = rng.integers(0, n, size=512).astype(np.int32)
+        specs.append(dict(coll="alltoall", m=512, n=N, k=64, tile_m=128, tile_n=128, workers=2, row_dst=rd))
+    wb = tuner.a2a_wave_bytes(specs)
+    assert len(wb) == n and len(wb[0]) == 4
+    # rank r's total off-rank bytes = rows routed elsewhere x N x 2
+    for r in range(n):
+        off = int((specs[r]["row_dst"] != r).sum())
+        assert sum(wb[r]) == off * N * 2
+    curve = [(2 ** 12, 5.0), (2 ** 20, 100.0), (2 ** 26, 400.0)]
+    G, t = tuner.tune_alltoall(specs, [50.0, 80.0], curve)
+    lat = lambda b: alg1.interp_latency_us(curve, b)
+    assert t == pytest.approx(alg1.search_multi(4, [50.0, 80.0], wb, lat)[1], rel=1e-12)
+    assert sum(G) == 4
