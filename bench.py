@@ -202,7 +202,9 @@ def main():
     import paper_2504_19519_b200 as fo
 
     torch.cuda.set_device(local)
-    if world > 1:
+    # under torchrun (even at one process) the distributed plumbing is live
+    use_dist = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peak_src = load_peaks()
     sms = fo.device_sm_count(local)
@@ -228,7 +230,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     # ---- NCCL context of the library (unique id broadcast over the process group)
-    if world > 1:
+    if use_dist:
         obj = [fo.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
@@ -237,7 +239,7 @@ def main():
     ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier(device_ids=[local])
 
     def timed(fn, steps, warm):
@@ -256,7 +258,7 @@ def main():
             torch.cuda.synchronize()
             ts.append(s.elapsed_time(e) * 1e3)
         mean = statistics.mean(ts)
-        if world > 1:
+        if use_dist:
             t = torch.tensor([mean], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             mean = t.item()
@@ -282,7 +284,7 @@ def main():
                 torch.cuda.synchronize()
                 ts[k].append(s.elapsed_time(e) * 1e3)
         means = {k: statistics.mean(v) for k, v in ts.items()}
-        if world > 1:
+        if use_dist:
             t = torch.tensor([means[k] for k in fns], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             means = {k: t[i].item() for i, k in enumerate(fns)}
@@ -385,7 +387,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
