@@ -241,16 +241,46 @@ static void stream_wait(fo_plan_s* p, WaitValue32Fn wait, cudaStream_t cs, int j
 // Per-group post-reorder (H11b) applies to the non-identity maps
 // when the fused op is elementwise per element (none / residual add); RMSNorm
 // needs whole rows and runs once after the last group.
+// AR ROWBAND with a fused op: every group is a band of complete rows, so the
+// op (residual add, RMSNorm over whole rows) can run on the band right after
+// the band's AllReduce.
+static bool band_post(const PlanHost& h) {
+  return h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND && h.post != FO_POST_NONE;
+}
+
 static bool use_group_post(const fo_plan_s* p) {
   const PlanHost& h = p->host;
   if (p->group_post == 0) return false;
+  if (band_post(h)) return true;
   const int map = post_map(h);
   return map != POSTMAP_IDENTITY && (h.post == FO_POST_NONE || h.post == FO_POST_ADD);
 }
 
-static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, const void* residual, cudaStream_t s) {
+static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, const void* residual,
+                           const void* gamma, cudaStream_t s) {
   const PlanHost& h = p->host;
-  if (h.post == FO_POST_ADD && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
+  if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
+  if (band_post(h)) {
+    // in place on the band's rows [r0*BM, r1*BM) of out (== src)
+    if (h.post == FO_POST_ADD_RMSNORM && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
+    const int64_t row0 = h.band_rows[2 * j] * h.BM, rows = (h.band_rows[2 * j + 1] - h.band_rows[2 * j]) * h.BM;
+    PostArgs a{};
+    a.map = POSTMAP_IDENTITY;
+    a.op = h.post;
+    a.src = reinterpret_cast<const char*>(src) + 2 * row0 * h.N;
+    a.out = reinterpret_cast<char*>(out) + 2 * row0 * h.N;
+    a.residual = reinterpret_cast<const char*>(residual) + 2 * row0 * h.N;
+    a.gamma = gamma;
+    a.rows = rows;
+    a.N = h.N;
+    a.BM = h.BM;
+    a.BN = h.BN;
+    a.Nt = h.Nt;
+    a.h = h.h;
+    a.eps = h.eps;
+    FO_CUDA(launch_post(a, s));
+    return;
+  }
   GroupPostArgs a{};
   a.map = post_map(h);
   a.op = h.post;
@@ -445,7 +475,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
           FO_CUDA(cudaEventRecord(c->ev_group[j], c->comm_stream));
           FO_CUDA(cudaStreamWaitEvent(c->post_stream, c->ev_group[j], 0));
           ps = c->post_stream;
-          run_group_post(p, j, post_src, out, residual, ps);
+          run_group_post(p, j, post_src, out, residual, gamma, ps);
         }
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j + 1, ps));
       }

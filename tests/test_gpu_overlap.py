@@ -119,3 +119,34 @@ def test_group_post_equals_single_post(ctx, coll, post):
     fo.run(ctx, p_off, A, Bt, o2, res if post != "none" else None)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("post", ["add", "add_rmsnorm"])
+def test_rowband_band_post_equals_single_post(ctx, post):
+    """ROWBAND: the fused add / RMSNorm runs per band right after the band's
+    AllReduce; it must equal the single post after the last group, and the
+    oracle within tolerance."""
+    from oracle import numerics as onum
+    from oracle import post as opost
+
+    M, N, K, S = 2048, 1024, 512, 8          # 256x256 pairs: 8x4 tiles, S=8 -> waves of 2 tile-rows
+    kw = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+              group_waves=[1, 2, 1], ar_layout="rowband", post=post)
+    p_on, p_off = fo.Plan(**kw), fo.Plan(**kw)
+    p_off.set_debug(group_post=0)
+    assert p_on.info["ar_layout"] == 1
+    A, Bt = synthetic.float_inputs(M, N, K, seed=21)
+    res = synthetic.normal_bf16((M, N), 1.0, 22)
+    gam = synthetic.normal_bf16((N,), 1.0, 23)
+    o1 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    args = (A.cuda(), Bt.cuda())
+    fo.run(ctx, p_on, *args, o1, res.cuda(), gam.cuda())
+    fo.run(ctx, p_off, *args, o2, res.cuda(), gam.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    x = onum.round_bf16(onum.gemm(A, Bt))
+    want = opost.add(x, onum.to_f64(res)) if post == "add" else opost.add_rmsnorm(x, onum.to_f64(res), onum.to_f64(gam), 1e-5)
+    g = o1.double().cpu().numpy()
+    rms = np.sqrt(np.mean(want * want))
+    assert np.max(np.abs(g - want) / np.maximum(np.abs(want), rms)) <= 1e-2
