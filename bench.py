@@ -304,6 +304,13 @@ def main():
 
     plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=list(groups),
                    ar_layout="auto", swizzle=0, rank=rank, world=world)
+    # fused-op convention (R17): the same layer followed by
+    # residual add + RMSNorm, fused into the (per-band) post-communication pass
+    nplan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=list(groups),
+                    ar_layout="auto", swizzle=0, rank=rank, world=world, post="add_rmsnorm")
+    resid = synthetic.normal_bf16((M, N), 1.0, 7, device="cuda")
+    gamma = synthetic.normal_bf16((N,), 1.0, 8, device="cuda")
+    out2 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     # the GEMM-only timing uses exactly the overlapped plan's execution order
     gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=plan.export_order())
 
@@ -326,7 +333,10 @@ def main():
     with ClockSampler(local) as clk:
         m = timed_multi({"ov": lambda: fo.run(ctx, plan, A, Bt, out),
                          "seq": lambda: fo.run_sequential(ctx, plan, A, Bt, out),
-                         "gemm": lambda: fo.gemm_stage(gplan, A, Bt, out)}, args.steps, args.warmup)
+                         "gemm": lambda: fo.gemm_stage(gplan, A, Bt, out),
+                         "ov_norm": lambda: fo.run(ctx, nplan, A, Bt, out2, resid, gamma),
+                         "seq_norm": lambda: fo.run_sequential(ctx, nplan, A, Bt, out2, resid, gamma)},
+                        args.steps, args.warmup)
     ov_us, seq_us, gk_us = m["ov"], m["seq"], m["gemm"]
     launches = launches_per_step * args.steps
 
@@ -374,6 +384,9 @@ def main():
             "tflops": round(world * flops / (ov_us * 1e-6) / 1e12, 1),
             "layer_roofline_us": round(layer_roof_us, 2), "frac_of_layer_roofline": round(layer_roof_us / ov_us, 4),
             "alg1_predicted_us": round(pred, 2), "spot_check": spot,
+            "fused_add_rmsnorm": {"overlapped_us": round(m["ov_norm"], 2), "sequential_us": round(m["seq_norm"], 2),
+                                  "speedup": round(m["seq_norm"] / m["ov_norm"], 4),
+                                  "note": "GEMM+AR+residual add+RMSNorm; overlapped runs the fused op per row band"},
             "roofline": {"bound": "tensor", "kernel": f"fo_gemm_tcgen05_kernel<{BN},{cg}>", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed alone per step)",
