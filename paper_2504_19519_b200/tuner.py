@@ -220,3 +220,15 @@ def tune_alltoall(specs: list, durations: list, curve: list, s1=2, sp=4, prune=T
 
     wb = a2a_wave_bytes(specs)
     return tune_search_multi(durations, wb, curve, s1=s1, sp=sp, prune=prune)
+
+
+def effective_curve(curve: list, post_us_per_byte: float, post_fixed_us: float = 0.0) -> list:
+    """Fold a per-group post-communication op (the fused add / RMSNorm that runs
+    right after each group's collective) into the bandwidth curve Alg. 1 sees:
+    the latency of a group of b bytes becomes collective(b) + post(b), with
+    post(b) = post_fixed_us + post_us_per_byte * b (measured offline)."""
+    out = []
+    for b, bw in curve:
+        t = b / (bw * 1e9) * 1e6 + post_fixed_us + post_us_per_byte * b
+        out.append((b, b / (t * 1e-6) / 1e9))
+    return out

@@ -84,3 +84,12 @@ def test_tune_alltoall_imbalanced_census():
     lat = lambda b: alg1.interp_latency_us(curve, b)
     assert t == pytest.approx(alg1.search_multi(4, [50.0, 80.0], wb, lat)[1], rel=1e-12)
     assert sum(G) == 4
+
+
+def test_effective_curve_adds_post_cost():
+    curve = [(1 << 20, 100.0), (1 << 24, 400.0)]
+    eff = tuner.effective_curve(curve, post_us_per_byte=1e-5, post_fixed_us=2.0)
+    for (b, bw), (_, ebw) in zip(curve, eff):
+        t = b / (bw * 1e9) * 1e6
+        te = b / (ebw * 1e9) * 1e6
+        assert te == pytest.approx(t + 2.0 + 1e-5 * b)
