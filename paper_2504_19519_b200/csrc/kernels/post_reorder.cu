@@ -168,12 +168,15 @@ __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p, 
   }
 }
 
-// Residual add + RMSNorm: one 256-thread block per row, the whole row held in
-// registers (MAXC chunks of 8 per thread, N <= 2048*MAXC), single pass over HBM:
-// read x (through the map) and residual once, write out once.
-template <int MAP, int MAXC>
-__global__ void __launch_bounds__(256) fo_post_rmsnorm_kernel(const PostArgs p, int lbn) {
-  __shared__ float red[8];
+// Residual add + RMSNorm: one THREADS-thread block per row, the whole row held
+// in registers (MAXC chunks of 8 per thread, N <= 8*THREADS*MAXC), single pass
+// over HBM: read x (through the map) and residual once, write out once.
+// 128-thread blocks with 4 chunks per thread keep 2x the rows (and 8
+// independent 16-byte loads per thread) in flight compared with 256 x 2.
+template <int MAP, int MAXC, int THREADS>
+__global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs p, int lbn) {
+  constexpr int WARPS = THREADS / 32;
+  __shared__ float red[WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t chunks = p.N >> 3;
   const int bn_mask = p.BN - 1;
@@ -187,25 +190,27 @@ __global__ void __launch_bounds__(256) fo_post_rmsnorm_kernel(const PostArgs p, 
     uint4 xv[MAXC], rv[MAXC];
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
-      const int64_t c = tid + 256 * i;
+      const int64_t c = tid + THREADS * i;
       if (c < chunks) {
         xv[i] = ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask));
         rv[i] = ld_stream(rrow + 8 * c);
       }
     }
-    float y[MAXC][8];
+    // y = x + residual is recomputed from the packed inputs in the second
+    // phase (identical fp32 ops) instead of being held: fewer registers, more
+    // rows in flight per SM
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
-      const int64_t c = tid + 256 * i;
+      const int64_t c = tid + THREADS * i;
       if (c < chunks) {
         float x[8], q[8];
         unpack8(xv[i], x);
         unpack8(rv[i], q);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          y[i][k] = x[k] + q[k];
-          ss += y[i][k] * y[i][k];
+          const float y = x[k] + q[k];
+          ss += y * y;
         }
       }
     }
@@ -215,18 +220,20 @@ __global__ void __launch_bounds__(256) fo_post_rmsnorm_kernel(const PostArgs p, 
     __syncthreads();
     float tot = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) tot += red[w];
+    for (int w = 0; w < WARPS; ++w) tot += red[w];
     __syncthreads();  // red[] reused by the next row
     const float rstd = rsqrtf(tot / (float)p.N + p.eps);
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
-      const int64_t c = tid + 256 * i;
+      const int64_t c = tid + THREADS * i;
       if (c < chunks) {
-        float g[8];
+        float x[8], q[8], g[8];
+        unpack8(xv[i], x);
+        unpack8(rv[i], q);
         unpack8(ld_coherent(gam + 8 * c), g);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) y[i][k] = y[i][k] * rstd * g[k];
-        st_stream(orow + 8 * c, pack8(y[i]));
+        for (int k = 0; k < 8; ++k) x[k] = (x[k] + q[k]) * rstd * g[k];
+        st_stream(orow + 8 * c, pack8(x));
       }
     }
   }
@@ -358,11 +365,12 @@ template <int MAP>
 cudaError_t launch_map(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int64_t chunks = a.N / 8;
   if (a.op == FO_POST_ADD_RMSNORM) {
-    const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 8);
-    if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 1><<<grid, 256, 0, stream>>>(a, lbn);
-    else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 2><<<grid, 256, 0, stream>>>(a, lbn);
-    else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 4><<<grid, 256, 0, stream>>>(a, lbn);
-    else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8><<<grid, 256, 0, stream>>>(a, lbn);
+    const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 16);
+    if (chunks <= 128) fo_post_rmsnorm_kernel<MAP, 1, 128><<<grid, 128, 0, stream>>>(a, lbn);
+    else if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 2, 128><<<grid, 128, 0, stream>>>(a, lbn);
+    else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 4, 128><<<grid, 128, 0, stream>>>(a, lbn);
+    else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 8, 128><<<grid, 128, 0, stream>>>(a, lbn);
+    else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8, 256><<<grid, 256, 0, stream>>>(a, lbn);
     else {
       const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)num_sms() * 8);
       fo_post_rmsnorm_wide_kernel<MAP><<<g2, 256, 0, stream>>>(a, lbn);
