@@ -54,7 +54,19 @@ def _headers():
     return hs
 
 
+def up_to_date() -> bool:
+    """The in-tree library is newer than every source and header (object files
+    are not needed: build/ does not travel to the GPU boxes)."""
+    if not os.path.exists(OUT):
+        return False
+    newest = max([os.path.getmtime(h) for h in _headers()] +
+                 [os.path.getmtime(os.path.join(CSRC, s)) for s in SOURCES])
+    return os.path.getmtime(OUT) >= newest
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
+    if not force and up_to_date():
+        return OUT
     inc, lib = nccl_dirs()
     os.makedirs(BUILD, exist_ok=True)
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
