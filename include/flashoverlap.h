@@ -191,8 +191,10 @@ fo_status fo_run(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* 
  * host->device copies of A, Bt (+ residual, gamma) into library-owned device
  * staging, the overlapped op, and the device->host copy of `out`, all on
  * `stream` (host-asynchronous when the host buffers are page-locked; the
- * caller synchronises the stream before reading `out`).  This is the
- * end-to-end entry point bench.py's `e2e` number is measured through. */
+ * caller synchronises the stream before reading `out`).  Any operand that is
+ * already a device pointer (e.g. resident weights Bt) is used in place and
+ * not copied.  This is the end-to-end entry point bench.py's `e2e` number is
+ * measured through. */
 fo_status fo_run_host(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
                       const void* residual, const void* gamma, void* stream);
 /* Non-overlapped baseline: the SAME GEMM kernel writing row-major C, then ONE

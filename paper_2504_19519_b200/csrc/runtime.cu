@@ -499,6 +499,16 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
   });
 }
 
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: plain host memory
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
 fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
                       const void* gamma, void* stream) {
   return guard([&] {
@@ -508,19 +518,25 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t a_bytes = 2 * (size_t)(h.M * h.K), b_bytes = 2 * (size_t)(h.N * h.K);
     const size_t o_bytes = 2 * (size_t)(h.out_rows * h.N);
-    if (!p->h_A) FO_CUDA(cudaMalloc(&p->h_A, a_bytes));
-    if (!p->h_Bt) FO_CUDA(cudaMalloc(&p->h_Bt, b_bytes));
-    if (!p->h_out) FO_CUDA(cudaMalloc(&p->h_out, o_bytes));
-    if (residual && !p->h_res) FO_CUDA(cudaMalloc(&p->h_res, o_bytes));
-    if (gamma && !p->h_gamma) FO_CUDA(cudaMalloc(&p->h_gamma, 2 * (size_t)h.N));
-    FO_CUDA(cudaMemcpyAsync(p->h_A, A, a_bytes, cudaMemcpyHostToDevice, s));
-    FO_CUDA(cudaMemcpyAsync(p->h_Bt, Bt, b_bytes, cudaMemcpyHostToDevice, s));
-    if (residual) FO_CUDA(cudaMemcpyAsync(p->h_res, residual, o_bytes, cudaMemcpyHostToDevice, s));
-    if (gamma) FO_CUDA(cudaMemcpyAsync(p->h_gamma, gamma, 2 * (size_t)h.N, cudaMemcpyHostToDevice, s));
-    fo_status st = fo_run(c, p, p->h_A, p->h_Bt, p->h_out, residual ? p->h_res : nullptr,
-                          gamma ? p->h_gamma : nullptr, stream);
+    // host operands are staged through library-owned device buffers; operands
+    // that already live on the device (e.g. resident weights) are used in place
+    auto stage = [&](const void* src, void*& buf, size_t bytes) -> const void* {
+      if (!src) return nullptr;
+      if (is_device_ptr(src)) return src;
+      if (!buf) FO_CUDA(cudaMalloc(&buf, bytes));
+      FO_CUDA(cudaMemcpyAsync(buf, src, bytes, cudaMemcpyHostToDevice, s));
+      return buf;
+    };
+    const void* dA = stage(A, p->h_A, a_bytes);
+    const void* dB = stage(Bt, p->h_Bt, b_bytes);
+    const void* dR = stage(residual, p->h_res, o_bytes);
+    const void* dG = stage(gamma, p->h_gamma, 2 * (size_t)h.N);
+    const bool out_dev = is_device_ptr(out);
+    if (!out_dev && !p->h_out) FO_CUDA(cudaMalloc(&p->h_out, o_bytes));
+    void* dO = out_dev ? out : p->h_out;
+    fo_status st = fo_run(c, p, dA, dB, dO, dR, dG, stream);
     if (st != FO_OK) throw Error(st, fo_last_error());
-    FO_CUDA(cudaMemcpyAsync(out, p->h_out, o_bytes, cudaMemcpyDeviceToHost, s));
+    if (!out_dev) FO_CUDA(cudaMemcpyAsync(out, dO, o_bytes, cudaMemcpyDeviceToHost, s));
   });
 }
 

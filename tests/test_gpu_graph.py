@@ -81,6 +81,11 @@ def test_run_host_matches_device_run():
     fo.run(ctx, plan, A.cuda(), Bt.cuda(), out_d, res.cuda(), gam.cuda())
     torch.cuda.synchronize()
     assert torch.equal(out_h, out_d.cpu())
+    # mixed: device-resident weights and gamma, host activations / residual / output
+    out_h2 = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    fo.run_host(ctx, plan, A.pin_memory(), Bt.cuda(), out_h2, res, gam.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(out_h2, out_d.cpu())
     ctx.close()
 
 
