@@ -74,6 +74,7 @@ void release_device(fo_plan_s* p) {
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(p->device);
+  if (p->d_recv == p->d_send) p->d_recv = nullptr;  // aliased at world 1
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
                     p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma,
@@ -130,8 +131,12 @@ static void ensure_device(fo_plan_s* p) {
   p->d_flags = p->d_counters + h.P;
   const bool need_send = !(h.coll == FO_NOCOMM || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND));
   if (need_send && h.send_elems) FO_CUDA(cudaMalloc(&p->d_send, 2 * h.send_elems));
-  if ((h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && h.recv_elems)
-    FO_CUDA(cudaMalloc(&p->d_recv, 2 * h.recv_elems));
+  if ((h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && h.recv_elems) {
+    // one rank: the receive layout ([group][source 0]) is the send layout, so
+    // the collective runs in place (no copy)
+    if (h.world == 1) p->d_recv = p->d_send;
+    else FO_CUDA(cudaMalloc(&p->d_recv, 2 * h.recv_elems));
+  }
 }
 
 static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst, int mode, bool signal) {
@@ -332,7 +337,8 @@ static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* ar_base) {
         if (cnt) {
           const int64_t so = (h.pool_base[h.rank] + h.send_start[(size_t)j * W + h.rank]) * h.BN;
           const int64_t ro = h.recv_off[(size_t)j * W + h.rank] * h.BN;
-          FO_CUDA(cudaMemcpyAsync(recv + 2 * ro, send + 2 * so, 2 * cnt * h.BN, cudaMemcpyDeviceToDevice, cs));
+          if (recv + 2 * ro != send + 2 * so)
+            FO_CUDA(cudaMemcpyAsync(recv + 2 * ro, send + 2 * so, 2 * cnt * h.BN, cudaMemcpyDeviceToDevice, cs));
         }
       }
       FO_NCCL(ncclGroupStart());
