@@ -1,0 +1,95 @@
+"""Alg. 1 predictor validation on one B200 (NEXT f1; the paper's E2 / fig:prediction
+analogue: mean prediction error 3.41% / 3.44%, searched
+partition >99% of the optimum).
+
+At one rank the collective moves no bytes, so each group's comm-stream work is
+the fused residual-add + RMSNorm of its row band (ROWBAND layout), whose cost
+is measured offline and folded into the curve (tuner.effective_curve, DESIGN.md
+R28).  For every candidate partition (all 2^(T-1) for T <= 8, a seeded sample
+otherwise) the predicted latency is compared with the measured fo_run latency;
+the predictive search's pick is compared with the measured optimum."""
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2504_19519_b200 as fo  # noqa: E402
+import synthetic  # noqa: E402
+from paper_2504_19519_b200 import tuner  # noqa: E402
+from tools.gemm_probe import timeit  # noqa: E402
+
+
+def candidates(T, limit, seed):
+    allc = []
+    for mask in range(1 << (T - 1)):
+        part, run = [], 0
+        for w in range(T):
+            run += 1
+            if w == T - 1 or (mask >> w) & 1:
+                part.append(run)
+                run = 0
+        allc.append(part)
+    if len(allc) <= limit:
+        return allc
+    rng = np.random.default_rng(seed)
+    pick = rng.choice(len(allc), size=limit, replace=False)
+    return [allc[i] for i in sorted(pick)] + [[1] * T, [T]]
+
+
+def main():
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    errs, ratios = [], []
+    for (M, N, K) in [(4096, 4096, 14336), (4096, 4096, 3584), (4096, 4096, 1792), (8192, 4096, 1024),
+                      (8192, 8192, 1024)]:
+        S = 64
+        tiles = (M // 256) * (N // 256)
+        T = -(-tiles // S)
+        A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.cell_seed(M, N, K), device="cuda")
+        res = synthetic.normal_bf16((M, N), 1.0, 1, device="cuda")
+        gam = synthetic.normal_bf16((N,), 1.0, 2, device="cuda")
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        out2 = torch.empty_like(out)
+        gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1)
+        dur = timeit(lambda: fo.gemm_stage(gplan, A, Bt, out), iters=10, flush=flush)
+        probe = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+                        ar_layout="rowband", post="add_rmsnorm")
+        norm_us = timeit(lambda: fo.post_stage(probe, out, out2, res, gam), iters=10, flush=flush)
+        curve = tuner.effective_curve(ctx.sample_curve("allreduce", [1 << s for s in range(18, 28)], iters=3),
+                                      norm_us / (M * N * 2))
+        rows = []
+        for G in candidates(T, 24, M + K):
+            plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+                           group_waves=G, ar_layout="rowband", post="add_rmsnorm")
+            pred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, curve)
+            meas = timeit(lambda: fo.run(ctx, plan, A, Bt, out, res, gam), iters=8, flush=flush)
+            rows.append((G, pred, meas))
+            errs.append(abs(meas - pred) / meas)
+        best_meas = min(r[2] for r in rows)
+        pick, pick_pred = fo.tune_search(dur, tiles, S, 256 * 256 * 2, curve)
+        pplan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+                        group_waves=list(pick), ar_layout="rowband", post="add_rmsnorm")
+        pick_meas = timeit(lambda: fo.run(ctx, pplan, A, Bt, out, res, gam), iters=8, flush=flush)
+        ratios.append(best_meas / pick_meas)
+        one = [r for r in rows if r[0] == [1] * T]
+        print(f"{M}x{N}x{K} T={T} gemm {dur:.1f} us, fused norm pass {norm_us:.1f} us, {len(rows)} partitions: "
+              f"mean |err| {100 * statistics.mean(abs(m - p) / m for _, p, m in rows):.2f}%, "
+              f"search picks {list(pick)} -> {pick_meas:.1f} us vs measured optimum {best_meas:.1f} us "
+              f"({100 * best_meas / pick_meas:.1f}%)"
+              + (f"; one-wave groups {one[0][2]:.1f} us" if one else ""), flush=True)
+        del A, Bt, res, out, out2
+        torch.cuda.empty_cache()
+    e = sorted(errs)
+    print(f"ALL: {len(errs)} (shape, partition) cases, prediction error mean {100 * statistics.mean(e):.2f}%, "
+          f"median {100 * e[len(e) // 2]:.2f}%, p90 {100 * e[int(0.9 * len(e))]:.2f}%, max {100 * e[-1]:.2f}%; "
+          f"searched / optimum: min {100 * min(ratios):.1f}%, mean {100 * statistics.mean(ratios):.1f}%")
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
