@@ -61,6 +61,8 @@ struct PostArgs {
   const int32_t* pos_of_tile;  // device
   const int32_t* src_row;      // device (A2A)
   float eps;
+  int smem_pad;                // dynamic smem (bytes, unused) requested per block: > the SM's
+                               // smem left beside a live GEMM CTA keeps the kernel off the GEMM's SMs
 };
 
 // Post-reorder of ONE wave group's data right after its collective (DESIGN.md
@@ -80,6 +82,7 @@ struct GroupPostArgs {
   int64_t sub_begin, sub_end;      // received subtokens of the group (A2A)
   const int32_t* recv_dst;         // device
   int grid_cap;                    // max blocks (0 = default)
+  int smem_pad;                    // as PostArgs::smem_pad
 };
 
 // Returns a cudaError_t-compatible code (0 = success).

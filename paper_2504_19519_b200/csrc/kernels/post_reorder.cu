@@ -366,21 +366,21 @@ cudaError_t launch_map(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int64_t chunks = a.N / 8;
   if (a.op == FO_POST_ADD_RMSNORM) {
     const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 16);
-    if (chunks <= 128) fo_post_rmsnorm_kernel<MAP, 1, 128><<<grid, 128, 0, stream>>>(a, lbn);
-    else if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 2, 128><<<grid, 128, 0, stream>>>(a, lbn);
-    else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 4, 128><<<grid, 128, 0, stream>>>(a, lbn);
-    else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 8, 128><<<grid, 128, 0, stream>>>(a, lbn);
-    else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8, 256><<<grid, 256, 0, stream>>>(a, lbn);
+    if (chunks <= 128) fo_post_rmsnorm_kernel<MAP, 1, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+    else if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 2, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+    else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 4, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+    else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 8, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+    else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8, 256><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
     else {
       const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)num_sms() * 8);
-      fo_post_rmsnorm_wide_kernel<MAP><<<g2, 256, 0, stream>>>(a, lbn);
+      fo_post_rmsnorm_wide_kernel<MAP><<<g2, 256, a.smem_pad, stream>>>(a, lbn);
     }
     return cudaGetLastError();
   }
   const int64_t units = a.rows * ((chunks + SEG_CHUNKS - 1) / SEG_CHUNKS);
   const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)num_sms() * 16);
-  if (a.op == FO_POST_ADD) fo_post_reorder_kernel<MAP, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn);
-  else fo_post_reorder_kernel<MAP, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn);
+  if (a.op == FO_POST_ADD) fo_post_reorder_kernel<MAP, FO_POST_ADD><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
+  else fo_post_reorder_kernel<MAP, FO_POST_NONE><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
   return cudaGetLastError();
 }
 
@@ -397,12 +397,12 @@ cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream) {
   const int cap = a.grid_cap > 0 ? a.grid_cap : num_sms() * 4;
   const int grid = (int)std::min<int64_t>((chunks + 255) / 256, cap);
   switch (a.map * 4 + a.op) {
-    case POSTMAP_SLOT * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_SLOT, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
-    case POSTMAP_SLOT * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_SLOT, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
-    case POSTMAP_RS * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_RS, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
-    case POSTMAP_RS * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_RS, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
-    case POSTMAP_A2A * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_A2A, FO_POST_NONE><<<grid, 256, 0, stream>>>(a, lbn); break;
-    case POSTMAP_A2A * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_A2A, FO_POST_ADD><<<grid, 256, 0, stream>>>(a, lbn); break;
+    case POSTMAP_SLOT * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_SLOT, FO_POST_NONE><<<grid, 256, a.smem_pad, stream>>>(a, lbn); break;
+    case POSTMAP_SLOT * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_SLOT, FO_POST_ADD><<<grid, 256, a.smem_pad, stream>>>(a, lbn); break;
+    case POSTMAP_RS * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_RS, FO_POST_NONE><<<grid, 256, a.smem_pad, stream>>>(a, lbn); break;
+    case POSTMAP_RS * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_RS, FO_POST_ADD><<<grid, 256, a.smem_pad, stream>>>(a, lbn); break;
+    case POSTMAP_A2A * 4 + FO_POST_NONE: fo_post_group_kernel<POSTMAP_A2A, FO_POST_NONE><<<grid, 256, a.smem_pad, stream>>>(a, lbn); break;
+    case POSTMAP_A2A * 4 + FO_POST_ADD: fo_post_group_kernel<POSTMAP_A2A, FO_POST_ADD><<<grid, 256, a.smem_pad, stream>>>(a, lbn); break;
     default: return cudaErrorInvalidValue;
   }
   count_launch();

@@ -246,6 +246,14 @@ static void stream_wait(fo_plan_s* p, WaitValue32Fn wait, cudaStream_t cs, int j
 // Per-group post-reorder (H11b) applies to the non-identity maps
 // when the fused op is elementwise per element (none / residual add); RMSNorm
 // needs whole rows and runs once after the last group.
+// Per-group post kernels run while the persistent GEMM still holds its S
+// workers.  Requesting more dynamic shared memory than a GEMM CTA leaves free
+// on its SM (>= 12 KB of 228 KB) keeps them on the SMs the GEMM left free —
+// the SM partition Alg. 1 assumes — instead of
+// co-residing with (and slowing) GEMM CTAs; once the GEMM's CTAs exit, every
+// SM takes them again.
+constexpr int kPartitionSmem = 24 * 1024;
+
 // AR ROWBAND with a fused op: every group is a band of complete rows, so the
 // op (residual add, RMSNorm over whole rows) can run on the band right after
 // the band's AllReduce.
@@ -283,6 +291,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
     a.Nt = h.Nt;
     a.h = h.h;
     a.eps = h.eps;
+    a.smem_pad = kPartitionSmem;
     FO_CUDA(launch_post(a, s));
     return;
   }
@@ -306,6 +315,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
   }
   a.recv_dst = p->d_recv_dst;
   a.grid_cap = 0;  // default: 4 blocks per SM
+  a.smem_pad = kPartitionSmem;
   FO_CUDA(launch_group_post(a, s));
 }
 

@@ -40,6 +40,9 @@ def candidates(T, limit, seed):
     return [allc[i] for i in sorted(pick)] + [[1] * T, [T]]
 
 
+MODE = sys.argv[1] if len(sys.argv) > 1 else "insitu"   # "insitu" | "standalone"
+
+
 def main():
     torch.cuda.set_device(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
@@ -60,8 +63,23 @@ def main():
         probe = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
                         ar_layout="rowband", post="add_rmsnorm")
         norm_us = timeit(lambda: fo.post_stage(probe, out, out2, res, gam), iters=10, flush=flush)
+        # in-situ offline stage (PAPER.md:498 (3), resource contention): the
+        # comm-stream work of a group measured inside an overlapped run, on the
+        # SMs the GEMM leaves free (group timestamps of the groups that overlap it)
+        insitu = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+                         group_waves=[1] * T, ar_layout="rowband", post="add_rmsnorm")
+        gts = torch.zeros(2 * T, dtype=torch.int64, device="cuda")
+        insitu.set_debug(None, gts)
+        costs = []
+        for _ in range(3):
+            fo.run(ctx, insitu, A, Bt, out, res, gam)
+            torch.cuda.synchronize()
+            g = gts.cpu().numpy()
+            costs += [(g[2 * j + 1] - g[2 * j]) / 1e3 for j in range(T - 1)]
+        band_bytes = (M // T) * N * 2
+        per_byte = statistics.median(costs) / band_bytes
         curve = tuner.effective_curve(ctx.sample_curve("allreduce", [1 << s for s in range(18, 28)], iters=3),
-                                      norm_us / (M * N * 2))
+                                      per_byte if MODE == "insitu" else norm_us / (M * N * 2))
         rows = []
         for G in candidates(T, 24, M + K):
             plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
@@ -77,7 +95,8 @@ def main():
         pick_meas = timeit(lambda: fo.run(ctx, pplan, A, Bt, out, res, gam), iters=8, flush=flush)
         ratios.append(best_meas / pick_meas)
         one = [r for r in rows if r[0] == [1] * T]
-        print(f"{M}x{N}x{K} T={T} gemm {dur:.1f} us, fused norm pass {norm_us:.1f} us, {len(rows)} partitions: "
+        print(f"[{MODE}] {M}x{N}x{K} T={T} gemm {dur:.1f} us, norm pass {norm_us:.1f} us standalone / "
+              f"{per_byte * M * N * 2:.1f} us in situ, {len(rows)} partitions: "
               f"mean |err| {100 * statistics.mean(abs(m - p) / m for _, p, m in rows):.2f}%, "
               f"search picks {list(pick)} -> {pick_meas:.1f} us vs measured optimum {best_meas:.1f} us "
               f"({100 * best_meas / pick_meas:.1f}%)"
@@ -85,7 +104,7 @@ def main():
         del A, Bt, res, out, out2
         torch.cuda.empty_cache()
     e = sorted(errs)
-    print(f"ALL: {len(errs)} (shape, partition) cases, prediction error mean {100 * statistics.mean(e):.2f}%, "
+    print(f"[{MODE}] ALL: {len(errs)} (shape, partition) cases, prediction error mean {100 * statistics.mean(e):.2f}%, "
           f"median {100 * e[len(e) // 2]:.2f}%, p90 {100 * e[int(0.9 * len(e))]:.2f}%, max {100 * e[-1]:.2f}%; "
           f"searched / optimum: min {100 * min(ratios):.1f}%, mean {100 * statistics.mean(ratios):.1f}%")
     ctx.close()
