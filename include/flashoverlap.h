@@ -256,8 +256,12 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      split into f K-slices run by otherwise idle workers of that
  *                      wave (needs R*f <= S); the slice-0 owner adds the fp32
  *                      partials in its epilogue and signals as usual; -1 — auto
- *                      (f = min(4, S/R) when 2R <= S).  Set before the first run. */
-typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2 } fo_option;
+ *                      (f = min(4, S/R) when 2R <= S).  Set before the first run.
+ *  FO_OPT_POST_SM_PARTITION 0 — per-group post kernels may co-reside with GEMM CTAs;
+ *                      1 — they request padding shared memory so they only run on
+ *                      the SMs the persistent GEMM leaves free (Alg. 1's SM split) */
+typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
+               FO_OPT_POST_SM_PARTITION = 3 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

@@ -247,11 +247,12 @@ static void stream_wait(fo_plan_s* p, WaitValue32Fn wait, cudaStream_t cs, int j
 // when the fused op is elementwise per element (none / residual add); RMSNorm
 // needs whole rows and runs once after the last group.
 // Per-group post kernels run while the persistent GEMM still holds its S
-// workers.  Requesting more dynamic shared memory than a GEMM CTA leaves free
-// on its SM (>= 12 KB of 228 KB) keeps them on the SMs the GEMM left free —
-// the SM partition Alg. 1 assumes — instead of
-// co-residing with (and slowing) GEMM CTAs; once the GEMM's CTAs exit, every
-// SM takes them again.
+// workers.  With FO_OPT_POST_SM_PARTITION they request more dynamic shared
+// memory than a GEMM CTA leaves free on its SM (>= 12 KB of 228 KB), which
+// keeps them on the SMs the GEMM left free — the SM partition Alg. 1 assumes
+// — instead of co-residing with GEMM CTAs.  Default off:
+// measured, the confined fused RMSNorm falls behind the GEMM
+// (profiles/r01_predictor_check.txt).
 constexpr int kPartitionSmem = 24 * 1024;
 
 // AR ROWBAND with a fused op: every group is a band of complete rows, so the
@@ -291,7 +292,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
     a.Nt = h.Nt;
     a.h = h.h;
     a.eps = h.eps;
-    a.smem_pad = kPartitionSmem;
+    a.smem_pad = p->post_sm_partition ? kPartitionSmem : 0;
     FO_CUDA(launch_post(a, s));
     return;
   }
@@ -315,7 +316,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
   }
   a.recv_dst = p->d_recv_dst;
   a.grid_cap = 0;  // default: 4 blocks per SM
-  a.smem_pad = kPartitionSmem;
+  a.smem_pad = p->post_sm_partition ? kPartitionSmem : 0;
   FO_CUDA(launch_group_post(a, s));
 }
 
@@ -793,6 +794,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_GROUP_POST:
         if (value < -1 || value > 1) fail(FO_ERR_INVALID_ARG, "group_post must be -1, 0 or 1");
         p->group_post = (int)value;
+        break;
+      case FO_OPT_POST_SM_PARTITION:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "post_sm_partition must be 0 or 1");
+        p->post_sm_partition = (int)value;
         break;
       case FO_OPT_TAIL_SPLIT:
         if (value < -1 || value > 16) fail(FO_ERR_INVALID_ARG, "tail_split must be -1..16");

@@ -150,3 +150,19 @@ def test_rowband_band_post_equals_single_post(ctx, post):
     g = o1.double().cpu().numpy()
     rms = np.sqrt(np.mean(want * want))
     assert np.max(np.abs(g - want) / np.maximum(np.abs(want), rms)) <= 1e-2
+
+
+def test_post_sm_partition_option_equal_results(ctx):
+    M, N, K, S = 2048, 1024, 512, 8
+    kw = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=S, swizzle=3, group_waves=[1, 1],
+              ar_layout="slot", post="add")
+    p_on, p_off = fo.Plan(**kw), fo.Plan(**kw)
+    p_on.set_option("post_sm_partition", 1)
+    A, Bt = synthetic.float_inputs(M, N, K, seed=31, device="cuda")
+    res = synthetic.normal_bf16((M, N), 1.0, 32, device="cuda")
+    o1 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    fo.run(ctx, p_on, A, Bt, o1, res)
+    fo.run(ctx, p_off, A, Bt, o2, res)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)

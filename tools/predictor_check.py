@@ -40,7 +40,10 @@ def candidates(T, limit, seed):
     return [allc[i] for i in sorted(pick)] + [[1] * T, [T]]
 
 
-MODE = sys.argv[1] if len(sys.argv) > 1 else "insitu"   # "insitu" | "standalone"
+MODE = sys.argv[1] if len(sys.argv) > 1 else "standalone"   # "standalone" | "insitu" (see note)
+# note: "insitu" divides each group's [wait released, post done] span by its
+# bytes; the span includes queueing behind earlier groups' posts, so it
+# overestimates the cost — kept only as a diagnostic
 
 
 def main():
