@@ -154,7 +154,7 @@ def test_rowband_band_post_equals_single_post(ctx, post):
 
 def test_post_sm_partition_option_equal_results(ctx):
     M, N, K, S = 2048, 1024, 512, 8
-    kw = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=S, swizzle=3, group_waves=[1, 1],
+    kw = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=S, swizzle=3, group_waves=[2, 3, 3],
               ar_layout="slot", post="add")
     p_on, p_off = fo.Plan(**kw), fo.Plan(**kw)
     p_on.set_option("post_sm_partition", 1)
