@@ -29,6 +29,27 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+# stdout must carry exactly one JSON line: NCCL's init banner ("NCCL version
+# ...", printed when NCCL_DEBUG=VERSION, e.g. set by the image) goes to stderr
+if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+    os.environ["NCCL_DEBUG"] = "WARN"
+
+
+class _StdoutToStderr:
+    """Route C-level stdout (NCCL/driver prints) to stderr inside the block."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 M_TOK, N_HID, K_FFN = 4096, 4096, 14336
 BM, BN = 256, 256   # tcgen05 cta_group::2 tile (CTA pair)
 
@@ -205,7 +226,8 @@ def main():
     # under torchrun (even at one process) the distributed plumbing is live
     use_dist = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
     if use_dist:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with _StdoutToStderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peak_src = load_peaks()
     sms = fo.device_sm_count(local)
     M, N, K = wl["M"], wl["N"], wl["K_loc"]
@@ -236,7 +258,8 @@ def main():
         uid = obj[0]
     else:
         uid = fo.unique_id()
-    ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
+    with _StdoutToStderr():
+        ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
 
     def barrier():
         if use_dist:
