@@ -209,3 +209,34 @@ def test_c2_bench_config_tp1_tail_split():
     trows = np.unique((tail_tiles // 16) * 256 + 17)
     _check_rows(out[torch.from_numpy(trows).cuda()], onum.gemm(A[trows], Bt))
     ctx.close()
+
+
+def test_c0_two_ranks_four_groups():
+    """configs[0]: M=N=256, K=512 split over 2 simulated ranks (K_loc=256),
+    AllReduce, 4 signal groups.  The tcgen05 M atom is 128, so 128x64 tiles
+    (R22): 8 tiles, S=2, T=4, groups (1,1,1,1).  Exact-integer regime,
+    bit-exact send buffers, counters and outputs for both ranks."""
+    from oracle import pipeline as opl
+    from oracle import plan as op
+
+    n, M, N, K = 2, 256, 256, 256
+    groups = [1, 1, 1, 1]
+    As, Bts = [], []
+    for r in range(n):
+        A, Bt = synthetic.exact_inputs(M, N, K, seed=synthetic.rank_seed(0, n, r), nnz_per_row=128)
+        As.append(A)
+        Bts.append(Bt)
+    oplan = op.make_plan(M, N, 128, 64, 2, groups, swizzle=2)
+    ores = opl.run_allreduce(As, Bts, oplan)
+    for r in range(n):
+        plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=128, tile_n=64, workers=2, swizzle=2,
+                       group_waves=groups, ar_layout="slot", rank=r, world=n)
+        send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, As[r].cuda(), Bts[r].cuda(), send)
+        torch.cuda.synchronize()
+        assert np.array_equal(send.double().cpu().numpy(), ores["send"][r])
+        assert plan.read_counters().tolist() == [2, 2, 2, 2]
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plan, torch.from_numpy(ores["recv"][r]).to(torch.bfloat16).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.double().cpu().numpy(), opl.plain_allreduce(As, Bts)[r])
