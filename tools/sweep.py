@@ -24,6 +24,7 @@ def main():
     sms = fo.device_sm_count(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    curve = ctx.sample_curve("allreduce", [1 << s for s in range(18, 28)], iters=3)  # 1-rank per-call cost
     print(f"{'M':>6} {'N=K':>6} {'tiles':>5} {'S':>3} {'T':>3} {'cublas_TF':>9} {'fo_TF':>7} {'frac':>5} "
           f"{'fo_run_us':>9} {'seq_us':>8} {'speedup':>7} layout groups")
     for M in (1024, 2048, 4096, 8192, 16384):
@@ -39,7 +40,7 @@ def main():
             T = -(-tiles // S)
             gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0)
             t_fo = timeit(lambda: fo.gemm_stage(gplan, A, Bt, C), iters=10, flush=flush)
-            groups = fo.tune_search(t_fo, tiles, S, 256 * 256 * 2, [(1 << 10, 1e6), (1 << 30, 1e6)])[0]
+            groups = fo.tune_search(t_fo, tiles, S, 256 * 256 * 2, curve)[0]
             plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
                            group_waves=list(groups), swizzle=0)
             t_ov = timeit(lambda: fo.run(ctx, plan, A, Bt, C), iters=10, flush=flush)
