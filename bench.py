@@ -240,8 +240,7 @@ def main():
         # achieving it; the SMs this frees are left to NCCL (R18)
         T_full = -(-tiles // (sms // cg))
         S = -(-tiles // T_full)
-    comm_sms = sms - cg * S
-    T = (tiles + S - 1) // S
+    comm_sms = sms - cg * S    # the NCCL CTA cap (SMs a quantisation-aware S leaves free)
 
     # ---- inputs (synthetic, seeded; SURVEY §8(d) recipe), resident in HBM
     import synthetic
@@ -313,35 +312,38 @@ def main():
             means = {k: t[i].item() for i, k in enumerate(fns)}
         return means
 
-    # ---- offline stage of Alg. 1 (untimed): GEMM duration at S, NCCL AR curve
-    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=0)
-    gemm_us, _ = timed(lambda: fo.gemm_stage(gplan, A, Bt, out), 5, 2)
-    # NCCL curve on the library's own communicator (CTA cap included); at one
-    # rank this is the fixed per-call cost of the degenerate collective
-    curve = ctx.sample_curve("allreduce", [1 << s for s in range(18, 27)], iters=5)
-    if args.groups:
-        groups = tuple(int(x) for x in args.groups.split(","))
-        pred = fo.tune_predict(groups, gemm_us, tiles, S, BM * BN * 2, curve)
-    else:
-        groups, pred = fo.tune_search(gemm_us, tiles, S, BM * BN * 2, curve)
-
-    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=list(groups),
-                   ar_layout="auto", swizzle=0, rank=rank, world=world)
-    # fused-op convention (R17, PAPER.md:394/671): the same layer followed by
-    # residual add + RMSNorm, fused into the (per-band) post-communication pass.
-    # Its groups are tuned with the fused op's measured cost folded into the
-    # comm-stream latency of every group (tuner.effective_curve).
+    # ---- offline + online stages of Alg. 1 (untimed, tuner.tune_layer): GEMM
+    # duration per candidate wave width S and layout, the NCCL curve on the
+    # library's communicator, Alg. 1 over the wave groups; the fused-op layer
+    # is tuned with its per-group fused op folded into the curve (R28)
     from paper_2504_19519_b200 import tuner as fot
+    if args.workers or args.groups:
+        T = (tiles + S - 1) // S
+        gplan0 = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=0)
+        gemm_us, _ = timed(lambda: fo.gemm_stage(gplan0, A, Bt, out), 5, 2)
+        curve = ctx.sample_curve("allreduce", [1 << s for s in range(18, 27)], iters=5)
+        groups = tuple(int(x) for x in args.groups.split(",")) if args.groups else \
+            fo.tune_search(gemm_us, tiles, S, BM * BN * 2, curve)[0]
+        pred = fo.tune_predict(groups, gemm_us, tiles, S, BM * BN * 2, curve)
+        spec = dict(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=0,
+                    group_waves=list(groups), ar_layout="auto")
+        nspec = dict(spec, post="add_rmsnorm")
+        pred_n = pred
+    else:
+        ch = fot.tune_layer(M, N, K, ctx, "allreduce", "none", tile_m=BM, tile_n=BN, device=local)
+        chn = fot.tune_layer(M, N, K, ctx, "allreduce", "add_rmsnorm", tile_m=BM, tile_n=BN, device=local)
+        S, groups, pred = ch.workers, tuple(ch.groups), ch.predicted_us
+        spec, nspec, pred_n = ch.spec(M, N, K, "allreduce"), chn.spec(M, N, K, "allreduce", "add_rmsnorm"), \
+            chn.predicted_us
+        T = (tiles + S - 1) // S
+    plan = fo.Plan(rank=rank, world=world, **spec)
+    # fused-op convention (R17, PAPER.md:394/671): the same layer followed by
+    # residual add + RMSNorm, fused into the (per-band) post-communication pass
+    nplan = fo.Plan(rank=rank, world=world, **nspec)
+    groups_n = nspec["group_waves"]
     resid = synthetic.normal_bf16((M, N), 1.0, 7, device="cuda")
     gamma = synthetic.normal_bf16((N,), 1.0, 8, device="cuda")
     out2 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    probe = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, ar_layout="rowband",
-                    swizzle=1, rank=rank, world=world, post="add_rmsnorm")
-    norm_us, _ = timed(lambda: fo.post_stage(probe, out, out2, resid, gamma), 5, 2)
-    ncurve = fot.effective_curve(curve, norm_us / (M * N * 2))
-    groups_n, pred_n = fo.tune_search(gemm_us, tiles, S, BM * BN * 2, ncurve)
-    nplan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=list(groups_n),
-                    ar_layout="auto", swizzle=0, rank=rank, world=world, post="add_rmsnorm")
     # the GEMM-only timing uses exactly the overlapped plan's execution order
     gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=plan.export_order())
 
@@ -408,7 +410,8 @@ def main():
             "ms_per_step": round(ov_us / 1e3, 4), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) weights)",
             "config": {**{k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective", "tile")},
-                       "workers": S, "comm_sms": comm_sms, "waves": T, "groups": list(groups),
+                       "workers": S, "comm_sms": sms - cg * S, "nccl_max_ctas": comm_sms if world > 1 else None,
+                       "waves": T, "groups": list(groups), "swizzle_order": "auto (DESIGN.md R25)",
                        "ar_layout": "rowband" if plan.info["ar_layout"] == 1 else "slot",
                        "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"tp{world}"},
             "speedup_vs_sequential": round(seq_us / ov_us, 4), "sequential_us": round(seq_us, 2),
@@ -417,7 +420,9 @@ def main():
             "alg1_predicted_us": round(pred, 2), "spot_check": spot,
             "fused_add_rmsnorm": {"overlapped_us": round(m["ov_norm"], 2), "sequential_us": round(m["seq_norm"], 2),
                                   "speedup": round(m["seq_norm"] / m["ov_norm"], 4), "groups": list(groups_n),
-                                  "alg1_predicted_us": round(pred_n, 2), "norm_pass_us": round(norm_us, 2),
+                                  "workers": nspec["workers"],
+                                  "layout": "rowband" if nplan.info["ar_layout"] == 1 else "slot",
+                                  "alg1_predicted_us": round(pred_n, 2),
                                   "note": "GEMM+AR+residual add+RMSNorm; overlapped runs the fused op per row band"},
             "roofline": {"bound": "tensor", "kernel": f"fo_gemm_tcgen05_kernel<{BN},{cg}>", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,

@@ -232,3 +232,114 @@ def effective_curve(curve: list, post_us_per_byte: float, post_fixed_us: float =
         t = b / (bw * 1e9) * 1e6 + post_fixed_us + post_us_per_byte * b
         out.append((b, b / (t * 1e-6) / 1e9))
     return out
+
+
+@dataclass
+class LayerChoice:
+    workers: int
+    swizzle: int
+    groups: list
+    layout: str          # "rowband" | "slot" (AllReduce) | "auto"
+    predicted_us: float
+    gemm_us: float
+    candidates: list     # (workers, layout, groups, predicted_us, gemm_us) of every candidate evaluated
+
+    def spec(self, M, N, K, coll, post="none", tile_m=TILE_M, tile_n=TILE_N) -> dict:
+        return dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=self.workers,
+                    swizzle=self.swizzle, group_waves=list(self.groups),
+                    ar_layout=self.layout if coll == "allreduce" else "auto", post=post)
+
+
+def candidate_workers(tiles: int, Nt: int, sms: int, coll: str, cg: int = 2) -> list:
+    """Offline stage (3) candidates for the wave width S (T is set
+    by the SMs the collective leaves): the fewest workers with the full GPU's
+    wave count, the full GPU, and (AllReduce) the widest S whose waves are whole
+    tile-rows (groups are then row bands: no reorder at all, H11a)."""
+    smax = sms // cg
+    cands = {default_workers(tiles, sms, cg), min(smax, tiles)}
+    if coll == "allreduce" and Nt <= smax:
+        cands.add((smax // Nt) * Nt)
+    return sorted(c for c in cands if c >= 1)
+
+
+def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_n=TILE_N, device=0,
+               sizes=None, iters=8, min_comm_sms=16) -> LayerChoice:
+    """Joint choice of S (wave width), layout and wave groups for one layer
+    (AllReduce / ReduceScatter; world from the context).
+
+    For each candidate S and layout: measure the GEMM in that plan's execution
+    order (offline stage (1)), use the collective's curve sampled on the
+    context's communicator (stage (2)), fold the per-group post work into it
+    (R28: the reorder of a slot layout and/or the fused op), run Alg. 1, and
+    add any post pass that cannot run per group (RMSNorm on a slot layout).
+    The lowest prediction wins."""
+    import torch
+
+    from . import post_stage
+
+    sms = device_sm_count(device)
+    Mt, Nt = M // tile_m, N // tile_n
+    tiles = Mt * Nt
+    world = ctx.world
+    curve = ctx.sample_curve(coll, sizes or [1 << s for s in range(18, 28)], iters=3)
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    Bt = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    out_rows = M if coll == "allreduce" else M // world
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    res = torch.randn(out_rows, N, device="cuda").to(torch.bfloat16)
+    gam = torch.randn(N, device="cuda").to(torch.bfloat16)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def timeit(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(iters):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            tot += s.elapsed_time(e) * 1e3
+        return tot / iters
+
+    def post_us(layout, op):
+        """Full-output post pass of `layout` with `op`, measured standalone."""
+        if op == "none" and layout == "rowband":
+            return 0.0
+        pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tile_m, tile_n=tile_n, workers=min(tiles, sms // 2),
+                  swizzle=1, ar_layout=layout if coll == "allreduce" else "auto", post=op, rank=ctx.rank,
+                  world=world)
+        recv = torch.zeros(pl.info["recv_elems"], dtype=torch.bfloat16, device="cuda")
+        o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+        return timeit(lambda: post_stage(pl, recv, o, res, gam))
+
+    out_bytes = out_rows * N * 2
+    layouts = ("rowband", "slot") if coll == "allreduce" else ("auto",)
+    evaluated = []
+    cg = tile_m // 128
+    cands = candidate_workers(tiles, Nt, sms, coll, cg)
+    if world > 1:
+        # the collective's kernels need SMs the persistent GEMM leaves free
+        # (Alg. 1 line 3); without them nothing overlaps
+        cands = [c for c in cands if sms - cg * c >= min_comm_sms] or [min(cands)]
+    for S in cands:
+        T = -(-tiles // S)
+        for layout in layouts:
+            if layout == "rowband" and S % Nt:
+                continue          # waves of whole tile-rows only
+            swz = 1 if layout == "rowband" else 0
+            probe = Plan(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
+                         group_waves=[T], ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world)
+            gp = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S,
+                      tile_order=probe.export_order())
+            dur = timeit(lambda: gemm_stage(gp, A, Bt, out))
+            per_group_op = post if (layout == "rowband" or post != "add_rmsnorm") else "none"
+            per_group = post_us(layout if layout != "auto" else "slot", per_group_op) / out_bytes
+            tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
+            G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, effective_curve(curve, per_group))
+            evaluated.append((S, layout, list(G), pred + tail, dur, swz))
+    best = min(evaluated, key=lambda e: e[3])
+    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], [e[:5] for e in evaluated])

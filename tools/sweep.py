@@ -13,6 +13,7 @@ import torch  # noqa: E402
 
 import paper_2504_19519_b200 as fo  # noqa: E402
 import synthetic  # noqa: E402
+from paper_2504_19519_b200 import tuner  # noqa: E402
 from tools.gemm_probe import timeit  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -24,7 +25,6 @@ def main():
     sms = fo.device_sm_count(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    curve = ctx.sample_curve("allreduce", [1 << s for s in range(18, 28)], iters=3)  # 1-rank per-call cost
     print(f"{'M':>6} {'N=K':>6} {'tiles':>5} {'S':>3} {'T':>3} {'cublas_TF':>9} {'fo_TF':>7} {'frac':>5} "
           f"{'fo_run_us':>9} {'seq_us':>8} {'speedup':>7} layout groups")
     for M in (1024, 2048, 4096, 8192, 16384):
@@ -35,14 +35,12 @@ def main():
             fl = 2.0 * M * N * K
             t_cb = timeit(lambda: torch.matmul(A, Bt.t(), out=C), iters=10, flush=flush)
             tiles = (M // 256) * (N // 256)
-            T_full = -(-tiles // (sms // 2))
-            S = -(-tiles // T_full)
-            T = -(-tiles // S)
-            gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0)
+            ch = tuner.tune_layer(M, N, K, ctx, "allreduce", "none")
+            S, T, groups = ch.workers, -(-tiles // ch.workers), ch.groups
+            plan = fo.Plan(**ch.spec(M, N, K, "allreduce"))
+            gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
+                            tile_order=plan.export_order())
             t_fo = timeit(lambda: fo.gemm_stage(gplan, A, Bt, C), iters=10, flush=flush)
-            groups = fo.tune_search(t_fo, tiles, S, 256 * 256 * 2, curve)[0]
-            plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
-                           group_waves=list(groups), swizzle=0)
             t_ov = timeit(lambda: fo.run(ctx, plan, A, Bt, C), iters=10, flush=flush)
             t_sq = timeit(lambda: fo.run_sequential(ctx, plan, A, Bt, C), iters=10, flush=flush)
             tf = fl / t_fo / 1e6
