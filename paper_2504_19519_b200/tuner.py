@@ -263,7 +263,7 @@ def candidate_workers(tiles: int, Nt: int, sms: int, coll: str, cg: int = 2) -> 
 
 
 def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_n=TILE_N, device=0,
-               sizes=None, iters=8, min_comm_sms=16) -> LayerChoice:
+               sizes=None, iters=8, min_comm_sms=16, verify=2) -> LayerChoice:
     """Joint choice of S (wave width), layout and wave groups for one layer
     (AllReduce / ReduceScatter; world from the context).
 
@@ -272,7 +272,11 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     context's communicator (stage (2)), fold the per-group post work into it
     (R28: the reorder of a slot layout and/or the fused op), run Alg. 1, and
     add any post pass that cannot run per group (RMSNorm on a slot layout).
-    The lowest prediction wins."""
+    The `verify` best predictions are then run for real (fo_run) and the
+    fastest wins: the predictor does not model the contention between the
+    GEMM and per-group post kernels.  At world > 1 every decision is rank 0's
+    (broadcast over the default process group) so all ranks build the same
+    plan."""
     import torch
 
     from . import post_stage
@@ -341,5 +345,32 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
             tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
             G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, effective_curve(curve, per_group))
             evaluated.append((S, layout, list(G), pred + tail, dur, swz))
-    best = min(evaluated, key=lambda e: e[3])
-    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], [e[:5] for e in evaluated])
+    import torch.distributed as dist
+
+    def agree(obj):
+        if world > 1 and dist.is_initialized():
+            box = [obj]
+            dist.broadcast_object_list(box, src=0)
+            return box[0]
+        return obj
+
+    evaluated = agree(sorted(evaluated, key=lambda e: e[3]))
+    from . import run as fo_run
+
+    measured = []
+    for (S, layout, G, pred, dur, swz) in evaluated[:max(1, verify)]:
+        spec = dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
+                    group_waves=G, ar_layout=layout if layout != "auto" else "auto", post=post)
+        pl = Plan(rank=ctx.rank, world=world, **spec)
+        o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+        args = (res, gam) if post != "none" else (None, None)
+        t = timeit(lambda: fo_run(ctx, pl, A, Bt, o, *args))
+        if world > 1 and dist.is_initialized():
+            tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = tt.item()
+        measured.append(t)
+    k = min(range(len(measured)), key=lambda i: measured[i])
+    best = evaluated[k]
+    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4],
+                       [e[:5] + ((measured[i],) if i < len(measured) else ()) for i, e in enumerate(evaluated)])
