@@ -101,3 +101,28 @@ def test_time_collective_world1():
     curve = ctx.sample_curve("allreduce", [1 << 16, 1 << 20], iters=2)
     assert len(curve) == 2 and all(b > 0 for _, b in curve)
     ctx.close()
+
+
+def test_tune_layer_world1_returns_a_valid_plan():
+    from paper_2504_19519_b200 import build
+    from paper_2504_19519_b200 import tuner
+
+    build.build()
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    M, N, K = 2048, 2048, 1024
+    for post in ("none", "add_rmsnorm"):
+        ch = tuner.tune_layer(M, N, K, ctx, "allreduce", post, iters=3, sizes=[1 << 18, 1 << 22])
+        tiles = (M // 256) * (N // 256)
+        assert sum(ch.groups) == -(-tiles // ch.workers)
+        assert len(ch.candidates) >= 2 and all(len(c) >= 5 for c in ch.candidates)
+        plan = fo.Plan(**ch.spec(M, N, K, "allreduce", post))
+        A, Bt = synthetic.float_inputs(M, N, K, seed=3, device="cuda")
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        res = synthetic.normal_bf16((M, N), 1.0, 4, device="cuda")
+        gam = synthetic.normal_bf16((N,), 1.0, 5, device="cuda")
+        fo.run(ctx, plan, A, Bt, out, *((res, gam) if post != "none" else ()))
+        torch.cuda.synchronize()
+    ch = tuner.tune_layer(M, N, K, ctx, "reducescatter", "none", iters=3, sizes=[1 << 18, 1 << 22])
+    assert ch.layout == "auto"
+    ctx.close()
