@@ -259,9 +259,17 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      (f = min(4, S/R) when 2R <= S).  Set before the first run.
  *  FO_OPT_POST_SM_PARTITION 0 — per-group post kernels may co-reside with GEMM CTAs;
  *                      1 — they request padding shared memory so they only run on
- *                      the SMs the persistent GEMM leaves free (Alg. 1's SM split) */
+ *                      the SMs the persistent GEMM leaves free (Alg. 1's SM split)
+ *  FO_OPT_HOST_PIPELINE 3 — bit 0: fo_run_host copies a host A in ~16 chunks of
+ *                      whole tile-rows on its own stream, each chunk released to
+ *                      the GEMM by a stream write the TMA producer waits on (the
+ *                      GEMM starts on the first chunk); bit 1: (AR ROWBAND) each
+ *                      group's rows are copied to the host right after its
+ *                      collective; 0 — whole-buffer copies before / after
+ *  FO_OPT_HOST_CHUNKS  8 — target number of A chunks (whole tile-rows each) for
+ *                      bit 0 above; set before the plan's first fo_run_host */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
-               FO_OPT_POST_SM_PARTITION = 3 } fo_option;
+               FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

@@ -39,6 +39,12 @@ struct GemmArgs {
   int split;                   // K slices per tail tile (1 = no split)
   float* workspace;            // fp32 partials [(tiles - tail_pos) * (split - 1)][TM][BN]
   uint32_t* flags;             // [(tiles - tail_pos) * CG] partial-ready counts (reset with the counters)
+  // ---- host-staged A (fo_run_host pipelining): A arrives in chunks of
+  // a_chunk_rows tile-rows; the producer loads a tile's A only once
+  // a_ready[ti / a_chunk_rows] has reached a_epoch (null: A is resident)
+  const uint32_t* a_ready;
+  uint32_t a_epoch;
+  int a_chunk_rows;
 };
 
 enum PostMode : int {

@@ -350,10 +350,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int ready_chunk = -1;
       for (int u = worker; u < p.units; u += nworkers) {
         const Unit un = decode_unit(p, u, KB);
         const int t = p.order[un.pos];
         const int ti = t / p.Nt, tj = t - ti * p.Nt;
+        if (p.a_ready && ti / p.a_chunk_rows != ready_chunk) {
+          // host-staged A: wait until this tile-row's chunk has landed (the
+          // copy stream's release write follows the chunk's H2D copy), then
+          // order the generic-proxy acquire before the async-proxy TMA reads
+          ready_chunk = ti / p.a_chunk_rows;
+          while ((int32_t)(ld_acquire(p.a_ready + ready_chunk) - p.a_epoch) < 0) __nanosleep(128);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         const int arow = ti * TM + (int)crank * BM;
         const int brow = tj * BN + (int)crank * C::B_ROWS;
         for (int kb = un.kb0; kb < un.kb1; ++kb) {

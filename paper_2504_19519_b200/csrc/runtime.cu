@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <climits>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -29,6 +31,10 @@ struct fo_ctx_s {
   cudaStream_t post_stream = nullptr;  // per-group post-reorder, chained to each group's collective
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_post_join = nullptr;
   std::vector<cudaEvent_t> ev_group;   // one per wave group (grown on demand)
+  // fo_run_host: chunked H2D of A and per-group D2H of out on their own streams
+  cudaStream_t h2d_stream[2] = {nullptr, nullptr}, d2h_stream = nullptr;
+  cudaEvent_t ev_h2d_fork = nullptr, ev_h2d_join[2] = {nullptr, nullptr}, ev_d2h_join = nullptr;
+  std::vector<cudaEvent_t> ev_d2h;     // group j's output final (grown on demand)
 };
 
 namespace fo {
@@ -46,6 +52,20 @@ namespace fo {
   } while (0)
 
 typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static WriteValue32Fn write_value_fn() {
+  static WriteValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(ptr);
+  });
+  return fn;
+}
 
 static WaitValue32Fn wait_value_fn() {
   static WaitValue32Fn fn = nullptr;
@@ -78,7 +98,7 @@ void release_device(fo_plan_s* p) {
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
                     p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma,
-                    (void*)p->d_ws})
+                    (void*)p->d_ws, (void*)p->d_a_ready})
     if (ptr) cudaFree(ptr);
   cudaSetDevice(cur);
   p->device = -1;
@@ -169,6 +189,11 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   a.split = p->split;
   a.workspace = p->d_ws;
   a.flags = p->d_flags;
+  if (p->a_staged_run) {
+    a.a_ready = p->d_a_ready;
+    a.a_epoch = p->a_epoch;
+    a.a_chunk_rows = p->a_chunk_rows;
+  }
   return a;
 }
 
@@ -427,6 +452,13 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       FO_CUDA(cudaEventCreateWithFlags(&c->ev_post_join, cudaEventDisableTiming));
+      for (int i = 0; i < 2; ++i) {
+        FO_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream[i], cudaStreamNonBlocking));
+        FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_join[i], cudaEventDisableTiming));
+      }
+      FO_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+      FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_fork, cudaEventDisableTiming));
+      FO_CUDA(cudaEventCreateWithFlags(&c->ev_d2h_join, cudaEventDisableTiming));
     } catch (...) {
       if (c->comm) ncclCommDestroy(c->comm);
       delete c;
@@ -449,8 +481,46 @@ fo_status fo_ctx_destroy(fo_ctx c) {
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_post_join) cudaEventDestroy(c->ev_post_join);
     for (cudaEvent_t e : c->ev_group) cudaEventDestroy(e);
+    for (cudaStream_t st : {c->h2d_stream[0], c->h2d_stream[1], c->d2h_stream})
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
+    for (cudaEvent_t e : {c->ev_h2d_fork, c->ev_h2d_join[0], c->ev_h2d_join[1], c->ev_d2h_join})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_d2h) cudaEventDestroy(e);
     delete c;
   });
+}
+
+// Rows [r0, r1) of the output that are final once group j is done — defined
+// when every group is a band of whole tile-rows written row-major in place
+// (AR ROWBAND, no-comm with band-aligned groups); false otherwise.
+static bool group_out_rows(const PlanHost& h, int j, int64_t* r0, int64_t* r1) {
+  if (!(h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND)) return false;
+  if ((int)h.band_rows.size() < 2 * h.P) return false;
+  *r0 = (int64_t)h.band_rows[2 * j] * h.BM;
+  *r1 = (int64_t)h.band_rows[2 * j + 1] * h.BM;
+  return true;
+}
+
+// fo_run_host: copy group j's final output rows to the host as soon as the
+// group is done (stream `done` = where its last op ran), overlapping the
+// device->host transfer with the remaining groups.
+static void group_d2h(fo_ctx c, fo_plan p, int j, const void* out, cudaStream_t done) {
+  const PlanHost& h = p->host;
+  int64_t r0 = 0, r1 = 0;
+  if (!group_out_rows(h, j, &r0, &r1)) return;
+  while ((int)c->ev_d2h.size() <= j) {
+    cudaEvent_t e;
+    FO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ev_d2h.push_back(e);
+  }
+  FO_CUDA(cudaEventRecord(c->ev_d2h[j], done));
+  FO_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->ev_d2h[j], 0));
+  const size_t off = 2 * (size_t)(r0 * h.N), bytes = 2 * (size_t)((r1 - r0) * h.N);
+  FO_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(p->d2h_host) + off, reinterpret_cast<const char*>(out) + off,
+                          bytes, cudaMemcpyDeviceToHost, c->d2h_stream));
 }
 
 fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
@@ -495,11 +565,13 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
           run_group_post(p, j, post_src, out, residual, gamma, ps);
         }
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j + 1, ps));
+        if (p->d2h_host) group_d2h(c, p, j, out, ps);
       }
     } else {
       // no communication: the comm stream only has to see the GEMM finish
       for (int j = 0; j < h.P; ++j) {
         stream_wait(p, wait, c->comm_stream, j);
+        if (p->d2h_host) group_d2h(c, p, j, out, c->comm_stream);
       }
     }
     // 5. post-communication reorder (+ fused op) when not done per group
@@ -512,6 +584,10 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     if (gpost && h.coll != FO_NOCOMM) {
       FO_CUDA(cudaEventRecord(c->ev_post_join, c->post_stream));
       FO_CUDA(cudaStreamWaitEvent(s, c->ev_post_join, 0));
+    }
+    if (p->d2h_host) {
+      FO_CUDA(cudaEventRecord(c->ev_d2h_join, c->d2h_stream));
+      FO_CUDA(cudaStreamWaitEvent(s, c->ev_d2h_join, 0));
     }
   });
 }
@@ -526,8 +602,35 @@ static bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Chunking of a host-staged A: ~16 chunks of whole tile-rows, copied in the
+// order the tile order first needs them.
+static void plan_a_chunks(fo_plan p) {
+  const PlanHost& h = p->host;
+  if (p->a_chunks) return;
+  p->a_chunk_rows = (int)((h.Mt + p->a_chunk_target - 1) / p->a_chunk_target);
+  p->a_chunks = (int)((h.Mt + p->a_chunk_rows - 1) / p->a_chunk_rows);
+  std::vector<int64_t> first(p->a_chunks, INT64_MAX);
+  for (int64_t pos = 0; pos < h.tiles; ++pos) {
+    const int ch = (int)((h.order[pos] / h.Nt) / p->a_chunk_rows);
+    first[ch] = std::min(first[ch], pos);
+  }
+  p->a_chunk_order.resize(p->a_chunks);
+  for (int i = 0; i < p->a_chunks; ++i) p->a_chunk_order[i] = i;
+  std::stable_sort(p->a_chunk_order.begin(), p->a_chunk_order.end(),
+                   [&](int x, int y) { return first[x] < first[y]; });
+  FO_CUDA(cudaMalloc(&p->d_a_ready, sizeof(uint32_t) * p->a_chunks));
+  FO_CUDA(cudaMemset(p->d_a_ready, 0, sizeof(uint32_t) * p->a_chunks));
+}
+
 fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
                       const void* gamma, void* stream) {
+  struct Transient {  // the per-call pipelining state never outlives the call
+    fo_plan p;
+    ~Transient() {
+      p->a_staged_run = false;
+      p->d2h_host = nullptr;
+    }
+  };
   return guard([&] {
     if (!c || !p || !A || !Bt || !out) fail(FO_ERR_INVALID_ARG, "null argument");
     ensure_device(p);
@@ -544,16 +647,62 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
       FO_CUDA(cudaMemcpyAsync(buf, src, bytes, cudaMemcpyHostToDevice, s));
       return buf;
     };
-    const void* dA = stage(A, p->h_A, a_bytes);
+    Transient guard_state{p};
+    WriteValue32Fn write = write_value_fn();
+    const bool a_host = !is_device_ptr(A);
+    // pipelined A: chunked copies on the H2D stream, each released to the GEMM
+    // producer by a stream write of this run's epoch (PAPER.md:368's
+    // signal/wait, applied to the input side); needs K-major A
+    const bool pipe_a = a_host && (p->host_pipeline & 1) && write && !(h.mn_major & 1);
+    const void* dA = nullptr;
+    if (pipe_a) {
+      plan_a_chunks(p);
+      if (!p->h_A) FO_CUDA(cudaMalloc(&p->h_A, a_bytes));
+      ++p->a_epoch;
+      // the copies may overwrite the staging only after the work already on
+      // `s` (the previous run's GEMM reads it); they are enqueued BEFORE the
+      // GEMM that waits on them, so no hardware-queue aliasing can order the
+      // GEMM ahead of the copies it waits for
+      FO_CUDA(cudaEventRecord(c->ev_h2d_fork, s));
+      for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamWaitEvent(c->h2d_stream[i], c->ev_h2d_fork, 0));
+      // chunks alternate between two copy streams so one chunk's release
+      // write never leaves the copy engine idle before the next chunk
+      const size_t row_bytes = 2 * (size_t)h.K;
+      for (size_t i = 0; i < p->a_chunk_order.size(); ++i) {
+        const int ch = p->a_chunk_order[i];
+        cudaStream_t cs = c->h2d_stream[i & 1];
+        const int64_t r0 = (int64_t)ch * p->a_chunk_rows * h.BM;
+        const int64_t r1 = std::min<int64_t>(h.M, r0 + (int64_t)p->a_chunk_rows * h.BM);
+        FO_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(p->h_A) + r0 * row_bytes,
+                                reinterpret_cast<const char*>(A) + r0 * row_bytes, (r1 - r0) * row_bytes,
+                                cudaMemcpyHostToDevice, cs));
+        CUresult r = write(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(p->d_a_ready + ch),
+                           p->a_epoch, 0);
+        if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+      }
+      for (int i = 0; i < 2; ++i) FO_CUDA(cudaEventRecord(c->ev_h2d_join[i], c->h2d_stream[i]));
+      p->a_staged_run = true;
+      dA = p->h_A;
+    } else {
+      dA = stage(A, p->h_A, a_bytes);
+    }
     const void* dB = stage(Bt, p->h_Bt, b_bytes);
     const void* dR = stage(residual, p->h_res, o_bytes);
     const void* dG = stage(gamma, p->h_gamma, 2 * (size_t)h.N);
     const bool out_dev = is_device_ptr(out);
     if (!out_dev && !p->h_out) FO_CUDA(cudaMalloc(&p->h_out, o_bytes));
     void* dO = out_dev ? out : p->h_out;
+    int64_t r0 = 0, r1 = 0;
+    // per-group D2H only when each group's rows are final after its own
+    // stream work (a post pass deferred to the end would rewrite them)
+    const bool pipe_out = !out_dev && (p->host_pipeline & 2) && group_out_rows(h, 0, &r0, &r1) &&
+                          (h.post == FO_POST_NONE || use_group_post(p));
+    if (pipe_out) p->d2h_host = out;
     fo_status st = fo_run(c, p, dA, dB, dO, dR, dG, stream);
     if (st != FO_OK) throw Error(st, fo_last_error());
-    if (!out_dev) FO_CUDA(cudaMemcpyAsync(out, dO, o_bytes, cudaMemcpyDeviceToHost, s));
+    if (pipe_a)
+      for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamWaitEvent(s, c->ev_h2d_join[i], 0));
+    if (!out_dev && !pipe_out) FO_CUDA(cudaMemcpyAsync(out, dO, o_bytes, cudaMemcpyDeviceToHost, s));
   });
 }
 
@@ -807,6 +956,15 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_WAIT_KERNEL:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "wait_kernel must be 0 or 1");
         p->wait_kernel = (int)value;
+        break;
+      case FO_OPT_HOST_CHUNKS:
+        if (value < 1 || value > 4096) fail(FO_ERR_INVALID_ARG, "host_chunks must be 1..4096");
+        if (p->a_chunks) fail(FO_ERR_STATE, "host_chunks must be set before the first fo_run_host");
+        p->a_chunk_target = (int)value;
+        break;
+      case FO_OPT_HOST_PIPELINE:
+        if (value < 0 || value > 3) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..3");
+        p->host_pipeline = (int)value;
         break;
       default:
         fail(FO_ERR_INVALID_ARG, "unknown option %d", option);

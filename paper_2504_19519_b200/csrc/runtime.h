@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "plan.h"
 
@@ -26,6 +27,17 @@ struct fo_plan_s {
   void* h_out = nullptr;
   void* h_res = nullptr;
   void* h_gamma = nullptr;
+  // ---- fo_run_host pipelining (FO_OPT_HOST_PIPELINE): A copied in chunks of
+  // a_chunk_rows tile-rows, each followed by a release write of the run's
+  // epoch into d_a_ready[chunk]; the GEMM producer waits per tile-row
+  int host_pipeline = 3;                          // bit 0: chunked A, bit 1: per-group D2H
+  uint32_t* d_a_ready = nullptr;
+  uint32_t a_epoch = 0;
+  int a_chunk_target = 8;                         // FO_OPT_HOST_CHUNKS
+  int a_chunk_rows = 0, a_chunks = 0;
+  std::vector<int> a_chunk_order;                 // chunks in order of first use
+  bool a_staged_run = false;                      // transient: this fo_run's GEMM waits on d_a_ready
+  void* d2h_host = nullptr;                       // transient: per-group D2H of out (AR ROWBAND) to here
   // ---- debug / evidence hooks (fo_plan_set_debug)
   unsigned long long* trace_tile_ts = nullptr;   // device [tiles]
   unsigned long long* trace_group_ts = nullptr;  // device [2P]: wait released, group done

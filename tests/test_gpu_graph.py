@@ -126,3 +126,47 @@ def test_tune_layer_world1_returns_a_valid_plan():
     ch = tuner.tune_layer(M, N, K, ctx, "reducescatter", "none", iters=3, sizes=[1 << 18, 1 << 22])
     assert ch.layout == "auto"
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["rowband", "rowband_norm", "slot", "rs", "nocomm", "ragged"])
+def test_run_host_pipelined_matches_device_run(case):
+    """FO_OPT_HOST_PIPELINE: A copied in tile-row chunks the GEMM producer
+    waits on, per-group D2H of ROWBAND output — bit-identical to fo_run on
+    device operands, over repeated calls with fresh A each time (a stale chunk
+    or a missed release shows up as a mismatch), pinned and pageable."""
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    M, N, K = (2304, 1024, 1024) if case == "ragged" else (4096, 1024, 1024)
+    coll = {"rs": "reducescatter", "nocomm": "nocomm"}.get(case, "allreduce")
+    post = "add_rmsnorm" if case == "rowband_norm" else "none"
+    layout = "slot" if case == "slot" else ("rowband" if coll == "allreduce" else "auto")
+    Nt = N // 256
+    S = 8 if case != "ragged" else 12
+    tiles = (M // 256) * Nt
+    T = -(-tiles // S)
+    plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
+                   group_waves=[1] * T if T <= 8 else [2] * (T // 2) + [1] * (T % 2),
+                   ar_layout=layout if coll == "allreduce" else "auto", swizzle=1, post=post)
+    res = synthetic.normal_bf16((M, N), 1.0, 6)
+    gam = synthetic.normal_bf16((N,), 1.0, 7)
+    Bt_d = synthetic.float_inputs(M, N, K, seed=9)[1].cuda()
+    extra_d = (res.cuda(), gam.cuda()) if post != "none" else ()
+    extra_h = (res.pin_memory(), gam.cuda()) if post != "none" else ()
+    for it, pinned in enumerate([True, True, False]):
+        A = synthetic.float_inputs(M, N, K, seed=20 + it)[0]
+        out_d = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        fo.run(ctx, plan, A.cuda(), Bt_d, out_d, *extra_d)
+        torch.cuda.synchronize()
+        for pipe in (3, 1, 2, 0):
+            plan.set_option("host_pipeline", pipe)
+            out_h = torch.full((M, N), float("nan"), dtype=torch.bfloat16)
+            A_h = A.clone()
+            if pinned:
+                out_h, A_h = out_h.pin_memory(), A_h.pin_memory()
+            fo.run_host(ctx, plan, A_h, Bt_d, out_h, *extra_h)
+            torch.cuda.synchronize()
+            assert torch.equal(out_h, out_d.cpu()), (case, it, pipe)
+    ctx.close()
