@@ -126,6 +126,65 @@ def random_row_dst(M: int, n: int, seed: int) -> np.ndarray:
     return rng.integers(0, n, size=M).astype(np.int32)
 
 
+def moe_topk(tokens: int, n_ranks: int, topk: int, seed: int, skew: float = 0.0, pad: int = 1) -> dict:
+    """Mixtral-style top-k routing with one expert per rank (expert e on rank
+    e; BASELINE.json configs[3], EP = number of experts) — the inputs of the
+    MoE combine that follows the expert GEMM + All-to-All (R31).
+
+    Tokens are spread evenly over the ranks (token t lives on rank t // (tokens
+    // n_ranks)).  Router logits ~ N(0,1) from `seed`, plus `skew` * (-log(e+1))
+    for expert e (skew > 0: a Zipf-like preference for low experts -> expert
+    load imbalance).  Each token picks its top-k experts; its
+    combine weights are the softmax over those k logits (fp32).
+
+    Returns dict:
+      top     [tokens, k] int   expert ids (descending logit)
+      weight  [tokens, k] f32   combine weights
+      row_token[e]  int64 [M_e] global token of each row expert e computes,
+                                rows sorted by (source rank, token id) as the
+                                dispatch All-to-All delivers them; with pad > 1
+                                M_e is rounded up to a multiple of pad by rows
+                                of token -1 (zero activations, kept on rank e)
+      row_dst[e]    int32 [M_e] source rank of each row (= the A2A destination)
+      combine_idx[r] int32 [tokens/n, k]: for rank r's local token l and slot i,
+                                the row of r's A2A output holding expert
+                                top[t, i]'s result (A2A output order: source
+                                expert ascending, then source row ascending)"""
+    g = _gen(seed)
+    logits = torch.randn(tokens, n_ranks, generator=g, dtype=torch.float64)
+    if skew:
+        logits = logits - skew * torch.log(torch.arange(1, n_ranks + 1, dtype=torch.float64))[None, :]
+    top_l, top = logits.topk(topk, dim=1)
+    weight = torch.softmax(top_l, dim=1).to(torch.float32).numpy()
+    top = top.numpy()
+    per_rank = tokens // n_ranks
+    row_token, row_dst = [], []
+    for e in range(n_ranks):
+        toks = np.flatnonzero((top == e).any(axis=1))          # ascending token id = (source, token) order
+        npad = (-len(toks)) % pad
+        row_token.append(np.concatenate([toks, np.full(npad, -1)]).astype(np.int64))
+        row_dst.append(np.concatenate([toks // per_rank, np.full(npad, e)]).astype(np.int32))
+    combine_idx = []
+    for r in range(n_ranks):
+        # rank r's A2A output: for each expert e ascending, the rows of e whose
+        # destination is r, in e's row order
+        base, pos = 0, {}
+        for e in range(n_ranks):
+            mine = row_token[e][row_dst[e] == r]
+            for q, t in enumerate(mine):
+                if t >= 0:
+                    pos[(int(t), e)] = base + q
+            base += len(mine)
+        idx = np.empty((per_rank, topk), np.int32)
+        for l in range(per_rank):
+            t = r * per_rank + l
+            for i in range(topk):
+                idx[l, i] = pos[(t, int(top[t, i]))]
+        combine_idx.append(idx)
+    return {"top": top, "weight": weight, "row_token": row_token, "row_dst": row_dst,
+            "combine_idx": combine_idx}
+
+
 def moe_routing(tokens: int, n_experts: int, topk: int, n_ranks: int, seed: int):
     """Mixtral-style top-k routing (BASELINE.json configs[3]; SURVEY.md ambiguity 20).
 
