@@ -171,6 +171,31 @@ fo_status fo_ctx_destroy(fo_ctx ctx);
 fo_status fo_ctx_time_collective(fo_ctx ctx, int32_t coll, int64_t bytes, int32_t iters, double* avg_us);
 
 /* ---------------------------------------------------------------- the overlapped op */
+/* MoE combine fused into the All-to-All post-reorder (R31; the A2A
+ * "transfer[s] the processed data back to the original GPUs after expert
+ * computation"; the post-reorder fused into the following
+ * elementwise kernel).  On the token-owning rank:
+ *   out[t] = sum_{i<topk} w[t*topk+i] * X[idx[t*topk+i]]  (+ residual[t])
+ * where X is this rank's standard A2A output (the rows fo_run would write,
+ * grouped by source rank ascending, then source row ascending) — read straight
+ * from the receive buffer through the plan's map, never materialised.
+ *   plan: an FO_ALLTOALL plan with post = FO_POST_NONE;
+ *   idx  device int32 [tokens, topk]: row of X for each (token, slot); a value
+ *        < 0 or >= info.out_rows is a dropped slot (contributes nothing);
+ *   w    device float [tokens, topk]: combine weights (e.g. the softmax over
+ *        the token's top-k router logits);
+ *   out  device bf16 [tokens, n]; residual device bf16 [tokens, n] or NULL.
+ * Accumulation in fp32 in slot order, one bf16 rounding.
+ * fo_run_combine = fo_run with the post pass replaced by the combine (runs
+ * once after the last group's exchange: a token's slots arrive in different
+ * groups); fo_combine_stage = the combine alone on a given receive buffer
+ * (single-GPU stage access for multi-rank parity).  Errors:
+ * FO_ERR_INVALID_ARG for a non-A2A plan, post != none, topk outside 1..64. */
+fo_status fo_run_combine(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out, const int32_t* idx,
+                         const float* w, int32_t topk, int64_t tokens, const void* residual, void* stream);
+fo_status fo_combine_stage(fo_plan plan, const void* recv, void* out, const int32_t* idx, const float* w,
+                           int32_t topk, int64_t tokens, const void* residual, void* stream);
+
 /* Overlapped GEMM + collective (+ post-reorder, + fused elementwise), stream
  * ordered on `stream` and host-asynchronous.  Collective: every rank calls it
  * with matching plans in the same order.  A plan must not run concurrently

@@ -222,6 +222,30 @@ def run_host(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, st
                              _stream(stream)))
 
 
+def run_combine(ctx: Context, plan: Plan, A, Bt, out, idx, w, residual=None, stream=None):
+    """fo_run_combine: the A2A plan's overlapped op with the MoE top-k combine
+    as its post pass (idx int32 [tokens, k], w float32 [tokens, k], out [tokens, n])."""
+    _check_combine(idx, w, out)
+    check(load().fo_run_combine(ctx._h, plan.handle, _ptr(A), _ptr(Bt), _ptr(out), _ptr(idx), _ptr(w),
+                                int(idx.shape[1]), int(idx.shape[0]), _ptr(residual), _stream(stream)))
+
+
+def combine_stage(plan: Plan, recv, out, idx, w, residual=None, stream=None):
+    """fo_combine_stage: the MoE combine alone on a receive buffer."""
+    _check_combine(idx, w, out)
+    check(load().fo_combine_stage(plan.handle, _ptr(recv), _ptr(out), _ptr(idx), _ptr(w), int(idx.shape[1]),
+                                  int(idx.shape[0]), _ptr(residual), _stream(stream)))
+
+
+def _check_combine(idx, w, out):
+    import torch
+
+    if idx.dtype != torch.int32 or w.dtype != torch.float32 or idx.shape != w.shape or idx.dim() != 2:
+        raise ValueError("idx must be int32 [tokens, k] and w float32 of the same shape")
+    if out.shape[0] != idx.shape[0]:
+        raise ValueError("out must have one row per token")
+
+
 def run_allgather(ctx: Context, plan: Plan, local, out, residual=None, gamma=None, row_exchange=True, stream=None):
     """RS follow-on: AllGather of the RS outputs (+ row exchange fused with the elementwise op)."""
     check(load().fo_run_allgather(ctx._h, plan.handle, _ptr(local), _ptr(out), _ptr(residual), _ptr(gamma),

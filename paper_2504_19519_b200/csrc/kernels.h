@@ -92,7 +92,24 @@ struct GroupPostArgs {
 };
 
 // Returns a cudaError_t-compatible code (0 = success).
+// MoE top-k combine fused into the A2A post-reorder (R31):
+// out[t] = sum_i w[t*k+i] * a2a_out[idx[t*k+i]] (+ residual[t]), where row r of
+// the standard A2A output is read straight from the receive buffer through
+// src_row (no intermediate [rows, N] buffer); fp32 accumulation, one bf16 rounding.
+struct CombineArgs {
+  const void* src;           // receive buffer (bf16 subtokens)
+  void* out;                 // [tokens, N] bf16
+  const void* residual;      // [tokens, N] bf16 or null
+  const int32_t* idx;        // [tokens, topk] device; < 0 or >= a2a_rows: dropped slot
+  const float* w;            // [tokens, topk] device
+  int topk;
+  int64_t tokens, N, a2a_rows;
+  int BN, Nt;
+  const int32_t* src_row;    // [a2a_rows, Nt] device (plan)
+};
+
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream);
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
 cudaError_t launch_post(const PostArgs& a, cudaStream_t stream);
 cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream);
 cudaError_t launch_timestamp(unsigned long long* dst, cudaStream_t stream);

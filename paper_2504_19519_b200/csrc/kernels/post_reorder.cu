@@ -384,7 +384,80 @@ cudaError_t launch_map(const PostArgs& a, int lbn, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// MoE combine: work unit = (token, 2 KB column segment), one warp; for each of
+// the token's k slots the warp gathers the slot's row segment from the
+// receive buffer (16-B loads, UNROLL in flight per lane) and accumulates
+// w * x in fp32; one bf16 rounding at the end (after the optional residual).
+__global__ void __launch_bounds__(256) fo_combine_kernel(const CombineArgs p, int lbn) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t chunks = p.N >> 3;
+  const int64_t upr = (chunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
+  const int64_t units = p.tokens * upr;
+  const int bn_mask = p.BN - 1;
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(p.residual);
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units; u += warps) {
+    const int64_t t = u / upr;
+    const int64_t c0 = (u - t * upr) * SEG_CHUNKS;
+    float acc[UNROLL][8];
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+    for (int i = 0; i < p.topk; ++i) {
+      const int64_t r = __ldg(p.idx + t * p.topk + i);
+      if (r < 0 || r >= p.a2a_rows) continue;  // dropped slot
+      const float wt = __ldg(p.w + t * p.topk + i);
+      const int32_t* tbl = p.src_row + r * p.Nt;
+      uint4 v[UNROLL];
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int64_t c = c0 + lane + 32 * k;
+        if (c < chunks) {
+          const int64_t col = 8 * c;
+          v[k] = ld_stream(src + (int64_t)__ldg(tbl + (col >> lbn)) * p.BN + (col & bn_mask));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        if (c0 + lane + 32 * k < chunks) {
+          float f[8];
+          unpack8(v[k], f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[k][e] = fmaf(wt, f[e], acc[k][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      const int64_t c = c0 + lane + 32 * k;
+      if (c >= chunks) continue;
+      if (res) {
+        float f[8];
+        unpack8(ld_stream(res + t * p.N + 8 * c), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[k][e] += f[e];
+      }
+      st_stream(out + t * p.N + 8 * c, pack8(acc[k]));
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
+  if (a.tokens <= 0) return cudaSuccess;
+  if (a.N % 8 || (a.BN & (a.BN - 1)) || a.topk < 1) return cudaErrorInvalidValue;
+  int lbn = 0;
+  while ((1 << lbn) < a.BN) ++lbn;
+  const int64_t units = a.tokens * ((a.N / 8 + SEG_CHUNKS - 1) / SEG_CHUNKS);
+  const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)num_sms() * 16);
+  fo_combine_kernel<<<grid, 256, 0, stream>>>(a, lbn);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_group_post(const GroupPostArgs& a, cudaStream_t stream) {
   if (a.BN & (a.BN - 1)) return cudaErrorInvalidValue;

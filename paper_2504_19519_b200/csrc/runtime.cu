@@ -542,7 +542,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     FO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
     // 3. GEMM with reorder + signal epilogue
     run_gemm(p, A, Bt, gemm_dst, epi_mode(h), true, s, p->trace_tile_ts);
-    const bool gpost = use_group_post(p);
+    const bool gpost = use_group_post(p) && !p->combine;
     const void* post_src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : p->d_recv);
     // 4. per-group wait + collective; the per-group post-reorder runs on the
     //    post stream, chained to its group's collective by an event, so the
@@ -576,8 +576,13 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     }
     // 5. post-communication reorder (+ fused op) when not done per group
     const int map = post_map(h);
-    if (!gpost && (map != POSTMAP_IDENTITY || h.post != FO_POST_NONE))
+    if (p->combine) {
+      CombineArgs ca = *p->combine;
+      ca.src = post_src;
+      FO_CUDA(launch_combine(ca, c->comm_stream));
+    } else if (!gpost && (map != POSTMAP_IDENTITY || h.post != FO_POST_NONE)) {
       run_post(p, map, post_src, out, residual, gamma, c->comm_stream);
+    }
     // 6. join
     FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
     FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
@@ -859,6 +864,57 @@ fo_status fo_post_stage(fo_plan p, const void* recv, void* out, const void* resi
     if (!p || !recv || !out) fail(FO_ERR_INVALID_ARG, "null argument");
     ensure_device(p);
     run_post(p, post_map(p->host), recv, out, residual, gamma, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+// MoE combine arguments (R31), validated against the plan.
+static CombineArgs combine_args(fo_plan p, const void* recv, void* out, const int32_t* idx, const float* w,
+                                int32_t topk, int64_t tokens, const void* residual) {
+  const PlanHost& h = p->host;
+  if (h.coll != FO_ALLTOALL) fail(FO_ERR_INVALID_ARG, "the MoE combine follows an All-to-All plan");
+  if (h.post != FO_POST_NONE) fail(FO_ERR_INVALID_ARG, "the combine replaces the plan's post op (use post=none)");
+  if (topk < 1 || topk > 64 || tokens < 0) fail(FO_ERR_INVALID_ARG, "topk must be 1..64 and tokens >= 0");
+  if (tokens > 0 && (!out || !idx || !w)) fail(FO_ERR_INVALID_ARG, "null argument");
+  CombineArgs a{};
+  a.src = recv;
+  a.out = out;
+  a.residual = residual;
+  a.idx = idx;
+  a.w = w;
+  a.topk = topk;
+  a.tokens = tokens;
+  a.N = h.N;
+  a.a2a_rows = h.out_rows;
+  a.BN = h.BN;
+  a.Nt = (int)h.Nt;
+  a.src_row = p->d_src_row;
+  return a;
+}
+
+fo_status fo_combine_stage(fo_plan p, const void* recv, void* out, const int32_t* idx, const float* w,
+                           int32_t topk, int64_t tokens, const void* residual, void* stream) {
+  return guard([&] {
+    if (!p || (!recv && p->host.recv_elems)) fail(FO_ERR_INVALID_ARG, "null argument");
+    ensure_device(p);
+    FO_CUDA(launch_combine(combine_args(p, recv, out, idx, w, topk, tokens, residual),
+                           reinterpret_cast<cudaStream_t>(stream)));
+  });
+}
+
+fo_status fo_run_combine(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const int32_t* idx,
+                         const float* w, int32_t topk, int64_t tokens, const void* residual, void* stream) {
+  struct Transient {
+    fo_plan p;
+    ~Transient() { p->combine = nullptr; }
+  };
+  return guard([&] {
+    if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    ensure_device(p);
+    const CombineArgs ca = combine_args(p, nullptr, out, idx, w, topk, tokens, residual);
+    Transient t{p};
+    p->combine = &ca;
+    fo_status st = fo_run(c, p, A, Bt, out, nullptr, nullptr, stream);
+    if (st != FO_OK) throw Error(st, fo_last_error());
   });
 }
 

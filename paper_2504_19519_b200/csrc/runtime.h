@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <vector>
 
+#include "kernels.h"
 #include "plan.h"
 
 struct fo_plan_s {
@@ -38,6 +39,7 @@ struct fo_plan_s {
   std::vector<int> a_chunk_order;                 // chunks in order of first use
   bool a_staged_run = false;                      // transient: this fo_run's GEMM waits on d_a_ready
   void* d2h_host = nullptr;                       // transient: per-group D2H of out (AR ROWBAND) to here
+  const fo::CombineArgs* combine = nullptr;       // transient: fo_run_combine replaces the A2A post pass
   // ---- debug / evidence hooks (fo_plan_set_debug)
   unsigned long long* trace_tile_ts = nullptr;   // device [tiles]
   unsigned long long* trace_group_ts = nullptr;  // device [2P]: wait released, group done

@@ -554,3 +554,88 @@ def test_rowband_with_swizzled_panels(ctx1, n):
         fo.run(ctx1, plan, _dev_bf16(As[0]), _dev_bf16(Bts[0]), out)
         torch.cuda.synchronize()
         assert np.array_equal(_host(out), opl.plain_allreduce(As, Bts)[0])
+
+
+# ------------------------------------------------------------------ MoE top-k combine (R31, NEXT f3)
+def _combine_close(g, o):
+    # fp32 accumulation of k bf16 rows, one bf16 rounding: <= 2^-8 relative
+    g, o = np.asarray(g, np.float64), np.asarray(o, np.float64)
+    return bool(np.all(np.abs(g - o) <= 2.0 ** -8 * np.abs(o) + 1e-6))
+
+
+@pytest.mark.parametrize("n,k,skew", [(2, 2, 0.0), (4, 2, 1.0), (8, 2, 0.0), (8, 2, 2.0), (4, 1, 0.0)])
+def test_moe_combine_stages(n, k, skew):
+    """Expert GEMM stage per rank (A2A plan), the oracle's exchange, then the
+    fused combine on each token rank vs the oracle's combine of its A2A output."""
+    BM, BN, N, K = 128, 128, 512, 256
+    tokens = 192 * n
+    rt = synthetic.moe_topk(tokens, n, k, seed=40000 + n, skew=skew, pad=BM)
+    X = synthetic.exact_int_A(tokens, K, 77, 64)
+    specs, oplans, As, Bts = [], [], [], []
+    for e in range(n):
+        rows = torch.from_numpy(rt["row_token"][e])
+        A = torch.where((rows >= 0)[:, None], X[rows.clamp(min=0)], torch.zeros((), dtype=X.dtype))
+        Bt = synthetic.exact_int_B(N, K, 500 + e)
+        M = A.shape[0]
+        tiles = (M // BM) * (N // BN)
+        S = max(1, tiles // 3)
+        T = op.num_waves(tiles, S)
+        part = [1, T - 1] if T > 1 else None
+        if part is None:
+            S = max(1, tiles // 2)
+            T = op.num_waves(tiles, S)
+            part = [1, T - 1]
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=1,
+                          group_waves=part, row_dst=rt["row_dst"][e]))
+        oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=1))
+        As.append(A), Bts.append(Bt)
+    ores = opl.run_alltoall(As, Bts, oplans, rt["row_dst"])
+    per = tokens // n
+    for r in range(n):
+        plan = fo.Plan(rank=r, world=n, peers=specs, **specs[r])
+        recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][r]]) if ores["recv"][r] else np.zeros(0)
+        idx = torch.from_numpy(rt["combine_idx"][r]).cuda()
+        w = torch.from_numpy(np.ascontiguousarray(rt["weight"][r * per:(r + 1) * per])).cuda()
+        res = synthetic.normal_bf16((per, N), 1.0, 900 + r)
+        out = torch.empty(per, N, dtype=torch.bfloat16, device="cuda")
+        fo.combine_stage(plan, _dev_bf16(recv), out, idx, w, _dev_bf16(res))
+        torch.cuda.synchronize()
+        want = opost.topk_combine(ores["out"][r], rt["combine_idx"][r], rt["weight"][r * per:(r + 1) * per],
+                                  residual=onum.to_f64(res))
+        assert _combine_close(_host(out), want), r
+        # dropped slots: every second token loses its last slot
+        idx2 = idx.clone()
+        idx2[::2, -1] = -1
+        fo.combine_stage(plan, _dev_bf16(recv), out, idx2, w)
+        torch.cuda.synchronize()
+        want2 = opost.topk_combine(ores["out"][r], idx2.cpu().numpy(), rt["weight"][r * per:(r + 1) * per])
+        assert _combine_close(_host(out), want2), r
+
+
+def test_moe_combine_full_path_world1(ctx1):
+    """fo_run_combine at one rank (one expert, top-1): GEMM + A2A (local) +
+    fused combine through the streams, vs the oracle."""
+    BM, BN, N, K = 256, 256, 1024, 512
+    tokens = 1024
+    rt = synthetic.moe_topk(tokens, 1, 1, seed=5, pad=BM)
+    A, Bt = synthetic.float_inputs(tokens, N, K, seed=8)
+    M = A.shape[0]
+    tiles = (M // BM) * (N // BN)
+    spec = dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=tiles // 4,
+                group_waves=[1, 1, 2], row_dst=rt["row_dst"][0])
+    plan = fo.Plan(peers=[spec], **spec)
+    # permute the slots: token t reads row perm[t] (a gather through the map)
+    perm = np.random.default_rng(3).permutation(tokens).astype(np.int32)[:, None]
+    w = torch.full((tokens, 1), 0.5, dtype=torch.float32, device="cuda")
+    out = torch.empty(tokens, N, dtype=torch.bfloat16, device="cuda")
+    fo.run_combine(ctx1, plan, _dev_bf16(A), _dev_bf16(Bt), out, torch.from_numpy(perm).cuda(), w)
+    torch.cuda.synchronize()
+    Y = opl.run_alltoall([A], [Bt], [op.make_plan(M, N, BM, BN, tiles // 4, [1, 1, 2])], rt["row_dst"],
+                         model_bf16=True)["out"][0]
+    want = opost.topk_combine(Y, perm, np.full((tokens, 1), 0.5))
+    # float regime: the GEMM's own bf16 rounding (fp32 accumulation) may differ
+    # from the model's by an ulp -> the north_star tolerance
+    assert _rel_err(_host(out), want) <= TOL
+    with pytest.raises(fo.FOError):
+        bad = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=4)
+        fo.run_combine(ctx1, bad, _dev_bf16(A), _dev_bf16(Bt), out, torch.from_numpy(perm).cuda(), w)
