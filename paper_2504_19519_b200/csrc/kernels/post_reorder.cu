@@ -406,6 +406,15 @@ __global__ void __launch_bounds__(256) fo_combine_kernel(const CombineArgs p, in
     for (int k = 0; k < UNROLL; ++k)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+    // the residual's loads go out first and land while the slots are gathered
+    uint4 rv[UNROLL];
+    if (res) {
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int64_t c = c0 + lane + 32 * k;
+        if (c < chunks) rv[k] = ld_stream(res + t * p.N + 8 * c);
+      }
+    }
     for (int i = 0; i < p.topk; ++i) {
       const int64_t r = __ldg(p.idx + t * p.topk + i);
       if (r < 0 || r >= p.a2a_rows) continue;  // dropped slot
@@ -436,7 +445,7 @@ __global__ void __launch_bounds__(256) fo_combine_kernel(const CombineArgs p, in
       if (c >= chunks) continue;
       if (res) {
         float f[8];
-        unpack8(ld_stream(res + t * p.N + 8 * c), f);
+        unpack8(rv[k], f);
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[k][e] += f[e];
       }
