@@ -21,7 +21,7 @@ import os
 from dataclasses import asdict, dataclass, field
 from typing import Callable, Optional
 
-from . import Plan, device_sm_count, gemm_stage, tune_search
+from . import Plan, device_sm_count, gemm_stage, tune_predict, tune_search
 
 TILE_M, TILE_N = 256, 256
 
@@ -262,8 +262,22 @@ def candidate_workers(tiles: int, Nt: int, sms: int, coll: str, cg: int = 2) -> 
     return sorted(c for c in cands if c >= 1)
 
 
+def compositions(T: int) -> list:
+    """All 2^(T-1) partitions of T waves into consecutive groups."""
+    out = []
+    for mask in range(1 << max(T - 1, 0)):
+        part, run = [], 0
+        for w in range(T):
+            run += 1
+            if w == T - 1 or (mask >> w) & 1:
+                part.append(run)
+                run = 0
+        out.append(part)
+    return out
+
+
 def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_n=TILE_N, device=0,
-               sizes=None, iters=8, min_comm_sms=16, verify=2) -> LayerChoice:
+               sizes=None, iters=8, min_comm_sms=16, verify=6, all_partitions_T=7) -> LayerChoice:
     """Joint choice of S (wave width), layout and wave groups for one layer
     (AllReduce / ReduceScatter; world from the context).
 
@@ -272,9 +286,10 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     context's communicator (stage (2)), fold the per-group post work into it
     (R28: the reorder of a slot layout and/or the fused op), run Alg. 1, and
     add any post pass that cannot run per group (RMSNorm on a slot layout).
-    The `verify` best predictions are then run for real (fo_run) and the
-    fastest wins: the predictor does not model the contention between the
-    GEMM and per-group post kernels.  At world > 1 every decision is rank 0's
+    For T <= all_partitions_T every partition is predicted (not only Alg. 1's
+    pick); the `verify` best predictions over all (S, layout, partition) are
+    then run for real (fo_run) and the fastest wins: the predictor does not
+    model the contention between the GEMM and per-group post kernels.  At world > 1 every decision is rank 0's
     (broadcast over the default process group) so all ranks build the same
     plan."""
     import torch
@@ -343,8 +358,14 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
             per_group_op = post if (layout == "rowband" or post != "add_rmsnorm") else "none"
             per_group = post_us(layout if layout != "auto" else "slot", per_group_op) / out_bytes
             tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
-            G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, effective_curve(curve, per_group))
+            eff = effective_curve(curve, per_group)
+            G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, eff)
             evaluated.append((S, layout, list(G), pred + tail, dur, swz))
+            if T <= all_partitions_T:
+                for comp in compositions(T):
+                    if comp != list(G):
+                        p2 = tune_predict(comp, dur, tiles, S, tile_m * tile_n * 2, eff)
+                        evaluated.append((S, layout, comp, p2 + tail, dur, swz))
     import torch.distributed as dist
 
     def agree(obj):
