@@ -332,6 +332,12 @@ def main():
     else:
         ch = fot.tune_layer(M, N, K, ctx, "allreduce", "none", tile_m=BM, tile_n=BN, device=local)
         chn = fot.tune_layer(M, N, K, ctx, "allreduce", "add_rmsnorm", tile_m=BM, tile_n=BN, device=local)
+        if rank == 0:
+            for name, c in (("plain", ch), ("fused", chn)):
+                for cand in c.candidates[:6]:
+                    print(f"[tune_layer {name}] S={cand[0]} layout={cand[1]} groups={cand[2]} "
+                          f"predicted {cand[3]:.1f} us" + (f", measured {cand[5]:.1f} us" if len(cand) > 5 else ""),
+                          file=sys.stderr)
         S, groups, pred = ch.workers, tuple(ch.groups), ch.predicted_us
         spec, nspec, pred_n = ch.spec(M, N, K, "allreduce"), chn.spec(M, N, K, "allreduce", "add_rmsnorm"), \
             chn.predicted_us

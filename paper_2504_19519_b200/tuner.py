@@ -277,7 +277,7 @@ def compositions(T: int) -> list:
 
 
 def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_n=TILE_N, device=0,
-               sizes=None, iters=8, min_comm_sms=16, verify=6, all_partitions_T=7) -> LayerChoice:
+               sizes=None, iters=10, min_comm_sms=16, verify=6, all_partitions_T=7) -> LayerChoice:
     """Joint choice of S (wave width), layout and wave groups for one layer
     (AllReduce / ReduceScatter; world from the context).
 
@@ -378,19 +378,36 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     evaluated = agree(sorted(evaluated, key=lambda e: e[3]))
     from . import run as fo_run
 
-    measured = []
+    # verification: the candidates are timed round-robin (one flushed run of
+    # each per round, `iters` rounds) and ranked by their median, so clock /
+    # power drift hits all of them alike and one lucky run cannot win
+    runs = []
     for (S, layout, G, pred, dur, swz) in evaluated[:max(1, verify)]:
         spec = dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
                     group_waves=G, ar_layout=layout if layout != "auto" else "auto", post=post)
         pl = Plan(rank=ctx.rank, world=world, **spec)
         o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
         args = (res, gam) if post != "none" else (None, None)
-        t = timeit(lambda: fo_run(ctx, pl, A, Bt, o, *args))
-        if world > 1 and dist.is_initialized():
-            tt = torch.tensor([t], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t = tt.item()
-        measured.append(t)
+        runs.append((pl, o, args))
+    for pl, o, args in runs:
+        for _ in range(2):
+            fo_run(ctx, pl, A, Bt, o, *args)
+    torch.cuda.synchronize()
+    samples = [[] for _ in runs]
+    for _ in range(max(3, iters)):
+        for i, (pl, o, args) in enumerate(runs):
+            flush.zero_()
+            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            fo_run(ctx, pl, A, Bt, o, *args)
+            e0.record()
+            torch.cuda.synchronize()
+            samples[i].append(s0.elapsed_time(e0) * 1e3)
+    measured = [sorted(v)[len(v) // 2] for v in samples]
+    if world > 1 and dist.is_initialized():
+        tt = torch.tensor(measured, device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        measured = tt.tolist()
     k = min(range(len(measured)), key=lambda i: measured[i])
     best = evaluated[k]
     return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4],
