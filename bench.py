@@ -350,6 +350,7 @@ def main():
     resid = synthetic.normal_bf16((M, N), 1.0, 7, device="cuda")
     gamma = synthetic.normal_bf16((N,), 1.0, 8, device="cuda")
     out2 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    out_cb = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     # the GEMM-only timing uses exactly the overlapped plan's execution order
     gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=plan.export_order())
 
@@ -374,9 +375,11 @@ def main():
                          "seq": lambda: fo.run_sequential(ctx, plan, A, Bt, out),
                          "gemm": lambda: fo.gemm_stage(gplan, A, Bt, out),
                          "ov_norm": lambda: fo.run(ctx, nplan, A, Bt, out2, resid, gamma),
-                         "seq_norm": lambda: fo.run_sequential(ctx, nplan, A, Bt, out2, resid, gamma)},
+                         "seq_norm": lambda: fo.run_sequential(ctx, nplan, A, Bt, out2, resid, gamma),
+                         # library comparator (not on the product path): the same GEMM through cuBLAS
+                         "cublas": lambda: torch.matmul(A, Bt.t(), out=out_cb)},
                         args.steps, args.warmup)
-    ov_us, seq_us, gk_us = m["ov"], m["seq"], m["gemm"]
+    ov_us, seq_us, gk_us, cb_us = m["ov"], m["seq"], m["gemm"], m["cublas"]
     launches = launches_per_step * args.steps
 
     # ---- e2e through the public API with host (pinned) buffers
@@ -444,7 +447,8 @@ def main():
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed alone per step)",
                          "frac_of_sustained_peak": round(achieved / peaks.get("bf16_tflops_sustained", peak), 4),
-                         "kernel_us": round(gk_us, 2), "flops_per_launch": flops},
+                         "kernel_us": round(gk_us, 2), "flops_per_launch": flops,
+                         "cublas_us": round(cb_us, 2), "frac_of_cublas_same_loop": round(cb_us / gk_us, 4)},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_us, 1), "unit": "us",
                     "h2d_bytes_per_step": int(M * K * 2), "d2h_bytes_per_step": int(M * N * 2),

@@ -292,9 +292,19 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      group's rows are copied to the host right after its
  *                      collective; 0 — whole-buffer copies before / after
  *  FO_OPT_HOST_CHUNKS  8 — target number of A chunks (whole tile-rows each) for
- *                      bit 0 above; set before the plan's first fo_run_host */
+ *                      bit 0 above; set before the plan's first fo_run_host
+ *  FO_OPT_LAST_GROUP_IN_ORDER 1 — the last group's collective (and its post
+ *                      pass) is issued on the caller stream right after the GEMM:
+ *                      the kernel boundary orders every tile's stores before it,
+ *                      so the last group needs no counter wait and its
+ *                      wait-release latency leaves the critical path (the
+ *                      caller stream first waits for the comm stream's earlier
+ *                      collectives: same call order on the communicator);
+ *                      0 — every group triggered by its counter on the comm
+ *                      stream (PAPER.md:368 applied to all groups) */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
-               FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5 } fo_option;
+               FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
+               FO_OPT_LAST_GROUP_IN_ORDER = 6 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

@@ -8,8 +8,12 @@
 //   4. comm stream, for each group j: cuStreamWaitValue32(counter_j >= |G_j|)
 //      (a front-end wait, no SM spent — replaces the paper's spinning signal
 //      kernel) then the NCCL call on group j's contiguous range
-//   5. comm stream: post-communication reorder (+ fused add / RMSNorm)
-//   6. join: record E1 on the comm stream; s waits on E1
+//      — except the last group (FO_OPT_LAST_GROUP_IN_ORDER, default): its
+//      collective follows the GEMM on s itself (stream order; s first waits for
+//      the comm stream's earlier collectives)
+//   5. post-communication reorder (+ fused add / RMSNorm): per group on the
+//      post stream, or once after the last collective
+//   6. join: s waits for the comm / post streams
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -347,9 +351,8 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
 
 // The collective of group j, on the comm stream ("Once the j-th
 // number reaches |G_j|, the communication of G_j starts").
-static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* ar_base) {
+static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* ar_base, cudaStream_t cs) {
   const PlanHost& h = p->host;
-  cudaStream_t cs = c->comm_stream;
   char* send = reinterpret_cast<char*>(p->d_send);
   char* recv = reinterpret_cast<char*>(p->d_recv);
   switch (h.coll) {
@@ -552,16 +555,32 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
       FO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       c->ev_group.push_back(e);
     }
+    // the last group in stream order (FO_OPT_LAST_GROUP_IN_ORDER): its
+    // collective follows the GEMM on s — the kernel boundary already orders
+    // every tile's stores, so no counter wait (and no wait-release latency)
+    // sits on the layer's critical path; s first waits for the comm stream's
+    // earlier collectives so the communicator sees the same call order
+    const bool last_on_s = p->last_in_order && h.coll != FO_NOCOMM;
+    cudaStream_t tail = last_on_s ? s : c->comm_stream;
     if (h.coll != FO_NOCOMM) {
       for (int j = 0; j < h.P; ++j) {
-        stream_wait(p, wait, c->comm_stream, j);
-        if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j, c->comm_stream));
-        group_collective(c, p, j, gemm_dst);
-        cudaStream_t ps = c->comm_stream;
+        const bool on_s = last_on_s && j == h.P - 1;
+        cudaStream_t cs = on_s ? s : c->comm_stream;
+        if (on_s) {
+          FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
+          FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+        } else {
+          stream_wait(p, wait, cs, j);
+        }
+        if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j, cs));
+        group_collective(c, p, j, gemm_dst, cs);
+        cudaStream_t ps = cs;
         if (gpost) {
-          FO_CUDA(cudaEventRecord(c->ev_group[j], c->comm_stream));
-          FO_CUDA(cudaStreamWaitEvent(c->post_stream, c->ev_group[j], 0));
-          ps = c->post_stream;
+          if (!on_s) {
+            FO_CUDA(cudaEventRecord(c->ev_group[j], cs));
+            FO_CUDA(cudaStreamWaitEvent(c->post_stream, c->ev_group[j], 0));
+            ps = c->post_stream;
+          }
           run_group_post(p, j, post_src, out, residual, gamma, ps);
         }
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j + 1, ps));
@@ -579,13 +598,15 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     if (p->combine) {
       CombineArgs ca = *p->combine;
       ca.src = post_src;
-      FO_CUDA(launch_combine(ca, c->comm_stream));
+      FO_CUDA(launch_combine(ca, tail));
     } else if (!gpost && (map != POSTMAP_IDENTITY || h.post != FO_POST_NONE)) {
-      run_post(p, map, post_src, out, residual, gamma, c->comm_stream);
+      run_post(p, map, post_src, out, residual, gamma, tail);
     }
-    // 6. join
-    FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
-    FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+    // 6. join (with the last group on s, s already waited for the comm stream)
+    if (!last_on_s) {
+      FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
+      FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+    }
     if (gpost && h.coll != FO_NOCOMM) {
       FO_CUDA(cudaEventRecord(c->ev_post_join, c->post_stream));
       FO_CUDA(cudaStreamWaitEvent(s, c->ev_post_join, 0));
@@ -1021,6 +1042,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_HOST_PIPELINE:
         if (value < 0 || value > 3) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..3");
         p->host_pipeline = (int)value;
+        break;
+      case FO_OPT_LAST_GROUP_IN_ORDER:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "last_group_in_order must be 0 or 1");
+        p->last_in_order = (int)value;
         break;
       default:
         fail(FO_ERR_INVALID_ARG, "unknown option %d", option);

@@ -45,6 +45,7 @@ struct fo_plan_s {
   unsigned long long* trace_group_ts = nullptr;  // device [2P]: wait released, group done
   int group_post = -1;                            // -1 auto, 0 off, 1 on
   int wait_kernel = 0;                            // 0 cuStreamWaitValue32, 1 spin-wait kernel
+  int last_in_order = 1;                          // last group's collective on the caller stream after the GEMM
   int post_sm_partition = 0;                      // FO_OPT_POST_SM_PARTITION
   int tail_split_req = 0;                         // FO_OPT_TAIL_SPLIT: 0/1 off, >=2 slices, -1 auto
   // ---- resolved tail split (set by ensure_device)

@@ -375,7 +375,16 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
             return box[0]
         return obj
 
-    evaluated = agree(sorted(evaluated, key=lambda e: e[3]))
+    evaluated = sorted(evaluated, key=lambda e: e[3])
+    # the single-group plan (no overlap: the whole GEMM, then one collective)
+    # is always among the verified candidates, so the chosen split is never
+    # one measured slower than not splitting at all
+    single = [e for e in evaluated if len(e[2]) == 1]
+    if single and not any(len(e[2]) == 1 for e in evaluated[:max(1, verify)]):
+        best1 = min(single, key=lambda e: (e[1] != "rowband", e[3]))
+        evaluated.remove(best1)
+        evaluated.insert(max(1, verify) - 1, best1)
+    evaluated = agree(evaluated)
     from . import run as fo_run
 
     # verification: the candidates are timed round-robin (one flushed run of

@@ -166,3 +166,35 @@ def test_post_sm_partition_option_equal_results(ctx):
     fo.run(ctx, p_off, A, Bt, o2, res)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("coll,post,layout", [("allreduce", "none", "slot"), ("allreduce", "add_rmsnorm", "slot"),
+                                              ("allreduce", "add_rmsnorm", "rowband"),
+                                              ("reducescatter", "add", "auto"), ("alltoall", "none", "auto")])
+def test_last_group_in_order_equals_counter_trigger(ctx, coll, post, layout):
+    """FO_OPT_LAST_GROUP_IN_ORDER: the last group's collective issued on the
+    caller stream after the GEMM gives bit-identical results to triggering it
+    by its counter on the comm stream, over repeated runs."""
+    M, N, K, S = 2048, 1024, 512, 8
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+              group_waves=[1, 2, 1], ar_layout=layout, post=post)
+    if coll == "alltoall":
+        kw["row_dst"] = np.zeros(M, np.int32)
+        mk = lambda: fo.Plan(rank=0, world=1, peers=[kw], **kw)
+    else:
+        mk = lambda: fo.Plan(**kw)
+    p_on, p_off = mk(), mk()
+    p_off.set_option("last_group_in_order", 0)
+    A, Bt = synthetic.float_inputs(M, N, K, seed=31, device="cuda")
+    rows = p_on.info["out_rows"]
+    res = synthetic.normal_bf16((rows, N), 1.0, 32, device="cuda") if post != "none" else None
+    gam = synthetic.normal_bf16((N,), 1.0, 33, device="cuda") if post == "add_rmsnorm" else None
+    o1 = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    for _ in range(20):
+        p_on.fill_buffers(0x7FC0)
+        o1.fill_(float("nan"))
+        fo.run(ctx, p_on, A, Bt, o1, res, gam)
+        fo.run(ctx, p_off, A, Bt, o2, res, gam)
+        torch.cuda.synchronize()
+        assert torch.equal(o1, o2)

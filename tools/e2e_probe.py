@@ -13,6 +13,13 @@ import synthetic  # noqa: E402
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="64:1x4:8:rowband;64:1x4:16:rowband;32:1x8:8:rowband;32:1x8:16:rowband;"
+                    "16:1x16:16:rowband;64:1,3:8:rowband;64:1,1,2:8:slot",
+                    help="';'-separated S:groups:chunks:layout entries; groups '1x4' = [1]*4")
+    ap.add_argument("--pipes", default="0,3")
+    args = ap.parse_args()
     torch.cuda.set_device(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     M, N, K = 4096, 4096, 14336
@@ -21,12 +28,14 @@ def main():
     Bt = Bt.cuda()
     out = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
     h2d = M * K * 2 / 1e9
-    for groups, layout, chunks in (([1, 1, 1, 1], "rowband", 4), ([1, 1, 1, 1], "rowband", 8),
-                                   ([1, 1, 1, 1], "rowband", 16), ([1, 3], "rowband", 8), ([1, 1, 2], "slot", 8)):
-        plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=64, swizzle=1,
+    for cfg in args.configs.split(";"):
+        S, g, chunks, layout = cfg.split(":")
+        S, chunks = int(S), int(chunks)
+        groups = [int(g.split("x")[0])] * int(g.split("x")[1]) if "x" in g else [int(x) for x in g.split(",")]
+        plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
                        group_waves=groups, ar_layout=layout)
         plan.set_option("host_chunks", chunks)
-        for pipe in (0, 1, 2, 3):
+        for pipe in map(int, args.pipes.split(",")):
             plan.set_option("host_pipeline", pipe)
             for _ in range(3):
                 fo.run_host(ctx, plan, A, Bt, out)
@@ -40,7 +49,7 @@ def main():
                 torch.cuda.synchronize()
                 ts.append(s.elapsed_time(e) * 1e3)
             ts.sort()
-            print(f"{layout:8s} groups={groups} chunks={chunks} pipeline={pipe}: e2e median {ts[5]:.1f} us "
+            print(f"S={S:3d} {layout:8s} groups={groups} chunks={chunks} pipeline={pipe}: e2e median {ts[5]:.1f} us "
                   f"(min {ts[0]:.1f}); H2D of A alone at 55 GB/s would be {h2d / 55e-6:.0f} us", flush=True)
     # the copies alone, and H2D concurrent with D2H
     o_d = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
