@@ -301,10 +301,22 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      caller stream first waits for the comm stream's earlier
  *                      collectives: same call order on the communicator);
  *                      0 — every group triggered by its counter on the comm
- *                      stream (PAPER.md:368 applied to all groups) */
+ *                      stream (PAPER.md:368 applied to all groups)
+ *  FO_OPT_WAVE_SYNC    0 — free-running persistent workers (default);
+ *                      1 — the persistent GEMM keeps its waves aligned (the
+ *                      hardware-scheduled waves of PAPER.md:235): a worker issues
+ *                      no load of its wave-(w+1) tile before every worker has
+ *                      issued the last load of its wave-w tile, so workers never
+ *                      drift into different operand panels and one wave's panels
+ *                      are read from HBM once (L2 reuse; less HBM power, higher
+ *                      clocks under the power cap); a scheduling constraint only,
+ *                      results are identical; ignored with a tail split.
+ *                      Measured: halves HBM reads of long-K many-wave GEMMs
+ *                      under ncu, no wall-clock change in interleaved timing
+ *                      (profiles/r01_wave_sync.txt), hence off by default */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
-               FO_OPT_LAST_GROUP_IN_ORDER = 6 } fo_option;
+               FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

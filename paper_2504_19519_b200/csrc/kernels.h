@@ -45,6 +45,13 @@ struct GemmArgs {
   const uint32_t* a_ready;
   uint32_t a_epoch;
   int a_chunk_rows;
+  // ---- wave alignment (FO_OPT_WAVE_SYNC): each CTA's producer adds 1 to
+  // wave_ctr[w] after issuing its wave-w tile's last load and issues no load
+  // of wave w+1 before wave w's count reached its target for this launch;
+  // counters only grow (launch `wave_epoch` of this plan expects
+  // (wave_epoch+1) * CG * |wave w| ), null = off
+  uint32_t* wave_ctr;
+  uint32_t wave_epoch;
 };
 
 enum PostMode : int {

@@ -365,6 +365,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int arow = ti * TM + (int)crank * BM;
         const int brow = tj * BN + (int)crank * C::B_ROWS;
+        const int wave = u / nworkers;
+        if (p.wave_ctr && wave > 0) {
+          // keep the waves aligned: no load of wave w before every CTA of
+          // wave w-1 has issued its last one (cyclic compare: monotone counters)
+          const uint32_t size = (uint32_t)min(nworkers, p.units - (wave - 1) * nworkers) * CG;
+          const uint32_t target = (p.wave_epoch + 1u) * size;
+          while ((int32_t)(ld_acquire(p.wave_ctr + wave - 1) - target) < 0) __nanosleep(64);
+        }
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           // K-major operand: one box [rows, 64 k]; MN-major operand: 64x64
@@ -391,6 +399,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             phase ^= 1;
           }
         }
+        if (p.wave_ctr) atomicAdd(p.wave_ctr + wave, 1u);
       }
     }
   } else if (warp == 1) {

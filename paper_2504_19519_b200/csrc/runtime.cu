@@ -102,7 +102,7 @@ void release_device(fo_plan_s* p) {
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
                     p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma,
-                    (void*)p->d_ws, (void*)p->d_a_ready})
+                    (void*)p->d_ws, (void*)p->d_a_ready, (void*)p->d_wave})
     if (ptr) cudaFree(ptr);
   cudaSetDevice(cur);
   p->device = -1;
@@ -150,6 +150,8 @@ static void ensure_device(fo_plan_s* p) {
     if (p->split > 1)
       FO_CUDA(cudaMalloc(&p->d_ws, sizeof(float) * (size_t)R * (p->split - 1) * h.BM * h.BN));
   }
+  FO_CUDA(cudaMalloc(&p->d_wave, sizeof(uint32_t) * (size_t)h.T));
+  FO_CUDA(cudaMemset(p->d_wave, 0, sizeof(uint32_t) * (size_t)h.T));
   FO_CUDA(cudaMalloc(&p->d_counters, sizeof(uint32_t) * p->ctr_words));
   FO_CUDA(cudaMemset(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words));
   p->d_flags = p->d_counters + h.P;
@@ -198,6 +200,10 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
     a.a_epoch = p->a_epoch;
     a.a_chunk_rows = p->a_chunk_rows;
   }
+  if (p->wave_sync && p->split == 1 && h.T > 1) {
+    a.wave_ctr = p->d_wave;
+    a.wave_epoch = p->gemm_launches;
+  }
   return a;
 }
 
@@ -217,6 +223,7 @@ static void run_gemm(fo_plan_s* p, const void* A, const void* Bt, void* dst, int
   GemmArgs a = gemm_args(p, A, Bt, dst, mode, signal);
   a.tile_ts = tile_ts;
   FO_CUDA(launch_gemm(a, s));
+  ++p->gemm_launches;  // every launch of the plan's GEMM advances the wave counters once
 }
 
 static void run_post(fo_plan_s* p, int map, const void* src, void* out, const void* residual, const void* gamma,
@@ -1042,6 +1049,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_HOST_PIPELINE:
         if (value < 0 || value > 3) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..3");
         p->host_pipeline = (int)value;
+        break;
+      case FO_OPT_WAVE_SYNC:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "wave_sync must be 0 or 1");
+        p->wave_sync = (int)value;
         break;
       case FO_OPT_LAST_GROUP_IN_ORDER:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "last_group_in_order must be 0 or 1");

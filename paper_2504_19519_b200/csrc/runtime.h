@@ -53,6 +53,10 @@ struct fo_plan_s {
   float* d_ws = nullptr;                          // fp32 partials of the split tail
   uint32_t* d_flags = nullptr;                    // = d_counters + P (one allocation, reset together)
   int ctr_words = 0;                              // P + tail flags
+  // ---- wave alignment of the persistent producers (FO_OPT_WAVE_SYNC)
+  int wave_sync = 0;
+  uint32_t* d_wave = nullptr;                     // [T] monotone per-wave issue counters
+  uint32_t gemm_launches = 0;                     // launches of this plan's GEMM so far (wave epoch)
 };
 
 namespace fo {

@@ -19,14 +19,18 @@ def main():
     ap.add_argument("--shape", default="4096x4096x14336")
     ap.add_argument("--workers", type=int, default=64)
     ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--wave", type=int, default=1)
+    ap.add_argument("--no-cublas", action="store_true")
     args = ap.parse_args()
     M, N, K = map(int, args.shape.split("x"))
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     B = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=args.workers, swizzle=0)
+    plan.set_option("wave_sync", args.wave)
     for _ in range(args.iters):
-        torch.matmul(A, B.t(), out=C)
+        if not args.no_cublas:
+            torch.matmul(A, B.t(), out=C)
         fo.gemm_stage(plan, A, B, C)
     torch.cuda.synchronize()
     print("ok")

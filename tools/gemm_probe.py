@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--bm", default="128,256")
     ap.add_argument("--swizzle", type=int, default=0)
     ap.add_argument("--split", default="0")
+    ap.add_argument("--wave", default="1", help="FO_OPT_WAVE_SYNC values to try")
     args = ap.parse_args()
     sms = fo.device_sm_count(0)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -53,16 +54,18 @@ def main():
                 for S in map(int, args.s.split(",")):
                   Sw = min(S, sms) // (bm // 128)
                   for split in map(int, args.split.split(",")):
+                   for wv in map(int, args.wave.split(",")):
                     plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=bm, tile_n=bn, workers=Sw,
                                    swizzle=args.swizzle)
                     try:
                         plan.set_option("tail_split", split)
+                        plan.set_option("wave_sync", wv)
                         t = timeit(lambda: fo.gemm_stage(plan, A, B, C), flush=flush)
                     except fo.FOError as e:
                         print(f"{sh} BM={bm} BN={bn} S={Sw} split={split}: {e}")
                         continue
                     err = (C.float() - ref).abs().max().item()
-                    print(f"{sh} fo BM={bm} BN={bn} S={Sw} split={split} {t:8.1f} us {fl / t / 1e6:7.1f} TF  "
+                    print(f"{sh} fo BM={bm} BN={bn} S={Sw} split={split} wave={wv} {t:8.1f} us {fl / t / 1e6:7.1f} TF  "
                           f"maxdiff {err:.3g}", flush=True)
 
 
