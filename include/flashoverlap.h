@@ -258,6 +258,10 @@ fo_status fo_post_stage(fo_plan plan, const void* recv, void* out, const void* r
  * [m, n] (what ncclAllGather of the ranks' RS outputs delivers). */
 fo_status fo_rowexchange_stage(fo_plan plan, const void* gathered, void* out, const void* residual,
                                const void* gamma, void* stream);
+/* CTAs per thread-block cluster the plan's GEMM launches with on the current
+ * device: 1 (128-row tiles), 2 (CTA pair, 256-row tiles) or 4 (two pairs with
+ * TMA multicast, FO_OPT_MULTICAST).  Binds the plan to the device like a run. */
+fo_status fo_plan_gemm_cluster(fo_plan plan, int32_t* cluster_ctas);
 /* Copy the plan's P counters to host (synchronises the device). */
 fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
 /* Debug / evidence hooks (tests, tools; never needed for correct use):
@@ -313,10 +317,20 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      results are identical; ignored with a tail split.
  *                      Measured: halves HBM reads of long-K many-wave GEMMs
  *                      under ncu, no wall-clock change in interleaved timing
- *                      (profiles/r01_wave_sync.txt), hence off by default */
+ *                      (profiles/r01_wave_sync.txt), hence off by default
+ *  FO_OPT_MULTICAST    0 — independent CTA pairs (default);
+ *                      1 — 256-row (CTA-pair) tiles with K-major operands, an even
+ *                      S and no tail split run as clusters of two pairs when all
+ *                      S/2 clusters fit on the device: the pairs run consecutive
+ *                      execution positions in lockstep and a shared A tile-row
+ *                      or B tile-column is loaded once per cluster and
+ *                      TMA-multicast to both pairs (17% fewer L2 sectors);
+ *                      results are identical.  Measured 12-20% slower: the
+ *                      shared stage-release barriers couple the two pairs'
+ *                      pipelines (profiles/r01_multicast.txt), hence off */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
-               FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7 } fo_option;
+               FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

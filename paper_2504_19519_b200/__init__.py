@@ -140,6 +140,15 @@ class Plan:
         check(load().fo_plan_read_counters(self._h, c.ctypes.data_as(C.POINTER(C.c_uint32))))
         return c
 
+    def gemm_cluster(self) -> int:
+        """CTAs per cluster of the plan's GEMM launch on the current device (1, 2, 4)."""
+        v = C.c_int32(0)
+        check(load().fo_plan_gemm_cluster(self._h, C.byref(v)))
+        return int(v.value)
+
+    def multicast_used(self) -> bool:
+        return self.gemm_cluster() == 4
+
     def set_debug(self, tile_ts=None, group_ts=None, group_post: int = -1):
         """Evidence hooks: device int64 tensors for tile / group timestamps; group_post -1/0/1."""
         self._dbg = (tile_ts, group_ts)  # keep alive

@@ -52,6 +52,8 @@ struct GemmArgs {
   // (wave_epoch+1) * CG * |wave w| ), null = off
   uint32_t* wave_ctr;
   uint32_t wave_epoch;
+  // ---- TMA multicast across clusters of two CTA pairs (FO_OPT_MULTICAST)
+  int multicast;
 };
 
 enum PostMode : int {
@@ -123,6 +125,7 @@ cudaError_t launch_timestamp(unsigned long long* dst, cudaStream_t stream);
 cudaError_t launch_wait(const uint32_t* counter, uint32_t target, cudaStream_t stream);
 cudaError_t launch_fill_u16(void* dst, int64_t count, uint16_t value, cudaStream_t stream);
 bool gemm_shape_supported(int BM, int BN);
+bool gemm_multicast_used(const GemmArgs& a);  // the launch would use clusters of two pairs
 void count_launch();
 int64_t launch_count();
 

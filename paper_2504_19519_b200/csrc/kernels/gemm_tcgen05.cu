@@ -132,6 +132,19 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
+// 2-SM TMA multicast (cluster of CTA pairs): the box lands at the same smem
+// offset in every CTA of `mask`; each destination's transaction bytes are
+// counted on the barrier at this offset in the destination's pair leader
+// (peer bit of the barrier address cleared, the CUTLASS SM100 2-SM form).
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* map, int x, int y, const void* bar,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask), "r"(x), "r"(y)
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -187,9 +200,10 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
 }
 
 // MMA completion -> mbarrier arrive; for a pair, multicast to the barrier at
-// the same offset in both CTAs.
+// the same offset in the CTAs of `mask` (the pair itself, or every CTA of a
+// cluster of pairs whose smem stages the pair's loads also fill).
 template <int CG>
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+__device__ __forceinline__ void umma_commit(uint64_t* bar, uint16_t mask = 0x3) {
   if constexpr (CG == 1) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -197,7 +211,7 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
-        "h"((uint16_t)0x3)
+        "h"(mask)
         : "memory");
   }
 }
@@ -285,14 +299,22 @@ __device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, in
 // S = gridDim.x/CG runs positions w, w+S, ... (wave floor(p/S)).
 // MJ: operand majorness (bit 0: A is [K, M] M-major, bit 1: Bt is [K, N]
 // N-major — the weight-gradient dW = dY^T X layout); 0 = both K-major.
-template <int BN, int CG, int MJ>
+// MC: CTA pairs per cluster.  MC = 2 (K-major, no tail split, even S): the
+// two pairs of a cluster run consecutive execution positions p, p^1 in
+// lockstep; when the two tiles share their A tile-row (or B tile-column), each
+// CTA loads half of its share of that operand and TMA-multicasts it to the
+// CTA at the same half of the other pair, so the operand crosses L2 once for
+// both tiles (tmA2 / tmB2: maps with half-height boxes).
+template <int BN, int CG, int MJ, int MC>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     fo_gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                            const GemmArgs p) {
   using C = Cfg<BN, CG>;
   constexpr int ST = C::STAGES;
   constexpr int TM = BM * CG;  // tile rows
   static_assert(!(MJ & 2) || (C::B_ROWS % 64 == 0), "MN-major B needs 64-row chunks");
+  static_assert(MC == 1 || (CG == 2 && MJ == 0), "multicast clusters: CTA pairs, K-major operands");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                   // ST x 16 KB
@@ -306,19 +328,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t crank = (CG == 1) ? 0u : cluster_rank();
-  const bool leader = (crank == 0);
+  const uint32_t crank = (CG * MC == 1) ? 0u : cluster_rank();
+  const uint32_t half = (CG == 1) ? 0u : (crank & 1u);  // this CTA's half of the pair's tile
+  const uint32_t pic = crank >> 1;                      // pair index inside the cluster (MC = 2)
+  const uint32_t lead_rank = crank & ~1u;               // the pair's leader CTA
+  const bool leader = (half == 0);
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pic));
   const int worker = blockIdx.x / CG;
   const int nworkers = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if constexpr (MC == 2) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA2)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // MC = 2: both pairs' MMAs release a stage (their loads fill each other's)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -340,7 +370,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   tc_fence_before();
-  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
+  if constexpr (CG * MC == 1) __syncthreads(); else cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int KB = (int)(p.K / BK);
@@ -363,8 +393,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           while ((int32_t)(ld_acquire(p.a_ready + ready_chunk) - p.a_epoch) < 0) __nanosleep(128);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        const int arow = ti * TM + (int)crank * BM;
-        const int brow = tj * BN + (int)crank * C::B_ROWS;
+        const int arow = ti * TM + (int)half * BM;
+        const int brow = tj * BN + (int)half * C::B_ROWS;
+        // multicast partner: the other pair of the cluster runs position u^1
+        bool mcA = false, mcB = false;
+        uint16_t mc_mask = 0;
+        if constexpr (MC == 2) {
+          if ((u ^ 1) < p.units) {
+            const int t2 = p.order[u ^ 1];
+            const int ti2 = t2 / p.Nt;
+            mcA = (ti2 == ti);
+            mcB = (t2 - ti2 * p.Nt == tj);
+            mc_mask = (uint16_t)((1u << half) | (1u << (2 + half)));
+          }
+        }
         const int wave = u / nworkers;
         if (p.wave_ctr && wave > 0) {
           // keep the waves aligned: no load of wave w before every CTA of
@@ -381,19 +423,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const bool mn = (map == &tmA) ? (MJ & 1) : (MJ & 2);
             if (!mn) {
               if constexpr (CG == 1) tma_load_2d(dst, map, kb * BK, rows0, &full[stage]);
-              else tma_load_2d_2sm(dst, map, kb * BK, rows0, mapa_shared(&full[stage], 0));
+              else tma_load_2d_2sm(dst, map, kb * BK, rows0, mapa_shared(&full[stage], lead_rank));
             } else {
               for (int h = 0; h < nrows / 64; ++h) {
                 uint8_t* d = reinterpret_cast<uint8_t*>(dst) + h * 8192;
                 if constexpr (CG == 1) tma_load_2d(d, map, rows0 + 64 * h, kb * BK, &full[stage]);
-                else tma_load_2d_2sm(d, map, rows0 + 64 * h, kb * BK, mapa_shared(&full[stage], 0));
+                else tma_load_2d_2sm(d, map, rows0 + 64 * h, kb * BK, mapa_shared(&full[stage], lead_rank));
               }
             }
           };
           // a pair's two CTAs' bytes are all counted on the leader's full barrier
           if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
-          load(sA + stage * A_STAGE_BYTES, &tmA, arow, BM);
-          load(sB + stage * C::B_STAGE_BYTES, &tmB, brow, C::B_ROWS);
+          if constexpr (MC == 2) {
+            // shared operand: this CTA loads rows [pic*h, pic*h + h) of its half
+            // and multicasts them to the same half of both pairs
+            if (mcA)
+              tma_load_2d_2sm_mc(sA + stage * A_STAGE_BYTES + pic * (A_STAGE_BYTES / 2), &tmA2, kb * BK,
+                                 arow + (int)pic * (BM / 2), &full[stage], mc_mask);
+            else
+              tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, arow, mapa_shared(&full[stage], lead_rank));
+            if (mcB)
+              tma_load_2d_2sm_mc(sB + stage * C::B_STAGE_BYTES + pic * (C::B_STAGE_BYTES / 2), &tmB2, kb * BK,
+                                 brow + (int)pic * (C::B_ROWS / 2), &full[stage], mc_mask);
+            else
+              tma_load_2d_2sm(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, brow, mapa_shared(&full[stage], lead_rank));
+          } else {
+            load(sA + stage * A_STAGE_BYTES, &tmA, arow, BM);
+            load(sB + stage * C::B_STAGE_BYTES, &tmB, brow, C::B_ROWS);
+          }
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
@@ -428,13 +485,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bdesc = (MJ & 2) ? sw128_mn_desc(sb + 2048 * k) : sw128_desc(sb) + 2 * k;
             umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
           }
-          umma_commit<CG>(&empty[stage]);  // frees the smem stage (in both CTAs) when these MMAs retire
+          // frees the smem stage when these MMAs retire: in both CTAs of the
+          // pair; with a multicast partner in all four CTAs (count 2 each), and
+          // alone (partner done) twice in the pair's own CTAs
+          if constexpr (MC == 2) {
+            if ((u ^ 1) < p.units) {
+              umma_commit<CG>(&empty[stage], 0xF);
+            } else {
+              umma_commit<CG>(&empty[stage], pair_mask);
+              umma_commit<CG>(&empty[stage], pair_mask);
+            }
+          } else {
+            umma_commit<CG>(&empty[stage]);
+          }
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit<CG>(&tfull[acc]);  // accumulator ready for the epilogue(s)
+        umma_commit<CG>(&tfull[acc], pair_mask);  // accumulator ready for the pair's epilogues
         if (++acc == 2) {
           acc = 0;
           aphase ^= 1;
@@ -445,7 +514,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ======================= epilogue: reorder-store + signal (this CTA's 128 rows)
     const int q = warp - 4;  // TMEM lane quarter: warp (4+q) may access lanes 32q..32q+31
     uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
-    const uint32_t tempty_leader0 = (CG == 1) ? 0u : mapa_shared(&tempty[0], 0);
+    const uint32_t tempty_leader0 = (CG == 1) ? 0u : mapa_shared(&tempty[0], lead_rank);
     int acc = 0;
     uint32_t aphase = 0;
     for (int u = worker; u < p.units; u += nworkers) {
@@ -455,14 +524,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int ti = t / p.Nt, tj = t - ti * p.Nt;
       const bool tail = (pos >= p.tail_pos) && p.split > 1;
       const int tt = pos - p.tail_pos;  // tail tile index
-      const int row = (int)crank * BM + q * 32 + lane;  // this thread's accumulator row in the tile
+      const int row = (int)half * BM + q * 32 + lane;  // this thread's accumulator row in the tile
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       if (tail && un.slice == 0) {
         // owner of a split tile: wait until the other K-slices' partials of
         // this CTA's rows are published (acquire), then fold them in below
         if (q == 0 && lane == 0) {
-          const uint32_t* f = p.flags + tt * CG + crank;
+          const uint32_t* f = p.flags + tt * CG + half;
           while (ld_acquire(f) < (uint32_t)(p.split - 1)) __nanosleep(32);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -525,7 +594,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int r = it * 4 + (lane >> 3);
           const int ch = lane & 7;
           const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + ch * 16);
-          __nv_bfloat16* d = row_dst<TM, BN>(p, pos, ti, tj, (int)crank * BM + q * 32 + r) + c * EPI_COLS + ch * 8;
+          __nv_bfloat16* d = row_dst<TM, BN>(p, pos, ti, tj, (int)half * BM + q * 32 + r) + c * EPI_COLS + ch * 8;
           *reinterpret_cast<uint4*>(d) = w;
         }
         __syncwarp();
@@ -533,7 +602,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (tail && un.slice > 0) {
         // partials of this CTA's rows stored -> one release increment of the tile's flag
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane == 0) red_release_add(p.flags + tt * CG + crank, 1u);
+        if (q == 0 && lane == 0) red_release_add(p.flags + tt * CG + half, 1u);
         if (++acc == 2) {
           acc = 0;
           aphase ^= 1;
@@ -554,7 +623,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   tc_fence_before();
-  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
+  if constexpr (CG * MC == 1) __syncthreads(); else cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     if constexpr (CG == 1)
@@ -606,11 +675,11 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int CG, int MJ>
+template <int BN, int CG, int MJ, int MC>
 cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
   using C = Cfg<BN, CG>;
   static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
-  auto kern = fo_gemm_tcgen05_kernel<BN, CG, MJ>;
+  auto kern = fo_gemm_tcgen05_kernel<BN, CG, MJ, MC>;
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
@@ -619,9 +688,16 @@ cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit);
   }
-  CUtensorMap mA, mB;
+  CUtensorMap mA, mB, mA2, mB2;
   if (!make_map(&mA, a.A, a.M, a.K, BM, MJ & 1) || !make_map(&mB, a.Bt, a.N, a.K, C::B_ROWS, MJ & 2))
     return cudaErrorInvalidValue;
+  if (MC == 2) {
+    if (!make_map(&mA2, a.A, a.M, a.K, BM / 2, false) || !make_map(&mB2, a.Bt, a.N, a.K, C::B_ROWS / 2, false))
+      return cudaErrorInvalidValue;
+  } else {
+    mA2 = mA;
+    mB2 = mB;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.workers * CG);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -629,15 +705,51 @@ cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CG * MC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mB, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mB, mA2, mB2, a);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// Clusters of two CTA pairs resident at once for this configuration (per
+// device, cached): a persistent grid of S pairs may use them only if all S/2
+// clusters fit.
+template <int BN>
+int max_pair_clusters() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = cache[dev & 63].load();
+  if (v) return v;
+  using C = Cfg<BN, 2>;
+  auto kern = fo_gemm_tcgen05_kernel<BN, 2, 0, 2>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(4);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = -1;
+  }
+  cache[dev & 63].store(n ? n : -1);
+  return n ? n : -1;
 }
 
 std::atomic<int64_t> g_launches{0};
@@ -654,25 +766,42 @@ bool gemm_shape_supported(int bm, int bn) {
 template <int BN, int CG>
 cudaError_t launch_mj(const GemmArgs& a, cudaStream_t stream) {
   switch (a.mn_major) {
-    case 0: return launch_cfg<BN, CG, 0>(a, stream);
-    case 1: return launch_cfg<BN, CG, 1>(a, stream);
-    case 2: return launch_cfg<BN, CG, 2>(a, stream);
-    case 3: return launch_cfg<BN, CG, 3>(a, stream);
+    case 0:
+      if constexpr (CG == 2) {
+        // TMA multicast across clusters of two pairs (FO_OPT_MULTICAST): even S,
+        // no tail split, every cluster resident
+        if (a.multicast && a.workers % 2 == 0 && a.split == 1 && max_pair_clusters<BN>() >= a.workers / 2)
+          return launch_cfg<BN, CG, 0, 2>(a, stream);
+      }
+      return launch_cfg<BN, CG, 0, 1>(a, stream);
+    case 1: return launch_cfg<BN, CG, 1, 1>(a, stream);
+    case 2: return launch_cfg<BN, CG, 2, 1>(a, stream);
+    case 3: return launch_cfg<BN, CG, 3, 1>(a, stream);
   }
   return cudaErrorInvalidValue;
+}
+
+bool gemm_multicast_used(const GemmArgs& a) {
+  if (!(a.BM == 256 && a.mn_major == 0 && a.multicast && a.workers % 2 == 0 && a.split == 1)) return false;
+  switch (a.BN) {
+    case 64: return false;
+    case 128: return max_pair_clusters<128>() >= a.workers / 2;
+    case 256: return max_pair_clusters<256>() >= a.workers / 2;
+  }
+  return false;
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
   if (a.mn_major && a.BN == 64) return cudaErrorInvalidValue;  // MN-major needs >= 64-row B chunks per CTA
   if (a.BM == 128) {
     switch (a.BN) {
-      case 64: return launch_cfg<64, 1, 0>(a, stream);
+      case 64: return launch_cfg<64, 1, 0, 1>(a, stream);
       case 128: return launch_mj<128, 1>(a, stream);
       case 256: return launch_mj<256, 1>(a, stream);
     }
   } else if (a.BM == 256) {
     switch (a.BN) {
-      case 64: return launch_cfg<64, 2, 0>(a, stream);
+      case 64: return launch_cfg<64, 2, 0, 1>(a, stream);
       case 128: return launch_mj<128, 2>(a, stream);
       case 256: return launch_mj<256, 2>(a, stream);
     }

@@ -200,6 +200,7 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
     a.a_epoch = p->a_epoch;
     a.a_chunk_rows = p->a_chunk_rows;
   }
+  a.multicast = p->multicast;
   if (p->wave_sync && p->split == 1 && h.T > 1) {
     a.wave_ctr = p->d_wave;
     a.wave_epoch = p->gemm_launches;
@@ -955,6 +956,15 @@ fo_status fo_plan_read_counters(fo_plan p, uint32_t* counters) {
   });
 }
 
+fo_status fo_plan_gemm_cluster(fo_plan p, int32_t* cluster_ctas) {
+  return guard([&] {
+    if (!p || !cluster_ctas) fail(FO_ERR_INVALID_ARG, "null argument");
+    ensure_device(p);
+    GemmArgs a = gemm_args(p, nullptr, nullptr, nullptr, EPI_ROWMAJOR, false);
+    *cluster_ctas = gemm_multicast_used(a) ? 4 : p->host.BM / 128;
+  });
+}
+
 int64_t fo_kernel_launch_count(void) { return launch_count(); }
 
 fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t iters, double* avg_us) {
@@ -1049,6 +1059,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_HOST_PIPELINE:
         if (value < 0 || value > 3) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..3");
         p->host_pipeline = (int)value;
+        break;
+      case FO_OPT_MULTICAST:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "multicast must be 0 or 1");
+        p->multicast = (int)value;
         break;
       case FO_OPT_WAVE_SYNC:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "wave_sync must be 0 or 1");

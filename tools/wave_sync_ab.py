@@ -1,4 +1,4 @@
-"""A/B of FO_OPT_WAVE_SYNC on the GEMM (dev tool): the two plans (and cuBLAS)
+"""A/B of a GEMM plan option (FO_OPT_WAVE_SYNC, FO_OPT_MULTICAST; dev tool): the two plans (and cuBLAS)
 run interleaved, L2 flushed before each, so clock / power drift hits all
 alike; medians."""
 import argparse
@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--shapes", default="4096x4096x14336,4096x16384x16384,8192x16384x16384,16384x16384x16384")
     ap.add_argument("--s", default="64,74")
     ap.add_argument("--iters", type=int, default=15)
+    ap.add_argument("--opt", default="wave_sync")
+    ap.add_argument("--vals", default="0,1")
     args = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for sh in args.shapes.split(","):
@@ -27,10 +29,10 @@ def main():
         C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         fns = {"cublas": lambda: torch.matmul(A, B.t(), out=C)}
         for S in map(int, args.s.split(",")):
-            for wv in (0, 1):
+            for wv in map(int, args.vals.split(",")):
                 pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0)
-                pl.set_option("wave_sync", wv)
-                fns[f"S={S} wave={wv}"] = (lambda pl=pl: fo.gemm_stage(pl, A, B, C))
+                pl.set_option(args.opt, wv)
+                fns[f"S={S} {args.opt}={wv}"] = (lambda pl=pl: fo.gemm_stage(pl, A, B, C))
         for f in fns.values():
             f()
         torch.cuda.synchronize()
@@ -47,7 +49,7 @@ def main():
         fl = 2.0 * M * N * K
         for k, v in ts.items():
             med = statistics.median(v)
-            print(f"{sh:20s} {k:14s} median {med:9.1f} us {fl / med / 1e6:7.1f} TF", flush=True)
+            print(f"{sh:20s} {k:18s} median {med:9.1f} us {fl / med / 1e6:7.1f} TF", flush=True)
         del A, B, C
 
 
