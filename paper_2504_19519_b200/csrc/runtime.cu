@@ -546,13 +546,18 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     if (!wait) fail(FO_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
     const bool rowband = (h.coll == FO_NOCOMM) || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND);
     void* gemm_dst = rowband ? out : p->d_send;
+    // a single group issued in stream order (R32) waits on no counter: the GEMM
+    // then neither signals nor needs the counting table reset
+    const bool counted = !(p->last_in_order && h.coll != FO_NOCOMM && h.P == 1);
     // 1. counting table reset (every run starts from zero)
-    FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
-    // 2. fork
-    FO_CUDA(cudaEventRecord(c->ev_fork, s));
-    FO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+    if (counted || p->split > 1) FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
+    // 2. fork (nothing to fork when the single group runs on s)
+    if (counted) {
+      FO_CUDA(cudaEventRecord(c->ev_fork, s));
+      FO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+    }
     // 3. GEMM with reorder + signal epilogue
-    run_gemm(p, A, Bt, gemm_dst, epi_mode(h), true, s, p->trace_tile_ts);
+    run_gemm(p, A, Bt, gemm_dst, epi_mode(h), counted, s, p->trace_tile_ts);
     const bool gpost = use_group_post(p) && !p->combine;
     const void* post_src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : p->d_recv);
     // 4. per-group wait + collective; the per-group post-reorder runs on the
@@ -575,8 +580,10 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
         const bool on_s = last_on_s && j == h.P - 1;
         cudaStream_t cs = on_s ? s : c->comm_stream;
         if (on_s) {
-          FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
-          FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+          if (h.P > 1) {
+            FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
+            FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+          }
         } else {
           stream_wait(p, wait, cs, j);
         }
@@ -615,7 +622,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
       FO_CUDA(cudaEventRecord(c->ev_join, c->comm_stream));
       FO_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
     }
-    if (gpost && h.coll != FO_NOCOMM) {
+    if (gpost && h.coll != FO_NOCOMM && !(last_on_s && h.P == 1)) {
       FO_CUDA(cudaEventRecord(c->ev_post_join, c->post_stream));
       FO_CUDA(cudaStreamWaitEvent(s, c->ev_post_join, 0));
     }

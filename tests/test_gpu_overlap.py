@@ -198,3 +198,32 @@ def test_last_group_in_order_equals_counter_trigger(ctx, coll, post, layout):
         fo.run(ctx, p_off, A, Bt, o2, res, gam)
         torch.cuda.synchronize()
         assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("coll,post,layout", [("allreduce", "none", "rowband"), ("allreduce", "add", "slot"),
+                                              ("allreduce", "add_rmsnorm", "rowband"),
+                                              ("reducescatter", "add", "auto"), ("alltoall", "none", "auto")])
+def test_single_group_in_order_equals_sequential(ctx, coll, post, layout):
+    """One group issued in stream order (R32): no counters, no fork — the
+    overlapped op must equal fo_run_sequential bit for bit, repeatedly."""
+    M, N, K, S = 2048, 1024, 512, 8
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+              group_waves=[4], ar_layout=layout, post=post)
+    if coll == "alltoall":
+        kw["row_dst"] = np.zeros(M, np.int32)
+        plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
+    else:
+        plan = fo.Plan(**kw)
+    A, Bt = synthetic.float_inputs(M, N, K, seed=35, device="cuda")
+    rows = plan.info["out_rows"]
+    res = synthetic.normal_bf16((rows, N), 1.0, 36, device="cuda") if post != "none" else None
+    gam = synthetic.normal_bf16((N,), 1.0, 37, device="cuda") if post == "add_rmsnorm" else None
+    want = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
+    fo.run_sequential(ctx, plan, A, Bt, want, res, gam)
+    got = torch.empty_like(want)
+    for _ in range(10):
+        plan.fill_buffers(0x7FC0)
+        got.fill_(float("nan"))
+        fo.run(ctx, plan, A, Bt, got, res, gam)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)

@@ -298,6 +298,8 @@ def test_tail_split_exact(ctx1, BM, BN, M, N, K, S, split):
     for coll in ("nocomm", "allreduce"):
         plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2, ar_layout="slot")
         plan.set_option("tail_split", split)
+        # one group: keep it counter-triggered so the counting table is exercised (R32)
+        plan.set_option("last_group_in_order", 0)
         out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         Ad, Bd = _dev_bf16(A), _dev_bf16(Bt)
         for _ in range(3):  # flags must reset between runs
