@@ -50,6 +50,31 @@ def main():
     if not torch.equal(out.cpu(), (A2.double() @ B2.double().t()).to(torch.bfloat16)):
         print("mismatch tail split")
         bad += 1
+    # TMA multicast across clusters of two pairs (FO_OPT_MULTICAST), an odd
+    # tile count (solo final round), and multi-group runs with the last group
+    # in stream order vs counter-triggered (R32), single in-order group
+    for bn in (128, 256):
+        Mm, Nm = 256 * 3, 256 * 3
+        A3, B3 = synthetic.exact_inputs(Mm, Nm, 256, seed=3, nnz_per_row=100)
+        plan = fo.Plan(coll="nocomm", m=Mm, n=Nm, k=256, tile_m=256, tile_n=bn, workers=4, swizzle=2)
+        plan.set_option("multicast", 1)
+        out = torch.empty(Mm, Nm, dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, A3.cuda(), B3.cuda(), out)
+        torch.cuda.synchronize()
+        if not torch.equal(out.cpu(), (A3.double() @ B3.double().t()).to(torch.bfloat16)):
+            print("mismatch multicast", bn)
+            bad += 1
+    for lio in (0, 1):
+        for groups in ([1, 1, 1], [3]):
+            plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=3, swizzle=2,
+                           group_waves=groups, ar_layout="slot")
+            plan.set_option("last_group_in_order", lio)
+            out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+            fo.run(ctx, plan, Ad, Bd, out)
+            torch.cuda.synchronize()
+            if not torch.equal(out, C):
+                print("mismatch last_group_in_order", lio, groups)
+                bad += 1
     # fused RMSNorm + row exchange
     plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=3, post="add_rmsnorm")
     local = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
