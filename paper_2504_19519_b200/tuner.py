@@ -347,9 +347,10 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     for S in cands:
         T = -(-tiles // S)
         for layout in layouts:
-            if layout == "rowband" and S % Nt:
-                continue          # waves of whole tile-rows only
-            swz = 1 if layout == "rowband" else 0
+            # multi-group ROWBAND needs waves of whole tile-rows; one group of
+            # every tile is a band (the whole output) for any S and order
+            single_only = layout == "rowband" and S % Nt != 0
+            swz = 1 if (layout == "rowband" and not single_only) else 0
             probe = Plan(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
                          group_waves=[T], ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world)
             gp = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S,
@@ -359,6 +360,10 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
             per_group = post_us(layout if layout != "auto" else "slot", per_group_op) / out_bytes
             tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
             eff = effective_curve(curve, per_group)
+            if single_only:
+                pred = tune_predict([T], dur, tiles, S, tile_m * tile_n * 2, eff)
+                evaluated.append((S, layout, [T], pred + tail, dur, swz))
+                continue
             G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, eff)
             evaluated.append((S, layout, list(G), pred + tail, dur, swz))
             if T <= all_partitions_T:

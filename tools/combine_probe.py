@@ -48,6 +48,22 @@ def main():
             byts = tokens * N * 2 * (k + 1 + (1 if with_res else 0))
             print(f"tokens={tokens} N={N} k={k} residual={with_res}: {us:.1f} us, {byts / us / 1e3:.0f} GB/s "
                   f"algorithmic ({byts / us / 1e3 / hbm:.2f} of {hbm:.0f} GB/s)", flush=True)
+        # achievable gather bandwidth at this size: torch.index_select of the same rows
+        flat = idx.flatten().long()
+        g = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
+        ts = []
+        for _ in range(20):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch.index_select(recv, 0, flat, out=g)
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e) * 1e3)
+        us = sorted(ts)[10]
+        byts = 2 * rows * N * 2
+        print(f"    torch.index_select of the same {rows} rows: {us:.1f} us, {byts / us / 1e3:.0f} GB/s "
+              f"({byts / us / 1e3 / hbm:.2f})", flush=True)
 
 
 if __name__ == "__main__":

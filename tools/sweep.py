@@ -14,9 +14,27 @@ import torch  # noqa: E402
 import paper_2504_19519_b200 as fo  # noqa: E402
 import synthetic  # noqa: E402
 from paper_2504_19519_b200 import tuner  # noqa: E402
-from tools.gemm_probe import timeit  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def interleaved(fns, flush, iters=10):
+    import statistics
+
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    ts = [[] for _ in fns]
+    for _ in range(iters):
+        for i, f in enumerate(fns):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            f()
+            e.record()
+            torch.cuda.synchronize()
+            ts[i].append(s.elapsed_time(e) * 1e3)
+    return [statistics.median(t) for t in ts]
 
 
 def main():
@@ -33,16 +51,18 @@ def main():
             A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.cell_seed(M, N, K), device="cuda")
             C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
             fl = 2.0 * M * N * K
-            t_cb = timeit(lambda: torch.matmul(A, Bt.t(), out=C), iters=10, flush=flush)
             tiles = (M // 256) * (N // 256)
             ch = tuner.tune_layer(M, N, K, ctx, "allreduce", "none")
             S, T, groups = ch.workers, -(-tiles // ch.workers), ch.groups
             plan = fo.Plan(**ch.spec(M, N, K, "allreduce"))
             gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
                             tile_order=plan.export_order())
-            t_fo = timeit(lambda: fo.gemm_stage(gplan, A, Bt, C), iters=10, flush=flush)
-            t_ov = timeit(lambda: fo.run(ctx, plan, A, Bt, C), iters=10, flush=flush)
-            t_sq = timeit(lambda: fo.run_sequential(ctx, plan, A, Bt, C), iters=10, flush=flush)
+            # interleaved (one flushed run of each per round, medians) so clock /
+            # power drift hits the four alike
+            t_cb, t_fo, t_ov, t_sq = interleaved([lambda: torch.matmul(A, Bt.t(), out=C),
+                                                  lambda: fo.gemm_stage(gplan, A, Bt, C),
+                                                  lambda: fo.run(ctx, plan, A, Bt, C),
+                                                  lambda: fo.run_sequential(ctx, plan, A, Bt, C)], flush)
             tf = fl / t_fo / 1e6
             print(f"{M:6d} {NK:6d} {tiles:5d} {S:3d} {T:3d} {fl / t_cb / 1e6:9.1f} {tf:7.1f} {tf / peak:5.2f} "
                   f"{t_ov:9.1f} {t_sq:8.1f} {t_sq / t_ov:7.3f} {'rowband' if plan.info['ar_layout'] == 1 else 'slot':7s} "
