@@ -64,6 +64,7 @@ def parse():
                     help="S = concurrent tile workers (CTA pairs); default: fewest workers with the same wave count as all SMs")
     ap.add_argument("--groups", default=None, help="explicit wave-group partition, e.g. 1,1,2 (default: Alg. 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-shards", action="store_true", help="skip the other configs' per-rank layers")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle sample")
     return ap.parse_args()
 
@@ -382,6 +383,44 @@ def main():
     ov_us, seq_us, gk_us, cb_us = m["ov"], m["seq"], m["gemm"], m["cublas"]
     launches = launches_per_step * args.steps
 
+    # ---- the other BASELINE.json configs' per-rank layers (their exchange
+    # needs the other ranks): the GEMM writing row-major C, the same GEMM with
+    # the layer's pre-communication reorder + signal epilogue (AR slot / RS
+    # subtiles / A2A pools — the paper's epilogue overhead),
+    # and cuBLAS on the same shard, interleaved
+    shards = {}
+    if world == 1 and not args.no_shards:
+        for name, Ms, Ns, Ks, coll in (("llama3-8b-down-proj tp2 shard (AR)", 4096, 4096, 7168, "allreduce"),
+                                       ("llama3-8b-down-proj tp4 shard (AR)", 4096, 4096, 3584, "allreduce"),
+                                       ("llama3-8b-down-proj tp8 shard (AR)", 4096, 4096, 1792, "allreduce"),
+                                       ("llama3-70b-o-proj tp8 shard (RS)", 8192, 8192, 1024, "reducescatter"),
+                                       ("mixtral-8x7b-w2 ep8 expert (A2A)", 1024, 4096, 14336, "alltoall")):
+            As_, Bs_ = synthetic.float_inputs(Ms, Ns, Ks, seed=synthetic.cell_seed(Ms, Ns, Ks), device="cuda")
+            Cs_ = torch.empty(Ms, Ns, dtype=torch.bfloat16, device="cuda")
+            t_ = (Ms // BM) * (Ns // BN)
+            Sw = -(-t_ // -(-t_ // (sms // cg)))
+            Tw = -(-t_ // Sw)
+            kw_ = dict(coll=coll, m=Ms, n=Ns, k=Ks, tile_m=BM, tile_n=BN, workers=Sw, swizzle=0,
+                       group_waves=[1] * Tw, ar_layout="slot" if coll == "allreduce" else "auto")
+            if coll == "alltoall":
+                kw_["row_dst"] = np.zeros(Ms, np.int32)
+                sp_ = fo.Plan(rank=0, world=1, peers=[kw_], **kw_)
+            else:
+                sp_ = fo.Plan(**kw_)
+            gp_ = fo.Plan(coll="nocomm", m=Ms, n=Ns, k=Ks, tile_m=BM, tile_n=BN, workers=Sw,
+                          tile_order=sp_.export_order())
+            send_ = torch.empty(sp_.info["send_elems"], dtype=torch.bfloat16, device="cuda")
+            mm = timed_multi({"gemm": lambda: fo.gemm_stage(gp_, As_, Bs_, Cs_),
+                              "epi": lambda: fo.gemm_stage(sp_, As_, Bs_, send_),
+                              "cublas": lambda: torch.matmul(As_, Bs_.t(), out=Cs_)}, 10, 2)
+            fl_ = 2.0 * Ms * Ns * Ks
+            shards[name] = {"M": Ms, "N": Ns, "K_loc": Ks, "workers": Sw, "waves": Tw,
+                            "gemm_us": round(mm["gemm"], 2), "gemm_tflops": round(fl_ / mm["gemm"] / 1e6, 1),
+                            "reorder_epilogue_us": round(mm["epi"], 2),
+                            "epilogue_overhead_pct": round(100.0 * (mm["epi"] / mm["gemm"] - 1.0), 2),
+                            "cublas_us": round(mm["cublas"], 2)}
+            del As_, Bs_, Cs_, send_
+
     # ---- e2e through the public API with host (pinned) buffers
     A_pin = A_h.pin_memory()
     out_pin = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
@@ -456,6 +495,7 @@ def main():
                     "note": "fo_run_host: activations A host->device (pinned; 8 tile-row chunks the GEMM "
                             "producer waits on), output device->host per row band right after its "
                             "collective; the weights are resident in HBM"},
+            "shard_layers_n1": shards or None,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

@@ -275,9 +275,12 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& p, int u, int KB) {
   return r;
 }
 
-// Destination of row `a` (0..TM-1) of the TM x BN tile at position `pos` = (ti, tj).
+// Destination of row `a` (0..TM-1) of the TM x BN tile at position `pos` =
+// (ti, tj); `rs_ps` / `rs_G` = first position and size of the tile's group
+// (RS), looked up once per tile by the caller.
 template <int TM, int BN>
-__device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, int ti, int tj, int a) {
+__device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, int ti, int tj, int a, int rs_ps,
+                                                  int rs_G) {
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.dst);
   switch (p.mode) {
     case EPI_ROWMAJOR:
@@ -285,10 +288,8 @@ __device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, in
     case EPI_SLOT:  // slot pos, row-major
       return base + ((int64_t)pos * TM + a) * BN;
     case EPI_RS: {  // subtile k = a / h goes to chunk k of the group
-      const int g = p.group_of_pos[pos];
-      const int ps = p.gpos[g], G = p.gpos[g + 1] - ps;
       const int k = a / p.h, a2 = a - k * p.h;
-      return base + ((int64_t)ps * TM + (int64_t)k * G * p.h + (int64_t)(pos - ps) * p.h + a2) * BN;
+      return base + ((int64_t)rs_ps * TM + (int64_t)k * rs_G * p.h + (int64_t)(pos - rs_ps) * p.h + a2) * BN;
     }
     default:  // EPI_A2A: row -> slot in its destination pool
       return base + (int64_t)p.row_slot[(int64_t)pos * TM + a] * BN;
@@ -536,6 +537,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
+      // this lane's 8 destination rows of the tile (rows it*4 + lane/8 of the
+      // warp's 32-row quarter), resolved once per tile
+      __nv_bfloat16* drow[8];
+      {
+        int rs_ps = 0, rs_G = 0;
+        if (p.mode == EPI_RS) {
+          const int g = p.group_of_pos[pos];
+          rs_ps = p.gpos[g];
+          rs_G = p.gpos[g + 1] - rs_ps;
+        }
+#pragma unroll
+        for (int it = 0; it < 8; ++it)
+          drow[it] = row_dst<TM, BN>(p, pos, ti, tj, (int)half * BM + q * 32 + it * 4 + (lane >> 3), rs_ps, rs_G) +
+                     (lane & 7) * 8;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / EPI_COLS; ++c) {
         uint32_t v[64];
@@ -594,8 +610,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int r = it * 4 + (lane >> 3);
           const int ch = lane & 7;
           const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + ch * 16);
-          __nv_bfloat16* d = row_dst<TM, BN>(p, pos, ti, tj, (int)half * BM + q * 32 + r) + c * EPI_COLS + ch * 8;
-          *reinterpret_cast<uint4*>(d) = w;
+          *reinterpret_cast<uint4*>(drow[it] + c * EPI_COLS) = w;
         }
         __syncwarp();
       }

@@ -51,7 +51,7 @@ def _draw(seed):
                 swizzle=swizzle, layout=layout, multicast=multicast)
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(64))
 def test_random_plan_matches_oracle(seed):
     c = _draw(seed)
     M, N, K, BM, BN, n, S = c["M"], c["N"], c["K"], c["BM"], c["BN"], c["n"], c["S"]
