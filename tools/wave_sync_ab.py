@@ -41,6 +41,7 @@ def main():
             for k, f in fns.items():
                 flush.zero_()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda._sleep(200_000)  # pre-load: device time only
                 s.record()
                 f()
                 e.record()
