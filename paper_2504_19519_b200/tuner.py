@@ -277,7 +277,7 @@ def compositions(T: int) -> list:
 
 
 def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_n=TILE_N, device=0,
-               sizes=None, iters=10, min_comm_sms=16, verify=6, all_partitions_T=7) -> LayerChoice:
+               sizes=None, iters=10, min_comm_sms=16, verify=8, all_partitions_T=7) -> LayerChoice:
     """Joint choice of S (wave width), layout and wave groups for one layer
     (AllReduce / ReduceScatter; world from the context).
 
@@ -309,31 +309,41 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     gam = torch.randn(N, device="cuda").to(torch.bfloat16)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    def timeit(fn):
-        for _ in range(2):
-            fn()
+    def timeit_many(fns, rounds):
+        """Device time of each fn: round-robin (one flushed run of each per
+        round) with the stream pre-loaded by a sleep kernel, medians — clock /
+        power drift hits every candidate alike and host enqueue is excluded."""
+        for f in fns:
+            for _ in range(2):
+                f()
         torch.cuda.synchronize()
-        tot = 0.0
-        for _ in range(iters):
-            flush.zero_()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            fn()
-            e.record()
-            torch.cuda.synchronize()
-            tot += s.elapsed_time(e) * 1e3
-        return tot / iters
+        ts = [[] for _ in fns]
+        for _ in range(rounds):
+            for i, f in enumerate(fns):
+                flush.zero_()
+                s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda._sleep(200_000)
+                s0.record()
+                f()
+                e0.record()
+                torch.cuda.synchronize()
+                ts[i].append(s0.elapsed_time(e0) * 1e3)
+        return [sorted(v)[len(v) // 2] for v in ts]
+
+    post_cache = {}
 
     def post_us(layout, op):
         """Full-output post pass of `layout` with `op`, measured standalone."""
         if op == "none" and layout == "rowband":
             return 0.0
-        pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tile_m, tile_n=tile_n, workers=min(tiles, sms // 2),
-                  swizzle=1, ar_layout=layout if coll == "allreduce" else "auto", post=op, rank=ctx.rank,
-                  world=world)
-        recv = torch.zeros(pl.info["recv_elems"], dtype=torch.bfloat16, device="cuda")
-        o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
-        return timeit(lambda: post_stage(pl, recv, o, res, gam))
+        if (layout, op) not in post_cache:
+            pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tile_m, tile_n=tile_n, workers=min(tiles, sms // 2),
+                      swizzle=1, ar_layout=layout if coll == "allreduce" else "auto", post=op, rank=ctx.rank,
+                      world=world)
+            recv = torch.zeros(pl.info["recv_elems"], dtype=torch.bfloat16, device="cuda")
+            o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+            post_cache[(layout, op)] = timeit_many([lambda: post_stage(pl, recv, o, res, gam)], iters)[0]
+        return post_cache[(layout, op)]
 
     out_bytes = out_rows * N * 2
     layouts = ("rowband", "slot") if coll == "allreduce" else ("auto",)
@@ -344,6 +354,9 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         # the collective's kernels need SMs the persistent GEMM leaves free
         # (Alg. 1 line 3); without them nothing overlaps
         cands = [c for c in cands if sms - cg * c >= min_comm_sms] or [min(cands)]
+    # offline stage (1): the GEMM in each candidate's execution order, all
+    # candidates timed together (round-robin)
+    probes = []
     for S in cands:
         T = -(-tiles // S)
         for layout in layouts:
@@ -355,22 +368,24 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
                          group_waves=[T], ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world)
             gp = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S,
                       tile_order=probe.export_order())
-            dur = timeit(lambda: gemm_stage(gp, A, Bt, out))
-            per_group_op = post if (layout == "rowband" or post != "add_rmsnorm") else "none"
-            per_group = post_us(layout if layout != "auto" else "slot", per_group_op) / out_bytes
-            tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
-            eff = effective_curve(curve, per_group)
-            if single_only:
-                pred = tune_predict([T], dur, tiles, S, tile_m * tile_n * 2, eff)
-                evaluated.append((S, layout, [T], pred + tail, dur, swz))
-                continue
-            G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, eff)
-            evaluated.append((S, layout, list(G), pred + tail, dur, swz))
-            if T <= all_partitions_T:
-                for comp in compositions(T):
-                    if comp != list(G):
-                        p2 = tune_predict(comp, dur, tiles, S, tile_m * tile_n * 2, eff)
-                        evaluated.append((S, layout, comp, p2 + tail, dur, swz))
+            probes.append((S, T, layout, single_only, swz, gp))
+    durs = timeit_many([(lambda gp=pr[5]: gemm_stage(gp, A, Bt, out)) for pr in probes], iters)
+    for (S, T, layout, single_only, swz, _), dur in zip(probes, durs):
+        per_group_op = post if (layout == "rowband" or post != "add_rmsnorm") else "none"
+        per_group = post_us(layout if layout != "auto" else "slot", per_group_op) / out_bytes
+        tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
+        eff = effective_curve(curve, per_group)
+        if single_only:
+            pred = tune_predict([T], dur, tiles, S, tile_m * tile_n * 2, eff)
+            evaluated.append((S, layout, [T], pred + tail, dur, swz))
+            continue
+        G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, eff)
+        evaluated.append((S, layout, list(G), pred + tail, dur, swz))
+        if T <= all_partitions_T:
+            for comp in compositions(T):
+                if comp != list(G):
+                    p2 = tune_predict(comp, dur, tiles, S, tile_m * tile_n * 2, eff)
+                    evaluated.append((S, layout, comp, p2 + tail, dur, swz))
     import torch.distributed as dist
 
     def agree(obj):
@@ -381,43 +396,40 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         return obj
 
     evaluated = sorted(evaluated, key=lambda e: e[3])
-    # the single-group plan (no overlap: the whole GEMM, then one collective)
-    # is always among the verified candidates, so the chosen split is never
-    # one measured slower than not splitting at all
+    # the verified set: the best prediction of every (S, layout) (the
+    # predictor ranks across wave widths only through noisy GEMM durations),
+    # the single-group plan (no overlap: the whole GEMM, then one collective —
+    # so the chosen split is never one measured slower than not splitting),
+    # then the global ranking, up to `verify` plans
+    nv = max(1, verify)
+    chosen = []
+    for e in evaluated:
+        if not any(c[0] == e[0] and c[1] == e[1] for c in chosen):
+            chosen.append(e)
     single = [e for e in evaluated if len(e[2]) == 1]
-    if single and not any(len(e[2]) == 1 for e in evaluated[:max(1, verify)]):
+    if single:
         best1 = min(single, key=lambda e: (e[1] != "rowband", e[3]))
-        evaluated.remove(best1)
-        evaluated.insert(max(1, verify) - 1, best1)
-    evaluated = agree(evaluated)
+        if best1 not in chosen:
+            chosen.append(best1)
+    for e in evaluated:
+        if len(chosen) >= nv:
+            break
+        if e not in chosen:
+            chosen.append(e)
+    evaluated = chosen + [e for e in evaluated if e not in chosen]
+    evaluated, nv = agree((evaluated, len(chosen)))
     from . import run as fo_run
 
-    # verification: the candidates are timed round-robin (one flushed run of
-    # each per round, `iters` rounds) and ranked by their median, so clock /
-    # power drift hits all of them alike and one lucky run cannot win
+    # verification: the candidates' fo_run timed round-robin, medians
     runs = []
-    for (S, layout, G, pred, dur, swz) in evaluated[:max(1, verify)]:
+    for (S, layout, G, pred, dur, swz) in evaluated[:nv]:
         spec = dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
                     group_waves=G, ar_layout=layout if layout != "auto" else "auto", post=post)
         pl = Plan(rank=ctx.rank, world=world, **spec)
         o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
         args = (res, gam) if post != "none" else (None, None)
         runs.append((pl, o, args))
-    for pl, o, args in runs:
-        for _ in range(2):
-            fo_run(ctx, pl, A, Bt, o, *args)
-    torch.cuda.synchronize()
-    samples = [[] for _ in runs]
-    for _ in range(max(3, iters)):
-        for i, (pl, o, args) in enumerate(runs):
-            flush.zero_()
-            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record()
-            fo_run(ctx, pl, A, Bt, o, *args)
-            e0.record()
-            torch.cuda.synchronize()
-            samples[i].append(s0.elapsed_time(e0) * 1e3)
-    measured = [sorted(v)[len(v) // 2] for v in samples]
+    measured = timeit_many([(lambda r=r: fo_run(ctx, r[0], A, Bt, r[1], *r[2])) for r in runs], max(3, iters))
     if world > 1 and dist.is_initialized():
         tt = torch.tensor(measured, device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
