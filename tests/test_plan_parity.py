@@ -184,6 +184,19 @@ def test_error_contract():
         fo.Plan(**{**base, "ar_layout": "rowband", "swizzle": 2, "group_waves": [1, 1]})
 
 
+def test_option_contract():
+    """fo_plan_set_option validates names and ranges on the host (no GPU)."""
+    pl = fo.Plan(coll="allreduce", m=256, n=256, k=64, tile_m=256, tile_n=128, workers=2)
+    for name, good, bad in (("last_group_in_order", (0, 1), (2, -1)), ("wave_sync", (0, 1), (2,)),
+                            ("multicast", (0, 1), (2,)), ("wait_kernel", (0, 1), (2,)),
+                            ("group_post", (-1, 0, 1), (2,)), ("host_pipeline", (0, 3), (4,))):
+        for v in good:
+            pl.set_option(name, v)
+        for v in bad:
+            with pytest.raises(fo.FOError, match="INVALID_ARG"):
+                pl.set_option(name, v)
+
+
 def test_tuner_matches_oracle():
     rng = np.random.default_rng(5)
     for _ in range(60):
