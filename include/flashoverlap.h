@@ -209,7 +209,11 @@ fo_status fo_combine_stage(fo_plan plan, const void* recv, void* out, const int3
  *   residual (FO_POST_ADD*): device bf16, same shape as out; gamma (RMSNorm): device bf16 [n].
  * Internals: counters reset, GEMM on the caller stream, per group a
  * stream-side wait (counter >= |G_j|) then the NCCL call on the comm stream,
- * post-reorder, join back to `stream`. */
+ * post-reorder, join back to `stream`; the last group's collective follows
+ * the GEMM on `stream` itself (FO_OPT_LAST_GROUP_IN_ORDER, default), and a
+ * single group then needs no counters, signals or fork at all (GEMM ->
+ * collective).  Errors: FO_ERR_STATE when the plan's rank/world differ from
+ * the context's; FO_ERR_CUDA / FO_ERR_NCCL wrap failed launches or calls. */
 fo_status fo_run(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
                  const void* residual, const void* gamma, void* stream);
 /* fo_run with HOST buffers (same shapes as fo_run): stream-ordered
