@@ -266,6 +266,16 @@ fo_status fo_rowexchange_stage(fo_plan plan, const void* gathered, void* out, co
  * device: 1 (128-row tiles), 2 (CTA pair, 256-row tiles) or 4 (two pairs with
  * TMA multicast, FO_OPT_MULTICAST).  Binds the plan to the device like a run. */
 fo_status fo_plan_gemm_cluster(fo_plan plan, int32_t* cluster_ctas);
+/* Debug watchdog (a hang from mismatched plans across ranks, a lost signal):
+ * wait up to timeout_ms for everything enqueued on `stream` (fo_run joins
+ * all of its streams into it) to finish.  FO_OK when it does.  Otherwise
+ * every counter of the plan is forced past any target so the pending trigger
+ * waits release, the context's NCCL communicator is aborted (ncclCommAbort:
+ * NCCL kernels still stuck on absent peers exit), the streams drain, the
+ * context refuses further runs (FO_ERR_STATE; destroy it and create a new
+ * one; the run's output is undefined), and FO_ERR_TIMEOUT is returned.
+ * Host-blocking; not graph-capturable. */
+fo_status fo_plan_sync(fo_ctx ctx, fo_plan plan, void* stream, int64_t timeout_ms);
 /* Copy the plan's P counters to host (synchronises the device). */
 fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
 /* Debug / evidence hooks (tests, tools; never needed for correct use):
@@ -331,10 +341,14 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      TMA-multicast to both pairs (17% fewer L2 sectors);
  *                      results are identical.  Measured 12-20% slower: the
  *                      shared stage-release barriers couple the two pairs'
- *                      pipelines (profiles/r01_multicast.txt), hence off */
+ *                      pipelines (profiles/r01_multicast.txt), hence off
+ *  FO_OPT_DEBUG_STALL_GROUP -1 — off; j — TEST ONLY: group j's trigger waits for
+ *                      one more signal than the GEMM sends, so the run never
+ *                      finishes (exercises the fo_plan_sync watchdog) */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
-               FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8 } fo_option;
+               FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8,
+               FO_OPT_DEBUG_STALL_GROUP = 10 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

@@ -225,6 +225,12 @@ def run(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=
                         _stream(stream)))
 
 
+def plan_sync(ctx: Context, plan: Plan, stream=None, timeout_ms: int = 10000):
+    """fo_plan_sync: the debug watchdog — wait for the plan's last run with a
+    timeout; on timeout the context is aborted and FOError(FO_ERR_TIMEOUT) raised."""
+    check(load().fo_plan_sync(ctx._h, plan.handle, _stream(stream), int(timeout_ms)))
+
+
 def run_host(ctx: Context, plan: Plan, A, Bt, out, residual=None, gamma=None, stream=None):
     """fo_run_host: A, Bt, out (and residual, gamma) are CPU tensors (pin them for async copies)."""
     check(load().fo_run_host(ctx._h, plan.handle, _ptr(A), _ptr(Bt), _ptr(out), _ptr(residual), _ptr(gamma),

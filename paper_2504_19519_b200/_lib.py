@@ -20,7 +20,7 @@ COLL = {"allreduce": 0, "reducescatter": 1, "alltoall": 2, "nocomm": 3}
 LAYOUT = {"slot": 0, "rowband": 1, "auto": 2}
 POST = {"none": 0, "add": 1, "add_rmsnorm": 2}
 OPTION = {"group_post": 0, "wait_kernel": 1, "tail_split": 2, "post_sm_partition": 3, "host_pipeline": 4, "host_chunks": 5,
-          "last_group_in_order": 6, "wave_sync": 7, "multicast": 8}
+          "last_group_in_order": 6, "wave_sync": 7, "multicast": 8, "debug_stall_group": 10}
 
 
 class FOError(RuntimeError):
@@ -87,6 +87,7 @@ _SIGS = [
     ("fo_run_combine", C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     ("fo_plan_read_counters", C.c_int, [_P, C.POINTER(C.c_uint32)]),
     ("fo_plan_gemm_cluster", C.c_int, [_P, C.POINTER(C.c_int32)]),
+    ("fo_plan_sync", C.c_int, [_P, _P, _P, C.c_int64]),
     ("fo_kernel_launch_count", C.c_int64, []),
     ("fo_plan_set_debug", C.c_int, [_P, _P, _P, C.c_int32]),
     ("fo_plan_fill_buffers", C.c_int, [_P, C.c_uint16, _P]),

@@ -19,7 +19,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <thread>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -29,6 +31,7 @@
 
 struct fo_ctx_s {
   int device = 0;
+  bool aborted = false;                // the watchdog (fo_plan_sync) aborted the communicator
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -270,7 +273,8 @@ static ncclDataType_t bf16() { return ncclBfloat16; }
 // reaches its target — a front-end stream wait (no SM) or the paper's
 // signaling kernel (a 1-warp spin on an acquire load).
 static void stream_wait(fo_plan_s* p, WaitValue32Fn wait, cudaStream_t cs, int j) {
-  const cuuint32_t target = signal_target(p->host, j);
+  // FO_OPT_DEBUG_STALL_GROUP: one more signal than the GEMM will ever send
+  const cuuint32_t target = signal_target(p->host, j) + (j == p->debug_stall_group ? 1u : 0u);
   if (p->wait_kernel) {
     FO_CUDA(launch_wait(p->d_counters + j, target, cs));
     return;
@@ -540,6 +544,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
     const PlanHost& h = p->host;
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
+    if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
     ensure_device(p);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     WaitValue32Fn wait = wait_value_fn();
@@ -751,6 +756,7 @@ fo_status fo_run_sequential(fo_ctx c, fo_plan p, const void* A, const void* Bt, 
                             const void* gamma, void* stream) {
   return guard([&] {
     if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
     const PlanHost& h = p->host;
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
     ensure_device(p);
@@ -838,6 +844,7 @@ fo_status fo_run_allgather(fo_ctx c, fo_plan p, const void* local, void* out, co
                            const void* gamma, int32_t row_exchange, void* stream) {
   return guard([&] {
     if (!c || !p || !local || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
     const PlanHost& h = p->host;
     if (h.coll != FO_REDUCESCATTER) fail(FO_ERR_INVALID_ARG, "AllGather follow-on needs a ReduceScatter plan");
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
@@ -954,6 +961,58 @@ fo_status fo_run_combine(fo_ctx c, fo_plan p, const void* A, const void* Bt, voi
   });
 }
 
+// Debug watchdog (H8): wait for the plan's last run on `stream` with a
+// timeout.  On timeout the communicator is aborted (in-flight NCCL kernels
+// exit), every counter of the plan is forced past any target so pending
+// stream waits / spin kernels release and the streams drain, and the context
+// refuses further runs.
+fo_status fo_plan_sync(fo_ctx c, fo_plan p, void* stream, int64_t timeout_ms) {
+  return guard([&] {
+    if (!c || !p) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (timeout_ms < 0) fail(FO_ERR_INVALID_ARG, "timeout_ms must be >= 0");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaEvent_t ev = nullptr;
+    FO_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    struct EvGuard {
+      cudaEvent_t e;
+      ~EvGuard() { cudaEventDestroy(e); }
+    } eg{ev};
+    FO_CUDA(cudaEventRecord(ev, s));
+    auto drained = [&](int64_t ms) {
+      const auto t0 = std::chrono::steady_clock::now();
+      while (true) {
+        const cudaError_t q = cudaEventQuery(ev);
+        if (q == cudaSuccess) return true;
+        if (q != cudaErrorNotReady) fail(FO_ERR_CUDA, "cudaEventQuery: %s", cudaGetErrorString(q));
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(ms)) return false;
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+      }
+    };
+    if (drained(timeout_ms)) return;
+    c->aborted = true;
+    // 1. release the trigger waits: every counter past any target (from a
+    //    fresh non-blocking stream; the stuck streams cannot run a memset)
+    if (p->d_counters) {
+      cudaStream_t rescue = nullptr;
+      FO_CUDA(cudaStreamCreateWithFlags(&rescue, cudaStreamNonBlocking));
+      FO_CUDA(cudaMemsetAsync(p->d_counters, 0x3f, sizeof(uint32_t) * p->ctr_words, rescue));
+      cudaStreamSynchronize(rescue);
+      cudaStreamDestroy(rescue);
+    }
+    // 2. the released NCCL calls either complete (peers present) or, still
+    //    stuck after another timeout, are killed by aborting the communicator
+    //    (ncclCommAbort makes in-flight NCCL kernels exit)
+    const bool done = drained(std::max<int64_t>(timeout_ms, 1000));
+    if (c->comm) {
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+    }
+    if (!done) drained(std::max<int64_t>(timeout_ms, 1000));
+    fail(FO_ERR_TIMEOUT, "plan run did not finish within %lld ms: waits released, communicator aborted",
+         (long long)timeout_ms);
+  });
+}
+
 fo_status fo_plan_read_counters(fo_plan p, uint32_t* counters) {
   return guard([&] {
     if (!p || !counters) fail(FO_ERR_INVALID_ARG, "null argument");
@@ -977,6 +1036,7 @@ int64_t fo_kernel_launch_count(void) { return launch_count(); }
 fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t iters, double* avg_us) {
   return guard([&] {
     if (!c || !avg_us || bytes <= 0 || iters < 1) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
     FO_CUDA(cudaSetDevice(c->device));
     const int W = c->world;
     const size_t count = (size_t)(bytes / 2 / W) * W;  // bf16 elements, divisible by world
@@ -1066,6 +1126,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_HOST_PIPELINE:
         if (value < 0 || value > 3) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..3");
         p->host_pipeline = (int)value;
+        break;
+      case FO_OPT_DEBUG_STALL_GROUP:
+        if (value < -1 || value >= p->host.P) fail(FO_ERR_INVALID_ARG, "debug_stall_group must be -1..P-1");
+        p->debug_stall_group = (int)value;
         break;
       case FO_OPT_MULTICAST:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "multicast must be 0 or 1");

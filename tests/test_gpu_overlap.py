@@ -227,3 +227,34 @@ def test_single_group_in_order_equals_sequential(ctx, coll, post, layout):
         fo.run(ctx, plan, A, Bt, got, res, gam)
         torch.cuda.synchronize()
         assert torch.equal(got, want)
+
+
+def test_watchdog_times_out_and_releases():
+    """fo_plan_sync (the debug watchdog, SURVEY §8(b) FO_ERR_TIMEOUT): a run
+    whose group 0 can never fire (FO_OPT_DEBUG_STALL_GROUP) is detected, the
+    communicator aborted, the waits released (the streams drain), and the
+    context refuses further runs; a healthy run syncs OK."""
+    c = fo.Context.create(0, 0, 1, fo.unique_id())
+    M, N, K, S = 2048, 1024, 512, 8
+    kw = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=2,
+              group_waves=[1, 2, 1], ar_layout="slot")
+    A, Bt = synthetic.float_inputs(M, N, K, seed=41, device="cuda")
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    good = fo.Plan(**kw)
+    fo.run(c, good, A, Bt, out)
+    fo.plan_sync(c, good, timeout_ms=5000)
+    for wait_kernel in (0, 1):
+        c2 = fo.Context.create(0, 0, 1, fo.unique_id())
+        bad = fo.Plan(**kw)
+        bad.set_option("wait_kernel", wait_kernel)
+        bad.set_option("debug_stall_group", 0)
+        fo.run(c2, bad, A, Bt, out)
+        with pytest.raises(fo.FOError, match="TIMEOUT"):
+            fo.plan_sync(c2, bad, timeout_ms=300)
+        torch.cuda.synchronize()          # everything drained after the release
+        with pytest.raises(fo.FOError, match="STATE"):
+            fo.run(c2, bad, A, Bt, out)
+        c2.close()
+    fo.run(c, good, A, Bt, out)           # other contexts are unaffected
+    fo.plan_sync(c, good, timeout_ms=5000)
+    c.close()
