@@ -30,8 +30,10 @@ struct GemmArgs {
   const int32_t* group_of_pos; // [tiles] device
   const int32_t* gpos;         // [P+1] device
   const int32_t* row_slot;     // [tiles*BM] device (A2A)
+  const int2* rs_info;         // [tiles] device (RS): {first position, size} of the position's group
   uint32_t* counters;          // [P] device, may be null
-  int h;                       // RS subtile rows
+  int h;                       // RS subtile rows (tile_m / world, a power of two)
+  int h_log2;
   unsigned long long* tile_ts; // optional [tiles] device: %globaltimer at signal
   // ---- tail split (split-K of the last partial wave across idle workers)
   int units;                   // work units: tail_pos + (tiles - tail_pos) * split

@@ -277,22 +277,23 @@ __device__ __forceinline__ Unit decode_unit(const GemmArgs& p, int u, int KB) {
 
 // Destination of row `a` (0..TM-1) of the TM x BN tile at position `pos` =
 // (ti, tj); `rs_ps` / `rs_G` = first position and size of the tile's group
-// (RS), looked up once per tile by the caller.
+// (RS) and `a2a_slot` = row_slot[pos*TM + a] (A2A), loaded by the caller one
+// tile ahead.
 template <int TM, int BN>
 __device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, int ti, int tj, int a, int rs_ps,
-                                                  int rs_G) {
+                                                  int rs_G, int a2a_slot) {
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.dst);
   switch (p.mode) {
     case EPI_ROWMAJOR:
       return base + ((int64_t)ti * TM + a) * p.ldc + (int64_t)tj * BN;
     case EPI_SLOT:  // slot pos, row-major
       return base + ((int64_t)pos * TM + a) * BN;
-    case EPI_RS: {  // subtile k = a / h goes to chunk k of the group
-      const int k = a / p.h, a2 = a - k * p.h;
-      return base + ((int64_t)rs_ps * TM + (int64_t)k * rs_G * p.h + (int64_t)(pos - rs_ps) * p.h + a2) * BN;
+    case EPI_RS: {  // subtile k = a / h goes to chunk k of the group (h = 2^h_log2)
+      const int k = a >> p.h_log2, a2 = a & (p.h - 1);
+      return base + ((int64_t)rs_ps * TM + (((k * rs_G + (pos - rs_ps)) << p.h_log2) + a2)) * BN;
     }
-    default:  // EPI_A2A: row -> slot in its destination pool
-      return base + (int64_t)p.row_slot[(int64_t)pos * TM + a] * BN;
+    default:  // EPI_A2A: row -> slot in its destination pool (row_slot, prefetched)
+      return base + (int64_t)a2a_slot * BN;
   }
 }
 
@@ -518,6 +519,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader0 = (CG == 1) ? 0u : mapa_shared(&tempty[0], lead_rank);
     int acc = 0;
     uint32_t aphase = 0;
+    // destination-table entries of the next tile (RS: group start / size of
+    // the position; A2A: this lane's 8 row slots), loaded one tile ahead
+    int2 nx_rs = make_int2(0, 0);
+    int32_t nx_slot[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) nx_slot[it] = 0;
+    auto prefetch_dst = [&](int npos) {
+      if (p.mode == EPI_RS) {
+        nx_rs = p.rs_info[npos];
+      } else if (p.mode == EPI_A2A) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it)
+          nx_slot[it] = p.row_slot[(int64_t)npos * TM + (int)half * BM + q * 32 + it * 4 + (lane >> 3)];
+      }
+    };
+    if (worker < p.units) prefetch_dst(decode_unit(p, worker, KB).pos);
     for (int u = worker; u < p.units; u += nworkers) {
       const Unit un = decode_unit(p, u, KB);
       const int pos = un.pos;
@@ -526,7 +543,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool tail = (pos >= p.tail_pos) && p.split > 1;
       const int tt = pos - p.tail_pos;  // tail tile index
       const int row = (int)half * BM + q * 32 + lane;  // this thread's accumulator row in the tile
+      // this lane's 8 destination rows of the tile (rows it*4 + lane/8 of the
+      // warp's 32-row quarter), resolved once per tile from table entries
+      // loaded during the previous tile (no memory latency here: at short K
+      // the epilogue is on the critical path)
+      __nv_bfloat16* drow[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it)
+        drow[it] = row_dst<TM, BN>(p, pos, ti, tj, (int)half * BM + q * 32 + it * 4 + (lane >> 3), nx_rs.x, nx_rs.y,
+                                   nx_slot[it]) +
+                   (lane & 7) * 8;
       mbar_wait(&tfull[acc], aphase);
+      if (u + nworkers < p.units) prefetch_dst(decode_unit(p, u + nworkers, KB).pos);
       tc_fence_after();
       if (tail && un.slice == 0) {
         // owner of a split tile: wait until the other K-slices' partials of
@@ -536,21 +564,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           while (ld_acquire(f) < (uint32_t)(p.split - 1)) __nanosleep(32);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-      }
-      // this lane's 8 destination rows of the tile (rows it*4 + lane/8 of the
-      // warp's 32-row quarter), resolved once per tile
-      __nv_bfloat16* drow[8];
-      {
-        int rs_ps = 0, rs_G = 0;
-        if (p.mode == EPI_RS) {
-          const int g = p.group_of_pos[pos];
-          rs_ps = p.gpos[g];
-          rs_G = p.gpos[g + 1] - rs_ps;
-        }
-#pragma unroll
-        for (int it = 0; it < 8; ++it)
-          drow[it] = row_dst<TM, BN>(p, pos, ti, tj, (int)half * BM + q * 32 + it * 4 + (lane >> 3), rs_ps, rs_G) +
-                     (lane & 7) * 8;
       }
 #pragma unroll 1
       for (int c = 0; c < BN / EPI_COLS; ++c) {

@@ -105,7 +105,7 @@ void release_device(fo_plan_s* p) {
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
                     p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma,
-                    (void*)p->d_ws, (void*)p->d_a_ready, (void*)p->d_wave})
+                    (void*)p->d_ws, (void*)p->d_a_ready, (void*)p->d_wave, (void*)p->d_rs_info})
     if (ptr) cudaFree(ptr);
   cudaSetDevice(cur);
   p->device = -1;
@@ -134,6 +134,14 @@ static void ensure_device(fo_plan_s* p) {
   p->d_group_of_pos = upload(h.group_of_pos);
   p->d_gpos = upload(h.gpos);
   p->d_row_slot = upload(h.row_slot);
+  if (h.coll == FO_REDUCESCATTER) {
+    std::vector<int2> info(h.tiles);
+    for (int q = 0; q < h.tiles; ++q) {
+      const int g = h.group_of_pos[q];
+      info[q] = make_int2(h.gpos[g], h.gpos[g + 1] - h.gpos[g]);
+    }
+    p->d_rs_info = upload(info);
+  }
   p->d_src_row = upload(h.src_row);
   p->d_recv_dst = upload(h.recv_dst);
   // ---- tail split: the R tiles of the last partial wave split into f K-slices
@@ -190,8 +198,11 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   a.group_of_pos = p->d_group_of_pos;
   a.gpos = p->d_gpos;
   a.row_slot = p->d_row_slot;
+  a.rs_info = p->d_rs_info;
   a.counters = signal ? p->d_counters : nullptr;
   a.h = h.h;
+  a.h_log2 = 0;
+  while ((1 << a.h_log2) < h.h) ++a.h_log2;
   a.tile_ts = nullptr;
   a.units = p->units;
   a.tail_pos = p->tail_pos;

@@ -16,6 +16,7 @@ struct fo_plan_s {
   int32_t* d_group_of_pos = nullptr;
   int32_t* d_gpos = nullptr;
   int32_t* d_row_slot = nullptr;
+  int2* d_rs_info = nullptr;        // RS: per position {group's first position, group size}
   int32_t* d_src_row = nullptr;
   uint32_t* d_counters = nullptr;
   void* d_send = nullptr;  // pre-reordered send buffer (bf16), library-owned
