@@ -436,10 +436,14 @@ def main():
     out_pin = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
 
     # the host path is PCIe-bound: the plan that hides most of it has one wave
-    # per group in row bands (the GEMM starts on the first A chunk and every
-    # band goes back to the host right after its collective)
-    Nt_ = N // BN
-    S_e = S if S % Nt_ == 0 else max(Nt_, (min(tiles, sms // cg) // Nt_) * Nt_)
+    # per group in row bands of ~1/8 of the output (the GEMM starts on the
+    # first A chunk, keeps pace with the 8 chunk copies, and every band goes
+    # back to the host right after its collective; the exposed tail is one
+    # band's GEMM + D2H — profiles/r01_e2e_probe2.txt)
+    Nt_, Mt_ = N // BN, M // BM
+    S_e = Nt_ * max(1, Mt_ // 8)
+    if S_e > sms // cg:
+        S_e = S if S % Nt_ == 0 else max(Nt_, (min(tiles, sms // cg) // Nt_) * Nt_)
     T_e = (tiles + S_e - 1) // S_e
     e2e_spec = dict(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S_e, swizzle=1,
                     group_waves=[1] * T_e, ar_layout="rowband")

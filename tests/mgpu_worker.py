@@ -7,8 +7,8 @@ NCCL over NVLink, per-group post-reorder) and fo_run_sequential on
 exact-integer inputs, and compares both with the plain definition computed by
 this script with torch.distributed in fp32 (exact for these integers):
 AllReduce = sum_r C_r; ReduceScatter = rows R_k of the sum (block-cyclic,
-DESIGN.md R8); All-to-All = concat over sources of the rows routed here
-(R9).  Exit status 0 = every comparison bit-exact.  Test infrastructure.
+DESIGN.md R8), and its AllGather + row exchange = the AllReduce result;
+All-to-All = concat over sources of the rows routed here (R9).  Exit status 0 = every comparison bit-exact.  Test infrastructure.
 """
 import os
 import sys
@@ -72,6 +72,13 @@ def main():
         fo.run_sequential(ctx, plan, A, Bt, seq)
         torch.cuda.synchronize()
         check(f"{coll}/{layout}/{groups}/sequential", seq, want, bad)
+        if coll == "reducescatter":
+            # RS follow-on (NEXT f2): AllGather + row exchange restores the
+            # standard row order, i.e. the AllReduce result
+            gathered = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+            fo.run_allgather(ctx, plan, out, gathered)
+            torch.cuda.synchronize()
+            check("reducescatter/allgather+rowexchange", gathered, full.to(torch.bfloat16), bad)
     # All-to-All (EP combine): imbalanced experts, random routing
     rng = np.random.default_rng(7)
     Ms = [256 * int(rng.integers(1, 5)) for _ in range(world)]
