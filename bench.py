@@ -363,7 +363,8 @@ def main():
     out2 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     out_cb = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     # the GEMM-only timing uses exactly the overlapped plan's execution order
-    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=plan.export_order())
+    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=plan.export_order(),
+                    options=spec.get("options"))
 
     # ---- full-size spot check (N=1: sampled rows vs an fp64 torch CPU product; not the oracle)
     fo.run(ctx, plan, A, Bt, out)
@@ -484,6 +485,7 @@ def main():
             "config": {**{k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective", "tile")},
                        "workers": S, "comm_sms": sms - cg * S, "nccl_max_ctas": comm_sms if world > 1 else None,
                        "waves": T, "groups": list(groups), "swizzle_order": "auto (DESIGN.md R25)",
+                       "tail_split": (spec.get("options") or {}).get("tail_split", 0),
                        "ar_layout": "rowband" if plan.info["ar_layout"] == 1 else "slot",
                        "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"tp{world}",
                        "timing": "device time: CUDA events on the launching stream, pre-loaded by a ~100 us sleep "

@@ -81,7 +81,8 @@ class Plan:
     """Host plan of one rank (fo_plan_create).  `peers` (All-to-All only): the
     PlanSpec of every rank, gathered by the caller (see dist.gather_specs)."""
 
-    def __init__(self, rank: int = 0, world: int = 1, peers: Optional[Sequence[PlanSpec]] = None, **kw):
+    def __init__(self, rank: int = 0, world: int = 1, peers: Optional[Sequence[PlanSpec]] = None,
+                 options: Optional[dict] = None, **kw):
         lib = load()
         self.spec = PlanSpec(**kw)
         self.rank, self.world = rank, world
@@ -103,6 +104,8 @@ class Plan:
         info = _lib.PlanInfoC()
         check(lib.fo_plan_get_info(h, C.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in info._fields_}
+        for name, value in (options or {}).items():   # fo_plan_set_option, e.g. {"tail_split": -1}
+            self.set_option(name, value)
 
     @property
     def handle(self):

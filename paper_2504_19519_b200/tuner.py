@@ -242,12 +242,16 @@ class LayerChoice:
     layout: str          # "rowband" | "slot" (AllReduce) | "auto"
     predicted_us: float
     gemm_us: float
-    candidates: list     # (workers, layout, groups, predicted_us, gemm_us) of every candidate evaluated
+    candidates: list     # (workers, layout[+tailsplit], groups, predicted_us, gemm_us[, measured_us])
+    tail_split: int = 0  # FO_OPT_TAIL_SPLIT of the chosen plan (0 off, -1 auto)
 
     def spec(self, M, N, K, coll, post="none", tile_m=TILE_M, tile_n=TILE_N) -> dict:
-        return dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=self.workers,
-                    swizzle=self.swizzle, group_waves=list(self.groups),
-                    ar_layout=self.layout if coll == "allreduce" else "auto", post=post)
+        d = dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=self.workers,
+                 swizzle=self.swizzle, group_waves=list(self.groups),
+                 ar_layout=self.layout if coll == "allreduce" else "auto", post=post)
+        if self.tail_split:
+            d["options"] = {"tail_split": self.tail_split}
+        return d
 
 
 def candidate_workers(tiles: int, Nt: int, sms: int, coll: str, cg: int = 2) -> list:
@@ -366,26 +370,30 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
             swz = 1 if (layout == "rowband" and not single_only) else 0
             probe = Plan(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
                          group_waves=[T], ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world)
-            gp = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S,
-                      tile_order=probe.export_order())
-            probes.append((S, T, layout, single_only, swz, gp))
+            # the last partial wave split along K over the idle workers
+            # (FO_OPT_TAIL_SPLIT auto: when 2R <= S for R tail tiles)
+            R = tiles - (T - 1) * S
+            for split in ((0, -1) if 0 < R and 2 * R <= S and K >= 128 else (0,)):
+                gp = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S,
+                          tile_order=probe.export_order(), options={"tail_split": split} if split else None)
+                probes.append((S, T, layout, single_only, swz, gp, split))
     durs = timeit_many([(lambda gp=pr[5]: gemm_stage(gp, A, Bt, out)) for pr in probes], iters)
-    for (S, T, layout, single_only, swz, _), dur in zip(probes, durs):
+    for (S, T, layout, single_only, swz, _, split), dur in zip(probes, durs):
         per_group_op = post if (layout == "rowband" or post != "add_rmsnorm") else "none"
         per_group = post_us(layout if layout != "auto" else "slot", per_group_op) / out_bytes
         tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
         eff = effective_curve(curve, per_group)
         if single_only:
             pred = tune_predict([T], dur, tiles, S, tile_m * tile_n * 2, eff)
-            evaluated.append((S, layout, [T], pred + tail, dur, swz))
+            evaluated.append((S, layout, [T], pred + tail, dur, swz, split))
             continue
         G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, eff)
-        evaluated.append((S, layout, list(G), pred + tail, dur, swz))
+        evaluated.append((S, layout, list(G), pred + tail, dur, swz, split))
         if T <= all_partitions_T:
             for comp in compositions(T):
                 if comp != list(G):
                     p2 = tune_predict(comp, dur, tiles, S, tile_m * tile_n * 2, eff)
-                    evaluated.append((S, layout, comp, p2 + tail, dur, swz))
+                    evaluated.append((S, layout, comp, p2 + tail, dur, swz, split))
     import torch.distributed as dist
 
     def agree(obj):
@@ -404,7 +412,7 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     nv = max(1, verify)
     chosen = []
     for e in evaluated:
-        if not any(c[0] == e[0] and c[1] == e[1] for c in chosen):
+        if not any(c[0] == e[0] and c[1] == e[1] and c[6] == e[6] for c in chosen):
             chosen.append(e)
     single = [e for e in evaluated if len(e[2]) == 1]
     if single:
@@ -422,10 +430,10 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
 
     # verification: the candidates' fo_run timed round-robin, medians
     runs = []
-    for (S, layout, G, pred, dur, swz) in evaluated[:nv]:
+    for (S, layout, G, pred, dur, swz, split) in evaluated[:nv]:
         spec = dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
                     group_waves=G, ar_layout=layout if layout != "auto" else "auto", post=post)
-        pl = Plan(rank=ctx.rank, world=world, **spec)
+        pl = Plan(rank=ctx.rank, world=world, options={"tail_split": split} if split else None, **spec)
         o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
         args = (res, gam) if post != "none" else (None, None)
         runs.append((pl, o, args))
@@ -436,5 +444,6 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         measured = tt.tolist()
     k = min(range(len(measured)), key=lambda i: measured[i])
     best = evaluated[k]
-    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4],
-                       [e[:5] + ((measured[i],) if i < len(measured) else ()) for i, e in enumerate(evaluated)])
+    cands = [(e[0], e[1] + ("+tailsplit" if e[6] else ""), e[2], e[3], e[4]) +
+             ((measured[i],) if i < len(measured) else ()) for i, e in enumerate(evaluated)]
+    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], cands, best[6])

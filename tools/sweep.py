@@ -56,7 +56,7 @@ def main():
             S, T, groups = ch.workers, -(-tiles // ch.workers), ch.groups
             plan = fo.Plan(**ch.spec(M, N, K, "allreduce"))
             gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
-                            tile_order=plan.export_order())
+                            tile_order=plan.export_order(), options=ch.spec(M, N, K, "allreduce").get("options"))
             # interleaved (one flushed run of each per round, medians) so clock /
             # power drift hits the four alike
             t_cb, t_fo, t_ov, t_sq = interleaved([lambda: torch.matmul(A, Bt.t(), out=C),
@@ -65,7 +65,8 @@ def main():
                                                   lambda: fo.run_sequential(ctx, plan, A, Bt, C)], flush)
             tf = fl / t_fo / 1e6
             print(f"{M:6d} {NK:6d} {tiles:5d} {S:3d} {T:3d} {fl / t_cb / 1e6:9.1f} {tf:7.1f} {tf / peak:5.2f} "
-                  f"{t_ov:9.1f} {t_sq:8.1f} {t_sq / t_ov:7.3f} {'rowband' if plan.info['ar_layout'] == 1 else 'slot':7s} "
+                  f"{t_ov:9.1f} {t_sq:8.1f} {t_sq / t_ov:7.3f} "
+                  f"{('rowband' if plan.info['ar_layout'] == 1 else 'slot') + ('+ts' if ch.tail_split else ''):10s} "
                   f"{list(groups)}", flush=True)
             del A, Bt, C
             torch.cuda.empty_cache()
