@@ -341,8 +341,9 @@ def main():
         nspec = dict(spec, post="add_rmsnorm")
         pred_n = pred
     else:
-        ch = fot.tune_layer(M, N, K, ctx, "allreduce", "none", tile_m=BM, tile_n=BN, device=local)
-        chn = fot.tune_layer(M, N, K, ctx, "allreduce", "add_rmsnorm", tile_m=BM, tile_n=BN, device=local)
+        shapes = [(BM, BN), (128, 256)]      # CTA-pair 256x256 and single-CTA 128x256 tiles
+        ch = fot.tune_layer(M, N, K, ctx, "allreduce", "none", device=local, tile_shapes=shapes)
+        chn = fot.tune_layer(M, N, K, ctx, "allreduce", "add_rmsnorm", device=local, tile_shapes=shapes)
         if rank == 0:
             for name, c in (("plain", ch), ("fused", chn)):
                 for cand in c.candidates[:6]:
@@ -352,7 +353,12 @@ def main():
         S, groups, pred = ch.workers, tuple(ch.groups), ch.predicted_us
         spec, nspec, pred_n = ch.spec(M, N, K, "allreduce"), chn.spec(M, N, K, "allreduce", "add_rmsnorm"), \
             chn.predicted_us
-        T = (tiles + S - 1) // S
+    # the chosen tile shape (tune_layer searches it; the explicit --workers /
+    # --groups path keeps 256x256)
+    BMc, BNc = spec["tile_m"], spec["tile_n"]
+    cgc = BMc // 128
+    tiles_c = (M // BMc) * (N // BNc)
+    T = (tiles_c + S - 1) // S
     plan = fo.Plan(rank=rank, world=world, **spec)
     # fused-op convention (R17): the same layer followed by
     # residual add + RMSNorm, fused into the (per-band) post-communication pass
@@ -363,8 +369,8 @@ def main():
     out2 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     out_cb = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     # the GEMM-only timing uses exactly the overlapped plan's execution order
-    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, tile_order=plan.export_order(),
-                    options=spec.get("options"))
+    gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BMc, tile_n=BNc, workers=S,
+                    tile_order=plan.export_order(), options=spec.get("options"))
 
     # ---- full-size spot check (N=1: sampled rows vs an fp64 torch CPU product; not the oracle)
     fo.run(ctx, plan, A, Bt, out)
@@ -464,7 +470,8 @@ def main():
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
-        traffic = tr.get(f"{M}x{N}x{K}/{BM}x{BN}/S{S}")
+        ts_key = "/ts" if (spec.get("options") or {}).get("tail_split") else ""
+        traffic = tr.get(f"{M}x{N}x{K}/{BMc}x{BNc}/S{S}{ts_key}")
     except Exception:
         pass
 
@@ -482,8 +489,8 @@ def main():
             "value": round(ov_us, 2), "unit": "us", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ov_us / 1e3, 4), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) weights)",
-            "config": {**{k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective", "tile")},
-                       "workers": S, "comm_sms": sms - cg * S, "nccl_max_ctas": comm_sms if world > 1 else None,
+            "config": {**{k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective")},
+                       "tile": f"{BMc}x{BNc}", "workers": S, "comm_sms": sms - cgc * S, "nccl_max_ctas": comm_sms if world > 1 else None,
                        "waves": T, "groups": list(groups), "swizzle_order": "auto (DESIGN.md R25)",
                        "tail_split": (spec.get("options") or {}).get("tail_split", 0),
                        "ar_layout": "rowband" if plan.info["ar_layout"] == 1 else "slot",
@@ -500,7 +507,7 @@ def main():
                                   "layout": "rowband" if nplan.info["ar_layout"] == 1 else "slot",
                                   "alg1_predicted_us": round(pred_n, 2),
                                   "note": "GEMM+AR+residual add+RMSNorm; overlapped runs the fused op per row band"},
-            "roofline": {"bound": "tensor", "kernel": f"fo_gemm_tcgen05_kernel<{BN},{cg}>", "achieved": round(achieved, 1),
+            "roofline": {"bound": "tensor", "kernel": f"fo_gemm_tcgen05_kernel<{BNc},{cgc}>", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed alone per step)",
                          "frac_of_sustained_peak": round(achieved / peaks.get("bf16_tflops_sustained", peak), 4),

@@ -242,11 +242,13 @@ class LayerChoice:
     layout: str          # "rowband" | "slot" (AllReduce) | "auto"
     predicted_us: float
     gemm_us: float
-    candidates: list     # (workers, layout[+tailsplit], groups, predicted_us, gemm_us[, measured_us])
+    candidates: list     # (workers, tile:layout[+tailsplit], groups, predicted_us, gemm_us[, measured_us])
     tail_split: int = 0  # FO_OPT_TAIL_SPLIT of the chosen plan (0 off, -1 auto)
+    tile_m: int = TILE_M
+    tile_n: int = TILE_N
 
-    def spec(self, M, N, K, coll, post="none", tile_m=TILE_M, tile_n=TILE_N) -> dict:
-        d = dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=self.workers,
+    def spec(self, M, N, K, coll, post="none") -> dict:
+        d = dict(coll=coll, m=M, n=N, k=K, tile_m=self.tile_m, tile_n=self.tile_n, workers=self.workers,
                  swizzle=self.swizzle, group_waves=list(self.groups),
                  ar_layout=self.layout if coll == "allreduce" else "auto", post=post)
         if self.tail_split:
@@ -281,7 +283,8 @@ def compositions(T: int) -> list:
 
 
 def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_n=TILE_N, device=0,
-               sizes=None, iters=10, min_comm_sms=16, verify=8, all_partitions_T=7) -> LayerChoice:
+               sizes=None, iters=10, min_comm_sms=16, verify=8, all_partitions_T=7,
+               tile_shapes=None) -> LayerChoice:
     """Joint choice of S (wave width), layout and wave groups for one layer
     (AllReduce / ReduceScatter; world from the context).
 
@@ -301,9 +304,13 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     from . import post_stage
 
     sms = device_sm_count(device)
-    Mt, Nt = M // tile_m, N // tile_n
-    tiles = Mt * Nt
     world = ctx.world
+    # tile shapes searched (PAPER.md:460 leaves the GEMM configuration to the
+    # tuner): those that tile the output and, for RS, split by world
+    shapes = [(tm, tn) for tm, tn in (tile_shapes or [(tile_m, tile_n)])
+              if M % tm == 0 and N % tn == 0 and (coll != "reducescatter" or tm % world == 0)]
+    if not shapes:
+        raise ValueError("no tile shape divides the layer")
     curve = ctx.sample_curve(coll, sizes or [1 << s for s in range(18, 28)], iters=3)
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     Bt = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
@@ -336,64 +343,70 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
 
     post_cache = {}
 
-    def post_us(layout, op):
+    def post_us(layout, op, tm, tn):
         """Full-output post pass of `layout` with `op`, measured standalone."""
         if op == "none" and layout == "rowband":
             return 0.0
-        if (layout, op) not in post_cache:
-            pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tile_m, tile_n=tile_n, workers=min(tiles, sms // 2),
+        key = (layout, op, tm, tn)
+        if key not in post_cache:
+            t_ = (M // tm) * (N // tn)
+            pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tm, tile_n=tn, workers=min(t_, sms // (tm // 128)),
                       swizzle=1, ar_layout=layout if coll == "allreduce" else "auto", post=op, rank=ctx.rank,
                       world=world)
             recv = torch.zeros(pl.info["recv_elems"], dtype=torch.bfloat16, device="cuda")
             o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
-            post_cache[(layout, op)] = timeit_many([lambda: post_stage(pl, recv, o, res, gam)], iters)[0]
-        return post_cache[(layout, op)]
+            post_cache[key] = timeit_many([lambda: post_stage(pl, recv, o, res, gam)], iters)[0]
+        return post_cache[key]
 
     out_bytes = out_rows * N * 2
     layouts = ("rowband", "slot") if coll == "allreduce" else ("auto",)
     evaluated = []
-    cg = tile_m // 128
-    cands = candidate_workers(tiles, Nt, sms, coll, cg)
-    if world > 1:
-        # the collective's kernels need SMs the persistent GEMM leaves free
-        # (Alg. 1 line 3); without them nothing overlaps
-        cands = [c for c in cands if sms - cg * c >= min_comm_sms] or [min(cands)]
     # offline stage (1): the GEMM in each candidate's execution order, all
-    # candidates timed together (round-robin)
+    # candidates (tile shape x S x layout x tail split) timed together
     probes = []
-    for S in cands:
-        T = -(-tiles // S)
-        for layout in layouts:
-            # multi-group ROWBAND needs waves of whole tile-rows; one group of
-            # every tile is a band (the whole output) for any S and order
-            single_only = layout == "rowband" and S % Nt != 0
-            swz = 1 if (layout == "rowband" and not single_only) else 0
-            probe = Plan(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
-                         group_waves=[T], ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world)
-            # the last partial wave split along K over the idle workers
-            # (FO_OPT_TAIL_SPLIT auto: when 2R <= S for R tail tiles)
-            R = tiles - (T - 1) * S
-            for split in ((0, -1) if 0 < R and 2 * R <= S and K >= 128 else (0,)):
-                gp = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S,
-                          tile_order=probe.export_order(), options={"tail_split": split} if split else None)
-                probes.append((S, T, layout, single_only, swz, gp, split))
+    for tm, tn in shapes:
+        Nt = N // tn
+        tiles = (M // tm) * Nt
+        cg = tm // 128
+        cands = candidate_workers(tiles, Nt, sms, coll, cg)
+        if world > 1:
+            # the collective's kernels need SMs the persistent GEMM leaves free
+            # (Alg. 1 line 3); without them nothing overlaps
+            cands = [c for c in cands if sms - cg * c >= min_comm_sms] or [min(cands)]
+        for S in cands:
+            T = -(-tiles // S)
+            for layout in layouts:
+                # multi-group ROWBAND needs waves of whole tile-rows; one group of
+                # every tile is a band (the whole output) for any S and order
+                single_only = layout == "rowband" and S % Nt != 0
+                swz = 1 if (layout == "rowband" and not single_only) else 0
+                probe = Plan(coll=coll, m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S, swizzle=swz,
+                             group_waves=[T], ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank,
+                             world=world)
+                # the last partial wave split along K over the idle workers
+                # (FO_OPT_TAIL_SPLIT auto: when 2R <= S for R tail tiles)
+                R = tiles - (T - 1) * S
+                for split in ((0, -1) if 0 < R and 2 * R <= S and K >= 128 else (0,)):
+                    gp = Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S,
+                              tile_order=probe.export_order(), options={"tail_split": split} if split else None)
+                    probes.append((S, T, layout, single_only, swz, gp, split, tm, tn, tiles))
     durs = timeit_many([(lambda gp=pr[5]: gemm_stage(gp, A, Bt, out)) for pr in probes], iters)
-    for (S, T, layout, single_only, swz, _, split), dur in zip(probes, durs):
+    for (S, T, layout, single_only, swz, _, split, tm, tn, tiles), dur in zip(probes, durs):
         per_group_op = post if (layout == "rowband" or post != "add_rmsnorm") else "none"
-        per_group = post_us(layout if layout != "auto" else "slot", per_group_op) / out_bytes
-        tail = post_us("slot", "add_rmsnorm") if (layout != "rowband" and post == "add_rmsnorm") else 0.0
+        per_group = post_us(layout if layout != "auto" else "slot", per_group_op, tm, tn) / out_bytes
+        tail = post_us("slot", "add_rmsnorm", tm, tn) if (layout != "rowband" and post == "add_rmsnorm") else 0.0
         eff = effective_curve(curve, per_group)
         if single_only:
-            pred = tune_predict([T], dur, tiles, S, tile_m * tile_n * 2, eff)
-            evaluated.append((S, layout, [T], pred + tail, dur, swz, split))
+            pred = tune_predict([T], dur, tiles, S, tm * tn * 2, eff)
+            evaluated.append((S, layout, [T], pred + tail, dur, swz, split, tm, tn))
             continue
-        G, pred = tune_search(dur, tiles, S, tile_m * tile_n * 2, eff)
-        evaluated.append((S, layout, list(G), pred + tail, dur, swz, split))
+        G, pred = tune_search(dur, tiles, S, tm * tn * 2, eff)
+        evaluated.append((S, layout, list(G), pred + tail, dur, swz, split, tm, tn))
         if T <= all_partitions_T:
             for comp in compositions(T):
                 if comp != list(G):
-                    p2 = tune_predict(comp, dur, tiles, S, tile_m * tile_n * 2, eff)
-                    evaluated.append((S, layout, comp, p2 + tail, dur, swz, split))
+                    p2 = tune_predict(comp, dur, tiles, S, tm * tn * 2, eff)
+                    evaluated.append((S, layout, comp, p2 + tail, dur, swz, split, tm, tn))
     import torch.distributed as dist
 
     def agree(obj):
@@ -412,7 +425,7 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     nv = max(1, verify)
     chosen = []
     for e in evaluated:
-        if not any(c[0] == e[0] and c[1] == e[1] and c[6] == e[6] for c in chosen):
+        if not any(c[0] == e[0] and c[1] == e[1] and c[6:9] == e[6:9] for c in chosen):
             chosen.append(e)
     single = [e for e in evaluated if len(e[2]) == 1]
     if single:
@@ -430,8 +443,8 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
 
     # verification: the candidates' fo_run timed round-robin, medians
     runs = []
-    for (S, layout, G, pred, dur, swz, split) in evaluated[:nv]:
-        spec = dict(coll=coll, m=M, n=N, k=K, tile_m=tile_m, tile_n=tile_n, workers=S, swizzle=swz,
+    for (S, layout, G, pred, dur, swz, split, tm, tn) in evaluated[:nv]:
+        spec = dict(coll=coll, m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S, swizzle=swz,
                     group_waves=G, ar_layout=layout if layout != "auto" else "auto", post=post)
         pl = Plan(rank=ctx.rank, world=world, options={"tail_split": split} if split else None, **spec)
         o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
@@ -444,6 +457,6 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         measured = tt.tolist()
     k = min(range(len(measured)), key=lambda i: measured[i])
     best = evaluated[k]
-    cands = [(e[0], e[1] + ("+tailsplit" if e[6] else ""), e[2], e[3], e[4]) +
+    cands = [(e[0], f"{e[7]}x{e[8]}:" + e[1] + ("+tailsplit" if e[6] else ""), e[2], e[3], e[4]) +
              ((measured[i],) if i < len(measured) else ()) for i, e in enumerate(evaluated)]
-    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], cands, best[6])
+    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], cands, best[6], best[7], best[8])

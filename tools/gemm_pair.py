@@ -21,7 +21,8 @@ def main():
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--wave", type=int, default=1)
     ap.add_argument("--no-cublas", action="store_true")
-    ap.add_argument("--multicast", type=int, default=1)
+    ap.add_argument("--multicast", type=int, default=0)
+    ap.add_argument("--tail-split", type=int, default=0)
     args = ap.parse_args()
     M, N, K = map(int, args.shape.split("x"))
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
@@ -30,6 +31,7 @@ def main():
     plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=args.workers, swizzle=0)
     plan.set_option("wave_sync", args.wave)
     plan.set_option("multicast", args.multicast)
+    plan.set_option("tail_split", args.tail_split)
     for _ in range(args.iters):
         if not args.no_cublas:
             torch.matmul(A, B.t(), out=C)

@@ -51,11 +51,11 @@ def main():
             A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.cell_seed(M, N, K), device="cuda")
             C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
             fl = 2.0 * M * N * K
-            tiles = (M // 256) * (N // 256)
-            ch = tuner.tune_layer(M, N, K, ctx, "allreduce", "none")
+            ch = tuner.tune_layer(M, N, K, ctx, "allreduce", "none", tile_shapes=[(256, 256), (128, 256)])
+            tiles = (M // ch.tile_m) * (N // ch.tile_n)
             S, T, groups = ch.workers, -(-tiles // ch.workers), ch.groups
             plan = fo.Plan(**ch.spec(M, N, K, "allreduce"))
-            gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
+            gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=ch.tile_m, tile_n=ch.tile_n, workers=S,
                             tile_order=plan.export_order(), options=ch.spec(M, N, K, "allreduce").get("options"))
             # interleaved (one flushed run of each per round, medians) so clock /
             # power drift hits the four alike
@@ -67,6 +67,7 @@ def main():
             print(f"{M:6d} {NK:6d} {tiles:5d} {S:3d} {T:3d} {fl / t_cb / 1e6:9.1f} {tf:7.1f} {tf / peak:5.2f} "
                   f"{t_ov:9.1f} {t_sq:8.1f} {t_sq / t_ov:7.3f} "
                   f"{('rowband' if plan.info['ar_layout'] == 1 else 'slot') + ('+ts' if ch.tail_split else ''):10s} "
+                  f"{ch.tile_m}x{ch.tile_n} "
                   f"{list(groups)}", flush=True)
             del A, Bt, C
             torch.cuda.empty_cache()
