@@ -29,6 +29,7 @@ def interleaved(fns, flush, iters=10):
         for i, f in enumerate(fns):
             flush.zero_()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)  # pre-load the stream: device time, host enqueue excluded
             s.record()
             f()
             e.record()
