@@ -318,6 +318,34 @@ def test_tail_split_exact(ctx1, BM, BN, M, N, K, S, split):
             assert np.array_equal(_host(out), C)
 
 
+@pytest.mark.parametrize("post", ["none", "add_rmsnorm"])
+def test_tail_split_rowband_single_group(ctx1, post):
+    """The tuner's bench plan shape (R34): ROWBAND, one group, auto tail split,
+    through fo_run — the exact-integer output equals the plain GEMM, and the
+    fused add + RMSNorm equals the split-free plan's bit for bit."""
+    M, N, K, S = 1024, 1024, 512, 7           # 16 tiles of 256x256, T = 3, R = 2 -> f = 3
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=78, nnz_per_row=256)
+    C = onum.gemm(A, Bt)
+    kw = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0,
+              group_waves=[3], ar_layout="rowband", post=post)
+    on = fo.Plan(options={"tail_split": -1}, **kw)
+    off = fo.Plan(**kw)
+    assert on.info["ar_layout"] == 1
+    Ad, Bd = _dev_bf16(A), _dev_bf16(Bt)
+    res = synthetic.normal_bf16((M, N), 1.0, 79, device="cuda") if post != "none" else None
+    gam = synthetic.normal_bf16((N,), 1.0, 80, device="cuda") if post != "none" else None
+    o1 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    for _ in range(3):
+        o1.fill_(float("nan"))
+        fo.run(ctx1, on, Ad, Bd, o1, res, gam)
+        fo.run(ctx1, off, Ad, Bd, o2, res, gam)
+        torch.cuda.synchronize()
+        assert torch.equal(o1, o2)
+    if post == "none":
+        assert np.array_equal(_host(o1), C)
+
+
 def test_tail_split_rejects_oversubscription():
     plan = fo.Plan(coll="nocomm", m=1024, n=1024, k=128, tile_m=256, tile_n=256, workers=4)  # T=4, R=4
     plan.set_option("tail_split", 2)   # 4 tail tiles x 2 > S = 4
