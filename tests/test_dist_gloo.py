@@ -1,4 +1,4 @@
-"""Multi-process (gloo, world size 2, CPU) test of the n > 1 host logic.
+"""Multi-process (gloo, world size 2 and 4, CPU) test of the n > 1 host logic.
 
 Each process builds its plan through paper_2504_19519_b200.dist (peer census
 over the process group for All-to-All), then runs the method's data movement
@@ -32,7 +32,7 @@ def _inputs(n, r, M, N, K):
     return rng.integers(-3, 4, size=(M, K)).astype(float), rng.integers(-3, 4, size=(N, K)).astype(float)
 
 
-def _worker(rank, port, coll, errq):
+def _worker(rank, port, coll, errq, WORLD=2):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -43,7 +43,7 @@ def _worker(rank, port, coll, errq):
 
         N, K, BN = 256, 8, 128
         if coll == "alltoall":
-            Ms = [384, 256]                      # imbalanced experts
+            Ms = [384, 256, 512, 256][:WORLD]    # imbalanced experts; T >= 2 each
             M = Ms[rank]
             rds = [np.random.default_rng(5 + s).integers(0, WORLD, size=Ms[s]).astype(np.int32) for s in range(WORLD)]
             tiles = (M // 128) * (N // BN)
@@ -116,14 +116,15 @@ def _worker(rank, port, coll, errq):
         raise
 
 
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("coll", ["allreduce", "reducescatter", "alltoall"])
-def test_two_rank_plan_contract(coll):
+def test_multi_rank_plan_contract(coll, world):
     from paper_2504_19519_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, coll, errq)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, coll, errq, world)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
