@@ -150,7 +150,10 @@ static void ensure_device(fo_plan_s* p) {
     const int KB = (int)(h.K / 64);
     const int R = h.tiles - (h.T - 1) * h.S;
     int f = p->tail_split_req;
-    if (f < 0) f = (R > 0 && 2 * R <= h.S) ? std::min(4, h.S / R) : 1;
+    if (f < 0) {  // auto: never more slices than k-blocks; no split when under 2
+      f = (R > 0 && 2 * R <= h.S) ? std::min(std::min(4, h.S / R), KB) : 1;
+      if (f < 2) f = 1;
+    }
     if (f > 1 && (R * f > h.S || f > KB))
       fail(FO_ERR_INVALID_ARG, "tail split %d: %d tail tiles x %d slices exceed S=%d or k-blocks=%d", f, R, f, h.S, KB);
     p->split = (f > 1) ? f : 1;

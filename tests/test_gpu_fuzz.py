@@ -1,7 +1,8 @@
 """Seeded random plans through the C ABI vs the CPU oracle (exact-integer
 regime, bit-exact): tile shape, grid, K, world size, wave width S, explicit
 random order or default swizzle, random wave partition, AllReduce (both
-layouts) or ReduceScatter, with and without TMA-multicast clusters.  Every
+layouts) or ReduceScatter, with and without TMA-multicast clusters and the
+tail split; and All-to-All with imbalanced experts and random routing.  Every
 rank's GEMM + pre-reorder epilogue (fo_gemm_stage) must equal the oracle's
 send buffer, its counters the group thresholds, and the post-reorder of the
 oracle's receive buffer (fo_post_stage) the plain GEMM -> collective result
@@ -47,8 +48,9 @@ def _draw(seed):
     swizzle = int(rng.integers(0, 4))
     layout = str(rng.choice(["slot", "auto"]))
     multicast = int(rng.random() < 0.5)
+    tail_split = -1 if rng.random() < 0.3 else 0     # auto: only where the last wave qualifies
     return dict(BM=BM, BN=BN, M=Mt * BM, N=Nt * BN, K=K, n=n, coll=coll, S=S, part=part, order=order,
-                swizzle=swizzle, layout=layout, multicast=multicast)
+                swizzle=swizzle, layout=layout, multicast=multicast, tail_split=tail_split)
 
 
 @pytest.mark.parametrize("seed", range(64))
@@ -69,6 +71,7 @@ def test_random_plan_matches_oracle(seed):
         else:
             pl = fo.Plan(coll="reducescatter", rank=r, world=n, **kw)
         pl.set_option("multicast", c["multicast"])
+        pl.set_option("tail_split", c["tail_split"])
         plans.append(pl)
     # the oracle with the library's own execution order (swizzle 0 = auto is a
     # library heuristic; its order is pinned separately by the plan parity tests)
@@ -94,3 +97,51 @@ def test_random_plan_matches_oracle(seed):
         fo.post_stage(plans[r], _bf16(ores["recv"][r]), out)
         torch.cuda.synchronize()
         assert np.array_equal(out.double().cpu().numpy(), plain[r]), f"{c} rank {r} output"
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_a2a_plan_matches_oracle(seed):
+    """All-to-All: per-rank expert sizes, random routing, S and partition (the
+    same P on every rank), tile shape; every rank's pools, counters and
+    post-reorder output bit-exact vs the oracle."""
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.choice([1, 2, 4, 8]))
+    BM = int(rng.choice([128, 256]))
+    BN = int(rng.choice([128, 256]))
+    Nt = int(rng.integers(1, 4))
+    N, K = Nt * BN, 64 * int(rng.integers(1, 5))
+    Mts = [int(rng.integers(1, 5)) for _ in range(n)]
+    P = min(int(rng.integers(1, 4)), min(Mts) * Nt)   # every rank needs at least P waves
+    specs, oplans, As, Bts, rds = [], [], [], [], []
+    for s_ in range(n):
+        Mt = Mts[s_]
+        M = Mt * BM
+        tiles = Mt * Nt
+        S = int(rng.integers(1, max(1, tiles // P) + 1))
+        T = op.num_waves(tiles, S)
+        if T < P:
+            S, T = 1, tiles
+        part = [1] * (P - 1) + [T - (P - 1)]
+        rd = synthetic.random_row_dst(M, n, 3000 + 10 * seed + s_)
+        A, Bt = synthetic.exact_inputs(M, N, K, seed=900 + 10 * seed + s_, nnz_per_row=64)
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2,
+                          group_waves=part, row_dst=rd))
+        oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=2))
+        As.append(A), Bts.append(Bt), rds.append(rd)
+    ores = opl.run_alltoall(As, Bts, oplans, rds)
+    plain = opl.plain_alltoall(As, Bts, rds)
+    for me in range(n):
+        plan = fo.Plan(rank=me, world=n, peers=specs, **specs[me])
+        send = torch.empty(plan.info["send_elems"], dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, As[me].cuda(), Bts[me].cuda(), send)
+        torch.cuda.synchronize()
+        flat = np.concatenate([ores["send"][me].pools[d].reshape(-1) for d in range(n)])
+        assert np.array_equal(send.double().cpu().numpy(), flat), f"seed {seed} rank {me} pools"
+        mult = BM // 128
+        want = [mult * t for t in op.group_thresholds(oplans[me].partition, oplans[me].S, oplans[me].ntiles)]
+        assert plan.read_counters().tolist() == want
+        recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][me]]) if ores["recv"][me] else np.zeros(0)
+        out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plan, _bf16(recv), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.double().cpu().numpy(), plain[me]), f"seed {seed} rank {me} output"
