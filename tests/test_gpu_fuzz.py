@@ -145,3 +145,51 @@ def test_random_a2a_plan_matches_oracle(seed):
         fo.post_stage(plan, _bf16(recv), out)
         torch.cuda.synchronize()
         assert np.array_equal(out.double().cpu().numpy(), plain[me]), f"seed {seed} rank {me} output"
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_run_equals_sequential(seed):
+    """The stream orchestration (fo_run: counters, triggers, per-group
+    collectives, per-group / fused post passes, last group in order) on random
+    world-1 plans equals fo_run_sequential bit for bit, on repeated runs with
+    poisoned buffers."""
+    rng = np.random.default_rng(7000 + seed)
+    BM = int(rng.choice([128, 256]))
+    BN = int(rng.choice([128, 256]))
+    Mt, Nt = int(rng.integers(1, 6)), int(rng.integers(1, 5))
+    M, N, K = Mt * BM, Nt * BN, 64 * int(rng.integers(1, 6))
+    tiles = Mt * Nt
+    S = int(rng.integers(1, tiles + 1))
+    T = op.num_waves(tiles, S)
+    part = synthetic.random_partition(T, seed)
+    coll = str(rng.choice(["allreduce", "reducescatter", "alltoall"]))
+    post = str(rng.choice(["none", "add", "add_rmsnorm"])) if coll != "alltoall" else "none"
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=part,
+              swizzle=int(rng.integers(0, 4)), ar_layout=str(rng.choice(["slot", "auto"])), post=post)
+    if coll == "alltoall":
+        kw["row_dst"] = np.zeros(M, np.int32)
+        plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
+    else:
+        plan = fo.Plan(**kw)
+    plan.set_option("last_group_in_order", int(rng.integers(0, 2)))
+    plan.set_option("wait_kernel", int(rng.integers(0, 2)))
+    plan.set_option("tail_split", -1 if rng.random() < 0.3 else 0)
+    plan.set_option("multicast", int(rng.random() < 0.3))
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    try:
+        A, Bt = synthetic.exact_inputs(M, N, K, seed=7100 + seed, nnz_per_row=128)
+        A, Bt = A.cuda(), Bt.cuda()
+        rows = plan.info["out_rows"]
+        res = synthetic.normal_bf16((rows, N), 1.0, seed, device="cuda") if post != "none" else None
+        gam = synthetic.normal_bf16((N,), 1.0, seed + 1, device="cuda") if post == "add_rmsnorm" else None
+        want = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
+        fo.run_sequential(ctx, plan, A, Bt, want, res, gam)
+        got = torch.empty_like(want)
+        for _ in range(3):
+            plan.fill_buffers(0x7FC0)
+            got.fill_(float("nan"))
+            fo.run(ctx, plan, A, Bt, got, res, gam)
+            torch.cuda.synchronize()
+            assert torch.equal(got, want), f"seed {seed}: {kw}"
+    finally:
+        ctx.close()
