@@ -15,6 +15,13 @@ enum EpiMode : int {
   EPI_A2A = 3        // A2A: row a of the tile -> its destination pool slot
 };
 
+// One K-range of a split tail tile (host-built table, see fo_gemm's my_unit):
+// role 1 = owner (the range starting at k-block 0; folds nparts-1 partials
+// from workspace slots slot.. in), role 2 = part (publishes to slot `slot`).
+struct GemmSeg {
+  int pos, kb0, kb1, role, slot, nparts, tt, pad;
+};
+
 struct GemmArgs {
   const void* A;      // [M, K] bf16 row-major (K-major) or [K, M] (mn_major bit 0)
   const void* Bt;     // [N, K] bf16 row-major (K-major) or [K, N] (mn_major bit 1)
@@ -36,10 +43,11 @@ struct GemmArgs {
   int h_log2;
   unsigned long long* tile_ts; // optional [tiles] device: %globaltimer at signal
   // ---- tail split (split-K of the last partial wave across idle workers)
-  int units;                   // work units: tail_pos + (tiles - tail_pos) * split
   int tail_pos;                // first execution position of the split tail (= tiles: no split)
-  int split;                   // K slices per tail tile (1 = no split)
-  float* workspace;            // fp32 partials [(tiles - tail_pos) * (split - 1)][TM][BN]
+  int split;                   // > 1: the tail is split (segments below); 1: no split
+  const GemmSeg* seg;          // [segments] the tail's K-ranges, grouped by worker
+  const int32_t* wseg;         // [S + 1] worker w's segments: seg[wseg[w] .. wseg[w+1])
+  float* workspace;            // fp32 partials [slots][TM][BN]
   uint32_t* flags;             // [(tiles - tail_pos) * CG] partial-ready counts (reset with the counters)
   // ---- host-staged A (fo_run_host pipelining): A arrives in chunks of
   // a_chunk_rows tile-rows; the producer loads a tile's A only once

@@ -250,27 +250,42 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
-// Work unit u -> execution position, K-slice and k-block range.  Units below
-// tail_pos are whole tiles (unit = position); the tail's tiles are split into
-// `split` K-slices taken by consecutive units (so by different workers of the
-// last wave).
+// The work of one worker: its k-th unit.  Units of the first tail_pos
+// positions are whole tiles (worker w runs positions w, w+S, ...); with a
+// split tail the worker then runs its segments of the tail tiles, listed by
+// the host in p.seg[p.wseg[w] .. p.wseg[w+1]) — a K-range of one tail tile
+// and its role: 0 whole tile, 1 owner (the K-range starting at k-block 0:
+// folds the other parts' fp32 partials in, writes and signals the tile),
+// 2 part (publishes its fp32 partial to workspace slot `slot`).
 struct Unit {
-  int pos, slice, kb0, kb1;
+  int pos, kb0, kb1, role, slot, nparts, tt;
 };
 
-__device__ __forceinline__ Unit decode_unit(const GemmArgs& p, int u, int KB) {
+__device__ __forceinline__ int unit_count(const GemmArgs& p, int worker, int nworkers) {
+  const int nreg = (p.tail_pos > worker) ? (p.tail_pos - worker + nworkers - 1) / nworkers : 0;
+  return nreg + (p.seg ? p.wseg[worker + 1] - p.wseg[worker] : 0);
+}
+
+__device__ __forceinline__ Unit my_unit(const GemmArgs& p, int worker, int nworkers, int k, int KB) {
+  const int nreg = (p.tail_pos > worker) ? (p.tail_pos - worker + nworkers - 1) / nworkers : 0;
   Unit r;
-  if (u < p.tail_pos) {
-    r.pos = u;
-    r.slice = 0;
+  if (k < nreg) {
+    r.pos = worker + k * nworkers;
     r.kb0 = 0;
     r.kb1 = KB;
+    r.role = 0;
+    r.slot = 0;
+    r.nparts = 1;
+    r.tt = 0;
   } else {
-    const int v = u - p.tail_pos;
-    r.pos = p.tail_pos + v / p.split;
-    r.slice = v % p.split;
-    r.kb0 = r.slice * KB / p.split;
-    r.kb1 = (r.slice + 1) * KB / p.split;
+    const GemmSeg sg = p.seg[p.wseg[worker] + (k - nreg)];
+    r.pos = sg.pos;
+    r.kb0 = sg.kb0;
+    r.kb1 = sg.kb1;
+    r.role = sg.role;
+    r.slot = sg.slot;
+    r.nparts = sg.nparts;
+    r.tt = sg.tt;
   }
   return r;
 }
@@ -383,8 +398,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int ready_chunk = -1;
-      for (int u = worker; u < p.units; u += nworkers) {
-        const Unit un = decode_unit(p, u, KB);
+      const int nu = unit_count(p, worker, nworkers);
+      for (int k = 0; k < nu; ++k) {
+        const Unit un = my_unit(p, worker, nworkers, k, KB);
+        const int u = un.pos;  // == worker + k*S without a split tail (multicast / wave sync)
         const int t = p.order[un.pos];
         const int ti = t / p.Nt, tj = t - ti * p.Nt;
         if (p.a_ready && ti / p.a_chunk_rows != ready_chunk) {
@@ -401,7 +418,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         bool mcA = false, mcB = false;
         uint16_t mc_mask = 0;
         if constexpr (MC == 2) {
-          if ((u ^ 1) < p.units) {
+          if ((u ^ 1) < p.tiles) {
             const int t2 = p.order[u ^ 1];
             const int ti2 = t2 / p.Nt;
             mcA = (ti2 == ti);
@@ -409,11 +426,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mc_mask = (uint16_t)((1u << half) | (1u << (2 + half)));
           }
         }
-        const int wave = u / nworkers;
+        const int wave = k;  // wave sync runs without a split tail: unit k = wave k
         if (p.wave_ctr && wave > 0) {
           // keep the waves aligned: no load of wave w before every CTA of
           // wave w-1 has issued its last one (cyclic compare: monotone counters)
-          const uint32_t size = (uint32_t)min(nworkers, p.units - (wave - 1) * nworkers) * CG;
+          const uint32_t size = (uint32_t)min(nworkers, p.tiles - (wave - 1) * nworkers) * CG;
           const uint32_t target = (p.wave_epoch + 1u) * size;
           while ((int32_t)(ld_acquire(p.wave_ctr + wave - 1) - target) < 0) __nanosleep(64);
         }
@@ -469,8 +486,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int u = worker; u < p.units; u += nworkers) {
-        const Unit un = decode_unit(p, u, KB);
+      const int nu = unit_count(p, worker, nworkers);
+      for (int k = 0; k < nu; ++k) {
+        const Unit un = my_unit(p, worker, nworkers, k, KB);
+        const int u = un.pos;
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -480,18 +499,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
           const uint32_t sb = smem_u32(sB + stage * C::B_STAGE_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
+          for (int kk = 0; kk < BK / 16; ++kk) {
             // K-major: +32 bytes along K inside the 128-byte swizzle row (+2 in the
             // >>4 address field); MN-major: +2 core groups of 8 k-rows (+2048 B)
-            const uint64_t adesc = (MJ & 1) ? sw128_mn_desc(sa + 2048 * k) : sw128_desc(sa) + 2 * k;
-            const uint64_t bdesc = (MJ & 2) ? sw128_mn_desc(sb + 2048 * k) : sw128_desc(sb) + 2 * k;
-            umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
+            const uint64_t adesc = (MJ & 1) ? sw128_mn_desc(sa + 2048 * kk) : sw128_desc(sa) + 2 * kk;
+            const uint64_t bdesc = (MJ & 2) ? sw128_mn_desc(sb + 2048 * kk) : sw128_desc(sb) + 2 * kk;
+            umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb != un.kb0 || kk != 0) ? 1u : 0u);
           }
           // frees the smem stage when these MMAs retire: in both CTAs of the
           // pair; with a multicast partner in all four CTAs (count 2 each), and
           // alone (partner done) twice in the pair's own CTAs
           if constexpr (MC == 2) {
-            if ((u ^ 1) < p.units) {
+            if ((u ^ 1) < p.tiles) {
               umma_commit<CG>(&empty[stage], 0xF);
             } else {
               umma_commit<CG>(&empty[stage], pair_mask);
@@ -534,14 +553,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           nx_slot[it] = p.row_slot[(int64_t)npos * TM + (int)half * BM + q * 32 + it * 4 + (lane >> 3)];
       }
     };
-    if (worker < p.units) prefetch_dst(decode_unit(p, worker, KB).pos);
-    for (int u = worker; u < p.units; u += nworkers) {
-      const Unit un = decode_unit(p, u, KB);
+    const int nu = unit_count(p, worker, nworkers);
+    if (nu > 0) prefetch_dst(my_unit(p, worker, nworkers, 0, KB).pos);
+    for (int k = 0; k < nu; ++k) {
+      const Unit un = my_unit(p, worker, nworkers, k, KB);
       const int pos = un.pos;
       const int t = p.order[pos];
       const int ti = t / p.Nt, tj = t - ti * p.Nt;
-      const bool tail = (pos >= p.tail_pos) && p.split > 1;
-      const int tt = pos - p.tail_pos;  // tail tile index
+      const bool owner = (un.role == 1), part = (un.role == 2);  // split tail tile roles
+      const int tt = un.tt;  // tail tile index (flags)
       const int row = (int)half * BM + q * 32 + lane;  // this thread's accumulator row in the tile
       // this lane's 8 destination rows of the tile (rows it*4 + lane/8 of the
       // warp's 32-row quarter), resolved once per tile from table entries
@@ -554,14 +574,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                    nx_slot[it]) +
                    (lane & 7) * 8;
       mbar_wait(&tfull[acc], aphase);
-      if (u + nworkers < p.units) prefetch_dst(decode_unit(p, u + nworkers, KB).pos);
+      if (k + 1 < nu) prefetch_dst(my_unit(p, worker, nworkers, k + 1, KB).pos);
       tc_fence_after();
-      if (tail && un.slice == 0) {
-        // owner of a split tile: wait until the other K-slices' partials of
-        // this CTA's rows are published (acquire), then fold them in below
+      if (owner) {
+        // owner of a split tile: wait until the other parts' partials of this
+        // CTA's rows are published (acquire), then fold them in below
         if (q == 0 && lane == 0) {
           const uint32_t* f = p.flags + tt * CG + half;
-          while (ld_acquire(f) < (uint32_t)(p.split - 1)) __nanosleep(32);
+          while (ld_acquire(f) < (uint32_t)(un.nparts - 1)) __nanosleep(32);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
@@ -581,23 +601,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else mbar_arrive_cluster(tempty_leader0 + 8u * acc);
           }
         }
-        if (tail) {
-          if (un.slice > 0) {
-            // K-slice producer: publish fp32 partials of this thread's row
-            float4* w = reinterpret_cast<float4*>(
-                p.workspace + (((int64_t)tt * (p.split - 1) + (un.slice - 1)) * TM + row) * BN + c * EPI_COLS);
+        // partial slot layout [chunk c][float4 x][tile row][4]: for a fixed x the
+        // warp's 32 rows are 32 consecutive float4 — coalesced stores and loads
+        if (part) {
+          // part of a split tile: publish fp32 partials of this thread's row
+          float4* w = reinterpret_cast<float4*>(p.workspace + (int64_t)un.slot * TM * BN) + (int64_t)c * 16 * TM + row;
 #pragma unroll
-            for (int x = 0; x < 16; ++x)
-              w[x] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
-                                 __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
-            continue;
-          }
-          for (int sl = 1; sl < p.split; ++sl) {
-            const float4* w = reinterpret_cast<const float4*>(
-                p.workspace + (((int64_t)tt * (p.split - 1) + (sl - 1)) * TM + row) * BN + c * EPI_COLS);
+          for (int x = 0; x < 16; ++x)
+            w[x * TM] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                    __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
+          continue;
+        }
+        if (owner) {
+          // the parts' partials in part order (deterministic), slots slot..slot+nparts-2
+          for (int sl = 0; sl < un.nparts - 1; ++sl) {
+            const float4* w = reinterpret_cast<const float4*>(p.workspace + (int64_t)(un.slot + sl) * TM * BN) +
+                              (int64_t)c * 16 * TM + row;
 #pragma unroll
             for (int x = 0; x < 16; ++x) {
-              const float4 f = w[x];
+              const float4 f = w[x * TM];
               v[4 * x] = __float_as_uint(__uint_as_float(v[4 * x]) + f.x);
               v[4 * x + 1] = __float_as_uint(__uint_as_float(v[4 * x + 1]) + f.y);
               v[4 * x + 2] = __float_as_uint(__uint_as_float(v[4 * x + 2]) + f.z);
@@ -627,7 +649,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
       }
-      if (tail && un.slice > 0) {
+      if (part) {
         // partials of this CTA's rows stored -> one release increment of the tile's flag
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (q == 0 && lane == 0) red_release_add(p.flags + tt * CG + half, 1u);

@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <climits>
 #include <thread>
@@ -105,7 +106,8 @@ void release_device(fo_plan_s* p) {
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
                     p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma,
-                    (void*)p->d_ws, (void*)p->d_a_ready, (void*)p->d_wave, (void*)p->d_rs_info})
+                    (void*)p->d_ws, (void*)p->d_a_ready, (void*)p->d_wave, (void*)p->d_rs_info,
+                    (void*)p->d_seg, (void*)p->d_wseg})
     if (ptr) cudaFree(ptr);
   cudaSetDevice(cur);
   p->device = -1;
@@ -144,25 +146,92 @@ static void ensure_device(fo_plan_s* p) {
   }
   p->d_src_row = upload(h.src_row);
   p->d_recv_dst = upload(h.recv_dst);
-  // ---- tail split: the R tiles of the last partial wave split into f K-slices
-  // taken by otherwise idle workers of that wave (R*f <= S, f <= k-blocks)
+  // ---- tail split: the R tiles of the last partial wave are split along K
+  // over the workers of that wave.  f >= 2: each into f equal K-slices on
+  // consecutive workers (R*f <= S); stream-K (-2): their R*KB k-blocks dealt
+  // out evenly to the workers in contiguous ranges (at most 4 parts per tile).
+  // The host lists every worker's K-ranges; the range starting at k-block 0
+  // owns the tile (it is its worker's last, the others' first segment, so no
+  // owner ever waits on a worker that is itself waiting).
   {
     const int KB = (int)(h.K / 64);
     const int R = h.tiles - (h.T - 1) * h.S;
     int f = p->tail_split_req;
-    if (f < 0) {  // auto: never more slices than k-blocks; no split when under 2
+    const bool streamk = (f == -2) && R > 0 && KB >= 2 && R < h.S;
+    if (f == -1) {  // auto: never more slices than k-blocks; no split when under 2
       f = (R > 0 && 2 * R <= h.S) ? std::min(std::min(4, h.S / R), KB) : 1;
       if (f < 2) f = 1;
     }
     if (f > 1 && (R * f > h.S || f > KB))
       fail(FO_ERR_INVALID_ARG, "tail split %d: %d tail tiles x %d slices exceed S=%d or k-blocks=%d", f, R, f, h.S, KB);
-    p->split = (f > 1) ? f : 1;
-    p->tail_pos = (p->split > 1) ? (h.T - 1) * h.S : h.tiles;
-    p->units = p->tail_pos + (h.tiles - p->tail_pos) * p->split;
+    std::vector<GemmSeg> segs;
+    std::vector<int32_t> wseg(h.S + 1, 0);
+    int nslots = 0;
+    const int tail0 = (h.T - 1) * h.S;
+    if (streamk || f > 1) {
+      // pieces[w] = (tile, kb0, kb1) of worker w, in global k order
+      std::vector<std::vector<std::array<int, 3>>> pieces(h.S);
+      if (streamk) {
+        const long total = (long)R * KB;
+        long L = (total + h.S - 1) / h.S;
+        L = std::max<long>(L, (KB + 3) / 4);  // at most ~4 parts per tile
+        for (int w = 0; w < h.S; ++w) {
+          long g0 = (long)w * L, g1 = std::min(total, g0 + L);
+          while (g0 < g1) {
+            const int r = (int)(g0 / KB), kb0 = (int)(g0 % KB);
+            const int kb1 = (int)std::min<long>(KB, kb0 + (g1 - g0));
+            pieces[w].push_back({r, kb0, kb1});
+            g0 += kb1 - kb0;
+          }
+        }
+      } else {
+        for (int r = 0; r < R; ++r)
+          for (int sl = 0; sl < f; ++sl) pieces[r * f + sl].push_back({r, sl * KB / f, (sl + 1) * KB / f});
+      }
+      // parts per tile and their slots (the non-owner parts of a tile take
+      // consecutive slots in k order)
+      std::vector<int> nparts(R, 0), first_slot(R, -1);
+      for (int w = 0; w < h.S; ++w)
+        for (auto& pc : pieces[w]) ++nparts[pc[0]];
+      for (int r = 0; r < R; ++r) {
+        first_slot[r] = nslots;
+        nslots += nparts[r] - 1;
+      }
+      std::vector<int> next_slot = first_slot;
+      for (int w = 0; w < h.S; ++w) {
+        wseg[w] = (int)segs.size();
+        for (auto& pc : pieces[w]) {
+          GemmSeg sg{};
+          sg.pos = tail0 + pc[0];
+          sg.kb0 = pc[1];
+          sg.kb1 = pc[2];
+          sg.tt = pc[0];
+          sg.nparts = nparts[pc[0]];
+          if (sg.nparts == 1) {
+            sg.role = 0;
+          } else if (pc[1] == 0) {
+            sg.role = 1;
+            sg.slot = first_slot[pc[0]];
+          } else {
+            sg.role = 2;
+            sg.slot = next_slot[pc[0]]++;
+          }
+          segs.push_back(sg);
+        }
+      }
+      wseg[h.S] = (int)segs.size();
+    }
+    const bool split = !segs.empty();
+    p->split = split ? std::max(2, f) : 1;
+    p->tail_pos = split ? tail0 : h.tiles;
+    p->units = split ? tail0 + (int)segs.size() : h.tiles;
     const int cg = h.BM / 128;
-    p->ctr_words = h.P + ((p->split > 1) ? R * cg : 0);
-    if (p->split > 1)
-      FO_CUDA(cudaMalloc(&p->d_ws, sizeof(float) * (size_t)R * (p->split - 1) * h.BM * h.BN));
+    p->ctr_words = h.P + (split ? R * cg : 0);
+    if (split) {
+      p->d_seg = upload(segs);
+      p->d_wseg = upload(wseg);
+      if (nslots > 0) FO_CUDA(cudaMalloc(&p->d_ws, sizeof(float) * (size_t)nslots * h.BM * h.BN));
+    }
   }
   FO_CUDA(cudaMalloc(&p->d_wave, sizeof(uint32_t) * (size_t)h.T));
   FO_CUDA(cudaMemset(p->d_wave, 0, sizeof(uint32_t) * (size_t)h.T));
@@ -207,9 +276,10 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   a.h_log2 = 0;
   while ((1 << a.h_log2) < h.h) ++a.h_log2;
   a.tile_ts = nullptr;
-  a.units = p->units;
   a.tail_pos = p->tail_pos;
   a.split = p->split;
+  a.seg = p->d_seg;
+  a.wseg = p->d_wseg;
   a.workspace = p->d_ws;
   a.flags = p->d_flags;
   if (p->a_staged_run) {
@@ -1124,7 +1194,7 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
         p->post_sm_partition = (int)value;
         break;
       case FO_OPT_TAIL_SPLIT:
-        if (value < -1 || value > 16) fail(FO_ERR_INVALID_ARG, "tail_split must be -1..16");
+        if (value < -2 || value > 16) fail(FO_ERR_INVALID_ARG, "tail_split must be -2..16");
         if (p->device >= 0) fail(FO_ERR_STATE, "tail_split must be set before the plan's first run");
         p->tail_split_req = (int)value;
         break;

@@ -48,10 +48,12 @@ struct fo_plan_s {
   int wait_kernel = 0;                            // 0 cuStreamWaitValue32, 1 spin-wait kernel
   int last_in_order = 1;                          // last group's collective on the caller stream after the GEMM
   int post_sm_partition = 0;                      // FO_OPT_POST_SM_PARTITION
-  int tail_split_req = 0;                         // FO_OPT_TAIL_SPLIT: 0/1 off, >=2 slices, -1 auto
+  int tail_split_req = 0;                         // FO_OPT_TAIL_SPLIT: 0/1 off, >=2 slices, -1 auto, -2 stream-K
   // ---- resolved tail split (set by ensure_device)
   int split = 1, tail_pos = 0, units = 0;
   float* d_ws = nullptr;                          // fp32 partials of the split tail
+  fo::GemmSeg* d_seg = nullptr;                   // the split tail's K-ranges by worker
+  int32_t* d_wseg = nullptr;                      // [S+1] per-worker segment offsets
   uint32_t* d_flags = nullptr;                    // = d_counters + P (one allocation, reset together)
   int ctr_words = 0;                              // P + tail flags
   // ---- wave alignment of the persistent producers (FO_OPT_WAVE_SYNC)

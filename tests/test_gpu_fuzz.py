@@ -48,7 +48,7 @@ def _draw(seed):
     swizzle = int(rng.integers(0, 4))
     layout = str(rng.choice(["slot", "auto"]))
     multicast = int(rng.random() < 0.5)
-    tail_split = -1 if rng.random() < 0.3 else 0     # auto: only where the last wave qualifies
+    tail_split = int(rng.choice([0, 0, -1, -2]))    # auto (where the last wave qualifies) / stream-K
     return dict(BM=BM, BN=BN, M=Mt * BM, N=Nt * BN, K=K, n=n, coll=coll, S=S, part=part, order=order,
                 swizzle=swizzle, layout=layout, multicast=multicast, tail_split=tail_split)
 
@@ -173,7 +173,7 @@ def test_random_run_equals_sequential(seed):
         plan = fo.Plan(**kw)
     plan.set_option("last_group_in_order", int(rng.integers(0, 2)))
     plan.set_option("wait_kernel", int(rng.integers(0, 2)))
-    plan.set_option("tail_split", -1 if rng.random() < 0.3 else 0)
+    plan.set_option("tail_split", int(rng.choice([0, 0, -1, -2])))
     plan.set_option("multicast", int(rng.random() < 0.3))
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     try:

@@ -291,6 +291,10 @@ def test_tile_timestamps_follow_waves(BM):
     (256, 128, 768, 1024, 256, 10, 2),      # 24 tiles, T=3, R=4 -> f=2
     (128, 256, 512, 1024, 1024, 14, 4),     # 16 tiles, T=2, R=2 -> f=4
     (256, 256, 2048, 2048, 2048, 28, -1),   # 64 tiles, T=3, R=8 -> f=3
+    (256, 256, 1024, 1024, 512, 12, -2),    # stream-K: 4 tail tiles x 8 k-blocks over 12 workers
+    (256, 256, 1024, 2048, 1024, 10, -2),   # stream-K, 1 wave: 32 tiles... T=4, R=2 over 10 workers
+    (256, 128, 768, 1024, 576, 20, -2),     # stream-K: 24 tiles, T=2, R=4, 9 k-blocks (uneven ranges)
+    (128, 256, 512, 1024, 1024, 14, -2),    # stream-K with single-CTA tiles
 ])
 def test_tail_split_exact(ctx1, BM, BN, M, N, K, S, split):
     A, Bt = synthetic.exact_inputs(M, N, K, seed=77, nnz_per_row=256)
