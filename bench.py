@@ -506,7 +506,11 @@ def main():
                                   "workers": nspec["workers"],
                                   "layout": "rowband" if nplan.info["ar_layout"] == 1 else "slot",
                                   "alg1_predicted_us": round(pred_n, 2),
-                                  "note": "GEMM+AR+residual add+RMSNorm; overlapped runs the fused op per row band"},
+                                  "note": "GEMM+AR+residual add+RMSNorm; " + (
+                                      "overlapped runs the fused op per row band right after its collective"
+                                      if len(groups_n) > 1 and nplan.info["ar_layout"] == 1 else
+                                      "the tuner's fastest plan has one group: the fused op runs once after "
+                                      "the collective (as in the sequential form)")},
             "roofline": {"bound": "tensor", "kernel": f"fo_gemm_tcgen05_kernel<{BNc},{cgc}>", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed alone per step)",
