@@ -304,12 +304,15 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *  FO_OPT_POST_SM_PARTITION 0 — per-group post kernels may co-reside with GEMM CTAs;
  *                      1 — they request padding shared memory so they only run on
  *                      the SMs the persistent GEMM leaves free (Alg. 1's SM split)
- *  FO_OPT_HOST_PIPELINE 3 — bit 0: fo_run_host copies a host A in ~16 chunks of
+ *  FO_OPT_HOST_PIPELINE 7 — bit 0: fo_run_host copies a host A in ~8 chunks of
  *                      whole tile-rows on its own stream, each chunk released to
  *                      the GEMM by a stream write the TMA producer waits on (the
  *                      GEMM starts on the first chunk); bit 1: (AR ROWBAND) each
  *                      group's rows are copied to the host right after its
- *                      collective; 0 — whole-buffer copies before / after
+ *                      collective; bit 2 (with bit 0): two device staging sets
+ *                      used by alternate calls, so a call's H2D overlaps the
+ *                      previous call's GEMM, collectives and D2H; 0 — whole-
+ *                      buffer copies before / after
  *  FO_OPT_HOST_CHUNKS  8 — target number of A chunks (whole tile-rows each) for
  *                      bit 0 above; set before the plan's first fo_run_host
  *  FO_OPT_LAST_GROUP_IN_ORDER 1 — the last group's collective (and its post

@@ -103,9 +103,15 @@ void release_device(fo_plan_s* p) {
   cudaGetDevice(&cur);
   cudaSetDevice(p->device);
   if (p->d_recv == p->d_send) p->d_recv = nullptr;  // aliased at world 1
+  for (cudaEvent_t& e : p->ev_set_done)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
   for (void* ptr : {(void*)p->d_order, (void*)p->d_pos_of_tile, (void*)p->d_group_of_pos, (void*)p->d_gpos,
                     (void*)p->d_row_slot, (void*)p->d_src_row, (void*)p->d_counters, p->d_send, p->d_recv,
                     p->d_rowmajor, (void*)p->d_recv_dst, p->h_A, p->h_Bt, p->h_out, p->h_res, p->h_gamma,
+                    p->h_A2, p->h_out2,
                     (void*)p->d_ws, (void*)p->d_a_ready, (void*)p->d_wave, (void*)p->d_rs_info,
                     (void*)p->d_seg, (void*)p->d_wseg})
     if (ptr) cudaFree(ptr);
@@ -283,7 +289,7 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   a.workspace = p->d_ws;
   a.flags = p->d_flags;
   if (p->a_staged_run) {
-    a.a_ready = p->d_a_ready;
+    a.a_ready = p->d_a_ready + (size_t)p->host_set * p->a_chunks;
     a.a_epoch = p->a_epoch;
     a.a_chunk_rows = p->a_chunk_rows;
   }
@@ -748,8 +754,8 @@ static void plan_a_chunks(fo_plan p) {
   for (int i = 0; i < p->a_chunks; ++i) p->a_chunk_order[i] = i;
   std::stable_sort(p->a_chunk_order.begin(), p->a_chunk_order.end(),
                    [&](int x, int y) { return first[x] < first[y]; });
-  FO_CUDA(cudaMalloc(&p->d_a_ready, sizeof(uint32_t) * p->a_chunks));
-  FO_CUDA(cudaMemset(p->d_a_ready, 0, sizeof(uint32_t) * p->a_chunks));
+  FO_CUDA(cudaMalloc(&p->d_a_ready, sizeof(uint32_t) * 2 * p->a_chunks));   // one flag set per staging set
+  FO_CUDA(cudaMemset(p->d_a_ready, 0, sizeof(uint32_t) * 2 * p->a_chunks));
 }
 
 fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
@@ -784,17 +790,35 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
     // producer by a stream write of this run's epoch (PAPER.md:368's
     // signal/wait, applied to the input side); needs K-major A
     const bool pipe_a = a_host && (p->host_pipeline & 1) && write && !(h.mn_major & 1);
+    // two staging sets (bit 2): this call uses set b, the previous call the
+    // other one, so this call's H2D only has to wait for the call before the
+    // previous one (the last user of set b) and overlaps the previous call's
+    // GEMM, collectives and D2H
+    const bool two_sets = pipe_a && (p->host_pipeline & 4);
+    p->host_set = two_sets ? (p->host_set ^ 1) : 0;
+    const int b = p->host_set;
+    void*& stA = (b == 0) ? p->h_A : p->h_A2;
+    void*& stO = (b == 0) ? p->h_out : p->h_out2;
     const void* dA = nullptr;
     if (pipe_a) {
       plan_a_chunks(p);
-      if (!p->h_A) FO_CUDA(cudaMalloc(&p->h_A, a_bytes));
+      if (!stA) FO_CUDA(cudaMalloc(&stA, a_bytes));
       ++p->a_epoch;
-      // the copies may overwrite the staging only after the work already on
-      // `s` (the previous run's GEMM reads it); they are enqueued BEFORE the
-      // GEMM that waits on them, so no hardware-queue aliasing can order the
-      // GEMM ahead of the copies it waits for
-      FO_CUDA(cudaEventRecord(c->ev_h2d_fork, s));
-      for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamWaitEvent(c->h2d_stream[i], c->ev_h2d_fork, 0));
+      // the copies may overwrite the staging only after its last user's GEMM
+      // (one staging set: the work already on `s`; two sets: the call that
+      // last used set b); they are enqueued BEFORE the GEMM that waits on
+      // them, so no hardware-queue aliasing can order the GEMM ahead of the
+      // copies it waits for
+      if (two_sets) {
+        if (!p->ev_set_done[b]) {
+          FO_CUDA(cudaEventCreateWithFlags(&p->ev_set_done[b], cudaEventDisableTiming));
+          FO_CUDA(cudaEventRecord(p->ev_set_done[b], s));
+        }
+        for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamWaitEvent(c->h2d_stream[i], p->ev_set_done[b], 0));
+      } else {
+        FO_CUDA(cudaEventRecord(c->ev_h2d_fork, s));
+        for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamWaitEvent(c->h2d_stream[i], c->ev_h2d_fork, 0));
+      }
       // chunks alternate between two copy streams so one chunk's release
       // write never leaves the copy engine idle before the next chunk
       const size_t row_bytes = 2 * (size_t)h.K;
@@ -803,16 +827,16 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
         cudaStream_t cs = c->h2d_stream[i & 1];
         const int64_t r0 = (int64_t)ch * p->a_chunk_rows * h.BM;
         const int64_t r1 = std::min<int64_t>(h.M, r0 + (int64_t)p->a_chunk_rows * h.BM);
-        FO_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(p->h_A) + r0 * row_bytes,
+        FO_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(stA) + r0 * row_bytes,
                                 reinterpret_cast<const char*>(A) + r0 * row_bytes, (r1 - r0) * row_bytes,
                                 cudaMemcpyHostToDevice, cs));
-        CUresult r = write(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(p->d_a_ready + ch),
-                           p->a_epoch, 0);
+        CUresult r = write(reinterpret_cast<CUstream>(cs),
+                           reinterpret_cast<CUdeviceptr>(p->d_a_ready + (size_t)b * p->a_chunks + ch), p->a_epoch, 0);
         if (r != CUDA_SUCCESS) fail(FO_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
       }
       for (int i = 0; i < 2; ++i) FO_CUDA(cudaEventRecord(c->ev_h2d_join[i], c->h2d_stream[i]));
       p->a_staged_run = true;
-      dA = p->h_A;
+      dA = stA;
     } else {
       dA = stage(A, p->h_A, a_bytes);
     }
@@ -820,8 +844,8 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
     const void* dR = stage(residual, p->h_res, o_bytes);
     const void* dG = stage(gamma, p->h_gamma, 2 * (size_t)h.N);
     const bool out_dev = is_device_ptr(out);
-    if (!out_dev && !p->h_out) FO_CUDA(cudaMalloc(&p->h_out, o_bytes));
-    void* dO = out_dev ? out : p->h_out;
+    if (!out_dev && !stO) FO_CUDA(cudaMalloc(&stO, o_bytes));
+    void* dO = out_dev ? out : stO;
     int64_t r0 = 0, r1 = 0;
     // per-group D2H only when each group's rows are final after its own
     // stream work (a post pass deferred to the end would rewrite them)
@@ -833,6 +857,7 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
     if (pipe_a)
       for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamWaitEvent(s, c->ev_h2d_join[i], 0));
     if (!out_dev && !pipe_out) FO_CUDA(cudaMemcpyAsync(out, dO, o_bytes, cudaMemcpyDeviceToHost, s));
+    if (two_sets) FO_CUDA(cudaEventRecord(p->ev_set_done[b], s));  // set b free once this call is done
   });
 }
 
@@ -1208,7 +1233,7 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
         p->a_chunk_target = (int)value;
         break;
       case FO_OPT_HOST_PIPELINE:
-        if (value < 0 || value > 3) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..3");
+        if (value < 0 || value > 7) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..7");
         p->host_pipeline = (int)value;
         break;
       case FO_OPT_DEBUG_STALL_GROUP:

@@ -32,7 +32,11 @@ struct fo_plan_s {
   // ---- fo_run_host pipelining (FO_OPT_HOST_PIPELINE): A copied in chunks of
   // a_chunk_rows tile-rows, each followed by a release write of the run's
   // epoch into d_a_ready[chunk]; the GEMM producer waits per tile-row
-  int host_pipeline = 3;                          // bit 0: chunked A, bit 1: per-group D2H
+  int host_pipeline = 7;                          // bit 0: chunked A, bit 1: per-group D2H, bit 2: 2 staging sets
+  void* h_A2 = nullptr;                           // second A / out staging set (bit 2: consecutive
+  void* h_out2 = nullptr;                         //   calls alternate, so call i+1's H2D overlaps call i)
+  int host_set = 0;                               // staging set of the next fo_run_host
+  cudaEvent_t ev_set_done[2] = {nullptr, nullptr};  // last call on set b finished (its staging is free)
   uint32_t* d_a_ready = nullptr;
   uint32_t a_epoch = 0;
   int a_chunk_target = 8;                         // FO_OPT_HOST_CHUNKS

@@ -160,7 +160,7 @@ def test_run_host_pipelined_matches_device_run(case):
         out_d = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         fo.run(ctx, plan, A.cuda(), Bt_d, out_d, *extra_d)
         torch.cuda.synchronize()
-        for pipe in (3, 1, 2, 0):
+        for pipe in (7, 3, 1, 2, 0):
             plan.set_option("host_pipeline", pipe)
             out_h = torch.full((M, N), float("nan"), dtype=torch.bfloat16)
             A_h = A.clone()
@@ -169,4 +169,35 @@ def test_run_host_pipelined_matches_device_run(case):
             fo.run_host(ctx, plan, A_h, Bt_d, out_h, *extra_h)
             torch.cuda.synchronize()
             assert torch.equal(out_h, out_d.cpu()), (case, it, pipe)
+    ctx.close()
+
+
+@pytest.mark.parametrize("layout", ["rowband", "slot"])
+def test_run_host_back_to_back_two_staging_sets(layout):
+    """FO_OPT_HOST_PIPELINE bit 2: consecutive fo_run_host calls alternate two
+    staging sets, so call i+1's H2D overlaps call i — issued back to back
+    without a host sync, each call with fresh activations and its own host
+    output, every output must equal the device run of its own inputs."""
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    M, N, K, S = 4096, 1024, 1024, 8
+    tiles = (M // 256) * (N // 256)
+    T = -(-tiles // S)
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, group_waves=[1] * T,
+                   ar_layout=layout, swizzle=1)
+    assert plan.info["ar_layout"] == (1 if layout == "rowband" else 0)
+    Bt_d = synthetic.float_inputs(M, N, K, seed=9)[1].cuda()
+    As = [synthetic.float_inputs(M, N, K, seed=40 + i)[0].pin_memory() for i in range(5)]
+    outs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16).pin_memory() for _ in range(5)]
+    for A_h, o in zip(As, outs):
+        fo.run_host(ctx, plan, A_h, Bt_d, o)
+    torch.cuda.synchronize()
+    for i, (A_h, o) in enumerate(zip(As, outs)):
+        want = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        fo.run(ctx, plan, A_h.cuda(), Bt_d, want)
+        torch.cuda.synchronize()
+        assert torch.equal(o, want.cpu()), (layout, i)
     ctx.close()
