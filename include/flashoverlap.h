@@ -77,7 +77,10 @@ typedef enum {
 typedef enum {
   FO_POST_NONE = 0,
   FO_POST_ADD = 1,          /* out = x + residual                                   */
-  FO_POST_ADD_RMSNORM = 2   /* y = x + residual; out = y / sqrt(mean(y^2) + eps) * gamma */
+  FO_POST_ADD_RMSNORM = 2,  /* y = x + residual; out = y / sqrt(mean(y^2) + eps) * gamma */
+  FO_POST_ADD_RMSNORM_RESIDUAL = 3  /* as ADD_RMSNORM, and y (bf16) is written back into the residual
+                                       buffer in place — the next layer's residual stream (the fused
+                                       add + RMSNorm of a pre-norm transformer block) */
 } fo_post;
 
 typedef struct fo_ctx_s* fo_ctx;

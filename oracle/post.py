@@ -8,6 +8,9 @@ does not define its RMSNorm; reading R12:
 
     y   = x + residual                    (FO_POST_ADD)
     out = y / sqrt(mean_j(y_j^2) + eps) * gamma   (FO_POST_ADD_RMSNORM, per row)
+    FO_POST_ADD_RMSNORM_RESIDUAL: the same out, and the residual buffer
+    becomes bf16(y) — the residual stream of a pre-norm transformer block
+    (NEXT f4's TP block; the fused add + RMSNorm of inference engines).
 
 MoE combine after the expert GEMM + All-to-All (the A2A
 "transfer[s] the processed data back to the original GPUs after expert
@@ -39,6 +42,15 @@ def rmsnorm(y, gamma, eps: float):
 
 def add_rmsnorm(x, residual, gamma, eps: float):
     return rmsnorm(add(x, residual), gamma, eps)
+
+
+def add_rmsnorm_residual(x, residual, gamma, eps: float):
+    """(out, new_residual): out = add_rmsnorm(x, residual); new_residual =
+    round-to-nearest-even bf16 of y = x + residual (the buffer is bf16)."""
+    from .numerics import round_bf16
+
+    y = add(x, residual)
+    return rmsnorm(y, gamma, eps), round_bf16(y)
 
 
 def topk_combine(x, idx, w, residual=None):

@@ -173,7 +173,10 @@ __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p, 
 // over HBM: read x (through the map) and residual once, write out once.
 // 128-thread blocks with 4 chunks per thread keep 2x the rows (and 8
 // independent 16-byte loads per thread) in flight compared with 256 x 2.
-template <int MAP, int MAXC, int THREADS>
+// RES: also write y = x + residual (bf16) back into the residual buffer (the
+// residual stream of a pre-norm block); each row's residual is read before
+// its own write, by the same thread, so in place is safe.
+template <int MAP, int MAXC, int THREADS, bool RES>
 __global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs p, int lbn) {
   constexpr int WARPS = THREADS / 32;
   __shared__ float red[WARPS];
@@ -232,7 +235,10 @@ __global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs
         unpack8(rv[i], q);
         unpack8(ld_coherent(gam + 8 * c), g);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = (x[k] + q[k]) * rstd * g[k];
+        for (int k = 0; k < 8; ++k) x[k] += q[k];
+        if (RES) st_stream(const_cast<__nv_bfloat16*>(rrow) + 8 * c, pack8(x));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = x[k] * rstd * g[k];
         st_stream(orow + 8 * c, pack8(x));
       }
     }
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs
 
 // Fallback for very wide rows (N > 16384): warp per row, two passes (the
 // second read hits L2).
-template <int MAP>
+template <int MAP, bool RES>
 __global__ void __launch_bounds__(256) fo_post_rmsnorm_wide_kernel(const PostArgs p, int lbn) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -270,7 +276,10 @@ __global__ void __launch_bounds__(256) fo_post_rmsnorm_wide_kernel(const PostArg
       unpack8(ld_coherent(rrow + 8 * c), y);
       unpack8(ld_coherent(gam + 8 * c), g);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = (x[i] + y[i]) * rstd * g[i];
+      for (int i = 0; i < 8; ++i) x[i] += y[i];
+      if (RES) st_stream(const_cast<__nv_bfloat16*>(rrow) + 8 * c, pack8(x));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = x[i] * rstd * g[i];
       st_stream(out + r * p.N + 8 * c, pack8(x));
     }
   }
@@ -361,22 +370,27 @@ int num_sms() {
   return n;
 }
 
+template <int MAP, bool RES>
+cudaError_t launch_rmsnorm(const PostArgs& a, int lbn, cudaStream_t stream) {
+  const int64_t chunks = a.N / 8;
+  const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 16);
+  if (chunks <= 128) fo_post_rmsnorm_kernel<MAP, 1, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 2, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 4, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 8, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8, 256, RES><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
+  else {
+    const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)num_sms() * 8);
+    fo_post_rmsnorm_wide_kernel<MAP, RES><<<g2, 256, a.smem_pad, stream>>>(a, lbn);
+  }
+  return cudaGetLastError();
+}
+
 template <int MAP>
 cudaError_t launch_map(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int64_t chunks = a.N / 8;
-  if (a.op == FO_POST_ADD_RMSNORM) {
-    const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 16);
-    if (chunks <= 128) fo_post_rmsnorm_kernel<MAP, 1, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-    else if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 2, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-    else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 4, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-    else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 8, 128><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-    else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8, 256><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
-    else {
-      const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)num_sms() * 8);
-      fo_post_rmsnorm_wide_kernel<MAP><<<g2, 256, a.smem_pad, stream>>>(a, lbn);
-    }
-    return cudaGetLastError();
-  }
+  if (a.op == FO_POST_ADD_RMSNORM) return launch_rmsnorm<MAP, false>(a, lbn, stream);
+  if (a.op == FO_POST_ADD_RMSNORM_RESIDUAL) return launch_rmsnorm<MAP, true>(a, lbn, stream);
   const int64_t units = a.rows * ((chunks + SEG_CHUNKS - 1) / SEG_CHUNKS);
   const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)num_sms() * 16);
   if (a.op == FO_POST_ADD) fo_post_reorder_kernel<MAP, FO_POST_ADD><<<grid, 256, a.smem_pad, stream>>>(a, lbn);

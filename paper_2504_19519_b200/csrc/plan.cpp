@@ -161,7 +161,7 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
                     int /*sm_count*/) {
   if (world < 1 || rank < 0 || rank >= world) fail(FO_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
   if (d.coll < FO_ALLREDUCE || d.coll > FO_NOCOMM) fail(FO_ERR_INVALID_ARG, "unknown coll %d", d.coll);
-  if (d.post < FO_POST_NONE || d.post > FO_POST_ADD_RMSNORM) fail(FO_ERR_INVALID_ARG, "unknown post %d", d.post);
+  if (d.post < FO_POST_NONE || d.post > FO_POST_ADD_RMSNORM_RESIDUAL) fail(FO_ERR_INVALID_ARG, "unknown post %d", d.post);
   Grid g = make_grid(d, world);
 
   PlanHost p;

@@ -254,6 +254,8 @@ static void ensure_device(fo_plan_s* p) {
   }
 }
 
+static bool is_rmsnorm(int post) { return post == FO_POST_ADD_RMSNORM || post == FO_POST_ADD_RMSNORM_RESIDUAL; }
+
 static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst, int mode, bool signal) {
   const PlanHost& h = p->host;
   GemmArgs a{};
@@ -324,7 +326,7 @@ static void run_post(fo_plan_s* p, int map, const void* src, void* out, const vo
                      cudaStream_t s) {
   const PlanHost& h = p->host;
   if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
-  if (h.post == FO_POST_ADD_RMSNORM && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
+  if (is_rmsnorm(h.post) && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
   PostArgs a{};
   a.map = map;
   a.op = h.post;
@@ -407,7 +409,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
   if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
   if (band_post(h)) {
     // in place on the band's rows [r0*BM, r1*BM) of out (== src)
-    if (h.post == FO_POST_ADD_RMSNORM && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
+    if (is_rmsnorm(h.post) && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
     const int64_t row0 = h.band_rows[2 * j] * h.BM, rows = (h.band_rows[2 * j + 1] - h.band_rows[2 * j]) * h.BM;
     PostArgs a{};
     a.map = POSTMAP_IDENTITY;
@@ -935,7 +937,7 @@ static void run_rowexchange(fo_plan_s* p, const void* gathered, void* out, const
   a.h = h.h;
   a.eps = h.eps;
   if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
-  if (h.post == FO_POST_ADD_RMSNORM && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
+  if (is_rmsnorm(h.post) && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
   FO_CUDA(launch_post(a, s));
 }
 

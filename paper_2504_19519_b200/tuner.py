@@ -392,9 +392,10 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
                     probes.append((S, T, layout, single_only, swz, gp, split, tm, tn, tiles))
     durs = timeit_many([(lambda gp=pr[5]: gemm_stage(gp, A, Bt, out)) for pr in probes], iters)
     for (S, T, layout, single_only, swz, _, split, tm, tn, tiles), dur in zip(probes, durs):
-        per_group_op = post if (layout == "rowband" or post != "add_rmsnorm") else "none"
+        norm = post in ("add_rmsnorm", "add_rmsnorm_res")
+        per_group_op = post if (layout == "rowband" or not norm) else "none"
         per_group = post_us(layout if layout != "auto" else "slot", per_group_op, tm, tn) / out_bytes
-        tail = post_us("slot", "add_rmsnorm", tm, tn) if (layout != "rowband" and post == "add_rmsnorm") else 0.0
+        tail = post_us("slot", post, tm, tn) if (layout != "rowband" and norm) else 0.0
         eff = effective_curve(curve, per_group)
         if single_only:
             pred = tune_predict([T], dur, tiles, S, tm * tn * 2, eff)

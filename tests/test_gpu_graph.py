@@ -2,6 +2,8 @@
 events, the persistent GEMM, cuStreamWaitValue32 nodes, NCCL calls, per-group
 post-reorder): capture once, replay with new inputs copied into the static
 buffers, compare with eager runs bit-exactly."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -201,3 +203,18 @@ def test_run_host_back_to_back_two_staging_sets(layout):
         torch.cuda.synchronize()
         assert torch.equal(o, want.cpu()), (layout, i)
     ctx.close()
+
+
+def test_tp_block_matches_reference():
+    """NEXT f4 second workload: the TP block (o_proj + AllReduce + fused add +
+    RMSNorm updating the residual stream, gate/up GEMM, down-proj + AllReduce +
+    residual add) through the library, overlapped and sequential, against a
+    PyTorch reference that rounds to bf16 where the library stores bf16."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "tp_block.py"), "--check"], cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count('"check"') == 2

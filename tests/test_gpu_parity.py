@@ -673,3 +673,34 @@ def test_moe_combine_full_path_world1(ctx1):
     with pytest.raises(fo.FOError):
         bad = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=4)
         fo.run_combine(ctx1, bad, _dev_bf16(A), _dev_bf16(Bt), out, torch.from_numpy(perm).cuda(), w)
+
+
+@pytest.mark.parametrize("coll,layout,groups", [("allreduce", "rowband", [1, 2, 1]), ("allreduce", "slot", [2, 2]),
+                                                ("reducescatter", "auto", [1, 3])])
+def test_add_rmsnorm_residual_in_place(ctx1, coll, layout, groups):
+    """FO_POST_ADD_RMSNORM_RESIDUAL (the residual stream of a pre-norm block,
+    NEXT f4): out equals the ADD_RMSNORM output bit for bit, and the residual
+    buffer is overwritten with bf16(x + residual) — bit-exact vs the oracle in
+    the exact-integer regime (per row band for ROWBAND, once at the end else)."""
+    M, N, K, S = 2048, 1024, 512, 8
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=91, nnz_per_row=200)
+    rows = M
+    kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1, group_waves=groups,
+              ar_layout=layout)
+    p_res = fo.Plan(post="add_rmsnorm_res", **kw)
+    p_norm = fo.Plan(post="add_rmsnorm", **kw)
+    rng = np.random.default_rng(92)
+    res0 = torch.from_numpy(rng.integers(-8, 9, size=(rows, N)).astype(np.float32)).to(torch.bfloat16)
+    gam = synthetic.normal_bf16((N,), 1.0, 93, device="cuda")
+    Ad, Bd = _dev_bf16(A), _dev_bf16(Bt)
+    o_norm = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx1, p_norm, Ad, Bd, o_norm, res0.cuda(), gam)
+    res = res0.cuda()
+    o_res = torch.empty_like(o_norm)
+    fo.run(ctx1, p_res, Ad, Bd, o_res, res, gam)
+    torch.cuda.synchronize()
+    assert torch.equal(o_res, o_norm)
+    C = onum.gemm(A, Bt)                                  # exact integers, bf16-representable
+    want_out, want_res = opost.add_rmsnorm_residual(C, _host(res0.cuda()), _host(gam), 1e-5)
+    assert np.array_equal(_host(res), want_res)
+    assert _rel_err(_host(o_res), want_out) <= TOL

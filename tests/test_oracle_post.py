@@ -27,3 +27,17 @@ def test_scale_invariance_and_add():
     b = post.add_rmsnorm(7 * x, 7 * r, g, 0.0)
     assert np.allclose(a, b, rtol=1e-12, atol=1e-12)
     assert np.array_equal(post.add(x, r), x + r)
+
+
+def test_add_rmsnorm_residual_keeps_the_rounded_sum():
+    """The residual-writing variant: out equals add_rmsnorm, and the new
+    residual is the bf16 rounding of x + residual — exact for sums that are
+    bf16-representable (small integers), rounded to nearest even otherwise."""
+    x = np.array([[1.0, 2.0, -3.0, 4.0], [256.0, 1.0, 0.5, -0.25]])
+    r = np.array([[1.0, 1.0, 1.0, 1.0], [1.0, 0.0, 0.0, 0.0]])
+    g = np.ones(4)
+    out, res = post.add_rmsnorm_residual(x, r, g, 1e-5)
+    assert np.array_equal(out, post.add_rmsnorm(x, r, g, 1e-5))
+    assert np.array_equal(res[0], [2.0, 3.0, -2.0, 5.0])
+    # 257 is not representable in bf16 (8 significant bits): ties to even -> 256
+    assert res[1, 0] == 256.0 and np.array_equal(res[1, 1:], [1.0, 0.5, -0.25])
