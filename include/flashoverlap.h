@@ -351,11 +351,17 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      pipelines (profiles/r01_multicast.txt), hence off
  *  FO_OPT_DEBUG_STALL_GROUP -1 — off; j — TEST ONLY: group j's trigger waits for
  *                      one more signal than the GEMM sends, so the run never
- *                      finishes (exercises the fo_plan_sync watchdog) */
+ *                      finishes (exercises the fo_plan_sync watchdog)
+ *  FO_OPT_GEMM_SWIGLU  0 — off; 1 — (no-comm plans, tile_n 256, no tail split)
+ *                      the GEMM's epilogue applies the SwiGLU of an MLP: with the
+ *                      weight rows interleaved in blocks of 128 (gate 0..127, up
+ *                      0..127, gate 128..255, up 128..255, ...), tile column block
+ *                      j writes C[:, 128j .. 128j+128) = silu(gate) * up from the
+ *                      fp32 accumulators (one bf16 rounding); C is [m, n/2] */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
                FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8,
-               FO_OPT_DEBUG_STALL_GROUP = 10 } fo_option;
+               FO_OPT_DEBUG_STALL_GROUP = 10, FO_OPT_GEMM_SWIGLU = 11 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

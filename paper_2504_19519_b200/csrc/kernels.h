@@ -12,7 +12,9 @@ enum EpiMode : int {
   EPI_ROWMAJOR = 0,  // C row-major with row stride ldc (no-comm, AR ROWBAND)
   EPI_SLOT = 1,      // AR: tile at position p -> slot p (BM*BN contiguous, row-major)
   EPI_RS = 2,        // RS: subtile k of the tile -> chunk k of its group
-  EPI_A2A = 3        // A2A: row a of the tile -> its destination pool slot
+  EPI_A2A = 3,       // A2A: row a of the tile -> its destination pool slot
+  EPI_SWIGLU = 4     // no-comm, BN = 256: tile columns [0,128) gate, [128,256) up (interleaved
+                     // weight rows); writes silu(gate) * up to C[:, tj*128 .. +128), row stride ldc
 };
 
 // One K-range of a split tail tile (host-built table, see fo_gemm's my_unit):

@@ -585,6 +585,66 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
+      if constexpr (BN == 256) {
+        if (p.mode == EPI_SWIGLU) {
+          // fused SwiGLU (the MLP's activation): gate columns [0,128) and up
+          // columns [128,256) of the accumulator, 32 output columns per step,
+          // silu(g) * u in fp32, one bf16 rounding; 8 rows x 64 B per store
+#pragma unroll 1
+          for (int c2 = 0; c2 < 4; ++c2) {
+            uint32_t g[32], up[32];
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + 32 * c2);
+            tmem_ld32(taddr, g);
+            tmem_ld32(taddr + 128, up);
+            tmem_wait_ld();
+            if (c2 == 3) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(tempty_leader0 + 8u * acc);
+              }
+            }
+            uint4* srow = reinterpret_cast<uint4*>(stg + lane * EPI_PITCH);
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              float o[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float gv = __uint_as_float(g[8 * x + e]);
+                o[e] = gv / (1.f + __expf(-gv)) * __uint_as_float(up[8 * x + e]);
+              }
+              uint4 w;
+              w.x = pack_bf16(__float_as_uint(o[0]), __float_as_uint(o[1]));
+              w.y = pack_bf16(__float_as_uint(o[2]), __float_as_uint(o[3]));
+              w.z = pack_bf16(__float_as_uint(o[4]), __float_as_uint(o[5]));
+              w.w = pack_bf16(__float_as_uint(o[6]), __float_as_uint(o[7]));
+              srow[x] = w;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const int r = it * 8 + (lane >> 2);
+              const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + (lane & 3) * 16);
+              __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.dst) +
+                                 ((int64_t)ti * TM + (int)half * BM + q * 32 + r) * p.ldc + (int64_t)tj * 128 +
+                                 32 * c2 + (lane & 3) * 8;
+              *reinterpret_cast<uint4*>(d) = w;
+            }
+            __syncwarp();
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (q == 0 && lane == 0) {
+            if (p.counters) red_release_add(&p.counters[p.group_of_pos[pos]], 1u);
+            if (p.tile_ts && leader) p.tile_ts[pos] = globaltimer();
+          }
+          if (++acc == 2) {
+            acc = 0;
+            aphase ^= 1;
+          }
+          continue;
+        }
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / EPI_COLS; ++c) {
         uint32_t v[64];

@@ -317,6 +317,12 @@ static void run_gemm(fo_plan_s* p, const void* A, const void* Bt, void* dst, int
                      cudaStream_t s, unsigned long long* tile_ts = nullptr) {
   if (!A || !Bt || !dst) fail(FO_ERR_INVALID_ARG, "null device pointer");
   GemmArgs a = gemm_args(p, A, Bt, dst, mode, signal);
+  if (p->swiglu && mode == EPI_ROWMAJOR) {  // FO_OPT_GEMM_SWIGLU: C is [m, n/2] = silu(gate) * up
+    if (p->host.BN != 256 || p->host.coll != FO_NOCOMM || p->split > 1)
+      fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan, tile_n 256 and no tail split");
+    a.mode = EPI_SWIGLU;
+    a.ldc = p->host.N / 2;
+  }
   a.tile_ts = tile_ts;
   FO_CUDA(launch_gemm(a, s));
   ++p->gemm_launches;  // every launch of the plan's GEMM advances the wave counters once
@@ -1237,6 +1243,12 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_HOST_PIPELINE:
         if (value < 0 || value > 7) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..7");
         p->host_pipeline = (int)value;
+        break;
+      case FO_OPT_GEMM_SWIGLU:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "gemm_swiglu must be 0 or 1");
+        if (value && (p->host.coll != FO_NOCOMM || p->host.BN != 256))
+          fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan with tile_n 256");
+        p->swiglu = (int)value;
         break;
       case FO_OPT_DEBUG_STALL_GROUP:
         if (value < -1 || value >= p->host.P) fail(FO_ERR_INVALID_ARG, "debug_stall_group must be -1..P-1");

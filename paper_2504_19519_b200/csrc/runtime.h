@@ -64,6 +64,7 @@ struct fo_plan_s {
   int wave_sync = 0;
   int multicast = 0;                              // FO_OPT_MULTICAST (measured slower: off)
   int debug_stall_group = -1;                     // FO_OPT_DEBUG_STALL_GROUP (watchdog test)
+  int swiglu = 0;                                 // FO_OPT_GEMM_SWIGLU (no-comm GEMM epilogue)
   uint32_t* d_wave = nullptr;                     // [T] monotone per-wave issue counters
   uint32_t gemm_launches = 0;                     // launches of this plan's GEMM so far (wave epoch)
 };

@@ -704,3 +704,28 @@ def test_add_rmsnorm_residual_in_place(ctx1, coll, layout, groups):
     want_out, want_res = opost.add_rmsnorm_residual(C, _host(res0.cuda()), _host(gam), 1e-5)
     assert np.array_equal(_host(res), want_res)
     assert _rel_err(_host(o_res), want_out) <= TOL
+
+
+@pytest.mark.parametrize("S,swz", [(8, 0), (3, 2)])
+def test_gemm_swiglu_epilogue(S, swz):
+    """FO_OPT_GEMM_SWIGLU: the fused MLP activation in the GEMM epilogue
+    equals silu(gate) * up of the fp64 product within one bf16 rounding
+    (interleaved weight rows: blocks of 128 gate / 128 up)."""
+    M, N2, K = 1024, 512, 768                     # output [M, 512] from a [M, 1024] GEMM
+    A, Wg = synthetic.float_inputs(M, N2, K, seed=61)
+    Wu = synthetic.float_inputs(M, N2, K, seed=62)[1]
+    Wi = torch.empty(2 * N2, K, dtype=torch.bfloat16)
+    for j in range(N2 // 128):
+        Wi[256 * j:256 * j + 128] = Wg[128 * j:128 * (j + 1)]
+        Wi[256 * j + 128:256 * (j + 1)] = Wu[128 * j:128 * (j + 1)]
+    plan = fo.Plan(coll="nocomm", m=M, n=2 * N2, k=K, tile_m=256, tile_n=256, workers=S, swizzle=swz)
+    plan.set_option("gemm_swiglu", 1)
+    out = torch.full((M, N2), float("nan"), dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, _dev_bf16(A), _dev_bf16(Wi), out)
+    torch.cuda.synchronize()
+    g = onum.gemm(A, Wg)
+    u = onum.gemm(A, Wu)
+    want = g / (1.0 + np.exp(-g)) * u
+    assert _rel_err(_host(out), want) <= TOL
+    with pytest.raises(fo.FOError, match="UNSUPPORTED"):
+        fo.Plan(coll="allreduce", m=M, n=2 * N2, k=K, tile_m=256, tile_n=256, workers=S).set_option("gemm_swiglu", 1)

@@ -5,11 +5,13 @@ synthetic weights, world = TP ranks (torchrun; one rank works too).
     h     = x + AllReduce(attn_out @ Wo_shardᵀ)          o_proj, row-parallel
     n     = RMSNorm(h) · γ                              fused: fo_run post=add_rmsnorm_res
                                                         (writes n, updates x -> h in place)
-    gu    = n @ Wgu_shardᵀ                               gate/up, column-parallel: our GEMM, no collective
-    a     = silu(g) · u                                  (PyTorch elementwise; outside the hot path)
+    a     = silu(n @ Wg_shardᵀ) · (n @ Wu_shardᵀ)          gate/up, column-parallel: our GEMM with the
+                                                        SwiGLU fused into its epilogue (FO_OPT_GEMM_SWIGLU;
+                                                        weight rows interleaved in blocks of 128)
     y     = h + AllReduce(a @ Wd_shardᵀ)                 down-proj, row-parallel: fo_run post=add
 
-The attention core is not part of this (its output is a synthetic input).
+The attention core is not part of this (its output is a synthetic input);
+every other step runs in the library's kernels.
 Both collective layers run overlapped (fo_run, tuned plans) and sequential
 (fo_run_sequential: GEMM -> one NCCL call -> the same fused op); the block
 time is reported for each.  --check runs a small block against a PyTorch
@@ -41,7 +43,8 @@ class Block:
         Hl, Il = H // world, I // world
         seed = synthetic.rank_seed(50000, world, rank)
         self.Wo = synthetic.normal_bf16((H, Hl), 0.02, seed + 1, device="cuda")        # [out H, in H/tp]
-        self.Wgu = synthetic.normal_bf16((2 * Il, H), 0.02, seed + 2, device="cuda")   # [gate|up I/tp, in H]
+        # gate/up rows interleaved in blocks of 128: [g0..127, u0..127, g128..255, ...]
+        self.Wgu = synthetic.normal_bf16((2 * Il, H), 0.02, seed + 2, device="cuda")
         self.Wd = synthetic.normal_bf16((H, Il), 0.02, seed + 3, device="cuda")        # [out H, in I/tp]
         self.gamma = synthetic.normal_bf16((H,), 1.0, 50001, device="cuda")
         if tuned:
@@ -58,19 +61,17 @@ class Block:
             self.p_o, self.p_d = simple(Hl, "add_rmsnorm_res"), simple(Il, "add")
         tiles_gu = (T // 256) * (2 * Il // 256)
         self.p_gu = fo.Plan(coll="nocomm", m=T, n=2 * Il, k=H, tile_m=256, tile_n=256,
-                            workers=-(-tiles_gu // -(-tiles_gu // 74)), swizzle=0)
+                            workers=-(-tiles_gu // -(-tiles_gu // 74)), swizzle=0, options={"gemm_swiglu": 1})
         self.n = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
-        self.gu = torch.empty(T, 2 * Il, dtype=torch.bfloat16, device="cuda")
+        self.a = torch.empty(T, Il, dtype=torch.bfloat16, device="cuda")
         self.y = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
 
     def forward(self, attn_out, x, overlapped=True):
         """x is the block input (residual stream); it is updated in place to h."""
         run = fo.run if overlapped else fo.run_sequential
         run(self.ctx, self.p_o, attn_out, self.Wo, self.n, x, self.gamma)
-        fo.gemm_stage(self.p_gu, self.n, self.Wgu, self.gu)
-        Il = self.I // self.world
-        a = torch.nn.functional.silu(self.gu[:, :Il]) * self.gu[:, Il:]
-        run(self.ctx, self.p_d, a, self.Wd, self.y, x)
+        fo.gemm_stage(self.p_gu, self.n, self.Wgu, self.a)      # a = silu(gate) * up, fused
+        run(self.ctx, self.p_d, self.a, self.Wd, self.y, x)
         return self.y
 
 
@@ -80,9 +81,9 @@ def reference(attn_out, x, blk, eps=1e-5):
     h = ((attn_out.float() @ blk.Wo.float().t()).to(bf).float() + x.float())
     n = (h * torch.rsqrt(h.pow(2).mean(1, keepdim=True) + eps) * blk.gamma.float()).to(bf)
     h = h.to(bf)
-    gu = (n.float() @ blk.Wgu.float().t()).to(bf)
-    Il = blk.I // blk.world
-    a = torch.nn.functional.silu(gu[:, :Il]) * gu[:, Il:]
+    gu = n.float() @ blk.Wgu.float().t()                    # fp32, as the fused epilogue sees it
+    blocks = gu.view(gu.shape[0], -1, 2, 128)
+    a = (torch.nn.functional.silu(blocks[:, :, 0]) * blocks[:, :, 1]).reshape(gu.shape[0], -1).to(bf)
     y = ((a.float() @ blk.Wd.float().t()).to(bf).float() + h.float()).to(bf)
     return y, h
 
