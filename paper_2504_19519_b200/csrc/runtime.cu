@@ -746,7 +746,7 @@ static bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// Chunking of a host-staged A: ~16 chunks of whole tile-rows, copied in the
+// Chunking of a host-staged A: ~FO_OPT_HOST_CHUNKS (8) chunks of whole tile-rows, copied in the
 // order the tile order first needs them.
 static void plan_a_chunks(fo_plan p) {
   const PlanHost& h = p->host;
