@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
       if constexpr (BN == 256) {
-        if (p.mode == EPI_SWIGLU) {
+        if (p.mode == EPI_SWIGLU && !part) {  // a split tile's parts publish fp32 partials below
           // fused SwiGLU (the MLP's activation): gate columns [0,128) and up
           // columns [128,256) of the accumulator, 32 output columns per step,
           // silu(g) * u in fp32, one bf16 rounding; 8 rows x 64 B per store
@@ -597,6 +597,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tmem_ld32(taddr, g);
             tmem_ld32(taddr + 128, up);
             tmem_wait_ld();
+            if (owner) {
+              // fold in the parts' partials of columns [32c2, +32) (gate) and
+              // [128 + 32c2, +32) (up): chunk c2/2 resp. 2 + c2/2, float4s 8(c2%2)..
+              for (int sl = 0; sl < un.nparts - 1; ++sl) {
+                const float4* w = reinterpret_cast<const float4*>(p.workspace + (int64_t)(un.slot + sl) * TM * BN);
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                  const float4 fg = w[((int64_t)(c2 >> 1) * 16 + 8 * (c2 & 1) + x) * TM + row];
+                  const float4 fu = w[((int64_t)(2 + (c2 >> 1)) * 16 + 8 * (c2 & 1) + x) * TM + row];
+                  g[4 * x] = __float_as_uint(__uint_as_float(g[4 * x]) + fg.x);
+                  g[4 * x + 1] = __float_as_uint(__uint_as_float(g[4 * x + 1]) + fg.y);
+                  g[4 * x + 2] = __float_as_uint(__uint_as_float(g[4 * x + 2]) + fg.z);
+                  g[4 * x + 3] = __float_as_uint(__uint_as_float(g[4 * x + 3]) + fg.w);
+                  up[4 * x] = __float_as_uint(__uint_as_float(up[4 * x]) + fu.x);
+                  up[4 * x + 1] = __float_as_uint(__uint_as_float(up[4 * x + 1]) + fu.y);
+                  up[4 * x + 2] = __float_as_uint(__uint_as_float(up[4 * x + 2]) + fu.z);
+                  up[4 * x + 3] = __float_as_uint(__uint_as_float(up[4 * x + 3]) + fu.w);
+                }
+              }
+            }
             if (c2 == 3) {
               tc_fence_before();
               __syncwarp();

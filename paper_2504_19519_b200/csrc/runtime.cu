@@ -318,8 +318,8 @@ static void run_gemm(fo_plan_s* p, const void* A, const void* Bt, void* dst, int
   if (!A || !Bt || !dst) fail(FO_ERR_INVALID_ARG, "null device pointer");
   GemmArgs a = gemm_args(p, A, Bt, dst, mode, signal);
   if (p->swiglu && mode == EPI_ROWMAJOR) {  // FO_OPT_GEMM_SWIGLU: C is [m, n/2] = silu(gate) * up
-    if (p->host.BN != 256 || p->host.coll != FO_NOCOMM || p->split > 1)
-      fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan, tile_n 256 and no tail split");
+    if (p->host.BN != 256 || p->host.coll != FO_NOCOMM)
+      fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan and tile_n 256");
     a.mode = EPI_SWIGLU;
     a.ldc = p->host.N / 2;
   }

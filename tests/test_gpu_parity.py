@@ -706,8 +706,8 @@ def test_add_rmsnorm_residual_in_place(ctx1, coll, layout, groups):
     assert _rel_err(_host(o_res), want_out) <= TOL
 
 
-@pytest.mark.parametrize("S,swz", [(8, 0), (3, 2)])
-def test_gemm_swiglu_epilogue(S, swz):
+@pytest.mark.parametrize("S,swz,split", [(8, 0, 0), (3, 2, 0), (7, 0, -1), (10, 0, -2)])
+def test_gemm_swiglu_epilogue(S, swz, split):
     """FO_OPT_GEMM_SWIGLU: the fused MLP activation in the GEMM epilogue
     equals silu(gate) * up of the fp64 product within one bf16 rounding
     (interleaved weight rows: blocks of 128 gate / 128 up)."""
@@ -720,6 +720,7 @@ def test_gemm_swiglu_epilogue(S, swz):
         Wi[256 * j + 128:256 * (j + 1)] = Wu[128 * j:128 * (j + 1)]
     plan = fo.Plan(coll="nocomm", m=M, n=2 * N2, k=K, tile_m=256, tile_n=256, workers=S, swizzle=swz)
     plan.set_option("gemm_swiglu", 1)
+    plan.set_option("tail_split", split)      # the owner folds the parts' partials in before the activation
     out = torch.full((M, N2), float("nan"), dtype=torch.bfloat16, device="cuda")
     fo.gemm_stage(plan, _dev_bf16(A), _dev_bf16(Wi), out)
     torch.cuda.synchronize()

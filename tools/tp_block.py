@@ -61,7 +61,7 @@ class Block:
             self.p_o, self.p_d = simple(Hl, "add_rmsnorm_res"), simple(Il, "add")
         tiles_gu = (T // 256) * (2 * Il // 256)
         self.p_gu = fo.Plan(coll="nocomm", m=T, n=2 * Il, k=H, tile_m=256, tile_n=256,
-                            workers=-(-tiles_gu // -(-tiles_gu // 74)), swizzle=0, options={"gemm_swiglu": 1})
+                            workers=-(-tiles_gu // -(-tiles_gu // 74)), swizzle=0, options={"gemm_swiglu": 1, "tail_split": -1})
         self.n = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
         self.a = torch.empty(T, Il, dtype=torch.bfloat16, device="cuda")
         self.y = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
