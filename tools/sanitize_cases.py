@@ -75,6 +75,23 @@ def main():
             if not torch.equal(out, C):
                 print("mismatch last_group_in_order", lio, groups)
                 bad += 1
+    # SwiGLU epilogue with a split tail, and the residual-writing RMSNorm
+    Ms, Ks = 256 * 3, 256
+    A4, W4 = synthetic.exact_inputs(Ms, 512, Ks, seed=4, nnz_per_row=50)
+    plan = fo.Plan(coll="nocomm", m=Ms, n=512, k=Ks, tile_m=256, tile_n=256, workers=5, swizzle=0)
+    plan.set_option("gemm_swiglu", 1)
+    plan.set_option("tail_split", -1)
+    sw = torch.empty(Ms, 256, dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, A4.cuda(), W4.cuda(), sw)
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=4, swizzle=1,
+                   group_waves=[1, 1], ar_layout="rowband", post="add_rmsnorm_res")
+    res2 = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, Ad, Bd, out, res2, gam)
+    torch.cuda.synchronize()
+    if not torch.equal(res2, C):
+        print("mismatch residual stream")
+        bad += 1
     # fused RMSNorm + row exchange
     plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=3, post="add_rmsnorm")
     local = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
