@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--workers", type=int, default=None,
                     help="S = concurrent tile workers (CTA pairs); default: fewest workers with the same wave count as all SMs")
     ap.add_argument("--groups", default=None, help="explicit wave-group partition, e.g. 1,1,2 (default: Alg. 1)")
+    ap.add_argument("--tail-split", type=int, default=0, help="FO_OPT_TAIL_SPLIT with --workers/--groups")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shards", action="store_true", help="skip the other configs' per-rank layers")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle sample")
@@ -338,6 +339,8 @@ def main():
         pred = fo.tune_predict(groups, gemm_us, tiles, S, BM * BN * 2, curve)
         spec = dict(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=0,
                     group_waves=list(groups), ar_layout="auto")
+        if args.tail_split:
+            spec["options"] = {"tail_split": args.tail_split}
         nspec = dict(spec, post="add_rmsnorm")
         pred_n = pred
     else:
