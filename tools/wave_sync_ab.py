@@ -30,8 +30,11 @@ def main():
         fns = {"cublas": lambda: torch.matmul(A, B.t(), out=C)}
         for S in map(int, args.s.split(",")):
             for wv in map(int, args.vals.split(",")):
-                pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0)
-                pl.set_option(args.opt, wv)
+                if args.opt == "swizzle":
+                    pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=wv)
+                else:
+                    pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0)
+                    pl.set_option(args.opt, wv)
                 fns[f"S={S} {args.opt}={wv}"] = (lambda pl=pl: fo.gemm_stage(pl, A, B, C))
         for f in fns.values():
             f()
