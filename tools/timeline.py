@@ -46,20 +46,60 @@ def one(ctx, coll, M, N, K, BN, S, groups, layout="slot", flush=None, wait_kerne
         lo, hi, _, _ = plan.group(j)
         print(f"  group {j}: tiles [{lo:4d},{hi:4d}) last signal {(t[lo:hi].max() - t0) / 1e3:8.1f} us | "
               f"wait released {(g[2 * j] - t0) / 1e3:8.1f} us | collective+post done {(g[2 * j + 1] - t0) / 1e3:8.1f} us")
+    return plan, t, g
+
+
+def chrome_trace(name, plan, t, g, S, pid):
+    """Chrome trace events (chrome://tracing / Perfetto) from the %globaltimer
+    stamps: one track per GEMM worker (tile p spans from the worker's previous
+    signal, or one median tile time before its first, to its own signal) and a
+    track for the communication stream (wait released -> collective + post
+    done), so the overlap of each group's collective with the GEMM's later
+    waves is visible as in an nsys timeline."""
+    ev = [{"name": "process_name", "ph": "M", "pid": pid, "args": {"name": name}}]
+    tiles = len(t)
+    per = {}
+    for p in range(tiles):
+        per.setdefault(p % S, []).append(p)
+    durs = [int(t[b] - t[a]) for ps in per.values() for a, b in zip(ps, ps[1:])]
+    med = int(np.median(durs)) if durs else 0
+    t0 = int(t.min()) - med  # ~ the GEMM's start
+    for w, ps in per.items():
+        prev = None
+        for p in ps:
+            end = int(t[p])
+            start = end - med if prev is None else prev
+            ev.append({"name": f"tile pos {p} (group {int(np.searchsorted([plan.group(j)[1] for j in range(plan.info['num_groups'])], p, side='right'))})",
+                       "ph": "X", "pid": pid, "tid": f"GEMM worker {w:02d}", "ts": (start - t0) / 1e3,
+                       "dur": max(end - start, 1) / 1e3})
+            prev = end
+    for j in range(len(g) // 2):
+        ev.append({"name": f"group {j}: collective + post", "ph": "X", "pid": pid, "tid": "comm stream",
+                   "ts": (int(g[2 * j]) - t0) / 1e3, "dur": max(int(g[2 * j + 1]) - int(g[2 * j]), 1) / 1e3})
+    return ev
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.parse_args()
+    ap.add_argument("--trace", default=None, help="also write a Chrome trace JSON of the first AR plans")
+    args = ap.parse_args()
     torch.cuda.set_device(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    events = []
     for wk in (0, 1):
-        one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 1, 1, 1], "slot", flush, wk)
-        one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 2, 1], "rowband", flush, wk)
+        r1 = one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 1, 1, 1], "slot", flush, wk)
+        r2 = one(ctx, "allreduce", 4096, 4096, 14336, 256, 64, [1, 2, 1], "rowband", flush, wk)
+        if args.trace and wk == 0:
+            events += chrome_trace("AR slot S=64 groups [1,1,1,1]", *r1, 64, 1)
+            events += chrome_trace("AR rowband S=64 groups [1,2,1]", *r2, 64, 2)
         one(ctx, "reducescatter", 8192, 8192, 1024, 256, 64, [2, 4, 6, 4], "auto", flush, wk)
         one(ctx, "alltoall", 1024, 4096, 14336, 128, 64, [1, 1], "auto", flush, wk)
     ctx.close()
+    if args.trace:
+        import json
+        with open(args.trace, "w") as f:
+            json.dump({"traceEvents": events, "displayTimeUnit": "ns"}, f)
 
 
 if __name__ == "__main__":
