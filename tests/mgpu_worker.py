@@ -72,6 +72,16 @@ def main():
         fo.run_sequential(ctx, plan, A, Bt, seq)
         torch.cuda.synchronize()
         check(f"{coll}/{layout}/{groups}/sequential", seq, want, bad)
+        # host buffers (chunked H2D the GEMM waits on, per-band D2H, two staging
+        # sets): back-to-back calls, each must equal the device result
+        outs = [torch.full((plan.info["out_rows"], N), float("nan"), dtype=torch.bfloat16).pin_memory()
+                for _ in range(3)]
+        A_h = A.cpu().pin_memory()
+        for o in outs:
+            fo.run_host(ctx, plan, A_h, Bt, o)
+        torch.cuda.synchronize()
+        for i, o in enumerate(outs):
+            check(f"{coll}/{layout}/{groups}/run_host[{i}]", o.cuda(), want, bad)
         if coll == "reducescatter":
             # RS follow-on (NEXT f2): AllGather + row exchange restores the
             # standard row order, i.e. the AllReduce result
