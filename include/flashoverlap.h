@@ -303,7 +303,10 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      wave (needs R*f <= S); the slice-0 owner adds the fp32
  *                      partials in its epilogue and signals as usual; -1 — auto
  *                      (f = min(4, S/R, k-blocks) when 2R <= S and that is >= 2;
- *                      else no split).  Set before the first run.
+ *                      else no split); -2 — stream-K tail: the tail's R x k-blocks
+ *                      dealt out evenly to the S workers in contiguous K-ranges
+ *                      (measured slower than -1, R34).  Works with every
+ *                      epilogue mode.  Set before the first run.
  *  FO_OPT_POST_SM_PARTITION 0 — per-group post kernels may co-reside with GEMM CTAs;
  *                      1 — they request padding shared memory so they only run on
  *                      the SMs the persistent GEMM leaves free (Alg. 1's SM split)
