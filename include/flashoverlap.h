@@ -164,6 +164,17 @@ fo_status fo_get_unique_id(uint8_t uid[128]);
  * GEMM leaves free; 0 = NCCL default.  Collective over the ranks. */
 fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128],
                         int32_t nccl_max_ctas, fo_ctx* out);
+/* Create a context on an EXISTING NCCL communicator (an ncclComm_t passed as
+ * void*, e.g. torch's ProcessGroupNCCL::_comm_ptr()): rank and world are read
+ * from it (ncclCommUserRank / ncclCommCount); it must live on `device`
+ * (ncclCommCuDevice), else FO_ERR_INVALID_ARG.  The communicator is BORROWED:
+ * fo_ctx_destroy does not destroy it and the fo_plan_sync watchdog does not
+ * abort it (it returns FO_ERR_TIMEOUT and the context stays unusable, aborting
+ * is the owner's call).  The caller keeps it alive until fo_ctx_destroy, and
+ * NCCL calls it issues on other streams are ordered against the library's only
+ * by the caller.  Local (not collective); the NCCL config (maxCTAs) is the
+ * owner's. */
+fo_status fo_ctx_create_from_comm(int32_t device, void* nccl_comm, fo_ctx* out);
 fo_status fo_ctx_destroy(fo_ctx ctx);
 
 /* Offline stage of the tuner ("the bandwidth curve is sampled

@@ -195,6 +195,15 @@ class Context:
         check(load().fo_ctx_create(device, rank, world, buf, nccl_max_ctas, C.byref(h)))
         return cls(h, device, rank, world)
 
+    @classmethod
+    def from_comm(cls, device: int, nccl_comm: int, rank=None, world=None) -> "Context":
+        """Context on an existing ncclComm_t (borrowed, never destroyed here);
+        the library takes rank and world from the communicator
+        (fo_ctx_create_from_comm); `rank`/`world` only label this object."""
+        h = C.c_void_p()
+        check(load().fo_ctx_create_from_comm(device, C.c_void_p(int(nccl_comm)), C.byref(h)))
+        return cls(h, device, rank, world)
+
     def time_collective(self, coll: str, nbytes: int, iters: int = 5) -> float:
         """Average us of one collective of `nbytes` on this context's communicator (tuning)."""
         out = C.c_double()

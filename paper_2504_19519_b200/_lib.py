@@ -73,6 +73,7 @@ _SIGS = [
     ("fo_get_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
     ("fo_ctx_create", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32,
                                 C.POINTER(_P)]),
+    ("fo_ctx_create_from_comm", C.c_int, [C.c_int32, _P, C.POINTER(_P)]),
     ("fo_ctx_destroy", C.c_int, [_P]),
     ("fo_ctx_time_collective", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double)]),
     ("fo_run", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),

@@ -33,6 +33,7 @@
 struct fo_ctx_s {
   int device = 0;
   bool aborted = false;                // the watchdog (fo_plan_sync) aborted the communicator
+  bool owns_comm = true;               // false: borrowed (fo_ctx_create_from_comm), never destroyed/aborted here
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -527,6 +528,27 @@ fo_status fo_device_sm_count(int32_t device, int32_t* sm_count) {
   });
 }
 
+// streams and events of a context (both constructors)
+static void init_streams(fo_ctx_s* c) {
+  int lo = 0, hi = 0;
+  FO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // highest priority for the communication stream
+  FO_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+  // post-reorder one step below the collectives (pending NCCL CTAs are
+  // scheduled first), still above default-priority work
+  FO_CUDA(cudaStreamCreateWithPriority(&c->post_stream, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+  FO_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  FO_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  FO_CUDA(cudaEventCreateWithFlags(&c->ev_post_join, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    FO_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream[i], cudaStreamNonBlocking));
+    FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_join[i], cudaEventDisableTiming));
+  }
+  FO_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_fork, cudaEventDisableTiming));
+  FO_CUDA(cudaEventCreateWithFlags(&c->ev_d2h_join, cudaEventDisableTiming));
+}
+
 fo_status fo_get_unique_id(uint8_t uid[128]) {
   return guard([&] {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -555,25 +577,35 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
         cfg.minCTAs = 1;
       }
       FO_NCCL(ncclCommInitRankConfig(&c->comm, world, id, rank, &cfg));
-      int lo = 0, hi = 0;
-      FO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      // highest priority for the communication stream
-      FO_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
-      // post-reorder one step below the collectives (pending NCCL CTAs are
-      // scheduled first), still above default-priority work
-      FO_CUDA(cudaStreamCreateWithPriority(&c->post_stream, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
-      FO_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-      FO_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-      FO_CUDA(cudaEventCreateWithFlags(&c->ev_post_join, cudaEventDisableTiming));
-      for (int i = 0; i < 2; ++i) {
-        FO_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream[i], cudaStreamNonBlocking));
-        FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_join[i], cudaEventDisableTiming));
-      }
-      FO_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
-      FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_fork, cudaEventDisableTiming));
-      FO_CUDA(cudaEventCreateWithFlags(&c->ev_d2h_join, cudaEventDisableTiming));
+      init_streams(c);
     } catch (...) {
       if (c->comm) ncclCommDestroy(c->comm);
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+fo_status fo_ctx_create_from_comm(int32_t device, void* nccl_comm, fo_ctx* out) {
+  return guard([&] {
+    if (!nccl_comm || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+    int count = 0, rank = 0, cudev = -1;
+    FO_NCCL(ncclCommCount(comm, &count));
+    FO_NCCL(ncclCommUserRank(comm, &rank));
+    FO_NCCL(ncclCommCuDevice(comm, &cudev));
+    if (cudev != device) fail(FO_ERR_INVALID_ARG, "communicator is on device %d, not %d", cudev, device);
+    FO_CUDA(cudaSetDevice(device));
+    auto* c = new fo_ctx_s();
+    c->device = device;
+    c->rank = rank;
+    c->world = count;
+    c->comm = comm;
+    c->owns_comm = false;
+    try {
+      init_streams(c);
+    } catch (...) {
       delete c;
       throw;
     }
@@ -586,7 +618,7 @@ fo_status fo_ctx_destroy(fo_ctx c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm && c->owns_comm) ncclCommDestroy(c->comm);
     if (c->post_stream) cudaStreamSynchronize(c->post_stream);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->post_stream) cudaStreamDestroy(c->post_stream);
@@ -1121,7 +1153,8 @@ fo_status fo_plan_sync(fo_ctx c, fo_plan p, void* stream, int64_t timeout_ms) {
     //    (ncclCommAbort makes in-flight NCCL kernels exit)
     const bool done = drained(std::max<int64_t>(timeout_ms, 1000));
     if (c->comm) {
-      ncclCommAbort(c->comm);
+      // a borrowed communicator is its owner's to abort; drop it either way
+      if (c->owns_comm) ncclCommAbort(c->comm);
       c->comm = nullptr;
     }
     if (!done) drained(std::max<int64_t>(timeout_ms, 1000));

@@ -25,6 +25,19 @@ def make_context(device: int, group=None, nccl_max_ctas: int = 0) -> Context:
     return Context.create(device, dist.get_rank(group), dist.get_world_size(group), uid, nccl_max_ctas)
 
 
+def context_from_process_group(device: int, group=None) -> Context:
+    """Context on the NCCL communicator torch's process group already holds
+    (ProcessGroupNCCL._comm_ptr(); borrowed: the group keeps owning it, so the
+    library adds no communicator of its own).  Collective: a one-element
+    all_reduce first makes sure the group's communicator exists."""
+    import torch
+    t = torch.zeros(1, device=torch.device("cuda", device))
+    dist.all_reduce(t, group=group)
+    pg = group if group is not None else dist.group.WORLD
+    comm = pg._get_backend(torch.device("cuda", device))._comm_ptr()
+    return Context.from_comm(device, comm, dist.get_rank(group), dist.get_world_size(group))
+
+
 def _plain(spec: dict) -> dict:
     out = {}
     for k, v in spec.items():
@@ -47,4 +60,4 @@ def make_plan(group=None, **spec) -> Plan:
     return Plan(rank=rank, world=world, peers=peers, **spec)
 
 
-__all__ = ["broadcast_unique_id", "make_context", "gather_specs", "make_plan", "PlanSpec"]
+__all__ = ["broadcast_unique_id", "make_context", "context_from_process_group", "gather_specs", "make_plan", "PlanSpec"]

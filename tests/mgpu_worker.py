@@ -8,7 +8,8 @@ exact-integer inputs, and compares both with the plain definition computed by
 this script with torch.distributed in fp32 (exact for these integers):
 AllReduce = sum_r C_r; ReduceScatter = rows R_k of the sum (block-cyclic,
 DESIGN.md R8), and its AllGather + row exchange = the AllReduce result;
-All-to-All = concat over sources of the rows routed here (R9).  Exit status 0 = every comparison bit-exact.  Test infrastructure.
+All-to-All = concat over sources of the rows routed here (R9).  One AllReduce
+also runs on a context built on torch's own communicator (fo_ctx_create_from_comm).  Exit status 0 = every comparison bit-exact.  Test infrastructure.
 """
 import os
 import sys
@@ -89,6 +90,23 @@ def main():
             fo.run_allgather(ctx, plan, out, gathered)
             torch.cuda.synchronize()
             check("reducescatter/allgather+rowexchange", gathered, full.to(torch.bfloat16), bad)
+    # a context on torch's own communicator (fo_ctx_create_from_comm: borrowed,
+    # the process group stays usable after the context is destroyed)
+    tctx = fodist.context_from_process_group(local)
+    A, Bt = exact_inputs(M, N, K, rank, world, 31)
+    plan = fodist.make_plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=8,
+                            swizzle=2, group_waves=[1, 2, 1], ar_layout="slot")
+    full = A.float() @ Bt.float().t()
+    dist.all_reduce(full)
+    out = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    fo.run(tctx, plan, A, Bt, out)
+    torch.cuda.synchronize()
+    check("allreduce/torch-comm", out, full.to(torch.bfloat16), bad)
+    tctx.close()
+    probe = torch.ones(1, device="cuda")
+    dist.all_reduce(probe)
+    if probe.item() != world:
+        bad.append("process group after borrowed-context destroy")
     # All-to-All (EP combine): imbalanced experts, random routing
     rng = np.random.default_rng(7)
     Ms = [256 * int(rng.integers(1, 5)) for _ in range(world)]

@@ -277,3 +277,10 @@ def test_tuner_multi_matches_oracle():
             assert alg1.predict_multi(got, list(durs), wb.tolist(), lat) == pytest.approx(want_t, rel=1e-12)
             _, dp_t = fo.tune_search_multi(durs, wb, curve, prune=dp)
             assert dp_t == pytest.approx(want_t, rel=1e-12)
+
+
+def test_ctx_from_comm_rejects_null():
+    # argument check precedes any NCCL/CUDA call: runs without a GPU
+    from paper_2504_19519_b200._lib import FOError
+    with pytest.raises(FOError, match="null"):
+        fo.Context.from_comm(0, 0)
