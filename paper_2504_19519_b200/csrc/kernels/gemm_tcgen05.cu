@@ -118,8 +118,23 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
   return r;
 }
 
+// arrive on a barrier of another CTA of the cluster.  Default semantics
+// (.release.cta): the only data ordered by it are TMEM reads, already ordered
+// by tcgen05.wait::ld + tcgen05.fence::before_thread_sync; .release.cluster
+// would add a MEMBAR.GPU that waits for the warp's outstanding global stores.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// one lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 // 2-SM TMA: data lands in this CTA's smem, the transaction bytes are counted
@@ -182,21 +197,35 @@ __device__ __forceinline__ constexpr uint32_t idesc_bf16() {
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// The four K=16 MMAs of one 64-wide k-block from ONE elected lane of a
+// converged warp: descriptors step by da / db (16-byte units) per MMA; the
+// first accumulates into D unless `acc` is 0.  One elect and one operand
+// transfer to uniform registers per k-block instead of per MMA.
 template <int CG>
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void umma_kblock(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t da, uint32_t db,
+                                            uint32_t idesc, uint32_t acc) {
+  static_assert(BK == 64, "four K=16 steps per k-block");
+#define FO_UMMA_CG(cg)                                                                          \
+  asm volatile(                                                                                 \
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, sa, sb;\n\t"         \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                       \
+      "setp.ne.b32 p, %4, 0;\n\t"                                                             \
+      "setp.eq.u32 t, 0, 0;\n\t"                                                              \
+      "cvt.u64.u32 sa, %5;\n\t"                                                               \
+      "cvt.u64.u32 sb, %6;\n\t"                                                               \
+      "add.s64 a1, %1, sa;\n\tadd.s64 a2, a1, sa;\n\tadd.s64 a3, a2, sa;\n\t"             \
+      "add.s64 b1, %2, sb;\n\tadd.s64 b2, b1, sb;\n\tadd.s64 b3, b2, sb;\n\t"             \
+      "@e tcgen05.mma.cta_group::" #cg ".kind::f16 [%0], %1, %2, %3, p;\n\t"                  \
+      "@e tcgen05.mma.cta_group::" #cg ".kind::f16 [%0], a1, b1, %3, t;\n\t"                  \
+      "@e tcgen05.mma.cta_group::" #cg ".kind::f16 [%0], a2, b2, %3, t;\n\t"                  \
+      "@e tcgen05.mma.cta_group::" #cg ".kind::f16 [%0], a3, b3, %3, t;\n\t}" ::"r"(d_tmem),  \
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(da), "r"(db))
   if constexpr (CG == 1) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    FO_UMMA_CG(1);
   } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    FO_UMMA_CG(2);
   }
+#undef FO_UMMA_CG
 }
 
 // MMA completion -> mbarrier arrive; for a pair, multicast to the barrier at
@@ -479,8 +508,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer (one thread of the leader CTA)
-    if (lane == 0 && leader) {
+    // ======================= MMA issuer (leader CTA): the whole warp runs the
+    // loop (warp-uniform operands stay in uniform registers), one elected lane
+    // issues each tcgen05.mma / commit
+    if (leader) {
       constexpr uint32_t idesc = idesc_bf16<TM, BN, MJ>();
       int stage = 0;
       uint32_t phase = 0;
@@ -498,33 +529,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);
           const uint32_t sb = smem_u32(sB + stage * C::B_STAGE_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // K-major: +32 bytes along K inside the 128-byte swizzle row (+2 in the
-            // >>4 address field); MN-major: +2 core groups of 8 k-rows (+2048 B)
-            const uint64_t adesc = (MJ & 1) ? sw128_mn_desc(sa + 2048 * kk) : sw128_desc(sa) + 2 * kk;
-            const uint64_t bdesc = (MJ & 2) ? sw128_mn_desc(sb + 2048 * kk) : sw128_desc(sb) + 2 * kk;
-            umma_bf16<CG>(d_tmem, adesc, bdesc, idesc, (kb != un.kb0 || kk != 0) ? 1u : 0u);
-          }
+          // per K=16 step: K-major +32 bytes along K inside the 128-byte swizzle
+          // row (+2 in the >>4 address field); MN-major +2 core groups of 8
+          // k-rows (+2048 B = +128); the field never carries (smem < 256 KB)
+          umma_kblock<CG>(d_tmem, (MJ & 1) ? sw128_mn_desc(sa) : sw128_desc(sa),
+                          (MJ & 2) ? sw128_mn_desc(sb) : sw128_desc(sb), (MJ & 1) ? 128u : 2u, (MJ & 2) ? 128u : 2u,
+                          idesc, kb != un.kb0 ? 1u : 0u);
           // frees the smem stage when these MMAs retire: in both CTAs of the
           // pair; with a multicast partner in all four CTAs (count 2 each), and
           // alone (partner done) twice in the pair's own CTAs
-          if constexpr (MC == 2) {
-            if ((u ^ 1) < p.tiles) {
-              umma_commit<CG>(&empty[stage], 0xF);
+          if (elect_one()) {
+            if constexpr (MC == 2) {
+              if ((u ^ 1) < p.tiles) {
+                umma_commit<CG>(&empty[stage], 0xF);
+              } else {
+                umma_commit<CG>(&empty[stage], pair_mask);
+                umma_commit<CG>(&empty[stage], pair_mask);
+              }
             } else {
-              umma_commit<CG>(&empty[stage], pair_mask);
-              umma_commit<CG>(&empty[stage], pair_mask);
+              umma_commit<CG>(&empty[stage]);
             }
-          } else {
-            umma_commit<CG>(&empty[stage]);
           }
+          __syncwarp();
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit<CG>(&tfull[acc], pair_mask);  // accumulator ready for the pair's epilogues
+        if (elect_one()) umma_commit<CG>(&tfull[acc], pair_mask);  // accumulator ready for the pair's epilogues
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           aphase ^= 1;

@@ -23,12 +23,14 @@ def main():
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--multicast", type=int, default=0)
     ap.add_argument("--tail-split", type=int, default=0)
+    ap.add_argument("--tile", default="256x256", help="tile_m x tile_n")
     args = ap.parse_args()
     M, N, K = map(int, args.shape.split("x"))
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     B = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=args.workers, swizzle=0)
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=int(args.tile.split("x")[0]),
+                   tile_n=int(args.tile.split("x")[1]), workers=args.workers, swizzle=0)
     plan.set_option("wave_sync", args.wave)
     plan.set_option("multicast", args.multicast)
     plan.set_option("tail_split", args.tail_split)
