@@ -17,7 +17,6 @@ import torch  # noqa: E402
 import paper_2504_19519_b200 as fo  # noqa: E402
 import synthetic  # noqa: E402
 
-TILES = [(256, 256), (256, 128), (128, 256), (128, 128)]
 
 
 def widths(tiles, cg):
@@ -29,7 +28,10 @@ def widths(tiles, cg):
         S = -(-tiles // T)
         if S <= full:
             out.add(S)
-    return sorted(out, reverse=True)[:4]
+    out = sorted(out, reverse=True)[:4]
+    if cg == 2 and full not in out:
+        out.append(full)          # stream-K candidates use every pair
+    return out
 
 
 def main():
@@ -37,6 +39,7 @@ def main():
     ap.add_argument("--shapes", default="1024x4096x4096,2048x4096x4096,4096x4096x4096,1024x8192x8192,"
                                         "4096x4096x1792,4096x4096x3584,8192x8192x2048")
     ap.add_argument("--iters", type=int, default=9)
+    ap.add_argument("--tiles", default="256x256,256x128,128x256,128x128")
     args = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for sh in args.shapes.split(","):
@@ -44,12 +47,12 @@ def main():
         A, Bt = synthetic.float_inputs(M, N, K, seed=3, device="cuda")
         C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         fns = {"cublas": lambda: torch.matmul(A, Bt.t(), out=C)}
-        for tm, tn in TILES:
+        for tm, tn in [tuple(map(int, t.split("x"))) for t in args.tiles.split(",")]:
             if M % tm or N % tn:
                 continue
             tiles = (M // tm) * (N // tn)
             for S in widths(tiles, 2 if tm == 256 else 1):
-                for ts in (0, -1):
+                for ts in ((0, -1, -2) if tm == 256 and tn == 256 else (0, -1)):
                     pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S, swizzle=0,
                                  options={"tail_split": ts})
                     fns[f"{tm}x{tn} S={S} ts={ts}"] = (lambda pl=pl: fo.gemm_stage(pl, A, Bt, C))
