@@ -371,11 +371,18 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      weight rows interleaved in blocks of 128 (gate 0..127, up
  *                      0..127, gate 128..255, up 128..255, ...), tile column block
  *                      j writes C[:, 128j .. 128j+128) = silu(gate) * up from the
- *                      fp32 accumulators (one bf16 rounding); C is [m, n/2] */
+ *                      fp32 accumulators (one bf16 rounding); C is [m, n/2]
+ *  FO_OPT_DIST_FOLD    1 (default) — with an f-slice tail split, the K-slices of a
+ *                      split tile reduce it together: 64-column chunk c is summed
+ *                      and stored by slice c % f, each slice publishing the fp32
+ *                      partials of the chunks it does not own; 0 — the slice
+ *                      starting at k-block 0 folds every chunk (the SwiGLU
+ *                      epilogue and the stream-K tail always fold this way) */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
                FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8,
-               FO_OPT_DEBUG_STALL_GROUP = 10, FO_OPT_GEMM_SWIGLU = 11 } fo_option;
+               FO_OPT_DEBUG_STALL_GROUP = 10, FO_OPT_GEMM_SWIGLU = 11,
+               FO_OPT_DIST_FOLD = 12 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

@@ -21,7 +21,8 @@ enum EpiMode : int {
 // role 1 = owner (the range starting at k-block 0; folds nparts-1 partials
 // from workspace slots slot.. in), role 2 = part (publishes to slot `slot`).
 struct GemmSeg {
-  int pos, kb0, kb1, role, slot, nparts, tt, pad;
+  int pos, kb0, kb1, role, slot, nparts, tt;
+  int idx;  // participant index of the tile in k order (0 = owner)
 };
 
 struct GemmArgs {
@@ -51,6 +52,12 @@ struct GemmArgs {
   const int32_t* wseg;         // [S + 1] worker w's segments: seg[wseg[w] .. wseg[w+1])
   float* workspace;            // fp32 partials [slots][TM][BN]
   uint32_t* flags;             // [(tiles - tail_pos) * CG] partial-ready counts (reset with the counters)
+  // distributed fold (f-slice split, every participant's last unit): 64-column
+  // chunk c of a split tile is reduced and stored by participant c % nparts;
+  // each participant publishes the chunks it does not own (the owner into
+  // slot + nparts - 1), and the last one to store signals the tile (`done`)
+  int dist_fold;
+  uint32_t* done;              // [(tiles - tail_pos) * CG] participants finished (reset with the counters)
   // ---- host-staged A (fo_run_host pipelining): A arrives in chunks of
   // a_chunk_rows tile-rows; the producer loads a tile's A only once
   // a_ready[ti / a_chunk_rows] has reached a_epoch (null: A is resident)

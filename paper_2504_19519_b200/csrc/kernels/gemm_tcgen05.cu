@@ -273,6 +273,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -287,7 +293,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 // folds the other parts' fp32 partials in, writes and signals the tile),
 // 2 part (publishes its fp32 partial to workspace slot `slot`).
 struct Unit {
-  int pos, kb0, kb1, role, slot, nparts, tt;
+  int pos, kb0, kb1, role, slot, nparts, tt, idx;
 };
 
 __device__ __forceinline__ int unit_count(const GemmArgs& p, int worker, int nworkers) {
@@ -306,6 +312,7 @@ __device__ __forceinline__ Unit my_unit(const GemmArgs& p, int worker, int nwork
     r.slot = 0;
     r.nparts = 1;
     r.tt = 0;
+    r.idx = 0;
   } else {
     const GemmSeg sg = p.seg[p.wseg[worker] + (k - nreg)];
     r.pos = sg.pos;
@@ -315,6 +322,7 @@ __device__ __forceinline__ Unit my_unit(const GemmArgs& p, int worker, int nwork
     r.slot = sg.slot;
     r.nparts = sg.nparts;
     r.tt = sg.tt;
+    r.idx = sg.idx;
   }
   return r;
 }
@@ -609,6 +617,104 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], aphase);
       if (k + 1 < nu) prefetch_dst(my_unit(p, worker, nworkers, k + 1, KB).pos);
       tc_fence_after();
+      if (p.dist_fold && p.mode != EPI_SWIGLU && (owner || part)) {
+        // distributed fold of a split tile (f-slices: every slice is its
+        // worker's last unit, so slices may wait on each other): slice `me`
+        // reduces and stores the 64-column chunks c with c % f == me and
+        // publishes the fp32 partials of the others to its own slot
+        constexpr int NC = BN / EPI_COLS;
+        const int f = un.nparts, me = un.idx;
+        const int base = owner ? un.slot : un.slot - me + 1;  // the tile's first slot
+        auto pslot = [&](int j) { return j == 0 ? base + f - 1 : base + j - 1; };
+        auto release_tmem = [&]() {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+            else mbar_arrive_cluster(tempty_leader0 + 8u * acc);
+          }
+        };
+        const bool has_own = me < NC;
+#pragma unroll 1
+        for (int c = 0; c < NC; ++c) {
+          if (c % f == me) continue;
+          uint32_t v[64];
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * EPI_COLS);
+          tmem_ld32(taddr, v);
+          tmem_ld32(taddr + 32, v + 32);
+          tmem_wait_ld();
+          float4* w = reinterpret_cast<float4*>(p.workspace + (int64_t)pslot(me) * TM * BN) + (int64_t)c * 16 * TM + row;
+#pragma unroll
+          for (int x = 0; x < 16; ++x)
+            w[x * TM] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                    __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
+        }
+        if (!has_own) release_tmem();
+        // published -> count it; then wait for every slice's partials
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) {
+          uint32_t* fl = p.flags + tt * CG + half;
+          red_release_add(fl, 1u);
+          while (ld_acquire(fl) < (uint32_t)f) __nanosleep(32);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int last_own = has_own ? me + ((NC - 1 - me) / f) * f : -1;
+#pragma unroll 1
+        for (int c = me; c < NC; c += f) {
+          uint32_t v[64];
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * EPI_COLS);
+          tmem_ld32(taddr, v);
+          tmem_ld32(taddr + 32, v + 32);
+          tmem_wait_ld();
+          if (c == last_own) release_tmem();
+          // the other slices' partials in k order (deterministic)
+          for (int j = 0; j < f; ++j) {
+            if (j == me) continue;
+            const float4* w =
+                reinterpret_cast<const float4*>(p.workspace + (int64_t)pslot(j) * TM * BN) + (int64_t)c * 16 * TM + row;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+              const float4 fv = w[x * TM];
+              v[4 * x] = __float_as_uint(__uint_as_float(v[4 * x]) + fv.x);
+              v[4 * x + 1] = __float_as_uint(__uint_as_float(v[4 * x + 1]) + fv.y);
+              v[4 * x + 2] = __float_as_uint(__uint_as_float(v[4 * x + 2]) + fv.z);
+              v[4 * x + 3] = __float_as_uint(__uint_as_float(v[4 * x + 3]) + fv.w);
+            }
+          }
+          uint4* srow = reinterpret_cast<uint4*>(stg + lane * EPI_PITCH);
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            uint4 o;
+            o.x = pack_bf16(v[8 * x + 0], v[8 * x + 1]);
+            o.y = pack_bf16(v[8 * x + 2], v[8 * x + 3]);
+            o.z = pack_bf16(v[8 * x + 4], v[8 * x + 5]);
+            o.w = pack_bf16(v[8 * x + 6], v[8 * x + 7]);
+            srow[x] = o;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + (lane >> 3);
+            const uint4 o = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + (lane & 7) * 16);
+            *reinterpret_cast<uint4*>(drow[it] + c * EPI_COLS) = o;
+          }
+          __syncwarp();
+        }
+        // the last slice to finish its chunks signals the tile (acq_rel: the
+        // other slices' stores, released by their increments, precede ours)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) {
+          if (atom_add_acq_rel(p.done + tt * CG + half, 1u) == (uint32_t)(f - 1)) {
+            if (p.counters) red_release_add(&p.counters[p.group_of_pos[pos]], 1u);
+            if (p.tile_ts && leader) p.tile_ts[pos] = globaltimer();
+          }
+        }
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+        continue;
+      }
       if (owner) {
         // owner of a split tile: wait until the other parts' partials of this
         // CTA's rows are published (acquire), then fold them in below

@@ -200,10 +200,13 @@ static void ensure_device(fo_plan_s* p) {
       std::vector<int> nparts(R, 0), first_slot(R, -1);
       for (int w = 0; w < h.S; ++w)
         for (auto& pc : pieces[w]) ++nparts[pc[0]];
+      // f-slices also reserve one slot per tile for the owner's own partial
+      // (the distributed fold, R34)
       for (int r = 0; r < R; ++r) {
         first_slot[r] = nslots;
-        nslots += nparts[r] - 1;
+        nslots += nparts[r] - 1 + (streamk ? 0 : 1);
       }
+      std::vector<int> next_idx(R, 0);
       std::vector<int> next_slot = first_slot;
       for (int w = 0; w < h.S; ++w) {
         wseg[w] = (int)segs.size();
@@ -214,6 +217,7 @@ static void ensure_device(fo_plan_s* p) {
           sg.kb1 = pc[2];
           sg.tt = pc[0];
           sg.nparts = nparts[pc[0]];
+          sg.idx = pc[1] == 0 ? 0 : ++next_idx[pc[0]];
           if (sg.nparts == 1) {
             sg.role = 0;
           } else if (pc[1] == 0) {
@@ -233,7 +237,8 @@ static void ensure_device(fo_plan_s* p) {
     p->tail_pos = split ? tail0 : h.tiles;
     p->units = split ? tail0 + (int)segs.size() : h.tiles;
     const int cg = h.BM / 128;
-    p->ctr_words = h.P + (split ? R * cg : 0);
+    p->dist_fold = split && !streamk;
+    p->ctr_words = h.P + (split ? R * cg * (p->dist_fold ? 2 : 1) : 0);
     if (split) {
       p->d_seg = upload(segs);
       p->d_wseg = upload(wseg);
@@ -291,6 +296,8 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   a.wseg = p->d_wseg;
   a.workspace = p->d_ws;
   a.flags = p->d_flags;
+  a.dist_fold = p->dist_fold && p->dist_fold_opt;
+  a.done = p->dist_fold ? p->d_flags + (h.tiles - p->tail_pos) * (h.BM / 128) : nullptr;
   if (p->a_staged_run) {
     a.a_ready = p->d_a_ready + (size_t)p->host_set * p->a_chunks;
     a.a_epoch = p->a_epoch;
@@ -1276,6 +1283,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_HOST_PIPELINE:
         if (value < 0 || value > 7) fail(FO_ERR_INVALID_ARG, "host_pipeline must be 0..7");
         p->host_pipeline = (int)value;
+        break;
+      case FO_OPT_DIST_FOLD:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "dist_fold must be 0 or 1");
+        p->dist_fold_opt = (int)value;
         break;
       case FO_OPT_GEMM_SWIGLU:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "gemm_swiglu must be 0 or 1");

@@ -55,6 +55,8 @@ struct fo_plan_s {
   int tail_split_req = 0;                         // FO_OPT_TAIL_SPLIT: 0/1 off, >=2 slices, -1 auto, -2 stream-K
   // ---- resolved tail split (set by ensure_device)
   int split = 1, tail_pos = 0, units = 0;
+  int dist_fold = 0;                              // f-slice split: distributed fold possible
+  int dist_fold_opt = 1;                          // FO_OPT_DIST_FOLD
   float* d_ws = nullptr;                          // fp32 partials of the split tail
   fo::GemmSeg* d_seg = nullptr;                   // the split tail's K-ranges by worker
   int32_t* d_wseg = nullptr;                      // [S+1] per-worker segment offsets

@@ -295,13 +295,21 @@ def test_tile_timestamps_follow_waves(BM):
     (256, 256, 1024, 2048, 1024, 10, -2),   # stream-K, 1 wave: 32 tiles... T=4, R=2 over 10 workers
     (256, 128, 768, 1024, 576, 20, -2),     # stream-K: 24 tiles, T=2, R=4, 9 k-blocks (uneven ranges)
     (128, 256, 512, 1024, 1024, 14, -2),    # stream-K with single-CTA tiles
+    (256, 64, 512, 512, 256, 12, 2),        # 16 tiles, R=4, f=2, one 64-col chunk: slice 1 owns none
+    (256, 128, 512, 1024, 512, 14, 3),      # 16 tiles, R=2, f=3, two chunks: slice 2 owns none
 ])
-def test_tail_split_exact(ctx1, BM, BN, M, N, K, S, split):
+@pytest.mark.parametrize("dist_fold", [1, 0])
+def test_tail_split_exact(ctx1, BM, BN, M, N, K, S, split, dist_fold):
+    """Split tail (R34), both folds of an f-slice split (FO_OPT_DIST_FOLD: the
+    slices reduce the tile together / the k-block-0 slice folds everything)."""
+    if split == -2 and dist_fold == 0:
+        pytest.skip("stream-K always folds in the owner")
     A, Bt = synthetic.exact_inputs(M, N, K, seed=77, nnz_per_row=256)
     C = onum.gemm(A, Bt)
     for coll in ("nocomm", "allreduce"):
         plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2, ar_layout="slot")
         plan.set_option("tail_split", split)
+        plan.set_option("dist_fold", dist_fold)
         # one group: keep it counter-triggered so the counting table is exercised (R32)
         plan.set_option("last_group_in_order", 0)
         out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")

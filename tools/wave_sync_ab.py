@@ -1,4 +1,4 @@
-"""A/B of a GEMM plan option (FO_OPT_WAVE_SYNC, FO_OPT_MULTICAST; dev tool): the two plans (and cuBLAS)
+"""A/B of a GEMM plan option (FO_OPT_WAVE_SYNC, FO_OPT_MULTICAST, FO_OPT_DIST_FOLD, ...; dev tool): the two plans (and cuBLAS)
 run interleaved, L2 flushed before each, so clock / power drift hits all
 alike; medians."""
 import argparse
@@ -20,7 +20,9 @@ def main():
     ap.add_argument("--iters", type=int, default=15)
     ap.add_argument("--opt", default="wave_sync")
     ap.add_argument("--vals", default="0,1")
+    ap.add_argument("--base", default="", help="options set on every plan, e.g. tail_split=-1")
     args = ap.parse_args()
+    base = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.base.split(",") if kv}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for sh in args.shapes.split(","):
         M, N, K = map(int, sh.split("x"))
@@ -33,7 +35,8 @@ def main():
                 if args.opt == "swizzle":
                     pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=wv)
                 else:
-                    pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0)
+                    pl = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0,
+                                 options=base)
                     pl.set_option(args.opt, wv)
                 fns[f"S={S} {args.opt}={wv}"] = (lambda pl=pl: fo.gemm_stage(pl, A, B, C))
         for f in fns.values():
