@@ -399,6 +399,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
     }
   }
+  if (warp == 3 && lane == 0) {
+    // warm L2 with the table entries the producer needs for its first TMA
+    // (cold after an L2 flush) while the setup below runs; non-blocking
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.order + worker));
+    if (p.seg) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.wseg + worker));
+  }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
@@ -435,11 +441,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int ready_chunk = -1;
+      // the first regular unit's tile is loaded independently of the segment
+      // table, so the two loads overlap
+      const bool reg0 = p.tail_pos > worker;
+      const int t_first = reg0 ? p.order[worker] : 0;
       const int nu = unit_count(p, worker, nworkers);
       for (int k = 0; k < nu; ++k) {
         const Unit un = my_unit(p, worker, nworkers, k, KB);
         const int u = un.pos;  // == worker + k*S without a split tail (multicast / wave sync)
-        const int t = p.order[un.pos];
+        const int t = (k == 0 && reg0) ? t_first : p.order[un.pos];
         const int ti = t / p.Nt, tj = t - ti * p.Nt;
         if (p.a_ready && ti / p.a_chunk_rows != ready_chunk) {
           // host-staged A: wait until this tile-row's chunk has landed (the
