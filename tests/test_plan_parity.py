@@ -189,7 +189,8 @@ def test_option_contract():
     pl = fo.Plan(coll="allreduce", m=256, n=256, k=64, tile_m=256, tile_n=128, workers=2)
     for name, good, bad in (("last_group_in_order", (0, 1), (2, -1)), ("wave_sync", (0, 1), (2,)),
                             ("multicast", (0, 1), (2,)), ("wait_kernel", (0, 1), (2,)),
-                            ("group_post", (-1, 0, 1), (2,)), ("host_pipeline", (0, 3, 7), (8,))):
+                            ("group_post", (-1, 0, 1), (2,)), ("host_pipeline", (0, 3, 7), (8,)),
+                            ("dist_fold", (0, 1), (2, -1))):
         for v in good:
             pl.set_option(name, v)
         for v in bad:
