@@ -171,14 +171,21 @@ __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p, 
 // Residual add + RMSNorm: one THREADS-thread block per row, the whole row held
 // in registers (MAXC chunks of 8 per thread, N <= 8*THREADS*MAXC), single pass
 // over HBM: read x (through the map) and residual once, write out once.
-// 128-thread blocks with 4 chunks per thread keep 2x the rows (and 8
-// independent 16-byte loads per thread) in flight compared with 256 x 2.
+// Rows of 2048..8192 columns use 256-thread blocks with 2..4 chunks per
+// thread and prefetch the block's next row (PF below): measured 2-4% faster
+// than 128 x 4 without the prefetch (profiles/r01_post_reorder_probe.txt);
+// a cluster of blocks per row with a DSMEM reduction was slower still.
 // RES: also write y = x + residual (bf16) back into the residual buffer (the
 // residual stream of a pre-norm block); each row's residual is read before
 // its own write, by the same thread, so in place is safe.
 template <int MAP, int MAXC, int THREADS, bool RES>
 __global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs p, int lbn) {
   constexpr int WARPS = THREADS / 32;
+  // rows of up to 4 chunks per thread also prefetch the block's next row while
+  // reducing / writing the current one: without it every resident block
+  // alternates a load phase and a reduce + store phase in step with the
+  // others, leaving HBM idle in between
+  constexpr bool PF = MAXC <= 4;
   __shared__ float red[WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t chunks = p.N >> 3;
@@ -186,18 +193,28 @@ __global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs
   const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
   const __nv_bfloat16* gam = reinterpret_cast<const __nv_bfloat16*>(p.gamma);
-  for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
+  uint4 xv[MAXC], rv[MAXC];
+  auto load_row = [&](int64_t r, uint4* xo, uint4* ro) {
     const RowSrc rs = row_src<MAP>(p, r);
     const __nv_bfloat16* rrow = reinterpret_cast<const __nv_bfloat16*>(p.residual) + r * p.N;
-    __nv_bfloat16* orow = out + r * p.N;
-    uint4 xv[MAXC], rv[MAXC];
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
       const int64_t c = tid + THREADS * i;
       if (c < chunks) {
-        xv[i] = ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask));
-        rv[i] = ld_stream(rrow + 8 * c);
+        xo[i] = ld_coherent(src + chunk_src<MAP>(rs, 8 * c, lbn, bn_mask));
+        ro[i] = ld_stream(rrow + 8 * c);
       }
+    }
+  };
+  if (PF && blockIdx.x < p.rows) load_row(blockIdx.x, xv, rv);
+  for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const __nv_bfloat16* rrow = reinterpret_cast<const __nv_bfloat16*>(p.residual) + r * p.N;
+    __nv_bfloat16* orow = out + r * p.N;
+    uint4 xn[MAXC], rn[MAXC];
+    if (PF) {
+      if (r + gridDim.x < p.rows) load_row(r + gridDim.x, xn, rn);
+    } else {
+      load_row(r, xv, rv);
     }
     // y = x + residual is recomputed from the packed inputs in the second
     // phase (identical fp32 ops) instead of being held: fewer registers, more
@@ -240,6 +257,13 @@ __global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs
 #pragma unroll
         for (int k = 0; k < 8; ++k) x[k] = x[k] * rstd * g[k];
         st_stream(orow + 8 * c, pack8(x));
+      }
+    }
+    if (PF) {
+#pragma unroll
+      for (int i = 0; i < MAXC; ++i) {
+        xv[i] = xn[i];
+        rv[i] = rn[i];
       }
     }
   }
@@ -376,8 +400,8 @@ cudaError_t launch_rmsnorm(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 16);
   if (chunks <= 128) fo_post_rmsnorm_kernel<MAP, 1, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
   else if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 2, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-  else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 4, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-  else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 8, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 2, 256, RES><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 4, 256, RES><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
   else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8, 256, RES><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
   else {
     const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)num_sms() * 8);
