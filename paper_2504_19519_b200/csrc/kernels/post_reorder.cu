@@ -171,10 +171,11 @@ __global__ void __launch_bounds__(256) fo_post_reorder_kernel(const PostArgs p, 
 // Residual add + RMSNorm: one THREADS-thread block per row, the whole row held
 // in registers (MAXC chunks of 8 per thread, N <= 8*THREADS*MAXC), single pass
 // over HBM: read x (through the map) and residual once, write out once.
-// Rows of 2048..8192 columns use 256-thread blocks with 2..4 chunks per
-// thread and prefetch the block's next row (PF below): measured 2-4% faster
-// than 128 x 4 without the prefetch (profiles/r01_post_reorder_probe.txt);
-// a cluster of blocks per row with a DSMEM reduction was slower still.
+// Rows of up to 8192 columns (<= 4 chunks per thread) prefetch the block's
+// next row (PF below) on a grid of resident blocks that loop over rows:
+// 9-16% faster than a block per row without the prefetch
+// (profiles/r01_post_reorder_probe.txt); a cluster of blocks per row with a
+// DSMEM reduction was slower.
 // RES: also write y = x + residual (bf16) back into the residual buffer (the
 // residual stream of a pre-norm block); each row's residual is read before
 // its own write, by the same thread, so in place is safe.
@@ -394,14 +395,45 @@ int num_sms() {
   return n;
 }
 
+// Grid of the prefetching row kernel: the blocks that are resident at once
+// (occupancy per SM x SMs, cached per instantiation and device), so every
+// block loops over several rows and its next-row prefetch overlaps the
+// current row instead of the block retiring after one row.
+template <int MAP, int MAXC, int THREADS, bool RES>
+int resident_grid(int smem) {
+  static int cache[64][2];  // [device][smem != 0] -> blocks per SM
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& v = cache[dev & 63][smem != 0];
+  if (!v) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fo_post_rmsnorm_kernel<MAP, MAXC, THREADS, RES>, THREADS,
+                                                      smem) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = 1;
+    }
+    v = n;
+  }
+  return v * num_sms();
+}
+
 template <int MAP, bool RES>
 cudaError_t launch_rmsnorm(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int64_t chunks = a.N / 8;
   const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 16);
-  if (chunks <= 128) fo_post_rmsnorm_kernel<MAP, 1, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-  else if (chunks <= 256) fo_post_rmsnorm_kernel<MAP, 2, 128, RES><<<grid, 128, a.smem_pad, stream>>>(a, lbn);
-  else if (chunks <= 512) fo_post_rmsnorm_kernel<MAP, 2, 256, RES><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
-  else if (chunks <= 1024) fo_post_rmsnorm_kernel<MAP, 4, 256, RES><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
+  auto pgrid = [&](int resident) { return (int)std::min<int64_t>(a.rows, resident); };
+  if (chunks <= 128)
+    fo_post_rmsnorm_kernel<MAP, 1, 128, RES>
+        <<<pgrid(resident_grid<MAP, 1, 128, RES>(a.smem_pad)), 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 256)
+    fo_post_rmsnorm_kernel<MAP, 2, 128, RES>
+        <<<pgrid(resident_grid<MAP, 2, 128, RES>(a.smem_pad)), 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 512)
+    fo_post_rmsnorm_kernel<MAP, 2, 256, RES>
+        <<<pgrid(resident_grid<MAP, 2, 256, RES>(a.smem_pad)), 256, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 1024)
+    fo_post_rmsnorm_kernel<MAP, 4, 256, RES>
+        <<<pgrid(resident_grid<MAP, 4, 256, RES>(a.smem_pad)), 256, a.smem_pad, stream>>>(a, lbn);
   else if (chunks <= 2048) fo_post_rmsnorm_kernel<MAP, 8, 256, RES><<<grid, 256, a.smem_pad, stream>>>(a, lbn);
   else {
     const int g2 = (int)std::min<int64_t>((a.rows + 7) / 8, (int64_t)num_sms() * 8);
