@@ -208,6 +208,14 @@ def test_c2_bench_config_tp1_tail_split():
     tail_tiles = order[3 * 74:]
     trows = np.unique((tail_tiles // 16) * 256 + 17)
     _check_rows(out[torch.from_numpy(trows).cuda()], onum.gemm(A[trows], Bt))
+    # 34 tail tiles in f = 2 slices: the distributed fold (default) adds the
+    # same two fp32 terms per element as the owner-only fold (a + b == b + a)
+    alt = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=74, group_waves=[1, 2, 1],
+                  swizzle=0, options={"tail_split": -1, "dist_fold": 0})
+    out2 = torch.empty_like(out)
+    fo.run(ctx, alt, A.cuda(), Bt.cuda(), out2)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
     ctx.close()
 
 
