@@ -377,7 +377,10 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      and stored by slice c % f, each slice publishing the fp32
  *                      partials of the chunks it does not own; 0 — the slice
  *                      starting at k-block 0 folds every chunk (the SwiGLU
- *                      epilogue and the stream-K tail always fold this way) */
+ *                      epilogue and the stream-K tail always fold this way).
+ *                      Slices wait on each other, which is safe because every
+ *                      slice is its worker's last unit and all workers are
+ *                      co-resident (workers x CTAs <= SMs is enforced) */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
                FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8,
