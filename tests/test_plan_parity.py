@@ -285,3 +285,22 @@ def test_ctx_from_comm_rejects_null():
     from paper_2504_19519_b200._lib import FOError
     with pytest.raises(FOError, match="null"):
         fo.Context.from_comm(0, 0)
+
+
+def test_binding_enums_match_header():
+    """The binding's name -> value tables equal the header's enums (ABI drift check)."""
+    from paper_2504_19519_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "flashoverlap.h")).read()
+
+    def enum(name):
+        body = re.search(r"typedef enum \{([^}]*)\}\s*" + name + ";", hdr, re.S).group(1)
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        return {k: int(v) for k, v in re.findall(r"(FO_\w+)\s*=\s*(\d+)", body)}
+
+    opts = enum("fo_option")
+    assert {"FO_OPT_" + k.upper(): v for k, v in _lib.OPTION.items()} == opts
+    assert {"FO_" + k.upper(): v for k, v in _lib.COLL.items()} == enum("fo_coll")
+    assert {"FO_LAYOUT_" + k.upper(): v for k, v in _lib.LAYOUT.items()} == enum("fo_ar_layout")
+    post = {"none": "FO_POST_NONE", "add": "FO_POST_ADD", "add_rmsnorm": "FO_POST_ADD_RMSNORM",
+            "add_rmsnorm_res": "FO_POST_ADD_RMSNORM_RESIDUAL"}
+    assert {post[k]: v for k, v in _lib.POST.items()} == enum("fo_post")
