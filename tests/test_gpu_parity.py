@@ -683,14 +683,18 @@ def test_moe_combine_full_path_world1(ctx1):
         fo.run_combine(ctx1, bad, _dev_bf16(A), _dev_bf16(Bt), out, torch.from_numpy(perm).cuda(), w)
 
 
-@pytest.mark.parametrize("coll,layout,groups", [("allreduce", "rowband", [1, 2, 1]), ("allreduce", "slot", [2, 2]),
-                                                ("reducescatter", "auto", [1, 3])])
-def test_add_rmsnorm_residual_in_place(ctx1, coll, layout, groups):
+@pytest.mark.parametrize("coll,layout,groups,N", [("allreduce", "rowband", [1, 2, 1], 1024),
+                                                  ("allreduce", "slot", [2, 2], 1024),
+                                                  ("reducescatter", "auto", [1, 3], 1024),
+                                                  # 4096 columns: resident row-looping grid with next-row prefetch
+                                                  ("allreduce", "rowband", [4, 8, 4], 4096),
+                                                  ("allreduce", "slot", [8, 8], 4096)])
+def test_add_rmsnorm_residual_in_place(ctx1, coll, layout, groups, N):
     """FO_POST_ADD_RMSNORM_RESIDUAL (the residual stream of a pre-norm block,
     NEXT f4): out equals the ADD_RMSNORM output bit for bit, and the residual
     buffer is overwritten with bf16(x + residual) — bit-exact vs the oracle in
     the exact-integer regime (per row band for ROWBAND, once at the end else)."""
-    M, N, K, S = 2048, 1024, 512, 8
+    M, K, S = 2048, 512, 8
     A, Bt = synthetic.exact_inputs(M, N, K, seed=91, nnz_per_row=200)
     rows = M
     kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1, group_waves=groups,
