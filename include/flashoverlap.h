@@ -155,6 +155,53 @@ fo_status fo_plan_export_send_map(fo_plan plan, int64_t* send_map);
 fo_status fo_plan_export_recv_map(fo_plan plan, int64_t* recv_map);
 fo_status fo_plan_export_a2a_counts(fo_plan plan, int64_t* a2a_send_cnt, int64_t* a2a_recv_cnt);
 
+/* ---------------------------------------------------------------- communication schedule
+ * The exact list of communication calls a plan issues ("Once the
+ * j-th number reaches |G_j|, the communication of G_j starts"
+ * NCCL AllReduce / ReduceScatter / send-recv All-to-All; PAPER.md:381-392 the
+ * contiguous per-group ranges).  fo_run and fo_run_sequential execute THESE
+ * calls, in this order, on the communicator (no other communication call is
+ * made on the data path), so a host-only test can check every offset, count
+ * and peer against the oracle, and that all ranks' schedules match, without a
+ * GPU.  Buffers are named, offsets and counts are in bf16 ELEMENTS:
+ *   FO_BUF_SEND    the plan's library-owned pre-reordered send buffer
+ *                  (info.send_elems)
+ *   FO_BUF_RECV    the plan's library-owned receive buffer (info.recv_elems;
+ *                  at world 1 it is the send buffer itself)
+ *   FO_BUF_OUT     the caller's `out` of fo_run / fo_run_sequential
+ *   FO_BUF_SCRATCH the sequential baseline's row-major C [m, n] (RS / A2A)
+ * Call semantics (NCCL's, bf16, sum):
+ *   ALLREDUCE      in place: buf src_buf, elements [src_off, src_off+count)
+ *   REDUCESCATTER  send src_buf[src_off, src_off + world*count), receive
+ *                  dst_buf[dst_off, dst_off + count)  (count = NCCL recvcount)
+ *   SEND / RECV    point-to-point with `peer`, count elements from src_buf at
+ *                  src_off (SEND) / into dst_buf at dst_off (RECV); only inside
+ *                  a GROUP_START ... GROUP_END bracket; sends and receives of
+ *                  one (source, destination) pair match in order
+ *   LOCAL_COPY     count elements src_buf[src_off..] -> dst_buf[dst_off..] on
+ *                  this rank (the All-to-All self part; skipped when source and
+ *                  destination coincide)
+ * `group` is the wave group the call belongs to (-1 for the sequential
+ * schedule).  schedule 0 = fo_run, 1 = fo_run_sequential.  capacity = entries
+ * `calls` can hold; *ncalls receives the schedule length (calls may be NULL to
+ * query it; FO_ERR_INVALID_ARG if capacity is too small).  Host only. */
+typedef enum { FO_CALL_ALLREDUCE = 0, FO_CALL_REDUCESCATTER = 1, FO_CALL_SEND = 2, FO_CALL_RECV = 3,
+               FO_CALL_LOCAL_COPY = 4, FO_CALL_GROUP_START = 5, FO_CALL_GROUP_END = 6 } fo_call_kind;
+typedef enum { FO_BUF_NONE = -1, FO_BUF_SEND = 0, FO_BUF_RECV = 1, FO_BUF_OUT = 2, FO_BUF_SCRATCH = 3 } fo_buf;
+typedef struct {
+  int32_t kind;      /* fo_call_kind */
+  int32_t group;     /* wave group j, -1 in the sequential schedule */
+  int32_t peer;      /* SEND / RECV: the other rank; else -1 */
+  int32_t src_buf;   /* fo_buf */
+  int32_t dst_buf;   /* fo_buf */
+  int32_t reserved;
+  int64_t src_off;   /* elements */
+  int64_t dst_off;   /* elements */
+  int64_t count;     /* elements (NCCL's count argument) */
+} fo_comm_call;
+fo_status fo_plan_export_calls(fo_plan plan, int32_t schedule, fo_comm_call* calls, int32_t capacity,
+                               int32_t* ncalls);
+
 /* ---------------------------------------------------------------- context (one per process / GPU) */
 /* NCCL unique id (128 bytes) made on one rank and broadcast by the caller. */
 fo_status fo_get_unique_id(uint8_t uid[128]);
@@ -241,8 +288,16 @@ fo_status fo_run(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* 
 fo_status fo_run_host(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
                       const void* residual, const void* gamma, void* stream);
 /* Non-overlapped baseline: the SAME GEMM kernel writing row-major C, then ONE
- * full-size NCCL call (AR in place; RS standard contiguous rows; A2A with
- * row_dst sorted ascending), then the fused elementwise op as its own pass. */
+ * full-size NCCL call, then the fused elementwise op as its own pass:
+ *   AR  -> ncclAllReduce in place on out [m, n] (same result as fo_run);
+ *   RS  -> ncclReduceScatter of row-major C: out [m/world, n] holds the
+ *          CONTIGUOUS global rows [rank*m/world, (rank+1)*m/world) (NCCL's
+ *          standard layout; fo_run's block-cyclic R_k is the paper's,
+ *          both are valid ReduceScatters of the same sum);
+ *   A2A -> one grouped send/recv: every maximal run of consecutive rows with
+ *          the same destination is one message (one per peer when row_dst is
+ *          sorted, the usual MoE layout); out as fo_run's.
+ * The calls are fo_plan_export_calls(plan, 1, ...). */
 fo_status fo_run_sequential(fo_ctx ctx, fo_plan plan, const void* A, const void* Bt, void* out,
                             const void* residual, const void* gamma, void* stream);
 

@@ -138,6 +138,19 @@ class Plan:
                                                r.ctypes.data_as(C.POINTER(C.c_int64))))
         return s.reshape(-1, self.world), r.reshape(-1, self.world)
 
+    def export_calls(self, schedule: int = 0) -> list:
+        """The communication calls fo_run (schedule 0) / fo_run_sequential (1)
+        issue, in order (fo_plan_export_calls): dicts with kind, group, peer,
+        src_buf, dst_buf, src_off, dst_off, count (elements)."""
+        lib = load()
+        n = C.c_int32()
+        check(lib.fo_plan_export_calls(self._h, int(schedule), None, 0, C.byref(n)))
+        arr = (_lib.CommCallC * max(1, n.value))()
+        check(lib.fo_plan_export_calls(self._h, int(schedule), arr, n.value, C.byref(n)))
+        return [dict(kind=_lib.CALL_KINDS[c.kind], group=c.group, peer=c.peer, src_buf=_lib.BUFS[c.src_buf],
+                     dst_buf=_lib.BUFS[c.dst_buf], src_off=c.src_off, dst_off=c.dst_off, count=c.count)
+                for c in arr[:n.value]]
+
     def read_counters(self) -> np.ndarray:
         c = np.empty(self.info["num_groups"], np.uint32)
         check(load().fo_plan_read_counters(self._h, c.ctypes.data_as(C.POINTER(C.c_uint32))))

@@ -55,6 +55,15 @@ class PlanInfoC(C.Structure):
     ]
 
 
+class CommCallC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("group", C.c_int32), ("peer", C.c_int32), ("src_buf", C.c_int32),
+                ("dst_buf", C.c_int32), ("reserved", C.c_int32), ("src_off", C.c_int64), ("dst_off", C.c_int64),
+                ("count", C.c_int64)]
+
+
+CALL_KINDS = ["allreduce", "reducescatter", "send", "recv", "local_copy", "group_start", "group_end"]
+BUFS = {-1: None, 0: "send", 1: "recv", 2: "out", 3: "scratch"}
+
 # (name, restype, argtypes) for every symbol include/flashoverlap.h declares
 _P = C.c_void_p
 _SIGS = [
@@ -71,6 +80,7 @@ _SIGS = [
     ("fo_plan_export_send_map", C.c_int, [_P, C.POINTER(C.c_int64)]),
     ("fo_plan_export_recv_map", C.c_int, [_P, C.POINTER(C.c_int64)]),
     ("fo_plan_export_a2a_counts", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("fo_plan_export_calls", C.c_int, [_P, C.c_int32, C.POINTER(CommCallC), C.c_int32, C.POINTER(C.c_int32)]),
     ("fo_get_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
     ("fo_ctx_create", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32,
                                 C.POINTER(_P)]),

@@ -120,4 +120,17 @@ fo_status fo_plan_export_a2a_counts(fo_plan plan, int64_t* send_cnt, int64_t* re
   });
 }
 
+fo_status fo_plan_export_calls(fo_plan plan, int32_t schedule, fo_comm_call* calls, int32_t capacity,
+                               int32_t* ncalls) {
+  return guard([&] {
+    if (!plan || !ncalls) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (schedule != 0 && schedule != 1) fail(FO_ERR_INVALID_ARG, "schedule must be 0 (fo_run) or 1 (sequential)");
+    const std::vector<fo_comm_call>& v = schedule == 0 ? plan->host.calls : plan->host.seq_calls;
+    *ncalls = (int32_t)v.size();
+    if (!calls) return;
+    if (capacity < (int32_t)v.size()) fail(FO_ERR_INVALID_ARG, "capacity %d < %zu calls", capacity, v.size());
+    if (!v.empty()) std::memcpy(calls, v.data(), sizeof(fo_comm_call) * v.size());
+  });
+}
+
 }  // extern "C"

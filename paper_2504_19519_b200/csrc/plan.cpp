@@ -321,7 +321,139 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
     }
   }
   if (p.coll != FO_ALLREDUCE) p.layout = (p.coll == FO_NOCOMM) ? FO_LAYOUT_ROWBAND : FO_LAYOUT_SLOT;
+  build_schedules(p, d, peers);
   return p;
+}
+
+static fo_comm_call make_call(int kind, int group, int peer, int sbuf, int dbuf, int64_t soff, int64_t doff,
+                              int64_t count) {
+  fo_comm_call c{};
+  c.kind = kind;
+  c.group = group;
+  c.peer = peer;
+  c.src_buf = sbuf;
+  c.dst_buf = dbuf;
+  c.src_off = soff;
+  c.dst_off = doff;
+  c.count = count;
+  return c;
+}
+
+// Maximal runs [r0, r1) of consecutive rows of `row_dst[0..m)` with destination `dst`.
+static std::vector<std::pair<int64_t, int64_t>> dst_runs(const int32_t* row_dst, int64_t m, int dst) {
+  std::vector<std::pair<int64_t, int64_t>> runs;
+  for (int64_t r = 0; r < m;) {
+    if (row_dst[r] != dst) {
+      ++r;
+      continue;
+    }
+    int64_t e = r;
+    while (e < m && row_dst[e] == dst) ++e;
+    runs.emplace_back(r, e);
+    r = e;
+  }
+  return runs;
+}
+
+void build_schedules(PlanHost& p, const fo_plan_desc& d, const fo_plan_desc* const* peers) {
+  p.calls.clear();
+  p.seq_calls.clear();
+  p.call_begin.assign(p.P + 1, 0);
+  const int W = p.world;
+  // ---- overlapped (fo_run): one call set per wave group, on the group's
+  // contiguous range
+  for (int j = 0; j < p.P; ++j) {
+    p.call_begin[j] = (int32_t)p.calls.size();
+    switch (p.coll) {
+      case FO_ALLREDUCE: {
+        // in place: ROWBAND reduces the group's row band of the caller's C,
+        // SLOT the group's slots of the send buffer
+        const int buf = (p.layout == FO_LAYOUT_ROWBAND) ? FO_BUF_OUT : FO_BUF_SEND;
+        const int64_t b = p.group_elem_begin(j), e = p.group_elem_end(j);
+        p.calls.push_back(make_call(FO_CALL_ALLREDUCE, j, -1, buf, buf, b, b, e - b));
+        break;
+      }
+      case FO_REDUCESCATTER: {
+        // chunk k of the group's range goes to rank k; rank k's chunks are
+        // stored in group order (receive layout [group][q][a'][BN])
+        const int64_t b = p.group_elem_begin(j), e = p.group_elem_end(j);
+        p.calls.push_back(make_call(FO_CALL_REDUCESCATTER, j, -1, FO_BUF_SEND, FO_BUF_RECV, b, b / W, (e - b) / W));
+        break;
+      }
+      case FO_ALLTOALL: {
+        // the self part is a local copy; every peer's part of pool d in one
+        // grouped send/recv
+        const int64_t cs = p.send_cnt[(size_t)j * W + p.rank];
+        if (cs)
+          p.calls.push_back(make_call(FO_CALL_LOCAL_COPY, j, p.rank, FO_BUF_SEND, FO_BUF_RECV,
+                                      (p.pool_base[p.rank] + p.send_start[(size_t)j * W + p.rank]) * p.BN,
+                                      p.recv_off[(size_t)j * W + p.rank] * p.BN, cs * p.BN));
+        p.calls.push_back(make_call(FO_CALL_GROUP_START, j, -1, FO_BUF_NONE, FO_BUF_NONE, 0, 0, 0));
+        for (int dd = 0; dd < W; ++dd) {
+          if (dd == p.rank) continue;
+          const int64_t sc = p.send_cnt[(size_t)j * W + dd];
+          if (sc)
+            p.calls.push_back(make_call(FO_CALL_SEND, j, dd, FO_BUF_SEND, FO_BUF_NONE,
+                                        (p.pool_base[dd] + p.send_start[(size_t)j * W + dd]) * p.BN, 0, sc * p.BN));
+          const int64_t rc = p.recv_cnt[(size_t)j * W + dd];
+          if (rc)
+            p.calls.push_back(make_call(FO_CALL_RECV, j, dd, FO_BUF_NONE, FO_BUF_RECV, 0,
+                                        p.recv_off[(size_t)j * W + dd] * p.BN, rc * p.BN));
+        }
+        p.calls.push_back(make_call(FO_CALL_GROUP_END, j, -1, FO_BUF_NONE, FO_BUF_NONE, 0, 0, 0));
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  p.call_begin[p.P] = (int32_t)p.calls.size();
+  // ---- sequential baseline (fo_run_sequential): one full-size call
+  const int64_t MN = p.M * p.N;
+  switch (p.coll) {
+    case FO_ALLREDUCE:
+      p.seq_calls.push_back(make_call(FO_CALL_ALLREDUCE, -1, -1, FO_BUF_OUT, FO_BUF_OUT, 0, 0, MN));
+      break;
+    case FO_REDUCESCATTER:
+      p.seq_calls.push_back(make_call(FO_CALL_REDUCESCATTER, -1, -1, FO_BUF_SCRATCH, FO_BUF_OUT, 0, 0, MN / W));
+      break;
+    case FO_ALLTOALL: {
+      // rows of row-major C in runs of one destination; a source's rows land
+      // at out rows src_base[s] + (their rank among its rows routed here)
+      auto desc = [&](int s) { return s == p.rank ? &d : peers[s]; };
+      std::vector<std::vector<fo_comm_call>> sends(W), recvs(W);
+      for (int dd = 0; dd < W; ++dd)
+        for (auto& rr : dst_runs(d.row_dst, d.m, dd))
+          sends[dd].push_back(make_call(FO_CALL_SEND, -1, dd, FO_BUF_SCRATCH, FO_BUF_NONE, rr.first * p.N, 0,
+                                        (rr.second - rr.first) * p.N));
+      for (int s = 0; s < W; ++s) {
+        int64_t o = p.src_base[s];
+        for (auto& rr : dst_runs(desc(s)->row_dst, desc(s)->m, p.rank)) {
+          recvs[s].push_back(make_call(FO_CALL_RECV, -1, s, FO_BUF_NONE, FO_BUF_OUT, 0, o * p.N,
+                                       (rr.second - rr.first) * p.N));
+          o += rr.second - rr.first;
+        }
+      }
+      // self part: local copies run by run
+      for (size_t i = 0; i < sends[p.rank].size(); ++i) {
+        fo_comm_call c = sends[p.rank][i];
+        c.kind = FO_CALL_LOCAL_COPY;
+        c.dst_buf = FO_BUF_OUT;
+        c.dst_off = recvs[p.rank][i].dst_off;
+        p.seq_calls.push_back(c);
+      }
+      p.seq_calls.push_back(make_call(FO_CALL_GROUP_START, -1, -1, FO_BUF_NONE, FO_BUF_NONE, 0, 0, 0));
+      for (int dd = 0; dd < W; ++dd) {
+        if (dd == p.rank) continue;
+        for (auto& c : sends[dd]) p.seq_calls.push_back(c);
+        for (auto& c : recvs[dd]) p.seq_calls.push_back(c);
+      }
+      p.seq_calls.push_back(make_call(FO_CALL_GROUP_END, -1, -1, FO_BUF_NONE, FO_BUF_NONE, 0, 0, 0));
+      break;
+    }
+    default:
+      break;
+  }
 }
 
 int64_t PlanHost::send_index(int64_t r, int64_t c) const {

@@ -51,6 +51,12 @@ struct PlanHost {
 
   std::vector<int64_t> band_rows;       // AR ROWBAND: [2P] tile-row band (r0, r1) of each group
 
+  // ---- communication schedules (fo_plan_export_calls): what fo_run /
+  // fo_run_sequential issue on the communicator, in order
+  std::vector<fo_comm_call> calls;      // overlapped, grouped by wave group
+  std::vector<int32_t> call_begin;      // [P+1] calls of group j = [call_begin[j], call_begin[j+1])
+  std::vector<fo_comm_call> seq_calls;  // sequential baseline
+
   // Group j's element range in the AR/RS send buffer (AR ROWBAND: its row band of C).
   int64_t group_elem_begin(int j) const {
     if (coll == FO_ALLREDUCE && layout == FO_LAYOUT_ROWBAND) return band_rows[2 * j] * BM * N;
@@ -76,5 +82,9 @@ int auto_swizzle(int Mt, int Nt, int S);
 // workers must be given explicitly).
 PlanHost build_plan(const fo_plan_desc& self, int rank, int world,
                     const fo_plan_desc* const* peers, int sm_count);
+
+// The overlapped and sequential communication schedules of a built plan
+// (peers: the A2A census descriptors, as for build_plan).
+void build_schedules(PlanHost& p, const fo_plan_desc& self, const fo_plan_desc* const* peers);
 
 }  // namespace fo

@@ -27,15 +27,15 @@
 #include <mutex>
 #include <vector>
 
+#include "comm.h"
 #include "kernels.h"
 #include "runtime.h"
 
 struct fo_ctx_s {
   int device = 0;
   bool aborted = false;                // the watchdog (fo_plan_sync) aborted the communicator
-  bool owns_comm = true;               // false: borrowed (fo_ctx_create_from_comm), never destroyed/aborted here
   int rank = 0, world = 1;
-  ncclComm_t comm = nullptr;
+  fo::Comm* comm = nullptr;            // NCCL (owned or borrowed) or the test loopback
   cudaStream_t comm_stream = nullptr;
   cudaStream_t post_stream = nullptr;  // per-group post-reorder, chained to each group's collective
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_post_join = nullptr;
@@ -88,6 +88,44 @@ static WaitValue32Fn wait_value_fn() {
   });
   return fn;
 }
+
+// ---- NCCL backend of fo::Comm (comm.h)
+struct NcclComm final : Comm {
+  ncclComm_t c;
+  int r, w;
+  bool owns;
+  NcclComm(ncclComm_t c_, int r_, int w_, bool o) : c(c_), r(r_), w(w_), owns(o) {}
+  ~NcclComm() override {
+    if (c && owns) ncclCommDestroy(c);
+  }
+  int rank() const override { return r; }
+  int world() const override { return w; }
+  ncclComm_t nccl() const override { return c; }
+  void allreduce(const void* send, void* recv, size_t count, cudaStream_t s) override {
+    FO_NCCL(ncclAllReduce(send, recv, count, ncclBfloat16, ncclSum, c, s));
+  }
+  void reducescatter(const void* send, void* recv, size_t recvcount, cudaStream_t s) override {
+    FO_NCCL(ncclReduceScatter(send, recv, recvcount, ncclBfloat16, ncclSum, c, s));
+  }
+  void allgather(const void* send, void* recv, size_t sendcount, cudaStream_t s) override {
+    FO_NCCL(ncclAllGather(send, recv, sendcount, ncclBfloat16, c, s));
+  }
+  void group_start() override { FO_NCCL(ncclGroupStart()); }
+  void group_end() override { FO_NCCL(ncclGroupEnd()); }
+  void send(const void* buf, size_t count, int peer, cudaStream_t s) override {
+    FO_NCCL(ncclSend(buf, count, ncclBfloat16, peer, c, s));
+  }
+  void recv(void* buf, size_t count, int peer, cudaStream_t s) override {
+    FO_NCCL(ncclRecv(buf, count, ncclBfloat16, peer, c, s));
+  }
+  void abort() override {
+    // a borrowed communicator is its owner's to abort; drop it either way
+    if (c && owns) ncclCommAbort(c);
+    c = nullptr;
+  }
+};
+
+Comm* make_nccl_comm(ncclComm_t comm, int rank, int world, bool owns) { return new NcclComm(comm, rank, world, owns); }
 
 template <class T>
 static T* upload(const std::vector<T>& v) {
@@ -373,8 +411,6 @@ static int post_map(const PlanHost& h) {
 // CTA pair, so group j completes at |G_j| * tile_m/128 signals.
 static cuuint32_t signal_target(const PlanHost& h, int j) { return (cuuint32_t)(h.group_tiles(j) * (h.BM / 128)); }
 
-static ncclDataType_t bf16() { return ncclBfloat16; }
-
 // Trigger: block the comm stream until group j's counter
 // reaches its target — a front-end stream wait (no SM) or the paper's
 // signaling kernel (a 1-warp spin on an acquire load).
@@ -467,57 +503,54 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
   FO_CUDA(launch_group_post(a, s));
 }
 
-// The collective of group j, on the comm stream ("Once the j-th
-// number reaches |G_j|, the communication of G_j starts").
-static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* ar_base, cudaStream_t cs) {
-  const PlanHost& h = p->host;
-  char* send = reinterpret_cast<char*>(p->d_send);
-  char* recv = reinterpret_cast<char*>(p->d_recv);
-  switch (h.coll) {
-    case FO_ALLREDUCE: {
-      char* base = reinterpret_cast<char*>(ar_base) + 2 * h.group_elem_begin(j);
-      const size_t count = (size_t)(h.group_elem_end(j) - h.group_elem_begin(j));
-      FO_NCCL(ncclAllReduce(base, base, count, bf16(), ncclSum, c->comm, cs));
-      break;
-    }
-    case FO_REDUCESCATTER: {
-      const int64_t b = h.group_elem_begin(j), e = h.group_elem_end(j);
-      FO_NCCL(ncclReduceScatter(send + 2 * b, recv + 2 * (b / h.world), (size_t)((e - b) / h.world), bf16(),
-                                ncclSum, c->comm, cs));
-      break;
-    }
-    case FO_ALLTOALL: {
-      const int W = h.world;
-      // self part: a device copy (no NCCL needed)
-      {
-        const int64_t cnt = h.send_cnt[(size_t)j * W + h.rank];
-        if (cnt) {
-          const int64_t so = (h.pool_base[h.rank] + h.send_start[(size_t)j * W + h.rank]) * h.BN;
-          const int64_t ro = h.recv_off[(size_t)j * W + h.rank] * h.BN;
-          if (recv + 2 * ro != send + 2 * so)
-            FO_CUDA(cudaMemcpyAsync(recv + 2 * ro, send + 2 * so, 2 * cnt * h.BN, cudaMemcpyDeviceToDevice, cs));
-        }
+// Execute calls [b, e) of a schedule (PlanHost::calls / seq_calls, the
+// fo_plan_export_calls contract) on stream `cs`.  bufs: FO_BUF_SEND, _RECV,
+// _OUT, _SCRATCH base pointers.
+static void exec_calls(fo_ctx_s* c, const std::vector<fo_comm_call>& calls, size_t b, size_t e, void* const bufs[4],
+                       cudaStream_t cs) {
+  auto at = [&](int buf, int64_t off) -> char* {
+    if (buf < 0 || buf > 3 || !bufs[buf]) fail(FO_ERR_STATE, "schedule names buffer %d, which this run does not have", buf);
+    return reinterpret_cast<char*>(bufs[buf]) + 2 * off;
+  };
+  for (size_t i = b; i < e; ++i) {
+    const fo_comm_call& k = calls[i];
+    switch (k.kind) {
+      case FO_CALL_ALLREDUCE:
+        c->comm->allreduce(at(k.src_buf, k.src_off), at(k.dst_buf, k.dst_off), (size_t)k.count, cs);
+        break;
+      case FO_CALL_REDUCESCATTER:
+        c->comm->reducescatter(at(k.src_buf, k.src_off), at(k.dst_buf, k.dst_off), (size_t)k.count, cs);
+        break;
+      case FO_CALL_SEND:
+        c->comm->send(at(k.src_buf, k.src_off), (size_t)k.count, k.peer, cs);
+        break;
+      case FO_CALL_RECV:
+        c->comm->recv(at(k.dst_buf, k.dst_off), (size_t)k.count, k.peer, cs);
+        break;
+      case FO_CALL_LOCAL_COPY: {
+        char* src = at(k.src_buf, k.src_off);
+        char* dst = at(k.dst_buf, k.dst_off);
+        if (src != dst) FO_CUDA(cudaMemcpyAsync(dst, src, 2 * (size_t)k.count, cudaMemcpyDeviceToDevice, cs));
+        break;
       }
-      FO_NCCL(ncclGroupStart());
-      for (int d = 0; d < W; ++d) {
-        if (d == h.rank) continue;
-        const int64_t sc = h.send_cnt[(size_t)j * W + d];
-        if (sc) {
-          const int64_t so = (h.pool_base[d] + h.send_start[(size_t)j * W + d]) * h.BN;
-          FO_NCCL(ncclSend(send + 2 * so, (size_t)(sc * h.BN), bf16(), d, c->comm, cs));
-        }
-        const int64_t rc = h.recv_cnt[(size_t)j * W + d];
-        if (rc) {
-          const int64_t ro = h.recv_off[(size_t)j * W + d] * h.BN;
-          FO_NCCL(ncclRecv(recv + 2 * ro, (size_t)(rc * h.BN), bf16(), d, c->comm, cs));
-        }
-      }
-      FO_NCCL(ncclGroupEnd());
-      break;
+      case FO_CALL_GROUP_START:
+        c->comm->group_start();
+        break;
+      case FO_CALL_GROUP_END:
+        c->comm->group_end();
+        break;
+      default:
+        fail(FO_ERR_STATE, "unknown schedule call kind %d", k.kind);
     }
-    default:
-      break;
   }
+}
+
+// The collective of group j ("Once the j-th number reaches
+// |G_j|, the communication of G_j starts"): the plan's calls of group j.
+static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* out, cudaStream_t cs) {
+  const PlanHost& h = p->host;
+  void* const bufs[4] = {p->d_send, p->d_recv, out, nullptr};
+  exec_calls(c, h.calls, (size_t)h.call_begin[j], (size_t)h.call_begin[j + 1], bufs, cs);
 }
 
 }  // namespace fo
@@ -583,10 +616,12 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
         cfg.maxCTAs = nccl_max_ctas;
         cfg.minCTAs = 1;
       }
-      FO_NCCL(ncclCommInitRankConfig(&c->comm, world, id, rank, &cfg));
+      ncclComm_t comm = nullptr;
+      FO_NCCL(ncclCommInitRankConfig(&comm, world, id, rank, &cfg));
+      c->comm = make_nccl_comm(comm, rank, world, true);
       init_streams(c);
     } catch (...) {
-      if (c->comm) ncclCommDestroy(c->comm);
+      delete c->comm;
       delete c;
       throw;
     }
@@ -608,11 +643,11 @@ fo_status fo_ctx_create_from_comm(int32_t device, void* nccl_comm, fo_ctx* out) 
     c->device = device;
     c->rank = rank;
     c->world = count;
-    c->comm = comm;
-    c->owns_comm = false;
+    c->comm = make_nccl_comm(comm, rank, count, false);
     try {
       init_streams(c);
     } catch (...) {
+      delete c->comm;
       delete c;
       throw;
     }
@@ -625,7 +660,8 @@ fo_status fo_ctx_destroy(fo_ctx c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
-    if (c->comm && c->owns_comm) ncclCommDestroy(c->comm);
+    delete c->comm;
+    c->comm = nullptr;
     if (c->post_stream) cudaStreamSynchronize(c->post_stream);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->post_stream) cudaStreamDestroy(c->post_stream);
@@ -730,7 +766,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
           stream_wait(p, wait, cs, j);
         }
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j, cs));
-        group_collective(c, p, j, gemm_dst, cs);
+        group_collective(c, p, j, out, cs);
         cudaStream_t ps = cs;
         if (gpost) {
           if (!on_s) {
@@ -919,45 +955,17 @@ fo_status fo_run_sequential(fo_ctx c, fo_plan p, const void* A, const void* Bt, 
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int64_t MN = h.M * h.N;
     if (p->split > 1) FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
-    switch (h.coll) {
-      case FO_NOCOMM:
-      case FO_ALLREDUCE:
-        run_gemm(p, A, Bt, out, EPI_ROWMAJOR, false, s);
-        if (h.coll == FO_ALLREDUCE) FO_NCCL(ncclAllReduce(out, out, (size_t)MN, bf16(), ncclSum, c->comm, s));
-        break;
-      case FO_REDUCESCATTER: {
-        if (!p->d_rowmajor) FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * MN));
-        run_gemm(p, A, Bt, p->d_rowmajor, EPI_ROWMAJOR, false, s);
-        FO_NCCL(ncclReduceScatter(p->d_rowmajor, out, (size_t)(MN / h.world), bf16(), ncclSum, c->comm, s));
-        break;
-      }
-      case FO_ALLTOALL: {
-        for (int64_t r = 1; r < h.M; ++r)
-          if (h.row_dst[r] < h.row_dst[r - 1]) fail(FO_ERR_UNSUPPORTED, "sequential A2A needs row_dst sorted");
-        if (!p->d_rowmajor) FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * MN));
-        run_gemm(p, A, Bt, p->d_rowmajor, EPI_ROWMAJOR, false, s);
-        char* src = reinterpret_cast<char*>(p->d_rowmajor);
-        char* dst = reinterpret_cast<char*>(out);
-        std::vector<int64_t> rows_to(h.world, 0);
-        for (int64_t r = 0; r < h.M; ++r) rows_to[h.row_dst[r]]++;
-        FO_NCCL(ncclGroupStart());
-        int64_t soff = 0;
-        for (int d = 0; d < h.world; ++d) {
-          const int64_t rc = h.src_base[d + 1] - h.src_base[d];
-          if (d == h.rank) {
-            if (rows_to[d])
-              FO_CUDA(cudaMemcpyAsync(dst + 2 * h.src_base[d] * h.N, src + 2 * soff * h.N, 2 * rows_to[d] * h.N,
-                                      cudaMemcpyDeviceToDevice, s));
-          } else {
-            if (rows_to[d]) FO_NCCL(ncclSend(src + 2 * soff * h.N, (size_t)(rows_to[d] * h.N), bf16(), d, c->comm, s));
-            if (rc) FO_NCCL(ncclRecv(dst + 2 * h.src_base[d] * h.N, (size_t)(rc * h.N), bf16(), d, c->comm, s));
-          }
-          soff += rows_to[d];
-        }
-        FO_NCCL(ncclGroupEnd());
-        break;
-      }
+    // the same GEMM writing row-major C (in place into out for AR / no-comm,
+    // into a scratch C for RS / A2A), then the plan's sequential schedule:
+    // one full-size collective (fo_plan_export_calls schedule 1)
+    void* C = out;
+    if (h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) {
+      if (!p->d_rowmajor) FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * MN));
+      C = p->d_rowmajor;
     }
+    run_gemm(p, A, Bt, C, EPI_ROWMAJOR, false, s);
+    void* const bufs[4] = {nullptr, nullptr, out, p->d_rowmajor};
+    exec_calls(c, h.seq_calls, 0, h.seq_calls.size(), bufs, s);
     if (h.post != FO_POST_NONE) run_post(p, POSTMAP_IDENTITY, out, out, residual, gamma, s);
   });
 }
@@ -1009,7 +1017,7 @@ fo_status fo_run_allgather(fo_ctx c, fo_plan p, const void* local, void* out, co
     const size_t local_elems = (size_t)(h.out_rows * h.N);
     if (!row_exchange) {
       // row order not needed downstream: gather straight into out
-      FO_NCCL(ncclAllGather(local, out, local_elems, bf16(), c->comm, s));
+      c->comm->allgather(local, out, local_elems, s);
       if (h.post != FO_POST_NONE) {
         PostArgs a{};
         a.map = POSTMAP_IDENTITY;
@@ -1031,7 +1039,7 @@ fo_status fo_run_allgather(fo_ctx c, fo_plan p, const void* local, void* out, co
       return;
     }
     if (!p->d_rowmajor) FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * (size_t)(h.M * h.N)));
-    FO_NCCL(ncclAllGather(local, p->d_rowmajor, local_elems, bf16(), c->comm, s));
+    c->comm->allgather(local, p->d_rowmajor, local_elems, s);
     run_rowexchange(p, p->d_rowmajor, out, residual, gamma, s);
   });
 }
@@ -1159,11 +1167,7 @@ fo_status fo_plan_sync(fo_ctx c, fo_plan p, void* stream, int64_t timeout_ms) {
     //    stuck after another timeout, are killed by aborting the communicator
     //    (ncclCommAbort makes in-flight NCCL kernels exit)
     const bool done = drained(std::max<int64_t>(timeout_ms, 1000));
-    if (c->comm) {
-      // a borrowed communicator is its owner's to abort; drop it either way
-      if (c->owns_comm) ncclCommAbort(c->comm);
-      c->comm = nullptr;
-    }
+    if (c->comm) c->comm->abort();
     if (!done) drained(std::max<int64_t>(timeout_ms, 1000));
     fail(FO_ERR_TIMEOUT, "plan run did not finish within %lld ms: waits released, communicator aborted",
          (long long)timeout_ms);
@@ -1206,19 +1210,19 @@ fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t 
     auto once = [&] {
       switch (coll) {
         case FO_ALLREDUCE:
-          FO_NCCL(ncclAllReduce(a, a, count, bf16(), ncclSum, c->comm, cs));
+          c->comm->allreduce(a, a, count, cs);
           break;
         case FO_REDUCESCATTER:
-          FO_NCCL(ncclReduceScatter(a, b, count / W, bf16(), ncclSum, c->comm, cs));
+          c->comm->reducescatter(a, b, count / W, cs);
           break;
         case FO_ALLTOALL: {
           const size_t per = count / W;
-          FO_NCCL(ncclGroupStart());
+          c->comm->group_start();
           for (int d = 0; d < W; ++d) {
-            FO_NCCL(ncclSend(reinterpret_cast<char*>(a) + 2 * per * d, per, bf16(), d, c->comm, cs));
-            FO_NCCL(ncclRecv(reinterpret_cast<char*>(b) + 2 * per * d, per, bf16(), d, c->comm, cs));
+            c->comm->send(reinterpret_cast<char*>(a) + 2 * per * d, per, d, cs);
+            c->comm->recv(reinterpret_cast<char*>(b) + 2 * per * d, per, d, cs);
           }
-          FO_NCCL(ncclGroupEnd());
+          c->comm->group_end();
           break;
         }
         default:

@@ -7,7 +7,9 @@ NCCL over NVLink, per-group post-reorder) and fo_run_sequential on
 exact-integer inputs, and compares both with the plain definition computed by
 this script with torch.distributed in fp32 (exact for these integers):
 AllReduce = sum_r C_r; ReduceScatter = rows R_k of the sum (block-cyclic,
-DESIGN.md R8), and its AllGather + row exchange = the AllReduce result;
+DESIGN.md R8) for fo_run and contiguous rows for fo_run_sequential (NCCL's
+standard ReduceScatter of row-major C), and the AllGather + row exchange = the
+AllReduce result;
 All-to-All = concat over sources of the rows routed here (R9).  One AllReduce
 also runs on a context built on torch's own communicator (fo_ctx_create_from_comm).  Exit status 0 = every comparison bit-exact.  Test infrastructure.
 """
@@ -72,7 +74,11 @@ def main():
         seq = torch.empty_like(out)
         fo.run_sequential(ctx, plan, A, Bt, seq)
         torch.cuda.synchronize()
-        check(f"{coll}/{layout}/{groups}/sequential", seq, want, bad)
+        # the sequential ReduceScatter is NCCL's standard one on row-major C:
+        # contiguous rows [rank*M/n, (rank+1)*M/n) (include/flashoverlap.h)
+        want_seq = want if coll == "allreduce" else \
+            full[rank * (M // world):(rank + 1) * (M // world)].to(torch.bfloat16)
+        check(f"{coll}/{layout}/{groups}/sequential", seq, want_seq, bad)
         # host buffers (chunked H2D the GEMM waits on, per-band D2H, two staging
         # sets): back-to-back calls, each must equal the device result
         outs = [torch.full((plan.info["out_rows"], N), float("nan"), dtype=torch.bfloat16).pin_memory()
@@ -133,6 +139,10 @@ def main():
         fo.run(ctx, plan, A, Bt, out)
     torch.cuda.synchronize()
     check("alltoall", out, want, bad)
+    seq = torch.full_like(out, float("nan"))
+    fo.run_sequential(ctx, plan, A, Bt, seq)     # unsorted row_dst: one message per run of a destination
+    torch.cuda.synchronize()
+    check("alltoall/sequential", seq, want, bad)
     ok = torch.tensor([0 if not bad else 1], device="cuda")
     dist.all_reduce(ok)
     ctx.close()

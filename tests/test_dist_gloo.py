@@ -1,11 +1,13 @@
 """Multi-process (gloo, world size 2 and 4, CPU) test of the n > 1 host logic.
 
 Each process builds its plan through paper_2504_19519_b200.dist (peer census
-over the process group for All-to-All), then runs the method's data movement
-with the plan's exported maps and group ranges, using gloo collectives on CPU
-tensors in place of NCCL (this is a TEST of the plan's multi-rank contract, not
-a product path), and compares every rank's output with the oracle's plain
-definition.  Bit-exact on integer data.
+over the process group for All-to-All), fills its send buffer through the
+plan's exported send map, then executes the plan's exported communication
+schedule (fo_plan_export_calls — the exact calls fo_run issues on NCCL) with
+gloo collectives and point-to-point messages on CPU tensors in place of NCCL
+(a TEST of the plan's multi-rank contract, not a product path), and compares
+every rank's output (through the exported receive map) with the oracle's plain
+definition; the sequential schedule likewise.  Bit-exact on integer data.
 """
 import os
 import socket
@@ -30,6 +32,51 @@ def _free_port():
 def _inputs(n, r, M, N, K):
     rng = np.random.default_rng(1000 + 17 * r + M)
     return rng.integers(-3, 4, size=(M, K)).astype(float), rng.integers(-3, 4, size=(N, K)).astype(float)
+
+
+def _gloo_exec(calls, bufs, rank, world):
+    """Execute a plan's exported schedule over gloo (test stand-in for NCCL):
+    AllReduce in place; ReduceScatter as an AllReduce of the send range keeping
+    this rank's chunk (gloo has no ReduceScatter); each GROUP_START..GROUP_END
+    as isend/irecv pairs matched by gloo in issue order; local copies."""
+    def view(name, off, cnt):
+        b = bufs[name]
+        assert 0 <= off and off + cnt <= b.size, (name, off, cnt, b.size)
+        return b[off:off + cnt]
+
+    i = 0
+    while i < len(calls):
+        c = calls[i]
+        if c["kind"] == "allreduce":
+            t = torch.from_numpy(view(c["src_buf"], c["src_off"], c["count"]).copy())
+            dist.all_reduce(t)
+            view(c["dst_buf"], c["dst_off"], c["count"])[:] = t.numpy()
+        elif c["kind"] == "reducescatter":
+            t = torch.from_numpy(view(c["src_buf"], c["src_off"], world * c["count"]).copy())
+            dist.all_reduce(t)
+            view(c["dst_buf"], c["dst_off"], c["count"])[:] = t.numpy()[rank * c["count"]:(rank + 1) * c["count"]]
+        elif c["kind"] == "local_copy":
+            view(c["dst_buf"], c["dst_off"], c["count"])[:] = view(c["src_buf"], c["src_off"], c["count"]).copy()
+        elif c["kind"] == "group_start":
+            reqs, landing = [], []
+            i += 1
+            while calls[i]["kind"] != "group_end":
+                c = calls[i]
+                if c["kind"] == "send":
+                    reqs.append(dist.isend(torch.from_numpy(view(c["src_buf"], c["src_off"], c["count"]).copy()),
+                                           c["peer"]))
+                else:
+                    t = torch.zeros(c["count"], dtype=torch.float64)
+                    reqs.append(dist.irecv(t, c["peer"]))
+                    landing.append((t, c))
+                i += 1
+            for q in reqs:
+                q.wait()
+            for t, c in landing:
+                view(c["dst_buf"], c["dst_off"], c["count"])[:] = t.numpy()
+        else:
+            raise AssertionError(f"unexpected call {c}")
+        i += 1
 
 
 def _worker(rank, port, coll, errq, WORLD=2):
@@ -60,47 +107,20 @@ def _worker(rank, port, coll, errq, WORLD=2):
         Y = A @ Bt.T
         send = np.zeros(plan.info["send_elems"])
         send[plan.export_send_map()] = Y.reshape(-1)
-        P = plan.info["num_groups"]
         recv = np.zeros(plan.info["recv_elems"])
+        # the plan's own communication schedule (fo_plan_export_calls, what
+        # fo_run issues on NCCL), driven through gloo's collectives and
+        # point-to-point messages
+        _gloo_exec(plan.export_calls(0), {"send": send, "recv": recv, "out": None}, rank, WORLD)
         if coll == "allreduce":
-            for j in range(P):
-                _, _, b, e = plan.group(j)
-                t = torch.from_numpy(send[b:e].copy())
-                dist.all_reduce(t)
-                recv[b:e] = t.numpy()
-        elif coll == "reducescatter":
-            for j in range(P):
-                _, _, b, e = plan.group(j)
-                t = torch.from_numpy(send[b:e].copy())
-                dist.all_reduce(t)                       # RS emulated as AR + keep my chunk
-                c = (e - b) // WORLD
-                recv[b // WORLD:b // WORLD + c] = t.numpy()[rank * c:(rank + 1) * c]
-        else:
-            sc, rc = plan.export_a2a_counts()
-            pool_base = np.concatenate([[0], np.cumsum(sc.sum(axis=0))])
-            start = np.vstack([np.zeros((1, WORLD), int), np.cumsum(sc, axis=0)[:-1]])
-            roff = np.concatenate([[0], np.cumsum(rc.reshape(-1))])[:-1].reshape(P, WORLD)
-            for j in range(P):
-                reqs = []
-                for d in range(WORLD):
-                    a = (pool_base[d] + start[j, d]) * BN
-                    if d == rank:
-                        b0 = roff[j, d] * BN
-                        recv[b0:b0 + sc[j, d] * BN] = send[a:a + sc[j, d] * BN]
-                        continue
-                    if sc[j, d]:
-                        reqs.append(dist.isend(torch.from_numpy(send[a:a + sc[j, d] * BN].copy()), d))
-                bufs = {}
-                for s in range(WORLD):
-                    if s != rank and rc[j, s]:
-                        bufs[s] = torch.zeros(int(rc[j, s]) * BN, dtype=torch.float64)
-                        reqs.append(dist.irecv(bufs[s], s))
-                for q in reqs:
-                    q.wait()
-                for s, b in bufs.items():
-                    b0 = roff[j, s] * BN
-                    recv[b0:b0 + rc[j, s] * BN] = b.numpy()
+            recv = send
         out = recv[plan.export_recv_map()].reshape(plan.info["out_rows"], N)
+        seq_out = np.full(plan.info["out_rows"] * N, np.nan)
+        seq_bufs = {"out": seq_out, "scratch": Y.reshape(-1).copy()}
+        if coll == "allreduce":
+            seq_bufs["out"] = Y.reshape(-1).copy()
+        _gloo_exec(plan.export_calls(1), seq_bufs, rank, WORLD)
+        seq_out = seq_bufs["out"].reshape(plan.info["out_rows"], N)
         As, Bts = zip(*[_inputs(WORLD, r, (Ms[r] if coll == "alltoall" else M), N, K) for r in range(WORLD)])
         if coll == "allreduce":
             want = opl.plain_allreduce(list(As), list(Bts))[rank]
@@ -109,6 +129,10 @@ def _worker(rank, port, coll, errq, WORLD=2):
         else:
             want = opl.plain_alltoall(list(As), list(Bts), rds)[rank]
         assert np.array_equal(out, want), f"rank {rank}: mismatch"
+        if coll == "reducescatter":   # the sequential RS: NCCL's contiguous rows
+            full = opl.plain_allreduce(list(As), list(Bts))[rank]
+            want = full[rank * (M // WORLD):(rank + 1) * (M // WORLD)]
+        assert np.array_equal(seq_out, want), f"rank {rank}: sequential mismatch"
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover
         import traceback
