@@ -223,6 +223,25 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
  * owner's. */
 fo_status fo_ctx_create_from_comm(int32_t device, void* nccl_comm, fo_ctx* out);
 fo_status fo_ctx_destroy(fo_ctx ctx);
+/* TEST BACKEND — W ranks of one process on ONE GPU.  A box with one GPU
+ * cannot run NCCL with two ranks, so these make the library's multi-rank data
+ * path (fo_run / fo_run_sequential / fo_run_allgather at world > 1: receive
+ * buffers, per-group calls on the comm stream, the last group on the caller
+ * stream, the plan's schedule) run for real on one device.
+ * fo_loopback_create: a group of `world` in-process ranks on `device` (host
+ * object `*group`).  fo_ctx_create_loopback: rank `rank`'s context in that
+ * group (its own comm / post streams, like fo_ctx_create); its communication
+ * calls are small kernels that meet the other ranks' calls at a device-side
+ * barrier and move the data with loads / stores (AllReduce: fp32 sum in rank
+ * order, one bf16 rounding).  The caller issues every rank's calls from its
+ * threads in any interleaving, each rank in the same order as with NCCL.
+ * A call sequence that differs between ranks (a hang with NCCL) or a barrier
+ * not reached within 20 s traps the device (the CUDA context is lost) instead
+ * of hanging.  Not CUDA-graph capturable.  fo_loopback_destroy fails with
+ * FO_ERR_STATE while contexts of the group exist.  Not for production use. */
+fo_status fo_loopback_create(int32_t device, int32_t world, void** group);
+fo_status fo_loopback_destroy(void* group);
+fo_status fo_ctx_create_loopback(void* group, int32_t rank, fo_ctx* out);
 
 /* Offline stage of the tuner ("the bandwidth curve is sampled
  * with multiple dense points"): average latency of one `coll` (AllReduce in

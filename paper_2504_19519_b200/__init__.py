@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib
 from ._lib import COLL, LAYOUT, POST, FOError, check, load
 
-__all__ = ["Plan", "Context", "run", "run_host", "run_allgather", "rowexchange_stage", "run_sequential", "gemm_stage", "gemm_stage_timed", "post_stage",
+__all__ = ["Plan", "Context", "LoopbackGroup", "run", "run_host", "run_allgather", "rowexchange_stage", "run_sequential", "gemm_stage", "gemm_stage_timed", "post_stage",
            "unique_id", "tune_search", "tune_predict", "kernel_launch_count", "FOError", "load",
            "device_sm_count"]
 
@@ -217,6 +217,14 @@ class Context:
         check(load().fo_ctx_create_from_comm(device, C.c_void_p(int(nccl_comm)), C.byref(h)))
         return cls(h, device, rank, world)
 
+    @classmethod
+    def loopback(cls, group: "LoopbackGroup", rank: int) -> "Context":
+        """TEST backend: rank `rank` of an in-process loopback group on one GPU
+        (fo_ctx_create_loopback)."""
+        h = C.c_void_p()
+        check(load().fo_ctx_create_loopback(group.handle, int(rank), C.byref(h)))
+        return cls(h, group.device, rank, group.world)
+
     def time_collective(self, coll: str, nbytes: int, iters: int = 5) -> float:
         """Average us of one collective of `nbytes` on this context's communicator (tuning)."""
         out = C.c_double()
@@ -232,6 +240,25 @@ class Context:
         if getattr(self, "_h", None) and self._h.value:
             check(load().fo_ctx_destroy(self._h))
             self._h = C.c_void_p()
+
+
+class LoopbackGroup:
+    """TEST backend (fo_loopback_create): `world` in-process ranks on one GPU,
+    so the multi-rank data path runs on a single-GPU box.  Not for production."""
+
+    def __init__(self, device: int, world: int):
+        self.device, self.world = device, world
+        h = C.c_void_p()
+        check(load().fo_loopback_create(int(device), int(world), C.byref(h)))
+        self.handle = h
+
+    def contexts(self):
+        return [Context.loopback(self, r) for r in range(self.world)]
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            check(load().fo_loopback_destroy(self.handle))
+            self.handle = C.c_void_p()
 
 
 def _ptr(t):

@@ -86,6 +86,9 @@ _SIGS = [
                                 C.POINTER(_P)]),
     ("fo_ctx_create_from_comm", C.c_int, [C.c_int32, _P, C.POINTER(_P)]),
     ("fo_ctx_destroy", C.c_int, [_P]),
+    ("fo_loopback_create", C.c_int, [C.c_int32, C.c_int32, C.POINTER(_P)]),
+    ("fo_loopback_destroy", C.c_int, [_P]),
+    ("fo_ctx_create_loopback", C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
     ("fo_ctx_time_collective", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double)]),
     ("fo_run", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_sequential", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),

@@ -25,6 +25,7 @@ SOURCES = [
     "plan.cpp",
     "tuner.cpp",
     "runtime.cu",
+    "loopback.cu",
     "kernels/gemm_tcgen05.cu",
     "kernels/post_reorder.cu",
 ]

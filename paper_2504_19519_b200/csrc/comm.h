@@ -33,7 +33,7 @@ struct Comm {
   // recv[q*count ...] = rank q's send[count]
   virtual void allgather(const void* send, void* recv, size_t sendcount, cudaStream_t s) = 0;
   virtual void group_start() = 0;
-  virtual void group_end() = 0;
+  virtual void group_end(cudaStream_t s) = 0;  // s: the stream of the group's calls
   virtual void send(const void* buf, size_t count, int peer, cudaStream_t s) = 0;
   virtual void recv(void* buf, size_t count, int peer, cudaStream_t s) = 0;
   // the watchdog: make in-flight calls exit (the communicator is unusable afterwards)
@@ -44,5 +44,15 @@ struct Comm {
 
 // NCCL backend; owns (destroys / may abort) the communicator iff `owns`.
 Comm* make_nccl_comm(ncclComm_t comm, int rank, int world, bool owns);
+
+// Loopback test backend (loopback.cu): a group of `world` in-process ranks on
+// one device; every rank's context gets make_loopback_comm(group, rank).
+struct LoopbackGroup;
+LoopbackGroup* loopback_create(int device, int world);
+void loopback_destroy(LoopbackGroup* g);
+int loopback_members(LoopbackGroup* g);
+int loopback_world(LoopbackGroup* g);
+int loopback_device(LoopbackGroup* g);
+Comm* make_loopback_comm(LoopbackGroup* g, int rank);
 
 }  // namespace fo

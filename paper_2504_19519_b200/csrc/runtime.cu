@@ -111,7 +111,7 @@ struct NcclComm final : Comm {
     FO_NCCL(ncclAllGather(send, recv, sendcount, ncclBfloat16, c, s));
   }
   void group_start() override { FO_NCCL(ncclGroupStart()); }
-  void group_end() override { FO_NCCL(ncclGroupEnd()); }
+  void group_end(cudaStream_t) override { FO_NCCL(ncclGroupEnd()); }
   void send(const void* buf, size_t count, int peer, cudaStream_t s) override {
     FO_NCCL(ncclSend(buf, count, ncclBfloat16, peer, c, s));
   }
@@ -537,7 +537,7 @@ static void exec_calls(fo_ctx_s* c, const std::vector<fo_comm_call>& calls, size
         c->comm->group_start();
         break;
       case FO_CALL_GROUP_END:
-        c->comm->group_end();
+        c->comm->group_end(cs);
         break;
       default:
         fail(FO_ERR_STATE, "unknown schedule call kind %d", k.kind);
@@ -580,13 +580,17 @@ static void init_streams(fo_ctx_s* c) {
   FO_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   FO_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   FO_CUDA(cudaEventCreateWithFlags(&c->ev_post_join, cudaEventDisableTiming));
-  for (int i = 0; i < 2; ++i) {
-    FO_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream[i], cudaStreamNonBlocking));
-    FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_join[i], cudaEventDisableTiming));
-  }
-  FO_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_join[i], cudaEventDisableTiming));
   FO_CUDA(cudaEventCreateWithFlags(&c->ev_h2d_fork, cudaEventDisableTiming));
   FO_CUDA(cudaEventCreateWithFlags(&c->ev_d2h_join, cudaEventDisableTiming));
+}
+
+// the copy streams of fo_run_host, created on first use (a context that
+// never stages host buffers holds only its comm and post streams)
+static void ensure_host_streams(fo_ctx_s* c) {
+  if (c->d2h_stream) return;
+  for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream[i], cudaStreamNonBlocking));
+  FO_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
 }
 
 fo_status fo_get_unique_id(uint8_t uid[128]) {
@@ -645,6 +649,44 @@ fo_status fo_ctx_create_from_comm(int32_t device, void* nccl_comm, fo_ctx* out) 
     c->world = count;
     c->comm = make_nccl_comm(comm, rank, count, false);
     try {
+      init_streams(c);
+    } catch (...) {
+      delete c->comm;
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+fo_status fo_loopback_create(int32_t device, int32_t world, void** group) {
+  return guard([&] {
+    if (!group) fail(FO_ERR_INVALID_ARG, "null argument");
+    *group = loopback_create(device, world);
+  });
+}
+
+fo_status fo_loopback_destroy(void* group) {
+  return guard([&] {
+    if (!group) return;
+    auto* g = static_cast<LoopbackGroup*>(group);
+    if (loopback_members(g)) fail(FO_ERR_STATE, "loopback group still has %d contexts", loopback_members(g));
+    loopback_destroy(g);
+  });
+}
+
+fo_status fo_ctx_create_loopback(void* group, int32_t rank, fo_ctx* out) {
+  return guard([&] {
+    if (!group || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    auto* g = static_cast<LoopbackGroup*>(group);
+    if (rank < 0 || rank >= loopback_world(g)) fail(FO_ERR_INVALID_ARG, "rank %d of %d", rank, loopback_world(g));
+    FO_CUDA(cudaSetDevice(loopback_device(g)));
+    auto* c = new fo_ctx_s();
+    c->device = loopback_device(g);
+    c->rank = rank;
+    c->world = loopback_world(g);
+    try {
+      c->comm = make_loopback_comm(g, rank);
       init_streams(c);
     } catch (...) {
       delete c->comm;
@@ -853,6 +895,8 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
   return guard([&] {
     if (!c || !p || !A || !Bt || !out) fail(FO_ERR_INVALID_ARG, "null argument");
     ensure_device(p);
+    FO_CUDA(cudaSetDevice(c->device));
+    ensure_host_streams(c);
     const PlanHost& h = p->host;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t a_bytes = 2 * (size_t)(h.M * h.K), b_bytes = 2 * (size_t)(h.N * h.K);
@@ -1222,7 +1266,7 @@ fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t 
             c->comm->send(reinterpret_cast<char*>(a) + 2 * per * d, per, d, cs);
             c->comm->recv(reinterpret_cast<char*>(b) + 2 * per * d, per, d, cs);
           }
-          c->comm->group_end();
+          c->comm->group_end(cs);
           break;
         }
         default:

@@ -1,0 +1,159 @@
+"""World-W run of the library's multi-rank data path on ONE GPU (test
+infrastructure, launched by tests/test_gpu_loopback.py in a subprocess).
+
+W in-process ranks share one B200 through the loopback communicator
+(fo_loopback_create / fo_ctx_create_loopback): every rank has its own context
+(comm + post streams), plan, caller stream and inputs, and the host issues the
+ranks' fo_run calls one after the other, exactly as W processes would each
+issue theirs.  The ranks' GEMMs, counter-triggered group calls on the comm
+streams, last-group calls on the caller streams, receive buffers and post
+passes all run for real; only the transport differs from NCCL.
+
+Inputs are in the exact-integer regime (A, B in {-1, 0, 1}, <= 256 nonzeros per
+output row over all ranks), so every partial sum is exact in bf16 and the
+outputs must equal the ORACLE's plain definitions (oracle/pipeline.py O8) bit
+for bit: AllReduce = sum_r C_r; ReduceScatter = rows R_k (fo_run) /
+contiguous rows (fo_run_sequential); All-to-All = concat over sources
+(all-to-all-v order); AllGather + row exchange = the AllReduce.
+
+usage: loopback_worker.py W  -> prints "loopback W=<W>: OK" and exits 0.
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2504_19519_b200 as fo  # noqa: E402
+import synthetic  # noqa: E402
+from oracle import pipeline as opl  # noqa: E402
+
+
+def main(W):
+    torch.cuda.set_device(0)
+    grp = fo.LoopbackGroup(0, W)
+    ctxs = grp.contexts()
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    bad = []
+
+    def check(name, got, want):
+        g = got.double().cpu().numpy() if isinstance(got, torch.Tensor) else got
+        if g.shape != want.shape or not np.array_equal(g, want):
+            diff = np.abs(g - want).max() if g.shape == want.shape else f"shape {g.shape} vs {want.shape}"
+            print(f"MISMATCH W={W} {name}: {diff}", flush=True)
+            bad.append(name)
+
+    def each(fn):
+        """Issue fn(r) for every rank on its own stream (host-asynchronous),
+        then wait for all of them."""
+        for r in range(W):
+            with torch.cuda.stream(streams[r]):
+                fn(r)
+        for s in streams:
+            s.synchronize()
+
+    M, N, K, BM, BN = 1024, 512, 256, 256, 128           # 16 tiles; S = 4 -> 4 waves
+    S = 4
+    inp = [synthetic.exact_inputs(M, N, K, seed=synthetic.rank_seed(61, W, r), nnz_per_row=max(1, 256 // W))
+           for r in range(W)]
+    As = [a.double().numpy() for a, _ in inp]
+    Bts = [b.double().numpy() for _, b in inp]
+    Ad = [a.cuda() for a, _ in inp]
+    Bd = [b.cuda() for _, b in inp]
+    torch.cuda.synchronize()
+    full = opl.plain_allreduce(As, Bts)[0]
+    for coll, layout, groups, split in (("allreduce", "slot", [1, 2, 1], 0), ("allreduce", "rowband", [1, 1, 2], 0),
+                                        ("allreduce", "rowband", [4], 0), ("allreduce", "slot", [2, 2], -1),
+                                        ("reducescatter", "auto", [2, 1, 1], 0),
+                                        ("reducescatter", "auto", [1, 3], -1)):
+        if coll == "reducescatter" and BM % W:
+            continue
+        spec = dict(coll=coll, m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S,
+                    swizzle=1 if layout == "rowband" else 2, group_waves=groups, ar_layout=layout)
+        # the split tail needs workers idle in the last wave: 3 full waves of 5 + 1
+        if split:
+            spec["workers"] = 5
+            spec["group_waves"] = [1, 3] if coll == "reducescatter" else [2, 2]
+        plans = [fo.Plan(rank=r, world=W, options={"tail_split": split} if split else None, **spec)
+                 for r in range(W)]
+        name = f"{coll}/{layout}/{spec['group_waves']}/split={split}"
+        if coll == "allreduce":
+            want = full
+        else:
+            want = opl.plain_reducescatter(As, Bts, BM)
+        outs = [torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda")
+                for p in plans]
+        torch.cuda.synchronize()
+        for trig in (1, 0):
+            for p in plans:
+                p.set_option("last_group_in_order", trig)
+            for _ in range(3):
+                each(lambda r: fo.run(ctxs[r], plans[r], Ad[r], Bd[r], outs[r], stream=streams[r]))
+            for r in range(W):
+                check(f"{name}/in_order={trig}/rank{r}", outs[r], want if coll == "allreduce" else want[r])
+        seq = [torch.full_like(o, float("nan")) for o in outs]
+        torch.cuda.synchronize()
+        each(lambda r: fo.run_sequential(ctxs[r], plans[r], Ad[r], Bd[r], seq[r], stream=streams[r]))
+        for r in range(W):
+            w = full if coll == "allreduce" else full[r * (M // W):(r + 1) * (M // W)]
+            check(f"{name}/sequential/rank{r}", seq[r], w)
+        if coll == "reducescatter":
+            gath = [torch.empty(M, N, dtype=torch.bfloat16, device="cuda") for _ in range(W)]
+            torch.cuda.synchronize()
+            each(lambda r: fo.run_allgather(ctxs[r], plans[r], outs[r], gath[r], stream=streams[r]))
+            for r in range(W):
+                check(f"{name}/allgather+rowexchange/rank{r}", gath[r], full)
+        # fo_run_host: host activations (chunked H2D the GEMM waits on, two staging sets)
+        if coll == "allreduce" and not split:
+            hosts = [[torch.full((M, N), float("nan"), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+                     for _ in range(W)]
+            A_h = [a.pin_memory() for a, _ in inp]
+            for i in range(2):
+                each(lambda r: fo.run_host(ctxs[r], plans[r], A_h[r], Bd[r], hosts[r][i], stream=streams[r]))
+            for r in range(W):
+                for i in range(2):
+                    check(f"{name}/run_host[{i}]/rank{r}", hosts[r][i], full)
+        for p in plans:
+            p.close()
+    # ---- All-to-All: imbalanced experts, random routing, same P on every rank
+    rng = np.random.default_rng(7 + W)
+    Ms = [256 * int(rng.integers(1, 5)) for _ in range(W)]
+    rds = [rng.integers(0, W, size=Ms[s]).astype(np.int32) for s in range(W)]
+    inp = [synthetic.exact_inputs(Ms[s], N, K, seed=synthetic.rank_seed(71, W, s), nnz_per_row=128)
+           for s in range(W)]
+    As = [a.double().numpy() for a, _ in inp]
+    Bts = [b.double().numpy() for _, b in inp]
+    Ad = [a.cuda() for a, _ in inp]
+    Bd = [b.cuda() for _, b in inp]
+    S2 = 2
+    specs = []
+    for s in range(W):
+        T = -(-(Ms[s] // BM) * (N // BN) // S2)
+        specs.append(dict(coll="alltoall", m=Ms[s], n=N, k=K, tile_m=BM, tile_n=BN, workers=S2, swizzle=2,
+                          group_waves=[1, T - 1], row_dst=rds[s]))
+    plans = [fo.Plan(rank=r, world=W, peers=specs, **specs[r]) for r in range(W)]
+    want = opl.plain_alltoall(As, Bts, rds)
+    outs = [torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda") for p in plans]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        each(lambda r: fo.run(ctxs[r], plans[r], Ad[r], Bd[r], outs[r], stream=streams[r]))
+    for r in range(W):
+        check(f"alltoall/rank{r}", outs[r], want[r])
+    seq = [torch.full_like(o, float("nan")) for o in outs]
+    torch.cuda.synchronize()
+    each(lambda r: fo.run_sequential(ctxs[r], plans[r], Ad[r], Bd[r], seq[r], stream=streams[r]))
+    for r in range(W):
+        check(f"alltoall/sequential/rank{r}", seq[r], want[r])
+    for p in plans:
+        p.close()
+    for c in ctxs:
+        c.close()
+    grp.close()
+    print(f"loopback W={W}: " + ("OK" if not bad else f"{len(bad)} mismatches"), flush=True)
+    return 0 if not bad else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main(int(sys.argv[1])))
