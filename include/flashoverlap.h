@@ -237,7 +237,11 @@ fo_status fo_ctx_destroy(fo_ctx ctx);
  * threads in any interleaving, each rank in the same order as with NCCL.
  * A call sequence that differs between ranks (a hang with NCCL) or a barrier
  * not reached within 20 s traps the device (the CUDA context is lost) instead
- * of hanging.  Not CUDA-graph capturable.  fo_loopback_destroy fails with
+ * of hanging.  Needs eager module loading (CUDA_MODULE_LOADING=EAGER before
+ * CUDA starts; else FO_ERR_UNSUPPORTED): a lazily loaded kernel's first launch
+ * may wait for running kernels, i.e. for another rank's call at its barrier.
+ * Prepare every plan (fo_plan_prepare) before the ranks issue: an allocation
+ * in one rank must not wait on another rank's call.  Not CUDA-graph capturable.  fo_loopback_destroy fails with
  * FO_ERR_STATE while contexts of the group exist.  Not for production use. */
 fo_status fo_loopback_create(int32_t device, int32_t world, void** group);
 fo_status fo_loopback_destroy(void* group);
@@ -364,6 +368,15 @@ fo_status fo_plan_gemm_cluster(fo_plan plan, int32_t* cluster_ctas);
  * one; the run's output is undefined), and FO_ERR_TIMEOUT is returned.
  * Host-blocking; not graph-capturable. */
 fo_status fo_plan_sync(fo_ctx ctx, fo_plan plan, void* stream, int64_t timeout_ms);
+/* Bind the plan to the current device and allocate, now, the device state its
+ * runs would otherwise allocate on first use: tables, counters, the send /
+ * receive buffers (always), the row-major scratch of fo_run_sequential /
+ * fo_run_allgather for RS / A2A plans (what & 1), and the staging buffers of
+ * fo_run_host for a host A and a host out (what & 2).  After it no run of the
+ * plan allocates (CUDA-graph capture; multi-rank issue where one rank's
+ * allocation must not wait on another rank's in-flight collective).
+ * Synchronises the device. */
+fo_status fo_plan_prepare(fo_plan plan, int32_t what);
 /* Copy the plan's P counters to host (synchronises the device). */
 fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
 /* Debug / evidence hooks (tests, tools; never needed for correct use):

@@ -156,6 +156,11 @@ class Plan:
         check(load().fo_plan_read_counters(self._h, c.ctypes.data_as(C.POINTER(C.c_uint32))))
         return c
 
+    def prepare(self, sequential: bool = True, host: bool = False):
+        """fo_plan_prepare: allocate the plan's device state now (tables,
+        buffers; the sequential / allgather scratch; fo_run_host staging)."""
+        check(load().fo_plan_prepare(self._h, (1 if sequential else 0) | (2 if host else 0)))
+
     def gemm_cluster(self) -> int:
         """CTAs per cluster of the plan's GEMM launch on the current device (1, 2, 4)."""
         v = C.c_int32(0)

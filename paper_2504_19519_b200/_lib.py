@@ -101,6 +101,7 @@ _SIGS = [
     ("fo_combine_stage", C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     ("fo_run_combine", C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     ("fo_plan_read_counters", C.c_int, [_P, C.POINTER(C.c_uint32)]),
+    ("fo_plan_prepare", C.c_int, [_P, C.c_int32]),
     ("fo_plan_gemm_cluster", C.c_int, [_P, C.POINTER(C.c_int32)]),
     ("fo_plan_sync", C.c_int, [_P, _P, _P, C.c_int64]),
     ("fo_kernel_launch_count", C.c_int64, []),

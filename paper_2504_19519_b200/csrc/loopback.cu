@@ -30,10 +30,13 @@
 // error code and traps (the process's CUDA context dies loudly; tests run it
 // in a subprocess).  All ranks must call in the same order, as with NCCL.
 // Not CUDA-graph capturable (descriptors are written by the host at issue).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <ctime>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -101,7 +104,7 @@ __device__ __forceinline__ unsigned long long now_ns() {
 }
 
 __device__ void fail_trap(int* err, int code) {
-  printf("loopback communicator: schedule mismatch / timeout (code %d) - trapping\n", code);
+  printf("loopback communicator: schedule mismatch / timeout (code %d, block %d) - trapping\n", code, blockIdx.x);
   atomicCAS(err, 0, code);
   __threadfence_system();
   __trap();
@@ -115,7 +118,12 @@ __device__ void barrier(const LbArgs& a, unsigned* c) {
     const unsigned long long t0 = now_ns();
     while ((int)(ld_acquire(c) - a.target) < 0) {
       if (*(volatile const int*)a.abort_flag) break;
-      if (now_ns() - t0 > kTimeoutNs) fail_trap(a.err, 1000 + a.kind);
+      if (now_ns() - t0 > kTimeoutNs) {
+        printf("loopback rank %d kind %d slot %d: barrier %s counter %u target %u (waiting since t=%llu ms)\n",
+               a.rank, a.kind, a.slot, (c == a.ctr + (size_t)a.slot * 2) ? "arrive" : "depart", ld_acquire(c),
+               a.target, (t0 / 1000000ull) % 1000000ull);
+        fail_trap(a.err, 1000 + a.kind);
+      }
       __nanosleep(256);
     }
   }
@@ -237,6 +245,12 @@ struct LoopbackGroup {
 
 namespace {
 
+unsigned long long wall_ms() {  // same clock domain as %globaltimer (ns since the epoch), in ms mod 1e6
+  timespec ts;
+  clock_gettime(CLOCK_REALTIME, &ts);
+  return ((unsigned long long)ts.tv_sec * 1000ull + ts.tv_nsec / 1000000) % 1000000ull;
+}
+
 struct LoopbackComm final : Comm {
   LoopbackGroup* g;
   int r;
@@ -245,7 +259,11 @@ struct LoopbackComm final : Comm {
   cudaStream_t group_stream = nullptr;
   std::vector<LbDesc> pending;
   cudaEvent_t slot_done[kRing] = {};
-  LoopbackComm(LoopbackGroup* g_, int r_) : g(g_), r(r_) {}
+  bool trace_ = false;
+  LoopbackComm(LoopbackGroup* g_, int r_) : g(g_), r(r_) {
+    const char* t = getenv("FO_LOOPBACK_TRACE");
+    trace_ = t && t[0] == '1';
+  }
   ~LoopbackComm() override {
     for (auto& e : slot_done)
       if (e) cudaEventDestroy(e);
@@ -291,6 +309,9 @@ struct LoopbackComm final : Comm {
       a.desc = slot_desc;
       a.ndesc = (int)desc->size();
     }
+    if (trace_)
+      fprintf(stderr, "[loopback] t=%llu ms rank %d call %llu slot %d kind %d count %lld ndesc %d stream %p\n",
+              wall_ms(), r, seq - 1, a.slot, kind, count, a.ndesc, (void*)s);
     lb_kernel<<<kCtas, 256, 0, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(FO_ERR_CUDA, "loopback launch: %s", cudaGetErrorString(e));
@@ -360,6 +381,21 @@ Comm* make_loopback_comm(LoopbackGroup* g, int rank) {
 
 LoopbackGroup* loopback_create(int device, int world) {
   if (world < 1 || world > 64) fail(FO_ERR_INVALID_ARG, "loopback world %d (1..64)", world);
+  // With lazy module loading the first launch of a kernel may wait for the
+  // kernels already running — here another rank's call spinning at the
+  // barrier for this rank: a deadlock NCCL's one-process-per-GPU never sees.
+  {
+    typedef CUresult (*GetModeFn)(CUmoduleLoadingMode*);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUmoduleLoadingMode mode = CU_MODULE_EAGER_LOADING;
+    if (cudaGetDriverEntryPoint("cuModuleGetLoadingMode", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      reinterpret_cast<GetModeFn>(fn)(&mode);
+    if (mode == CU_MODULE_LAZY_LOADING)
+      fail(FO_ERR_UNSUPPORTED,
+           "the loopback communicator needs eager module loading: set CUDA_MODULE_LOADING=EAGER before CUDA starts");
+  }
   auto* g = new LoopbackGroup();
   g->device = device;
   g->world = world;

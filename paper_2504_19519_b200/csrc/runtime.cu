@@ -1218,6 +1218,26 @@ fo_status fo_plan_sync(fo_ctx c, fo_plan p, void* stream, int64_t timeout_ms) {
   });
 }
 
+fo_status fo_plan_prepare(fo_plan p, int32_t what) {
+  return guard([&] {
+    if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
+    if (what < 0 || what > 3) fail(FO_ERR_INVALID_ARG, "what must be a mask of 1 | 2");
+    ensure_device(p);
+    const PlanHost& h = p->host;
+    if ((what & 1) && (h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && !p->d_rowmajor)
+      FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * (size_t)(h.M * h.N)));
+    if (what & 2) {
+      const size_t a_bytes = 2 * (size_t)(h.M * h.K), o_bytes = 2 * (size_t)(h.out_rows * h.N);
+      if (!(h.mn_major & 1)) plan_a_chunks(p);
+      for (void** b : {&p->h_A, &p->h_A2})
+        if (!*b) FO_CUDA(cudaMalloc(b, a_bytes));
+      for (void** b : {&p->h_out, &p->h_out2})
+        if (!*b) FO_CUDA(cudaMalloc(b, o_bytes));
+    }
+    FO_CUDA(cudaDeviceSynchronize());
+  });
+}
+
 fo_status fo_plan_read_counters(fo_plan p, uint32_t* counters) {
   return guard([&] {
     if (!p || !counters) fail(FO_ERR_INVALID_ARG, "null argument");

@@ -3,9 +3,9 @@ infrastructure, launched by tests/test_gpu_loopback.py in a subprocess).
 
 W in-process ranks share one B200 through the loopback communicator
 (fo_loopback_create / fo_ctx_create_loopback): every rank has its own context
-(comm + post streams), plan, caller stream and inputs, and the host issues the
-ranks' fo_run calls one after the other, exactly as W processes would each
-issue theirs.  The ranks' GEMMs, counter-triggered group calls on the comm
+(comm + post streams), plan, caller stream and inputs, and every rank's calls
+are issued from its own host thread, exactly as W processes would each issue
+theirs.  The ranks' GEMMs, counter-triggered group calls on the comm
 streams, last-group calls on the caller streams, receive buffers and post
 passes all run for real; only the transport differs from NCCL.
 
@@ -20,8 +20,11 @@ usage: loopback_worker.py W  -> prints "loopback W=<W>: OK" and exits 0.
 """
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from concurrent.futures import ThreadPoolExecutor  # noqa: E402
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -29,6 +32,9 @@ import torch  # noqa: E402
 import paper_2504_19519_b200 as fo  # noqa: E402
 import synthetic  # noqa: E402
 from oracle import pipeline as opl  # noqa: E402
+
+
+TRACE = os.environ.get("FO_LOOPBACK_TRACE") == "1"
 
 
 def main(W):
@@ -45,14 +51,24 @@ def main(W):
             print(f"MISMATCH W={W} {name}: {diff}", flush=True)
             bad.append(name)
 
+    pool = ThreadPoolExecutor(W)
+
     def each(fn):
-        """Issue fn(r) for every rank on its own stream (host-asynchronous),
-        then wait for all of them."""
-        for r in range(W):
+        """Issue fn(r) for every rank from its own host thread on its own
+        stream — as W processes would; a host call that blocks in one rank
+        (a synchronous allocation or copy) never stops the others from issuing
+        the calls its kernels wait for — then wait for all of them."""
+        def one(r):
+            torch.cuda.set_device(0)
+            if TRACE:
+                print(f"[host] t={int(time.time() * 1000) % 1000000} ms rank {r} issue", file=sys.stderr, flush=True)
             with torch.cuda.stream(streams[r]):
                 fn(r)
-        for s in streams:
-            s.synchronize()
+            if TRACE:
+                print(f"[host] t={int(time.time() * 1000) % 1000000} ms rank {r} issued", file=sys.stderr, flush=True)
+            streams[r].synchronize()
+        for f in [pool.submit(one, r) for r in range(W)]:
+            f.result()
 
     M, N, K, BM, BN = 1024, 512, 256, 256, 128           # 16 tiles; S = 4 -> 4 waves
     S = 4
@@ -78,7 +94,10 @@ def main(W):
             spec["group_waves"] = [1, 3] if coll == "reducescatter" else [2, 2]
         plans = [fo.Plan(rank=r, world=W, options={"tail_split": split} if split else None, **spec)
                  for r in range(W)]
+        for p in plans:     # no rank allocates while another's collective is in flight
+            p.prepare(sequential=True, host=True)
         name = f"{coll}/{layout}/{spec['group_waves']}/split={split}"
+        print(f"[W={W}] {name}", flush=True)
         if coll == "allreduce":
             want = full
         else:
@@ -106,7 +125,11 @@ def main(W):
             for r in range(W):
                 check(f"{name}/allgather+rowexchange/rank{r}", gath[r], full)
         # fo_run_host: host activations (chunked H2D the GEMM waits on, two staging sets)
-        if coll == "allreduce" and not split:
+        # (W <= 4: with its three copy streams a rank has six streams, and
+        # more than 32 streams alias the device's hardware queues, where one
+        # rank's pending stream wait can block another rank's launch — a
+        # one-process artefact; with NCCL every rank is its own process)
+        if coll == "allreduce" and not split and W <= 4:
             hosts = [[torch.full((M, N), float("nan"), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
                      for _ in range(W)]
             A_h = [a.pin_memory() for a, _ in inp]
@@ -134,6 +157,9 @@ def main(W):
         specs.append(dict(coll="alltoall", m=Ms[s], n=N, k=K, tile_m=BM, tile_n=BN, workers=S2, swizzle=2,
                           group_waves=[1, T - 1], row_dst=rds[s]))
     plans = [fo.Plan(rank=r, world=W, peers=specs, **specs[r]) for r in range(W)]
+    print(f"[W={W}] alltoall Ms={Ms}", flush=True)
+    for p in plans:
+        p.prepare(sequential=True)
     want = opl.plain_alltoall(As, Bts, rds)
     outs = [torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda") for p in plans]
     torch.cuda.synchronize()

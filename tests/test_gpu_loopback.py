@@ -18,7 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_loopback_world(world):
-    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    # eager module loading: a lazily loaded kernel's first launch may wait for
+    # running kernels, i.e. for another in-process rank's call at its barrier
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "loopback_worker.py"), str(world)], cwd=ROOT,
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and f"loopback W={world}: OK" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
