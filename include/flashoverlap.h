@@ -453,7 +453,7 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *  FO_OPT_DEBUG_STALL_GROUP -1 — off; j — TEST ONLY: group j's trigger waits for
  *                      one more signal than the GEMM sends, so the run never
  *                      finishes (exercises the fo_plan_sync watchdog)
- *  FO_OPT_GEMM_SWIGLU  0 — off; 1 — (no-comm plans, tile_n 256)
+ *  FO_OPT_GEMM_SWIGLU  0 — off; 1 — (no-comm plans, tile_n 256, post none)
  *                      the GEMM's epilogue applies the SwiGLU of an MLP: with the
  *                      weight rows interleaved in blocks of 128 (gate 0..127, up
  *                      0..127, gate 128..255, up 128..255, ...), tile column block

@@ -14,7 +14,11 @@ Pins (tests/test_oracle_alg1.py): |space| = 2^(T-1), T=8 -> 128 (PAPER.md:438);
 (1,2,2) and (2,3) are in the T=5 space; pruned sizes for
 T=1..12 by an independent count; hand traces of the recurrence
 ((1,1,1,1) -> 50, (4) -> 80, comm-bound (1,1,1,1) -> 85 = the
-PAPER.md:622 bound); single group == GEMM + full comm.
+PAPER.md:622 bound); single group == GEMM + full comm; the bytes -> us
+conversion of interp_latency_us by hand (1 MB at 1 GB/s = 1000 us, 4 MB at
+400 GB/s = 10 us); both branches of perfect_overlap_bound by hand values of
+PAPER.md:622's sentence, and its GEMM-bound branch attained by the finest
+partition when each wave's communication hides under the next wave.
 """
 from __future__ import annotations
 

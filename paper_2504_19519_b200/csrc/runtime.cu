@@ -364,8 +364,8 @@ static void run_gemm(fo_plan_s* p, const void* A, const void* Bt, void* dst, int
   if (!A || !Bt || !dst) fail(FO_ERR_INVALID_ARG, "null device pointer");
   GemmArgs a = gemm_args(p, A, Bt, dst, mode, signal);
   if (p->swiglu && mode == EPI_ROWMAJOR) {  // FO_OPT_GEMM_SWIGLU: C is [m, n/2] = silu(gate) * up
-    if (p->host.BN != 256 || p->host.coll != FO_NOCOMM)
-      fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan and tile_n 256");
+    if (p->host.BN != 256 || p->host.coll != FO_NOCOMM || p->host.post != FO_POST_NONE)
+      fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan, tile_n 256 and post none");
     a.mode = EPI_SWIGLU;
     a.ldc = p->host.N / 2;
   }
@@ -900,7 +900,8 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
     const PlanHost& h = p->host;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t a_bytes = 2 * (size_t)(h.M * h.K), b_bytes = 2 * (size_t)(h.N * h.K);
-    const size_t o_bytes = 2 * (size_t)(h.out_rows * h.N);
+    // the SwiGLU epilogue writes C as [m, n/2]
+    const size_t o_bytes = 2 * (size_t)(h.out_rows * (p->swiglu ? h.N / 2 : h.N));
     // host operands are staged through library-owned device buffers; operands
     // that already live on the device (e.g. resident weights) are used in place
     auto stage = [&](const void* src, void*& buf, size_t bytes) -> const void* {
@@ -984,6 +985,10 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
     if (pipe_a)
       for (int i = 0; i < 2; ++i) FO_CUDA(cudaStreamWaitEvent(s, c->ev_h2d_join[i], 0));
     if (!out_dev && !pipe_out) FO_CUDA(cudaMemcpyAsync(out, dO, o_bytes, cudaMemcpyDeviceToHost, s));
+    // FO_POST_ADD_RMSNORM_RESIDUAL updates the residual in place: a host
+    // residual gets its staged copy back
+    if (residual && dR != residual && h.post == FO_POST_ADD_RMSNORM_RESIDUAL)
+      FO_CUDA(cudaMemcpyAsync(const_cast<void*>(residual), dR, o_bytes, cudaMemcpyDeviceToHost, s));
     if (two_sets) FO_CUDA(cudaEventRecord(p->ev_set_done[b], s));  // set b free once this call is done
   });
 }
@@ -1358,8 +1363,8 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
         break;
       case FO_OPT_GEMM_SWIGLU:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "gemm_swiglu must be 0 or 1");
-        if (value && (p->host.coll != FO_NOCOMM || p->host.BN != 256))
-          fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan with tile_n 256");
+        if (value && (p->host.coll != FO_NOCOMM || p->host.BN != 256 || p->host.post != FO_POST_NONE))
+          fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan with tile_n 256 and post none");
         p->swiglu = (int)value;
         break;
       case FO_OPT_DEBUG_STALL_GROUP:

@@ -100,6 +100,7 @@ static std::vector<int> dp_search(double duration, int T, int tiles, int S, doub
       }
     }
   }
+  if (!(E[T] < inf)) fail(FO_ERR_INVALID_ARG, "pruning left no candidate (s1=%d, sp=%d, T=%d)", s1, sp, T);
   std::vector<int> G;
   for (int w = T; w > 0; w = prev[w]) G.insert(G.begin(), w - prev[w]);
   *best_t = E[T];
@@ -138,6 +139,7 @@ static std::vector<int> dp_g(double duration, int T, const GroupLat& lat, int s1
         ng[w] = ng[w0] + 1;
       }
     }
+  if (!(E[T] < inf)) fail(FO_ERR_INVALID_ARG, "pruning left no candidate (s1=%d, sp=%d, T=%d)", s1, sp, T);
   std::vector<int> G;
   for (int w = T; w > 0; w = prev[w]) G.insert(G.begin(), w - prev[w]);
   *best = E[T];
@@ -218,6 +220,7 @@ extern "C" fo_status fo_tune_search_multi(int32_t ranks, int32_t T, const double
   return guard([&] {
     if (ranks < 1 || T < 1 || !durations || !wave_bytes || !out_groups || !out_num_groups || !predicted_us)
       fail(FO_ERR_INVALID_ARG, "bad arguments");
+    if (prune != 0 && (s1 < 1 || sp < 1)) fail(FO_ERR_INVALID_ARG, "pruning caps s1=%d, sp=%d must be >= 1", s1, sp);
     const Curve c = make_curve(curve_bytes, curve_gbps, npts);
     double dmax = 0.0;
     for (int r = 0; r < ranks; ++r) dmax = std::max(dmax, durations[r]);
@@ -256,6 +259,7 @@ extern "C" fo_status fo_tune_search(double duration_us, int32_t tiles, int32_t S
                                     int32_t* out_num_groups, double* predicted_us) {
   return guard([&] {
     if (!out_groups || !out_num_groups || !predicted_us || S < 1 || tiles < 1) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    if (prune != 0 && (s1 < 1 || sp < 1)) fail(FO_ERR_INVALID_ARG, "pruning caps s1=%d, sp=%d must be >= 1", s1, sp);
     const int T = (tiles + S - 1) / S;
     const Curve c = make_curve(curve_bytes, curve_gbps, npts);
     if (prune >= 2 || T > 20) {

@@ -1,12 +1,17 @@
 """GPU parity at BASELINE.json's full sizes (configs[1..3]) in the launch
-configuration bench.py uses (256x256 CTA-pair tiles, S = 64 pairs), on sampled
-outputs the oracle computes one by one (fp64, float regime, tolerance 1e-2).
+configuration bench.py uses (256x256 CTA-pair tiles, S = 64 pairs), on the
+FULL output matrices against the fp64 oracle (float regime, tolerance 1e-2).
 
 Multi-rank configurations run every rank's GEMM + pre-reorder epilogue on the
 one GPU through fo_gemm_stage; the collective between them is emulated on the
-GPU by this test (sums / slices / copies over the plan's group ranges) and each
-receiver's post-reorder runs through fo_post_stage.  The single-rank bench
-configuration runs through fo_run with the real NCCL.
+GPU by this test as NCCL's ring computes a bf16 sum — the bf16 partials added
+one rank at a time, rounded to bf16 after every hop — over the plan's group
+ranges, and each receiver's post-reorder runs through fo_post_stage.  The
+result is held to (a) the first-order rounding bound of that summation against
+the unrounded fp64 definition, |g - o| <= u (sum_r |p_r| + sum_k |s_k|)
+(u = 2^-9, p_r the fp64 partials, s_k the computed running sums), and (b) the
+north_star 1e-2 against the oracle in its bf16-epilogue model (R11).
+The single-rank bench configuration runs through fo_run with the real NCCL.
 """
 import numpy as np
 import pytest
@@ -34,20 +39,27 @@ def _dev():
 U = 2.0 ** -9  # bf16 unit roundoff
 
 
-def _check_rows(got_rows, want_rows, partials=None):
+def _check_rows(got_rows, want_rows, partials=None, running=None):
     """Tolerance check (R10/R11).
 
-    want_rows: the oracle value.  With `partials` (per-rank fp64 rows) the
-    oracle is taken in its bf16-epilogue model (each rank's partial rounded to
-    bf16, R10: the send buffer is bf16 by construction) and compared at 1e-2;
-    the unrounded fp64 definition is then checked against the elementwise
-    rounding bound |g - o| <= 2u (sum_r |p_r| + |o|)."""
-    g = got_rows.double().cpu().numpy()
+    want_rows: the oracle value (fp64).  With `partials` (per-rank fp64 values)
+    the oracle is taken in its bf16-epilogue model (each rank's partial rounded
+    to bf16, R10: the send buffer is bf16 by construction) for the 1e-2 metric,
+    and the unrounded fp64 definition is held to the elementwise first-order
+    bound of the emulated bf16 ring sum: |g - o| <= u (sum_r |p_r| + sum_k
+    |s_k|), `running` = sum_k |s_k| over the computed running sums (without it,
+    one rounding of the total: u (sum_r |p_r| + |o|))."""
+    g = got_rows.double().cpu().numpy() if isinstance(got_rows, torch.Tensor) else got_rows
     o = np.asarray(want_rows, np.float64)
     if partials is not None:
-        model = sum(onum.round_bf16(p) for p in partials)
-        bound = 2 * U * (sum(np.abs(p) for p in partials) + np.abs(o))
+        absum = np.zeros_like(o)
+        model = np.zeros_like(o)
+        for p in partials:
+            absum += np.abs(p)
+            model += onum.round_bf16(p)
+        bound = 1.01 * U * (absum + (running if running is not None else np.abs(o)))
         assert np.all(np.abs(g - o) <= bound), "outside the bf16 rounding bound of the plain definition"
+        del absum, bound
         o = model
     rms = np.sqrt(np.mean(o * o))
     err = np.max(np.abs(g - o) / np.maximum(np.abs(o), rms))
@@ -55,8 +67,21 @@ def _check_rows(got_rows, want_rows, partials=None):
     return err
 
 
-def _sample(n, k, seed):
-    return np.sort(np.random.default_rng(seed).choice(n, size=k, replace=False))
+def _ring_sum(sends):
+    """NCCL-style bf16 ring reduction of the ranks' bf16 send buffers: added
+    one rank at a time in fp32, rounded to bf16 after every hop.  Returns the
+    bf16 sum and sum_k |s_k| (fp64, on the CPU) for the rounding bound."""
+    acc = sends[0].clone()
+    run = torch.zeros(acc.numel(), dtype=torch.float64)
+    for x in sends[1:]:
+        acc = (acc.float() + x.float()).to(torch.bfloat16)
+        run += acc.double().abs().cpu()
+    return acc, run.numpy()
+
+
+def _gemm_full(A, Bt):
+    """fp64 oracle GEMM of a whole (CPU) operand pair."""
+    return onum.gemm(A.cpu() if isinstance(A, torch.Tensor) else A, Bt.cpu() if isinstance(Bt, torch.Tensor) else Bt)
 
 
 def test_c2_bench_config_tp1_fo_run():
@@ -69,8 +94,7 @@ def test_c2_bench_config_tp1_fo_run():
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     fo.run(ctx, plan, A.cuda(), Bt.cuda(), out)
     torch.cuda.synchronize()
-    rows = _sample(M, 24, 1)
-    _check_rows(out[torch.from_numpy(rows).cuda()], onum.gemm(A[rows], Bt))
+    _check_rows(out, _gemm_full(A, Bt))
     ctx.close()
 
 
@@ -79,26 +103,31 @@ def test_c2_tp8_allreduce(layout):
     """configs[1] at TP=8: M=N=4096, K_loc=1792, 8 ranks."""
     n, M, N, K = 8, 4096, 4096, 14336 // 8
     groups = [1, 2, 1]
-    acc = torch.zeros(M * N, dtype=torch.float32, device="cuda")
-    As, Bts, plans = [], [], []
+    As, Bts, plans, sends = [], [], [], []
     for r in range(n):
         A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.rank_seed(20000, n, r), device="cuda")
         plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=groups,
                        ar_layout=layout, rank=r, world=n)
         send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
         fo.gemm_stage(plan, A, Bt, send)
-        acc += send.float()
+        sends.append(send)
         As.append(A)
         Bts.append(Bt)
         plans.append(plan)
-    recv = acc.to(torch.bfloat16)
-    rows = _sample(M, 16, 2)
-    parts = [onum.gemm(As[r][rows].cpu(), Bts[r].cpu()) for r in range(n)]
+    # every group's AllReduce reduces the same positions on all ranks, so the
+    # ring sum of the whole buffers is the per-group sums side by side
+    recv, running = _ring_sum(sends)
+    del sends
+    parts = [_gemm_full(As[r], Bts[r]) for r in range(n)]
+    want = sum(parts)
     for r in (0, n - 1):
         out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plans[r], recv, out)
         torch.cuda.synchronize()
-        _check_rows(out[torch.from_numpy(rows).cuda()], sum(parts), parts)
+        # the running sums live in send-buffer order: bring them to C's order
+        run_c = running[plans[r].export_send_map()].reshape(M, N)
+        err = _check_rows(out, want, parts, run_c)
+        print(f"TP=8 AllReduce ({layout}), rank {r}: max rel err vs the bf16-epilogue model {err:.3e}")
 
 
 def test_c3_tp8_reducescatter():
@@ -107,16 +136,16 @@ def test_c3_tp8_reducescatter():
     groups = [2, 4, 6, 4]  # T = 1024 tiles / 64 = 16
     plans = [fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, group_waves=groups,
                      rank=r, world=n) for r in range(n)]
-    acc = torch.zeros(M * N, dtype=torch.float32, device="cuda")
-    As, Bts = [], []
+    As, Bts, sends = [], [], []
     for r in range(n):
         A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.rank_seed(30000, n, r), device="cuda")
         send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
         fo.gemm_stage(plans[r], A, Bt, send)
-        acc += send.float()
+        sends.append(send)
         As.append(A)
         Bts.append(Bt)
-    summed = acc.to(torch.bfloat16)
+    summed, running = _ring_sum(sends)
+    del sends
     h = BM // n
     for k in (0, 5):
         # ReduceScatter of every group range: rank k keeps chunk k
@@ -129,10 +158,12 @@ def test_c3_tp8_reducescatter():
         out = torch.empty(M // n, N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plans[k], recv, out)
         torch.cuda.synchronize()
-        lrows = _sample(M // n, 16, 3 + k)
-        grows = [orr.rs_local_to_global_row(int(l), BM, h, k) for l in lrows]
-        parts = [onum.gemm(As[r][grows].cpu(), Bts[r].cpu()) for r in range(n)]
-        _check_rows(out[torch.from_numpy(lrows).cuda()], sum(parts), parts)
+        # every local row of rank k: global row floor(l/h)*BM + k*h + l%h (R8)
+        grows = [orr.rs_local_to_global_row(l, BM, h, k) for l in range(M // n)]
+        parts = [_gemm_full(As[r][grows], Bts[r]) for r in range(n)]
+        run_c = running[plans[k].export_send_map()].reshape(M, N)[grows]
+        err = _check_rows(out, sum(parts), parts, run_c)
+        print(f"TP=8 ReduceScatter, rank {k}: max rel err vs the bf16-epilogue model {err:.3e}")
 
 
 @pytest.mark.parametrize("routing", ["balanced", "router"])
@@ -183,10 +214,9 @@ def test_c4_ep8_alltoall(routing):
         fo.post_stage(plans[d], recv, out)
         torch.cuda.synchronize()
         # output row -> (source, source row) in all-to-all-v order
-        src_rows = [(s, int(r)) for s in range(n) for r in np.flatnonzero(rds[s] == d)]
-        sample = _sample(len(src_rows), 16, 7 + d)
-        want = np.stack([onum.gemm(As[s][[r]].cpu(), Bts[s].cpu())[0] for s, r in (src_rows[i] for i in sample)])
-        _check_rows(out[torch.from_numpy(sample).cuda()], want)
+        want = np.concatenate([_gemm_full(As[s][torch.from_numpy(np.flatnonzero(rds[s] == d)).cuda()], Bts[s])
+                               for s in range(n)], axis=0)
+        _check_rows(out, want)
 
 
 def test_c2_bench_config_tp1_tail_split():
@@ -201,13 +231,7 @@ def test_c2_bench_config_tp1_tail_split():
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     fo.run(ctx, plan, A.cuda(), Bt.cuda(), out)
     torch.cuda.synchronize()
-    rows = _sample(M, 24, 5)
-    _check_rows(out[torch.from_numpy(rows).cuda()], onum.gemm(A[rows], Bt))
-    # the tail tiles (last wave positions) in particular
-    order = plan.export_order()
-    tail_tiles = order[3 * 74:]
-    trows = np.unique((tail_tiles // 16) * 256 + 17)
-    _check_rows(out[torch.from_numpy(trows).cuda()], onum.gemm(A[trows], Bt))
+    _check_rows(out, _gemm_full(A, Bt))          # every element, the split tail tiles included
     # 34 tail tiles in f = 2 slices: the distributed fold (default) adds the
     # same two fp32 terms per element as the owner-only fold (a + b == b + a)
     alt = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=74, group_waves=[1, 2, 1],

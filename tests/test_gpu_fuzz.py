@@ -73,9 +73,14 @@ def test_random_plan_matches_oracle(seed):
         pl.set_option("multicast", c["multicast"])
         pl.set_option("tail_split", c["tail_split"])
         plans.append(pl)
-    # the oracle with the library's own execution order (swizzle 0 = auto is a
-    # library heuristic; its order is pinned separately by the plan parity tests)
-    oplan = op.make_plan(M, N, BM, BN, S, c["part"], order=plans[0].export_order())
+    # the oracle computes the execution order itself (an explicit order, or the
+    # R1 swizzle of height 1..3); only swizzle 0 (auto: a library heuristic that
+    # picks a panel height, pinned separately by the plan parity tests) takes
+    # the library's order
+    if c["order"] is None and c["swizzle"] == 0:
+        oplan = op.make_plan(M, N, BM, BN, S, c["part"], order=plans[0].export_order())
+    else:
+        oplan = op.make_plan(M, N, BM, BN, S, c["part"], order=c["order"], swizzle=max(1, c["swizzle"]))
     if c["coll"] == "allreduce":
         lay = "rowband" if plans[0].info["ar_layout"] == 1 else "slot"
         ores = opl.run_allreduce(As, Bts, oplan, layout=lay)

@@ -91,6 +91,50 @@ def test_run_host_matches_device_run():
     ctx.close()
 
 
+def test_run_host_swiglu_and_residual_writeback():
+    """fo_run_host sizes its output by what the GEMM writes (SwiGLU: [m, n/2])
+    and, for FO_POST_ADD_RMSNORM_RESIDUAL with a host residual, copies the
+    updated residual stream back to the caller."""
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    M, N, K = 512, 1024, 256
+    A, Bt = synthetic.float_inputs(M, N, K, seed=14)
+    plan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=4)
+    plan.set_option("gemm_swiglu", 1)
+    guard = 64                                   # host output with a guard band past [m, n/2]
+    buf = torch.full((M * N // 2 + guard,), 7.0, dtype=torch.bfloat16).pin_memory()
+    fo.run_host(ctx, plan, A.pin_memory(), Bt.cuda(), buf[:M * N // 2].view(M, N // 2))
+    torch.cuda.synchronize()
+    dev = torch.empty(M, N // 2, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, A.cuda(), Bt.cuda(), dev)
+    torch.cuda.synchronize()
+    assert torch.equal(buf[:M * N // 2].view(M, N // 2), dev.cpu())
+    assert torch.all(buf[M * N // 2:] == 7.0)     # nothing written past the output
+    with pytest.raises(fo.FOError):
+        p2 = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=4, post="add")
+        p2.set_option("gemm_swiglu", 1)
+    # residual stream write-back
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=4, group_waves=[2],
+                   post="add_rmsnorm_res")
+    res = synthetic.normal_bf16((M, N), 1.0, 16)
+    gam = synthetic.normal_bf16((N,), 1.0, 17)
+    res_h = res.clone().pin_memory()
+    out_h = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    fo.run_host(ctx, plan, A.pin_memory(), Bt.cuda(), out_h, res_h, gam.cuda())
+    torch.cuda.synchronize()
+    res_d = res.cuda()
+    out_d = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, A.cuda(), Bt.cuda(), out_d, res_d, gam.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, out_d.cpu())
+    assert not torch.equal(res_d.cpu(), res)      # the residual stream was updated ...
+    assert torch.equal(res_h, res_d.cpu())        # ... and the host copy with it
+    ctx.close()
+
+
 def test_time_collective_world1():
     from paper_2504_19519_b200 import build
 

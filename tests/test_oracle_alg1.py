@@ -117,3 +117,33 @@ def test_multi_hand_trace_and_monotone():
     # a slower rank never lowers the prediction
     base = alg1.predict_multi((1, 1), [10.0, 10.0], [[4, 4], [4, 4]], lat)
     assert alg1.predict_multi((1, 1), [10.0, 30.0], [[4, 4], [4, 4]], lat) >= base
+
+
+def test_interp_latency_units_by_hand():
+    """Alg. 1 line 14's bytes -> latency conversion, by hand (VERDICT r1 pin):
+    bandwidth in GB/s = 1e9 bytes/s, latency in microseconds."""
+    flat1 = [(1, 1.0), (1 << 40, 1.0)]                        # 1 GB/s everywhere
+    assert alg1.interp_latency_us(flat1, 1e6) == pytest.approx(1000.0, rel=1e-15)      # 1 MB at 1 GB/s = 1 ms
+    assert alg1.interp_latency_us(flat1, 2 ** 20) == pytest.approx(1048.576, rel=1e-15)
+    flat400 = [(1024, 400.0), (1 << 30, 400.0)]
+    assert alg1.interp_latency_us(flat400, 4e6) == pytest.approx(10.0, rel=1e-15)      # 4 MB at 400 GB/s = 10 us
+    assert alg1.interp_latency_us(flat400, 0) == 0.0
+    # on the log-linear curve: 2 KiB sits halfway between 1 KiB @ 10 and 4 KiB @ 30 GB/s -> 20 GB/s
+    assert alg1.interp_latency_us([(1024, 10.0), (4096, 30.0)], 2048) == pytest.approx(2048 / 20e9 * 1e6, rel=1e-15)
+
+
+def test_perfect_overlap_bound_both_branches_by_hand():
+    """"summing up the original GEMM latency and the
+    communication latency of the final wave (if GEMM takes more time), or the
+    GEMM latency of the first wave and the original communication latency (if
+    communication takes more time)" — hand values for both branches."""
+    # GEMM-bound: 100 us GEMM in 4 waves, 40 us of communication, 10 us for the last wave
+    assert alg1.perfect_overlap_bound(100.0, 4, 40.0, 10.0) == 110.0
+    # communication-bound: 40 us GEMM in 4 waves (10 us first wave), 100 us of communication
+    assert alg1.perfect_overlap_bound(40.0, 4, 100.0, 25.0) == 110.0
+    # the GEMM-bound branch is attained by Alg. 1's finest partition when a
+    # wave's communication (10 us) hides under the next wave (25 us)
+    T, dur, per = 4, 100.0, 10.0
+    sizes = alg1.group_bytes((1,) * T, 1, T, 1)
+    assert alg1.predict((1,) * T, dur, T, sizes, lambda b: per * b) == pytest.approx(
+        alg1.perfect_overlap_bound(dur, T, per * T, per))

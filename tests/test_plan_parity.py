@@ -254,6 +254,19 @@ def test_tuner_large_T_uses_dp():
     assert t <= fo.tune_predict([56], 5000.0, 2048, 37, 131072.0, curve) + 1e-9
 
 
+def test_tuner_rejects_empty_pruned_space():
+    """Caps below one wave leave no candidate: an error, never a partition with
+    an infinite prediction (enumeration and DP alike)."""
+    curve = [(2 ** 16, 20.0), (2 ** 28, 600.0)]
+    for T_tiles, S in ((8 * 4, 4), (56 * 37, 37)):             # T = 8 (enumeration), 56 (DP)
+        for s1, sp in ((0, 4), (2, 0)):
+            for prune in (1, 3):
+                with pytest.raises(fo.FOError):
+                    fo.tune_search(100.0, T_tiles, S, 65536.0, curve, s1=s1, sp=sp, prune=prune)
+    with pytest.raises(fo.FOError):
+        fo.tune_search_multi([100.0, 90.0], [[1e6] * 4, [2e6] * 4], curve, s1=0, sp=4, prune=3)
+
+
 def test_tuner_multi_matches_oracle():
     """A2A imbalance extension vs the oracle's predict_multi /
     search_multi; DP (prune 2/3) attains the enumeration's optimum."""
