@@ -297,6 +297,16 @@ def main():
             mean = t.item()
         return mean, ts
 
+    def dist_stats(v):
+        q = sorted(v)
+
+        def pct(f):  # nearest-rank percentile
+            return q[min(len(q) - 1, max(0, int(round(f * (len(q) - 1)))))]
+        return {"mean": round(statistics.mean(q), 2), "median": round(statistics.median(q), 2),
+                "p10": round(pct(0.1), 2), "p90": round(pct(0.9), 2), "n": len(q)}
+
+    stats_out = {}
+
     def timed_multi(fns, steps, warm):
         """Interleaved timing: every iteration runs each variant once (flush +
         barrier + events around each), so all variants see the same clocks."""
@@ -322,6 +332,11 @@ def main():
             t = torch.tensor([means[k] for k in fns], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             means = {k: t[i].item() for i, k in enumerate(fns)}
+            # per-step max over ranks for the distribution statistics
+            ts_t = torch.tensor([ts[k] for k in fns], device="cuda", dtype=torch.float64)
+            dist.all_reduce(ts_t, op=dist.ReduceOp.MAX)
+            ts = {k: ts_t[i].tolist() for i, k in enumerate(fns)}
+        stats_out.update({k: dist_stats(v) for k, v in ts.items()})
         return means
 
     # ---- offline + online stages of Alg. 1 (untimed, tuner.tune_layer): GEMM
@@ -503,9 +518,25 @@ def main():
     flops = 2.0 * M * N * K
     achieved = flops / (gk_us * 1e-6) / 1e12
     peak = peaks["bf16_tflops"]
-    nvlink_gbs = 770.0
-    bus = 2.0 * (world - 1) / world * M * N * 2
-    layer_roof_us = max(flops / (peak * 1e12) * 1e6, bus / (nvlink_gbs * 1e9) * 1e6)
+    # NVLink: the measured peer-copy bandwidth per direction of this pool's
+    # B200s (B200_PROFILING.md: 770 GB/s; 900 GB/s nominal)
+    nvlink_gbs, nvlink_src = 770.0, "measured peer copy per direction, B200_PROFILING.md (900 nominal)"
+    S_B = M * N * 2
+    bus_ring = 2.0 * (world - 1) / world * S_B      # nccl-tests bus bytes of an AllReduce
+    bus_nvls = 1.0 * (world - 1) / world * S_B      # what crosses each link with in-switch reduction
+    gemm_roof_us = flops / (peak * 1e12) * 1e6
+    layer_roof_us = max(gemm_roof_us, bus_ring / (nvlink_gbs * 1e9) * 1e6)
+    layer_roof_nvls_us = max(gemm_roof_us, bus_nvls / (nvlink_gbs * 1e9) * 1e6)
+    # PAPER.md:622 perfect-overlap bound from the measured pieces: the GEMM
+    # (same order, same S) and the collective of the full output / of the last
+    # wave on the library's communicator
+    comm_full_us = ctx.time_collective("allreduce", S_B, 5)
+    last_wave_bytes = (tiles_c - (T - 1) * S) * BMc * BNc * 2
+    comm_last_us = ctx.time_collective("allreduce", last_wave_bytes, 5)
+    if gk_us >= comm_full_us:
+        pob_us = gk_us + comm_last_us
+    else:
+        pob_us = gk_us / T + comm_full_us
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
@@ -535,10 +566,26 @@ def main():
                        "ar_layout": "rowband" if plan.info["ar_layout"] == 1 else "slot",
                        "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"tp{world}",
                        "timing": "device time: CUDA events on the launching stream, pre-loaded by a ~100 us sleep "
-                                 "kernel so host enqueue latency (~12 us per call) is excluded; e2e includes it"},
+                                 "kernel so host enqueue latency (~12 us per call) is excluded; e2e includes it; "
+                                 "value = mean of the timed steps (max over ranks), step_stats_us has median/p10/p90"},
+            "note": ("N=1: the overlapped op is the GEMM followed by a 1-rank NCCL AllReduce that moves no data, so "
+                     "speedup_vs_sequential is ~1 by construction; the multi-rank exchange runs at N>1"
+                     if world == 1 else f"TP={world}: every rank's GEMM overlaps its wave groups' NCCL AllReduce"),
             "speedup_vs_sequential": round(seq_us / ov_us, 4), "sequential_us": round(seq_us, 2),
             "tflops": round(world * flops / (ov_us * 1e-6) / 1e12, 1),
             "layer_roofline_us": round(layer_roof_us, 2), "frac_of_layer_roofline": round(layer_roof_us / ov_us, 4),
+            "layer_roofline": {"gemm_us": round(gemm_roof_us, 2),
+                               "allreduce_ring_us": round(bus_ring / (nvlink_gbs * 1e9) * 1e6, 2),
+                               "allreduce_nvls_us": round(bus_nvls / (nvlink_gbs * 1e9) * 1e6, 2),
+                               "max_ring_us": round(layer_roof_us, 2), "max_nvls_us": round(layer_roof_nvls_us, 2),
+                               "nvlink_gbs": nvlink_gbs, "nvlink_source": nvlink_src,
+                               "tensor_peak_tflops": peak, "tensor_peak_source": f"{peak_src} bf16_tflops (burst)"},
+            "perfect_overlap_bound_us": round(pob_us, 2), "frac_of_perfect_overlap": round(pob_us / ov_us, 4),
+            "perfect_overlap_inputs": {"gemm_us": round(gk_us, 2), "comm_full_us": round(comm_full_us, 2),
+                                       "comm_last_wave_us": round(comm_last_us, 2), "waves": T,
+                                       "rule": "PAPER.md:622: GEMM + last-wave comm if GEMM-bound, else "
+                                               "first-wave GEMM + full comm"},
+            "step_stats_us": {k: stats_out.get(k) for k in ("ov", "seq", "gemm", "cublas")},
             "alg1_predicted_us": round(pred, 2), "spot_check": spot,
             "fused_add_rmsnorm": {"overlapped_us": round(m["ov_norm"], 2), "sequential_us": round(m["seq_norm"], 2),
                                   "speedup": round(m["seq_norm"] / m["ov_norm"], 4), "groups": list(groups_n),
@@ -552,6 +599,9 @@ def main():
                                       "the collective (as in the sequential form)")},
             "roofline": {"bound": "tensor", "kernel": f"fo_gemm_tcgen05_kernel<{BNc},{cgc}>", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed "
+                                           "ncu --set full capture of this shape/plan (profiles/gemm_traffic.json)"
+                                           if traffic else None,
                          "peak_source": f"{peak_src} bf16_tflops (burst; kernel timed alone per step)",
                          "frac_of_sustained_peak": round(achieved / peaks.get("bf16_tflops_sustained", peak), 4),
                          "kernel_us": round(gk_us, 2), "flops_per_launch": flops,

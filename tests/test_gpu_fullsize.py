@@ -7,10 +7,15 @@ one GPU through fo_gemm_stage; the collective between them is emulated on the
 GPU by this test as NCCL's ring computes a bf16 sum — the bf16 partials added
 one rank at a time, rounded to bf16 after every hop — over the plan's group
 ranges, and each receiver's post-reorder runs through fo_post_stage.  The
-result is held to (a) the first-order rounding bound of that summation against
-the unrounded fp64 definition, |g - o| <= u (sum_r |p_r| + sum_k |s_k|)
-(u = 2^-9, p_r the fp64 partials, s_k the computed running sums), and (b) the
-north_star 1e-2 against the oracle in its bf16-epilogue model (R11).
+result is held to (a) the first-order rounding bound of the whole computation
+against the unrounded fp64 definition, |g - o| <= u (sum_r |p_r| + sum_k |s_k|)
++ K 2^-23 sum_r |A_r||B_r|^T (u = 2^-9, p_r the fp64 partials, s_k the
+computed running sums of the ring, the last term each rank's fp32
+accumulation over its K products), and (b) the
+north_star 1e-2 against the oracle in its bf16 model of the same arithmetic
+(bf16 partials, bf16 after every ring hop; R11).  Against the plain
+fp64 definition the TP=8 error is printed, not asserted: a bf16 ring sum of 8
+partials exceeds 1e-2 at the tails by itself (R11).
 The single-rank bench configuration runs through fo_run with the real NCCL.
 """
 import numpy as np
@@ -39,26 +44,42 @@ def _dev():
 U = 2.0 ** -9  # bf16 unit roundoff
 
 
-def _check_rows(got_rows, want_rows, partials=None, running=None):
+def _check_rows(got_rows, want_rows, partials=None, running=None, absprod=None, K=0):
     """Tolerance check (R10/R11).
 
     want_rows: the oracle value (fp64).  With `partials` (per-rank fp64 values)
     the oracle is taken in its bf16-epilogue model (each rank's partial rounded
-    to bf16, R10: the send buffer is bf16 by construction) for the 1e-2 metric,
+    to bf16, R10: the send buffer is bf16 by construction; with `running`, also
+    the ring's bf16 rounding after every hop, in rank order) for the 1e-2 metric,
     and the unrounded fp64 definition is held to the elementwise first-order
     bound of the emulated bf16 ring sum: |g - o| <= u (sum_r |p_r| + sum_k
     |s_k|), `running` = sum_k |s_k| over the computed running sums (without it,
-    one rounding of the total: u (sum_r |p_r| + |o|))."""
+    one rounding of the total: u (sum_r |p_r| + |o|)), plus the fp32
+    accumulation of each rank's K products, K 2^-23 sum_r (|A_r| |B_r|^T)
+    (`absprod`; 2^-23 allows a truncating accumulator)."""
     g = got_rows.double().cpu().numpy() if isinstance(got_rows, torch.Tensor) else got_rows
     o = np.asarray(want_rows, np.float64)
     if partials is not None:
         absum = np.zeros_like(o)
-        model = np.zeros_like(o)
+        model = None
         for p in partials:
             absum += np.abs(p)
-            model += onum.round_bf16(p)
+            q = onum.round_bf16(p)
+            if model is None:
+                model = q
+            elif running is not None:            # NCCL's ring: bf16 after every hop
+                model = onum.round_bf16(model + q)
+            else:
+                model = model + q
         bound = 1.01 * U * (absum + (running if running is not None else np.abs(o)))
-        assert np.all(np.abs(g - o) <= bound), "outside the bf16 rounding bound of the plain definition"
+        if absprod is not None:
+            bound += 1.01 * K * 2.0 ** -23 * absprod
+        ratio = np.max(np.abs(g - o) / bound)
+        print(f"  |g - o| / rounding bound: max {ratio:.3f}")
+        assert ratio <= 1.0, "outside the bf16 rounding bound of the plain definition"
+        rms0 = np.sqrt(np.mean(o * o))
+        print(f"  max rel err vs the plain fp64 definition (no tolerance; DESIGN.md R11): "
+              f"{np.max(np.abs(g - o) / np.maximum(np.abs(o), rms0)):.3e}")
         del absum, bound
         o = model
     rms = np.sqrt(np.mean(o * o))
@@ -82,6 +103,15 @@ def _ring_sum(sends):
 def _gemm_full(A, Bt):
     """fp64 oracle GEMM of a whole (CPU) operand pair."""
     return onum.gemm(A.cpu() if isinstance(A, torch.Tensor) else A, Bt.cpu() if isinstance(Bt, torch.Tensor) else Bt)
+
+
+def _absprod(As, Bts):
+    """sum_r |A_r| |B_r|^T in fp64 (the scale of the fp32 accumulation error)."""
+    out = None
+    for A, Bt in zip(As, Bts):
+        x = _gemm_full(A.abs(), Bt.abs())
+        out = x if out is None else out + x
+    return out
 
 
 def test_c2_bench_config_tp1_fo_run():
@@ -120,13 +150,14 @@ def test_c2_tp8_allreduce(layout):
     del sends
     parts = [_gemm_full(As[r], Bts[r]) for r in range(n)]
     want = sum(parts)
+    absprod = _absprod(As, Bts)
     for r in (0, n - 1):
         out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plans[r], recv, out)
         torch.cuda.synchronize()
         # the running sums live in send-buffer order: bring them to C's order
         run_c = running[plans[r].export_send_map()].reshape(M, N)
-        err = _check_rows(out, want, parts, run_c)
+        err = _check_rows(out, want, parts, run_c, absprod, K)
         print(f"TP=8 AllReduce ({layout}), rank {r}: max rel err vs the bf16-epilogue model {err:.3e}")
 
 
@@ -162,7 +193,7 @@ def test_c3_tp8_reducescatter():
         grows = [orr.rs_local_to_global_row(l, BM, h, k) for l in range(M // n)]
         parts = [_gemm_full(As[r][grows], Bts[r]) for r in range(n)]
         run_c = running[plans[k].export_send_map()].reshape(M, N)[grows]
-        err = _check_rows(out, sum(parts), parts, run_c)
+        err = _check_rows(out, sum(parts), parts, run_c, _absprod([A[grows] for A in As], Bts), K)
         print(f"TP=8 ReduceScatter, rank {k}: max rel err vs the bf16-epilogue model {err:.3e}")
 
 
