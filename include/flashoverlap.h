@@ -346,6 +346,12 @@ fo_status fo_gemm_stage(fo_plan plan, const void* A, const void* Bt, void* send,
  * pattern evidence, the analogue of PAPER.md:230 fig:wave). */
 fo_status fo_gemm_stage_timed(fo_plan plan, const void* A, const void* Bt, void* send,
                               unsigned long long* tile_ts, void* stream);
+/* Run only wave group j's post-communication reorder (the per-group pass of
+ * fo_run: slot / RS / A2A layouts, post none or add) from a caller device
+ * receive buffer of info.recv_elems bf16; the rows of group j in `out` are
+ * written.  FO_ERR_UNSUPPORTED for other layouts / ops. */
+fo_status fo_group_post_stage(fo_plan plan, int32_t j, const void* recv, void* out, const void* residual,
+                              void* stream);
 /* Run only the post-communication reorder (+ fused op) from a caller device
  * receive buffer of info.recv_elems bf16. */
 fo_status fo_post_stage(fo_plan plan, const void* recv, void* out, const void* residual,

@@ -346,6 +346,11 @@ def post_stage(plan: Plan, recv, out, residual=None, gamma=None, stream=None):
     check(load().fo_post_stage(plan.handle, _ptr(recv), _ptr(out), _ptr(residual), _ptr(gamma), _stream(stream)))
 
 
+def group_post_stage(plan: Plan, j: int, recv, out, residual=None, stream=None):
+    """fo_group_post_stage: wave group j's post-reorder alone (the per-group pass of fo_run)."""
+    check(load().fo_group_post_stage(plan.handle, int(j), _ptr(recv), _ptr(out), _ptr(residual), _stream(stream)))
+
+
 def kernel_launch_count() -> int:
     return int(load().fo_kernel_launch_count())
 

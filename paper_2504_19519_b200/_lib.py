@@ -98,6 +98,7 @@ _SIGS = [
     ("fo_gemm_stage", C.c_int, [_P, _P, _P, _P, _P]),
     ("fo_gemm_stage_timed", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("fo_post_stage", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("fo_group_post_stage", C.c_int, [_P, C.c_int32, _P, _P, _P, _P]),
     ("fo_combine_stage", C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     ("fo_run_combine", C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     ("fo_plan_read_counters", C.c_int, [_P, C.POINTER(C.c_uint32)]),

@@ -171,6 +171,7 @@ static void ensure_device(fo_plan_s* p) {
   if (h.S * (h.BM / 128) > sms)
     fail(FO_ERR_INVALID_ARG, "workers=%d x %d CTAs exceeds the %d SMs (waves would not be resident)", h.S,
          h.BM / 128, sms);
+  p->free_sms = sms - h.S * (h.BM / 128);
   int major = 0, minor = 0;
   FO_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
   FO_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
@@ -498,7 +499,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
     a.sub_end = (j + 1 < h.P) ? h.recv_off[(size_t)(j + 1) * W] : h.recv_elems / h.BN;
   }
   a.recv_dst = p->d_recv_dst;
-  a.grid_cap = 0;  // default: 4 blocks per SM
+  a.grid_cap = 0;  // default: 4 blocks per SM (warp kernel) / one per SM (bulk kernel)
   a.smem_pad = p->post_sm_partition ? kPartitionSmem : 0;
   FO_CUDA(launch_group_post(a, s));
 }
@@ -1111,6 +1112,20 @@ fo_status fo_gemm_stage_timed(fo_plan p, const void* A, const void* Bt, void* se
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
     run_gemm(p, A, Bt, send, epi_mode(p->host), true, s, tile_ts);
+  });
+}
+
+fo_status fo_group_post_stage(fo_plan p, int32_t j, const void* recv, void* out, const void* residual,
+                              void* stream) {
+  return guard([&] {
+    if (!p || !recv || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    const PlanHost& h = p->host;
+    if (j < 0 || j >= h.P) fail(FO_ERR_INVALID_ARG, "group %d out of range", j);
+    const int map = post_map(h);
+    if (map == POSTMAP_IDENTITY || !(h.post == FO_POST_NONE || h.post == FO_POST_ADD))
+      fail(FO_ERR_UNSUPPORTED, "per-group post pass needs a slot / RS / A2A layout and post none or add");
+    ensure_device(p);
+    run_group_post(p, j, recv, out, residual, nullptr, reinterpret_cast<cudaStream_t>(stream));
   });
 }
 

@@ -52,6 +52,7 @@ struct fo_plan_s {
   int wait_kernel = 0;                            // 0 cuStreamWaitValue32, 1 spin-wait kernel
   int last_in_order = 1;                          // last group's collective on the caller stream after the GEMM
   int post_sm_partition = 0;                      // FO_OPT_POST_SM_PARTITION
+  int free_sms = 0;                               // SMs the persistent GEMM leaves free (set by ensure_device)
   int tail_split_req = 0;                         // FO_OPT_TAIL_SPLIT: 0/1 off, >=2 slices, -1 auto, -2 stream-K
   // ---- resolved tail split (set by ensure_device)
   int split = 1, tail_pos = 0, units = 0;
