@@ -358,6 +358,7 @@ def main():
             spec["options"] = {"tail_split": args.tail_split}
         nspec = dict(spec, post="add_rmsnorm")
         pred_n = pred
+        curve_bw = None
     else:
         shapes = [(BM, BN), (128, 256)]      # CTA-pair 256x256 and single-CTA 128x256 tiles
         ch = fot.tune_layer(M, N, K, ctx, "allreduce", "none", device=local, tile_shapes=shapes)
@@ -369,6 +370,7 @@ def main():
                           f"predicted {cand[3]:.1f} us" + (f", measured {cand[5]:.1f} us" if len(cand) > 5 else ""),
                           file=sys.stderr)
         S, groups, pred = ch.workers, tuple(ch.groups), ch.predicted_us
+        curve_bw = ch.curve
         spec, nspec, pred_n = ch.spec(M, N, K, "allreduce"), chn.spec(M, N, K, "allreduce", "add_rmsnorm"), \
             chn.predicted_us
     # the chosen tile shape (tune_layer searches it; the explicit --workers /
@@ -586,6 +588,10 @@ def main():
                                        "rule": "PAPER.md:622: GEMM + last-wave comm if GEMM-bound, else "
                                                "first-wave GEMM + full comm"},
             "step_stats_us": {k: stats_out.get(k) for k in ("ov", "seq", "gemm", "cublas")},
+            "nccl_allreduce_curve": ({"unit": "bytes, algbw GB/s, busbw GB/s (nccl-tests convention)",
+                                      "comm": f"library communicator, maxCTAs={comm_sms if world > 1 else 'default'}",
+                                      "points": [[int(b), round(a, 1), round(bb, 1)] for b, a, bb in curve_bw]}
+                                     if curve_bw else None),
             "alg1_predicted_us": round(pred, 2), "spot_check": spot,
             "fused_add_rmsnorm": {"overlapped_us": round(m["ov_norm"], 2), "sequential_us": round(m["seq_norm"], 2),
                                   "speedup": round(m["seq_norm"] / m["ov_norm"], 4), "groups": list(groups_n),

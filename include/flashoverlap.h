@@ -211,6 +211,41 @@ fo_status fo_get_unique_id(uint8_t uid[128]);
  * GEMM leaves free; 0 = NCCL default.  Collective over the ranks. */
 fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128],
                         int32_t nccl_max_ctas, fo_ctx* out);
+/* Communicator configuration of fo_ctx_create_config (all 0 = NCCL defaults,
+ * plain buffers; fo_ctx_create(..., max) = {max, 0, 0, 0, 0}).
+ *   nccl_max_ctas / nccl_min_ctas  ncclConfig_t.maxCTAs / minCTAs: the CTAs
+ *       NCCL may use, sized to the SMs the persistent GEMM leaves free
+ *       (R18);
+ *   cta_policy  ncclConfig_t.CTAPolicy: 0 default, 1 NCCL_CTA_POLICY_EFFICIENCY
+ *       (fewest CTAs that keep the bandwidth), 2 NCCL_CTA_POLICY_ZERO;
+ *   nvls_ctas   ncclConfig_t.nvlsCTAs (CTAs of the NVLS in-switch reduction);
+ *   buffers     0: plans allocate their send / receive buffers with
+ *       cudaMalloc; 1: with ncclMemAlloc, registered with the communicator
+ *       (ncclCommRegister: zero-copy / NVLS-capable buffers);
+ *       2: ncclMemAlloc + ncclCommWindowRegister (NCCL_WIN_COLL_SYMMETRIC for
+ *       AllReduce / ReduceScatter plans, whose buffers have the same size on
+ *       every rank).  A plan's buffers are allocated and registered for the
+ *       context it first runs with (collective: every rank's first run of the
+ *       plan); running it with another context is FO_ERR_STATE.  The
+ *       registrations are released by fo_plan_destroy or fo_ctx_destroy,
+ *       whichever comes first. */
+typedef struct {
+  int32_t nccl_max_ctas;
+  int32_t nccl_min_ctas;
+  int32_t cta_policy;
+  int32_t nvls_ctas;
+  int32_t buffers;
+} fo_ctx_config;
+fo_status fo_ctx_create_config(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128],
+                               const fo_ctx_config* config, fo_ctx* out);
+/* Device memory for a caller buffer NCCL will read / write (e.g. the `out` of
+ * an AllReduce ROWBAND plan, reduced in place): ncclMemAlloc, registered with
+ * the context's communicator per its `buffers` mode (none for mode 0).
+ * fo_mem_free deregisters and frees (synchronises the device).  Window
+ * registration (mode 2) is collective: every rank allocates the same size in
+ * the same order. */
+fo_status fo_mem_alloc(fo_ctx ctx, int64_t bytes, void** ptr);
+fo_status fo_mem_free(fo_ctx ctx, void* ptr);
 /* Create a context on an EXISTING NCCL communicator (an ncclComm_t passed as
  * void*, e.g. torch's ProcessGroupNCCL::_comm_ptr()): rank and world are read
  * from it (ncclCommUserRank / ncclCommCount); it must live on `device`
@@ -250,9 +285,13 @@ fo_status fo_ctx_create_loopback(void* group, int32_t rank, fo_ctx* out);
 /* Offline stage of the tuner ("the bandwidth curve is sampled
  * with multiple dense points"): average latency of one `coll` (AllReduce in
  * place, ReduceScatter, or equal-split All-to-All) of `bytes` total message
- * bytes on the context's own communicator and comm stream (its CTA cap
- * included).  Collective; synchronises the host (tuning only). */
-fo_status fo_ctx_time_collective(fo_ctx ctx, int32_t coll, int64_t bytes, int32_t iters, double* avg_us);
+ * bytes on the context's own communicator and comm stream (its CTA cap and
+ * buffer registration included), and (busbw_gbps, may be NULL) the bus
+ * bandwidth in the nccl-tests convention: AllReduce 2(n-1)/n x bytes,
+ * ReduceScatter / All-to-All (n-1)/n x bytes, per second.  Collective;
+ * synchronises the host (tuning only). */
+fo_status fo_ctx_time_collective(fo_ctx ctx, int32_t coll, int64_t bytes, int32_t iters, double* avg_us,
+                                 double* busbw_gbps);
 
 /* ---------------------------------------------------------------- the overlapped op */
 /* MoE combine fused into the All-to-All post-reorder (R31; the A2A
@@ -374,7 +413,8 @@ fo_status fo_plan_gemm_cluster(fo_plan plan, int32_t* cluster_ctas);
  * one; the run's output is undefined), and FO_ERR_TIMEOUT is returned.
  * Host-blocking; not graph-capturable. */
 fo_status fo_plan_sync(fo_ctx ctx, fo_plan plan, void* stream, int64_t timeout_ms);
-/* Bind the plan to the current device and allocate, now, the device state its
+/* Bind the plan to the current device (and, ctx != NULL, to that context: its
+ * buffer registration, as on a first fo_run) and allocate, now, the device state its
  * runs would otherwise allocate on first use: tables, counters, the send /
  * receive buffers (always), the row-major scratch of fo_run_sequential /
  * fo_run_allgather for RS / A2A plans (what & 1), and the staging buffers of
@@ -382,7 +422,7 @@ fo_status fo_plan_sync(fo_ctx ctx, fo_plan plan, void* stream, int64_t timeout_m
  * plan allocates (CUDA-graph capture; multi-rank issue where one rank's
  * allocation must not wait on another rank's in-flight collective).
  * Synchronises the device. */
-fo_status fo_plan_prepare(fo_plan plan, int32_t what);
+fo_status fo_plan_prepare(fo_ctx ctx, fo_plan plan, int32_t what);
 /* Copy the plan's P counters to host (synchronises the device). */
 fo_status fo_plan_read_counters(fo_plan plan, uint32_t* counters);
 /* Debug / evidence hooks (tests, tools; never needed for correct use):

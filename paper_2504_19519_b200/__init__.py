@@ -156,10 +156,12 @@ class Plan:
         check(load().fo_plan_read_counters(self._h, c.ctypes.data_as(C.POINTER(C.c_uint32))))
         return c
 
-    def prepare(self, sequential: bool = True, host: bool = False):
+    def prepare(self, sequential: bool = True, host: bool = False, ctx: "Optional[Context]" = None):
         """fo_plan_prepare: allocate the plan's device state now (tables,
-        buffers; the sequential / allgather scratch; fo_run_host staging)."""
-        check(load().fo_plan_prepare(self._h, (1 if sequential else 0) | (2 if host else 0)))
+        buffers — registered with `ctx`'s communicator when it registers; the
+        sequential / allgather scratch; fo_run_host staging)."""
+        check(load().fo_plan_prepare(ctx._h if ctx is not None else None, self._h,
+                                     (1 if sequential else 0) | (2 if host else 0)))
 
     def gemm_cluster(self) -> int:
         """CTAs per cluster of the plan's GEMM launch on the current device (1, 2, 4)."""
@@ -207,11 +209,36 @@ class Context:
         self._h, self.device, self.rank, self.world = handle, device, rank, world
 
     @classmethod
-    def create(cls, device: int, rank: int, world: int, uid: bytes, nccl_max_ctas: int = 0) -> "Context":
+    def create(cls, device: int, rank: int, world: int, uid: bytes, nccl_max_ctas: int = 0, nccl_min_ctas: int = 0,
+               cta_policy: str = "default", nvls_ctas: int = 0, buffers: str = "plain") -> "Context":
+        """fo_ctx_create_config: the library's NCCL communicator (CTA caps,
+        CTA policy, NVLS CTAs) and the buffer registration mode of its plans
+        ("plain" cudaMalloc, "registered" ncclMemAlloc + ncclCommRegister,
+        "window" ncclMemAlloc + symmetric window registration)."""
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        cfg = _lib.CtxConfigC(int(nccl_max_ctas), int(nccl_min_ctas), _lib.CTA_POLICY[cta_policy], int(nvls_ctas),
+                              _lib.BUFFERS[buffers])
         h = C.c_void_p()
-        check(load().fo_ctx_create(device, rank, world, buf, nccl_max_ctas, C.byref(h)))
-        return cls(h, device, rank, world)
+        check(load().fo_ctx_create_config(device, rank, world, buf, C.byref(cfg), C.byref(h)))
+        ctx = cls(h, device, rank, world)
+        ctx.buffers = buffers
+        return ctx
+
+    def mem_alloc(self, shape, dtype=None):
+        """A torch tensor on device memory from fo_mem_alloc (ncclMemAlloc,
+        registered per the context's buffer mode); freed with the tensor's
+        last reference through fo_mem_free."""
+        import torch
+        dtype = dtype or torch.bfloat16
+        n = 1
+        for d in shape:
+            n *= int(d)
+        nbytes = n * torch.empty(0, dtype=dtype).element_size()
+        ptr = C.c_void_p()
+        check(load().fo_mem_alloc(self._h, int(nbytes), C.byref(ptr)))
+        holder = _DeviceBuf(self, ptr.value, tuple(int(d) for d in shape), dtype)
+        t = torch.as_tensor(holder, device=torch.device("cuda", self.device))
+        return t.view(dtype) if dtype == torch.bfloat16 else t
 
     @classmethod
     def from_comm(cls, device: int, nccl_comm: int, rank=None, world=None) -> "Context":
@@ -230,11 +257,26 @@ class Context:
         check(load().fo_ctx_create_loopback(group.handle, int(rank), C.byref(h)))
         return cls(h, group.device, rank, group.world)
 
+    def time_collective_bw(self, coll: str, nbytes: int, iters: int = 5):
+        """(average us, bus GB/s) of one collective of `nbytes` (fo_ctx_time_collective)."""
+        out, bw = C.c_double(), C.c_double()
+        check(load().fo_ctx_time_collective(self._h, COLL[coll], int(nbytes), int(iters), C.byref(out), C.byref(bw)))
+        return out.value, bw.value
+
     def time_collective(self, coll: str, nbytes: int, iters: int = 5) -> float:
         """Average us of one collective of `nbytes` on this context's communicator (tuning)."""
         out = C.c_double()
-        check(load().fo_ctx_time_collective(self._h, COLL[coll], int(nbytes), int(iters), C.byref(out)))
+        check(load().fo_ctx_time_collective(self._h, COLL[coll], int(nbytes), int(iters), C.byref(out), None))
         return out.value
+
+    def sample_curve_bw(self, coll: str, sizes=None, iters: int = 5):
+        """(bytes, algorithm GB/s, bus GB/s) samples of `coll` on this communicator."""
+        sizes = sizes or [1 << s for s in range(16, 28)]
+        out = []
+        for sz in sizes:
+            us, bus = self.time_collective_bw(coll, sz, iters)
+            out.append((sz, sz / (us * 1e-6) / 1e9, bus))
+        return out
 
     def sample_curve(self, coll: str, sizes=None, iters: int = 5):
         """(bytes, GB/s) samples of `coll` on this communicator (Alg. 1 line 5)."""
@@ -245,6 +287,25 @@ class Context:
         if getattr(self, "_h", None) and self._h.value:
             check(load().fo_ctx_destroy(self._h))
             self._h = C.c_void_p()
+
+
+class _DeviceBuf:
+    """__cuda_array_interface__ view of an fo_mem_alloc buffer; frees it (fo_mem_free) when collected."""
+
+    def __init__(self, ctx, ptr, shape, dtype):
+        import torch
+        self.ctx, self.ptr = ctx, ptr
+        # bf16 has no array-interface type string: exposed as int16, viewed back by mem_alloc
+        typestr = {torch.bfloat16: "<i2", torch.float16: "<f2", torch.float32: "<f4", torch.int32: "<i4"}[dtype]
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3}
+        self._dtype = dtype
+
+    def __del__(self):
+        try:
+            if self.ctx._h and self.ctx._h.value:
+                load().fo_mem_free(self.ctx._h, C.c_void_p(self.ptr))
+        except Exception:
+            pass
 
 
 class LoopbackGroup:

@@ -55,6 +55,15 @@ class PlanInfoC(C.Structure):
     ]
 
 
+class CtxConfigC(C.Structure):
+    _fields_ = [("nccl_max_ctas", C.c_int32), ("nccl_min_ctas", C.c_int32), ("cta_policy", C.c_int32),
+                ("nvls_ctas", C.c_int32), ("buffers", C.c_int32)]
+
+
+CTA_POLICY = {"default": 0, "efficiency": 1, "zero": 2}
+BUFFERS = {"plain": 0, "registered": 1, "window": 2}
+
+
 class CommCallC(C.Structure):
     _fields_ = [("kind", C.c_int32), ("group", C.c_int32), ("peer", C.c_int32), ("src_buf", C.c_int32),
                 ("dst_buf", C.c_int32), ("reserved", C.c_int32), ("src_off", C.c_int64), ("dst_off", C.c_int64),
@@ -89,7 +98,12 @@ _SIGS = [
     ("fo_loopback_create", C.c_int, [C.c_int32, C.c_int32, C.POINTER(_P)]),
     ("fo_loopback_destroy", C.c_int, [_P]),
     ("fo_ctx_create_loopback", C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
-    ("fo_ctx_time_collective", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double)]),
+    ("fo_ctx_time_collective", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]),
+    ("fo_ctx_create_config", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint8),
+                                       C.POINTER(CtxConfigC), C.POINTER(_P)]),
+    ("fo_mem_alloc", C.c_int, [_P, C.c_int64, C.POINTER(_P)]),
+    ("fo_mem_free", C.c_int, [_P, _P]),
     ("fo_run", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_sequential", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("fo_run_host", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
@@ -102,7 +116,7 @@ _SIGS = [
     ("fo_combine_stage", C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     ("fo_run_combine", C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int64, _P, _P]),
     ("fo_plan_read_counters", C.c_int, [_P, C.POINTER(C.c_uint32)]),
-    ("fo_plan_prepare", C.c_int, [_P, C.c_int32]),
+    ("fo_plan_prepare", C.c_int, [_P, _P, C.c_int32]),
     ("fo_plan_gemm_cluster", C.c_int, [_P, C.POINTER(C.c_int32)]),
     ("fo_plan_sync", C.c_int, [_P, _P, _P, C.c_int64]),
     ("fo_kernel_launch_count", C.c_int64, []),

@@ -44,6 +44,17 @@ struct fo_ctx_s {
   cudaStream_t h2d_stream[2] = {nullptr, nullptr}, d2h_stream = nullptr;
   cudaEvent_t ev_h2d_fork = nullptr, ev_h2d_join[2] = {nullptr, nullptr}, ev_d2h_join = nullptr;
   std::vector<cudaEvent_t> ev_d2h;     // group j's output final (grown on demand)
+  // NCCL buffer registration (fo_ctx_config.buffers): 0 plain cudaMalloc,
+  // 1 ncclMemAlloc + ncclCommRegister, 2 ncclMemAlloc + window registration
+  int mem_mode = 0;
+  std::vector<fo_plan_s*> reg_plans;   // plans whose buffers are registered with this context's comm
+  struct UserBuf {
+    void* ptr;
+    size_t bytes;
+    void* handle;                      // ncclCommRegister handle
+    ncclWindow_t win;
+  };
+  std::vector<UserBuf> user_bufs;      // fo_mem_alloc
 };
 
 namespace fo {
@@ -136,12 +147,39 @@ static T* upload(const std::vector<T>& v) {
   return d;
 }
 
+// Undo the NCCL registration of a plan's send / receive buffers (the
+// registering context's communicator must still be alive).
+static void deregister_plan(fo_plan_s* p) {
+  fo_ctx_s* c = p->reg_ctx;
+  if (!c) return;
+  ncclComm_t comm = c->comm ? c->comm->nccl() : nullptr;
+  if (comm) {
+    for (void* h : {p->reg_send, p->reg_recv})
+      if (h) ncclCommDeregister(comm, h);
+    for (ncclWindow_t w : {p->win_send, p->win_recv})
+      if (w) ncclCommWindowDeregister(comm, w);
+  }
+  p->reg_send = p->reg_recv = nullptr;
+  p->win_send = p->win_recv = nullptr;
+  auto& v = c->reg_plans;
+  v.erase(std::remove(v.begin(), v.end(), p), v.end());
+  p->reg_ctx = nullptr;
+}
+
 void release_device(fo_plan_s* p) {
   if (p->device < 0) return;
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(p->device);
+  deregister_plan(p);
   if (p->d_recv == p->d_send) p->d_recv = nullptr;  // aliased at world 1
+  if (p->nccl_mem) {  // send / receive buffers from ncclMemAlloc
+    for (void*& b : {std::ref(p->d_send), std::ref(p->d_recv)})
+      if (b) {
+        ncclMemFree(b);
+        b = nullptr;
+      }
+  }
   for (cudaEvent_t& e : p->ev_set_done)
     if (e) {
       cudaEventDestroy(e);
@@ -290,13 +328,45 @@ static void ensure_device(fo_plan_s* p) {
   FO_CUDA(cudaMemset(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words));
   p->d_flags = p->d_counters + h.P;
   const bool need_send = !(h.coll == FO_NOCOMM || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND));
-  if (need_send && h.send_elems) FO_CUDA(cudaMalloc(&p->d_send, 2 * h.send_elems));
+  // the buffers NCCL reads and writes: plain device memory, or (a context
+  // configured for registration) ncclMemAlloc'd so NCCL can register them
+  // for zero-copy / NVLS
+  p->nccl_mem = p->mem_mode > 0;
+  auto alloc = [&](void** b, size_t bytes) {
+    if (p->nccl_mem) FO_NCCL(ncclMemAlloc(b, bytes));
+    else FO_CUDA(cudaMalloc(b, bytes));
+  };
+  if (need_send && h.send_elems) alloc(&p->d_send, 2 * h.send_elems);
   if ((h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && h.recv_elems) {
     // one rank: the receive layout ([group][source 0]) is the send layout, so
     // the collective runs in place (no copy)
     if (h.world == 1) p->d_recv = p->d_send;
-    else FO_CUDA(cudaMalloc(&p->d_recv, 2 * h.recv_elems));
+    else alloc(&p->d_recv, 2 * h.recv_elems);
   }
+}
+
+// Bind a plan to the context it first runs with (its buffers are allocated for
+// that context's registration mode) and register its send / receive buffers
+// with the context's communicator.  Window registration is collective: every
+// rank's first run of the plan (itself collective) performs it.
+static void bind_ctx(fo_ctx_s* c, fo_plan_s* p) {
+  if (p->device < 0) p->mem_mode = c->comm && c->comm->nccl() ? c->mem_mode : 0;
+  ensure_device(p);
+  if (p->mem_mode == 0 || p->reg_ctx == c) return;
+  if (p->reg_ctx) fail(FO_ERR_STATE, "plan's buffers are registered with another context");
+  ncclComm_t comm = c->comm ? c->comm->nccl() : nullptr;
+  if (!comm) return;
+  const PlanHost& h = p->host;
+  const bool sym = p->mem_mode == 2 && h.coll != FO_ALLTOALL;  // equal sizes on every rank
+  auto reg = [&](void* b, size_t bytes, void** handle, ncclWindow_t* win) {
+    if (!b || !bytes) return;
+    if (p->mem_mode == 2) FO_NCCL(ncclCommWindowRegister(comm, b, bytes, win, sym ? NCCL_WIN_COLL_SYMMETRIC : 0));
+    else FO_NCCL(ncclCommRegister(comm, b, bytes, handle));
+  };
+  reg(p->d_send, 2 * (size_t)h.send_elems, &p->reg_send, &p->win_send);
+  if (p->d_recv != p->d_send) reg(p->d_recv, 2 * (size_t)h.recv_elems, &p->reg_recv, &p->win_recv);
+  p->reg_ctx = c;
+  c->reg_plans.push_back(p);
 }
 
 static bool is_rmsnorm(int post) { return post == FO_POST_ADD_RMSNORM || post == FO_POST_ADD_RMSNORM_RESIDUAL; }
@@ -603,24 +673,34 @@ fo_status fo_get_unique_id(uint8_t uid[128]) {
   });
 }
 
-fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128], int32_t nccl_max_ctas,
-                        fo_ctx* out) {
+fo_status fo_ctx_create_config(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128],
+                               const fo_ctx_config* config, fo_ctx* out) {
   return guard([&] {
     if (!uid || !out || world < 1 || rank < 0 || rank >= world) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    fo_ctx_config k{};
+    if (config) k = *config;
+    if (k.nccl_max_ctas < 0 || k.nccl_min_ctas < 0 || k.nvls_ctas < 0 || k.cta_policy < 0 || k.cta_policy > 2 ||
+        k.buffers < 0 || k.buffers > 2)
+      fail(FO_ERR_INVALID_ARG, "bad fo_ctx_config");
     FO_CUDA(cudaSetDevice(device));
     auto* c = new fo_ctx_s();
     c->device = device;
     c->rank = rank;
     c->world = world;
+    c->mem_mode = k.buffers;
     try {
       ncclUniqueId id;
       std::memcpy(&id, uid, 128);
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
       cfg.blocking = 1;
-      if (nccl_max_ctas > 0) {
-        cfg.maxCTAs = nccl_max_ctas;
-        cfg.minCTAs = 1;
+      if (k.nccl_max_ctas > 0) {
+        cfg.maxCTAs = k.nccl_max_ctas;
+        cfg.minCTAs = k.nccl_min_ctas > 0 ? std::min(k.nccl_min_ctas, k.nccl_max_ctas) : 1;
+      } else if (k.nccl_min_ctas > 0) {
+        cfg.minCTAs = k.nccl_min_ctas;
       }
+      if (k.cta_policy > 0) cfg.CTAPolicy = k.cta_policy == 1 ? NCCL_CTA_POLICY_EFFICIENCY : NCCL_CTA_POLICY_ZERO;
+      if (k.nvls_ctas > 0) cfg.nvlsCTAs = k.nvls_ctas;
       ncclComm_t comm = nullptr;
       FO_NCCL(ncclCommInitRankConfig(&comm, world, id, rank, &cfg));
       c->comm = make_nccl_comm(comm, rank, world, true);
@@ -632,6 +712,13 @@ fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8
     }
     *out = c;
   });
+}
+
+fo_status fo_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128], int32_t nccl_max_ctas,
+                        fo_ctx* out) {
+  fo_ctx_config k{};
+  k.nccl_max_ctas = nccl_max_ctas;
+  return fo_ctx_create_config(device, rank, world, uid, &k, out);
 }
 
 fo_status fo_ctx_create_from_comm(int32_t device, void* nccl_comm, fo_ctx* out) {
@@ -703,6 +790,15 @@ fo_status fo_ctx_destroy(fo_ctx c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    cudaDeviceSynchronize();
+    while (!c->reg_plans.empty()) deregister_plan(c->reg_plans.back());
+    for (auto& b : c->user_bufs) {
+      ncclComm_t comm = c->comm ? c->comm->nccl() : nullptr;
+      if (comm && b.handle) ncclCommDeregister(comm, b.handle);
+      if (comm && b.win) ncclCommWindowDeregister(comm, b.win);
+      ncclMemFree(b.ptr);
+    }
+    c->user_bufs.clear();
     delete c->comm;
     c->comm = nullptr;
     if (c->post_stream) cudaStreamSynchronize(c->post_stream);
@@ -761,7 +857,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     const PlanHost& h = p->host;
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
     if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
-    ensure_device(p);
+    bind_ctx(c, p);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     WaitValue32Fn wait = wait_value_fn();
     if (!wait) fail(FO_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
@@ -895,7 +991,7 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
   };
   return guard([&] {
     if (!c || !p || !A || !Bt || !out) fail(FO_ERR_INVALID_ARG, "null argument");
-    ensure_device(p);
+    bind_ctx(c, p);
     FO_CUDA(cudaSetDevice(c->device));
     ensure_host_streams(c);
     const PlanHost& h = p->host;
@@ -1001,7 +1097,7 @@ fo_status fo_run_sequential(fo_ctx c, fo_plan p, const void* A, const void* Bt, 
     if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
     const PlanHost& h = p->host;
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
-    ensure_device(p);
+    bind_ctx(c, p);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int64_t MN = h.M * h.N;
     if (p->split > 1) FO_CUDA(cudaMemsetAsync(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words, s));
@@ -1062,7 +1158,7 @@ fo_status fo_run_allgather(fo_ctx c, fo_plan p, const void* local, void* out, co
     const PlanHost& h = p->host;
     if (h.coll != FO_REDUCESCATTER) fail(FO_ERR_INVALID_ARG, "AllGather follow-on needs a ReduceScatter plan");
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
-    ensure_device(p);
+    bind_ctx(c, p);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t local_elems = (size_t)(h.out_rows * h.N);
     if (!row_exchange) {
@@ -1238,11 +1334,48 @@ fo_status fo_plan_sync(fo_ctx c, fo_plan p, void* stream, int64_t timeout_ms) {
   });
 }
 
-fo_status fo_plan_prepare(fo_plan p, int32_t what) {
+fo_status fo_mem_alloc(fo_ctx c, int64_t bytes, void** ptr) {
+  return guard([&] {
+    if (!c || !ptr || bytes <= 0) fail(FO_ERR_INVALID_ARG, "bad arguments");
+    FO_CUDA(cudaSetDevice(c->device));
+    fo_ctx_s::UserBuf b{};
+    b.bytes = (size_t)bytes;
+    FO_NCCL(ncclMemAlloc(&b.ptr, b.bytes));
+    ncclComm_t comm = c->comm ? c->comm->nccl() : nullptr;
+    try {
+      if (comm && c->mem_mode == 1) FO_NCCL(ncclCommRegister(comm, b.ptr, b.bytes, &b.handle));
+      if (comm && c->mem_mode == 2) FO_NCCL(ncclCommWindowRegister(comm, b.ptr, b.bytes, &b.win, NCCL_WIN_COLL_SYMMETRIC));
+    } catch (...) {
+      ncclMemFree(b.ptr);
+      throw;
+    }
+    c->user_bufs.push_back(b);
+    *ptr = b.ptr;
+  });
+}
+
+fo_status fo_mem_free(fo_ctx c, void* ptr) {
+  return guard([&] {
+    if (!c || !ptr) fail(FO_ERR_INVALID_ARG, "null argument");
+    auto& v = c->user_bufs;
+    auto it = std::find_if(v.begin(), v.end(), [&](const fo_ctx_s::UserBuf& b) { return b.ptr == ptr; });
+    if (it == v.end()) fail(FO_ERR_INVALID_ARG, "pointer not from fo_mem_alloc on this context");
+    FO_CUDA(cudaSetDevice(c->device));
+    FO_CUDA(cudaDeviceSynchronize());
+    ncclComm_t comm = c->comm ? c->comm->nccl() : nullptr;
+    if (comm && it->handle) FO_NCCL(ncclCommDeregister(comm, it->handle));
+    if (comm && it->win) FO_NCCL(ncclCommWindowDeregister(comm, it->win));
+    FO_NCCL(ncclMemFree(it->ptr));
+    v.erase(it);
+  });
+}
+
+fo_status fo_plan_prepare(fo_ctx c, fo_plan p, int32_t what) {
   return guard([&] {
     if (!p) fail(FO_ERR_INVALID_ARG, "null plan");
     if (what < 0 || what > 3) fail(FO_ERR_INVALID_ARG, "what must be a mask of 1 | 2");
-    ensure_device(p);
+    if (c) bind_ctx(c, p);
+    else ensure_device(p);
     const PlanHost& h = p->host;
     if ((what & 1) && (h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && !p->d_rowmajor)
       FO_CUDA(cudaMalloc(&p->d_rowmajor, 2 * (size_t)(h.M * h.N)));
@@ -1278,7 +1411,8 @@ fo_status fo_plan_gemm_cluster(fo_plan p, int32_t* cluster_ctas) {
 
 int64_t fo_kernel_launch_count(void) { return launch_count(); }
 
-fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t iters, double* avg_us) {
+fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t iters, double* avg_us,
+                                 double* busbw_gbps) {
   return guard([&] {
     if (!c || !avg_us || bytes <= 0 || iters < 1) fail(FO_ERR_INVALID_ARG, "bad arguments");
     if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
@@ -1286,10 +1420,29 @@ fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t 
     const int W = c->world;
     const size_t count = (size_t)(bytes / 2 / W) * W;  // bf16 elements, divisible by world
     if (count == 0) fail(FO_ERR_INVALID_ARG, "message too small");
+    // the buffers the context's plans would use: registered ones when the
+    // context registers (the curve then includes NVLS / zero-copy paths)
     void *a = nullptr, *b = nullptr;
-    FO_CUDA(cudaMalloc(&a, 2 * count));
-    FO_CUDA(cudaMalloc(&b, 2 * count));
+    ncclComm_t comm = c->comm ? c->comm->nccl() : nullptr;
+    const bool reg = c->mem_mode > 0 && comm;
+    void *ha = nullptr, *hb = nullptr;
+    ncclWindow_t wa = nullptr, wb = nullptr;
+    if (reg) {
+      FO_NCCL(ncclMemAlloc(&a, 2 * count));
+      FO_NCCL(ncclMemAlloc(&b, 2 * count));
+      if (c->mem_mode == 2) {
+        FO_NCCL(ncclCommWindowRegister(comm, a, 2 * count, &wa, NCCL_WIN_COLL_SYMMETRIC));
+        FO_NCCL(ncclCommWindowRegister(comm, b, 2 * count, &wb, NCCL_WIN_COLL_SYMMETRIC));
+      } else {
+        FO_NCCL(ncclCommRegister(comm, a, 2 * count, &ha));
+        FO_NCCL(ncclCommRegister(comm, b, 2 * count, &hb));
+      }
+    } else {
+      FO_CUDA(cudaMalloc(&a, 2 * count));
+      FO_CUDA(cudaMalloc(&b, 2 * count));
+    }
     FO_CUDA(cudaMemset(a, 0, 2 * count));
+    FO_CUDA(cudaDeviceSynchronize());
     cudaStream_t cs = c->comm_stream;
     auto once = [&] {
       switch (coll) {
@@ -1324,10 +1477,26 @@ fo_status fo_ctx_time_collective(fo_ctx c, int32_t coll, int64_t bytes, int32_t 
     float ms = 0.f;
     FO_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     *avg_us = 1e3 * ms / iters;
+    // bus bandwidth, nccl-tests convention: AllReduce 2(n-1)/n S, ReduceScatter
+    // and All-to-All (n-1)/n S, over the message's total bytes S
+    if (busbw_gbps) {
+      const double S = 2.0 * (double)count, n = (double)W;
+      const double factor = (coll == FO_ALLREDUCE) ? 2.0 * (n - 1) / n : (n - 1) / n;
+      *busbw_gbps = (*avg_us > 0) ? S * factor / (*avg_us * 1e-6) / 1e9 : 0.0;
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaFree(a);
-    cudaFree(b);
+    if (reg) {
+      for (void* h : {ha, hb})
+        if (h) ncclCommDeregister(comm, h);
+      for (ncclWindow_t w : {wa, wb})
+        if (w) ncclCommWindowDeregister(comm, w);
+      ncclMemFree(a);
+      ncclMemFree(b);
+    } else {
+      cudaFree(a);
+      cudaFree(b);
+    }
   });
 }
 

@@ -7,6 +7,10 @@
 #include "kernels.h"
 #include "plan.h"
 
+#include <nccl.h>
+
+struct fo_ctx_s;
+
 struct fo_plan_s {
   fo::PlanHost host;
   // ---- device state (created lazily on first device use)
@@ -22,6 +26,12 @@ struct fo_plan_s {
   void* d_send = nullptr;  // pre-reordered send buffer (bf16), library-owned
   void* d_recv = nullptr;  // receive buffer (RS / A2A)
   void* d_rowmajor = nullptr;  // sequential baseline scratch (RS / A2A row-major C)
+  // ---- NCCL buffer registration (fo_ctx_config.buffers of the first context)
+  int mem_mode = 0;            // 0 plain, 1 ncclMemAlloc + ncclCommRegister, 2 + window registration
+  bool nccl_mem = false;       // d_send / d_recv came from ncclMemAlloc
+  fo_ctx_s* reg_ctx = nullptr; // context whose communicator holds the registrations
+  void *reg_send = nullptr, *reg_recv = nullptr;
+  ncclWindow_t win_send = nullptr, win_recv = nullptr;
   int32_t* d_recv_dst = nullptr;  // A2A received subtoken -> output position
   // ---- device staging for fo_run_host (lazily allocated)
   void* h_A = nullptr;

@@ -244,6 +244,7 @@ class LayerChoice:
     gemm_us: float
     candidates: list     # (workers, tile:layout[+tailsplit], groups, predicted_us, gemm_us[, measured_us])
     tail_split: int = 0  # FO_OPT_TAIL_SPLIT of the chosen plan (0 off, -1 auto)
+    curve: list = field(default_factory=list)  # (bytes, algbw GB/s, busbw GB/s) on the context's communicator
     tile_m: int = TILE_M
     tile_n: int = TILE_N
 
@@ -311,7 +312,8 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
               if M % tm == 0 and N % tn == 0 and (coll != "reducescatter" or tm % world == 0)]
     if not shapes:
         raise ValueError("no tile shape divides the layer")
-    curve = ctx.sample_curve(coll, sizes or [1 << s for s in range(18, 28)], iters=3)
+    curve_bw = ctx.sample_curve_bw(coll, sizes or [1 << s for s in range(18, 28)], iters=3)
+    curve = [(b, alg) for b, alg, _ in curve_bw]
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     Bt = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     out_rows = M if coll == "allreduce" else M // world
@@ -460,4 +462,5 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     best = evaluated[k]
     cands = [(e[0], f"{e[7]}x{e[8]}:" + e[1] + ("+tailsplit" if e[6] else ""), e[2], e[3], e[4]) +
              ((measured[i],) if i < len(measured) else ()) for i, e in enumerate(evaluated)]
-    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], cands, best[6], best[7], best[8])
+    return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], cands, best[6], best[7], best[8],
+                       curve_bw)

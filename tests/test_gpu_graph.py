@@ -135,6 +135,54 @@ def test_run_host_swiglu_and_residual_writeback():
     ctx.close()
 
 
+@pytest.mark.parametrize("buffers", ["registered", "window"])
+def test_registered_buffers_world1(buffers):
+    """fo_ctx_config.buffers: plans' send / receive buffers from ncclMemAlloc,
+    registered with the communicator (ncclCommRegister / symmetric windows),
+    and a caller `out` from fo_mem_alloc: every layout stays bit-identical to
+    fo_run_sequential; time_collective reports the bus bandwidth."""
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    torch.cuda.set_device(0)
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id(), nccl_max_ctas=16, cta_policy="efficiency", buffers=buffers)
+    M, N, K = 1024, 1024, 256
+    A, Bt = synthetic.exact_inputs(M, N, K, seed=21, nnz_per_row=64)
+    A, Bt = A.cuda(), Bt.cuda()
+    for coll, lay, groups in (("allreduce", "slot", [1, 1, 2]), ("allreduce", "rowband", [2, 2]),
+                              ("reducescatter", "auto", [1, 3])):
+        plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=4, swizzle=1 if lay == "rowband" else 2,
+                       group_waves=groups, ar_layout=lay)
+        plan.prepare(ctx=ctx)
+        want = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        fo.run_sequential(ctx, plan, A, Bt, want)
+        out = ctx.mem_alloc((M, N))
+        for _ in range(2):
+            out.fill_(float("nan"))
+            fo.run(ctx, plan, A, Bt, out)
+            torch.cuda.synchronize()
+            assert torch.equal(out, want), (buffers, coll, lay)
+        del out
+        plan.close()
+    rd = synthetic.random_row_dst(M, 1, 3)
+    spec = dict(coll="alltoall", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=4, group_waves=[1, 3], row_dst=rd)
+    plan = fo.Plan(rank=0, world=1, peers=[spec], **spec)
+    want = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run_sequential(ctx, plan, A, Bt, want)
+    out = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, A, Bt, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+    us, bus = ctx.time_collective_bw("allreduce", 1 << 22, 3)
+    assert us > 0 and bus == 0.0               # one rank: 2(n-1)/n = 0 bus bytes
+    ctx2 = fo.Context.create(0, 0, 1, fo.unique_id())
+    with pytest.raises(fo.FOError):            # registered with ctx, not ctx2
+        fo.run(ctx2, plan, A, Bt, out)
+    plan.close()
+    ctx2.close()
+    ctx.close()
+
+
 def test_time_collective_world1():
     from paper_2504_19519_b200 import build
 
