@@ -244,9 +244,9 @@ class LayerChoice:
     gemm_us: float
     candidates: list     # (workers, tile:layout[+tailsplit], groups, predicted_us, gemm_us[, measured_us])
     tail_split: int = 0  # FO_OPT_TAIL_SPLIT of the chosen plan (0 off, -1 auto)
-    curve: list = field(default_factory=list)  # (bytes, algbw GB/s, busbw GB/s) on the context's communicator
     tile_m: int = TILE_M
     tile_n: int = TILE_N
+    curve: list = field(default_factory=list)  # (bytes, algbw GB/s, busbw GB/s) on the context's communicator
 
     def spec(self, M, N, K, coll, post="none") -> dict:
         d = dict(coll=coll, m=M, n=N, k=K, tile_m=self.tile_m, tile_n=self.tile_n, workers=self.workers,
