@@ -513,12 +513,21 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      epilogue and the stream-K tail always fold this way).
  *                      Slices wait on each other, which is safe because every
  *                      slice is its worker's last unit and all workers are
- *                      co-resident (workers x CTAs <= SMs is enforced) */
+ *                      co-resident (workers x CTAs <= SMs is enforced)
+ *  FO_OPT_K_SNAKE      -1 (default) — auto: 1 when K >= 64 k-blocks (4096), else 0;
+ *                      0 — every tile runs its k-blocks first to last; 1 — a
+ *                      worker's odd units (its odd waves) run them last to first,
+ *                      so a wave starts on the k-slices of the operand panels the
+ *                      previous wave read last, which are still in L2 (fewer
+ *                      HBM re-reads of the panels consecutive waves share); the
+ *                      fp32 accumulation order of those tiles is reversed.
+ *                      Measured (profiles/r02_ksnake.txt): 4096^2 x 14336, S=74 +
+ *                      split tail: HBM reads 598 -> 526 MB, 292.9 -> 288.9 us */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
                FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8,
                FO_OPT_DEBUG_STALL_GROUP = 10, FO_OPT_GEMM_SWIGLU = 11,
-               FO_OPT_DIST_FOLD = 12 } fo_option;
+               FO_OPT_DIST_FOLD = 12, FO_OPT_K_SNAKE = 13 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

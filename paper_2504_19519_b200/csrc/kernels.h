@@ -73,6 +73,10 @@ struct GemmArgs {
   uint32_t wave_epoch;
   // ---- TMA multicast across clusters of two CTA pairs (FO_OPT_MULTICAST)
   int multicast;
+  // ---- FO_OPT_K_SNAKE: a worker's odd units run their k-blocks last to first,
+  // so a wave starts on the k-slices of the operand panels the previous wave
+  // read last (still in L2)
+  int k_snake;
 };
 
 enum PostMode : int {

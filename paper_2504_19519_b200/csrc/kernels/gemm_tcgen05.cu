@@ -481,7 +481,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t target = (p.wave_epoch + 1u) * size;
           while ((int32_t)(ld_acquire(p.wave_ctr + wave - 1) - target) < 0) __nanosleep(64);
         }
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        const bool rev = p.k_snake && (k & 1);
+        for (int kk = un.kb0; kk < un.kb1; ++kk) {
+          const int kb = rev ? un.kb0 + un.kb1 - 1 - kk : kk;
           mbar_wait(&empty[stage], phase ^ 1);
           // K-major operand: one box [rows, 64 k]; MN-major operand: 64x64
           // boxes [64 k, 64 mn], one per 64-row chunk, 8 KB apart
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {  // (order-free here: the producer decides which k-block)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(sA + stage * A_STAGE_BYTES);

@@ -413,6 +413,10 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
     a.a_chunk_rows = p->a_chunk_rows;
   }
   a.multicast = p->multicast;
+  // auto (-1): on for long K, where a wave's panels are long enough for the
+  // reversal to matter (measured: -12% HBM reads and -1.4% time at 4096^2 x
+  // 14336; within noise or slightly slower at 16 k-blocks)
+  a.k_snake = p->k_snake < 0 ? (h.K / 64 >= 64) : p->k_snake;
   if (p->wave_sync && p->split == 1 && h.T > 1) {
     a.wave_ctr = p->d_wave;
     a.wave_epoch = p->gemm_launches;
@@ -1562,6 +1566,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_WAVE_SYNC:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "wave_sync must be 0 or 1");
         p->wave_sync = (int)value;
+        break;
+      case FO_OPT_K_SNAKE:
+        if (value < -1 || value > 1) fail(FO_ERR_INVALID_ARG, "k_snake must be -1, 0 or 1");
+        p->k_snake = (int)value;
         break;
       case FO_OPT_LAST_GROUP_IN_ORDER:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "last_group_in_order must be 0 or 1");
