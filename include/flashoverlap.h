@@ -92,7 +92,8 @@ typedef struct {
   int32_t coll;          /* fo_coll */
   int32_t ar_layout;     /* fo_ar_layout (AllReduce only) */
   int64_t m, n, k;       /* this rank's GEMM: A [m,k], Bt [n,k], C [m,n]; k = K/world for TP */
-  int32_t tile_m;        /* 128 (cta_group::1) or 256 (cta_group::2 pair) */
+  int32_t tile_m;        /* 64 or 128 (one CTA, tcgen05.mma M=64 / M=128; 64: K-major operands, no tail split)
+                            or 256 (cta_group::2 CTA pair) */
   int32_t tile_n;        /* 64, 128 or 256 */
   int32_t workers;       /* S >= 1 = concurrent tile workers = wave width (grid of the persistent GEMM) */
   const int32_t* tile_order; /* [tiles] permutation of tile ids, or NULL => default swizzle */

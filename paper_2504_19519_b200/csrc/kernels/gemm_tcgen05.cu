@@ -36,7 +36,6 @@ namespace {
 
 constexpr int BM = 128;                     // rows per CTA (a CTA pair covers 256)
 constexpr int BK = 64;                      // 64 bf16 = 128 B = one swizzle row
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int EPI_COLS = 64;                // columns staged per epilogue chunk
 constexpr int EPI_PITCH = EPI_COLS * 2 + 16;  // padded row pitch (bank-conflict free)
 constexpr int EPI_WARP_BYTES = 32 * EPI_PITCH;
@@ -47,11 +46,15 @@ constexpr int NUM_THREADS = 256;
 // CTA pair (tcgen05 cta_group::2): each CTA stages its 128 rows of A and
 // BN/2 rows of B, the leader issues M=256 MMAs, each CTA's TMEM holds its
 // 128 accumulator rows.
-template <int BN, int CG>
+// RB = accumulator rows per CTA: 128, or 64 (cta_group::1 only: tcgen05.mma
+// M=64, whose D rows 16q..16q+15 sit in TMEM lanes 32q..32q+15 — the
+// "half subpartition" layout — so each epilogue warp owns 16 rows).
+template <int BN, int CG, int RB = 128>
 struct Cfg {
+  static constexpr int A_STAGE = RB * BK * 2;            // A rows staged per CTA
   static constexpr int B_ROWS = BN / CG;                 // B rows staged per CTA
   static constexpr int B_STAGE_BYTES = B_ROWS * BK * 2;
-  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+  static constexpr int STAGE_BYTES = A_STAGE + B_STAGE_BYTES;
   static constexpr int BUDGET = 232448 - 1024 - EPI_BYTES - 256;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulator stages
@@ -359,14 +362,17 @@ __device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, in
 // CTA loads half of its share of that operand and TMA-multicasts it to the
 // CTA at the same half of the other pair, so the operand crosses L2 once for
 // both tiles (tmA2 / tmB2: maps with half-height boxes).
-template <int BN, int CG, int MJ, int MC>
+template <int BN, int CG, int MJ, int MC, int RB = 128>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     fo_gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                            const GemmArgs p) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, RB>;
   constexpr int ST = C::STAGES;
-  constexpr int TM = BM * CG;  // tile rows
+  constexpr int TM = RB * CG;  // tile rows
+  constexpr int A_STAGE_BYTES = C::A_STAGE;
+  constexpr int RPW = RB / 4;  // accumulator rows per epilogue warp (TMEM lanes 32q .. 32q + RPW - 1)
+  static_assert(RB == 128 || (RB == 64 && CG == 1 && MJ == 0 && MC == 1), "64-row tiles: one CTA, K-major");
   static_assert(!(MJ & 2) || (C::B_ROWS % 64 == 0), "MN-major B needs 64-row chunks");
   static_assert(MC == 1 || (CG == 2 && MJ == 0), "multicast clusters: CTA pairs, K-major operands");
   extern __shared__ uint8_t smem_raw[];
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           while ((int32_t)(ld_acquire(p.a_ready + ready_chunk) - p.a_epoch) < 0) __nanosleep(128);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        const int arow = ti * TM + (int)half * BM;
+        const int arow = ti * TM + (int)half * RB;
         const int brow = tj * BN + (int)half * C::B_ROWS;
         // multicast partner: the other pair of the cluster runs position u^1
         bool mcA = false, mcB = false;
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // and multicasts them to the same half of both pairs
             if (mcA)
               tma_load_2d_2sm_mc(sA + stage * A_STAGE_BYTES + pic * (A_STAGE_BYTES / 2), &tmA2, kb * BK,
-                                 arow + (int)pic * (BM / 2), &full[stage], mc_mask);
+                                 arow + (int)pic * (RB / 2), &full[stage], mc_mask);
             else
               tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, kb * BK, arow, mapa_shared(&full[stage], lead_rank));
             if (mcB)
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else
               tma_load_2d_2sm(sB + stage * C::B_STAGE_BYTES, &tmB, kb * BK, brow, mapa_shared(&full[stage], lead_rank));
           } else {
-            load(sA + stage * A_STAGE_BYTES, &tmA, arow, BM);
+            load(sA + stage * A_STAGE_BYTES, &tmA, arow, RB);
             load(sB + stage * C::B_STAGE_BYTES, &tmB, brow, C::B_ROWS);
           }
           if (++stage == ST) {
@@ -597,13 +603,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int32_t nx_slot[8];
 #pragma unroll
     for (int it = 0; it < 8; ++it) nx_slot[it] = 0;
+    static_assert(RPW == 32 || RPW == 16, "rows per epilogue warp");
     auto prefetch_dst = [&](int npos) {
       if (p.mode == EPI_RS) {
         nx_rs = p.rs_info[npos];
       } else if (p.mode == EPI_A2A) {
 #pragma unroll
-        for (int it = 0; it < 8; ++it)
-          nx_slot[it] = p.row_slot[(int64_t)npos * TM + (int)half * BM + q * 32 + it * 4 + (lane >> 3)];
+        for (int it = 0; it < RPW / 4; ++it)
+          nx_slot[it] = p.row_slot[(int64_t)npos * TM + (int)half * RB + q * RPW + it * 4 + (lane >> 3)];
       }
     };
     const int nu = unit_count(p, worker, nworkers);
@@ -615,15 +622,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int ti = t / p.Nt, tj = t - ti * p.Nt;
       const bool owner = (un.role == 1), part = (un.role == 2);  // split tail tile roles
       const int tt = un.tt;  // tail tile index (flags)
-      const int row = (int)half * BM + q * 32 + lane;  // this thread's accumulator row in the tile
+      const int row = (int)half * RB + q * RPW + lane;  // this thread's accumulator row in the tile (lane < RPW)
       // this lane's 8 destination rows of the tile (rows it*4 + lane/8 of the
       // warp's 32-row quarter), resolved once per tile from table entries
       // loaded during the previous tile (no memory latency here: at short K
       // the epilogue is on the critical path)
       __nv_bfloat16* drow[8];
 #pragma unroll
-      for (int it = 0; it < 8; ++it)
-        drow[it] = row_dst<TM, BN>(p, pos, ti, tj, (int)half * BM + q * 32 + it * 4 + (lane >> 3), nx_rs.x, nx_rs.y,
+      for (int it = 0; it < RPW / 4; ++it)
+        drow[it] = row_dst<TM, BN>(p, pos, ti, tj, (int)half * RB + q * RPW + it * 4 + (lane >> 3), nx_rs.x, nx_rs.y,
                                    nx_slot[it]) +
                    (lane & 7) * 8;
       mbar_wait(&tfull[acc], aphase);
@@ -705,7 +712,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           __syncwarp();
 #pragma unroll
-          for (int it = 0; it < 8; ++it) {
+          for (int it = 0; it < RPW / 4; ++it) {
             const int r = it * 4 + (lane >> 3);
             const uint4 o = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + (lane & 7) * 16);
             *reinterpret_cast<uint4*>(drow[it] + c * EPI_COLS) = o;
@@ -798,7 +805,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int r = it * 8 + (lane >> 2);
               const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + (lane & 3) * 16);
               __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.dst) +
-                                 ((int64_t)ti * TM + (int)half * BM + q * 32 + r) * p.ldc + (int64_t)tj * 128 +
+                                 ((int64_t)ti * TM + (int)half * RB + q * 32 + r) * p.ldc + (int64_t)tj * 128 +
                                  32 * c2 + (lane & 3) * 8;
               *reinterpret_cast<uint4*>(d) = w;
             }
@@ -872,7 +879,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         // coalesced copy-out: each instruction moves 4 rows x 128 B
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
+        for (int it = 0; it < RPW / 4; ++it) {
           const int r = it * 4 + (lane >> 3);
           const int ch = lane & 7;
           const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + ch * 16);
@@ -956,11 +963,11 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int CG, int MJ, int MC>
+template <int BN, int CG, int MJ, int MC, int RB = 128>
 cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, RB>;
   static std::atomic<uint64_t> attr_set{0};  // one bit per device (the attribute is per device context)
-  auto kern = fo_gemm_tcgen05_kernel<BN, CG, MJ, MC>;
+  auto kern = fo_gemm_tcgen05_kernel<BN, CG, MJ, MC, RB>;
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
@@ -970,10 +977,10 @@ cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
     attr_set.fetch_or(bit);
   }
   CUtensorMap mA, mB, mA2, mB2;
-  if (!make_map(&mA, a.A, a.M, a.K, BM, MJ & 1) || !make_map(&mB, a.Bt, a.N, a.K, C::B_ROWS, MJ & 2))
+  if (!make_map(&mA, a.A, a.M, a.K, RB, MJ & 1) || !make_map(&mB, a.Bt, a.N, a.K, C::B_ROWS, MJ & 2))
     return cudaErrorInvalidValue;
   if (MC == 2) {
-    if (!make_map(&mA2, a.A, a.M, a.K, BM / 2, false) || !make_map(&mB2, a.Bt, a.N, a.K, C::B_ROWS / 2, false))
+    if (!make_map(&mA2, a.A, a.M, a.K, RB / 2, false) || !make_map(&mB2, a.Bt, a.N, a.K, C::B_ROWS / 2, false))
       return cudaErrorInvalidValue;
   } else {
     mA2 = mA;
@@ -1041,7 +1048,7 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 bool gemm_shape_supported(int bm, int bn) {
-  return (bm == 128 || bm == 256) && (bn == 64 || bn == 128 || bn == 256);
+  return (bm == 64 || bm == 128 || bm == 256) && (bn == 64 || bn == 128 || bn == 256);
 }
 
 template <int BN, int CG>
@@ -1074,7 +1081,15 @@ bool gemm_multicast_used(const GemmArgs& a) {
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
   if (a.mn_major && a.BN == 64) return cudaErrorInvalidValue;  // MN-major needs >= 64-row B chunks per CTA
-  if (a.BM == 128) {
+  if (a.BM == 64) {
+    // tcgen05.mma M=64 (one CTA): K-major operands, no split tail / SwiGLU
+    if (a.mn_major || a.split > 1 || a.mode == EPI_SWIGLU) return cudaErrorInvalidValue;
+    switch (a.BN) {
+      case 64: return launch_cfg<64, 1, 0, 1, 64>(a, stream);
+      case 128: return launch_cfg<128, 1, 0, 1, 64>(a, stream);
+      case 256: return launch_cfg<256, 1, 0, 1, 64>(a, stream);
+    }
+  } else if (a.BM == 128) {
     switch (a.BN) {
       case 64: return launch_cfg<64, 1, 0, 1>(a, stream);
       case 128: return launch_mj<128, 1>(a, stream);

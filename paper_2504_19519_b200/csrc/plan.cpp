@@ -67,7 +67,7 @@ static int auto_swizzle_ar(int Mt, int Nt, int S, const std::vector<int32_t>& gp
 }
 
 static void check_tile_shape(int BM, int BN) {
-  if (BM != 128 && BM != 256) fail(FO_ERR_UNSUPPORTED, "tile_m=%d not compiled (128 or 256)", BM);
+  if (BM != 64 && BM != 128 && BM != 256) fail(FO_ERR_UNSUPPORTED, "tile_m=%d not compiled (64, 128 or 256)", BM);
   if (BN != 64 && BN != 128 && BN != 256) fail(FO_ERR_UNSUPPORTED, "tile_n=%d not compiled (64/128/256)", BN);
 }
 

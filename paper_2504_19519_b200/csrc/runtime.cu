@@ -71,6 +71,9 @@ namespace fo {
     if (r_ != ncclSuccess) fail(FO_ERR_NCCL, "%s: %s (%s:%d)", #x, ncclGetErrorString(r_), __FILE__, __LINE__); \
   } while (0)
 
+// CTAs that run (and signal) one tile: a CTA pair for 256-row tiles
+static inline int ctas_per_tile(int BM) { return BM == 256 ? 2 : 1; }
+
 typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
@@ -206,10 +209,12 @@ static void ensure_device(fo_plan_s* p) {
     fail(FO_ERR_UNSUPPORTED, "tile %dx%d not compiled into this build", h.BM, h.BN);
   int sms = 0;
   FO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (h.S * (h.BM / 128) > sms)
+  if (h.S * ctas_per_tile(h.BM) > sms)
     fail(FO_ERR_INVALID_ARG, "workers=%d x %d CTAs exceeds the %d SMs (waves would not be resident)", h.S,
-         h.BM / 128, sms);
-  p->free_sms = sms - h.S * (h.BM / 128);
+         ctas_per_tile(h.BM), sms);
+  if (h.BM == 64 && (h.mn_major || p->tail_split_req > 1 || p->tail_split_req < 0))
+    fail(FO_ERR_UNSUPPORTED, "64-row tiles (tcgen05 M=64): K-major operands and no tail split");
+  p->free_sms = sms - h.S * ctas_per_tile(h.BM);
   int major = 0, minor = 0;
   FO_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
   FO_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
@@ -313,7 +318,7 @@ static void ensure_device(fo_plan_s* p) {
     p->split = split ? std::max(2, f) : 1;
     p->tail_pos = split ? tail0 : h.tiles;
     p->units = split ? tail0 + (int)segs.size() : h.tiles;
-    const int cg = h.BM / 128;
+    const int cg = ctas_per_tile(h.BM);
     p->dist_fold = split && !streamk;
     p->ctr_words = h.P + (split ? R * cg * (p->dist_fold ? 2 : 1) : 0);
     if (split) {
@@ -406,7 +411,7 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   a.workspace = p->d_ws;
   a.flags = p->d_flags;
   a.dist_fold = p->dist_fold && p->dist_fold_opt;
-  a.done = p->dist_fold ? p->d_flags + (h.tiles - p->tail_pos) * (h.BM / 128) : nullptr;
+  a.done = p->dist_fold ? p->d_flags + (h.tiles - p->tail_pos) * ctas_per_tile(h.BM) : nullptr;
   if (p->a_staged_run) {
     a.a_ready = p->d_a_ready + (size_t)p->host_set * p->a_chunks;
     a.a_epoch = p->a_epoch;
@@ -484,7 +489,9 @@ static int post_map(const PlanHost& h) {
 
 // Each CTA signals once per tile it finishes; a 256-row tile is finished by a
 // CTA pair, so group j completes at |G_j| * tile_m/128 signals.
-static cuuint32_t signal_target(const PlanHost& h, int j) { return (cuuint32_t)(h.group_tiles(j) * (h.BM / 128)); }
+static cuuint32_t signal_target(const PlanHost& h, int j) {
+  return (cuuint32_t)(h.group_tiles(j) * ctas_per_tile(h.BM));
+}
 
 // Trigger: block the comm stream until group j's counter
 // reaches its target — a front-end stream wait (no SM) or the paper's
@@ -1409,7 +1416,7 @@ fo_status fo_plan_gemm_cluster(fo_plan p, int32_t* cluster_ctas) {
     if (!p || !cluster_ctas) fail(FO_ERR_INVALID_ARG, "null argument");
     ensure_device(p);
     GemmArgs a = gemm_args(p, nullptr, nullptr, nullptr, EPI_ROWMAJOR, false);
-    *cluster_ctas = gemm_multicast_used(a) ? 4 : p->host.BM / 128;
+    *cluster_ctas = gemm_multicast_used(a) ? 4 : ctas_per_tile(p->host.BM);
   });
 }
 
@@ -1551,7 +1558,7 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
         break;
       case FO_OPT_GEMM_SWIGLU:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "gemm_swiglu must be 0 or 1");
-        if (value && (p->host.coll != FO_NOCOMM || p->host.BN != 256 || p->host.post != FO_POST_NONE))
+        if (value && (p->host.coll != FO_NOCOMM || p->host.BN != 256 || p->host.BM == 64 || p->host.post != FO_POST_NONE))
           fail(FO_ERR_UNSUPPORTED, "the SwiGLU epilogue needs a no-comm plan with tile_n 256 and post none");
         p->swiglu = (int)value;
         break;

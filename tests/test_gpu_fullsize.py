@@ -293,10 +293,11 @@ def test_c2_bench_config_tp1_tail_split():
 
 
 def test_c0_two_ranks_four_groups():
-    """configs[0]: M=N=256, K=512 split over 2 simulated ranks (K_loc=256),
-    AllReduce, 4 signal groups.  The tcgen05 M atom is 128, so 128x64 tiles
-    (R22): 8 tiles, S=2, T=4, groups (1,1,1,1).  Exact-integer regime,
-    bit-exact send buffers, counters and outputs for both ranks."""
+    """configs[0] exactly as BASELINE.json states it: M=N=256, K=512 split over
+    2 simulated ranks (K_loc=256), AllReduce, 64x64 tiles (tcgen05.mma M=64),
+    4 signal groups: 16 tiles, S=4, T=4, groups (1,1,1,1) of 4 tiles each.
+    Exact-integer regime, bit-exact send buffers, counters and outputs for both
+    ranks."""
     from oracle import pipeline as opl
     from oracle import plan as op
 
@@ -307,16 +308,18 @@ def test_c0_two_ranks_four_groups():
         A, Bt = synthetic.exact_inputs(M, N, K, seed=synthetic.rank_seed(0, n, r), nnz_per_row=128)
         As.append(A)
         Bts.append(Bt)
-    oplan = op.make_plan(M, N, 128, 64, 2, groups, swizzle=2)
+    oplan = op.make_plan(M, N, 64, 64, 4, groups, swizzle=2)
+    assert oplan.ntiles == 16 and oplan.T == 4
     ores = opl.run_allreduce(As, Bts, oplan)
     for r in range(n):
-        plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=128, tile_n=64, workers=2, swizzle=2,
+        plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=64, tile_n=64, workers=4, swizzle=2,
                        group_waves=groups, ar_layout="slot", rank=r, world=n)
+        assert plan.info["tiles"] == 16 and plan.info["waves"] == 4
         send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
         fo.gemm_stage(plan, As[r].cuda(), Bts[r].cuda(), send)
         torch.cuda.synchronize()
         assert np.array_equal(send.double().cpu().numpy(), ores["send"][r])
-        assert plan.read_counters().tolist() == [2, 2, 2, 2]
+        assert plan.read_counters().tolist() == [4, 4, 4, 4]
         out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plan, torch.from_numpy(ores["recv"][r]).to(torch.bfloat16).cuda(), out)
         torch.cuda.synchronize()

@@ -61,13 +61,13 @@ def _rel_err(g, o):
 
 def _counters_ok(plan, oplan):
     # each CTA signals once per tile it finishes; a 256-row tile is finished by a CTA pair
-    mult = oplan.BM // 128
+    mult = max(1, oplan.BM // 128)
     want = [mult * t for t in op.group_thresholds(oplan.partition, oplan.S, oplan.ntiles)]
     assert plan.read_counters().tolist() == want
 
 
 # ------------------------------------------------------------------ plain GEMM
-@pytest.mark.parametrize("BM", [128, 256])
+@pytest.mark.parametrize("BM", [64, 128, 256])
 @pytest.mark.parametrize("BN", [64, 128, 256])
 @pytest.mark.parametrize("shape", [(256, 256, 64), (768, 512, 320), (512, 768, 1024)])
 def test_gemm_rowmajor_exact(BM, BN, shape):
@@ -85,7 +85,7 @@ def test_gemm_rowmajor_exact(BM, BN, shape):
     _counters_ok(plan, op.make_plan(M, N, BM, BN, S, None, swizzle=2))
 
 
-@pytest.mark.parametrize("BM", [128, 256])
+@pytest.mark.parametrize("BM", [64, 128, 256])
 @pytest.mark.parametrize("BN", [128, 256])
 def test_gemm_float_regime(BM, BN):
     M, N, K = 512, 512, 2048
@@ -174,7 +174,7 @@ def test_reducescatter_stages_exact(n, case):
         assert np.array_equal(_host(out), plain[r])
 
 
-@pytest.mark.parametrize("BM", [128, 256])
+@pytest.mark.parametrize("BM", [64, 128, 256])
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
 def test_alltoall_stages_exact(n, BM):
     rng = np.random.default_rng(n)
