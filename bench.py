@@ -418,6 +418,7 @@ def main():
                          "cublas": lambda: torch.matmul(A, Bt.t(), out=out_cb)},
                         args.steps, args.warmup)
     ov_us, seq_us, gk_us, cb_us = m["ov"], m["seq"], m["gemm"], m["cublas"]
+    main_stats = dict(stats_out)   # (later timed_multi calls reuse the keys)
     launches = launches_per_step * args.steps
 
     # ---- the other BASELINE.json configs' per-rank layers (their exchange
@@ -587,7 +588,7 @@ def main():
                                        "comm_last_wave_us": round(comm_last_us, 2), "waves": T,
                                        "rule": "PAPER.md:622: GEMM + last-wave comm if GEMM-bound, else "
                                                "first-wave GEMM + full comm"},
-            "step_stats_us": {k: stats_out.get(k) for k in ("ov", "seq", "gemm", "cublas")},
+            "step_stats_us": {k: main_stats.get(k) for k in ("ov", "seq", "gemm", "cublas")},
             "nccl_allreduce_curve": ({"unit": "bytes, algbw GB/s, busbw GB/s (nccl-tests convention)",
                                       "comm": f"library communicator, maxCTAs={comm_sms if world > 1 else 'default'}",
                                       "points": [[int(b), round(a, 1), round(bb, 1)] for b, a, bb in curve_bw]}
