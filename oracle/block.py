@@ -8,15 +8,16 @@ PAPER.md:262 (TP row-parallel linear followed by AllReduce), PAPER.md:394 and
 671 (the post-communication reorder fused into the following RMSNorm),
 PAPER.md:559-578 (the Llama end-to-end setting).  Per rank r:
 
-    h   = x + sum_r bf16(attn_r @ Wo_r^T)          o_proj + AllReduce (O4, O6, O8)
+    c   = bf16(sum_r bf16(attn_r @ Wo_r^T))        o_proj + AllReduce (O4, O6, O8)
+    h   = x + c
     n   = bf16(RMSNorm(h) * gamma); x <- bf16(h)   fused add + RMSNorm, residual stream
     gu  = n @ Wgu_r^T                              gate/up (column-parallel), fp64
     a_r = bf16(silu(g) * u)                        SwiGLU on the interleaved layout below
-    y   = bf16(bf16(h) + sum_r bf16(a_r @ Wd_r^T))  down-proj + AllReduce + residual add
+    y   = bf16(bf16(h) + bf16(sum_r bf16(a_r @ Wd_r^T)))   down-proj + AllReduce + residual add
 
 bf16 roundings sit exactly where the library stores bf16 (R10: the
-GEMM epilogue's output, the fused op's outputs); the AllReduce sums those bf16
-partials in fp64 (R11).  The fused op's sum y = x + c is rounded once, when it
+GEMM epilogue's output, the AllReduce's bf16 buffer, the fused op's outputs);
+the AllReduce sums the bf16 partials in fp64 and rounds the sum once (R11).  The fused op's sum y = x + c is rounded once, when it
 is stored.
 
 SwiGLU weight layout (FO_OPT_GEMM_SWIGLU, include/flashoverlap.h): the gate
@@ -60,7 +61,7 @@ def tp_block(attn, x, Wo, Wgu, Wd, gamma, eps: float = 1e-5):
     n = len(attn)
     rb = numerics.round_bf16
     # o_proj, row-parallel: each rank's bf16 partial, AllReduce (sum)
-    c = sum(rb(numerics.gemm(attn[r], Wo[r])) for r in range(n))
+    c = rb(sum(rb(numerics.gemm(attn[r], Wo[r])) for r in range(n)))
     # fused add + RMSNorm that also writes the residual stream back
     n_out, h_bf16 = post.add_rmsnorm_residual(c, x, gamma, eps)
     n_bf16 = rb(n_out)
@@ -69,5 +70,5 @@ def tp_block(attn, x, Wo, Wgu, Wd, gamma, eps: float = 1e-5):
     for r in range(n):
         a_r = rb(swiglu_interleaved(numerics.gemm(n_bf16, Wgu[r])))
         parts.append(rb(numerics.gemm(a_r, Wd[r])))
-    y = rb(post.add(sum(parts), h_bf16))
+    y = rb(post.add(rb(sum(parts)), h_bf16))
     return y, h_bf16

@@ -49,7 +49,7 @@ def test_one_rank_is_the_plain_block():
     for b in range(I // 128):
         gcol, ucol = gu[:, 256 * b:256 * b + 128], gu[:, 256 * b + 128:256 * b + 256]
         a[:, 128 * b:128 * b + 128] = gcol / (1 + np.exp(-gcol)) * ucol
-    y = rb(rb(rb(a) @ Wd.T) + rb(hh))
+    y = rb(rb(rb(rb(a) @ Wd.T)) + rb(hh))
     got_y, got_h = ob.tp_block([attn], x, [Wo], [Wgu], [Wd], gamma)
     np.testing.assert_array_equal(got_h, rb(hh))
     np.testing.assert_allclose(got_y, y, rtol=0, atol=0)
