@@ -261,6 +261,19 @@ def main():
         uid = fo.unique_id()
     with _StdoutToStderr():
         ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
+    # the sequential baseline's NCCL call runs alone, so it gets NCCL's default
+    # CTA count (its own communicator) instead of the overlapped op's SM cap
+    if world > 1:
+        if use_dist:
+            obj = [fo.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid_seq = obj[0]
+        else:
+            uid_seq = fo.unique_id()
+        with _StdoutToStderr():
+            ctx_seq = fo.Context.create(local, rank, world, uid_seq)
+    else:
+        ctx_seq = ctx
 
     def barrier():
         if use_dist:
@@ -391,6 +404,19 @@ def main():
     # the GEMM-only timing uses exactly the overlapped plan's execution order
     gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=BMc, tile_n=BNc, workers=S,
                     tile_order=plan.export_order(), options=spec.get("options"))
+    # the sequential baseline: the overlapped plan at one rank (same thing);
+    # at N > 1 the GEMM alone on the whole GPU (every 256x256 CTA pair, split
+    # tail), its output then one NCCL call with NCCL's default CTAs — not the
+    # overlapped plan's narrower wave width
+    if world > 1:
+        S_seq = sms // 2
+        T_seq = -(-((M // 256) * (N // 256)) // S_seq)
+        seq_spec = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S_seq, swizzle=0,
+                        group_waves=[T_seq], ar_layout="auto", options={"tail_split": -1})
+        seqplan = fo.Plan(rank=rank, world=world, **seq_spec)
+        nseqplan = fo.Plan(rank=rank, world=world, **dict(seq_spec, post="add_rmsnorm"))
+    else:
+        seqplan, nseqplan = plan, nplan
 
     # ---- full-size spot check (N=1: sampled rows vs an fp64 torch CPU product; not the oracle)
     fo.run(ctx, plan, A, Bt, out)
@@ -410,10 +436,10 @@ def main():
     launches_per_step = fo.kernel_launch_count() - l0
     with ClockSampler(local) as clk:
         m = timed_multi({"ov": lambda: fo.run(ctx, plan, A, Bt, out),
-                         "seq": lambda: fo.run_sequential(ctx, plan, A, Bt, out),
+                         "seq": lambda: fo.run_sequential(ctx_seq, seqplan, A, Bt, out),
                          "gemm": lambda: fo.gemm_stage(gplan, A, Bt, out),
                          "ov_norm": lambda: fo.run(ctx, nplan, A, Bt, out2, resid, gamma),
-                         "seq_norm": lambda: fo.run_sequential(ctx, nplan, A, Bt, out2, resid, gamma),
+                         "seq_norm": lambda: fo.run_sequential(ctx_seq, nseqplan, A, Bt, out2, resid, gamma),
                          # library comparator (not on the product path): the same GEMM through cuBLAS
                          "cublas": lambda: torch.matmul(A, Bt.t(), out=out_cb)},
                         args.steps, args.warmup)
@@ -575,6 +601,10 @@ def main():
                      "speedup_vs_sequential is ~1 by construction; the multi-rank exchange runs at N>1"
                      if world == 1 else f"TP={world}: every rank's GEMM overlaps its wave groups' NCCL AllReduce"),
             "speedup_vs_sequential": round(seq_us / ov_us, 4), "sequential_us": round(seq_us, 2),
+            "sequential_config": ("the overlapped plan's GEMM writing row-major C, then one NCCL AllReduce"
+                                  if world == 1 else
+                                  f"GEMM alone on all {sms // 2} CTA pairs (split tail), then one NCCL AllReduce on "
+                                  "a communicator with NCCL's default CTA count"),
             "tflops": round(world * flops / (ov_us * 1e-6) / 1e12, 1),
             "layer_roofline_us": round(layer_roof_us, 2), "frac_of_layer_roofline": round(layer_roof_us / ov_us, 4),
             "layer_roofline": {"gemm_us": round(gemm_roof_us, 2),
@@ -628,6 +658,8 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    if ctx_seq is not ctx:
+        ctx_seq.close()
     ctx.close()
     if use_dist:
         dist.destroy_process_group()
