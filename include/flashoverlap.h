@@ -523,12 +523,20 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      HBM re-reads of the panels consecutive waves share); the
  *                      fp32 accumulation order of those tiles is reversed.
  *                      Measured (profiles/r02_ksnake.txt): 4096^2 x 14336, S=74 +
- *                      split tail: HBM reads 598 -> 526 MB, 292.9 -> 288.9 us */
+ *                      split tail: HBM reads 598 -> 526 MB, 292.9 -> 288.9 us
+ *  FO_OPT_TMA_STORE    1 (default) — whole tiles written to row-major C or to AR
+ *                      slots leave the epilogue as TMA stores (one 64-column box
+ *                      per warp from the 128B-swizzled staging buffer); with
+ *                      counters the signalling warp waits for the stores'
+ *                      completion (cp.async.bulk.wait_group 0 + async-proxy
+ *                      fence) before its release add; 0 — 16-byte st.global from
+ *                      the staging buffer (always used for RS / A2A layouts and
+ *                      split-tail tiles) */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
                FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8,
                FO_OPT_DEBUG_STALL_GROUP = 10, FO_OPT_GEMM_SWIGLU = 11,
-               FO_OPT_DIST_FOLD = 12, FO_OPT_K_SNAKE = 13 } fo_option;
+               FO_OPT_DIST_FOLD = 12, FO_OPT_K_SNAKE = 13, FO_OPT_TMA_STORE = 14 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

@@ -77,6 +77,11 @@ struct GemmArgs {
   // so a wave starts on the k-slices of the operand panels the previous wave
   // read last (still in L2)
   int k_snake;
+  // ---- epilogue stores: tma_store_ok (runtime: FO_OPT_TMA_STORE) lets the
+  // launcher use TMA stores for whole tiles in EPI_ROWMAJOR / EPI_SLOT;
+  // tma_store is set by the launcher when it built the destination map
+  int tma_store_ok;
+  int tma_store;
 };
 
 enum PostMode : int {

@@ -37,8 +37,12 @@ namespace {
 constexpr int BM = 128;                     // rows per CTA (a CTA pair covers 256)
 constexpr int BK = 64;                      // 64 bf16 = 128 B = one swizzle row
 constexpr int EPI_COLS = 64;                // columns staged per epilogue chunk
-constexpr int EPI_PITCH = EPI_COLS * 2 + 16;  // padded row pitch (bank-conflict free)
-constexpr int EPI_WARP_BYTES = 32 * EPI_PITCH;
+// Epilogue staging: per warp 32 rows x 128 B (one 64-column bf16 chunk), the
+// 16-byte chunks of row r at position x ^ (r & 7) — the TMA 128-byte swizzle,
+// so the buffer is both a bank-conflict-free transpose stage for the 16-byte
+// st.global path and the source box of a SWIZZLE_128B TMA store.
+constexpr int EPI_ROW = EPI_COLS * 2;
+constexpr int EPI_WARP_BYTES = 32 * EPI_ROW;
 constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
 constexpr int NUM_THREADS = 256;
 
@@ -270,6 +274,22 @@ __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// staging addresses (swizzled, see EPI_ROW)
+__device__ __forceinline__ uint4* stg_at(uint8_t* stg, int r, int x) {
+  return reinterpret_cast<uint4*>(stg + r * EPI_ROW + ((x ^ (r & 7)) << 4));
+}
+
+// TMA store of a 64-column x `rows`-row box from swizzled shared memory
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -366,7 +386,7 @@ template <int BN, int CG, int MJ, int MC, int RB = 128>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     fo_gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                           const GemmArgs p) {
+                           const __grid_constant__ CUtensorMap tmC, const GemmArgs p) {
   using C = Cfg<BN, CG, RB>;
   constexpr int ST = C::STAGES;
   constexpr int TM = RB * CG;  // tile rows
@@ -400,6 +420,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (p.tma_store) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
     if constexpr (MC == 2) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA2)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
@@ -700,7 +721,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v[4 * x + 3] = __float_as_uint(__uint_as_float(v[4 * x + 3]) + fv.w);
             }
           }
-          uint4* srow = reinterpret_cast<uint4*>(stg + lane * EPI_PITCH);
 #pragma unroll
           for (int x = 0; x < 8; ++x) {
             uint4 o;
@@ -708,13 +728,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             o.y = pack_bf16(v[8 * x + 2], v[8 * x + 3]);
             o.z = pack_bf16(v[8 * x + 4], v[8 * x + 5]);
             o.w = pack_bf16(v[8 * x + 6], v[8 * x + 7]);
-            srow[x] = o;
+            *stg_at(stg, lane, x) = o;
           }
           __syncwarp();
 #pragma unroll
           for (int it = 0; it < RPW / 4; ++it) {
             const int r = it * 4 + (lane >> 3);
-            const uint4 o = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + (lane & 7) * 16);
+            const uint4 o = *stg_at(stg, r, lane & 7);
             *reinterpret_cast<uint4*>(drow[it] + c * EPI_COLS) = o;
           }
           __syncwarp();
@@ -783,7 +803,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 else mbar_arrive_cluster(tempty_leader0 + 8u * acc);
               }
             }
-            uint4* srow = reinterpret_cast<uint4*>(stg + lane * EPI_PITCH);
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
               float o[8];
@@ -797,13 +816,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               w.y = pack_bf16(__float_as_uint(o[2]), __float_as_uint(o[3]));
               w.z = pack_bf16(__float_as_uint(o[4]), __float_as_uint(o[5]));
               w.w = pack_bf16(__float_as_uint(o[6]), __float_as_uint(o[7]));
-              srow[x] = w;
+              *stg_at(stg, lane, x) = w;
             }
             __syncwarp();
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
               const int r = it * 8 + (lane >> 2);
-              const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + (lane & 3) * 16);
+              const uint4 w = *stg_at(stg, r, lane & 3);
               __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.dst) +
                                  ((int64_t)ti * TM + (int)half * RB + q * 32 + r) * p.ldc + (int64_t)tj * 128 +
                                  32 * c2 + (lane & 3) * 8;
@@ -865,16 +884,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
+        // TMA store (row-major C / AR slot, whole tiles): the staging buffer
+        // must be read out by the previous chunk's store before it is refilled
+        const bool tma = p.tma_store && !owner;
+        if (tma) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
         // stage row `lane` (this thread's TMEM lane) as bf16
-        uint4* srow = reinterpret_cast<uint4*>(stg + lane * EPI_PITCH);
+        if (lane < RPW) {
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          uint4 w;
-          w.x = pack_bf16(v[8 * x + 0], v[8 * x + 1]);
-          w.y = pack_bf16(v[8 * x + 2], v[8 * x + 3]);
-          w.z = pack_bf16(v[8 * x + 4], v[8 * x + 5]);
-          w.w = pack_bf16(v[8 * x + 6], v[8 * x + 7]);
-          srow[x] = w;
+          for (int x = 0; x < 8; ++x) {
+            uint4 w;
+            w.x = pack_bf16(v[8 * x + 0], v[8 * x + 1]);
+            w.y = pack_bf16(v[8 * x + 2], v[8 * x + 3]);
+            w.z = pack_bf16(v[8 * x + 4], v[8 * x + 5]);
+            w.w = pack_bf16(v[8 * x + 6], v[8 * x + 7]);
+            *stg_at(stg, lane, x) = w;
+          }
+        }
+        if (tma) {
+          // the warp's RPW rows x 64 columns as one box (generic-proxy smem
+          // writes made visible to the async proxy first)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int r0 = (int)half * RB + q * RPW;
+            if (p.mode == EPI_SLOT) tma_store_2d(&tmC, stg, c * EPI_COLS, pos * TM + r0);
+            else tma_store_2d(&tmC, stg, tj * BN + c * EPI_COLS, ti * TM + r0);
+            bulk_commit();
+          }
+          continue;
         }
         __syncwarp();
         // coalesced copy-out: each instruction moves 4 rows x 128 B
@@ -882,7 +922,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int it = 0; it < RPW / 4; ++it) {
           const int r = it * 4 + (lane >> 3);
           const int ch = lane & 7;
-          const uint4 w = *reinterpret_cast<const uint4*>(stg + r * EPI_PITCH + ch * 16);
+          const uint4 w = *stg_at(stg, r, ch);
           *reinterpret_cast<uint4*>(drow[it] + c * EPI_COLS) = w;
         }
         __syncwarp();
@@ -898,7 +938,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         continue;
       }
       // all 128 epilogue threads of this CTA finished their stores -> one
-      // release add (a pair signals twice per tile: counters count half tiles)
+      // release add (a pair signals twice per tile: counters count half tiles);
+      // TMA stores are complete (not just read out) and ordered before the
+      // release by the async-proxy fence
+      if (p.tma_store && !owner && p.counters && lane == 0) {
+        bulk_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (q == 0 && lane == 0) {
         if (p.counters) red_release_add(&p.counters[p.group_of_pos[pos]], 1u);
@@ -910,6 +956,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
+  if (warp >= 4 && lane == 0 && p.tma_store) bulk_wait_all();  // the staging must outlive the stores
   tc_fence_before();
   if constexpr (CG * MC == 1) __syncthreads(); else cluster_sync();
   if (warp == 2) {
@@ -986,6 +1033,26 @@ cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
     mA2 = mA;
     mB2 = mB;
   }
+  // TMA-store epilogue for whole tiles into row-major C or AR slots: the
+  // destination as a 2-D bf16 tensor, box = 64 columns x one warp's rows
+  GemmArgs g = a;
+  CUtensorMap mC = mA;
+  g.tma_store = 0;
+  if ((a.mode == EPI_ROWMAJOR || a.mode == EPI_SLOT) && !(reinterpret_cast<uintptr_t>(a.dst) & 15) &&
+      (a.mode == EPI_SLOT || (a.ldc * 2) % 16 == 0) && a.tma_store_ok) {
+    const int64_t rows = a.mode == EPI_SLOT ? (int64_t)a.tiles * RB * CG : a.M;
+    const int64_t cols = a.mode == EPI_SLOT ? BN : a.N;
+    const int64_t pitch = a.mode == EPI_SLOT ? BN : a.ldc;
+    EncodeTiledFn enc = get_encode();
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(pitch * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)EPI_COLS, (cuuint32_t)(RB / 4)};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc && enc(&mC, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.dst, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      g.tma_store = 1;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.workers * CG);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -998,7 +1065,7 @@ cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mB, mA2, mB2, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mB, mA2, mB2, mC, g);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -422,6 +422,7 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
   // reversal to matter (measured: -12% HBM reads and -1.4% time at 4096^2 x
   // 14336; within noise or slightly slower at 16 k-blocks)
   a.k_snake = p->k_snake < 0 ? (h.K / 64 >= 64) : p->k_snake;
+  a.tma_store_ok = p->tma_store;
   if (p->wave_sync && p->split == 1 && h.T > 1) {
     a.wave_ctr = p->d_wave;
     a.wave_epoch = p->gemm_launches;
@@ -1573,6 +1574,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_WAVE_SYNC:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "wave_sync must be 0 or 1");
         p->wave_sync = (int)value;
+        break;
+      case FO_OPT_TMA_STORE:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "tma_store must be 0 or 1");
+        p->tma_store = (int)value;
         break;
       case FO_OPT_K_SNAKE:
         if (value < -1 || value > 1) fail(FO_ERR_INVALID_ARG, "k_snake must be -1, 0 or 1");

@@ -1,5 +1,5 @@
-"""FO_OPT_K_SNAKE A/B (dev tool): the GEMM with every tile's k-blocks first to
-last vs odd waves last to first, interleaved with cuBLAS, L2 flushed, device
+"""GEMM plan-option A/B (dev tool): the same GEMM with option OPT = 0 and 1
+(env AB_OPT, default k_snake), interleaved with cuBLAS, L2 flushed, device
 time medians; one line per (shape, S, tail split)."""
 import os
 import statistics
@@ -26,9 +26,10 @@ def main():
         Bt = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
         C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         plans = []
-        for snake in (0, 1):
+        opt = os.environ.get("AB_OPT", "k_snake")
+        for v in (0, 1):
             p = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0,
-                        options={"tail_split": ts, "k_snake": snake} if ts else {"k_snake": snake})
+                        options={"tail_split": ts, opt: v} if ts else {opt: v})
             plans.append(p)
         fns = [lambda p=p: fo.gemm_stage(p, A, Bt, C) for p in plans] + [lambda: torch.matmul(A, Bt.t(), out=C)]
         for f in fns:
@@ -48,9 +49,9 @@ def main():
                 ts_[i].append(s.elapsed_time(e) * 1e3)
         med = [statistics.median(v) for v in ts_]
         fl = 2.0 * M * N * K
-        print(f"{M}x{N}x{K} S={S} ts={ts}: forward {med[0]:8.2f} us ({fl / med[0] / 1e6:6.0f} TF/s)  "
-              f"snake {med[1]:8.2f} us ({fl / med[1] / 1e6:6.0f} TF/s)  cuBLAS {med[2]:8.2f} us  "
-              f"snake/forward {med[1] / med[0]:.4f}", flush=True)
+        print(f"{M}x{N}x{K} S={S} ts={ts}: {opt}=0 {med[0]:8.2f} us ({fl / med[0] / 1e6:6.0f} TF/s)  "
+              f"{opt}=1 {med[1]:8.2f} us ({fl / med[1] / 1e6:6.0f} TF/s)  cuBLAS {med[2]:8.2f} us  "
+              f"ratio 1/0 {med[1] / med[0]:.4f}", flush=True)
 
 
 if __name__ == "__main__":

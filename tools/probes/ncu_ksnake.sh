@@ -1,7 +1,7 @@
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()"
-timeout 600 python tools/ksnake_probe.py > gpurun_out/ksnake.txt 2>&1; cat gpurun_out/ksnake.txt
+timeout 600 python tools/gemm_ab_probe.py > gpurun_out/ksnake.txt 2>&1; cat gpurun_out/ksnake.txt
 # dram bytes of the bench shape, forward vs snake
 cat > /tmp/one.py <<'PY'
 import sys, torch
