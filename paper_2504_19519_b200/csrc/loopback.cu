@@ -52,7 +52,11 @@ namespace {
 
 constexpr int kRing = 64;           // mailbox / descriptor slots per rank
 constexpr int kMaxDesc = 8192;      // p2p descriptors per (slot, rank)
-constexpr int kCtas = 8;            // CTAs per loopback call
+// CTAs per loopback call and rank: every CTA of a call on every rank must be
+// resident at once (they meet at the barrier), so W * ctas stays at 128
+// (beside the ranks' GEMMs, which leave no registers for these kernels on
+// their SMs)
+inline int lb_ctas(int world) { return world >= 32 ? 4 : (128 / world > 32 ? 32 : 128 / world); }
 constexpr unsigned long long kTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
 enum LbKind : int { LB_ALLREDUCE = 0, LB_REDUCESCATTER = 1, LB_ALLGATHER = 2, LB_P2P = 3 };
@@ -75,7 +79,7 @@ struct LbMail {
 
 struct LbArgs {
   int kind, rank, world, slot;
-  unsigned target;           // W * kCtas * (uses of this slot so far, this one included)
+  unsigned target;           // W * ctas * (uses of this slot so far, this one included)
   const void* src;
   void* dst;
   long long count;
@@ -85,6 +89,7 @@ struct LbArgs {
   unsigned* ctr;             // device [kRing][2] arrive / depart (monotone)
   int* err;                  // device: first error code
   const int* abort_flag;     // pinned host, mapped: set by abort()
+  int trace;                 // FO_LOOPBACK_TRACE=2: per-call phase times from CTA 0
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -117,7 +122,7 @@ __device__ void barrier(const LbArgs& a, unsigned* c) {
     red_release(c, 1u);
     const unsigned long long t0 = now_ns();
     while ((int)(ld_acquire(c) - a.target) < 0) {
-      if (*(volatile const int*)a.abort_flag) break;
+      if (*(volatile const int*)a.abort_flag) break;  // (host-mapped: one PCIe read per spin, thread 0 only)
       if (now_ns() - t0 > kTimeoutNs) {
         printf("loopback rank %d kind %d slot %d: barrier %s counter %u target %u (waiting since t=%llu ms)\n",
                a.rank, a.kind, a.slot, (c == a.ctr + (size_t)a.slot * 2) ? "arrive" : "depart", ld_acquire(c),
@@ -138,9 +143,29 @@ __device__ __forceinline__ unsigned short f2b(float f) {  // round to nearest ev
   return (unsigned short)(u >> 16);
 }
 
+// grid-wide copy of n bf16: 16-byte vectors, 4 in flight per thread, when aligned
+__device__ void lb_copy(unsigned short* __restrict__ dst, const unsigned short* __restrict__ src, long long n,
+                        long long tid, long long nthr) {
+  if (n % 8 == 0 && !(reinterpret_cast<uintptr_t>(dst) & 15) && !(reinterpret_cast<uintptr_t>(src) & 15)) {
+    const long long step = 8 * nthr;
+    for (long long e0 = 8 * tid; e0 < n; e0 += 4 * step) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e0 + u * step < n) v[u] = *reinterpret_cast<const uint4*>(src + e0 + u * step);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e0 + u * step < n) *reinterpret_cast<uint4*>(dst + e0 + u * step) = v[u];
+    }
+  } else {
+    for (long long e = tid; e < n; e += nthr) dst[e] = src[e];
+  }
+}
+
 __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a) {
   LbMail* mail = a.mail + (size_t)a.slot * a.world;
   unsigned* ctr = a.ctr + (size_t)a.slot * 2;
+  const unsigned long long t_start = (a.trace && threadIdx.x == 0) ? now_ns() : 0ull;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     LbMail m;
     m.src = a.src;
@@ -153,7 +178,13 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a) {
     __threadfence();
   }
   barrier(a, ctr + 0);
-  if (*(volatile const int*)a.abort_flag) return;
+  const unsigned long long t_arrived = (a.trace && threadIdx.x == 0) ? now_ns() : 0ull;
+  {
+    __shared__ int s_abort;
+    if (threadIdx.x == 0) s_abort = *(volatile const int*)a.abort_flag;
+    __syncthreads();
+    if (s_abort) return;
+  }
   // every rank must be in the same kind of call with the same count
   if (threadIdx.x == 0 && blockIdx.x == 0)
     for (int q = 0; q < a.world; ++q) {
@@ -163,55 +194,106 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nthr = (long long)gridDim.x * blockDim.x;
   const int W = a.world;
-  if (a.kind == LB_ALLREDUCE) {
-    const long long lo = a.count * a.rank / W, hi = a.count * (a.rank + 1) / W;
-    for (long long e = lo + tid; e < hi; e += nthr) {
-      float acc = 0.f;
-      for (int q = 0; q < W; ++q) acc += b2f(reinterpret_cast<const unsigned short*>(mail[q].src)[e]);
-      const unsigned short v = f2b(acc);
-      for (int q = 0; q < W; ++q) reinterpret_cast<unsigned short*>(mail[q].dst)[e] = v;
+  // 16-byte vectors (8 bf16) when every pointer and the count allow it
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  if (a.kind == LB_ALLREDUCE || a.kind == LB_REDUCESCATTER) {
+    const bool ar = a.kind == LB_ALLREDUCE;
+    // the ranks' pointers, once (the mailbox is global memory the stores
+    // below might alias, so the compiler would reload it every element)
+    __shared__ const unsigned short* s_src[64];
+    __shared__ unsigned short* s_dst[64];
+    if (threadIdx.x < W) {
+      s_src[threadIdx.x] = reinterpret_cast<const unsigned short*>(mail[threadIdx.x].src);
+      s_dst[threadIdx.x] = reinterpret_cast<unsigned short*>(mail[threadIdx.x].dst);
     }
-  } else if (a.kind == LB_REDUCESCATTER) {
-    const long long off = a.count * a.rank;
-    for (long long e = tid; e < a.count; e += nthr) {
-      float acc = 0.f;
-      for (int q = 0; q < W; ++q) acc += b2f(reinterpret_cast<const unsigned short*>(mail[q].src)[off + e]);
-      reinterpret_cast<unsigned short*>(a.dst)[e] = f2b(acc);
+    __syncthreads();
+    // AllReduce: rank r reduces chunk r of the range into EVERY rank's buffer;
+    // ReduceScatter: rank r reduces block r of the sources into its own buffer
+    const long long lo = ar ? a.count * a.rank / W : 0, hi = ar ? a.count * (a.rank + 1) / W : a.count;
+    const long long soff = ar ? 0 : a.count * a.rank;
+    unsigned short* mydst = reinterpret_cast<unsigned short*>(a.dst);
+    bool vec = (a.count % 8 == 0) && (lo % 8 == 0) && (hi % 8 == 0) && al16(mydst);
+    for (int q = 0; q < W && vec; ++q) vec = al16(s_src[q]) && (ar ? al16(s_dst[q]) : true);
+    if (vec) {
+      constexpr int U = 4;  // vectors per thread in flight
+      const long long step = 8 * nthr;
+      for (long long e0 = lo + 8 * tid; e0 < hi; e0 += U * step) {
+        float acc[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
+        for (int q = 0; q < W; ++q) {
+          uint4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const long long e = e0 + u * step;
+            if (e < hi) v[u] = *reinterpret_cast<const uint4*>(s_src[q] + soff + e);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const unsigned short* h = reinterpret_cast<const unsigned short*>(&v[u]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[u][i] += b2f(h[i]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long e = e0 + u * step;
+          if (e >= hi) continue;
+          uint4 o;
+          unsigned short* ho = reinterpret_cast<unsigned short*>(&o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ho[i] = f2b(acc[u][i]);
+          if (ar) {
+            for (int q = 0; q < W; ++q) *reinterpret_cast<uint4*>(s_dst[q] + e) = o;
+          } else {
+            *reinterpret_cast<uint4*>(mydst + e) = o;
+          }
+        }
+      }
+    } else {
+      for (long long e = lo + tid; e < hi; e += nthr) {
+        float acc = 0.f;
+        for (int q = 0; q < W; ++q) acc += b2f(s_src[q][soff + e]);
+        const unsigned short v = f2b(acc);
+        if (ar) {
+          for (int q = 0; q < W; ++q) s_dst[q][e] = v;
+        } else {
+          mydst[e] = v;
+        }
+      }
     }
   } else if (a.kind == LB_ALLGATHER) {
     for (int q = 0; q < W; ++q)
-      for (long long e = tid; e < a.count; e += nthr)
-        reinterpret_cast<unsigned short*>(a.dst)[q * a.count + e] =
-            reinterpret_cast<const unsigned short*>(mail[q].src)[e];
+      lb_copy(reinterpret_cast<unsigned short*>(a.dst) + q * a.count,
+              reinterpret_cast<const unsigned short*>(mail[q].src), a.count, tid, nthr);
   } else {
-    __shared__ long long s_src_idx;
-    for (int i = blockIdx.x; i < a.ndesc; i += gridDim.x) {
+    // every receive of mine: the matching send of the peer (k-th receive
+    // from s = k-th send from s to me, counts equal), copied by all CTAs
+    for (int i = 0; i < a.ndesc; ++i) {
       const LbDesc d = a.desc[i];
       if (d.kind != 1) continue;
-      if (threadIdx.x == 0) {
-        // k = number of my receives from d.peer before i
-        int k = 0;
-        for (int t = 0; t < i; ++t) k += (a.desc[t].kind == 1 && a.desc[t].peer == d.peer);
-        const LbMail ms = mail[d.peer];
-        long long found = -1;
-        for (int t = 0, seen = 0; t < ms.ndesc; ++t) {
-          const LbDesc sd = ms.desc[t];
-          if (sd.kind == 0 && sd.peer == a.rank) {
-            if (seen == k) {
-              found = t;
-              break;
-            }
-            ++seen;
+      int k = 0;
+      for (int t = 0; t < i; ++t) k += (a.desc[t].kind == 1 && a.desc[t].peer == d.peer);
+      const LbMail ms = mail[d.peer];
+      long long found = -1;
+      for (int t = 0, seen = 0; t < ms.ndesc; ++t) {
+        const LbDesc sd = ms.desc[t];
+        if (sd.kind == 0 && sd.peer == a.rank) {
+          if (seen == k) {
+            found = t;
+            break;
           }
+          ++seen;
         }
-        if (found < 0 || ms.desc[found].count != d.count) fail_trap(a.err, 3000 + d.peer);
-        s_src_idx = found;
       }
-      __syncthreads();
-      const unsigned short* src = reinterpret_cast<const unsigned short*>(mail[d.peer].desc[s_src_idx].ptr);
-      unsigned short* dst = reinterpret_cast<unsigned short*>(d.ptr);
-      for (long long e = threadIdx.x; e < d.count; e += blockDim.x) dst[e] = src[e];
-      __syncthreads();
+      if (found < 0 || ms.desc[found].count != d.count) {
+        if (threadIdx.x == 0) fail_trap(a.err, 3000 + d.peer);
+        return;
+      }
+      lb_copy(reinterpret_cast<unsigned short*>(d.ptr), reinterpret_cast<const unsigned short*>(ms.desc[found].ptr),
+              d.count, tid, nthr);
     }
     // every send of mine must be received by its peer (else the peer's
     // receive list is short: NCCL would hang)
@@ -226,7 +308,12 @@ __global__ void __launch_bounds__(256) lb_kernel(const LbArgs a) {
       }
   }
   __threadfence();
+  const unsigned long long t_moved = (a.trace && threadIdx.x == 0) ? now_ns() : 0ull;
   barrier(a, ctr + 1);
+  if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("[lb] rank %d cta %d kind %d count %lld: arrive %.1f us, move %.1f us, depart %.1f us\n", a.rank,
+           blockIdx.x, a.kind, a.count, (t_arrived - t_start) / 1e3, (t_moved - t_arrived) / 1e3,
+           (now_ns() - t_moved) / 1e3);
 }
 
 }  // namespace
@@ -260,9 +347,11 @@ struct LoopbackComm final : Comm {
   std::vector<LbDesc> pending;
   cudaEvent_t slot_done[kRing] = {};
   bool trace_ = false;
+  int trace_level_ = 0;
   LoopbackComm(LoopbackGroup* g_, int r_) : g(g_), r(r_) {
     const char* t = getenv("FO_LOOPBACK_TRACE");
-    trace_ = t && t[0] == '1';
+    trace_level_ = t ? atoi(t) : 0;
+    trace_ = trace_level_ == 1;
   }
   ~LoopbackComm() override {
     for (auto& e : slot_done)
@@ -278,7 +367,7 @@ struct LoopbackComm final : Comm {
   // overwritten
   int next_slot(unsigned* target) {
     const int slot = (int)(seq % kRing);
-    *target = (unsigned)(g->world * kCtas) * (unsigned)(seq / kRing + 1);
+    *target = (unsigned)(g->world * lb_ctas(g->world)) * (unsigned)(seq / kRing + 1);
     ++seq;
     if (slot_done[slot]) {
       cudaError_t e = cudaEventSynchronize(slot_done[slot]);
@@ -302,6 +391,7 @@ struct LoopbackComm final : Comm {
     a.ctr = g->ctr;
     a.err = g->err;
     a.abort_flag = g->abort_flag;
+    a.trace = trace_level_ >= 2;
     if (desc) {
       if ((int)desc->size() > kMaxDesc) fail(FO_ERR_UNSUPPORTED, "loopback: %zu p2p calls in one group", desc->size());
       LbDesc* slot_desc = g->arena + ((size_t)a.slot * g->world + r) * kMaxDesc;
@@ -312,7 +402,7 @@ struct LoopbackComm final : Comm {
     if (trace_)
       fprintf(stderr, "[loopback] t=%llu ms rank %d call %llu slot %d kind %d count %lld ndesc %d stream %p\n",
               wall_ms(), r, seq - 1, a.slot, kind, count, a.ndesc, (void*)s);
-    lb_kernel<<<kCtas, 256, 0, s>>>(a);
+    lb_kernel<<<lb_ctas(g->world), 256, 0, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(FO_ERR_CUDA, "loopback launch: %s", cudaGetErrorString(e));
     count_launch();

@@ -79,10 +79,78 @@ def chrome_trace(name, plan, t, g, S, pid):
     return ev
 
 
+def loopback(W, coll, M, N, K, S, groups, layout, trace_events=None):
+    """World-W run on one GPU through the loopback communicator (R37): every
+    rank's tile signals and, on its comm stream, each group's wait release and
+    exchange + post completion, on one clock (%globaltimer).  The exchange is
+    real (rank r's group j data reaches the other ranks while the GEMMs run)
+    but not NVLink: the loopback's kernels share the one GPU's SMs and HBM."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    grp = fo.LoopbackGroup(0, W)
+    ctxs = grp.contexts()
+    plans, As, Bts, outs, tts, gts = [], [], [], [], [], []
+    for r in range(W):
+        kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1 if layout == "rowband" else 2,
+                  group_waves=groups, ar_layout=layout)
+        pl = fo.Plan(rank=r, world=W, **kw)
+        pl.prepare(sequential=True)
+        A, Bt = synthetic.float_inputs(M, N, K, seed=100 + r, device="cuda")
+        plans.append(pl), As.append(A), Bts.append(Bt)
+        outs.append(torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda"))
+        tts.append(torch.zeros(pl.info["tiles"], dtype=torch.int64, device="cuda"))
+        gts.append(torch.zeros(2 * len(groups), dtype=torch.int64, device="cuda"))
+        pl.set_debug(tts[r], gts[r])
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    pool = ThreadPoolExecutor(W)
+
+    def each(fn):
+        def one_(r):
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(streams[r]):
+                fn(r)
+            streams[r].synchronize()
+        for f in [pool.submit(one_, r) for r in range(W)]:
+            f.result()
+    for _ in range(3):
+        each(lambda r: fo.run(ctxs[r], plans[r], As[r], Bts[r], outs[r], stream=streams[r]))
+    torch.cuda.synchronize()
+    ts = [x.cpu().numpy() for x in tts]
+    gs = [x.cpu().numpy() for x in gts]
+    t0 = min(t.min() for t in ts)
+    print(f"\nloopback world {W}: {coll} {M}x{N}x{K} S={S} groups={groups} layout={layout} (one GPU, all ranks)")
+    for r in range(W):
+        t, g = ts[r], gs[r]
+        print(f"  rank {r}: GEMM last tile signal {(t.max() - t0) / 1e3:8.1f} us")
+        for j in range(len(groups)):
+            lo, hi, _, _ = plans[r].group(j)
+            print(f"    group {j}: tiles [{lo:4d},{hi:4d}) last signal {(t[lo:hi].max() - t0) / 1e3:8.1f} us | "
+                  f"wait released {(g[2 * j] - t0) / 1e3:8.1f} us | exchange+post done {(g[2 * j + 1] - t0) / 1e3:8.1f} us")
+        if trace_events is not None:
+            trace_events += chrome_trace(f"loopback rank {r}: {coll} groups {groups}", plans[r], t, g, S, 10 + r)
+    for p in plans:
+        p.close()
+    for c in ctxs:
+        c.close()
+    grp.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--trace", default=None, help="also write a Chrome trace JSON of the first AR plans")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="world size of a one-GPU loopback run (needs CUDA_MODULE_LOADING=EAGER) instead")
     args = ap.parse_args()
+    if args.loopback:
+        torch.cuda.set_device(0)
+        events = []
+        loopback(args.loopback, "allreduce", 4096, 4096, 3584, 32, [2, 2, 4], "rowband", events)
+        loopback(args.loopback, "reducescatter", 4096, 4096, 2048, 32, [2, 2, 4], "auto", events)
+        if args.trace:
+            import json
+            with open(args.trace, "w") as f:
+                json.dump({"traceEvents": events, "displayTimeUnit": "ns"}, f)
+        return
     torch.cuda.set_device(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
