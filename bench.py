@@ -559,6 +559,11 @@ def main():
     # PAPER.md:622 perfect-overlap bound from the measured pieces: the GEMM
     # (same order, same S) and the collective of the full output / of the last
     # wave on the library's communicator
+    # the CTA cap's cost: the same collective on the uncapped communicator
+    uncapped = None
+    if world > 1:
+        uncapped = [[sz] + [round(x, 1) for x in ctx_seq.time_collective_bw("allreduce", sz, 5)]
+                    for sz in (1 << 22, 1 << 23, 1 << 24, S_B)]
     comm_full_us = ctx.time_collective("allreduce", S_B, 5)
     last_wave_bytes = (tiles_c - (T - 1) * S) * BMc * BNc * 2
     comm_last_us = ctx.time_collective("allreduce", last_wave_bytes, 5)
@@ -623,6 +628,8 @@ def main():
                                       "comm": f"library communicator, maxCTAs={comm_sms if world > 1 else 'default'}",
                                       "points": [[int(b), round(a, 1), round(bb, 1)] for b, a, bb in curve_bw]}
                                      if curve_bw else None),
+            "nccl_allreduce_uncapped": ({"unit": "bytes, us, busbw GB/s", "comm": "NCCL default CTA count",
+                                         "points": uncapped} if uncapped else None),
             "alg1_predicted_us": round(pred, 2), "spot_check": spot,
             "fused_add_rmsnorm": {"overlapped_us": round(m["ov_norm"], 2), "sequential_us": round(m["seq_norm"], 2),
                                   "speedup": round(m["seq_norm"] / m["ov_norm"], 4), "groups": list(groups_n),
