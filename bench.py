@@ -556,14 +556,14 @@ def main():
     gemm_roof_us = flops / (peak * 1e12) * 1e6
     layer_roof_us = max(gemm_roof_us, bus_ring / (nvlink_gbs * 1e9) * 1e6)
     layer_roof_nvls_us = max(gemm_roof_us, bus_nvls / (nvlink_gbs * 1e9) * 1e6)
-    # PAPER.md:622 perfect-overlap bound from the measured pieces: the GEMM
-    # (same order, same S) and the collective of the full output / of the last
-    # wave on the library's communicator
     # the CTA cap's cost: the same collective on the uncapped communicator
     uncapped = None
     if world > 1:
         uncapped = [[sz] + [round(x, 1) for x in ctx_seq.time_collective_bw("allreduce", sz, 5)]
                     for sz in (1 << 22, 1 << 23, 1 << 24, S_B)]
+    # PAPER.md:622 perfect-overlap bound from the measured pieces: the GEMM
+    # (same order, same S) and the collective of the full output / of the last
+    # wave on the library's communicator
     comm_full_us = ctx.time_collective("allreduce", S_B, 5)
     last_wave_bytes = (tiles_c - (T - 1) * S) * BMc * BNc * 2
     comm_last_us = ctx.time_collective("allreduce", last_wave_bytes, 5)
