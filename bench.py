@@ -261,6 +261,18 @@ def main():
         uid = fo.unique_id()
     with _StdoutToStderr():
         ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
+    # a second overlapped-op communicator with a wider CTA cap: the tuner
+    # searches the SM split (GEMM workers vs NCCL CTAs) across both
+    ctxs = [ctx]
+    if world > 1:
+        if use_dist:
+            obj = [fo.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid2 = obj[0]
+        else:
+            uid2 = fo.unique_id()
+        with _StdoutToStderr():
+            ctxs.append(fo.Context.create(local, rank, world, uid2, nccl_max_ctas=max(comm_sms + 12, 32)))
     # the sequential baseline's NCCL call runs alone, so it gets NCCL's default
     # CTA count (its own communicator) instead of the overlapped op's SM cap
     if world > 1:
@@ -372,10 +384,11 @@ def main():
         nspec = dict(spec, post="add_rmsnorm")
         pred_n = pred
         curve_bw = None
+        nctx = ctx
     else:
         shapes = [(BM, BN), (128, 256)]      # CTA-pair 256x256 and single-CTA 128x256 tiles
-        ch = fot.tune_layer(M, N, K, ctx, "allreduce", "none", device=local, tile_shapes=shapes)
-        chn = fot.tune_layer(M, N, K, ctx, "allreduce", "add_rmsnorm", device=local, tile_shapes=shapes)
+        ch = fot.tune_layer(M, N, K, ctxs, "allreduce", "none", device=local, tile_shapes=shapes)
+        chn = fot.tune_layer(M, N, K, ctxs, "allreduce", "add_rmsnorm", device=local, tile_shapes=shapes)
         if rank == 0:
             for name, c in (("plain", ch), ("fused", chn)):
                 for cand in c.candidates[:6]:
@@ -384,6 +397,7 @@ def main():
                           file=sys.stderr)
         S, groups, pred = ch.workers, tuple(ch.groups), ch.predicted_us
         curve_bw = ch.curve
+        ctx, nctx = ctxs[ch.ctx_index], ctxs[chn.ctx_index]   # the communicators the tuner chose
         spec, nspec, pred_n = ch.spec(M, N, K, "allreduce"), chn.spec(M, N, K, "allreduce", "add_rmsnorm"), \
             chn.predicted_us
     # the chosen tile shape (tune_layer searches it; the explicit --workers /
@@ -438,7 +452,7 @@ def main():
         m = timed_multi({"ov": lambda: fo.run(ctx, plan, A, Bt, out),
                          "seq": lambda: fo.run_sequential(ctx_seq, seqplan, A, Bt, out),
                          "gemm": lambda: fo.gemm_stage(gplan, A, Bt, out),
-                         "ov_norm": lambda: fo.run(ctx, nplan, A, Bt, out2, resid, gamma),
+                         "ov_norm": lambda: fo.run(nctx, nplan, A, Bt, out2, resid, gamma),
                          "seq_norm": lambda: fo.run_sequential(ctx_seq, nseqplan, A, Bt, out2, resid, gamma),
                          # library comparator (not on the product path): the same GEMM through cuBLAS
                          "cublas": lambda: torch.matmul(A, Bt.t(), out=out_cb)},
@@ -594,7 +608,8 @@ def main():
             "ms_per_step": round(ov_us / 1e3, 4), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) weights)",
             "config": {**{k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective")},
-                       "tile": f"{BMc}x{BNc}", "workers": S, "comm_sms": sms - cgc * S, "nccl_max_ctas": comm_sms if world > 1 else None,
+                       "tile": f"{BMc}x{BNc}", "workers": S, "comm_sms": sms - cgc * S,
+                       "nccl_max_ctas": getattr(ctx, "nccl_max_ctas", None) if world > 1 else None,
                        "waves": T, "groups": list(groups), "swizzle_order": "auto (DESIGN.md R25)",
                        "tail_split": (spec.get("options") or {}).get("tail_split", 0),
                        "ar_layout": "rowband" if plan.info["ar_layout"] == 1 else "slot",
@@ -625,7 +640,8 @@ def main():
                                                "first-wave GEMM + full comm"},
             "step_stats_us": {k: main_stats.get(k) for k in ("ov", "seq", "gemm", "cublas")},
             "nccl_allreduce_curve": ({"unit": "bytes, algbw GB/s, busbw GB/s (nccl-tests convention)",
-                                      "comm": f"library communicator, maxCTAs={comm_sms if world > 1 else 'default'}",
+                                      "comm": f"library communicator, maxCTAs="
+                                              f"{getattr(ctx, 'nccl_max_ctas', 0) if world > 1 else 'default'}",
                                       "points": [[int(b), round(a, 1), round(bb, 1)] for b, a, bb in curve_bw]}
                                      if curve_bw else None),
             "nccl_allreduce_uncapped": ({"unit": "bytes, us, busbw GB/s", "comm": "NCCL default CTA count",
@@ -667,7 +683,8 @@ def main():
         print(json.dumps(line), flush=True)
     if ctx_seq is not ctx:
         ctx_seq.close()
-    ctx.close()
+    for c in ctxs:
+        c.close()
     if use_dist:
         dist.destroy_process_group()
 

@@ -222,6 +222,7 @@ class Context:
         check(load().fo_ctx_create_config(device, rank, world, buf, C.byref(cfg), C.byref(h)))
         ctx = cls(h, device, rank, world)
         ctx.buffers = buffers
+        ctx.nccl_max_ctas = int(nccl_max_ctas)
         return ctx
 
     def mem_alloc(self, shape, dtype=None):

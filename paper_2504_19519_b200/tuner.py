@@ -246,7 +246,8 @@ class LayerChoice:
     tail_split: int = 0  # FO_OPT_TAIL_SPLIT of the chosen plan (0 off, -1 auto)
     tile_m: int = TILE_M
     tile_n: int = TILE_N
-    curve: list = field(default_factory=list)  # (bytes, algbw GB/s, busbw GB/s) on the context's communicator
+    curve: list = field(default_factory=list)  # (bytes, algbw GB/s, busbw GB/s) on the chosen context's communicator
+    ctx_index: int = 0   # which of the contexts passed to tune_layer (their NCCL CTA caps) the plan runs on
 
     def spec(self, M, N, K, coll, post="none") -> dict:
         d = dict(coll=coll, m=M, n=N, k=K, tile_m=self.tile_m, tile_n=self.tile_n, workers=self.workers,
@@ -299,21 +300,37 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     then run for real (fo_run) and the fastest wins: the predictor does not
     model the contention between the GEMM and per-group post kernels.  At world > 1 every decision is rank 0's
     (broadcast over the default process group) so all ranks build the same
-    plan."""
+    plan.
+
+    `ctx` may be a list of contexts on the same ranks whose communicators
+    differ in their NCCL CTA cap (`nccl_max_ctas`): the SM split between the
+    persistent GEMM and the collective is then
+    searched too — every S that leaves a context's CTAs their SMs is a
+    candidate with that context's sampled curve, and the measured
+    verification picks the context (`LayerChoice.ctx_index`)."""
     import torch
 
     from . import post_stage
 
     sms = device_sm_count(device)
+    ctxs = list(ctx) if isinstance(ctx, (list, tuple)) else [ctx]
+    ctx = ctxs[0]
     world = ctx.world
+    caps = [int(getattr(c, "nccl_max_ctas", 0) or 0) for c in ctxs]
     # tile shapes searched (PAPER.md:460 leaves the GEMM configuration to the
     # tuner; SURVEY §8 a8): those that tile the output and, for RS, split by world
     shapes = [(tm, tn) for tm, tn in (tile_shapes or [(tile_m, tile_n)])
               if M % tm == 0 and N % tn == 0 and (coll != "reducescatter" or tm % world == 0)]
     if not shapes:
         raise ValueError("no tile shape divides the layer")
-    curve_bw = ctx.sample_curve_bw(coll, sizes or [1 << s for s in range(18, 28)], iters=3)
-    curve = [(b, alg) for b, alg, _ in curve_bw]
+    curves_bw = [c.sample_curve_bw(coll, sizes or [1 << s for s in range(18, 28)], iters=3) for c in ctxs]
+    curves = [[(b, alg) for b, alg, _ in cb] for cb in curves_bw]
+
+    def ctx_ok(ci, S, cg):
+        """S leaves the SMs context ci's collective needs (world 1: anything)."""
+        if world == 1:
+            return True
+        return sms - cg * S >= max(min_comm_sms, caps[ci])
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     Bt = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     out_rows = M if coll == "allreduce" else M // world
@@ -352,7 +369,7 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         key = (layout, op, tm, tn)
         if key not in post_cache:
             t_ = (M // tm) * (N // tn)
-            pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tm, tile_n=tn, workers=min(t_, sms // (tm // 128)),
+            pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tm, tile_n=tn, workers=min(t_, sms // max(1, tm // 128)),
                       swizzle=1, ar_layout=layout if coll == "allreduce" else "auto", post=op, rank=ctx.rank,
                       world=world)
             recv = torch.zeros(pl.info["recv_elems"], dtype=torch.bfloat16, device="cuda")
@@ -369,12 +386,15 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     for tm, tn in shapes:
         Nt = N // tn
         tiles = (M // tm) * Nt
-        cg = tm // 128
+        cg = max(1, tm // 128)
         cands = candidate_workers(tiles, Nt, sms, coll, cg)
         if world > 1:
             # the collective's kernels need SMs the persistent GEMM leaves free
-            # (Alg. 1 line 3); without them nothing overlaps
-            cands = [c for c in cands if sms - cg * c >= min_comm_sms] or [min(cands)]
+            # (Alg. 1 line 3); without them nothing overlaps.  Each context's
+            # widest S that leaves its CTAs their SMs is a candidate too
+            cands = sorted(set(cands) | {(sms - max(min_comm_sms, c)) // cg for c in caps})
+            cands = [c for c in cands if c >= 1 and any(ctx_ok(ci, c, cg) for ci in range(len(ctxs)))] \
+                or [min(cands)]
         for S in cands:
             T = -(-tiles // S)
             for layout in layouts:
@@ -398,18 +418,21 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         per_group_op = post if (layout == "rowband" or not norm) else "none"
         per_group = post_us(layout if layout != "auto" else "slot", per_group_op, tm, tn) / out_bytes
         tail = post_us("slot", post, tm, tn) if (layout != "rowband" and norm) else 0.0
-        eff = effective_curve(curve, per_group)
-        if single_only:
-            pred = tune_predict([T], dur, tiles, S, tm * tn * 2, eff)
-            evaluated.append((S, layout, [T], pred + tail, dur, swz, split, tm, tn))
-            continue
-        G, pred = tune_search(dur, tiles, S, tm * tn * 2, eff)
-        evaluated.append((S, layout, list(G), pred + tail, dur, swz, split, tm, tn))
-        if T <= all_partitions_T:
-            for comp in compositions(T):
-                if comp != list(G):
-                    p2 = tune_predict(comp, dur, tiles, S, tm * tn * 2, eff)
-                    evaluated.append((S, layout, comp, p2 + tail, dur, swz, split, tm, tn))
+        for ci in range(len(ctxs)):
+            if not ctx_ok(ci, S, max(1, tm // 128)):
+                continue
+            eff = effective_curve(curves[ci], per_group)
+            if single_only:
+                pred = tune_predict([T], dur, tiles, S, tm * tn * 2, eff)
+                evaluated.append((S, layout, [T], pred + tail, dur, swz, split, tm, tn, ci))
+                continue
+            G, pred = tune_search(dur, tiles, S, tm * tn * 2, eff)
+            evaluated.append((S, layout, list(G), pred + tail, dur, swz, split, tm, tn, ci))
+            if T <= all_partitions_T:
+                for comp in compositions(T):
+                    if comp != list(G):
+                        p2 = tune_predict(comp, dur, tiles, S, tm * tn * 2, eff)
+                        evaluated.append((S, layout, comp, p2 + tail, dur, swz, split, tm, tn, ci))
     import torch.distributed as dist
 
     def agree(obj):
@@ -428,7 +451,7 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     nv = max(1, verify)
     chosen = []
     for e in evaluated:
-        if not any(c[0] == e[0] and c[1] == e[1] and c[6:9] == e[6:9] for c in chosen):
+        if not any(c[0] == e[0] and c[1] == e[1] and c[6:10] == e[6:10] for c in chosen):
             chosen.append(e)
     single = [e for e in evaluated if len(e[2]) == 1]
     if single:
@@ -446,21 +469,22 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
 
     # verification: the candidates' fo_run timed round-robin, medians
     runs = []
-    for (S, layout, G, pred, dur, swz, split, tm, tn) in evaluated[:nv]:
+    for (S, layout, G, pred, dur, swz, split, tm, tn, ci) in evaluated[:nv]:
         spec = dict(coll=coll, m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S, swizzle=swz,
                     group_waves=G, ar_layout=layout if layout != "auto" else "auto", post=post)
         pl = Plan(rank=ctx.rank, world=world, options={"tail_split": split} if split else None, **spec)
         o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
         args = (res, gam) if post != "none" else (None, None)
-        runs.append((pl, o, args))
-    measured = timeit_many([(lambda r=r: fo_run(ctx, r[0], A, Bt, r[1], *r[2])) for r in runs], max(3, iters))
+        runs.append((pl, o, args, ctxs[ci]))
+    measured = timeit_many([(lambda r=r: fo_run(r[3], r[0], A, Bt, r[1], *r[2])) for r in runs], max(3, iters))
     if world > 1 and dist.is_initialized():
         tt = torch.tensor(measured, device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         measured = tt.tolist()
     k = min(range(len(measured)), key=lambda i: measured[i])
     best = evaluated[k]
-    cands = [(e[0], f"{e[7]}x{e[8]}:" + e[1] + ("+tailsplit" if e[6] else ""), e[2], e[3], e[4]) +
+    cands = [(e[0], f"{e[7]}x{e[8]}:" + e[1] + ("+tailsplit" if e[6] else "") +
+              (f"+ctas{caps[e[9]]}" if len(ctxs) > 1 else ""), e[2], e[3], e[4]) +
              ((measured[i],) if i < len(measured) else ()) for i, e in enumerate(evaluated)]
     return LayerChoice(best[0], best[5], best[2], best[1], best[3], best[4], cands, best[6], best[7], best[8],
-                       curve_bw)
+                       curves_bw[best[9]], best[9])

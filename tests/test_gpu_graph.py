@@ -219,6 +219,16 @@ def test_tune_layer_world1_returns_a_valid_plan():
         torch.cuda.synchronize()
     ch = tuner.tune_layer(M, N, K, ctx, "reducescatter", "none", iters=3, sizes=[1 << 18, 1 << 22])
     assert ch.layout == "auto"
+    # two communicators (CTA caps): the SM split is searched across both and
+    # the chosen context's index comes back
+    ctx2 = fo.Context.create(0, 0, 1, fo.unique_id(), nccl_max_ctas=32)
+    ch = tuner.tune_layer(M, N, K, [ctx, ctx2], "allreduce", "none", iters=3, sizes=[1 << 18, 1 << 22])
+    assert ch.ctx_index in (0, 1)
+    assert any("+ctas32" in c[1] for c in ch.candidates) and any("+ctas0" in c[1] for c in ch.candidates)
+    plan = fo.Plan(**ch.spec(M, N, K, "allreduce"))
+    fo.run([ctx, ctx2][ch.ctx_index], plan, A, Bt, out)
+    torch.cuda.synchronize()
+    ctx2.close()
     ctx.close()
 
 
