@@ -11,7 +11,8 @@ At --gpus 1 this is TP=1 (K=14336, the AllReduce is a 1-rank NCCL call).
 
 One JSON line on rank 0.  Timing: W untimed warm-up steps, then K steps, each
 bracketed by (barrier,) an L2 flush (256 MiB write, outside the timed span) and
-CUDA events on the launching stream; per-step device time, max over ranks.
+CUDA events on the launching stream; per-step device time, max over ranks;
+the value is the median step (mean, p10, p90 in step_stats_us).
 """
 from __future__ import annotations
 
@@ -315,12 +316,12 @@ def main():
             e.record()
             torch.cuda.synchronize()
             ts.append(s.elapsed_time(e) * 1e3)
-        mean = statistics.mean(ts)
+        med = statistics.median(ts)
         if use_dist:
-            t = torch.tensor([mean], device="cuda", dtype=torch.float64)
+            t = torch.tensor([med], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            mean = t.item()
-        return mean, ts
+            med = t.item()
+        return med, ts
 
     def dist_stats(v):
         q = sorted(v)
@@ -352,17 +353,16 @@ def main():
                 e.record()
                 torch.cuda.synchronize()
                 ts[k].append(s.elapsed_time(e) * 1e3)
-        means = {k: statistics.mean(v) for k, v in ts.items()}
         if use_dist:
-            t = torch.tensor([means[k] for k in fns], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            means = {k: t[i].item() for i, k in enumerate(fns)}
-            # per-step max over ranks for the distribution statistics
+            # per-step max over ranks (a step ends when its slowest rank does)
             ts_t = torch.tensor([ts[k] for k in fns], device="cuda", dtype=torch.float64)
             dist.all_reduce(ts_t, op=dist.ReduceOp.MAX)
             ts = {k: ts_t[i].tolist() for i, k in enumerate(fns)}
         stats_out.update({k: dist_stats(v) for k, v in ts.items()})
-        return means
+        # the median step: a host stall longer than the ~100 us preload (e.g.
+        # while nvidia-smi samples the clocks) inflates one step by
+        # milliseconds and would dominate a mean of 20
+        return {k: statistics.median(v) for k, v in ts.items()}
 
     # ---- offline + online stages of Alg. 1 (untimed, tuner.tune_layer): GEMM
     # duration per candidate wave width S and layout, the NCCL curve on the
@@ -616,7 +616,8 @@ def main():
                        "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"tp{world}",
                        "timing": "device time: CUDA events on the launching stream, pre-loaded by a ~100 us sleep "
                                  "kernel so host enqueue latency (~12 us per call) is excluded; e2e includes it; "
-                                 "value = mean of the timed steps (max over ranks), step_stats_us has median/p10/p90"},
+                                 "value = median of the timed steps (each the max over ranks), step_stats_us has "
+                                 "mean/p10/p90"},
             "note": ("N=1: the overlapped op is the GEMM followed by a 1-rank NCCL AllReduce that moves no data, so "
                      "speedup_vs_sequential is ~1 by construction; the multi-rank exchange runs at N>1"
                      if world == 1 else f"TP={world}: every rank's GEMM overlaps its wave groups' NCCL AllReduce"),
