@@ -423,10 +423,14 @@ def main():
     # tail), its output then one NCCL call with NCCL's default CTAs — not the
     # overlapped plan's narrower wave width
     if world > 1:
-        S_seq = sms // 2
+        # the standalone GEMM's best wave width: all pairs with the split tail
+        # for long K, the fewest pairs with the full wave count for short K
+        # (measured, profiles/r02_tp_shard_probe.txt)
+        long_k = K >= 3584
+        S_seq = sms // 2 if long_k else -(-((M // 256) * (N // 256)) // -(-((M // 256) * (N // 256)) // (sms // 2)))
         T_seq = -(-((M // 256) * (N // 256)) // S_seq)
         seq_spec = dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S_seq, swizzle=0,
-                        group_waves=[T_seq], ar_layout="auto", options={"tail_split": -1})
+                        group_waves=[T_seq], ar_layout="auto", options={"tail_split": -1} if long_k else None)
         seqplan = fo.Plan(rank=rank, world=world, **seq_spec)
         nseqplan = fo.Plan(rank=rank, world=world, **dict(seq_spec, post="add_rmsnorm"))
     else:
@@ -624,8 +628,9 @@ def main():
             "speedup_vs_sequential": round(seq_us / ov_us, 4), "sequential_us": round(seq_us, 2),
             "sequential_config": ("the overlapped plan's GEMM writing row-major C, then one NCCL AllReduce"
                                   if world == 1 else
-                                  f"GEMM alone on all {sms // 2} CTA pairs (split tail), then one NCCL AllReduce on "
-                                  "a communicator with NCCL's default CTA count"),
+                                  f"GEMM alone at its best wave width (S={seqplan.info['workers']} CTA pairs"
+                                  f"{', split tail' if K >= 3584 else ''}), then one NCCL AllReduce on a "
+                                  "communicator with NCCL's default CTA count"),
             "tflops": round(world * flops / (ov_us * 1e-6) / 1e12, 1),
             "layer_roofline_us": round(layer_roof_us, 2), "frac_of_layer_roofline": round(layer_roof_us / ov_us, 4),
             "layer_roofline": {"gemm_us": round(gemm_roof_us, 2),
