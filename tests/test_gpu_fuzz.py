@@ -1,8 +1,8 @@
 """Seeded random plans through the C ABI vs the CPU oracle (exact-integer
 regime, bit-exact): tile shape, grid, K, world size, wave width S, explicit
 random order or default swizzle, random wave partition, AllReduce (both
-layouts) or ReduceScatter, with and without TMA-multicast clusters and the
-tail split; and All-to-All with imbalanced experts and random routing.  Every
+layouts) or ReduceScatter, with and without TMA-multicast clusters, the tail
+split, the K-snake order and the TMA-store epilogue; and All-to-All with imbalanced experts and random routing.  Every
 rank's GEMM + pre-reorder epilogue (fo_gemm_stage) must equal the oracle's
 send buffer, its counters the group thresholds, and the post-reorder of the
 oracle's receive buffer (fo_post_stage) the plain GEMM -> collective result
@@ -51,8 +51,11 @@ def _draw(seed):
     tail_split = int(rng.choice([0, 0, -1, -2]))    # auto (where the last wave qualifies) / stream-K
     if BM == 64:
         tail_split = 0                               # 64-row tiles (tcgen05 M=64) run whole tiles only
+    k_snake = int(rng.choice([-1, 0, 1]))
+    tma_store = int(rng.random() < 0.7)
     return dict(BM=BM, BN=BN, M=Mt * BM, N=Nt * BN, K=K, n=n, coll=coll, S=S, part=part, order=order,
-                swizzle=swizzle, layout=layout, multicast=multicast, tail_split=tail_split)
+                swizzle=swizzle, layout=layout, multicast=multicast, tail_split=tail_split, k_snake=k_snake,
+                tma_store=tma_store)
 
 
 @pytest.mark.parametrize("seed", range(64))
@@ -74,6 +77,8 @@ def test_random_plan_matches_oracle(seed):
             pl = fo.Plan(coll="reducescatter", rank=r, world=n, **kw)
         pl.set_option("multicast", c["multicast"])
         pl.set_option("tail_split", c["tail_split"])
+        pl.set_option("k_snake", c["k_snake"])
+        pl.set_option("tma_store", c["tma_store"])
         plans.append(pl)
     # the oracle computes the execution order itself (an explicit order, or the
     # R1 swizzle of height 1..3); only swizzle 0 (auto: a library heuristic that
@@ -183,6 +188,8 @@ def test_random_run_equals_sequential(seed):
     ts = int(rng.choice([0, 0, -1, -2]))
     plan.set_option("tail_split", ts if BM != 64 else 0)   # 64-row tiles run whole tiles only
     plan.set_option("multicast", int(rng.random() < 0.3))
+    plan.set_option("k_snake", int(rng.choice([-1, 0, 1])))
+    plan.set_option("tma_store", int(rng.random() < 0.7))
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     try:
         A, Bt = synthetic.exact_inputs(M, N, K, seed=7100 + seed, nnz_per_row=128)
