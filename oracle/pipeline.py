@@ -52,12 +52,12 @@ def plain_allreduce(As, Bts, model_bf16=False):
 
 
 # ------------------------------------------------------------------ ReduceScatter
-def run_reducescatter(As, Bts, plan: Plan, model_bf16=False):
+def run_reducescatter(As, Bts, plan: Plan, layout="slot", model_bf16=False):
     n = len(As)
     Ys = [_Y(As[r], Bts[r], model_bf16) for r in range(n)]
-    bufs = [reorder.rs_pre(Ys[r], plan, n) for r in range(n)]
-    recv = collectives.reduce_scatter_groups(bufs, reorder.group_elem_ranges(plan))
-    outs = [reorder.rs_post(recv[k], plan, n) for k in range(n)]
+    bufs = [reorder.rs_pre(Ys[r], plan, n, layout) for r in range(n)]
+    recv = collectives.reduce_scatter_groups(bufs, reorder.group_elem_ranges(plan, layout))
+    outs = [reorder.rs_post(recv[k], plan, n, layout) for k in range(n)]
     return {"Y": Ys, "send": bufs, "recv": recv, "out": outs}
 
 

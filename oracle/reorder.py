@@ -21,6 +21,15 @@ indices are reordered based on their execution order".
       holds the k-th subtile of every tile of the group, tiles in execution
       order:  buf[ps*BM*BN + k*G*h*BN + q*h*BN + a'*BN + b]
                  = Y[i*BM + k*h + a', j*BN + b],   q = p - ps.
+      Layout "rowband" (R40): when the groups are the bands of whole
+      tile-rows [r0, r1) in ascending order (band j starts where band j-1
+      ends), the unit is still the k-th subtile ("the k-th subtile
+      within a tile always resides on the k-th GPU"), but chunk k of band j
+      holds the k-th subtiles as complete rows, tile-row by tile-row
+      (B = r1 - r0):
+              buf[r0*BM*N + k*B*h*N + ((i - r0)*h + a')*N + c]
+                 = Y[i*BM + k*h + a', c],   i in [r0, r1)
+      so rank k receives its block-cyclic rows R_k already in output order.
   A2A: unit = subtoken (one row of one tile, BN elements).  One
       memory pool per destination rank; subtokens are appended in execution
       order (p ascending, then row inside the tile ascending).  Group j's
@@ -52,6 +61,19 @@ def rowband_of_group(plan: Plan, lo: int, hi: int):
     if tiles != list(range(r0 * plan.Nt, r1 * plan.Nt)):
         return None
     return r0, r1
+
+
+def rs_rowband_ok(plan: Plan) -> bool:
+    """ReduceScatter rowband layout: every group is a band of complete
+    tile-rows and the bands follow each other top to bottom in group order
+    (the receive buffer concatenates the groups' chunks in group order)."""
+    nxt = 0
+    for lo, hi in plan.ranges:
+        band = rowband_of_group(plan, lo, hi)
+        if band is None or band[0] != nxt:
+            return False
+        nxt = band[1]
+    return True
 
 
 def ar_rowband_ok(plan: Plan) -> bool:
@@ -102,11 +124,23 @@ def rs_subtile_rows(plan: Plan, n: int) -> int:
     return plan.BM // n
 
 
-def rs_pre(Y: np.ndarray, plan: Plan, n: int) -> np.ndarray:
-    """O5 for ReduceScatter (formula in the module header)."""
+def rs_pre(Y: np.ndarray, plan: Plan, n: int, layout: str = "slot") -> np.ndarray:
+    """O5 for ReduceScatter (formulas in the module header)."""
     BM, BN = plan.BM, plan.BN
     h = rs_subtile_rows(plan, n)
     buf = np.empty(plan.M * plan.N, dtype=Y.dtype)
+    if layout == "rowband":
+        if not rs_rowband_ok(plan):
+            raise OracleError("RS rowband layout needs the groups to be ascending bands of complete tile-rows")
+        N = plan.N
+        for lo, hi in plan.ranges:
+            r0, r1 = rowband_of_group(plan, lo, hi)
+            B = r1 - r0
+            for k in range(n):
+                for i in range(r0, r1):
+                    off = r0 * BM * N + k * B * h * N + (i - r0) * h * N
+                    buf[off:off + h * N] = Y[i * BM + k * h:i * BM + (k + 1) * h, :].reshape(-1)
+        return buf
     for ps, pe in plan.ranges:
         G = pe - ps
         for p in range(ps, pe):
@@ -119,11 +153,15 @@ def rs_pre(Y: np.ndarray, plan: Plan, n: int) -> np.ndarray:
     return buf
 
 
-def rs_chunk(buf: np.ndarray, plan: Plan, n: int, group: int, k: int) -> np.ndarray:
+def rs_chunk(buf: np.ndarray, plan: Plan, n: int, group: int, k: int, layout: str = "slot") -> np.ndarray:
     """Chunk k of group `group`: what ReduceScatter on the group range delivers to rank k."""
     BM, BN = plan.BM, plan.BN
     h = rs_subtile_rows(plan, n)
     ps, pe = plan.ranges[group]
+    if layout == "rowband":
+        r0, r1 = rowband_of_group(plan, ps, pe)
+        off = r0 * BM * plan.N + k * (r1 - r0) * h * plan.N
+        return buf[off:off + (r1 - r0) * h * plan.N]
     G = pe - ps
     off = ps * BM * BN + k * G * h * BN
     return buf[off:off + G * h * BN]
@@ -135,13 +173,22 @@ def rs_local_to_global_row(l: int, BM: int, h: int, k: int) -> int:
     return (l // h) * BM + k * h + (l % h)
 
 
-def rs_post(recv: np.ndarray, plan: Plan, n: int) -> np.ndarray:
+def rs_post(recv: np.ndarray, plan: Plan, n: int, layout: str = "slot") -> np.ndarray:
     """O7 for ReduceScatter on one rank: the received buffer (group chunks
     concatenated in group order, each G*h*BN elements) -> local [M/n, N] rows
-    in block-cyclic order (local row i*h + a' <- tile-row i, subtile row a')."""
+    in block-cyclic order (local row i*h + a' <- tile-row i, subtile row a').
+    Rowband: band j's chunk holds local rows [r0*h, r1*h) in order."""
     BM, BN = plan.BM, plan.BN
     h = rs_subtile_rows(plan, n)
     out = np.empty((plan.M // n, plan.N), dtype=recv.dtype)
+    if layout == "rowband":
+        off = 0
+        for lo, hi in plan.ranges:
+            r0, r1 = rowband_of_group(plan, lo, hi)
+            sz = (r1 - r0) * h * plan.N
+            out[r0 * h:r1 * h, :] = recv[off:off + sz].reshape((r1 - r0) * h, plan.N)
+            off += sz
+        return out
     for ps, pe in plan.ranges:
         for p in range(ps, pe):
             q = p - ps

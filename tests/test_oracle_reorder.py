@@ -185,3 +185,77 @@ def test_a2a_errors():
         orr.a2a_pre(np.zeros((4, 4)), pl, [0, 1, 2], 2)
     with pytest.raises(op.OracleError):
         orr.a2a_pre(np.zeros((4, 4)), pl, [0, 1, 2, 0], 2)
+
+
+# ---------------------------------------------------------------- RS rowband (R40)
+def _band_plan(rng, n):
+    """A plan whose groups are ascending bands of complete tile-rows (random
+    tile order inside each band, random band sizes)."""
+    BM = int(rng.choice((1, 2))) * n
+    BN = int(rng.integers(1, 4))
+    Mt, Nt = int(rng.integers(1, 6)), int(rng.integers(1, 4))
+    rows_per_wave = int(rng.integers(1, Mt + 1))
+    S = rows_per_wave * Nt
+    T = -(-Mt // rows_per_wave)
+    part = synthetic.random_partition(T, int(rng.integers(1 << 20)))
+    order = []
+    for r in range(Mt):
+        order += [int(t) for t in rng.permutation(np.arange(r * Nt, (r + 1) * Nt))]
+    # tile-rows in ascending order, tiles of one tile-row shuffled among the band
+    return op.make_plan(Mt * BM, Nt * BN, BM, BN, S, part, order=order)
+
+
+def test_rs_rowband_hand_example():
+    """4x4 output, 2x2 tiles, n = 2 (h = 1), one group of both tile-rows:
+    chunk 0 = the k=0 subtile rows of tile-rows 0 and 1 = global rows 0, 2;
+    chunk 1 = rows 1, 3 (worked by hand from PAPER.md:390: the k-th subtile
+    of every tile goes to GPU k).  Rank 0 then holds R_0 = {0, 2}."""
+    pl = op.make_plan(4, 4, 2, 2, 4, [1], swizzle=1)
+    Y = np.repeat(np.arange(4, dtype=float)[:, None], 4, axis=1)  # value = row id
+    assert orr.rs_rowband_ok(pl)
+    buf = orr.rs_pre(Y, pl, 2, "rowband")
+    assert buf.reshape(4, 4)[:, 0].astype(int).tolist() == [0, 2, 1, 3]
+    assert orr.rs_chunk(buf, pl, 2, 0, 0, "rowband").reshape(-1, 4)[:, 0].tolist() == [0, 2]
+    assert orr.rs_chunk(buf, pl, 2, 0, 1, "rowband").reshape(-1, 4)[:, 0].tolist() == [1, 3]
+    # two groups of one tile-row each: every chunk is one row, in row order
+    pl2 = op.make_plan(4, 4, 2, 2, 2, [1, 1], swizzle=1)
+    buf2 = orr.rs_pre(Y, pl2, 2, "rowband")
+    assert buf2.reshape(4, 4)[:, 0].astype(int).tolist() == [0, 1, 2, 3]
+
+
+def test_rs_rowband_legality():
+    """Bands must be complete tile-rows AND ascending in group order."""
+    # raster, waves = whole tile-rows: legal
+    assert orr.rs_rowband_ok(op.make_plan(8, 4, 2, 2, 2, [1, 1, 1, 1], swizzle=1))
+    # tile-row 1 before tile-row 0: bands exist but descend
+    pl = op.make_plan(4, 4, 2, 2, 2, [1, 1], order=[2, 3, 0, 1])
+    assert orr.ar_rowband_ok(pl) and not orr.rs_rowband_ok(pl)
+    with pytest.raises(op.OracleError):
+        orr.rs_pre(np.zeros((4, 4)), pl, 2, "rowband")
+    # column-major inside a 2-row panel with single-wave groups of 2 tiles: not bands
+    assert not orr.rs_rowband_ok(op.make_plan(4, 4, 2, 2, 2, [1, 1], swizzle=2))
+
+
+def test_rs_rowband_equals_definition_bruteforce():
+    """Overlapped RS in the rowband layout == plain RS (rows R_k of the sum),
+    on integer data, for random band plans at n = 1..4; the layout is a
+    bijection and its receive buffer is the output itself (row-major)."""
+    rng = np.random.default_rng(40)
+    for n in (1, 2, 3, 4):
+        for _ in range(40):
+            pl = _band_plan(rng, n)
+            assert orr.rs_rowband_ok(pl)
+            K = 3
+            As = [rng.integers(-3, 4, size=(pl.M, K)).astype(float) for _ in range(n)]
+            Bts = [rng.integers(-3, 4, size=(pl.N, K)).astype(float) for _ in range(n)]
+            res = opl.run_reducescatter(As, Bts, pl, layout="rowband")
+            plain = opl.plain_reducescatter(As, Bts, pl.BM)
+            for k in range(n):
+                assert np.array_equal(res["out"][k], plain[k])
+                assert np.array_equal(res["recv"][k], res["out"][k].reshape(-1))
+            idx = orr.rs_pre(np.arange(pl.M * pl.N, dtype=float).reshape(pl.M, pl.N), pl, n, "rowband")
+            assert np.array_equal(np.sort(idx), np.arange(pl.M * pl.N))
+            # same output as the paper's subtile (slot) layout
+            slot = opl.run_reducescatter(As, Bts, pl)
+            for k in range(n):
+                assert np.array_equal(slot["out"][k], res["out"][k])
