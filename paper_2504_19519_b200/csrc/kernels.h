@@ -13,8 +13,10 @@ enum EpiMode : int {
   EPI_SLOT = 1,      // AR: tile at position p -> slot p (BM*BN contiguous, row-major)
   EPI_RS = 2,        // RS: subtile k of the tile -> chunk k of its group
   EPI_A2A = 3,       // A2A: row a of the tile -> its destination pool slot
-  EPI_SWIGLU = 4     // no-comm, BN = 256: tile columns [0,128) gate, [128,256) up (interleaved
+  EPI_SWIGLU = 4,    // no-comm, BN = 256: tile columns [0,128) gate, [128,256) up (interleaved
                      // weight rows); writes silu(gate) * up to C[:, tj*128 .. +128), row stride ldc
+  EPI_RS_BAND = 5    // RS ROWBAND (R40): row a of tile-row i (band [r0, r0+B)) -> row
+                     // r0*BM + ((a/h)*B + i - r0)*h + a%h of a row-major [M, ldc] buffer
 };
 
 // One K-range of a split tail tile (host-built table, see fo_gemm's my_unit):
@@ -41,6 +43,7 @@ struct GemmArgs {
   const int32_t* gpos;         // [P+1] device
   const int32_t* row_slot;     // [tiles*BM] device (A2A)
   const int2* rs_info;         // [tiles] device (RS): {first position, size} of the position's group
+                               // (EPI_RS_BAND: {first tile-row, tile-rows} of its band)
   uint32_t* counters;          // [P] device, may be null
   int h;                       // RS subtile rows (tile_m / world, a power of two)
   int h_log2;

@@ -350,6 +350,15 @@ __device__ __forceinline__ Unit my_unit(const GemmArgs& p, int worker, int nwork
   return r;
 }
 
+// RS ROWBAND (R40): buffer row of row `a` of tile-row `ti` in the
+// band of tile-rows [r0, r0 + B): subtile k = a / h goes to chunk k of the band
+// (rows [r0*TM + k*B*h, +B*h)), tile-row by tile-row.
+template <int TM>
+__device__ __forceinline__ int64_t rs_band_row(const GemmArgs& p, int ti, int a, int r0, int B) {
+  const int k = a >> p.h_log2, a2 = a & (p.h - 1);
+  return (int64_t)r0 * TM + ((int64_t)(k * B + (ti - r0)) << p.h_log2) + a2;
+}
+
 // Destination of row `a` (0..TM-1) of the TM x BN tile at position `pos` =
 // (ti, tj); `rs_ps` / `rs_G` = first position and size of the tile's group
 // (RS) and `a2a_slot` = row_slot[pos*TM + a] (A2A), loaded by the caller one
@@ -367,6 +376,8 @@ __device__ __forceinline__ __nv_bfloat16* row_dst(const GemmArgs& p, int pos, in
       const int k = a >> p.h_log2, a2 = a & (p.h - 1);
       return base + ((int64_t)rs_ps * TM + (((k * rs_G + (pos - rs_ps)) << p.h_log2) + a2)) * BN;
     }
+    case EPI_RS_BAND:  // DESIGN.md R40: band [rs_ps, rs_ps + rs_G) of tile-rows, chunk k = its k-th subtile rows
+      return base + rs_band_row<TM>(p, ti, a, rs_ps, rs_G) * p.ldc + (int64_t)tj * BN;
     default:  // EPI_A2A: row -> slot in its destination pool (row_slot, prefetched)
       return base + (int64_t)a2a_slot * BN;
   }
@@ -626,7 +637,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int it = 0; it < 8; ++it) nx_slot[it] = 0;
     static_assert(RPW == 32 || RPW == 16, "rows per epilogue warp");
     auto prefetch_dst = [&](int npos) {
-      if (p.mode == EPI_RS) {
+      if (p.mode == EPI_RS || p.mode == EPI_RS_BAND) {
         nx_rs = p.rs_info[npos];
       } else if (p.mode == EPI_A2A) {
 #pragma unroll
@@ -649,6 +660,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // loaded during the previous tile (no memory latency here: at short K
       // the epilogue is on the critical path)
       __nv_bfloat16* drow[8];
+      const int2 cur_rs = nx_rs;  // this tile's RS group / band (nx_rs moves on to the next tile)
 #pragma unroll
       for (int it = 0; it < RPW / 4; ++it)
         drow[it] = row_dst<TM, BN>(p, pos, ti, tj, (int)half * RB + q * RPW + it * 4 + (lane >> 3), nx_rs.x, nx_rs.y,
@@ -911,6 +923,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) {
             const int r0 = (int)half * RB + q * RPW;
             if (p.mode == EPI_SLOT) tma_store_2d(&tmC, stg, c * EPI_COLS, pos * TM + r0);
+            else if (p.mode == EPI_RS_BAND)  // h >= RPW: the warp's rows are consecutive buffer rows
+              tma_store_2d(&tmC, stg, tj * BN + c * EPI_COLS, (int)rs_band_row<TM>(p, ti, r0, cur_rs.x, cur_rs.y));
             else tma_store_2d(&tmC, stg, tj * BN + c * EPI_COLS, ti * TM + r0);
             bulk_commit();
           }
@@ -1033,13 +1047,15 @@ cudaError_t launch_cfg(const GemmArgs& a, cudaStream_t stream) {
     mA2 = mA;
     mB2 = mB;
   }
-  // TMA-store epilogue for whole tiles into row-major C or AR slots: the
-  // destination as a 2-D bf16 tensor, box = 64 columns x one warp's rows
+  // TMA-store epilogue for whole tiles into row-major C, AR slots or RS
+  // bands (when a warp's rows stay inside one subtile, h >= rows per warp):
+  // the destination as a 2-D bf16 tensor, box = 64 columns x one warp's rows
   GemmArgs g = a;
   CUtensorMap mC = mA;
   g.tma_store = 0;
-  if ((a.mode == EPI_ROWMAJOR || a.mode == EPI_SLOT) && !(reinterpret_cast<uintptr_t>(a.dst) & 15) &&
-      (a.mode == EPI_SLOT || (a.ldc * 2) % 16 == 0) && a.tma_store_ok) {
+  const bool tma_mode = a.mode == EPI_ROWMAJOR || a.mode == EPI_SLOT || (a.mode == EPI_RS_BAND && a.h >= RB / 4);
+  if (tma_mode && !(reinterpret_cast<uintptr_t>(a.dst) & 15) && (a.mode == EPI_SLOT || (a.ldc * 2) % 16 == 0) &&
+      a.tma_store_ok) {
     const int64_t rows = a.mode == EPI_SLOT ? (int64_t)a.tiles * RB * CG : a.M;
     const int64_t cols = a.mode == EPI_SLOT ? BN : a.N;
     const int64_t pitch = a.mode == EPI_SLOT ? BN : a.ldc;

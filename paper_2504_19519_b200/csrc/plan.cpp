@@ -45,9 +45,10 @@ int auto_swizzle(int Mt, int Nt, int S) {
   return best;
 }
 
-// AllReduce: prefer panel heights whose panels end exactly on the group
-// boundaries (every group is then a band of whole tile-rows -> ROWBAND layout,
-// no reorder at all) unless the unconstrained footprint is much smaller.
+// AllReduce / ReduceScatter: prefer panel heights whose panels end exactly on
+// the group boundaries (every group is then a band of whole tile-rows, panels
+// top to bottom -> ROWBAND layout, no reorder at all) unless the
+// unconstrained footprint is much smaller.
 static int auto_swizzle_ar(int Mt, int Nt, int S, const std::vector<int32_t>& gpos) {
   const int any = auto_swizzle(Mt, Nt, S);
   int band = -1;
@@ -121,8 +122,9 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
     if (d.swizzle < 0) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 0");
     int s = d.swizzle;
     if (s == 0)
-      s = (d.coll == FO_ALLREDUCE && d.ar_layout != FO_LAYOUT_SLOT) ? auto_swizzle_ar(g.Mt, g.Nt, d.workers, g.gpos)
-                                                                     : auto_swizzle(g.Mt, g.Nt, d.workers);
+      s = ((d.coll == FO_ALLREDUCE || d.coll == FO_REDUCESCATTER) && d.ar_layout != FO_LAYOUT_SLOT)
+              ? auto_swizzle_ar(g.Mt, g.Nt, d.workers, g.gpos)
+              : auto_swizzle(g.Mt, g.Nt, d.workers);
     g.order = default_order(g.Mt, g.Nt, s);
   }
   (void)world;
@@ -155,6 +157,36 @@ static A2ASide a2a_census(const fo_plan_desc& d, const Grid& g, int world) {
     }
   }
   return a;
+}
+
+// ROWBAND legality (H11a, R40): every group's tiles are exactly the
+// complete tile-rows of one contiguous band [r0, r1) (any order inside); fills
+// band_rows.  `ascending`: the bands must also follow each other top to bottom
+// in group order (ReduceScatter: the receive buffer concatenates the groups'
+// chunks, which is then the output itself).
+static bool band_layout(PlanHost& p, bool ascending) {
+  p.band_rows.assign(2 * p.P, 0);
+  int64_t next = 0;
+  for (int j = 0; j < p.P; ++j) {
+    const int lo = p.gpos[j], hi = p.gpos[j + 1];
+    if ((hi - lo) % p.Nt) return false;
+    int rmin = p.Mt, rmax = -1;
+    std::vector<char> seen((size_t)(hi - lo), 0);
+    for (int q = lo; q < hi; ++q) rmin = std::min(rmin, p.order[q] / p.Nt);
+    const int r1 = rmin + (hi - lo) / p.Nt;
+    for (int q = lo; q < hi; ++q) {
+      const int t = p.order[q] - rmin * p.Nt;
+      if (t < 0 || t >= hi - lo || seen[t]) return false;
+      seen[t] = 1;
+      rmax = std::max(rmax, p.order[q] / p.Nt);
+    }
+    if (rmax >= r1) return false;
+    if (ascending && rmin != next) return false;
+    next = r1;
+    p.band_rows[2 * j] = rmin;
+    p.band_rows[2 * j + 1] = r1;
+  }
+  return true;
 }
 
 PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_desc* const* peers,
@@ -196,28 +228,7 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
     case FO_ALLREDUCE: {
       // ROWBAND (H11a) is legal iff every group's tiles are exactly
       // the complete tile-rows of one contiguous band [r0, r1) (any order inside).
-      bool ok = true;
-      p.band_rows.assign(2 * p.P, 0);
-      for (int j = 0; j < p.P && ok; ++j) {
-        const int lo = p.gpos[j], hi = p.gpos[j + 1];
-        if ((hi - lo) % p.Nt) {
-          ok = false;
-          break;
-        }
-        int rmin = p.Mt, rmax = -1;
-        std::vector<char> seen((size_t)(hi - lo), 0);
-        for (int q = lo; q < hi; ++q) rmin = std::min(rmin, p.order[q] / p.Nt);
-        const int r1 = rmin + (hi - lo) / p.Nt;
-        for (int q = lo; q < hi && ok; ++q) {
-          const int t = p.order[q] - rmin * p.Nt;
-          if (t < 0 || t >= hi - lo || seen[t]) ok = false;
-          else seen[t] = 1;
-          rmax = std::max(rmax, p.order[q] / p.Nt);
-        }
-        ok = ok && rmax < r1;
-        p.band_rows[2 * j] = rmin;
-        p.band_rows[2 * j + 1] = r1;
-      }
+      const bool ok = band_layout(p, false);
       if (d.ar_layout == FO_LAYOUT_ROWBAND && !ok)
         fail(FO_ERR_UNSUPPORTED, "ROWBAND layout needs a raster order and tile-row group boundaries");
       p.layout = (d.ar_layout == FO_LAYOUT_SLOT) ? FO_LAYOUT_SLOT
@@ -227,14 +238,23 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
       p.send_elems = p.recv_elems = MN;
       break;
     }
-    case FO_REDUCESCATTER:
+    case FO_REDUCESCATTER: {
       // subtile of h = BM/n rows (R7)
       if (p.BM % world) fail(FO_ERR_SHAPE, "tile_m=%d not divisible by world=%d", p.BM, world);
       p.h = p.BM / world;
       p.out_rows = p.M / world;
       p.send_elems = MN;
+      // ROWBAND (R40): ascending bands of whole tile-rows; chunk k
+      // of a band = the k-th subtile rows of its tiles as complete rows, so
+      // the ReduceScatter delivers the output rows in place (no receive buffer)
+      const bool ok = d.ar_layout != FO_LAYOUT_SLOT && band_layout(p, true);
+      if (d.ar_layout == FO_LAYOUT_ROWBAND && !ok)
+        fail(FO_ERR_UNSUPPORTED, "RS ROWBAND layout needs ascending bands of whole tile-rows as groups");
+      p.layout = ok ? FO_LAYOUT_ROWBAND : FO_LAYOUT_SLOT;
+      if (!ok) p.band_rows.clear();
       p.recv_elems = MN / world;
       break;
+    }
     case FO_ALLTOALL: {
       if (!d.row_dst) fail(FO_ERR_INVALID_ARG, "All-to-All needs row_dst");
       for (int64_t r = 0; r < p.M; ++r)
@@ -320,7 +340,8 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
       break;
     }
   }
-  if (p.coll != FO_ALLREDUCE) p.layout = (p.coll == FO_NOCOMM) ? FO_LAYOUT_ROWBAND : FO_LAYOUT_SLOT;
+  if (p.coll == FO_NOCOMM) p.layout = FO_LAYOUT_ROWBAND;
+  else if (p.coll == FO_ALLTOALL) p.layout = FO_LAYOUT_SLOT;
   build_schedules(p, d, peers);
   return p;
 }
@@ -375,9 +396,13 @@ void build_schedules(PlanHost& p, const fo_plan_desc& d, const fo_plan_desc* con
       }
       case FO_REDUCESCATTER: {
         // chunk k of the group's range goes to rank k; rank k's chunks are
-        // stored in group order (receive layout [group][q][a'][BN])
+        // stored in group order (receive layout [group][q][a'][BN]); ROWBAND:
+        // straight into the output rows of the band (at one rank the GEMM
+        // writes the output itself and the call is in place)
         const int64_t b = p.group_elem_begin(j), e = p.group_elem_end(j);
-        p.calls.push_back(make_call(FO_CALL_REDUCESCATTER, j, -1, FO_BUF_SEND, FO_BUF_RECV, b, b / W, (e - b) / W));
+        const bool band = p.layout == FO_LAYOUT_ROWBAND;
+        p.calls.push_back(make_call(FO_CALL_REDUCESCATTER, j, -1, band && W == 1 ? FO_BUF_OUT : FO_BUF_SEND,
+                                    band ? FO_BUF_OUT : FO_BUF_RECV, b, b / W, (e - b) / W));
         break;
       }
       case FO_ALLTOALL: {
@@ -467,8 +492,12 @@ int64_t PlanHost::send_index(int64_t r, int64_t c) const {
       return ((int64_t)q * BM + a) * BN + b;  // slot q, row-major
     case FO_REDUCESCATTER: {
       const int j = group_of_pos[q];
-      const int ps = gpos[j], G = gpos[j + 1] - gpos[j];
       const int k = a / h, a2 = a % h;
+      if (layout == FO_LAYOUT_ROWBAND) {  // DESIGN.md R40
+        const int64_t r0 = band_rows[2 * j], B = band_rows[2 * j + 1] - r0;
+        return (r0 * BM + (k * B + (i - r0)) * h + a2) * N + c;
+      }
+      const int ps = gpos[j], G = gpos[j + 1] - gpos[j];
       return (int64_t)ps * BM * BN + (int64_t)k * G * h * BN + (int64_t)(q - ps) * h * BN + (int64_t)a2 * BN + b;
     }
     case FO_ALLTOALL:
@@ -488,6 +517,7 @@ int64_t PlanHost::recv_index(int64_t r, int64_t c) const {
       return ((int64_t)q * BM + r % BM) * BN + b;
     }
     case FO_REDUCESCATTER: {
+      if (layout == FO_LAYOUT_ROWBAND) return r * N + c;  // received in output order (R40)
       // local row l = i*h + a'  <-  receive row q*h + a' (group chunks in order)
       const int q = pos_of_tile[(r / h) * Nt + jc];
       return ((int64_t)q * h + r % h) * BN + b;

@@ -16,7 +16,7 @@ namespace fo {
 struct PlanHost {
   // ---- descriptor (copied)
   int coll = FO_NOCOMM;
-  int layout = FO_LAYOUT_SLOT;  // resolved AR layout
+  int layout = FO_LAYOUT_SLOT;  // resolved AR / RS layout
   int64_t M = 0, N = 0, K = 0;
   int BM = 128, BN = 128;
   int S = 0;                    // wave width (0 until resolved against a device)
@@ -49,7 +49,7 @@ struct PlanHost {
   int64_t out_rows = 0;
   int64_t send_elems = 0, recv_elems = 0;
 
-  std::vector<int64_t> band_rows;       // AR ROWBAND: [2P] tile-row band (r0, r1) of each group
+  std::vector<int64_t> band_rows;       // AR / RS ROWBAND: [2P] tile-row band (r0, r1) of each group
 
   // ---- communication schedules (fo_plan_export_calls): what fo_run /
   // fo_run_sequential issue on the communicator, in order
@@ -57,13 +57,20 @@ struct PlanHost {
   std::vector<int32_t> call_begin;      // [P+1] calls of group j = [call_begin[j], call_begin[j+1])
   std::vector<fo_comm_call> seq_calls;  // sequential baseline
 
-  // Group j's element range in the AR/RS send buffer (AR ROWBAND: its row band of C).
+  // AllReduce / ReduceScatter with every group a band of whole tile-rows
+  // (H11a, R40): no post-communication reorder.
+  bool banded() const { return (coll == FO_ALLREDUCE || coll == FO_REDUCESCATTER) && layout == FO_LAYOUT_ROWBAND; }
+  // Output rows per tile-row of a banded plan (AR: BM; RS: the h rows of each
+  // tile-row that land on this rank).
+  int band_out_rows() const { return coll == FO_REDUCESCATTER ? h : BM; }
+
+  // Group j's element range in the AR/RS send buffer (ROWBAND: its row band of C).
   int64_t group_elem_begin(int j) const {
-    if (coll == FO_ALLREDUCE && layout == FO_LAYOUT_ROWBAND) return band_rows[2 * j] * BM * N;
+    if (banded()) return band_rows[2 * j] * BM * N;
     return (int64_t)gpos[j] * BM * BN;
   }
   int64_t group_elem_end(int j) const {
-    if (coll == FO_ALLREDUCE && layout == FO_LAYOUT_ROWBAND) return band_rows[2 * j + 1] * BM * N;
+    if (banded()) return band_rows[2 * j + 1] * BM * N;
     return (int64_t)gpos[j + 1] * BM * BN;
   }
   int group_tiles(int j) const { return gpos[j + 1] - gpos[j]; }

@@ -226,10 +226,13 @@ static void ensure_device(fo_plan_s* p) {
   p->d_gpos = upload(h.gpos);
   p->d_row_slot = upload(h.row_slot);
   if (h.coll == FO_REDUCESCATTER) {
+    // per position: {first position, size} of its group; ROWBAND (R40):
+    // {first tile-row, tile-rows} of its band
     std::vector<int2> info(h.tiles);
     for (int q = 0; q < h.tiles; ++q) {
       const int g = h.group_of_pos[q];
-      info[q] = make_int2(h.gpos[g], h.gpos[g + 1] - h.gpos[g]);
+      info[q] = h.banded() ? make_int2((int)h.band_rows[2 * g], (int)(h.band_rows[2 * g + 1] - h.band_rows[2 * g]))
+                           : make_int2(h.gpos[g], h.gpos[g + 1] - h.gpos[g]);
     }
     p->d_rs_info = upload(info);
   }
@@ -332,7 +335,10 @@ static void ensure_device(fo_plan_s* p) {
   FO_CUDA(cudaMalloc(&p->d_counters, sizeof(uint32_t) * p->ctr_words));
   FO_CUDA(cudaMemset(p->d_counters, 0, sizeof(uint32_t) * p->ctr_words));
   p->d_flags = p->d_counters + h.P;
-  const bool need_send = !(h.coll == FO_NOCOMM || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND));
+  // banded plans reduce in place in the output (AR; RS at one rank) or
+  // scatter straight into it (RS): no send buffer resp. no receive buffer
+  const bool need_send = !(h.coll == FO_NOCOMM || (h.coll == FO_ALLREDUCE && h.banded()) ||
+                           (h.coll == FO_REDUCESCATTER && h.banded() && h.world == 1));
   // the buffers NCCL reads and writes: plain device memory, or (a context
   // configured for registration) ncclMemAlloc'd so NCCL can register them
   // for zero-copy / NVLS
@@ -342,7 +348,7 @@ static void ensure_device(fo_plan_s* p) {
     else FO_CUDA(cudaMalloc(b, bytes));
   };
   if (need_send && h.send_elems) alloc(&p->d_send, 2 * h.send_elems);
-  if ((h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && h.recv_elems) {
+  if ((h.coll == FO_REDUCESCATTER || h.coll == FO_ALLTOALL) && h.recv_elems && !h.banded()) {
     // one rank: the receive layout ([group][source 0]) is the send layout, so
     // the collective runs in place (no copy)
     if (h.world == 1) p->d_recv = p->d_send;
@@ -434,7 +440,7 @@ static GemmArgs gemm_args(fo_plan_s* p, const void* A, const void* Bt, void* dst
 static int epi_mode(const PlanHost& h) {
   switch (h.coll) {
     case FO_ALLREDUCE: return h.layout == FO_LAYOUT_ROWBAND ? EPI_ROWMAJOR : EPI_SLOT;
-    case FO_REDUCESCATTER: return EPI_RS;
+    case FO_REDUCESCATTER: return h.banded() ? EPI_RS_BAND : EPI_RS;
     case FO_ALLTOALL: return EPI_A2A;
     default: return EPI_ROWMAJOR;
   }
@@ -482,7 +488,7 @@ static void run_post(fo_plan_s* p, int map, const void* src, void* out, const vo
 static int post_map(const PlanHost& h) {
   switch (h.coll) {
     case FO_ALLREDUCE: return h.layout == FO_LAYOUT_ROWBAND ? POSTMAP_IDENTITY : POSTMAP_SLOT;
-    case FO_REDUCESCATTER: return POSTMAP_RS;
+    case FO_REDUCESCATTER: return h.banded() ? POSTMAP_IDENTITY : POSTMAP_RS;
     case FO_ALLTOALL: return POSTMAP_A2A;
     default: return POSTMAP_IDENTITY;
   }
@@ -521,12 +527,10 @@ static void stream_wait(fo_plan_s* p, WaitValue32Fn wait, cudaStream_t cs, int j
 // (profiles/r01_predictor_check.txt).
 constexpr int kPartitionSmem = 24 * 1024;
 
-// AR ROWBAND with a fused op: every group is a band of complete rows, so the
-// op (residual add, RMSNorm over whole rows) can run on the band right after
-// the band's AllReduce.
-static bool band_post(const PlanHost& h) {
-  return h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND && h.post != FO_POST_NONE;
-}
+// AR / RS ROWBAND with a fused op: every group is a band of complete rows, so
+// the op (residual add, RMSNorm over whole rows) can run on the band right
+// after the band's AllReduce / ReduceScatter.
+static bool band_post(const PlanHost& h) { return h.banded() && h.post != FO_POST_NONE; }
 
 static bool use_group_post(const fo_plan_s* p) {
   const PlanHost& h = p->host;
@@ -541,9 +545,11 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
   const PlanHost& h = p->host;
   if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
   if (band_post(h)) {
-    // in place on the band's rows [r0*BM, r1*BM) of out (== src)
+    // in place on the band's output rows [r0*R, r1*R) of out (== src); R =
+    // BM (AR) or h (RS: the band's rows that landed on this rank)
     if (is_rmsnorm(h.post) && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
-    const int64_t row0 = h.band_rows[2 * j] * h.BM, rows = (h.band_rows[2 * j + 1] - h.band_rows[2 * j]) * h.BM;
+    const int64_t R = h.band_out_rows();
+    const int64_t row0 = h.band_rows[2 * j] * R, rows = (h.band_rows[2 * j + 1] - h.band_rows[2 * j]) * R;
     PostArgs a{};
     a.map = POSTMAP_IDENTITY;
     a.op = h.post;
@@ -833,13 +839,13 @@ fo_status fo_ctx_destroy(fo_ctx c) {
 }
 
 // Rows [r0, r1) of the output that are final once group j is done — defined
-// when every group is a band of whole tile-rows written row-major in place
-// (AR ROWBAND, no-comm with band-aligned groups); false otherwise.
+// when every group is a band of whole tile-rows that lands row-major in the
+// output (AR / RS ROWBAND); false otherwise.
 static bool group_out_rows(const PlanHost& h, int j, int64_t* r0, int64_t* r1) {
-  if (!(h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND)) return false;
+  if (!h.banded()) return false;
   if ((int)h.band_rows.size() < 2 * h.P) return false;
-  *r0 = (int64_t)h.band_rows[2 * j] * h.BM;
-  *r1 = (int64_t)h.band_rows[2 * j + 1] * h.BM;
+  *r0 = (int64_t)h.band_rows[2 * j] * h.band_out_rows();
+  *r1 = (int64_t)h.band_rows[2 * j + 1] * h.band_out_rows();
   return true;
 }
 
@@ -873,8 +879,13 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     WaitValue32Fn wait = wait_value_fn();
     if (!wait) fail(FO_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
-    const bool rowband = (h.coll == FO_NOCOMM) || (h.coll == FO_ALLREDUCE && h.layout == FO_LAYOUT_ROWBAND);
-    void* gemm_dst = rowband ? out : p->d_send;
+    // the GEMM writes the output itself for no-comm and in-place banded
+    // plans (AR ROWBAND; RS ROWBAND at one rank), else the send buffer; a
+    // banded RS scatters into the output, so every banded plan's
+    // post-communication data is `out`
+    const bool rowband = (h.coll == FO_NOCOMM) || h.banded();
+    const bool gemm_out = (h.coll == FO_NOCOMM) || (h.banded() && (h.coll == FO_ALLREDUCE || h.world == 1));
+    void* gemm_dst = gemm_out ? out : p->d_send;
     // a single group issued in stream order (R32) waits on no counter: the GEMM
     // then neither signals nor needs the counting table reset
     const bool counted = !(p->last_in_order && h.coll != FO_NOCOMM && h.P == 1);

@@ -234,12 +234,17 @@ def effective_curve(curve: list, post_us_per_byte: float, post_fixed_us: float =
     return out
 
 
+# collectives with a ROWBAND layout (AR: in place; RS: scattered straight into
+# the output, R40)
+BANDED = ("allreduce", "reducescatter")
+
+
 @dataclass
 class LayerChoice:
     workers: int
     swizzle: int
     groups: list
-    layout: str          # "rowband" | "slot" (AllReduce) | "auto"
+    layout: str          # "rowband" | "slot" (AllReduce / ReduceScatter) | "auto" (All-to-All)
     predicted_us: float
     gemm_us: float
     candidates: list     # (workers, tile:layout[+tailsplit], groups, predicted_us, gemm_us[, measured_us])
@@ -252,7 +257,7 @@ class LayerChoice:
     def spec(self, M, N, K, coll, post="none") -> dict:
         d = dict(coll=coll, m=M, n=N, k=K, tile_m=self.tile_m, tile_n=self.tile_n, workers=self.workers,
                  swizzle=self.swizzle, group_waves=list(self.groups),
-                 ar_layout=self.layout if coll == "allreduce" else "auto", post=post)
+                 ar_layout=self.layout if coll in BANDED else "auto", post=post)
         if self.tail_split:
             d["options"] = {"tail_split": self.tail_split}
         return d
@@ -261,11 +266,12 @@ class LayerChoice:
 def candidate_workers(tiles: int, Nt: int, sms: int, coll: str, cg: int = 2) -> list:
     """Offline stage (3) candidates for the wave width S (T is set
     by the SMs the collective leaves): the fewest workers with the full GPU's
-    wave count, the full GPU, and (AllReduce) the widest S whose waves are whole
-    tile-rows (groups are then row bands: no reorder at all, H11a)."""
+    wave count, the full GPU, and (AllReduce / ReduceScatter) the widest S whose
+    waves are whole tile-rows (groups are then row bands: no reorder at all,
+    DESIGN.md H11a, R40)."""
     smax = sms // cg
     cands = {default_workers(tiles, sms, cg), min(smax, tiles)}
-    if coll == "allreduce" and Nt <= smax:
+    if coll in BANDED and Nt <= smax:
         cands.add((smax // Nt) * Nt)
     return sorted(c for c in cands if c >= 1)
 
@@ -370,7 +376,7 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         if key not in post_cache:
             t_ = (M // tm) * (N // tn)
             pl = Plan(coll=coll, m=M, n=N, k=64, tile_m=tm, tile_n=tn, workers=min(t_, sms // max(1, tm // 128)),
-                      swizzle=1, ar_layout=layout if coll == "allreduce" else "auto", post=op, rank=ctx.rank,
+                      swizzle=1, ar_layout=layout if coll in BANDED else "auto", post=op, rank=ctx.rank,
                       world=world)
             recv = torch.zeros(pl.info["recv_elems"], dtype=torch.bfloat16, device="cuda")
             o = torch.empty(pl.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
@@ -378,7 +384,7 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         return post_cache[key]
 
     out_bytes = out_rows * N * 2
-    layouts = ("rowband", "slot") if coll == "allreduce" else ("auto",)
+    layouts = ("rowband", "slot") if coll in BANDED else ("auto",)
     evaluated = []
     # offline stage (1): the GEMM in each candidate's execution order, all
     # candidates (tile shape x S x layout x tail split) timed together

@@ -83,6 +83,7 @@ def main(W):
     for coll, layout, groups, split in (("allreduce", "slot", [1, 2, 1], 0), ("allreduce", "rowband", [1, 1, 2], 0),
                                         ("allreduce", "rowband", [4], 0), ("allreduce", "slot", [2, 2], -1),
                                         ("reducescatter", "auto", [2, 1, 1], 0),
+                                        ("reducescatter", "rowband", [1, 1, 2], 0),
                                         ("reducescatter", "auto", [1, 3], -1)):
         if coll == "reducescatter" and BM % W:
             continue
@@ -129,15 +130,17 @@ def main(W):
         # more than 32 streams alias the device's hardware queues, where one
         # rank's pending stream wait can block another rank's launch — a
         # one-process artefact; with NCCL every rank is its own process)
-        if coll == "allreduce" and not split and W <= 4:
-            hosts = [[torch.full((M, N), float("nan"), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-                     for _ in range(W)]
+        # (RS rowband: its bands land in `out` row-major, so each band goes back
+        # to the host right after its ReduceScatter, as for AR rowband)
+        if (coll == "allreduce" or layout == "rowband") and not split and W <= 4:
+            hosts = [[torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16).pin_memory()
+                      for _ in range(2)] for p in plans]
             A_h = [a.pin_memory() for a, _ in inp]
             for i in range(2):
                 each(lambda r: fo.run_host(ctxs[r], plans[r], A_h[r], Bd[r], hosts[r][i], stream=streams[r]))
             for r in range(W):
                 for i in range(2):
-                    check(f"{name}/run_host[{i}]/rank{r}", hosts[r][i], full)
+                    check(f"{name}/run_host[{i}]/rank{r}", hosts[r][i], full if coll == "allreduce" else want[r])
         for p in plans:
             p.close()
     # ---- All-to-All: imbalanced experts, random routing, same P on every rank

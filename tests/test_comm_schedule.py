@@ -91,26 +91,41 @@ def test_allreduce_schedule(world, layout):
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_reducescatter_schedule(world):
-    rng = np.random.default_rng(200 + world)
+@pytest.mark.parametrize("layout", ["slot", "rowband"])
+def test_reducescatter_schedule(world, layout):
+    rng = np.random.default_rng(200 + world + (7 if layout == "rowband" else 0))
     for _ in range(12):
         BM, BN, M, N, S, part, order, swz = _case(rng, world, "reducescatter")
+        if layout == "rowband":
+            # raster order, waves of whole tile-rows: ascending bands (R40)
+            Nt = N // BN
+            S = Nt * int(rng.integers(1, M // BM + 1))
+            T = -(-(M // BM) * Nt // S)
+            part, order, swz = _partition(rng, T), None, 1
         opl = _oracle_plan(M, N, BM, BN, S, part, order, swz)
         spec = dict(coll="reducescatter", m=M, n=N, k=64, tile_m=BM, tile_n=BN, workers=S, tile_order=order,
-                    swizzle=swz, group_waves=part)
+                    swizzle=swz, group_waves=part, ar_layout=layout)
         plans = [_lib_plan(r, world, **spec) for r in range(world)]
+        assert all(p.info["ar_layout"] == (1 if layout == "rowband" else 0) for p in plans)
         Ys = [_ints(rng, (M, N)) for _ in range(world)]
-        sends = [orr.rs_pre(Y, opl, world) for Y in Ys]
-        want = oc.reduce_scatter_groups(sends, orr.group_elem_ranges(opl))
+        sends = [orr.rs_pre(Y, opl, world, layout) for Y in Ys]
+        want = oc.reduce_scatter_groups(sends, orr.group_elem_ranges(opl, layout))
         bufs = []
         for r in range(world):
-            b = {"send": sends[r].copy()}
-            b["recv"] = b["send"] if world == 1 else np.full(plans[r].info["recv_elems"], np.nan)
+            if layout == "rowband":
+                # the band's rows land in `out` (at one rank the GEMM wrote it: in place)
+                b = {"out": sends[r].copy() if world == 1 else np.full(M // world * N, np.nan),
+                     "send": sends[r].copy()}
+            else:
+                b = {"send": sends[r].copy()}
+                b["recv"] = b["send"] if world == 1 else np.full(plans[r].info["recv_elems"], np.nan)
             bufs.append(b)
         assert comm_sim.run([p.export_calls(0) for p in plans], bufs) == len(part)
         for r in range(world):
-            got = bufs[r]["recv"][:plans[r].info["recv_elems"]]
+            got = bufs[r]["out" if layout == "rowband" else "recv"][:plans[r].info["recv_elems"]]
             np.testing.assert_array_equal(got, want[r])
+            if layout == "rowband":   # received in output order: no post-communication reorder
+                np.testing.assert_array_equal(got.reshape(M // world, N), orr.rs_post(want[r], opl, world, layout))
         # sequential: ncclReduceScatter of row-major C -> contiguous rows
         seq = [{"scratch": Y.reshape(-1).copy(), "out": np.full(M // world * N, np.nan)} for Y in Ys]
         assert comm_sim.run([p.export_calls(1) for p in plans], seq) == 1

@@ -14,6 +14,7 @@ import torch
 import synthetic
 from oracle import pipeline as opl
 from oracle import plan as op
+from oracle import reorder as orr
 
 pytestmark = pytest.mark.gpu
 
@@ -53,6 +54,13 @@ def _draw(seed):
         tail_split = 0                               # 64-row tiles (tcgen05 M=64) run whole tiles only
     k_snake = int(rng.choice([-1, 0, 1]))
     tma_store = int(rng.random() < 0.7)
+    if coll == "reducescatter" and rng.random() < 0.4:
+        # ascending bands of whole tile-rows (raster, waves of whole tile-rows):
+        # the RS rowband layout (R40) under "auto"
+        S = Nt * int(rng.integers(1, Mt + 1))
+        T = op.num_waves(tiles, S)
+        part = synthetic.random_partition(T, seed)
+        order, swizzle = None, 1
     return dict(BM=BM, BN=BN, M=Mt * BM, N=Nt * BN, K=K, n=n, coll=coll, S=S, part=part, order=order,
                 swizzle=swizzle, layout=layout, multicast=multicast, tail_split=tail_split, k_snake=k_snake,
                 tma_store=tma_store)
@@ -74,7 +82,7 @@ def test_random_plan_matches_oracle(seed):
         if c["coll"] == "allreduce":
             pl = fo.Plan(coll="allreduce", ar_layout=c["layout"], rank=r, world=n, **kw)
         else:
-            pl = fo.Plan(coll="reducescatter", rank=r, world=n, **kw)
+            pl = fo.Plan(coll="reducescatter", ar_layout=c["layout"], rank=r, world=n, **kw)
         pl.set_option("multicast", c["multicast"])
         pl.set_option("tail_split", c["tail_split"])
         pl.set_option("k_snake", c["k_snake"])
@@ -94,7 +102,9 @@ def test_random_plan_matches_oracle(seed):
         plain = opl.plain_allreduce(As, Bts)
         out_rows = M
     else:
-        ores = opl.run_reducescatter(As, Bts, oplan)
+        lay = "rowband" if plans[0].info["ar_layout"] == 1 else "slot"
+        assert (lay == "rowband") == (c["layout"] == "auto" and orr.rs_rowband_ok(oplan)), c
+        ores = opl.run_reducescatter(As, Bts, oplan, layout=lay)
         plain = opl.plain_reducescatter(As, Bts, BM)
         out_rows = M // n
     mult = max(1, BM // 128)

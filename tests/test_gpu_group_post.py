@@ -72,9 +72,12 @@ def test_group_post_inside_fo_run():
     M, N, K = 2048, 2048, 512
     A, Bt = synthetic.exact_inputs(M, N, K, seed=5, nnz_per_row=64)
     A, Bt = A.cuda(), Bt.cuda()
-    for coll, lay in (("allreduce", "slot"), ("reducescatter", "auto")):
+    # RS "auto" here is the rowband layout (R40: waves of 2 whole tile-rows,
+    # panels of 2): no post pass at all
+    for coll, lay in (("allreduce", "slot"), ("reducescatter", "slot"), ("reducescatter", "auto")):
         plan = fo.Plan(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=16, swizzle=2,
                        group_waves=[1, 2, 1], ar_layout=lay)
+        assert plan.info["ar_layout"] == (1 if lay == "auto" else 0)
         plan.set_option("group_post", 1)
         want = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         fo.run_sequential(ctx, plan, A, Bt, want)

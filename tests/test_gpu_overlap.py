@@ -170,7 +170,9 @@ def test_post_sm_partition_option_equal_results(ctx):
 
 @pytest.mark.parametrize("coll,post,layout", [("allreduce", "none", "slot"), ("allreduce", "add_rmsnorm", "slot"),
                                               ("allreduce", "add_rmsnorm", "rowband"),
-                                              ("reducescatter", "add", "auto"), ("alltoall", "none", "auto")])
+                                              ("reducescatter", "add", "slot"), ("reducescatter", "add", "auto"),
+                                              ("reducescatter", "add_rmsnorm", "rowband"),
+                                              ("alltoall", "none", "auto")])
 def test_last_group_in_order_equals_counter_trigger(ctx, coll, post, layout):
     """FO_OPT_LAST_GROUP_IN_ORDER: the last group's collective issued on the
     caller stream after the GEMM gives bit-identical results to triggering it
@@ -202,7 +204,8 @@ def test_last_group_in_order_equals_counter_trigger(ctx, coll, post, layout):
 
 @pytest.mark.parametrize("coll,post,layout", [("allreduce", "none", "rowband"), ("allreduce", "add", "slot"),
                                               ("allreduce", "add_rmsnorm", "rowband"),
-                                              ("reducescatter", "add", "auto"), ("alltoall", "none", "auto")])
+                                              ("reducescatter", "add", "slot"), ("reducescatter", "add", "auto"),
+                                              ("alltoall", "none", "auto")])
 def test_single_group_in_order_equals_sequential(ctx, coll, post, layout):
     """One group issued in stream order (R32): no counters, no fork — the
     overlapped op must equal fo_run_sequential bit for bit, repeatedly."""

@@ -162,7 +162,7 @@ def test_reducescatter_stages_exact(n, case):
     plain = opl.plain_reducescatter(As, Bts, BM)
     for r in range(n):
         plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=swz, group_waves=groups,
-                       rank=r, world=n)
+                       ar_layout="slot", rank=r, world=n)
         send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
         fo.gemm_stage(plan, _dev_bf16(As[r]), _dev_bf16(Bts[r]), send)
         torch.cuda.synchronize()
@@ -170,6 +170,43 @@ def test_reducescatter_stages_exact(n, case):
         _counters_ok(plan, oplan)
         out = torch.empty(M // n, N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plan, _dev_bf16(ores["recv"][r]), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(out), plain[r])
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("BM,BN,Mt,Nt,rows_per_wave,K", [(256, 256, 6, 3, 1, 256), (256, 128, 8, 2, 2, 128),
+                                                         (128, 256, 5, 4, 1, 192), (64, 128, 6, 2, 2, 128)])
+def test_reducescatter_rowband_stages_exact(n, BM, BN, Mt, Nt, rows_per_wave, K):
+    """RS ROWBAND (R40): raster order, waves of whole tile-rows, random
+    partitions -> ascending bands; every rank's send buffer (EPI_RS_BAND: TMA
+    stores when h >= a warp's rows, st.global below), counters, and the
+    received chunks (the output itself) bit-exact vs the oracle."""
+    if BM % n:
+        pytest.skip("tile_m not divisible by world")
+    M, N = Mt * BM, Nt * BN
+    S = rows_per_wave * Nt
+    tiles = Mt * Nt
+    groups = _groups(tiles, S, 7 * n + BM)
+    As, Bts = _rank_inputs(n, M, N, K, 260 + n)
+    oplan = op.make_plan(M, N, BM, BN, S, groups, swizzle=1)
+    assert orr.rs_rowband_ok(oplan)
+    ores = opl.run_reducescatter(As, Bts, oplan, layout="rowband")
+    plain = opl.plain_reducescatter(As, Bts, BM)
+    for r in range(n):
+        plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=1,
+                       group_waves=groups, rank=r, world=n)
+        assert plan.info["ar_layout"] == 1
+        for tma in (1, 0):
+            plan.set_option("tma_store", tma)
+            send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+            fo.gemm_stage(plan, _dev_bf16(As[r]), _dev_bf16(Bts[r]), send)
+            torch.cuda.synchronize()
+            assert np.array_equal(_host(send), ores["send"][r]), f"rank {r} send buffer (tma_store={tma})"
+            _counters_ok(plan, oplan)
+        assert np.array_equal(ores["recv"][r].reshape(M // n, N), plain[r])
+        out = torch.empty(M // n, N, dtype=torch.bfloat16, device="cuda")
+        fo.post_stage(plan, _dev_bf16(ores["recv"][r]), out)   # identity map
         torch.cuda.synchronize()
         assert np.array_equal(_host(out), plain[r])
 
@@ -538,12 +575,13 @@ def test_rs_one_row_subtiles():
     As, Bts = _rank_inputs(1, M, N, K, 77)
     oplan = op.make_plan(M, N, BM, BN, S, None)
     Y = onum.gemm(As[0], Bts[0])
-    buf = orr.rs_pre(Y, oplan, n)
-    plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, rank=5, world=n)
-    send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
-    fo.gemm_stage(plan, _dev_bf16(As[0]), _dev_bf16(Bts[0]), send)
-    torch.cuda.synchronize()
-    assert np.array_equal(_host(send), buf)
+    for lay in ("slot", "rowband"):   # S = 1, one tile-row per wave: both layouts are legal
+        plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, rank=5, world=n,
+                       ar_layout=lay)
+        send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, _dev_bf16(As[0]), _dev_bf16(Bts[0]), send)
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(send), orr.rs_pre(Y, oplan, n, lay)), lay
 
 
 def test_alltoall_rank_receiving_nothing():

@@ -97,19 +97,31 @@ def test_allreduce_maps(layout):
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_reducescatter_maps(world):
+@pytest.mark.parametrize("layout", ["slot", "auto"])
+def test_reducescatter_maps(world, layout):
     rng = np.random.default_rng(20 + world)
-    for _ in range(25):
+    for it in range(25):
         c = _rand_case(rng, "reducescatter", world)
+        if it % 3 == 0:  # waves of whole tile-row panels -> ascending bands (R40) under raster order
+            Nt = c["N"] // c["BN"]
+            c["swz"] = 1
+            c["S"] = Nt * int(rng.integers(1, 4))
+            c["order"] = None
+            Mt = c["M"] // c["BM"]
+            c["part"] = synthetic.random_partition(op.num_waves(Mt * Nt, c["S"]), it)
         o = _op_plan(c)
         for rank in range(world):
-            pl = _fo_plan(c, "reducescatter", rank=rank, world=world)
+            pl = _fo_plan(c, "reducescatter", rank=rank, world=world, layout=layout)
+            lay = "rowband" if pl.info["ar_layout"] == 1 else "slot"
+            assert (lay == "rowband") == (layout == "auto" and orr.rs_rowband_ok(o))
             Y = np.arange(c["M"] * c["N"], dtype=float).reshape(c["M"], c["N"])
-            buf = orr.rs_pre(Y, o, world)
+            buf = orr.rs_pre(Y, o, world, lay)
             assert np.array_equal(pl.export_send_map(), _oracle_send_map(buf))
             n_recv = c["M"] * c["N"] // world
-            post = orr.rs_post(np.arange(n_recv, dtype=float), o, world)
+            post = orr.rs_post(np.arange(n_recv, dtype=float), o, world, lay)
             assert np.array_equal(pl.export_recv_map(), post.reshape(-1).astype(np.int64))
+            for j, ((lo, hi), (elo, ehi)) in enumerate(zip(o.ranges, orr.group_elem_ranges(o, lay))):
+                assert pl.group(j) == (lo, hi, elo, ehi)
             assert pl.info["rs_subtile_rows"] == c["BM"] // world
             assert pl.info["out_rows"] == c["M"] // world
 

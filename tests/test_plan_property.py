@@ -63,9 +63,11 @@ def test_plan_maps_match_oracle(c):
         post = orr.ar_post(np.arange(c["M"] * c["N"], dtype=float), o, lay)
         ranges = orr.group_elem_ranges(o, lay)
     else:
-        buf = orr.rs_pre(Y, o, c["world"])
-        post = orr.rs_post(np.arange(c["M"] * c["N"] // c["world"], dtype=float), o, c["world"])
-        ranges = orr.group_elem_ranges(o)
+        lay = "rowband" if pl.info["ar_layout"] == 1 else "slot"
+        assert (lay == "rowband") == (c["layout"] == "auto" and orr.rs_rowband_ok(o))
+        buf = orr.rs_pre(Y, o, c["world"], lay)
+        post = orr.rs_post(np.arange(c["M"] * c["N"] // c["world"], dtype=float), o, c["world"], lay)
+        ranges = orr.group_elem_ranges(o, lay)
     inv = np.empty(buf.size, np.int64)
     inv[buf.astype(np.int64)] = np.arange(buf.size)
     assert np.array_equal(pl.export_send_map(), inv)
