@@ -88,7 +88,7 @@ def row_exchange(gathered: np.ndarray, BM: int, n: int) -> np.ndarray:
 
 
 # ------------------------------------------------------------------ All-to-All
-def run_alltoall(As, Bts, plans, row_dsts, model_bf16=False):
+def run_alltoall(As, Bts, plans, row_dsts, model_bf16=False, layout="slot"):
     """plans[s], row_dsts[s]: source rank s's own plan (its M may differ from
     the others', PAPER.md:264 imbalance) and row destinations."""
     n = len(As)
@@ -96,7 +96,7 @@ def run_alltoall(As, Bts, plans, row_dsts, model_bf16=False):
     if any(len(p.ranges) != P for p in plans):
         raise reorder.OracleError("all ranks need the same number of wave groups")
     Ys = [_Y(As[s], Bts[s], model_bf16) for s in range(n)]
-    sends = [reorder.a2a_pre(Ys[s], plans[s], row_dsts[s], n) for s in range(n)]
+    sends = [reorder.a2a_pre(Ys[s], plans[s], row_dsts[s], n, layout) for s in range(n)]
     recv = collectives.alltoall_groups(sends, P)
     N, BN = plans[0].N, plans[0].BN
     outs = [reorder.a2a_post(recv[d], [sends[s].meta[d] for s in range(n)], row_dsts, d, N, BN)

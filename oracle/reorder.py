@@ -34,6 +34,11 @@ indices are reordered based on their execution order".
       memory pool per destination rank; subtokens are appended in execution
       order (p ascending, then row inside the tile ascending).  Group j's
       subtokens form one contiguous range of every pool.
+      Layout "rowband" (R41): when every source's groups are
+      ascending bands of whole tile-rows, group j's subtokens are appended
+      row by row (source row ascending, then tile-column ascending), i.e.
+      pool d holds complete rows in source-row order; the part of group j a
+      receiver gets from source s is then a run of consecutive output rows.
 
 Pins (tests/test_oracle_reorder.py): post(pre(X)) == X bit-exactly
 ("the output in (d) is the same as (a)"); every element lands in
@@ -210,7 +215,12 @@ class A2ASend:
         self.ranges = [[None] * P for _ in range(n)]
 
 
-def a2a_pre(Y: np.ndarray, plan: Plan, row_dst, n: int) -> A2ASend:
+def a2a_rowband_ok(plans) -> bool:
+    """A2A rowband: every source's groups are ascending bands of complete tile-rows."""
+    return all(rs_rowband_ok(pl) for pl in plans)
+
+
+def a2a_pre(Y: np.ndarray, plan: Plan, row_dst, n: int, layout: str = "slot") -> A2ASend:
     """O5 for All-to-All (module header)."""
     BM, BN = plan.BM, plan.BN
     row_dst = np.asarray(row_dst).reshape(-1)
@@ -220,8 +230,20 @@ def a2a_pre(Y: np.ndarray, plan: Plan, row_dst, n: int) -> A2ASend:
         raise OracleError("row_dst out of range")
     P = len(plan.ranges)
     s = A2ASend(n, P)
+    if layout == "rowband" and not rs_rowband_ok(plan):
+        raise OracleError("A2A rowband layout needs ascending bands of complete tile-rows as groups")
     for gj, (ps, pe) in enumerate(plan.ranges):
         start = [len(s.pools[d]) for d in range(n)]
+        if layout == "rowband":
+            r0, r1 = rowband_of_group(plan, ps, pe)
+            for row in range(r0 * BM, r1 * BM):
+                d = int(row_dst[row])
+                for j in range(plan.Nt):
+                    s.pools[d].append(Y[row, j * BN:(j + 1) * BN].copy())
+                    s.meta[d].append((row, j))
+            for d in range(n):
+                s.ranges[d][gj] = (start[d], len(s.pools[d]))
+            continue
         for p in range(ps, pe):
             i, j = plan.tile_of_position(p)
             for a in range(BM):

@@ -259,3 +259,58 @@ def test_rs_rowband_equals_definition_bruteforce():
             slot = opl.run_reducescatter(As, Bts, pl)
             for k in range(n):
                 assert np.array_equal(slot["out"][k], res["out"][k])
+
+
+# ---------------------------------------------------------------- A2A rowband (R41)
+def test_a2a_rowband_hand_example():
+    """4x4 output of 2x2 tiles, row_dst = [1, 0, 1, 1], raster, one tile-row
+    per group.  Worked by hand: the paper's layout (subtokens in
+    execution order p, then row) fills pool 1 with (0,0),(0,1),(2,0),(3,0),
+    (2,1),(3,1); the rowband layout keeps rows whole: (0,0),(0,1),(2,0),(2,1),
+    (3,0),(3,1); pool 0 is (1,0),(1,1) in both."""
+    pl = op.make_plan(4, 4, 2, 2, 2, [1, 1], swizzle=1)
+    Y = np.arange(16, dtype=float).reshape(4, 4)
+    rd = [1, 0, 1, 1]
+    slot = orr.a2a_pre(Y, pl, rd, 2)
+    band = orr.a2a_pre(Y, pl, rd, 2, "rowband")
+    assert slot.meta[1] == [(0, 0), (0, 1), (2, 0), (3, 0), (2, 1), (3, 1)]
+    assert band.meta[1] == [(0, 0), (0, 1), (2, 0), (2, 1), (3, 0), (3, 1)]
+    assert band.meta[0] == slot.meta[0] == [(1, 0), (1, 1)]
+    assert band.ranges[1] == [(0, 2), (2, 6)] and band.ranges[0] == [(0, 2), (2, 2)]
+    assert np.array_equal(band.pools[1].reshape(-1), Y[[0, 2, 3]].reshape(-1))
+
+
+def test_a2a_rowband_equals_definition_bruteforce():
+    """Per-group A2A in the rowband layout == the plain all-to-all-v, for
+    imbalanced sources with random routing at n = 1..4; and what a receiver
+    gets from one source in one group is a run of consecutive complete output
+    rows (so it can be received straight into the output)."""
+    rng = np.random.default_rng(41)
+    for n in (1, 2, 3, 4):
+        for _ in range(25):
+            BM, BN, Nt = int(rng.choice((1, 2, 3))), int(rng.integers(1, 3)), int(rng.integers(1, 3))
+            P = int(rng.integers(1, 3))
+            plans, rds, As, Bts = [], [], [], []
+            for _s in range(n):
+                Mt = int(rng.integers(P, P + 3))
+                plans.append(op.make_plan(Mt * BM, Nt * BN, BM, BN, Nt, [1] * (P - 1) + [Mt - P + 1], swizzle=1))
+                rds.append(rng.integers(0, n, size=Mt * BM))
+                As.append(rng.integers(-3, 4, size=(Mt * BM, 2)).astype(float))
+                Bts.append(rng.integers(-3, 4, size=(Nt * BN, 2)).astype(float))
+            assert orr.a2a_rowband_ok(plans)
+            res = opl.run_alltoall(As, Bts, plans, rds, layout="rowband")
+            plain = opl.plain_alltoall(As, Bts, rds)
+            for d in range(n):
+                assert np.array_equal(res["out"][d], plain[d])
+            for s_ in range(n):
+                snd = res["send"][s_]
+                for d in range(n):
+                    rows_to_d = list(np.flatnonzero(np.asarray(rds[s_]) == d))
+                    for (a, b) in snd.ranges[d]:
+                        meta = snd.meta[d][a:b]
+                        assert len(meta) % Nt == 0
+                        rows = [meta[i][0] for i in range(0, len(meta), Nt)]
+                        assert all(meta[i] == (rows[i // Nt], i % Nt) for i in range(len(meta)))
+                        if rows:
+                            k0 = rows_to_d.index(rows[0])
+                            assert rows == rows_to_d[k0:k0 + len(rows)]
