@@ -65,7 +65,7 @@ typedef enum {
   FO_NOCOMM = 3         /* plain GEMM writing row-major C (sequential baseline, tuner)  */
 } fo_coll;
 
-/* AllReduce / ReduceScatter buffer layout (H11a, R40). */
+/* AllReduce / ReduceScatter / All-to-All buffer layout (H11a, R40, R41). */
 typedef enum {
   FO_LAYOUT_SLOT = 0,    /* paper: AR: tile at position p -> contiguous slot p (tile_m*tile_n elems, row-major);
                             RS: subtile k of every tile of a group -> chunk k of the group */
@@ -73,9 +73,13 @@ typedef enum {
                             both reorders are the identity.  RS (bands must also be ascending in group order):
                             chunk k of a band holds the k-th subtile rows of its tiles as complete rows, so the
                             ReduceScatter of the band lands the rank's block-cyclic rows R_k directly in `out`
-                            (no receive buffer, no post-communication reorder) */
+                            (no receive buffer, no post-communication reorder).  A2A (every source's bands
+                            ascending, decided from the census descriptors so all ranks agree): pools hold complete
+                            rows in source-row order and each group's rows from a source are received straight
+                            into their output rows (R41) */
   FO_LAYOUT_AUTO = 2     /* ROWBAND when legal, else SLOT; with swizzle 0 the default order prefers panel heights
-                            whose panels end on the group boundaries (AR and RS) */
+                            whose panels end on the group boundaries (AR and RS; ROWBAND asked for explicitly:
+                            any collective) */
 } fo_ar_layout;
 
 /* Elementwise op fused into the post-communication reorder (R12). */
@@ -95,7 +99,7 @@ typedef struct fo_plan_s* fo_plan;
  * read during fo_plan_create only. */
 typedef struct {
   int32_t coll;          /* fo_coll */
-  int32_t ar_layout;     /* fo_ar_layout (AllReduce and ReduceScatter; ignored otherwise) */
+  int32_t ar_layout;     /* fo_ar_layout (AllReduce, ReduceScatter, All-to-All; ignored for no-comm) */
   int64_t m, n, k;       /* this rank's GEMM: A [m,k], Bt [n,k], C [m,n]; k = K/world for TP */
   int32_t tile_m;        /* 64 or 128 (one CTA, tcgen05.mma M=64 / M=128; 64: K-major operands, no tail split)
                             or 256 (cta_group::2 CTA pair) */
@@ -121,7 +125,7 @@ typedef struct {
   int32_t workers;       /* S actually used */
   int32_t waves;         /* T */
   int32_t num_groups;    /* P */
-  int32_t ar_layout;     /* resolved layout (AllReduce / ReduceScatter; SLOT for All-to-All, ROWBAND no-comm) */
+  int32_t ar_layout;     /* resolved layout (ROWBAND for no-comm) */
   int32_t rs_subtile_rows; /* h = tile_m / world (ReduceScatter) */
   int64_t send_elems;    /* elements of the pre-reordered send buffer */
   int64_t recv_elems;    /* elements of the receive layout (AR: == send; RS ROWBAND: it is `out` itself) */

@@ -49,8 +49,8 @@ int auto_swizzle(int Mt, int Nt, int S) {
 // the group boundaries (every group is then a band of whole tile-rows, panels
 // top to bottom -> ROWBAND layout, no reorder at all) unless the
 // unconstrained footprint is much smaller.
-static int auto_swizzle_ar(int Mt, int Nt, int S, const std::vector<int32_t>& gpos) {
-  const int any = auto_swizzle(Mt, Nt, S);
+// The band-aligned panel height with the smallest wave footprint (-1: none).
+static int band_swizzle(int Mt, int Nt, int S, const std::vector<int32_t>& gpos, long* fp_out) {
   int band = -1;
   long band_fp = -1;
   for (int s = 1; s <= Mt; ++s) {
@@ -63,6 +63,14 @@ static int auto_swizzle_ar(int Mt, int Nt, int S, const std::vector<int32_t>& gp
       band_fp = fp;
     }
   }
+  if (fp_out) *fp_out = band_fp;
+  return band;
+}
+
+static int auto_swizzle_ar(int Mt, int Nt, int S, const std::vector<int32_t>& gpos) {
+  const int any = auto_swizzle(Mt, Nt, S);
+  long band_fp = -1;
+  const int band = band_swizzle(Mt, Nt, S, gpos, &band_fp);
   if (band > 0 && 4 * band_fp <= 5 * wave_footprint(Mt, Nt, S, any)) return band;
   return any;
 }
@@ -121,10 +129,16 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
   } else {
     if (d.swizzle < 0) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 0");
     int s = d.swizzle;
-    if (s == 0)
-      s = ((d.coll == FO_ALLREDUCE || d.coll == FO_REDUCESCATTER) && d.ar_layout != FO_LAYOUT_SLOT)
+    if (s == 0) {
+      // ROWBAND asked for: the best band-aligned panel height; AUTO (AR / RS):
+      // band-aligned unless its footprint is much larger; otherwise (and
+      // A2A AUTO) the footprint-minimal height
+      const int band = d.ar_layout == FO_LAYOUT_ROWBAND ? band_swizzle(g.Mt, g.Nt, d.workers, g.gpos, nullptr) : -1;
+      s = band > 0 ? band
+          : ((d.coll == FO_ALLREDUCE || d.coll == FO_REDUCESCATTER) && d.ar_layout != FO_LAYOUT_SLOT)
               ? auto_swizzle_ar(g.Mt, g.Nt, d.workers, g.gpos)
               : auto_swizzle(g.Mt, g.Nt, d.workers);
+    }
     g.order = default_order(g.Mt, g.Nt, s);
   }
   (void)world;
@@ -164,29 +178,34 @@ static A2ASide a2a_census(const fo_plan_desc& d, const Grid& g, int world) {
 // band_rows.  `ascending`: the bands must also follow each other top to bottom
 // in group order (ReduceScatter: the receive buffer concatenates the groups'
 // chunks, which is then the output itself).
-static bool band_layout(PlanHost& p, bool ascending) {
-  p.band_rows.assign(2 * p.P, 0);
+static bool bands_of(int Mt, int Nt, int P, const std::vector<int32_t>& gpos, const std::vector<int32_t>& order,
+                     bool ascending, std::vector<int64_t>* band_rows) {
+  band_rows->assign(2 * P, 0);
   int64_t next = 0;
-  for (int j = 0; j < p.P; ++j) {
-    const int lo = p.gpos[j], hi = p.gpos[j + 1];
-    if ((hi - lo) % p.Nt) return false;
-    int rmin = p.Mt, rmax = -1;
+  for (int j = 0; j < P; ++j) {
+    const int lo = gpos[j], hi = gpos[j + 1];
+    if ((hi - lo) % Nt) return false;
+    int rmin = Mt, rmax = -1;
     std::vector<char> seen((size_t)(hi - lo), 0);
-    for (int q = lo; q < hi; ++q) rmin = std::min(rmin, p.order[q] / p.Nt);
-    const int r1 = rmin + (hi - lo) / p.Nt;
+    for (int q = lo; q < hi; ++q) rmin = std::min(rmin, order[q] / Nt);
+    const int r1 = rmin + (hi - lo) / Nt;
     for (int q = lo; q < hi; ++q) {
-      const int t = p.order[q] - rmin * p.Nt;
+      const int t = order[q] - rmin * Nt;
       if (t < 0 || t >= hi - lo || seen[t]) return false;
       seen[t] = 1;
-      rmax = std::max(rmax, p.order[q] / p.Nt);
+      rmax = std::max(rmax, order[q] / Nt);
     }
     if (rmax >= r1) return false;
     if (ascending && rmin != next) return false;
     next = r1;
-    p.band_rows[2 * j] = rmin;
-    p.band_rows[2 * j + 1] = r1;
+    (*band_rows)[2 * j] = rmin;
+    (*band_rows)[2 * j + 1] = r1;
   }
   return true;
+}
+
+static bool band_layout(PlanHost& p, bool ascending) {
+  return bands_of(p.Mt, p.Nt, p.P, p.gpos, p.order, ascending, &p.band_rows);
 }
 
 PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_desc* const* peers,
@@ -260,25 +279,7 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
       for (int64_t r = 0; r < p.M; ++r)
         if (d.row_dst[r] < 0 || d.row_dst[r] >= world) fail(FO_ERR_INVALID_ARG, "row_dst[%lld] out of range", (long long)r);
       p.row_dst.assign(d.row_dst, d.row_dst + p.M);
-      // ---- send side (self)
-      A2ASide me = a2a_census(d, g, world);
-      p.send_cnt = me.cnt;
-      p.send_start = me.start;
-      p.pool_base.assign(world + 1, 0);
-      for (int dd = 0; dd < world; ++dd) p.pool_base[dd + 1] = p.pool_base[dd] + me.total[dd];
-      p.send_elems = p.pool_base[world] * p.BN;
-      p.row_slot.assign((size_t)p.tiles * p.BM, -1);
-      {
-        std::vector<int64_t> fill(world, 0);
-        for (int q = 0; q < p.tiles; ++q) {
-          int i = p.order[q] / p.Nt;
-          for (int r = 0; r < p.BM; ++r) {
-            int dst = p.row_dst[(int64_t)i * p.BM + r];
-            p.row_slot[(size_t)q * p.BM + r] = (int32_t)(p.pool_base[dst] + fill[dst]++);
-          }
-        }
-      }
-      // ---- receive side: needs every source's descriptor (the census exchange)
+      // ---- every source's grid (the census exchange: peers' descriptors)
       if (!peers) fail(FO_ERR_INVALID_ARG, "All-to-All needs the peers' descriptors");
       std::vector<Grid> pg(world);
       for (int s = 0; s < world; ++s) {
@@ -289,6 +290,51 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
         if (!ps->row_dst) fail(FO_ERR_INVALID_ARG, "peer %d: row_dst missing", s);
         pg[s] = make_grid(*ps, world);
         if (pg[s].P != p.P) fail(FO_ERR_INVALID_ARG, "peer %d has %d groups, self %d", s, pg[s].P, p.P);
+      }
+      // ROWBAND (R41): every source asks for it (or AUTO) and every
+      // source's groups are ascending bands of whole tile-rows — decided from
+      // the same descriptors on every rank, so senders and receivers agree
+      bool band = true;
+      std::vector<std::vector<int64_t>> bands(world);
+      for (int s = 0; s < world && band; ++s) {
+        const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
+        band = ps->ar_layout != FO_LAYOUT_SLOT &&
+               bands_of(pg[s].Mt, pg[s].Nt, pg[s].P, pg[s].gpos, pg[s].order, true, &bands[s]);
+      }
+      if (d.ar_layout == FO_LAYOUT_ROWBAND && !band)
+        fail(FO_ERR_UNSUPPORTED, "A2A ROWBAND layout needs every source's groups to be ascending bands of whole tile-rows");
+      p.layout = band ? FO_LAYOUT_ROWBAND : FO_LAYOUT_SLOT;
+      if (band) p.band_rows = bands[rank];
+      // ---- send side (self)
+      A2ASide me = a2a_census(d, g, world);
+      p.send_cnt = me.cnt;
+      p.send_start = me.start;
+      p.pool_base.assign(world + 1, 0);
+      for (int dd = 0; dd < world; ++dd) p.pool_base[dd + 1] = p.pool_base[dd] + me.total[dd];
+      p.send_elems = p.pool_base[world] * p.BN;
+      p.row_slot.assign((size_t)p.tiles * p.BM, -1);
+      {
+        std::vector<int64_t> fill(world, 0);
+        if (band) {
+          // pool d: complete rows, source row ascending (bands ascending), then
+          // tile-column: subtoken (row, jc) of tile (row/BM, jc) at position q
+          for (int64_t r = 0; r < p.M; ++r) {
+            const int dst = p.row_dst[r];
+            const int i = (int)(r / p.BM);
+            for (int jc = 0; jc < p.Nt; ++jc) {
+              const int q = p.pos_of_tile[i * p.Nt + jc];
+              p.row_slot[(size_t)q * p.BM + r % p.BM] = (int32_t)(p.pool_base[dst] + fill[dst]++);
+            }
+          }
+        } else {
+          for (int q = 0; q < p.tiles; ++q) {
+            int i = p.order[q] / p.Nt;
+            for (int r = 0; r < p.BM; ++r) {
+              int dst = p.row_dst[(int64_t)i * p.BM + r];
+              p.row_slot[(size_t)q * p.BM + r] = (int32_t)(p.pool_base[dst] + fill[dst]++);
+            }
+          }
+        }
       }
       // output rows: sources ascending, then source rows ascending (all-to-all-v order)
       p.src_base.assign(world + 1, 0);
@@ -302,13 +348,32 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
         p.src_base[s + 1] = p.src_base[s] + c;
       }
       p.out_rows = p.src_base[world];
-      // receive layout [group j][source s] (R9)
+      // receive layout [group j][source s] (R9); ROWBAND: the output
+      // itself — group j's rows from source s are the run of output rows
+      // starting at the first of them (R41)
       p.recv_cnt.assign((size_t)p.P * world, 0);
       p.recv_off.assign((size_t)p.P * world, 0);
       std::vector<A2ASide> sides(world);
       for (int s = 0; s < world; ++s) {
         const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
         sides[s] = a2a_census(*ps, pg[s], world);
+      }
+      if (band) {
+        for (int j = 0; j < p.P; ++j)
+          for (int s = 0; s < world; ++s) {
+            const fo_plan_desc* ps = (s == rank) ? &d : peers[s];
+            p.recv_cnt[(size_t)j * world + s] = sides[s].cnt[(size_t)j * world + rank];
+            const int64_t b0 = bands[s][2 * j] * ps->tile_m, b1 = bands[s][2 * j + 1] * ps->tile_m;
+            int64_t first = -1;
+            for (int64_t r = b0; r < b1 && first < 0; ++r)
+              if (ps->row_dst[r] == rank) first = rank_of_row[s][r];
+            p.recv_off[(size_t)j * world + s] = first < 0 ? 0 : (p.src_base[s] + first) * p.Nt;
+          }
+        p.recv_elems = p.out_rows * p.N;
+        p.src_row.resize((size_t)p.out_rows * p.Nt);
+        p.recv_dst.resize((size_t)p.out_rows * p.Nt);
+        for (int64_t x = 0; x < p.out_rows * p.Nt; ++x) p.src_row[(size_t)x] = p.recv_dst[(size_t)x] = (int32_t)x;
+        break;
       }
       int64_t off = 0;
       for (int j = 0; j < p.P; ++j)
@@ -341,7 +406,6 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
     }
   }
   if (p.coll == FO_NOCOMM) p.layout = FO_LAYOUT_ROWBAND;
-  else if (p.coll == FO_ALLTOALL) p.layout = FO_LAYOUT_SLOT;
   build_schedules(p, d, peers);
   return p;
 }

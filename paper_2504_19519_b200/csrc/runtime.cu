@@ -489,7 +489,7 @@ static int post_map(const PlanHost& h) {
   switch (h.coll) {
     case FO_ALLREDUCE: return h.layout == FO_LAYOUT_ROWBAND ? POSTMAP_IDENTITY : POSTMAP_SLOT;
     case FO_REDUCESCATTER: return h.banded() ? POSTMAP_IDENTITY : POSTMAP_RS;
-    case FO_ALLTOALL: return POSTMAP_A2A;
+    case FO_ALLTOALL: return h.layout == FO_LAYOUT_ROWBAND ? POSTMAP_IDENTITY : POSTMAP_A2A;
     default: return POSTMAP_IDENTITY;
   }
 }
@@ -635,10 +635,11 @@ static void exec_calls(fo_ctx_s* c, const std::vector<fo_comm_call>& calls, size
 }
 
 // The collective of group j ("Once the j-th number reaches
-// |G_j|, the communication of G_j starts"): the plan's calls of group j.
-static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* out, cudaStream_t cs) {
+// |G_j|, the communication of G_j starts"): the plan's calls of group j on
+// the run's send / receive buffers.
+static void group_collective(fo_ctx_s* c, fo_plan_s* p, int j, void* send, void* recv, void* out, cudaStream_t cs) {
   const PlanHost& h = p->host;
-  void* const bufs[4] = {p->d_send, p->d_recv, out, nullptr};
+  void* const bufs[4] = {send, recv, out, nullptr};
   exec_calls(c, h.calls, (size_t)h.call_begin[j], (size_t)h.call_begin[j + 1], bufs, cs);
 }
 
@@ -885,7 +886,14 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     // post-communication data is `out`
     const bool rowband = (h.coll == FO_NOCOMM) || h.banded();
     const bool gemm_out = (h.coll == FO_NOCOMM) || (h.banded() && (h.coll == FO_ALLREDUCE || h.world == 1));
-    void* gemm_dst = gemm_out ? out : p->d_send;
+    // A2A ROWBAND (R41): the groups' rows are received straight into `out`
+    // (the output layout), except under the MoE combine, whose `out` is the
+    // combined tokens: then into the library's receive buffer; at one rank
+    // send, receive and output layouts coincide
+    const bool a2a_band = h.coll == FO_ALLTOALL && h.layout == FO_LAYOUT_ROWBAND;
+    void* recv_buf = (a2a_band && !p->combine) ? out : p->d_recv;
+    void* send_buf = (a2a_band && !p->combine && h.world == 1) ? out : p->d_send;
+    void* gemm_dst = gemm_out ? out : send_buf;
     // a single group issued in stream order (R32) waits on no counter: the GEMM
     // then neither signals nor needs the counting table reset
     const bool counted = !(p->last_in_order && h.coll != FO_NOCOMM && h.P == 1);
@@ -899,7 +907,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
     // 3. GEMM with reorder + signal epilogue
     run_gemm(p, A, Bt, gemm_dst, epi_mode(h), counted, s, p->trace_tile_ts);
     const bool gpost = use_group_post(p) && !p->combine;
-    const void* post_src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : p->d_recv);
+    const void* post_src = (h.coll == FO_ALLREDUCE) ? (rowband ? out : p->d_send) : (rowband ? out : recv_buf);
     // 4. per-group wait + collective; the per-group post-reorder runs on the
     //    post stream, chained to its group's collective by an event, so the
     //    next group's collective never queues behind a reorder
@@ -928,7 +936,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
           stream_wait(p, wait, cs, j);
         }
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j, cs));
-        group_collective(c, p, j, out, cs);
+        group_collective(c, p, j, send_buf, recv_buf, out, cs);
         cudaStream_t ps = cs;
         if (gpost) {
           if (!on_s) {

@@ -145,7 +145,7 @@ def main(W):
             p.close()
     # ---- All-to-All: imbalanced experts, random routing, same P on every rank
     rng = np.random.default_rng(7 + W)
-    Ms = [256 * int(rng.integers(1, 5)) for _ in range(W)]
+    Ms = [256 * int(rng.integers(2, 5)) for _ in range(W)]   # >= 2 tile-rows: two one-row waves
     rds = [rng.integers(0, W, size=Ms[s]).astype(np.int32) for s in range(W)]
     inp = [synthetic.exact_inputs(Ms[s], N, K, seed=synthetic.rank_seed(71, W, s), nnz_per_row=128)
            for s in range(W)]
@@ -153,30 +153,34 @@ def main(W):
     Bts = [b.double().numpy() for _, b in inp]
     Ad = [a.cuda() for a, _ in inp]
     Bd = [b.cuda() for _, b in inp]
-    S2 = 2
-    specs = []
-    for s in range(W):
-        T = -(-(Ms[s] // BM) * (N // BN) // S2)
-        specs.append(dict(coll="alltoall", m=Ms[s], n=N, k=K, tile_m=BM, tile_n=BN, workers=S2, swizzle=2,
-                          group_waves=[1, T - 1], row_dst=rds[s]))
-    plans = [fo.Plan(rank=r, world=W, peers=specs, **specs[r]) for r in range(W)]
-    print(f"[W={W}] alltoall Ms={Ms}", flush=True)
-    for p in plans:
-        p.prepare(sequential=True)
     want = opl.plain_alltoall(As, Bts, rds)
-    outs = [torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda") for p in plans]
-    torch.cuda.synchronize()
-    for _ in range(3):
-        each(lambda r: fo.run(ctxs[r], plans[r], Ad[r], Bd[r], outs[r], stream=streams[r]))
-    for r in range(W):
-        check(f"alltoall/rank{r}", outs[r], want[r])
-    seq = [torch.full_like(o, float("nan")) for o in outs]
-    torch.cuda.synchronize()
-    each(lambda r: fo.run_sequential(ctxs[r], plans[r], Ad[r], Bd[r], seq[r], stream=streams[r]))
-    for r in range(W):
-        check(f"alltoall/sequential/rank{r}", seq[r], want[r])
-    for p in plans:
-        p.close()
+    # the paper's subtoken pools (S = 2) and R41's rows received straight into
+    # the output (raster, one tile-row per wave)
+    for layout, S2, swz in (("slot", 2, 2), ("rowband", N // BN, 1)):
+        specs = []
+        for s in range(W):
+            T = -(-(Ms[s] // BM) * (N // BN) // S2)
+            specs.append(dict(coll="alltoall", m=Ms[s], n=N, k=K, tile_m=BM, tile_n=BN, workers=S2, swizzle=swz,
+                              group_waves=[1, T - 1], row_dst=rds[s], ar_layout=layout))
+        plans = [fo.Plan(rank=r, world=W, peers=specs, **specs[r]) for r in range(W)]
+        assert all(p.info["ar_layout"] == (1 if layout == "rowband" else 0) for p in plans)
+        print(f"[W={W}] alltoall/{layout} Ms={Ms}", flush=True)
+        for p in plans:
+            p.prepare(sequential=True)
+        outs = [torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda")
+                for p in plans]
+        torch.cuda.synchronize()
+        for _ in range(3):
+            each(lambda r: fo.run(ctxs[r], plans[r], Ad[r], Bd[r], outs[r], stream=streams[r]))
+        for r in range(W):
+            check(f"alltoall/{layout}/rank{r}", outs[r], want[r])
+        seq = [torch.full_like(o, float("nan")) for o in outs]
+        torch.cuda.synchronize()
+        each(lambda r: fo.run_sequential(ctxs[r], plans[r], Ad[r], Bd[r], seq[r], stream=streams[r]))
+        for r in range(W):
+            check(f"alltoall/{layout}/sequential/rank{r}", seq[r], want[r])
+        for p in plans:
+            p.close()
     for c in ctxs:
         c.close()
     grp.close()

@@ -136,7 +136,8 @@ def test_reducescatter_schedule(world, layout):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("routing", ["random", "sorted", "skewed"])
-def test_alltoall_schedule(world, routing):
+@pytest.mark.parametrize("layout", ["slot", "rowband"])
+def test_alltoall_schedule(world, routing, layout):
     rng = np.random.default_rng(300 + world + {"random": 0, "sorted": 50, "skewed": 90}[routing])
     for _ in range(6):
         BM = int(rng.choice([128, 256]))
@@ -144,6 +145,8 @@ def test_alltoall_schedule(world, routing):
         N = BN * int(rng.integers(1, 4))
         Ms = [BM * int(rng.integers(1, 4)) for _ in range(world)]          # imbalanced experts
         S = int(rng.integers(1, 3))
+        if layout == "rowband":
+            S = N // BN      # raster, one tile-row per wave: ascending bands on every source (R41)
         Ts = [-(-(m // BM) * (N // BN) // S) for m in Ms]
         P = int(rng.integers(1, min(Ts) + 1))                             # a common number of groups
         parts = []
@@ -160,12 +163,13 @@ def test_alltoall_schedule(world, routing):
             else:
                 rd = np.sort(rng.integers(0, world, size=Ms[s]))
             rds.append(rd.astype(np.int32))
-        specs = [dict(coll="alltoall", m=Ms[s], n=N, k=64, tile_m=BM, tile_n=BN, workers=S, swizzle=1 + s % 2,
-                      group_waves=parts[s], row_dst=rds[s]) for s in range(world)]
+        swz = [1 if layout == "rowband" else 1 + s % 2 for s in range(world)]
+        specs = [dict(coll="alltoall", m=Ms[s], n=N, k=64, tile_m=BM, tile_n=BN, workers=S, swizzle=swz[s],
+                      group_waves=parts[s], row_dst=rds[s], ar_layout=layout) for s in range(world)]
         plans = [fo.Plan(rank=r, world=world, peers=specs, **specs[r]) for r in range(world)]
-        opls = [op.make_plan(Ms[s], N, BM, BN, S, parts[s], swizzle=1 + s % 2) for s in range(world)]
+        opls = [op.make_plan(Ms[s], N, BM, BN, S, parts[s], swizzle=swz[s]) for s in range(world)]
         Ys = [_ints(rng, (Ms[s], N)) for s in range(world)]
-        osends = [orr.a2a_pre(Ys[s], opls[s], rds[s], world) for s in range(world)]
+        osends = [orr.a2a_pre(Ys[s], opls[s], rds[s], world, layout) for s in range(world)]
         orecv = oc.alltoall_groups(osends, P)
         bufs = []
         for r in range(world):
@@ -174,6 +178,11 @@ def test_alltoall_schedule(world, routing):
             bufs.append(b)
         comm_sim.run([p.export_calls(0) for p in plans], bufs)
         for d in range(world):
+            if layout == "rowband":
+                # the receive layout is the output: the all-to-all-v rows themselves
+                want = np.concatenate([Ys[s][rds[s] == d] for s in range(world)], axis=0).reshape(-1)
+                np.testing.assert_array_equal(bufs[d]["recv"], want)
+                continue
             want = np.concatenate([a.reshape(-1) for _, a in orecv[d]]) if orecv[d] else np.zeros(0)
             np.testing.assert_array_equal(bufs[d]["recv"][:want.size], want)
         # sequential: runs of one destination, all-to-all-v output order

@@ -134,27 +134,34 @@ def test_random_a2a_plan_matches_oracle(seed):
     N, K = Nt * BN, 64 * int(rng.integers(1, 5))
     Mts = [int(rng.integers(1, 5)) for _ in range(n)]
     P = min(int(rng.integers(1, 4)), min(Mts) * Nt)   # every rank needs at least P waves
+    layout = "auto" if seed % 2 else "slot"
+    bands = layout == "auto" and seed % 4 == 1
     specs, oplans, As, Bts, rds = [], [], [], [], []
     for s_ in range(n):
         Mt = Mts[s_]
         M = Mt * BM
         tiles = Mt * Nt
         S = int(rng.integers(1, max(1, tiles // P) + 1))
+        swz = 2
+        if bands and Mt >= P:   # raster, waves of whole tile-rows: R41 rowband under "auto"
+            S, swz = Nt, 1
         T = op.num_waves(tiles, S)
         if T < P:
             S, T = 1, tiles
         part = [1] * (P - 1) + [T - (P - 1)]
         rd = synthetic.random_row_dst(M, n, 3000 + 10 * seed + s_)
         A, Bt = synthetic.exact_inputs(M, N, K, seed=900 + 10 * seed + s_, nnz_per_row=64)
-        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2,
-                          group_waves=part, row_dst=rd))
-        oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=2))
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=swz,
+                          group_waves=part, row_dst=rd, ar_layout=layout))
+        oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=swz))
         As.append(A), Bts.append(Bt), rds.append(rd)
-    ores = opl.run_alltoall(As, Bts, oplans, rds)
+    lay = "rowband" if layout == "auto" and orr.a2a_rowband_ok(oplans) else "slot"
+    ores = opl.run_alltoall(As, Bts, oplans, rds, layout=lay)
     plain = opl.plain_alltoall(As, Bts, rds)
     for me in range(n):
         plan = fo.Plan(rank=me, world=n, peers=specs, **specs[me])
         send = torch.empty(plan.info["send_elems"], dtype=torch.bfloat16, device="cuda")
+        assert plan.info["ar_layout"] == (1 if lay == "rowband" else 0), f"seed {seed}"
         fo.gemm_stage(plan, As[me].cuda(), Bts[me].cuda(), send)
         torch.cuda.synchronize()
         flat = np.concatenate([ores["send"][me].pools[d].reshape(-1) for d in range(n)])
@@ -162,7 +169,10 @@ def test_random_a2a_plan_matches_oracle(seed):
         mult = max(1, BM // 128)
         want = [mult * t for t in op.group_thresholds(oplans[me].partition, oplans[me].S, oplans[me].ntiles)]
         assert plan.read_counters().tolist() == want
-        recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][me]]) if ores["recv"][me] else np.zeros(0)
+        if lay == "rowband":   # received straight into the output layout
+            recv = ores["out"][me].reshape(-1)
+        else:
+            recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][me]]) if ores["recv"][me] else np.zeros(0)
         out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plan, _bf16(recv), out)
         torch.cuda.synchronize()

@@ -218,7 +218,15 @@ def test_tune_layer_world1_returns_a_valid_plan():
         fo.run(ctx, plan, A, Bt, out, *((res, gam) if post != "none" else ()))
         torch.cuda.synchronize()
     ch = tuner.tune_layer(M, N, K, ctx, "reducescatter", "none", iters=3, sizes=[1 << 18, 1 << 22])
-    assert ch.layout == "auto"
+    assert ch.layout in ("rowband", "slot")            # both RS layouts are searched (R40)
+    assert any(":rowband" in c[1] for c in ch.candidates) and any(":slot" in c[1] for c in ch.candidates)
+    plan = fo.Plan(**ch.spec(M, N, K, "reducescatter"))
+    assert plan.info["ar_layout"] == (1 if ch.layout == "rowband" else 0)
+    fo.run(ctx, plan, A, Bt, out)
+    want = torch.empty_like(out)
+    fo.run_sequential(ctx, plan, A, Bt, want)    # one rank: the RS output is every row, in order
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
     # two communicators (CTA caps): the SM split is searched across both and
     # the chosen context's index comes back
     ctx2 = fo.Context.create(0, 0, 1, fo.unique_id(), nccl_max_ctas=32)

@@ -44,7 +44,7 @@ def _plans(kind, post):
         M = 256 * (s + 1)
         rd = synthetic.random_row_dst(M, n, 50 + s)
         specs.append(dict(coll="alltoall", m=M, n=512, k=64, tile_m=256, tile_n=128, workers=2, swizzle=1,
-                          group_waves=[1, -(-(M // 256) * 4 // 2) - 1], row_dst=rd, post=post))
+                          group_waves=[1, -(-(M // 256) * 4 // 2) - 1], row_dst=rd, post=post, ar_layout="slot"))
     return fo.Plan(rank=1, world=n, peers=specs, **specs[1])
 
 

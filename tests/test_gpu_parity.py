@@ -213,34 +213,45 @@ def test_reducescatter_rowband_stages_exact(n, BM, BN, Mt, Nt, rows_per_wave, K)
 
 @pytest.mark.parametrize("BM", [64, 128, 256])
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
-def test_alltoall_stages_exact(n, BM):
+@pytest.mark.parametrize("layout", ["slot", "rowband"])
+def test_alltoall_stages_exact(n, BM, layout):
+    """Every rank's pools (the paper's subtoken order, or R41's complete rows),
+    counters and post pass bit-exact vs the oracle."""
     rng = np.random.default_rng(n)
     N, K, BN, P = 512, 128, 128, 2
+    Nt = N // BN
     specs, oplans, As, Bts, rds = [], [], [], [], []
     for s in range(n):
         Mt = int(rng.integers(2, 5))
         M = Mt * BM
-        tiles = Mt * (N // BN)
+        tiles = Mt * Nt
         S = int(rng.integers(1, tiles // P + 1))
+        swz = 2
+        if layout == "rowband":   # raster, waves of whole tile-rows
+            S, swz = Nt * int(rng.integers(1, Mt // P + 1)), 1
         T = op.num_waves(tiles, S)
         part = [1] * (P - 1) + [T - (P - 1)]
         rd = synthetic.random_row_dst(M, n, 1000 + s)
         A, Bt = synthetic.exact_inputs(M, N, K, seed=300 + s, nnz_per_row=64)
-        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=2,
-                          group_waves=part, row_dst=rd))
-        oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=2))
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=swz,
+                          group_waves=part, row_dst=rd, ar_layout=layout))
+        oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=swz))
         As.append(A), Bts.append(Bt), rds.append(rd)
-    ores = opl.run_alltoall(As, Bts, oplans, rds)
+    ores = opl.run_alltoall(As, Bts, oplans, rds, layout=layout)
     plain = opl.plain_alltoall(As, Bts, rds)
     for me in range(n):
         plan = fo.Plan(rank=me, world=n, peers=specs, **specs[me])
+        assert plan.info["ar_layout"] == (1 if layout == "rowband" else 0)
         send = torch.empty(plan.info["send_elems"], dtype=torch.bfloat16, device="cuda")
         fo.gemm_stage(plan, _dev_bf16(As[me]), _dev_bf16(Bts[me]), send)
         torch.cuda.synchronize()
         flat = np.concatenate([ores["send"][me].pools[d].reshape(-1) for d in range(n)])
         assert np.array_equal(_host(send), flat)
         _counters_ok(plan, oplans[me])
-        recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][me]]) if ores["recv"][me] else np.zeros(0)
+        if layout == "rowband":   # the receive layout is the output itself
+            recv = ores["out"][me].reshape(-1)
+        else:
+            recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][me]]) if ores["recv"][me] else np.zeros(0)
         out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plan, _dev_bf16(recv), out)
         torch.cuda.synchronize()
@@ -592,7 +603,8 @@ def test_alltoall_rank_receiving_nothing():
         M = 256 * (s + 1)
         rd = np.zeros(M, np.int32)
         A, Bt = synthetic.exact_inputs(M, N, K, seed=90 + s, nnz_per_row=64)
-        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=2, group_waves=[1, (M // BM * 2 + 1) // 2 - 1], row_dst=rd))
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=2, group_waves=[1, (M // BM * 2 + 1) // 2 - 1], row_dst=rd,
+                          ar_layout="slot"))
         oplans.append(op.make_plan(M, N, BM, BN, 2, specs[-1]["group_waves"]))
         As.append(A), Bts.append(Bt), rds.append(rd)
     ores = opl.run_alltoall(As, Bts, oplans, rds)
@@ -666,7 +678,7 @@ def test_moe_combine_stages(n, k, skew):
             T = op.num_waves(tiles, S)
             part = [1, T - 1]
         specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=1,
-                          group_waves=part, row_dst=rt["row_dst"][e]))
+                          group_waves=part, row_dst=rt["row_dst"][e], ar_layout="slot"))
         oplans.append(op.make_plan(M, N, BM, BN, S, part, swizzle=1))
         As.append(A), Bts.append(Bt)
     ores = opl.run_alltoall(As, Bts, oplans, rt["row_dst"])

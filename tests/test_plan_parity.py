@@ -127,32 +127,39 @@ def test_reducescatter_maps(world, layout):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
-def test_alltoall_maps_and_census(world):
+@pytest.mark.parametrize("layout", ["slot", "auto"])
+def test_alltoall_maps_and_census(world, layout):
     rng = np.random.default_rng(30 + world)
     for case in range(12):
         BN = int(rng.choice([64, 128]))
         Nt = int(rng.integers(1, 3))
         N = Nt * BN
         P = int(rng.integers(1, 3))
+        bands = layout == "auto" and case % 2 == 0   # raster, waves of whole tile-rows (R41)
         specs, oplans, row_dsts = [], [], []
         for s in range(world):
             Mt = int(rng.integers(max(1, P), 4))
             tiles = Mt * Nt
             # choose S so that T >= P
             S = int(rng.integers(1, max(1, tiles // P) + 1))
+            order = synthetic.random_order(tiles, int(rng.integers(1 << 30))) if rng.random() < 0.5 else None
+            if bands:
+                S, order = Nt * int(rng.integers(1, max(1, Mt // P) + 1)), None
             T = op.num_waves(tiles, S)
             part = [1] * (P - 1) + [T - (P - 1)]
-            order = synthetic.random_order(tiles, int(rng.integers(1 << 30))) if rng.random() < 0.5 else None
             rd = synthetic.random_row_dst(Mt * 128, world, int(rng.integers(1 << 30)))
             specs.append(dict(coll="alltoall", m=Mt * 128, n=N, k=64, tile_m=128, tile_n=BN, workers=S,
-                              tile_order=order, swizzle=1, group_waves=part, row_dst=rd))
+                              tile_order=order, swizzle=1, group_waves=part, row_dst=rd, ar_layout=layout))
             oplans.append(op.make_plan(Mt * 128, N, 128, BN, S, part, order=order, swizzle=1))
             row_dsts.append(rd)
-        sends = [orr.a2a_pre(np.arange(oplans[s].M * N, dtype=float).reshape(-1, N), oplans[s], row_dsts[s], world)
-                 for s in range(world)]
+        lay = "rowband" if layout == "auto" and orr.a2a_rowband_ok(oplans) else "slot"
+        assert lay == "rowband" or not bands
+        sends = [orr.a2a_pre(np.arange(oplans[s].M * N, dtype=float).reshape(-1, N), oplans[s], row_dsts[s], world,
+                             lay) for s in range(world)]
         recv = oc.alltoall_groups(sends, P)
         for me in range(world):
             pl = fo.Plan(rank=me, world=world, peers=specs, **specs[me])
+            assert pl.info["ar_layout"] == (1 if lay == "rowband" else 0)
             # send map: pools concatenated by destination
             flat = np.concatenate([sends[me].pools[d].reshape(-1) for d in range(world)])
             assert np.array_equal(pl.export_send_map(), _oracle_send_map(flat))
@@ -163,6 +170,12 @@ def test_alltoall_maps_and_census(world):
                     assert sc[j, d] == b - a
                     a, b = sends[d].ranges[me][j]
                     assert rc[j, d] == b - a
+            if lay == "rowband":
+                # received straight into the output rows: the receive map is the identity
+                rows = sum(int((np.asarray(row_dsts[s]) == me).sum()) for s in range(world))
+                assert pl.info["out_rows"] == rows
+                assert np.array_equal(pl.export_recv_map(), np.arange(rows * N))
+                continue
             # recv map: receive layout [group][source]
             parts, idx = [], 0
             for s, chunk in recv[me]:
