@@ -216,7 +216,8 @@ def test_c3_tp8_reducescatter():
 
 
 @pytest.mark.parametrize("routing", ["balanced", "router"])
-def test_c4_ep8_alltoall(routing):
+@pytest.mark.parametrize("layout", ["slot", "auto"])
+def test_c4_ep8_alltoall(routing, layout):
     """configs[3]: Mixtral-8x7B w2 (hidden 4096, ffn 14336), 8 experts one per
     rank, 4096 tokens top-2 -> ~1024 rows per expert, A2A back to the token
     owners (PAPER.md:264)."""
@@ -234,7 +235,7 @@ def test_c4_ep8_alltoall(routing):
         Se = min(S, tiles)
         T = -(-tiles // Se)
         specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BNe, workers=Se,
-                          group_waves=[1, T - 1] if T > 1 else [1], row_dst=rds[e]))
+                          group_waves=[1, T - 1] if T > 1 else [1], row_dst=rds[e], ar_layout=layout))
     if any(len(s["group_waves"]) != P for s in specs):
         pytest.skip("an expert got a single wave")
     plans = [fo.Plan(rank=e, world=n, peers=specs, **specs[e]) for e in range(n)]
@@ -247,18 +248,27 @@ def test_c4_ep8_alltoall(routing):
         sends.append(send)
         As.append(A)
         Bts.append(Bt)
-    counts = [p.export_a2a_counts() for p in plans]  # (send[P, n], recv[P, n]) per rank
+    # the exchange emulated from the plans' own communication schedules
+    # (fo_plan_export_calls): every receive on rank d is paired, in order, with
+    # the matching send of its source (NCCL's send/recv pairing); the self part
+    # is the local copy.  Layout-agnostic: the paper's [group][source] receive
+    # buffer, or R41's output rows (every source's groups are bands here when
+    # the routing pads the experts to whole waves of tile-rows)
+    calls = [p.export_calls(0) for p in plans]
+    sends_to = [{d: [c for c in calls[s_] if c["kind"] == "send" and c["peer"] == d] for d in range(n)}
+                for s_ in range(n)]
     for d in (0, n - 1):
-        parts = []
-        for j in range(P):
-            for s in range(n):
-                sc = counts[s][0]
-                pool_base = int(sc.sum(axis=0)[:d].sum())
-                start = int(sc[:j, d].sum())
-                cnt = int(sc[j, d])
-                parts.append(sends[s][(pool_base + start) * BNe:(pool_base + start + cnt) * BNe])
-        recv = torch.cat(parts)
-        assert recv.numel() == plans[d].info["recv_elems"]
+        recv = torch.full((plans[d].info["recv_elems"],), float("nan"), dtype=torch.bfloat16, device="cuda")
+        cursor = [0] * n
+        for c in calls[d]:
+            if c["kind"] == "recv":
+                m = sends_to[c["peer"]][d][cursor[c["peer"]]]
+                cursor[c["peer"]] += 1
+                assert m["count"] == c["count"] and m["group"] == c["group"]
+                recv[c["dst_off"]:c["dst_off"] + c["count"]] = sends[c["peer"]][m["src_off"]:m["src_off"] + m["count"]]
+            elif c["kind"] == "local_copy":
+                recv[c["dst_off"]:c["dst_off"] + c["count"]] = sends[d][c["src_off"]:c["src_off"] + c["count"]]
+        assert all(cursor[s_] == len(sends_to[s_][d]) for s_ in range(n))
         out = torch.empty(plans[d].info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
         fo.post_stage(plans[d], recv, out)
         torch.cuda.synchronize()
@@ -266,6 +276,7 @@ def test_c4_ep8_alltoall(routing):
         want = np.concatenate([_gemm_full(As[s][torch.from_numpy(np.flatnonzero(rds[s] == d)).cuda()], Bts[s])
                                for s in range(n)], axis=0)
         _check_rows(out, want)
+    print(f"C4 EP=8 A2A ({routing}): layout {'rowband' if plans[0].info['ar_layout'] == 1 else 'slot'}")
 
 
 def test_c2_bench_config_tp1_tail_split():
