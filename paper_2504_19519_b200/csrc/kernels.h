@@ -109,6 +109,8 @@ struct PostArgs {
   float eps;
   int smem_pad;                // dynamic smem (bytes, unused) requested per block: > the SM's
                                // smem left beside a live GEMM CTA keeps the kernel off the GEMM's SMs
+  int bulk_ok;                 // add + RMSNorm may stage rows in smem by bulk copies (launches that do
+                               // not run beside the persistent GEMM)
 };
 
 // Post-reorder of ONE wave group's data right after its collective (DESIGN.md

@@ -270,6 +270,154 @@ __global__ void __launch_bounds__(THREADS) fo_post_rmsnorm_kernel(const PostArgs
   }
 }
 
+// Residual add + RMSNorm with the rows staged in shared memory by bulk copies
+// (cp.async.bulk, the TMA's linear mode): for launches that do not share the
+// GPU with the persistent GEMM (the final / sequential / stage post pass; its
+// shared memory keeps it off SMs a GEMM CTA holds).  Warp 0 keeps `stages`
+// rows per block in flight (x through the map — one copy per BN-wide run, or
+// the whole row for identity maps — and the residual row), so the bytes in
+// flight per SM are set by shared memory, not by registers: the register
+// kernel above holds ~2 rows per block and reaches 0.63-0.72 of the HBM copy
+// bandwidth on 4096-8192-column rows (profiles/r02_post_probe.txt).  Each
+// thread reads its CPT 16-byte chunks of a row from shared memory once, the
+// block reduces the sum of squares, and warp 0 refills the slot for the
+// block's row `stages` ahead before the normalised row is written.
+namespace bulkcp {
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+}  // namespace bulkcp
+
+constexpr int BULK_THREADS = 256;
+
+template <int MAP, int CPT, bool RES>
+__global__ void __launch_bounds__(BULK_THREADS) fo_post_rmsnorm_bulk_kernel(const PostArgs p, int lbn, int stages) {
+  extern __shared__ __align__(128) uint8_t bsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int WARPS = BULK_THREADS / 32;
+  const int64_t N = p.N;
+  const int chunks = (int)(N >> 3);
+  const uint32_t row_bytes = (uint32_t)(N * 2);
+  uint8_t* slots = bsm;  // [stages][x row | residual row]
+  uint64_t* full = reinterpret_cast<uint64_t*>(bsm + (size_t)stages * 2 * row_bytes);
+  float* red = reinterpret_cast<float*>(full + stages);  // [2][WARPS], alternating rows
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
+  const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(p.residual);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  const __nv_bfloat16* gam = reinterpret_cast<const __nv_bfloat16*>(p.gamma);
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) bulkcp::mbar_init(&full[s], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  const int Nt = (int)(N >> lbn);
+  const uint32_t run_bytes = (uint32_t)(p.BN * 2);
+  // warp 0: stage row r into slot s (x through the map, the residual row)
+  auto issue = [&](int64_t r, int s) {
+    uint8_t* xs = slots + (size_t)s * 2 * row_bytes;
+    const RowSrc rs = row_src<MAP>(p, r);
+    if (lane == 0) bulkcp::mbar_expect_tx(&full[s], 2 * row_bytes);
+    __syncwarp();
+    if (MAP == POSTMAP_IDENTITY || MAP == POSTMAP_ROWX) {
+      if (lane == 0) bulkcp::g2s(xs, src + rs.roff, row_bytes, &full[s]);
+    } else {
+      for (int jc = lane; jc < Nt; jc += 32)
+        bulkcp::g2s(xs + (size_t)jc * run_bytes, src + (int64_t)__ldg(rs.tbl + jc) * rs.tscale + rs.roff, run_bytes,
+                    &full[s]);
+    }
+    if (lane == 1) bulkcp::g2s(xs + row_bytes, res + r * N, row_bytes, &full[s]);
+  };
+  const int64_t step = gridDim.x;
+  if (warp == 0)
+    for (int s = 0; s < stages; ++s) {
+      const int64_t r = blockIdx.x + s * step;
+      if (r < p.rows) issue(r, s);
+    }
+  uint4 gv[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = tid + BULK_THREADS * i;
+    if (c < chunks) gv[i] = *reinterpret_cast<const uint4*>(gam + 8 * (int64_t)c);
+  }
+  int s = 0, it = 0;
+  uint32_t phase = 0;
+  for (int64_t r = blockIdx.x; r < p.rows; r += step, ++it) {
+    bulkcp::mbar_wait(&full[s], phase);
+    const uint4* xs = reinterpret_cast<const uint4*>(slots + (size_t)s * 2 * row_bytes);
+    const uint4* rsd = reinterpret_cast<const uint4*>(slots + (size_t)s * 2 * row_bytes + row_bytes);
+    float y[CPT][8];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int c = tid + BULK_THREADS * i;
+      if (c < chunks) {
+        float q[8];
+        unpack8(xs[c], y[i]);
+        unpack8(rsd[c], q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          y[i][k] += q[k];
+          ss += y[i][k] * y[i][k];
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    float* rb = red + (it & 1) * WARPS;
+    if (lane == 0) rb[warp] = ss;
+    __syncthreads();  // every thread's smem reads of slot s are done, the partial sums are in
+    if (warp == 0) {
+      const int64_t rn = r + (int64_t)stages * step;
+      if (rn < p.rows) issue(rn, s);
+    }
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) tot += rb[w];
+    const float rstd = rsqrtf(tot / (float)N + p.eps);
+    __nv_bfloat16* orow = out + r * N;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int c = tid + BULK_THREADS * i;
+      if (c < chunks) {
+        if (RES) st_stream(const_cast<__nv_bfloat16*>(res) + r * N + 8 * c, pack8(y[i]));
+        float g[8], o[8];
+        unpack8(gv[i], g);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = y[i][k] * rstd * g[k];
+        st_stream(orow + 8 * c, pack8(o));
+      }
+    }
+    if (++s == stages) {
+      s = 0;
+      phase ^= 1;
+    }
+  }
+}
+
 // Fallback for very wide rows (N > 16384): warp per row, two passes (the
 // second read hits L2).
 template <int MAP, bool RES>
@@ -417,17 +565,63 @@ int resident_grid(int smem) {
   return v * num_sms();
 }
 
+// The bulk-staged kernel: stages per block from a ~100 KB budget (two blocks
+// per SM at 8192 columns), grid = the resident blocks; returns false when it
+// does not apply (rows wider than 16384 columns, unaligned buffers).
+template <int MAP, bool RES, int CPT>
+bool launch_rmsnorm_bulk_cpt(const PostArgs& a, int lbn, cudaStream_t stream) {
+  const size_t slot = 4 * (size_t)a.N;
+  const int stages = (int)std::max<size_t>(2, std::min<size_t>(4, (100u << 10) / slot));
+  const int smem = (int)(stages * slot + stages * 8 + 2 * 8 * sizeof(float));
+  auto kern = fo_post_rmsnorm_bulk_kernel<MAP, CPT, RES>;
+  static int attr_dev_mask = 0;  // per device bit: the dynamic-smem attribute is set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_dev_mask & (1 << (dev & 31)))) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    attr_dev_mask |= 1 << (dev & 31);
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BULK_THREADS, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  const int grid = (int)std::min<int64_t>(a.rows, (int64_t)per_sm * num_sms());
+  kern<<<grid, BULK_THREADS, smem, stream>>>(a, lbn, stages);
+  return true;
+}
+
+template <int MAP, bool RES>
+bool launch_rmsnorm_bulk(const PostArgs& a, int lbn, cudaStream_t stream) {
+  const int64_t chunks = a.N / 8;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (!a.bulk_ok || !al16(a.src) || !al16(a.residual) || !al16(a.gamma) || a.BN < 8) return false;
+  if (chunks <= BULK_THREADS) return launch_rmsnorm_bulk_cpt<MAP, RES, 1>(a, lbn, stream);
+  if (chunks <= 2 * BULK_THREADS) return launch_rmsnorm_bulk_cpt<MAP, RES, 2>(a, lbn, stream);
+  if (chunks <= 4 * BULK_THREADS) return launch_rmsnorm_bulk_cpt<MAP, RES, 4>(a, lbn, stream);
+  if (chunks <= 8 * BULK_THREADS) return launch_rmsnorm_bulk_cpt<MAP, RES, 8>(a, lbn, stream);
+  return false;
+}
+
+// Both kernels give each thread the chunks c = tid + 256 i (the register
+// kernel's 128-thread configuration only below 129 chunks, where the extra
+// warps of the bulk kernel hold none) and sum in the same order, so a per-band
+// pass beside the GEMM and a whole-output pass after it agree bit for bit.
 template <int MAP, bool RES>
 cudaError_t launch_rmsnorm(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int64_t chunks = a.N / 8;
+  if (launch_rmsnorm_bulk<MAP, RES>(a, lbn, stream)) return cudaGetLastError();
   const int grid = (int)std::min<int64_t>(a.rows, (int64_t)num_sms() * 16);
   auto pgrid = [&](int resident) { return (int)std::min<int64_t>(a.rows, resident); };
   if (chunks <= 128)
     fo_post_rmsnorm_kernel<MAP, 1, 128, RES>
         <<<pgrid(resident_grid<MAP, 1, 128, RES>(a.smem_pad)), 128, a.smem_pad, stream>>>(a, lbn);
-  else if (chunks <= 256)
-    fo_post_rmsnorm_kernel<MAP, 2, 128, RES>
-        <<<pgrid(resident_grid<MAP, 2, 128, RES>(a.smem_pad)), 128, a.smem_pad, stream>>>(a, lbn);
+  else if (chunks <= 256)  // 256 threads x 1 chunk: the bulk kernel's chunk -> thread map (same fp32 sum order)
+    fo_post_rmsnorm_kernel<MAP, 1, 256, RES>
+        <<<pgrid(resident_grid<MAP, 1, 256, RES>(a.smem_pad)), 256, a.smem_pad, stream>>>(a, lbn);
   else if (chunks <= 512)
     fo_post_rmsnorm_kernel<MAP, 2, 256, RES>
         <<<pgrid(resident_grid<MAP, 2, 256, RES>(a.smem_pad)), 256, a.smem_pad, stream>>>(a, lbn);

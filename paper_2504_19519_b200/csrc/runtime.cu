@@ -482,6 +482,7 @@ static void run_post(fo_plan_s* p, int map, const void* src, void* out, const vo
   a.pos_of_tile = p->d_pos_of_tile;
   a.src_row = p->d_src_row;
   a.eps = h.eps;
+  a.bulk_ok = 1;  // the whole-output pass runs after the GEMM
   FO_CUDA(launch_post(a, s));
 }
 
@@ -540,8 +541,10 @@ static bool use_group_post(const fo_plan_s* p) {
   return map != POSTMAP_IDENTITY && (h.post == FO_POST_NONE || h.post == FO_POST_ADD);
 }
 
+// `after_gemm`: the pass is ordered after the GEMM kernel (the last group on
+// the caller stream), so it may use the bulk-staged RMSNorm.
 static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, const void* residual,
-                           const void* gamma, cudaStream_t s) {
+                           const void* gamma, cudaStream_t s, bool after_gemm = false) {
   const PlanHost& h = p->host;
   if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
   if (band_post(h)) {
@@ -565,6 +568,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
     a.h = h.h;
     a.eps = h.eps;
     a.smem_pad = p->post_sm_partition ? kPartitionSmem : 0;
+    a.bulk_ok = after_gemm ? 1 : 0;
     FO_CUDA(launch_post(a, s));
     return;
   }
@@ -944,7 +948,7 @@ fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, 
             FO_CUDA(cudaStreamWaitEvent(c->post_stream, c->ev_group[j], 0));
             ps = c->post_stream;
           }
-          run_group_post(p, j, post_src, out, residual, gamma, ps);
+          run_group_post(p, j, post_src, out, residual, gamma, ps, on_s);
         }
         if (p->trace_group_ts) FO_CUDA(launch_timestamp(p->trace_group_ts + 2 * j + 1, ps));
         if (p->d2h_host) group_d2h(c, p, j, out, ps);
@@ -1166,6 +1170,7 @@ static void run_rowexchange(fo_plan_s* p, const void* gathered, void* out, const
   a.Nt = h.Nt;
   a.h = h.h;
   a.eps = h.eps;
+  a.bulk_ok = 1;
   if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
   if (is_rmsnorm(h.post) && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
   FO_CUDA(launch_post(a, s));
@@ -1210,6 +1215,7 @@ fo_status fo_run_allgather(fo_ctx c, fo_plan p, const void* local, void* out, co
         a.Nt = h.Nt;
         a.h = h.h;
         a.eps = h.eps;
+        a.bulk_ok = 1;
         if (!residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
         FO_CUDA(launch_post(a, s));
       }
