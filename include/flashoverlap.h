@@ -539,13 +539,21 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      counters the signalling warp waits for the stores'
  *                      completion (cp.async.bulk.wait_group 0 + async-proxy
  *                      fence) before its release add; 0 — 16-byte st.global from
- *                      the staging buffer (always used for RS / A2A layouts and
- *                      split-tail tiles) */
+ *                      the staging buffer (always used for the RS slot and A2A
+ *                      layouts, RS bands with h < 32 and split-tail tiles; RS
+ *                      ROWBAND with h >= 32 uses TMA stores too)
+ *  FO_OPT_POST_BULK    1 (default) — an add + RMSNorm pass ordered after the GEMM
+ *                      (the whole-output pass, fo_run_sequential's, the stage
+ *                      entry points', the last band's) stages its rows in shared
+ *                      memory by bulk copies, 2-4 rows per block in flight; 0 —
+ *                      the register kernel (always used beside the GEMM); both
+ *                      give the same bits */
 typedef enum { FO_OPT_GROUP_POST = 0, FO_OPT_WAIT_KERNEL = 1, FO_OPT_TAIL_SPLIT = 2,
                FO_OPT_POST_SM_PARTITION = 3, FO_OPT_HOST_PIPELINE = 4, FO_OPT_HOST_CHUNKS = 5,
                FO_OPT_LAST_GROUP_IN_ORDER = 6, FO_OPT_WAVE_SYNC = 7, FO_OPT_MULTICAST = 8,
                FO_OPT_DEBUG_STALL_GROUP = 10, FO_OPT_GEMM_SWIGLU = 11,
-               FO_OPT_DIST_FOLD = 12, FO_OPT_K_SNAKE = 13, FO_OPT_TMA_STORE = 14 } fo_option;
+               FO_OPT_DIST_FOLD = 12, FO_OPT_K_SNAKE = 13, FO_OPT_TMA_STORE = 14,
+               FO_OPT_POST_BULK = 15 } fo_option;
 fo_status fo_plan_set_option(fo_plan plan, int32_t option, int64_t value);
 /* Fill the library-owned send/receive buffers of the plan with a bf16 bit
  * pattern on `stream` (poison for the memory-ordering stress test). */

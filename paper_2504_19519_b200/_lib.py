@@ -21,7 +21,8 @@ LAYOUT = {"slot": 0, "rowband": 1, "auto": 2}
 POST = {"none": 0, "add": 1, "add_rmsnorm": 2, "add_rmsnorm_res": 3}
 OPTION = {"group_post": 0, "wait_kernel": 1, "tail_split": 2, "post_sm_partition": 3, "host_pipeline": 4, "host_chunks": 5,
           "last_group_in_order": 6, "wave_sync": 7, "multicast": 8, "debug_stall_group": 10, "gemm_swiglu": 11,
-          "dist_fold": 12, "k_snake": 13, "tma_store": 14}
+          "dist_fold": 12, "k_snake": 13, "tma_store": 14,
+          "post_bulk": 15}
 
 
 class FOError(RuntimeError):

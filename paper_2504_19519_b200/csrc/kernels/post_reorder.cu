@@ -599,6 +599,11 @@ bool launch_rmsnorm_bulk(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int64_t chunks = a.N / 8;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   if (!a.bulk_ok || !al16(a.src) || !al16(a.residual) || !al16(a.gamma) || a.BN < 8) return false;
+  // measured (profiles/r02_post_probe.txt): ahead only where many rows per
+  // block keep the ring full — 8192^2: 1.00 vs 0.97 of the copy bandwidth on
+  // whole rows, 0.79 vs 0.72 through the slot map; at 4096^2 and below the
+  // prologue dominates and the register kernel is 5-15% faster
+  if (a.rows * a.N * 2 < (int64_t(64) << 20)) return false;
   if (chunks <= BULK_THREADS) return launch_rmsnorm_bulk_cpt<MAP, RES, 1>(a, lbn, stream);
   if (chunks <= 2 * BULK_THREADS) return launch_rmsnorm_bulk_cpt<MAP, RES, 2>(a, lbn, stream);
   if (chunks <= 4 * BULK_THREADS) return launch_rmsnorm_bulk_cpt<MAP, RES, 4>(a, lbn, stream);

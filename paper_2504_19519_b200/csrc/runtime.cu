@@ -482,7 +482,7 @@ static void run_post(fo_plan_s* p, int map, const void* src, void* out, const vo
   a.pos_of_tile = p->d_pos_of_tile;
   a.src_row = p->d_src_row;
   a.eps = h.eps;
-  a.bulk_ok = 1;  // the whole-output pass runs after the GEMM
+  a.bulk_ok = p->post_bulk;  // the whole-output pass runs after the GEMM
   FO_CUDA(launch_post(a, s));
 }
 
@@ -568,7 +568,7 @@ static void run_group_post(fo_plan_s* p, int j, const void* src, void* out, cons
     a.h = h.h;
     a.eps = h.eps;
     a.smem_pad = p->post_sm_partition ? kPartitionSmem : 0;
-    a.bulk_ok = after_gemm ? 1 : 0;
+    a.bulk_ok = after_gemm ? p->post_bulk : 0;
     FO_CUDA(launch_post(a, s));
     return;
   }
@@ -1170,7 +1170,7 @@ static void run_rowexchange(fo_plan_s* p, const void* gathered, void* out, const
   a.Nt = h.Nt;
   a.h = h.h;
   a.eps = h.eps;
-  a.bulk_ok = 1;
+  a.bulk_ok = p->post_bulk;
   if (h.post != FO_POST_NONE && !residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
   if (is_rmsnorm(h.post) && !gamma) fail(FO_ERR_INVALID_ARG, "RMSNorm needs gamma");
   FO_CUDA(launch_post(a, s));
@@ -1215,7 +1215,7 @@ fo_status fo_run_allgather(fo_ctx c, fo_plan p, const void* local, void* out, co
         a.Nt = h.Nt;
         a.h = h.h;
         a.eps = h.eps;
-        a.bulk_ok = 1;
+        a.bulk_ok = p->post_bulk;
         if (!residual) fail(FO_ERR_INVALID_ARG, "post op needs a residual");
         FO_CUDA(launch_post(a, s));
       }
@@ -1603,6 +1603,10 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
       case FO_OPT_TMA_STORE:
         if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "tma_store must be 0 or 1");
         p->tma_store = (int)value;
+        break;
+      case FO_OPT_POST_BULK:
+        if (value < 0 || value > 1) fail(FO_ERR_INVALID_ARG, "post_bulk must be 0 or 1");
+        p->post_bulk = (int)value;
         break;
       case FO_OPT_K_SNAKE:
         if (value < -1 || value > 1) fail(FO_ERR_INVALID_ARG, "k_snake must be -1, 0 or 1");

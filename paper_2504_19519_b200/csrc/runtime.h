@@ -78,6 +78,7 @@ struct fo_plan_s {
   int multicast = 0;                              // FO_OPT_MULTICAST (measured slower: off)
   int k_snake = -1;                               // FO_OPT_K_SNAKE (-1 auto: K >= 64 k-blocks)
   int tma_store = 1;                              // FO_OPT_TMA_STORE
+  int post_bulk = 1;                              // FO_OPT_POST_BULK
   int debug_stall_group = -1;                     // FO_OPT_DEBUG_STALL_GROUP (watchdog test)
   int swiglu = 0;                                 // FO_OPT_GEMM_SWIGLU (no-comm GEMM epilogue)
   uint32_t* d_wave = nullptr;                     // [T] monotone per-wave issue counters

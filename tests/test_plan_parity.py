@@ -215,7 +215,8 @@ def test_option_contract():
     for name, good, bad in (("last_group_in_order", (0, 1), (2, -1)), ("wave_sync", (0, 1), (2,)),
                             ("multicast", (0, 1), (2,)), ("wait_kernel", (0, 1), (2,)),
                             ("group_post", (-1, 0, 1), (2,)), ("host_pipeline", (0, 3, 7), (8,)),
-                            ("dist_fold", (0, 1), (2, -1))):
+                            ("dist_fold", (0, 1), (2, -1)), ("tma_store", (0, 1), (2,)),
+                            ("post_bulk", (0, 1), (2, -1))):
         for v in good:
             pl.set_option(name, v)
         for v in bad:

@@ -67,6 +67,14 @@ def main():
         ("A2A slot n=8 1024x4096 256x256", None, 8, 0),
         ("AR slot 8192x8192 256x256 S64", dict(coll="allreduce", m=8192, n=8192, k=64, tile_m=256, tile_n=256,
                                                 workers=64, swizzle=2, group_waves=[4, 4, 8], ar_layout="slot"), 1, 0),
+        # ROWBAND plans (H11a, R40): the post pass is only the fused op, on rows in place
+        ("AR rowband 4096x4096 S64", dict(coll="allreduce", m=4096, n=4096, k=64, tile_m=256, tile_n=256,
+                                          workers=64, swizzle=1, group_waves=[1, 2, 1], ar_layout="rowband"), 1, 0),
+        ("RS rowband n=8 8192x8192 S64", dict(coll="reducescatter", m=8192, n=8192, k=64, tile_m=256, tile_n=256,
+                                              workers=64, swizzle=1, group_waves=[2, 4, 6, 4], ar_layout="rowband"),
+         8, 0),
+        ("AR rowband 8192x8192 S64", dict(coll="allreduce", m=8192, n=8192, k=64, tile_m=256, tile_n=256,
+                                          workers=64, swizzle=1, group_waves=[4, 4, 8], ar_layout="rowband"), 1, 0),
     ]
     print(f"# HBM peak {peak:.0f} GB/s (MEASURED_PEAKS.json); GB/s = algorithmic bytes (read + write) / median time",
           flush=True)
@@ -84,8 +92,8 @@ def main():
                 plan_args = [(dict(specs[rank], post=op), dict(rank=rank, world=world, peers=specs))
                              for op in ("none", "add", "add_rmsnorm")]
             else:
-                plan_args = [(dict(spec, post=op), dict(rank=rank, world=world))
-                             for op in ("none", "add", "add_rmsnorm")]
+                ops = ("add_rmsnorm",) if spec["ar_layout"] == "rowband" else ("none", "add", "add_rmsnorm")
+                plan_args = [(dict(spec, post=op), dict(rank=rank, world=world)) for op in ops]
             for sp, kw in plan_args:
                 plan = fo.Plan(**kw, **sp)
                 rows, N = plan.info["out_rows"], plan.info["out_cols"]
@@ -93,18 +101,28 @@ def main():
                 out = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
                 res = torch.randn(rows, N, device="cuda").to(torch.bfloat16)
                 gam = torch.randn(N, device="cuda").to(torch.bfloat16)
-                t = timeit(lambda: fo.post_stage(plan, recv, out, res, gam), flush_fn, args.iters)
                 nb = 2 * rows * N * 2 + (rows * N * 2 if sp["post"] != "none" else 0)
                 src = recv[:rows * N].view(rows, N)
-                if sp["post"] == "none":
-                    tr = timeit(lambda: out.copy_(src), flush_fn, args.iters)
-                    ref = "torch copy_"
-                else:
-                    tr = timeit(lambda: torch.add(src, res, out=out), flush_fn, args.iters)
-                    ref = "torch add"
-                print(f"{name:34s} post={sp['post']:12s} {t:8.2f} us {nb / t / 1e3:7.0f} GB/s ({nb / t / 1e3 / peak:.2f} "
-                      f"of peak) | {ref:11s} {tr:8.2f} us {nb / tr / 1e3:7.0f} GB/s ({nb / tr / 1e3 / peak:.2f})  "
-                      f"[{nb / 1e6:.1f} MB]", flush=True)
+                variants = [("", 1)] if sp["post"] != "add_rmsnorm" else [(" bulk", 1), (" regs", 0)]
+                for tag, bulk in variants:
+                    plan.set_option("post_bulk", bulk)
+                    t = timeit(lambda: fo.post_stage(plan, recv, out, res, gam), flush_fn, args.iters)
+                    if sp["post"] == "none":
+                        tr = timeit(lambda: out.copy_(src), flush_fn, args.iters)
+                        ref = "torch copy_"
+                    else:
+                        tr = timeit(lambda: torch.add(src, res, out=out), flush_fn, args.iters)
+                        ref = "torch add"
+                    print(f"{name:34s} post={sp['post'] + tag:17s} {t:8.2f} us {nb / t / 1e3:7.0f} GB/s "
+                          f"({nb / t / 1e3 / peak:.2f} of peak) | {ref:11s} {tr:8.2f} us {nb / tr / 1e3:7.0f} GB/s "
+                          f"({nb / tr / 1e3 / peak:.2f})  [{nb / 1e6:.1f} MB]", flush=True)
+                if sp["post"] == "add_rmsnorm":
+                    # the unfused library form: torch add, then torch's rms_norm (two HBM passes)
+                    def unfused():
+                        y = torch.add(src, res)
+                        torch.nn.functional.rms_norm(y, (N,), gam, 1e-5)
+                    tu = timeit(unfused, flush_fn, args.iters)
+                    print(f"{'':34s} {'torch add + F.rms_norm (unfused)':34s} {tu:8.2f} us", flush=True)
 
 
 if __name__ == "__main__":
