@@ -515,6 +515,41 @@ def main():
                             "reorder_epilogue_us": round(mm["epi"], 2),
                             "epilogue_overhead_pct": round(100.0 * (mm["epi"] / mm["gemm"] - 1.0), 2),
                             "cublas_us": round(mm["cublas"], 2)}
+            # this rank's side of the layer in the paper's layout (SLOT: the
+            # epilogue reorder + the post-communication pass over the output)
+            # and in ROWBAND (H11a / R40 / R41: the collective lands
+            # the rows in the output, no post pass); the collective moves the
+            # same bytes in both (n=8 ranks' plans for RS / A2A, rank 0's side)
+            nr_ = 8 if coll != "allreduce" else 1
+            lay_t = {}
+            try:
+                fns_ = {}
+                for lay in ("slot", "rowband"):
+                    Ntl = Ns // BN
+                    gw = [1] * Tw if Sw % Ntl == 0 else [Tw]
+                    kl = dict(coll=coll, m=Ms, n=Ns, k=Ks, tile_m=BM, tile_n=BN, workers=Sw, swizzle=0,
+                              group_waves=gw, ar_layout=lay)
+                    if coll == "alltoall":
+                        rds_ = [synthetic.balanced_moe_row_dst(Ms // nr_, nr_)] * nr_
+                        lp = fo.Plan(rank=0, world=nr_, peers=[dict(kl, row_dst=r_) for r_ in rds_],
+                                     options={"tail_split": ts_} if ts_ else None, row_dst=rds_[0], **kl)
+                    else:
+                        lp = fo.Plan(rank=0, world=nr_ if coll == "reducescatter" else 1,
+                                     options={"tail_split": ts_} if ts_ else None, **kl)
+                    snd = torch.empty(max(1, lp.info["send_elems"]), dtype=torch.bfloat16, device="cuda")
+                    rcv = torch.zeros(max(1, lp.info["recv_elems"]), dtype=torch.bfloat16, device="cuda")
+                    o_ = torch.empty(lp.info["out_rows"], Ns, dtype=torch.bfloat16, device="cuda")
+                    fns_[lay + "_epi"] = (lambda lp=lp, snd=snd: fo.gemm_stage(lp, As_, Bs_, snd))
+                    if lay == "slot":
+                        fns_["slot_post"] = (lambda lp=lp, rcv=rcv, o_=o_: fo.post_stage(lp, rcv, o_))
+                mt = timed_multi(fns_, 10, 2)
+                for lay in ("slot", "rowband"):
+                    post_ = mt.get(lay + "_post", 0.0)
+                    lay_t[lay] = {"epilogue_us": round(mt[lay + "_epi"], 2), "post_us": round(post_, 2),
+                                  "rank_work_us": round(mt[lay + "_epi"] + post_, 2)}
+            except Exception as ex:  # pragma: no cover - evidence only
+                lay_t = {"error": str(ex)[:200]}
+            shards[name]["layouts"] = lay_t
             del As_, Bs_, Cs_
 
     # ---- e2e through the public API with host (pinned) buffers

@@ -87,3 +87,56 @@ def test_group_post_inside_fo_run():
             torch.cuda.synchronize()
             assert torch.equal(out, want), coll
     ctx.close()
+
+
+@pytest.mark.parametrize("kind", ["ar_slot", "ar_rowband", "rs_slot", "a2a_slot", "rowx"])
+@pytest.mark.parametrize("post", ["add_rmsnorm", "add_rmsnorm_res"])
+def test_bulk_rmsnorm_equals_register_kernel(kind, post):
+    """The bulk-staged add + RMSNorm (rows in shared memory by cp.async.bulk,
+    outputs >= 64 MB) gives the register kernel's bits through every map (same
+    chunk -> thread map and fp32 sum order), and matches the oracle's
+    add + RMSNorm within the north_star tolerance."""
+    from oracle import numerics as onum
+    from oracle import post as opost
+    M, N = 8192, 4096
+    base = dict(m=M, n=N, k=64, tile_m=256, tile_n=256, workers=64, post=post)
+    if kind == "ar_slot":
+        plan = fo.Plan(coll="allreduce", swizzle=2, group_waves=[2, 2, 4], ar_layout="slot", **base)
+    elif kind == "ar_rowband":
+        plan = fo.Plan(coll="allreduce", swizzle=1, group_waves=[2, 2, 4], ar_layout="rowband", **base)
+    elif kind in ("rs_slot", "rowx"):
+        base["m"] = 2 * M                     # 2 ranks: 8192 output rows each
+        plan = fo.Plan(coll="reducescatter", swizzle=2, group_waves=[4, 12], ar_layout="slot", rank=1, world=2, **base)
+    else:
+        spec = dict(coll="alltoall", swizzle=2, group_waves=[2, 6], row_dst=np.zeros(M, np.int32), ar_layout="slot",
+                    **base)
+        plan = fo.Plan(rank=0, world=1, peers=[spec], **spec)
+    rows = plan.info["out_rows"] if kind != "rowx" else base["m"]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n_in = plan.info["recv_elems"] if kind != "rowx" else rows * N
+    recv = torch.randn(n_in, generator=g, device="cuda").to(torch.bfloat16)
+    res0 = torch.randn(rows, N, generator=g, device="cuda").to(torch.bfloat16)
+    gam = torch.randn(N, generator=g, device="cuda").to(torch.bfloat16)
+    outs, ress = [], []
+    for bulk in (1, 0):
+        plan.set_option("post_bulk", bulk)
+        out = torch.full((rows, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+        res = res0.clone()
+        if kind == "rowx":
+            fo.rowexchange_stage(plan, recv, out, res, gam)
+        else:
+            fo.post_stage(plan, recv, out, res, gam)
+        torch.cuda.synchronize()
+        outs.append(out)
+        ress.append(res)
+    assert rows * N * 2 >= 64 << 20                   # the bulk kernel's size class
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(ress[0], ress[1])
+    # against the oracle: x = the reordered received data, read back from the
+    # no-op pass (post none on the same map)
+    if kind == "ar_rowband":
+        x = recv.view(rows, N).double().cpu().numpy()
+        want = opost.add_rmsnorm(x, onum.to_f64(res0.cpu()), onum.to_f64(gam.cpu()), 1e-5)
+        got = outs[0].double().cpu().numpy()
+        rms = np.sqrt(np.mean(want * want))
+        assert float(np.max(np.abs(got - want) / np.maximum(np.abs(want), rms))) <= 1e-2
