@@ -704,9 +704,12 @@ def test_moe_combine_stages(n, k, skew):
         assert _combine_close(_host(out), want2), r
 
 
-def test_moe_combine_full_path_world1(ctx1):
+@pytest.mark.parametrize("layout", ["slot", "rowband"])
+def test_moe_combine_full_path_world1(ctx1, layout):
     """fo_run_combine at one rank (one expert, top-1): GEMM + A2A (local) +
-    fused combine through the streams, vs the oracle."""
+    fused combine through the streams, vs the oracle; ROWBAND (R41): the rows
+    land in the library's receive buffer in the output layout and the combine
+    reads them through the identity map."""
     BM, BN, N, K = 256, 256, 1024, 512
     tokens = 1024
     rt = synthetic.moe_topk(tokens, 1, 1, seed=5, pad=BM)
@@ -714,16 +717,20 @@ def test_moe_combine_full_path_world1(ctx1):
     M = A.shape[0]
     tiles = (M // BM) * (N // BN)
     spec = dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=tiles // 4,
-                group_waves=[1, 1, 2], row_dst=rt["row_dst"][0])
+                group_waves=[1, 1, 2], row_dst=rt["row_dst"][0], ar_layout=layout)
+    if layout == "rowband":   # raster, one tile-row per wave
+        spec.update(workers=N // BN, swizzle=1, group_waves=[1, 1, M // BM - 2])
     plan = fo.Plan(peers=[spec], **spec)
+    assert plan.info["ar_layout"] == (1 if layout == "rowband" else 0)
     # permute the slots: token t reads row perm[t] (a gather through the map)
     perm = np.random.default_rng(3).permutation(tokens).astype(np.int32)[:, None]
     w = torch.full((tokens, 1), 0.5, dtype=torch.float32, device="cuda")
     out = torch.empty(tokens, N, dtype=torch.bfloat16, device="cuda")
     fo.run_combine(ctx1, plan, _dev_bf16(A), _dev_bf16(Bt), out, torch.from_numpy(perm).cuda(), w)
     torch.cuda.synchronize()
-    Y = opl.run_alltoall([A], [Bt], [op.make_plan(M, N, BM, BN, tiles // 4, [1, 1, 2])], rt["row_dst"],
-                         model_bf16=True)["out"][0]
+    Y = opl.run_alltoall([A], [Bt], [op.make_plan(M, N, BM, BN, spec["workers"], spec["group_waves"],
+                                                  swizzle=spec.get("swizzle", 1))], rt["row_dst"],
+                         model_bf16=True, layout=layout)["out"][0]
     want = opost.topk_combine(Y, perm, np.full((tokens, 1), 0.5))
     # float regime: the GEMM's own bf16 rounding (fp32 accumulation) may differ
     # from the model's by an ulp -> the north_star tolerance
