@@ -292,6 +292,24 @@ fo_status fo_loopback_create(int32_t device, int32_t world, void** group);
 fo_status fo_loopback_destroy(void* group);
 fo_status fo_ctx_create_loopback(void* group, int32_t rank, fo_ctx* out);
 
+/* EVALUATION BACKEND — an emulated NVLink group on ONE GPU (not a
+ * communicator).  The context acts as rank `rank` of `world`; each of its
+ * collectives is a kernel of `ctas` CTAs (256 threads) on the comm stream that
+ * moves the call's local HBM traffic (reads the send range, writes the receive
+ * range) and lasts at least latency_us + bus_bytes / link_gbps, bus_bytes per
+ * rank in the nccl-tests convention (AllReduce 2(n-1)/n x bytes; ReduceScatter
+ * and AllGather (n-1)/n x the full buffer; a grouped send/recv max(sent,
+ * received) bytes).  Results are NOT the collective's: AllReduce leaves the
+ * rank's own partial, ReduceScatter delivers its own chunk, AllGather
+ * replicates its part, receives are zeroed.  It lets one B200 validate Alg. 1's
+ * predictor and the overlap schedule against collectives
+ * whose duration grows with the group's bytes (tools/predictor_check.py
+ * --emulate).  FO_ERR_INVALID_ARG for world < 1, rank out of range,
+ * link_gbps <= 0, latency_us < 0 or ctas outside 1..1024.  Not for production
+ * use; never a benchmark value. */
+fo_status fo_ctx_create_emulated(int32_t device, int32_t rank, int32_t world, double link_gbps, double latency_us,
+                                 int32_t ctas, fo_ctx* out);
+
 /* Offline stage of the tuner ("the bandwidth curve is sampled
  * with multiple dense points"): average latency of one `coll` (AllReduce in
  * place, ReduceScatter, or equal-split All-to-All) of `bytes` total message

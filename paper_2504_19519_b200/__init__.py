@@ -258,6 +258,20 @@ class Context:
         check(load().fo_ctx_create_loopback(group.handle, int(rank), C.byref(h)))
         return cls(h, group.device, rank, group.world)
 
+    @classmethod
+    def emulated(cls, device: int, rank: int, world: int, link_gbps: float = 770.0, latency_us: float = 6.0,
+                 ctas: int = 16) -> "Context":
+        """EVALUATION backend (fo_ctx_create_emulated): rank `rank` of an
+        emulated `world`-rank NVLink group on one GPU; collectives take
+        latency_us + bus bytes / link_gbps and move their local HBM traffic;
+        their results are not the collective's (timing only)."""
+        h = C.c_void_p()
+        check(load().fo_ctx_create_emulated(int(device), int(rank), int(world), float(link_gbps), float(latency_us),
+                                            int(ctas), C.byref(h)))
+        ctx = cls(h, device, rank, world)
+        ctx.emulated = dict(link_gbps=float(link_gbps), latency_us=float(latency_us), ctas=int(ctas))
+        return ctx
+
     def time_collective_bw(self, coll: str, nbytes: int, iters: int = 5):
         """(average us, bus GB/s) of one collective of `nbytes` (fo_ctx_time_collective)."""
         out, bw = C.c_double(), C.c_double()

@@ -99,6 +99,8 @@ _SIGS = [
     ("fo_loopback_create", C.c_int, [C.c_int32, C.c_int32, C.POINTER(_P)]),
     ("fo_loopback_destroy", C.c_int, [_P]),
     ("fo_ctx_create_loopback", C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    ("fo_ctx_create_emulated", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32,
+                                         C.POINTER(_P)]),
     ("fo_ctx_time_collective", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]),
     ("fo_ctx_create_config", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint8),

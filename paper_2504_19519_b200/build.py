@@ -26,6 +26,7 @@ SOURCES = [
     "tuner.cpp",
     "runtime.cu",
     "loopback.cu",
+    "emulated.cu",
     "kernels/gemm_tcgen05.cu",
     "kernels/post_reorder.cu",
 ]

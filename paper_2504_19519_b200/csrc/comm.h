@@ -13,6 +13,11 @@
 //                   stores.  It lets a single-GPU box run fo_run end to end at
 //                   world 2/4/8 (streams, stream waits, call order, offsets,
 //                   counts, peers) against the oracle.
+//  * EmuComm      — EVALUATION backend (fo_ctx_create_emulated): one rank whose
+//                   collectives take the time NVLink would (bytes / link
+//                   bandwidth + latency) and move their local HBM traffic on
+//                   the SMs the GEMM leaves free; it validates Alg. 1's
+//                   predictor and the overlap schedule on one GPU.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -54,5 +59,11 @@ int loopback_members(LoopbackGroup* g);
 int loopback_world(LoopbackGroup* g);
 int loopback_device(LoopbackGroup* g);
 Comm* make_loopback_comm(LoopbackGroup* g, int rank);
+
+// Emulated-link EVALUATION backend (emulated.cu): rank `rank` of `world` whose
+// collectives are kernels moving the call's local HBM traffic for at least
+// latency_us + bus bytes / link_gbps (timing only; results are not the
+// collective's).
+Comm* make_emulated_comm(int rank, int world, double link_gbps, double latency_us, int ctas);
 
 }  // namespace fo

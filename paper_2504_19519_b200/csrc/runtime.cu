@@ -808,6 +808,30 @@ fo_status fo_ctx_create_loopback(void* group, int32_t rank, fo_ctx* out) {
   });
 }
 
+fo_status fo_ctx_create_emulated(int32_t device, int32_t rank, int32_t world, double link_gbps, double latency_us,
+                                 int32_t ctas, fo_ctx* out) {
+  return guard([&] {
+    if (!out) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(FO_ERR_INVALID_ARG, "rank %d of %d", rank, world);
+    if (!(link_gbps > 0) || latency_us < 0 || ctas < 1 || ctas > 1024)
+      fail(FO_ERR_INVALID_ARG, "link_gbps > 0, latency_us >= 0, 1 <= ctas <= 1024");
+    FO_CUDA(cudaSetDevice(device));
+    auto* c = new fo_ctx_s();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    try {
+      c->comm = make_emulated_comm(rank, world, link_gbps, latency_us, ctas);
+      init_streams(c);
+    } catch (...) {
+      delete c->comm;
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
 fo_status fo_ctx_destroy(fo_ctx c) {
   return guard([&] {
     if (!c) return;

@@ -40,7 +40,7 @@ def candidates(T, limit, seed):
     return [allc[i] for i in sorted(pick)] + [[1] * T, [T]]
 
 
-MODE = sys.argv[1] if len(sys.argv) > 1 else "standalone"   # "standalone" | "insitu" (see note)
+MODE = sys.argv[1] if len(sys.argv) > 1 else "standalone"   # "standalone" | "insitu" | "emulate" (see notes)
 # note: "insitu" divides each group's [wait released, post done] span by its
 # bytes; the span includes queueing behind earlier groups' posts, so it
 # overestimates the cost — kept only as a diagnostic
@@ -113,5 +113,92 @@ def main():
     ctx.close()
 
 
+def timeit_pre(fn, flush, iters=8, warm=2):
+    """Device time of fn on a stream pre-loaded by a sleep kernel (host launch
+    cost outside the events), L2 flushed, median."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        flush.zero_()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e) * 1e3)
+    return sorted(ts)[len(ts) // 2]
+
+
+def main_emulate(link_gbps=770.0, latency_us=6.0, ctas=16):
+    """Emulated NVLink (fo_ctx_create_emulated; timing only): the TP shards of
+    BASELINE configs[1..2] at their real world sizes, each collective taking
+    latency + bus bytes / link bandwidth on 16 CTAs of the SMs the GEMM
+    leaves free.  Per shape: the offline stages (GEMM duration at S, the
+    curve sampled on the emulated communicator), Alg. 1's prediction of every
+    partition (all 2^(T-1) for T <= 8, a seeded sample of 24 otherwise) vs
+    the measured fo_run, the predictive search's pick vs the measured optimum
+    (PAPER.md:638-647), and the overlapped layer vs GEMM -> one collective."""
+    torch.cuda.set_device(0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    errs, ratios = [], []
+    print(f"[emulate] link {link_gbps} GB/s per direction, latency {latency_us} us, {ctas} CTAs per call", flush=True)
+    for (M, N, K, n, coll) in [(4096, 4096, 7168, 2, "allreduce"), (4096, 4096, 3584, 4, "allreduce"),
+                               (4096, 4096, 1792, 8, "allreduce"), (8192, 8192, 1024, 8, "reducescatter")]:
+        ctx = fo.Context.emulated(0, 0, n, link_gbps, latency_us, ctas)
+        S = 64
+        tiles = (M // 256) * (N // 256)
+        T = -(-tiles // S)
+        A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.cell_seed(M, N, K), device="cuda")
+        rows = M if coll == "allreduce" else M // n
+        out = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
+        C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        spec = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=0, ar_layout="rowband")
+        probe = fo.Plan(rank=0, world=n, group_waves=[1] * T, **spec)
+        gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
+                        tile_order=probe.export_order())
+        dur = timeit_pre(lambda: fo.gemm_stage(gplan, A, Bt, C), flush, iters=10)
+        sizes = [1 << s for s in range(18, 28)]
+        curve = ctx.sample_curve(coll, sizes, iters=5)
+        rows_ = []
+        for G in candidates(T, 24, M + K + n):
+            plan = fo.Plan(rank=0, world=n, group_waves=G, **spec)
+            pred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, curve)
+            meas = timeit_pre(lambda: fo.run(ctx, plan, A, Bt, out), flush)
+            rows_.append((G, pred, meas))
+            errs.append(abs(meas - pred) / meas)
+        best = min(rows_, key=lambda r: r[2])
+        pick, _ = fo.tune_search(dur, tiles, S, 256 * 256 * 2, curve)
+        pplan = fo.Plan(rank=0, world=n, group_waves=list(pick), **spec)
+        pick_meas = timeit_pre(lambda: fo.run(ctx, pplan, A, Bt, out), flush)
+        ratios.append(best[2] / pick_meas)
+        # sequential: the GEMM on every SM (all 74 CTA pairs, split tail), then one collective
+        seq = fo.Plan(rank=0, world=n, group_waves=[-(-tiles // 74)], options={"tail_split": -1},
+                      **dict(spec, workers=74, ar_layout="auto"))
+        seq_us = timeit_pre(lambda: fo.run_sequential(ctx, seq, A, Bt, out), flush)
+        comm_full = ctx.time_collective(coll, M * N * 2, 5)
+        e = [abs(m - p) / m for _, p, m in rows_]
+        print(f"[emulate] {coll} n={n} {M}x{N}x{K}: T={T}, GEMM {dur:.1f} us at S={S}, full collective "
+              f"{comm_full:.1f} us; {len(rows_)} partitions: prediction error mean {100 * statistics.mean(e):.2f}% "
+              f"max {100 * max(e):.2f}%; search picks {list(pick)} -> {pick_meas:.1f} us, measured optimum "
+              f"{best[0]} {best[2]:.1f} us ({100 * best[2] / pick_meas:.1f}%); sequential {seq_us:.1f} us -> "
+              f"speedup {seq_us / pick_meas:.3f}x (best {seq_us / best[2]:.3f}x)", flush=True)
+        for G, p_, m_ in sorted(rows_, key=lambda r: r[2])[:4]:
+            print(f"           {str(G):28s} predicted {p_:7.1f} us  measured {m_:7.1f} us", flush=True)
+        del A, Bt, out, C
+        torch.cuda.empty_cache()
+        ctx.close()
+    e = sorted(errs)
+    print(f"[emulate] ALL: {len(errs)} (shape, partition) cases, prediction error mean {100 * statistics.mean(e):.2f}%, "
+          f"median {100 * e[len(e) // 2]:.2f}%, p90 {100 * e[int(0.9 * len(e))]:.2f}%, max {100 * e[-1]:.2f}%; "
+          f"searched / optimum: min {100 * min(ratios):.1f}%, mean {100 * statistics.mean(ratios):.1f}%", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if MODE == "emulate":
+        main_emulate()
+    else:
+        main()
