@@ -294,7 +294,7 @@ fo_status fo_ctx_create_loopback(void* group, int32_t rank, fo_ctx* out);
 
 /* EVALUATION BACKEND — an emulated NVLink group on ONE GPU (not a
  * communicator).  The context acts as rank `rank` of `world`; each of its
- * collectives is a kernel of `ctas` CTAs (256 threads) on the comm stream that
+ * collectives is a kernel of `ctas` CTAs (512 threads) on the comm stream that
  * moves the call's local HBM traffic (reads the send range, writes the receive
  * range) and lasts at least latency_us + bus_bytes / link_gbps, bus_bytes per
  * rank in the nccl-tests convention (AllReduce 2(n-1)/n x bytes; ReduceScatter

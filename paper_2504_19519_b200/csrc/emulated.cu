@@ -9,7 +9,7 @@
 // per-group calls, the last group in stream order) are validated by the paper
 // against real collectives whose duration grows with the group's bytes
 // (PAPER.md:625-647).  This backend gives every call that shape: a kernel of
-// `ctas` CTAs on the communication stream that
+// `ctas` CTAs (512 threads) on the communication stream that
 //   1. moves the call's LOCAL HBM traffic (reads the send range, writes the
 //      receive range, as a rank's NCCL kernels do), and
 //   2. does not finish before latency_us + bus_bytes / link_gbps after it
@@ -39,19 +39,44 @@ namespace {
 // dst[j] = src[j % n_src] for j < n_dst (16-byte vectors; src null: zeros),
 // plus a read-only sweep of rd[0 .. n_rd) (the send data a reduction reads);
 // then spin until `dur_ns` after the CTA started (the CTAs of a call start
-// together on the SMs the GEMM leaves free).
-__global__ void fo_emu_link_kernel(const uint4* rd, int64_t n_rd, const uint4* src, int64_t n_src, uint4* dst,
-                                   int64_t n_dst, unsigned long long dur_ns) {
+// together on the SMs the GEMM leaves free).  Each thread keeps EMU_UNROLL
+// 16-byte loads in flight (64 KB per CTA), like a collective's copy loop, so
+// a few CTAs move the call's bytes at the link rate instead of at the rate
+// one load per thread allows.
+constexpr int EMU_THREADS = 512;
+constexpr int EMU_UNROLL = 8;
+
+__global__ void __launch_bounds__(EMU_THREADS) fo_emu_link_kernel(const uint4* rd, int64_t n_rd, const uint4* src,
+                                                                  int64_t n_src, uint4* dst, int64_t n_dst,
+                                                                  unsigned long long dur_ns) {
   unsigned long long t0, now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t span = (int64_t)gridDim.x * blockDim.x;  // consecutive threads -> consecutive vectors
   uint32_t acc = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_rd; i += stride) {
-    const uint4 v = __ldcs(rd + i);
-    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  for (int64_t base = 0; base < n_rd; base += span * EMU_UNROLL) {
+    uint4 v[EMU_UNROLL];
+#pragma unroll
+    for (int u = 0; u < EMU_UNROLL; ++u) {
+      const int64_t i = base + u * span + tid;
+      v[u] = i < n_rd ? __ldcs(rd + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < EMU_UNROLL; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
   }
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_dst; j += stride)
-    dst[j] = src ? src[j % n_src] : make_uint4(0, 0, 0, 0);
+  for (int64_t base = 0; base < n_dst; base += span * EMU_UNROLL) {
+    uint4 v[EMU_UNROLL];
+#pragma unroll
+    for (int u = 0; u < EMU_UNROLL; ++u) {
+      const int64_t j = base + u * span + tid;
+      v[u] = (src && j < n_dst) ? __ldcs(src + (j % n_src)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < EMU_UNROLL; ++u) {
+      const int64_t j = base + u * span + tid;
+      if (j < n_dst) __stcs(dst + j, v[u]);
+    }
+  }
   if (acc == 0x9e3779b9u && n_rd < 0) dst[0] = make_uint4(acc, 0, 0, 0);  // keeps the read sweep (never true)
   if (threadIdx.x == 0) {
     while (true) {
@@ -84,7 +109,7 @@ struct EmuComm : Comm {
   }
   void launch(const void* rd, size_t rd_bytes, const void* src, size_t src_bytes, void* dst, size_t dst_bytes,
               double bus_bytes, cudaStream_t s) {
-    fo_emu_link_kernel<<<ctas, 256, 0, s>>>(static_cast<const uint4*>(rd), (int64_t)(rd_bytes / 16),
+    fo_emu_link_kernel<<<ctas, EMU_THREADS, 0, s>>>(static_cast<const uint4*>(rd), (int64_t)(rd_bytes / 16),
                                             static_cast<const uint4*>(src), (int64_t)(src_bytes / 16),
                                             static_cast<uint4*>(dst), (int64_t)(dst_bytes / 16), wire_ns(bus_bytes));
     count_launch();

@@ -163,6 +163,10 @@ def main_emulate(link_gbps=770.0, latency_us=6.0, ctas=16):
         dur = timeit_pre(lambda: fo.gemm_stage(gplan, A, Bt, C), flush, iters=10)
         sizes = [1 << s for s in range(18, 28)]
         curve = ctx.sample_curve(coll, sizes, iters=5)
+        fac = 2.0 * (n - 1) / n if coll == "allreduce" else (n - 1) / n
+        print(f"[emulate] {coll} n={n} curve (bytes: measured us / link model us): " + ", ".join(
+            f"{b_ >> 20} MB: {b_ / (g_ * 1e3):.1f}/{latency_us + fac * b_ / (link_gbps * 1e3):.1f}"
+            for b_, g_ in curve if b_ >= 1 << 21), flush=True)
         rows_ = []
         for G in candidates(T, 24, M + K + n):
             plan = fo.Plan(rank=0, world=n, group_waves=G, **spec)
