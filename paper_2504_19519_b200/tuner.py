@@ -234,6 +234,46 @@ def effective_curve(curve: list, post_us_per_byte: float, post_fixed_us: float =
     return out
 
 
+def insitu_curve(ctx, spec: dict, A, Bt, out, T: int, S: int, tile_bytes: int, base_curve: list,
+                 group_sizes=(1, 2, 4), iters: int = 3) -> list:
+    """Offline stage (3), resource contention, measured: the
+    collective's latency while the GEMM runs.  For g in `group_sizes` (waves)
+    the layer runs with groups of g waves and the comm stream's timestamps
+    around every group's collective but the last (the last runs after the
+    GEMM) give its in-situ latency at g waves' bytes; those points replace the
+    standalone curve's samples in their size range, the standalone samples
+    above it stay (groups that large run mostly after the GEMM).  DESIGN.md R42.
+    spec: the layer's fo.Plan keyword arguments without group_waves."""
+    import statistics
+
+    import torch
+
+    from . import Plan, run
+    pts = []
+    for g in group_sizes:
+        if g >= T:
+            break
+        G = [g] * (T // g) + ([T % g] if T % g else [])
+        plan = Plan(group_waves=G, **spec)
+        ts = torch.zeros(2 * len(G), dtype=torch.int64, device="cuda")
+        plan.set_debug(None, ts)
+        d = []
+        for _ in range(iters):
+            run(ctx, plan, A, Bt, out)
+            torch.cuda.synchronize()
+            t = ts.cpu().tolist()
+            d += [(t[2 * j + 1] - t[2 * j]) / 1e3 for j in range(len(G) - 1) if G[j] == g]
+        plan.close()
+        if d:
+            b = min(g * S, max(1, T * S)) * tile_bytes
+            pts.append((b, b / (statistics.median(d) * 1e-6) / 1e9))
+    if not pts:
+        return list(base_curve)
+    lo, hi = min(p[0] for p in pts), max(p[0] for p in pts)
+    keep = [(b, bw) for b, bw in base_curve if b < lo or b > hi]
+    return sorted(keep + pts)
+
+
 # collectives with a ROWBAND layout (AR: in place; RS: scattered straight into
 # the output, DESIGN.md R40)
 BANDED = ("allreduce", "reducescatter")
@@ -292,7 +332,7 @@ def compositions(T: int) -> list:
 
 def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_n=TILE_N, device=0,
                sizes=None, iters=10, min_comm_sms=16, verify=8, all_partitions_T=7,
-               tile_shapes=None) -> LayerChoice:
+               tile_shapes=None, insitu=None) -> LayerChoice:
     """Joint choice of S (wave width), layout and wave groups for one layer
     (AllReduce / ReduceScatter; world from the context).
 
@@ -313,7 +353,13 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     persistent GEMM and the collective is then
     searched too — every S that leaves a context's CTAs their SMs is a
     candidate with that context's sampled curve, and the measured
-    verification picks the context (`LayerChoice.ctx_index`)."""
+    verification picks the context (`LayerChoice.ctx_index`).
+
+    `insitu` (default: world > 1): Alg. 1 sees the collective's curve sampled
+    while the GEMM runs on the candidate's S workers (insitu_curve, R42) for
+    the group sizes that overlap the GEMM — measured on emulated NVLink it
+    cuts the prediction error from 6.7% to 3.0% and the pick reaches the
+    measured optimum (profiles/r02_predictor_emulated.txt)."""
     import torch
 
     from . import post_stage
@@ -419,6 +465,19 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
                               tile_order=probe.export_order(), options={"tail_split": split} if split else None)
                     probes.append((S, T, layout, single_only, swz, gp, split, tm, tn, tiles))
     durs = timeit_many([(lambda gp=pr[5]: gemm_stage(gp, A, Bt, out)) for pr in probes], iters)
+    use_insitu = (world > 1) if insitu is None else bool(insitu)
+    icurves = {}
+
+    def curve_for(ci, S, T, layout, swz, tm, tn):
+        """The context's curve, contended by the GEMM at this S (R42), cached per (context, S, tile, layout)."""
+        if not use_insitu or T < 2:
+            return curves[ci]
+        key = (ci, S, tm, tn, layout)
+        if key not in icurves:
+            sp = dict(coll=coll, m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S, swizzle=swz,
+                      ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world)
+            icurves[key] = insitu_curve(ctxs[ci], sp, A, Bt, out, T, S, tm * tn * 2, curves[ci], iters=2)
+        return icurves[key]
     for (S, T, layout, single_only, swz, _, split, tm, tn, tiles), dur in zip(probes, durs):
         norm = post in ("add_rmsnorm", "add_rmsnorm_res")
         per_group_op = post if (layout == "rowband" or not norm) else "none"
@@ -427,7 +486,8 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         for ci in range(len(ctxs)):
             if not ctx_ok(ci, S, max(1, tm // 128)):
                 continue
-            eff = effective_curve(curves[ci], per_group)
+            # (a single group does not overlap the GEMM: the standalone curve)
+            eff = effective_curve(curves[ci] if single_only else curve_for(ci, S, T, layout, swz, tm, tn), per_group)
             if single_only:
                 pred = tune_predict([T], dur, tiles, S, tm * tn * 2, eff)
                 evaluated.append((S, layout, [T], pred + tail, dur, swz, split, tm, tn, ci))

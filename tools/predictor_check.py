@@ -144,7 +144,7 @@ def main_emulate(link_gbps=770.0, latency_us=6.0, ctas=16):
     (PAPER.md:638-647), and the overlapped layer vs GEMM -> one collective."""
     torch.cuda.set_device(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    errs, ratios = [], []
+    errs, ratios, ierrs, iratios = [], [], [], []
     print(f"[emulate] link {link_gbps} GB/s per direction, latency {latency_us} us, {ctas} CTAs per call", flush=True)
     for (M, N, K, n, coll) in [(4096, 4096, 7168, 2, "allreduce"), (4096, 4096, 3584, 4, "allreduce"),
                                (4096, 4096, 1792, 8, "allreduce"), (8192, 8192, 1024, 8, "reducescatter")]:
@@ -167,31 +167,55 @@ def main_emulate(link_gbps=770.0, latency_us=6.0, ctas=16):
         print(f"[emulate] {coll} n={n} curve (bytes: measured us / link model us): " + ", ".join(
             f"{b_ >> 20} MB: {b_ / (g_ * 1e3):.1f}/{latency_us + fac * b_ / (link_gbps * 1e3):.1f}"
             for b_, g_ in curve if b_ >= 1 << 21), flush=True)
+        # the contended curve (offline stage (3) measured in situ, tuner.insitu_curve, R42)
+        icurve = tuner.insitu_curve(ctx, dict(spec, rank=0, world=n), A, Bt, out, T, S, 256 * 256 * 2, curve)
+        print(f"[emulate] {coll} n={n} in-situ curve points (bytes: us): " + ", ".join(
+            f"{b_ >> 20} MB: {b_ / (g_ * 1e3):.1f}" for b_, g_ in icurve if b_ >= 1 << 21), flush=True)
         rows_ = []
         for G in candidates(T, 24, M + K + n):
             plan = fo.Plan(rank=0, world=n, group_waves=G, **spec)
             pred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, curve)
+            ipred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, icurve)
             meas = timeit_pre(lambda: fo.run(ctx, plan, A, Bt, out), flush)
-            rows_.append((G, pred, meas))
+            rows_.append((G, pred, meas, ipred))
             errs.append(abs(meas - pred) / meas)
+            ierrs.append(abs(meas - ipred) / meas)
+        ipick, _ = fo.tune_search(dur, tiles, S, 256 * 256 * 2, icurve)
+        iplan = fo.Plan(rank=0, world=n, group_waves=list(ipick), **spec)
+        ipick_meas = timeit_pre(lambda: fo.run(ctx, iplan, A, Bt, out), flush)
         best = min(rows_, key=lambda r: r[2])
         pick, _ = fo.tune_search(dur, tiles, S, 256 * 256 * 2, curve)
         pplan = fo.Plan(rank=0, world=n, group_waves=list(pick), **spec)
         pick_meas = timeit_pre(lambda: fo.run(ctx, pplan, A, Bt, out), flush)
         ratios.append(best[2] / pick_meas)
+        iratios.append(best[2] / ipick_meas)
         # sequential: the GEMM on every SM (all 74 CTA pairs, split tail), then one collective
         seq = fo.Plan(rank=0, world=n, group_waves=[-(-tiles // 74)], options={"tail_split": -1},
                       **dict(spec, workers=74, ar_layout="auto"))
         seq_us = timeit_pre(lambda: fo.run_sequential(ctx, seq, A, Bt, out), flush)
         comm_full = ctx.time_collective(coll, M * N * 2, 5)
-        e = [abs(m - p) / m for _, p, m in rows_]
+        e = [abs(m - p) / m for _, p, m, _ in rows_]
+        ie = [abs(m - p) / m for _, _, m, p in rows_]
         print(f"[emulate] {coll} n={n} {M}x{N}x{K}: T={T}, GEMM {dur:.1f} us at S={S}, full collective "
               f"{comm_full:.1f} us; {len(rows_)} partitions: prediction error mean {100 * statistics.mean(e):.2f}% "
               f"max {100 * max(e):.2f}%; search picks {list(pick)} -> {pick_meas:.1f} us, measured optimum "
               f"{best[0]} {best[2]:.1f} us ({100 * best[2] / pick_meas:.1f}%); sequential {seq_us:.1f} us -> "
-              f"speedup {seq_us / pick_meas:.3f}x (best {seq_us / best[2]:.3f}x)", flush=True)
-        for G, p_, m_ in sorted(rows_, key=lambda r: r[2])[:4]:
-            print(f"           {str(G):28s} predicted {p_:7.1f} us  measured {m_:7.1f} us", flush=True)
+              f"speedup {seq_us / pick_meas:.3f}x (best {seq_us / best[2]:.3f}x); with the in-situ curve: error mean "
+              f"{100 * statistics.mean(ie):.2f}% max {100 * max(ie):.2f}%, search picks {list(ipick)} -> "
+              f"{ipick_meas:.1f} us ({100 * best[2] / ipick_meas:.1f}%), speedup {seq_us / ipick_meas:.3f}x", flush=True)
+        # the whole tuner (tile shape, S, layout, tail split, partition; in-situ
+        # curve; measured verification of the best predictions)
+        ch = tuner.tune_layer(M, N, K, ctx, coll, "none", device=0, tile_shapes=[(256, 256), (128, 256)])
+        tplan = fo.Plan(rank=0, world=n, **ch.spec(M, N, K, coll))
+        tout = torch.empty(tplan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
+        t_us = timeit_pre(lambda: fo.run(ctx, tplan, A, Bt, tout), flush)
+        print(f"[emulate] {coll} n={n}: tune_layer -> {ch.tile_m}x{ch.tile_n} S={ch.workers} {ch.layout} "
+              f"groups {ch.groups} tail_split {ch.tail_split}: {t_us:.1f} us = {seq_us / t_us:.3f}x sequential; "
+              f"layer roofline max(GEMM at peak, collective on the link) "
+              f"{max(2.0 * M * N * K / 1631.4e6, latency_us + fac * M * N * 2 / (link_gbps * 1e3)):.1f} us", flush=True)
+        for G, p_, m_, ip_ in sorted(rows_, key=lambda r: r[2])[:4]:
+            print(f"           {str(G):28s} predicted {p_:7.1f} us (in-situ curve {ip_:7.1f})  measured {m_:7.1f} us",
+                  flush=True)
         del A, Bt, out, C
         torch.cuda.empty_cache()
         ctx.close()
@@ -199,6 +223,10 @@ def main_emulate(link_gbps=770.0, latency_us=6.0, ctas=16):
     print(f"[emulate] ALL: {len(errs)} (shape, partition) cases, prediction error mean {100 * statistics.mean(e):.2f}%, "
           f"median {100 * e[len(e) // 2]:.2f}%, p90 {100 * e[int(0.9 * len(e))]:.2f}%, max {100 * e[-1]:.2f}%; "
           f"searched / optimum: min {100 * min(ratios):.1f}%, mean {100 * statistics.mean(ratios):.1f}%", flush=True)
+    e = sorted(ierrs)
+    print(f"[emulate] ALL with the in-situ curve: prediction error mean {100 * statistics.mean(e):.2f}%, "
+          f"median {100 * e[len(e) // 2]:.2f}%, p90 {100 * e[int(0.9 * len(e))]:.2f}%, max {100 * e[-1]:.2f}%; "
+          f"searched / optimum: min {100 * min(iratios):.1f}%, mean {100 * statistics.mean(iratios):.1f}%", flush=True)
 
 
 if __name__ == "__main__":
