@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shards", action="store_true", help="skip the other configs' per-rank layers")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle sample")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="DEV ONLY: one process acting as rank 0 of N with the emulated-link evaluation backend "
+                         "(fo_ctx_create_emulated; timing model, not NVLink) — exercises the N>1 code paths on one GPU")
     return ap.parse_args()
 
 
@@ -213,6 +216,9 @@ def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    emulate = args.emulate_world > 1 and "WORLD_SIZE" not in os.environ
+    if emulate:
+        world, rank = args.emulate_world, 0
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and "WORLD_SIZE" in os.environ:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
@@ -254,18 +260,27 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     # ---- NCCL context of the library (unique id broadcast over the process group)
-    if use_dist:
+    def emu_ctx(cap):
+        c = fo.Context.emulated(local, rank, world, 770.0, 6.0, ctas=min(max(cap, 16), 32))
+        c.nccl_max_ctas = cap
+        return c
+    if emulate:
+        ctx = emu_ctx(max(1, comm_sms))
+        ctxs = [ctx, emu_ctx(max(comm_sms + 12, 32))]
+        ctx_seq = emu_ctx(0)
+    elif use_dist:
         obj = [fo.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     else:
         uid = fo.unique_id()
-    with _StdoutToStderr():
-        ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
-    # a second overlapped-op communicator with a wider CTA cap: the tuner
-    # searches the SM split (GEMM workers vs NCCL CTAs) across both
-    ctxs = [ctx]
-    if world > 1:
+    if not emulate:
+        with _StdoutToStderr():
+            ctx = fo.Context.create(local, rank, world, uid, nccl_max_ctas=max(1, comm_sms) if world > 1 else 0)
+        # a second overlapped-op communicator with a wider CTA cap: the tuner
+        # searches the SM split (GEMM workers vs NCCL CTAs) across both
+        ctxs = [ctx]
+    if world > 1 and not emulate:
         if use_dist:
             obj = [fo.unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -276,7 +291,9 @@ def main():
             ctxs.append(fo.Context.create(local, rank, world, uid2, nccl_max_ctas=max(comm_sms + 12, 32)))
     # the sequential baseline's NCCL call runs alone, so it gets NCCL's default
     # CTA count (its own communicator) instead of the overlapped op's SM cap
-    if world > 1:
+    if emulate:
+        pass
+    elif world > 1:
         if use_dist:
             obj = [fo.unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -645,7 +662,9 @@ def main():
             "metric": "overlapped GEMM+AllReduce us per layer",
             "value": round(ov_us, 2), "unit": "us", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ov_us / 1e3, 4), "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) weights)",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) activations, N(0,0.02^2) weights)"
+            + ("; EMULATED NVLink (--emulate-world: one GPU, collectives = link-model kernels; NOT a measurement)"
+               if emulate else ""),
             "config": {**{k: wl[k] for k in ("workload", "M", "N", "K_loc", "tp", "collective")},
                        "tile": f"{BMc}x{BNc}", "workers": S, "comm_sms": sms - cgc * S,
                        "nccl_max_ctas": getattr(ctx, "nccl_max_ctas", None) if world > 1 else None,
