@@ -99,6 +99,54 @@ def main():
     full = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     fo.run_allgather(ctx, plan, local, full, res, gam)
     torch.cuda.synchronize()
+    # round 2: ROWBAND layouts of RS (EPI_RS_BAND, TMA-stored and 16-B
+    # subtile rows) and A2A, at world 1 (NCCL) and as world-4 stages
+    for coll in ("reducescatter", "alltoall"):
+        for post in ("none", "add"):
+            kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=128, workers=4, swizzle=1, group_waves=[1, 1],
+                      ar_layout="rowband", post=post)
+            if coll == "alltoall":
+                kw["row_dst"] = np.zeros(M, np.int32)
+                plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
+            else:
+                plan = fo.Plan(**kw)
+            out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+            fo.run(ctx, plan, Ad, Bd, out, res if post != "none" else None)
+            torch.cuda.synchronize()
+            if not torch.equal(out, C):
+                print(f"mismatch {coll} rowband post={post}")
+                bad += 1
+    for n, bn in ((4, 128), (8, 256)):   # h = 64 (TMA stores) / h = 32 with 256-column tiles
+        plan = fo.Plan(coll="reducescatter", m=M, n=N, k=K, tile_m=256, tile_n=bn, workers=N // bn, swizzle=1,
+                       group_waves=[1, 1], ar_layout="rowband", rank=1, world=n)
+        send = torch.empty(M * N, dtype=torch.bfloat16, device="cuda")
+        fo.gemm_stage(plan, Ad, Bd, send)
+    specs = []
+    for s_ in range(4):
+        specs.append(dict(coll="alltoall", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=4, swizzle=1,
+                          group_waves=[1, 1], ar_layout="rowband", row_dst=(np.arange(M) % 4).astype(np.int32)))
+    plan = fo.Plan(rank=2, world=4, peers=specs, **specs[2])
+    send = torch.empty(plan.info["send_elems"], dtype=torch.bfloat16, device="cuda")
+    fo.gemm_stage(plan, Ad, Bd, send)
+    # the bulk-staged add + RMSNorm (>= 64 MB outputs) through the slot map, residual written back
+    Mb, Nb = 8192, 4096
+    plan = fo.Plan(coll="allreduce", m=Mb, n=Nb, k=64, tile_m=256, tile_n=256, workers=64, swizzle=2,
+                   group_waves=[2, 2, 4], ar_layout="slot", post="add_rmsnorm_res")
+    recv = torch.randn(Mb * Nb, device="cuda").to(torch.bfloat16)
+    rb = torch.randn(Mb, Nb, device="cuda").to(torch.bfloat16)
+    ob = torch.empty(Mb, Nb, dtype=torch.bfloat16, device="cuda")
+    fo.post_stage(plan, recv, ob, rb, torch.ones(Nb, dtype=torch.bfloat16, device="cuda"))
+    # the emulated-link evaluation backend: fo_run at emulated world 4
+    ectx = fo.Context.emulated(0, 0, 4, 770.0, 6.0, 16)
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=128, workers=4, swizzle=1,
+                   group_waves=[1, 1], ar_layout="rowband", rank=0, world=4)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ectx, plan, Ad, Bd, out)
+    torch.cuda.synchronize()
+    if not torch.equal(out, C):
+        print("mismatch emulated-link fo_run")
+        bad += 1
+    ectx.close()
     ctx.close()
     print("sanitize cases done, mismatches:", bad)
     sys.exit(1 if bad else 0)
