@@ -477,8 +477,13 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      (f = min(4, S/R, k-blocks) when 2R <= S and that is >= 2;
  *                      else no split); -2 — stream-K tail: the tail's R x k-blocks
  *                      dealt out evenly to the S workers in contiguous K-ranges
- *                      (measured slower than -1, R34).  Works with every
- *                      epilogue mode.  Set before the first run.
+ *                      (measured slower than -1, R34); -3 — DP + suffix
+ *                      helpers for a last wave of R > S/2 tiles (e.g. a one-wave
+ *                      GEMM of 64 tiles on 74 pairs): each tail tile's own worker
+ *                      runs k-blocks [0, x), the S-R idle workers run the suffixes
+ *                      [x, KB) of consecutive tail tiles, x = KB - KB/(1 +
+ *                      ceil(R/(S-R))) (R43).  Works with every epilogue
+ *                      mode.  Set before the first run.
  *  FO_OPT_POST_SM_PARTITION 0 — per-group post kernels may co-reside with GEMM CTAs;
  *                      1 — they request padding shared memory so they only run on
  *                      the SMs the persistent GEMM leaves free (Alg. 1's SM split)

@@ -242,6 +242,12 @@ static void ensure_device(fo_plan_s* p) {
   // over the workers of that wave.  f >= 2: each into f equal K-slices on
   // consecutive workers (R*f <= S); stream-K (-2): their R*KB k-blocks dealt
   // out evenly to the workers in contiguous ranges (at most 4 parts per tile).
+  // -3 (DP + suffix helpers, for a last wave of more than S/2 tiles): every
+  // tail tile's worker runs k-blocks [0, x) and the S - R idle workers run the
+  // suffixes [x, KB) of consecutive tail tiles, x chosen so the busiest helper
+  // (ceil(R / (S-R)) suffixes) ends with the owners: the owners stay in
+  // k-lockstep (the operand panels stay shared in L2, unlike stream-K) and
+  // the wave takes x instead of KB k-blocks.
   // The host lists every worker's K-ranges; the range starting at k-block 0
   // owns the tile (it is its worker's last, the others' first segment, so no
   // owner ever waits on a worker that is itself waiting).
@@ -250,6 +256,7 @@ static void ensure_device(fo_plan_s* p) {
     const int R = h.tiles - (h.T - 1) * h.S;
     int f = p->tail_split_req;
     const bool streamk = (f == -2) && R > 0 && KB >= 2 && R < h.S;
+    const bool suffix = (f == -3) && R > 0 && KB >= 4 && 2 * R > h.S && R < h.S;
     if (f == -1) {  // auto: never more slices than k-blocks; no split when under 2
       f = (R > 0 && 2 * R <= h.S) ? std::min(std::min(4, h.S / R), KB) : 1;
       if (f < 2) f = 1;
@@ -260,7 +267,7 @@ static void ensure_device(fo_plan_s* p) {
     std::vector<int32_t> wseg(h.S + 1, 0);
     int nslots = 0;
     const int tail0 = (h.T - 1) * h.S;
-    if (streamk || f > 1) {
+    if (streamk || suffix || f > 1) {
       // pieces[w] = (tile, kb0, kb1) of worker w, in global k order
       std::vector<std::vector<std::array<int, 3>>> pieces(h.S);
       if (streamk) {
@@ -276,6 +283,14 @@ static void ensure_device(fo_plan_s* p) {
             g0 += kb1 - kb0;
           }
         }
+      } else if (suffix) {
+        const int H = h.S - R;
+        const int per = (R + H - 1) / H;          // suffixes of the busiest helper
+        const int y = std::max(1, KB / (1 + per));  // suffix length: x = KB - y ~ per * y
+        const int x = KB - y;
+        for (int r = 0; r < R; ++r) pieces[r].push_back({r, 0, x});
+        for (int hh = 0, r = 0; hh < H; ++hh)
+          for (int c = 0; c < R / H + (hh < R % H ? 1 : 0); ++c, ++r) pieces[R + hh].push_back({r, x, KB});
       } else {
         for (int r = 0; r < R; ++r)
           for (int sl = 0; sl < f; ++sl) pieces[r * f + sl].push_back({r, sl * KB / f, (sl + 1) * KB / f});
@@ -289,7 +304,7 @@ static void ensure_device(fo_plan_s* p) {
       // (the distributed fold, R34)
       for (int r = 0; r < R; ++r) {
         first_slot[r] = nslots;
-        nslots += nparts[r] - 1 + (streamk ? 0 : 1);
+        nslots += nparts[r] - 1 + ((streamk || suffix) ? 0 : 1);
       }
       std::vector<int> next_idx(R, 0);
       std::vector<int> next_slot = first_slot;
@@ -322,7 +337,7 @@ static void ensure_device(fo_plan_s* p) {
     p->tail_pos = split ? tail0 : h.tiles;
     p->units = split ? tail0 + (int)segs.size() : h.tiles;
     const int cg = ctas_per_tile(h.BM);
-    p->dist_fold = split && !streamk;
+    p->dist_fold = split && !streamk && !suffix;
     p->ctr_words = h.P + (split ? R * cg * (p->dist_fold ? 2 : 1) : 0);
     if (split) {
       p->d_seg = upload(segs);
@@ -1585,7 +1600,7 @@ fo_status fo_plan_set_option(fo_plan p, int32_t option, int64_t value) {
         p->post_sm_partition = (int)value;
         break;
       case FO_OPT_TAIL_SPLIT:
-        if (value < -2 || value > 16) fail(FO_ERR_INVALID_ARG, "tail_split must be -2..16");
+        if (value < -3 || value > 16) fail(FO_ERR_INVALID_ARG, "tail_split must be -3..16");
         if (p->device >= 0) fail(FO_ERR_STATE, "tail_split must be set before the plan's first run");
         p->tail_split_req = (int)value;
         break;

@@ -54,6 +54,8 @@ def _draw(seed):
         tail_split = 0                               # 64-row tiles (tcgen05 M=64) run whole tiles only
     k_snake = int(rng.choice([-1, 0, 1]))
     tma_store = int(rng.random() < 0.7)
+    if tail_split != 0 and rng.random() < 0.35:
+        tail_split = -3                              # DP + suffix helpers (R43; off unless R > S/2)
     if coll == "reducescatter" and rng.random() < 0.4:
         # ascending bands of whole tile-rows (raster, waves of whole tile-rows):
         # the RS rowband layout (R40) under "auto"
@@ -210,6 +212,8 @@ def test_random_run_equals_sequential(seed):
     plan.set_option("multicast", int(rng.random() < 0.3))
     plan.set_option("k_snake", int(rng.choice([-1, 0, 1])))
     plan.set_option("tma_store", int(rng.random() < 0.7))
+    if ts != 0 and BM != 64 and rng.random() < 0.35:
+        plan.set_option("tail_split", -3)            # DP + suffix helpers (R43; off unless R > S/2)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     try:
         A, Bt = synthetic.exact_inputs(M, N, K, seed=7100 + seed, nnz_per_row=128)

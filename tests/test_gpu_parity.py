@@ -345,13 +345,16 @@ def test_tile_timestamps_follow_waves(BM):
     (128, 256, 512, 1024, 1024, 14, -2),    # stream-K with single-CTA tiles
     (256, 64, 512, 512, 256, 12, 2),        # 16 tiles, R=4, f=2, one 64-col chunk: slice 1 owns none
     (256, 128, 512, 1024, 512, 14, 3),      # 16 tiles, R=2, f=3, two chunks: slice 2 owns none
+    (256, 256, 1024, 4096, 2048, 74, -3),   # DP + suffix (R43): one wave of 64 tiles on 74 pairs, x = 28 of 32
+    (128, 256, 1024, 2048, 1024, 100, -3),  # DP + suffix, single-CTA tiles: 64 tiles, 36 helpers, 2 each
+    (256, 128, 768, 1024, 576, 14, -3),     # DP + suffix: 24 tiles, T=2, R=10 > S/2, 9 k-blocks (uneven)
 ])
 @pytest.mark.parametrize("dist_fold", [1, 0])
 def test_tail_split_exact(ctx1, BM, BN, M, N, K, S, split, dist_fold):
     """Split tail (R34), both folds of an f-slice split (FO_OPT_DIST_FOLD: the
     slices reduce the tile together / the k-block-0 slice folds everything)."""
-    if split == -2 and dist_fold == 0:
-        pytest.skip("stream-K always folds in the owner")
+    if split in (-2, -3) and dist_fold == 0:
+        pytest.skip("stream-K / DP + suffix always fold in the owner")
     A, Bt = synthetic.exact_inputs(M, N, K, seed=77, nnz_per_row=256)
     C = onum.gemm(A, Bt)
     for coll in ("nocomm", "allreduce"):
