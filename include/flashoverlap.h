@@ -482,8 +482,9 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *                      GEMM of 64 tiles on 74 pairs): each tail tile's own worker
  *                      runs k-blocks [0, x), the S-R idle workers run the suffixes
  *                      [x, KB) of consecutive tail tiles, x = KB - KB/(1 +
- *                      ceil(R/(S-R))) (R43).  Works with every epilogue
- *                      mode.  Set before the first run.
+ *                      ceil(R/(S-R))) (R43; correct, measured slower than
+ *                      the plain grid, profiles/r02_suffix_probe.txt).  Works with
+ *                      every epilogue mode.  Set before the first run.
  *  FO_OPT_POST_SM_PARTITION 0 — per-group post kernels may co-reside with GEMM CTAs;
  *                      1 — they request padding shared memory so they only run on
  *                      the SMs the persistent GEMM leaves free (Alg. 1's SM split)
