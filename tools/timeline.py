@@ -17,14 +17,14 @@ import synthetic  # noqa: E402
 from tools.gemm_probe import timeit  # noqa: E402
 
 
-def one(ctx, coll, M, N, K, BN, S, groups, layout="slot", flush=None, wait_kernel=0):
+def one(ctx, coll, M, N, K, BN, S, groups, layout="slot", flush=None, wait_kernel=0, world=1):
     kw = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=BN, workers=S, swizzle=1 if layout == "rowband" else 2,
               group_waves=groups, ar_layout=layout)
     if coll == "alltoall":
         kw["row_dst"] = np.zeros(M, np.int32)
         plan = fo.Plan(rank=0, world=1, peers=[kw], **kw)
     else:
-        plan = fo.Plan(**kw)
+        plan = fo.Plan(rank=0, world=world, **kw)
     plan.set_option("wait_kernel", wait_kernel)
     A, Bt = synthetic.float_inputs(M, N, K, seed=1, device="cuda")
     out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
@@ -38,7 +38,7 @@ def one(ctx, coll, M, N, K, BN, S, groups, layout="slot", flush=None, wait_kerne
     torch.cuda.synchronize()
     t, g = tile_ts.cpu().numpy(), group_ts.cpu().numpy()
     t0 = t.min()
-    print(f"\n{coll} {M}x{N}x{K} tile 256x{BN} S={S} groups={groups} layout={plan.info['ar_layout']} "
+    print(f"\n{coll} n={world} {M}x{N}x{K} tile 256x{BN} S={S} groups={groups} layout={plan.info['ar_layout']} "
           f"trigger={'spin-kernel' if wait_kernel else 'stream-wait'}: "
           f"fo_run {t_ov:.1f} us, sequential {t_seq:.1f} us, speedup {t_seq / t_ov:.3f}")
     print(f"  GEMM: first tile signal 0.0 us, last tile signal {(t.max() - t0) / 1e3:.1f} us")
@@ -140,7 +140,30 @@ def main():
     ap.add_argument("--trace", default=None, help="also write a Chrome trace JSON of the first AR plans")
     ap.add_argument("--loopback", type=int, default=0,
                     help="world size of a one-GPU loopback run (needs CUDA_MODULE_LOADING=EAGER) instead")
+    ap.add_argument("--emulate", type=int, default=0,
+                    help="rank 0 of this world size on the emulated-link evaluation backend (R42; timing model)")
     args = ap.parse_args()
+    if args.emulate:
+        torch.cuda.set_device(0)
+        n = args.emulate
+        ctx = fo.Context.emulated(0, 0, n, 770.0, 6.0, 16)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        events = []
+        print(f"EMULATED NVLink (fo_ctx_create_emulated: 770 GB/s per direction, 6 us latency, 16 CTAs per call): "
+              f"rank 0 of {n}; a timing model, not a measurement of NVLink")
+        K = 14336 // n
+        r1 = one(ctx, "allreduce", 4096, 4096, K, 256, 64, [1, 1, 1, 1], "rowband", flush, 0, n)
+        r2 = one(ctx, "allreduce", 4096, 4096, K, 256, 64, [1, 3], "rowband", flush, 0, n)
+        r3 = one(ctx, "reducescatter", 8192, 8192, 1024, 256, 64, [1, 4, 8, 3], "rowband", flush, 0, n)
+        events += chrome_trace(f"emulated TP={n} AR rowband S=64 groups [1,1,1,1]", *r1, 64, 1)
+        events += chrome_trace(f"emulated TP={n} AR rowband S=64 groups [1,3]", *r2, 64, 2)
+        events += chrome_trace(f"emulated TP={n} RS rowband S=64 groups [1,4,8,3]", *r3, 64, 3)
+        ctx.close()
+        if args.trace:
+            import json
+            with open(args.trace, "w") as f:
+                json.dump({"traceEvents": events, "displayTimeUnit": "ns"}, f)
+        return
     if args.loopback:
         torch.cuda.set_device(0)
         events = []
