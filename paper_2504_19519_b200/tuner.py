@@ -235,15 +235,17 @@ def effective_curve(curve: list, post_us_per_byte: float, post_fixed_us: float =
 
 
 def insitu_curve(ctx, spec: dict, A, Bt, out, T: int, S: int, tile_bytes: int, base_curve: list,
-                 group_sizes=(1, 2, 4), iters: int = 3) -> list:
+                 group_sizes=(1, 2, 4), iters: int = 3, run_args=()) -> list:
     """Offline stage (3), resource contention, measured: the
-    collective's latency while the GEMM runs.  For g in `group_sizes` (waves)
-    the layer runs with groups of g waves and the comm stream's timestamps
-    around every group's collective but the last (the last runs after the
-    GEMM) give its in-situ latency at g waves' bytes; those points replace the
-    standalone curve's samples in their size range, the standalone samples
-    above it stay (groups that large run mostly after the GEMM).  DESIGN.md R42.
-    spec: the layer's fo.Plan keyword arguments without group_waves."""
+    comm-stream work of a group while the GEMM runs.  For g in `group_sizes`
+    (waves) the layer runs with groups (g, T-g); the comm stream's timestamps
+    around group 0's collective (+ its per-group post pass, when `spec` has a
+    fused op: then `run_args` = (residual, gamma)) give its in-situ latency at
+    g waves' bytes — group 0 never queues behind an earlier group's work.
+    Those points replace the standalone curve's samples in their size range;
+    the standalone samples above it stay (groups that large run mostly after
+    the GEMM).  DESIGN.md R42.  spec: the layer's fo.Plan keyword arguments
+    without group_waves."""
     import statistics
 
     import torch
@@ -253,20 +255,18 @@ def insitu_curve(ctx, spec: dict, A, Bt, out, T: int, S: int, tile_bytes: int, b
     for g in group_sizes:
         if g >= T:
             break
-        G = [g] * (T // g) + ([T % g] if T % g else [])
-        plan = Plan(group_waves=G, **spec)
-        ts = torch.zeros(2 * len(G), dtype=torch.int64, device="cuda")
+        plan = Plan(group_waves=[g, T - g], **spec)
+        ts = torch.zeros(4, dtype=torch.int64, device="cuda")
         plan.set_debug(None, ts)
         d = []
         for _ in range(iters):
-            run(ctx, plan, A, Bt, out)
+            run(ctx, plan, A, Bt, out, *run_args)
             torch.cuda.synchronize()
             t = ts.cpu().tolist()
-            d += [(t[2 * j + 1] - t[2 * j]) / 1e3 for j in range(len(G) - 1) if G[j] == g]
+            d.append((t[1] - t[0]) / 1e3)
         plan.close()
-        if d:
-            b = min(g * S, max(1, T * S)) * tile_bytes
-            pts.append((b, b / (statistics.median(d) * 1e-6) / 1e9))
+        b = g * S * tile_bytes
+        pts.append((b, b / (statistics.median(d) * 1e-6) / 1e9))
     if not pts:
         return list(base_curve)
     lo, hi = min(p[0] for p in pts), max(p[0] for p in pts)
@@ -355,11 +355,12 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
     candidate with that context's sampled curve, and the measured
     verification picks the context (`LayerChoice.ctx_index`).
 
-    `insitu` (default: world > 1): Alg. 1 sees the collective's curve sampled
-    while the GEMM runs on the candidate's S workers (insitu_curve, R42) for
-    the group sizes that overlap the GEMM — measured on emulated NVLink it
-    cuts the prediction error from 6.7% to 3.0% and the pick reaches the
-    measured optimum (profiles/r02_predictor_emulated.txt)."""
+    `insitu` (default: world > 1, or a fused op): Alg. 1 sees the collective's
+    (+ per-group op's) curve sampled while the GEMM runs on the candidate's S
+    workers (insitu_curve, R42) for the group sizes that overlap the GEMM —
+    measured on emulated NVLink it cuts the prediction error from 6.7% to 3.0%
+    and the pick reaches the measured optimum
+    (profiles/r02_predictor_emulated.txt)."""
     import torch
 
     from . import post_stage
@@ -465,18 +466,25 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
                               tile_order=probe.export_order(), options={"tail_split": split} if split else None)
                     probes.append((S, T, layout, single_only, swz, gp, split, tm, tn, tiles))
     durs = timeit_many([(lambda gp=pr[5]: gemm_stage(gp, A, Bt, out)) for pr in probes], iters)
-    use_insitu = (world > 1) if insitu is None else bool(insitu)
+    # in-situ curves (R42): at world > 1, and wherever a fused op runs per
+    # group beside the GEMM (its cost there is bounded by the free SMs, far
+    # above its standalone cost: profiles/r02_band_post_probe.txt)
+    use_insitu = (world > 1 or post != "none") if insitu is None else bool(insitu)
     icurves = {}
 
-    def curve_for(ci, S, T, layout, swz, tm, tn):
-        """The context's curve, contended by the GEMM at this S (R42), cached per (context, S, tile, layout)."""
+    def curve_for(ci, S, T, layout, swz, tm, tn, op, base):
+        """`base` (the context's curve with the per-group op folded in),
+        contended by the GEMM at this S: the in-situ points of group 0's
+        comm-stream work incl. the op (R42), cached per (context, S, tile,
+        layout, op)."""
         if not use_insitu or T < 2:
-            return curves[ci]
-        key = (ci, S, tm, tn, layout)
+            return base
+        key = (ci, S, tm, tn, layout, op)
         if key not in icurves:
             sp = dict(coll=coll, m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S, swizzle=swz,
-                      ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world)
-            icurves[key] = insitu_curve(ctxs[ci], sp, A, Bt, out, T, S, tm * tn * 2, curves[ci], iters=2)
+                      ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank, world=world, post=op)
+            icurves[key] = insitu_curve(ctxs[ci], sp, A, Bt, out, T, S, tm * tn * 2, base, iters=3,
+                                        run_args=(res, gam) if op != "none" else ())
         return icurves[key]
     for (S, T, layout, single_only, swz, _, split, tm, tn, tiles), dur in zip(probes, durs):
         norm = post in ("add_rmsnorm", "add_rmsnorm_res")
@@ -487,7 +495,8 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
             if not ctx_ok(ci, S, max(1, tm // 128)):
                 continue
             # (a single group does not overlap the GEMM: the standalone curve)
-            eff = effective_curve(curves[ci] if single_only else curve_for(ci, S, T, layout, swz, tm, tn), per_group)
+            base = effective_curve(curves[ci], per_group)
+            eff = base if single_only else curve_for(ci, S, T, layout, swz, tm, tn, per_group_op, base)
             if single_only:
                 pred = tune_predict([T], dur, tiles, S, tm * tn * 2, eff)
                 evaluated.append((S, layout, [T], pred + tail, dur, swz, split, tm, tn, ci))

@@ -50,7 +50,7 @@ def main():
     torch.cuda.set_device(0)
     ctx = fo.Context.create(0, 0, 1, fo.unique_id())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    errs, ratios = [], []
+    errs, ratios, ierrs, iratios = [], [], [], []
     for (M, N, K) in [(4096, 4096, 14336), (4096, 4096, 3584), (4096, 4096, 1792), (8192, 4096, 1024),
                       (8192, 8192, 1024)]:
         S = 64
@@ -62,10 +62,10 @@ def main():
         out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
         out2 = torch.empty_like(out)
         gplan = fo.Plan(coll="nocomm", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1)
-        dur = timeit(lambda: fo.gemm_stage(gplan, A, Bt, out), iters=10, flush=flush)
+        dur = timeit_pre(lambda: fo.gemm_stage(gplan, A, Bt, out), flush, iters=10)
         probe = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
                         ar_layout="rowband", post="add_rmsnorm")
-        norm_us = timeit(lambda: fo.post_stage(probe, out, out2, res, gam), iters=10, flush=flush)
+        norm_us = timeit_pre(lambda: fo.post_stage(probe, out, out2, res, gam), flush, iters=10)
         # in-situ offline stage (PAPER.md:498 (3), resource contention): the
         # comm-stream work of a group measured inside an overlapped run, on the
         # SMs the GEMM leaves free (group timestamps of the groups that overlap it)
@@ -83,33 +83,50 @@ def main():
         per_byte = statistics.median(costs) / band_bytes
         curve = tuner.effective_curve(ctx.sample_curve("allreduce", [1 << s for s in range(18, 28)], iters=3),
                                       per_byte if MODE == "insitu" else norm_us / (M * N * 2))
+        # R42: group 0's band post measured beside the GEMM (groups (g, T-g))
+        icurve = tuner.insitu_curve(ctx, dict(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S,
+                                              swizzle=1, ar_layout="rowband", post="add_rmsnorm"),
+                                    A, Bt, out, T, S, 256 * 256 * 2, curve, run_args=(res, gam))
         rows = []
         for G in candidates(T, 24, M + K):
             plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
                            group_waves=G, ar_layout="rowband", post="add_rmsnorm")
             pred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, curve)
-            meas = timeit(lambda: fo.run(ctx, plan, A, Bt, out, res, gam), iters=8, flush=flush)
+            ipred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, icurve)
+            meas = timeit_pre(lambda: fo.run(ctx, plan, A, Bt, out, res, gam), flush)
             rows.append((G, pred, meas))
             errs.append(abs(meas - pred) / meas)
+            ierrs.append(abs(meas - ipred) / meas)
+        ipick, _ = fo.tune_search(dur, tiles, S, 256 * 256 * 2, icurve)
+        iplan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
+                        group_waves=list(ipick), ar_layout="rowband", post="add_rmsnorm")
+        ipick_meas = timeit_pre(lambda: fo.run(ctx, iplan, A, Bt, out, res, gam), flush)
         best_meas = min(r[2] for r in rows)
         pick, pick_pred = fo.tune_search(dur, tiles, S, 256 * 256 * 2, curve)
         pplan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
                         group_waves=list(pick), ar_layout="rowband", post="add_rmsnorm")
-        pick_meas = timeit(lambda: fo.run(ctx, pplan, A, Bt, out, res, gam), iters=8, flush=flush)
+        pick_meas = timeit_pre(lambda: fo.run(ctx, pplan, A, Bt, out, res, gam), flush)
         ratios.append(best_meas / pick_meas)
+        iratios.append(best_meas / ipick_meas)
         one = [r for r in rows if r[0] == [1] * T]
         print(f"[{MODE}] {M}x{N}x{K} T={T} gemm {dur:.1f} us, norm pass {norm_us:.1f} us standalone / "
               f"{per_byte * M * N * 2:.1f} us in situ, {len(rows)} partitions: "
               f"mean |err| {100 * statistics.mean(abs(m - p) / m for _, p, m in rows):.2f}%, "
               f"search picks {list(pick)} -> {pick_meas:.1f} us vs measured optimum {best_meas:.1f} us "
               f"({100 * best_meas / pick_meas:.1f}%)"
-              + (f"; one-wave groups {one[0][2]:.1f} us" if one else ""), flush=True)
+              + (f"; one-wave groups {one[0][2]:.1f} us" if one else "")
+              + f"; in-situ curve: error mean {100 * statistics.mean(ierrs[-len(rows):]):.2f}%, picks {list(ipick)} -> "
+              f"{ipick_meas:.1f} us ({100 * best_meas / ipick_meas:.1f}%)", flush=True)
         del A, Bt, res, out, out2
         torch.cuda.empty_cache()
     e = sorted(errs)
     print(f"[{MODE}] ALL: {len(errs)} (shape, partition) cases, prediction error mean {100 * statistics.mean(e):.2f}%, "
           f"median {100 * e[len(e) // 2]:.2f}%, p90 {100 * e[int(0.9 * len(e))]:.2f}%, max {100 * e[-1]:.2f}%; "
           f"searched / optimum: min {100 * min(ratios):.1f}%, mean {100 * statistics.mean(ratios):.1f}%")
+    e = sorted(ierrs)
+    print(f"[{MODE}] ALL with the in-situ curve (R42): prediction error mean {100 * statistics.mean(e):.2f}%, "
+          f"median {100 * e[len(e) // 2]:.2f}%, p90 {100 * e[int(0.9 * len(e))]:.2f}%, max {100 * e[-1]:.2f}%; "
+          f"searched / optimum: min {100 * min(iratios):.1f}%, mean {100 * statistics.mean(iratios):.1f}%")
     ctx.close()
 
 
