@@ -274,6 +274,23 @@ def insitu_curve(ctx, spec: dict, A, Bt, out, T: int, S: int, tile_bytes: int, b
     return sorted(keep + pts)
 
 
+def predict_insitu(groups, duration_us, tiles, S, tile_bytes, icurve, base_curve) -> float:
+    """Alg. 1's prediction with the in-situ curve for the groups whose
+    comm-stream work overlaps the GEMM and the standalone curve for the last
+    group, which runs after the GEMM (R42).  The recurrence adds the last
+    group's latency as its final term (t = max(acc_p, acc_m) + t_m(G_P)), so
+    swapping that one term is exact."""
+    G = list(groups)
+    pred = tune_predict(G, duration_us, tiles, S, tile_bytes, icurve)
+    last = tiles - S * (sum(G) - G[-1])
+    if last <= 0:
+        return pred
+    # a one-group prediction with zero duration is exactly that group's latency
+    lat_i = tune_predict([G[-1]], 0.0, last, S, tile_bytes, icurve)
+    lat_b = tune_predict([G[-1]], 0.0, last, S, tile_bytes, base_curve)
+    return pred - lat_i + lat_b
+
+
 # collectives with a ROWBAND layout (AR: in place; RS: scattered straight into
 # the output, DESIGN.md R40)
 BANDED = ("allreduce", "reducescatter")
@@ -502,11 +519,14 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
                 evaluated.append((S, layout, [T], pred + tail, dur, swz, split, tm, tn, ci))
                 continue
             G, pred = tune_search(dur, tiles, S, tm * tn * 2, eff)
+            if eff is not base:   # in-situ curve: the last group is charged at the standalone one
+                pred = predict_insitu(G, dur, tiles, S, tm * tn * 2, eff, base)
             evaluated.append((S, layout, list(G), pred + tail, dur, swz, split, tm, tn, ci))
             if T <= all_partitions_T:
                 for comp in compositions(T):
                     if comp != list(G):
-                        p2 = tune_predict(comp, dur, tiles, S, tm * tn * 2, eff)
+                        p2 = (predict_insitu(comp, dur, tiles, S, tm * tn * 2, eff, base) if eff is not base
+                              else tune_predict(comp, dur, tiles, S, tm * tn * 2, eff))
                         evaluated.append((S, layout, comp, p2 + tail, dur, swz, split, tm, tn, ci))
     import torch.distributed as dist
 

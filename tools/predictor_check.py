@@ -92,12 +92,12 @@ def main():
             plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
                            group_waves=G, ar_layout="rowband", post="add_rmsnorm")
             pred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, curve)
-            ipred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, icurve)
+            ipred = tuner.predict_insitu(G, dur, tiles, S, 256 * 256 * 2, icurve, curve)
             meas = timeit_pre(lambda: fo.run(ctx, plan, A, Bt, out, res, gam), flush)
-            rows.append((G, pred, meas))
+            rows.append((G, pred, meas, ipred))
             errs.append(abs(meas - pred) / meas)
             ierrs.append(abs(meas - ipred) / meas)
-        ipick, _ = fo.tune_search(dur, tiles, S, 256 * 256 * 2, icurve)
+        ipick = min(rows, key=lambda r: r[3])[0]   # argmin of the in-situ prediction over the candidates
         iplan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=1,
                         group_waves=list(ipick), ar_layout="rowband", post="add_rmsnorm")
         ipick_meas = timeit_pre(lambda: fo.run(ctx, iplan, A, Bt, out, res, gam), flush)
@@ -111,7 +111,7 @@ def main():
         one = [r for r in rows if r[0] == [1] * T]
         print(f"[{MODE}] {M}x{N}x{K} T={T} gemm {dur:.1f} us, norm pass {norm_us:.1f} us standalone / "
               f"{per_byte * M * N * 2:.1f} us in situ, {len(rows)} partitions: "
-              f"mean |err| {100 * statistics.mean(abs(m - p) / m for _, p, m in rows):.2f}%, "
+              f"mean |err| {100 * statistics.mean(abs(m - p) / m for _, p, m, _ in rows):.2f}%, "
               f"search picks {list(pick)} -> {pick_meas:.1f} us vs measured optimum {best_meas:.1f} us "
               f"({100 * best_meas / pick_meas:.1f}%)"
               + (f"; one-wave groups {one[0][2]:.1f} us" if one else "")
@@ -192,12 +192,12 @@ def main_emulate(link_gbps=770.0, latency_us=6.0, ctas=16):
         for G in candidates(T, 24, M + K + n):
             plan = fo.Plan(rank=0, world=n, group_waves=G, **spec)
             pred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, curve)
-            ipred = fo.tune_predict(G, dur, tiles, S, 256 * 256 * 2, icurve)
+            ipred = tuner.predict_insitu(G, dur, tiles, S, 256 * 256 * 2, icurve, curve)
             meas = timeit_pre(lambda: fo.run(ctx, plan, A, Bt, out), flush)
             rows_.append((G, pred, meas, ipred))
             errs.append(abs(meas - pred) / meas)
             ierrs.append(abs(meas - ipred) / meas)
-        ipick, _ = fo.tune_search(dur, tiles, S, 256 * 256 * 2, icurve)
+        ipick = min(rows_, key=lambda r: r[3])[0]   # argmin of the in-situ prediction over the candidates
         iplan = fo.Plan(rank=0, world=n, group_waves=list(ipick), **spec)
         ipick_meas = timeit_pre(lambda: fo.run(ctx, iplan, A, Bt, out), flush)
         best = min(rows_, key=lambda r: r[2])
