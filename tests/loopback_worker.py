@@ -179,6 +179,19 @@ def main(W):
         each(lambda r: fo.run_sequential(ctxs[r], plans[r], Ad[r], Bd[r], seq[r], stream=streams[r]))
         for r in range(W):
             check(f"alltoall/{layout}/sequential/rank{r}", seq[r], want[r])
+        # the MoE combine as the post pass (R31): top-2 with weights 1 and 0
+        # over a permutation of the A2A output rows — the combined rows are the
+        # A2A rows in the permuted order, exactly (fp32 1*x + 0*y, one rounding)
+        perms = [np.random.default_rng(50 + r).permutation(p.info["out_rows"]).astype(np.int32) for r, p in
+                 enumerate(plans)]
+        idxs = [torch.from_numpy(np.stack([pm, pm[::-1].copy()], 1)).cuda() for pm in perms]
+        ws = [torch.tensor([[1.0, 0.0]], device="cuda").repeat(len(pm), 1).contiguous() for pm in perms]
+        comb = [torch.full((len(pm), N), float("nan"), dtype=torch.bfloat16, device="cuda") for pm in perms]
+        torch.cuda.synchronize()
+        for _ in range(2):
+            each(lambda r: fo.run_combine(ctxs[r], plans[r], Ad[r], Bd[r], comb[r], idxs[r], ws[r], stream=streams[r]))
+        for r in range(W):
+            check(f"alltoall/{layout}/combine/rank{r}", comb[r], want[r][perms[r]])
         for p in plans:
             p.close()
     for c in ctxs:
