@@ -79,7 +79,7 @@ def _gloo_exec(calls, bufs, rank, world):
         i += 1
 
 
-def _worker(rank, port, coll, errq, WORLD=2):
+def _worker(rank, port, coll, errq, WORLD=2, layout="slot"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -96,13 +96,19 @@ def _worker(rank, port, coll, errq, WORLD=2):
             tiles = (M // 128) * (N // BN)
             S = 2
             T = (tiles + S - 1) // S
-            spec = dict(coll="alltoall", m=M, n=N, k=64, tile_n=BN, workers=S, swizzle=2,
-                        group_waves=[1, T - 1], row_dst=rds[rank])
+            if layout == "rowband":   # raster, one tile-row per wave (R41)
+                S = N // BN
+                T = (tiles + S - 1) // S
+            spec = dict(coll="alltoall", m=M, n=N, k=64, tile_n=BN, workers=S, swizzle=2 if layout == "slot" else 1,
+                        group_waves=[1, T - 1], row_dst=rds[rank], ar_layout=layout)
         else:
             M = 512
             spec = dict(coll=coll, m=M, n=N, k=64, tile_n=BN, workers=3, swizzle=2, group_waves=[1, 1, 1],
                         ar_layout="slot")
+            if layout == "rowband":   # raster, one tile-row per wave (H11a / R40)
+                spec.update(workers=N // BN, swizzle=1, group_waves=[1, 1, 2], ar_layout="rowband")
         plan = fodist.make_plan(**spec)
+        assert plan.info["ar_layout"] == (1 if layout == "rowband" else 0)
         A, Bt = _inputs(WORLD, rank, M, N, K)
         Y = A @ Bt.T
         send = np.zeros(plan.info["send_elems"])
@@ -110,8 +116,14 @@ def _worker(rank, port, coll, errq, WORLD=2):
         recv = np.zeros(plan.info["recv_elems"])
         # the plan's own communication schedule (fo_plan_export_calls, what
         # fo_run issues on NCCL), driven through gloo's collectives and
-        # point-to-point messages
-        _gloo_exec(plan.export_calls(0), {"send": send, "recv": recv, "out": None}, rank, WORLD)
+        # point-to-point messages; ROWBAND AR reduces C in place and RS
+        # scatters into `out` (both the output layout)
+        bufs = {"send": send, "recv": recv, "out": None}
+        if layout == "rowband" and coll == "allreduce":
+            bufs = {"send": None, "recv": None, "out": send}
+        elif layout == "rowband" and coll == "reducescatter":
+            bufs = {"send": send, "recv": None, "out": recv}
+        _gloo_exec(plan.export_calls(0), bufs, rank, WORLD)
         if coll == "allreduce":
             recv = send
         out = recv[plan.export_recv_map()].reshape(plan.info["out_rows"], N)
@@ -142,13 +154,14 @@ def _worker(rank, port, coll, errq, WORLD=2):
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("coll", ["allreduce", "reducescatter", "alltoall"])
-def test_multi_rank_plan_contract(coll, world):
+@pytest.mark.parametrize("layout", ["slot", "rowband"])
+def test_multi_rank_plan_contract(coll, world, layout):
     from paper_2504_19519_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, coll, errq, world)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, port, coll, errq, world, layout)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
