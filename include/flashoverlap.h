@@ -329,7 +329,8 @@ fo_status fo_ctx_time_collective(fo_ctx ctx, int32_t coll, int64_t bytes, int32_
  *   out[t] = sum_{i<topk} w[t*topk+i] * X[idx[t*topk+i]]  (+ residual[t])
  * where X is this rank's standard A2A output (the rows fo_run would write,
  * grouped by source rank ascending, then source row ascending) — read straight
- * from the receive buffer through the plan's map, never materialised.
+ * from the receive buffer through the plan's map, never materialised (a
+ * ROWBAND plan receives in the output layout into the library's buffer).
  *   plan: an FO_ALLTOALL plan with post = FO_POST_NONE;
  *   idx  device int32 [tokens, topk]: row of X for each (token, slot); a value
  *        < 0 or >= info.out_rows is a dropped slot (contributes nothing);
@@ -360,7 +361,9 @@ fo_status fo_combine_stage(fo_plan plan, const void* recv, void* out, const int3
  *   residual (FO_POST_ADD*): device bf16, same shape as out; gamma (RMSNorm): device bf16 [n].
  * Internals: counters reset, GEMM on the caller stream, per group a
  * stream-side wait (counter >= |G_j|) then the NCCL call on the comm stream,
- * post-reorder, join back to `stream`; the last group's collective follows
+ * post-reorder (none for ROWBAND plans: the AR reduces `out` in place, the RS
+ * and the A2A receives write `out` directly, so `out` is written by NCCL),
+ * join back to `stream`; the last group's collective follows
  * the GEMM on `stream` itself (FO_OPT_LAST_GROUP_IN_ORDER, default), and a
  * single group then needs no counters, signals or fork at all (GEMM ->
  * collective).  Errors: FO_ERR_STATE when the plan's rank/world differ from
