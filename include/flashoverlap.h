@@ -248,8 +248,9 @@ typedef struct {
 } fo_ctx_config;
 fo_status fo_ctx_create_config(int32_t device, int32_t rank, int32_t world, const uint8_t uid[128],
                                const fo_ctx_config* config, fo_ctx* out);
-/* Device memory for a caller buffer NCCL will read / write (e.g. the `out` of
- * an AllReduce ROWBAND plan, reduced in place): ncclMemAlloc, registered with
+/* Device memory for a caller buffer NCCL will read / write (the `out` of a
+ * ROWBAND plan: AllReduce reduces it in place, ReduceScatter and the A2A
+ * receives write it): ncclMemAlloc, registered with
  * the context's communicator per its `buffers` mode (none for mode 0).
  * fo_mem_free deregisters and frees (synchronises the device).  Window
  * registration (mode 2) is collective: every rank allocates the same size in
@@ -494,8 +495,8 @@ fo_status fo_plan_set_debug(fo_plan plan, unsigned long long* tile_ts, unsigned 
  *  FO_OPT_HOST_PIPELINE 7 — bit 0: fo_run_host copies a host A in ~8 chunks of
  *                      whole tile-rows on its own stream, each chunk released to
  *                      the GEMM by a stream write the TMA producer waits on (the
- *                      GEMM starts on the first chunk); bit 1: (AR ROWBAND) each
- *                      group's rows are copied to the host right after its
+ *                      GEMM starts on the first chunk); bit 1: (AR / RS ROWBAND)
+ *                      each group's output rows are copied to the host right after its
  *                      collective; bit 2 (with bit 0): two device staging sets
  *                      used by alternate calls, so a call's H2D overlaps the
  *                      previous call's GEMM, collectives and D2H; 0 — whole-
