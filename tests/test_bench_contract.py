@@ -51,3 +51,21 @@ def test_gpu_arm_contract():
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 8])
+def test_gpu_arm_n_gt_1_code_paths_emulated(n):
+    """bench.py's N>1 code paths (tuner across two CTA caps with in-situ
+    curves, the sequential baseline at its own wave width on an uncapped
+    communicator, e2e, perfect-overlap bound, max-over-ranks plumbing) run on
+    one GPU with --emulate-world (the emulated-link evaluation backend, R42);
+    the line says so in `data`.  Only the real multi-GPU run (torchrun, NCCL)
+    measures NVLink."""
+    d = _run(["--emulate-world", str(n), "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-shards"], 1200)
+    assert BASE_KEYS <= set(d)
+    assert d["n_gpus"] == n and d["value"] > 0 and "EMULATED" in d["data"]
+    assert d["config"]["tp"] == n and d["config"]["K_loc"] == 14336 // n
+    assert d["sequential_us"] > 0 and d["layer_roofline"]["allreduce_ring_us"] > 0
+    assert d["nccl_allreduce_uncapped"]["points"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 4096 * (14336 // n) * 2
