@@ -687,6 +687,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         };
         const bool has_own = me < NC;
+        // the worker's previous tile may have left TMA stores reading the staging
+        if (p.tma_store) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
 #pragma unroll 1
         for (int c = 0; c < NC; ++c) {
           if (c % f == me) continue;
@@ -896,10 +901,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-        // TMA store (row-major C / AR slot, whole tiles): the staging buffer
-        // must be read out by the previous chunk's store before it is refilled
+        // TMA store (row-major C / AR slot / RS bands, whole tiles): the
+        // staging buffer must be read out by the previous chunk's store (also
+        // the previous tile's, for an owner's 16-byte path) before it is
+        // refilled.  (A second staging buffer per warp, letting chunk c fill
+        // one while chunk c-1's store reads the other, measured no faster:
+        // profiles/r02_epilogue_ab.txt)
         const bool tma = p.tma_store && !owner;
-        if (tma) {
+        if (p.tma_store) {
           if (lane == 0) bulk_wait_read0();
           __syncwarp();
         }
