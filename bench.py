@@ -404,8 +404,11 @@ def main():
         nctx = ctx
     else:
         shapes = [(BM, BN), (128, 256)]      # CTA-pair 256x256 and single-CTA 128x256 tiles
-        ch = fot.tune_layer(M, N, K, ctxs, "allreduce", "none", device=local, tile_shapes=shapes)
-        chn = fot.tune_layer(M, N, K, ctxs, "allreduce", "add_rmsnorm", device=local, tile_shapes=shapes)
+        # the uncapped communicator too: a single group overlaps nothing and
+        # runs best as the sequential plan (all SMs, NCCL's default CTAs)
+        tune_ctxs = ctxs + ([ctx_seq] if ctx_seq is not ctx else [])
+        ch = fot.tune_layer(M, N, K, tune_ctxs, "allreduce", "none", device=local, tile_shapes=shapes)
+        chn = fot.tune_layer(M, N, K, tune_ctxs, "allreduce", "add_rmsnorm", device=local, tile_shapes=shapes)
         if rank == 0:
             for name, c in (("plain", ch), ("fused", chn)):
                 for cand in c.candidates[:6]:
@@ -414,7 +417,7 @@ def main():
                           file=sys.stderr)
         S, groups, pred = ch.workers, tuple(ch.groups), ch.predicted_us
         curve_bw = ch.curve
-        ctx, nctx = ctxs[ch.ctx_index], ctxs[chn.ctx_index]   # the communicators the tuner chose
+        ctx, nctx = tune_ctxs[ch.ctx_index], tune_ctxs[chn.ctx_index]   # the communicators the tuner chose
         spec, nspec, pred_n = ch.spec(M, N, K, "allreduce"), chn.spec(M, N, K, "allreduce", "add_rmsnorm"), \
             chn.predicted_us
     # the chosen tile shape (tune_layer searches it; the explicit --workers /
@@ -741,9 +744,7 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if ctx_seq is not ctx:
-        ctx_seq.close()
-    for c in ctxs:
+    for c in {id(x): x for x in ctxs + [ctx_seq]}.values():   # every distinct context once
         c.close()
     if use_dist:
         dist.destroy_process_group()

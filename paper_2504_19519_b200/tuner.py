@@ -458,19 +458,27 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         tiles = (M // tm) * Nt
         cg = max(1, tm // 128)
         cands = candidate_workers(tiles, Nt, sms, coll, cg)
+        full = set()
         if world > 1:
             # the collective's kernels need SMs the persistent GEMM leaves free
             # (Alg. 1 line 3); without them nothing overlaps.  Each context's
             # widest S that leaves its CTAs their SMs is a candidate too
-            cands = sorted(set(cands) | {(sms - max(min_comm_sms, c)) // cg for c in caps})
+            allc = set(cands)
+            cands = sorted(allc | {(sms - max(min_comm_sms, c)) // cg for c in caps})
             cands = [c for c in cands if c >= 1 and any(ctx_ok(ci, c, cg) for ci in range(len(ctxs)))] \
                 or [min(cands)]
+            # a single group overlaps nothing: the whole GEMM, then the
+            # collective with every SM — so the wave widths that leave NCCL no
+            # SMs are candidates for it alone, on any context (the plan is then
+            # the sequential one and the tuner never picks worse than it)
+            full = {c for c in allc if c not in cands}
+            cands = sorted(set(cands) | full)
         for S in cands:
             T = -(-tiles // S)
             for layout in layouts:
                 # multi-group ROWBAND needs waves of whole tile-rows; one group of
                 # every tile is a band (the whole output) for any S and order
-                single_only = layout == "rowband" and S % Nt != 0
+                single_only = (layout == "rowband" and S % Nt != 0) or S in full
                 swz = 1 if (layout == "rowband" and not single_only) else 0
                 probe = Plan(coll=coll, m=M, n=N, k=K, tile_m=tm, tile_n=tn, workers=S, swizzle=swz,
                              group_waves=[T], ar_layout=layout if layout != "auto" else "auto", rank=ctx.rank,
@@ -509,7 +517,7 @@ def tune_layer(M, N, K, ctx, coll="allreduce", post="none", tile_m=TILE_M, tile_
         per_group = post_us(layout if layout != "auto" else "slot", per_group_op, tm, tn) / out_bytes
         tail = post_us("slot", post, tm, tn) if (layout != "rowband" and norm) else 0.0
         for ci in range(len(ctxs)):
-            if not ctx_ok(ci, S, max(1, tm // 128)):
+            if not single_only and not ctx_ok(ci, S, max(1, tm // 128)):
                 continue
             # (a single group does not overlap the GEMM: the standalone curve)
             base = effective_curve(curves[ci], per_group)

@@ -49,12 +49,15 @@ def main():
     for n in [int(x) for x in args.n.split(",")]:
         ctx = fo.Context.emulated(0, 0, n, args.gbps, args.lat, 16)
         ctx.nccl_max_ctas = 16
+        ctx_u = fo.Context.emulated(0, 0, n, args.gbps, args.lat, 32)   # "uncapped": NCCL's default CTAs
+        ctx_u.nccl_max_ctas = 0
+        ctxs = [ctx, ctx_u]
         for coll in args.colls.split(","):
             for nk in [int(x) for x in args.nk.split(",")]:
                 for M in [int(x) for x in args.ms.split(",")]:
                     N = K = nk
                     A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.cell_seed(M, N, K), device="cuda")
-                    ch = tuner.tune_layer(M, N, K, ctx, coll, "none", device=0, iters=3, verify=4,
+                    ch = tuner.tune_layer(M, N, K, ctxs, coll, "none", device=0, iters=3, verify=4,
                                           tile_shapes=[(256, 256), (128, 256)])
                     plan = fo.Plan(rank=0, world=n, **ch.spec(M, N, K, coll))
                     out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
@@ -65,19 +68,20 @@ def main():
                     seq = fo.Plan(rank=0, world=n, coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=S_seq,
                                   swizzle=0, group_waves=[T_seq], ar_layout="auto",
                                   options={"tail_split": -1} if 0 < R and 2 * R <= S_seq else None)
-                    t_ov, t_seq = interleaved([lambda: fo.run(ctx, plan, A, Bt, out),
-                                               lambda: fo.run_sequential(ctx, seq, A, Bt, out)], flush, iters=5)
+                    t_ov, t_seq = interleaved([lambda: fo.run(ctxs[ch.ctx_index], plan, A, Bt, out),
+                                               lambda: fo.run_sequential(ctx_u, seq, A, Bt, out)], flush, iters=5)
                     fac = 2.0 * (n - 1) / n if coll == "allreduce" else (n - 1) / n
                     roof = max(2.0 * M * N * K / (peak * 1e6), args.lat + fac * M * N * 2 / (args.gbps * 1e3))
                     cells += 1
                     wins += t_ov < t_seq
                     fracs.append(roof / t_ov)
                     print(f"{coll:13s} n={n} {M:5d}x{N:5d}x{K:5d}: overlapped {t_ov:9.1f} us ({ch.tile_m}x{ch.tile_n} "
-                          f"S={ch.workers} {ch.layout} groups {ch.groups} ts={ch.tail_split}), sequential {t_seq:9.1f} us, "
+                          f"S={ch.workers} {ch.layout} groups {ch.groups} ts={ch.tail_split} ctx{ch.ctx_index}), sequential {t_seq:9.1f} us, "
                           f"speedup {t_seq / t_ov:.3f}, roofline {roof:8.1f} us = {roof / t_ov:.2f}", flush=True)
                     del A, Bt, out
                     torch.cuda.empty_cache()
         ctx.close()
+        ctx_u.close()
     fracs.sort()
     print(f"# {cells} cells: overlapped faster than sequential in {wins}; fraction of the layer roofline: "
           f"median {fracs[len(fracs) // 2]:.2f}, min {fracs[0]:.2f}, max {fracs[-1]:.2f}", flush=True)
