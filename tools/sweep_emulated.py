@@ -44,7 +44,7 @@ def main():
     sms = fo.device_sm_count(0)
     print(f"# EMULATED link {args.gbps} GB/s per direction, {args.lat} us latency, 16 CTAs per call (R42); "
           f"GEMM peak {peak} TF/s (MEASURED_PEAKS.json)", flush=True)
-    wins, cells = 0, 0
+    wins, ties, cells = 0, 0, 0
     fracs = []
     for n in [int(x) for x in args.n.split(",")]:
         ctx = fo.Context.emulated(0, 0, n, args.gbps, args.lat, 16)
@@ -73,7 +73,8 @@ def main():
                     fac = 2.0 * (n - 1) / n if coll == "allreduce" else (n - 1) / n
                     roof = max(2.0 * M * N * K / (peak * 1e6), args.lat + fac * M * N * 2 / (args.gbps * 1e3))
                     cells += 1
-                    wins += t_ov < t_seq
+                    wins += t_ov < 0.99 * t_seq
+                    ties += 0.99 * t_seq <= t_ov <= 1.01 * t_seq
                     fracs.append(roof / t_ov)
                     print(f"{coll:13s} n={n} {M:5d}x{N:5d}x{K:5d}: overlapped {t_ov:9.1f} us ({ch.tile_m}x{ch.tile_n} "
                           f"S={ch.workers} {ch.layout} groups {ch.groups} ts={ch.tail_split} ctx{ch.ctx_index}), sequential {t_seq:9.1f} us, "
@@ -83,7 +84,8 @@ def main():
         ctx.close()
         ctx_u.close()
     fracs.sort()
-    print(f"# {cells} cells: overlapped faster than sequential in {wins}; fraction of the layer roofline: "
+    print(f"# {cells} cells: overlapped faster than sequential (by > 1%) in {wins}, within 1% in {ties}, slower in "
+          f"{cells - wins - ties}; fraction of the layer roofline: "
           f"median {fracs[len(fracs) // 2]:.2f}, min {fracs[0]:.2f}, max {fracs[-1]:.2f}", flush=True)
 
 
