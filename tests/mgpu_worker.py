@@ -49,7 +49,8 @@ def main():
     bad = []
     M, N, K = 2048, 1024, 512                   # 256x256 pairs: 8x4 tiles; S = 8 -> 4 waves
     for coll, layout, groups in (("allreduce", "slot", [1, 2, 1]), ("allreduce", "rowband", [1, 1, 2]),
-                                 ("allreduce", "rowband", [4]), ("reducescatter", "auto", [2, 1, 1])):
+                                 ("allreduce", "rowband", [4]), ("reducescatter", "slot", [2, 1, 1]),
+                                 ("reducescatter", "rowband", [1, 1, 2])):
         A, Bt = exact_inputs(M, N, K, rank, world, 11)
         spec = dict(coll=coll, m=M, n=N, k=K, tile_m=256, tile_n=256, workers=8,
                     swizzle=1 if layout == "rowband" else 2, group_waves=groups, ar_layout=layout)
@@ -113,18 +114,13 @@ def main():
     dist.all_reduce(probe)
     if probe.item() != world:
         bad.append("process group after borrowed-context destroy")
-    # All-to-All (EP combine): imbalanced experts, random routing
+    # All-to-All (EP combine): imbalanced experts, random routing; the paper's
+    # subtoken pools and the ROWBAND rows received straight into `out` (R41)
     rng = np.random.default_rng(7)
-    Ms = [256 * int(rng.integers(1, 5)) for _ in range(world)]
+    Ms = [256 * int(rng.integers(2, 5)) for _ in range(world)]    # >= 2 tile-rows: two one-row waves
     rds = [np.random.default_rng(100 + s).integers(0, world, size=Ms[s]).astype(np.int32) for s in range(world)]
     Me = Ms[rank]
     A, Bt = exact_inputs(Me, N, K, rank, world, 23)
-    tiles = (Me // 256) * (N // 256)
-    S = 2
-    T = -(-tiles // S)
-    spec = dict(coll="alltoall", m=Me, n=N, k=K, tile_m=256, tile_n=256, workers=S, swizzle=2,
-                group_waves=[1, T - 1], row_dst=rds[rank])   # T >= 2 on every rank: the same P = 2
-    plan = fodist.make_plan(**spec)
     C = (A.float() @ Bt.float().t()).to(torch.bfloat16)
     # plain A2A: rows with dst d go to rank d, source-major then row-major
     send = [C[torch.from_numpy(rds[rank] == d).cuda()] for d in range(world)]
@@ -134,15 +130,23 @@ def main():
     recv = [torch.empty(int(c.item()), N, dtype=torch.bfloat16, device="cuda") for c in recv_counts]
     dist.all_to_all(recv, send)
     want = torch.cat(recv, 0)
-    out = torch.full((plan.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda")
-    for _ in range(3):
-        fo.run(ctx, plan, A, Bt, out)
-    torch.cuda.synchronize()
-    check("alltoall", out, want, bad)
-    seq = torch.full_like(out, float("nan"))
-    fo.run_sequential(ctx, plan, A, Bt, seq)     # unsorted row_dst: one message per run of a destination
-    torch.cuda.synchronize()
-    check("alltoall/sequential", seq, want, bad)
+    tiles = (Me // 256) * (N // 256)
+    for layout in ("slot", "rowband"):
+        S = 2 if layout == "slot" else N // 256
+        T = -(-tiles // S)
+        spec = dict(coll="alltoall", m=Me, n=N, k=K, tile_m=256, tile_n=256, workers=S,
+                    swizzle=2 if layout == "slot" else 1, group_waves=[1, T - 1], row_dst=rds[rank],
+                    ar_layout=layout)   # T >= 2 on every rank: the same P = 2
+        plan = fodist.make_plan(**spec)
+        out = torch.full((plan.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda")
+        for _ in range(3):
+            fo.run(ctx, plan, A, Bt, out)
+        torch.cuda.synchronize()
+        check(f"alltoall/{layout}", out, want, bad)
+        seq = torch.full_like(out, float("nan"))
+        fo.run_sequential(ctx, plan, A, Bt, seq)     # unsorted row_dst: one message per run of a destination
+        torch.cuda.synchronize()
+        check(f"alltoall/{layout}/sequential", seq, want, bad)
     ok = torch.tensor([0 if not bad else 1], device="cuda")
     dist.all_reduce(ok)
     ctx.close()
