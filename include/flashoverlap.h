@@ -107,7 +107,10 @@ typedef struct {
   int32_t workers;       /* S >= 1 = concurrent tile workers = wave width (grid of the persistent GEMM) */
   const int32_t* tile_order; /* [tiles] permutation of tile ids, or NULL => default swizzle */
   int32_t swizzle;       /* default order: row-panels of `swizzle` tile-rows, column-major inside (R1);
-                            0 = auto: the panel height minimising the tile-rows + tile-columns one wave touches */
+                            0 = auto: the panel height minimising the tile-rows + tile-columns the waves touch,
+                            summed over all waves (the operand panels streamed from HBM; R25), or the Hilbert
+                            order when that is 5% lower (and no band layout needs panels); -1 = a generalized
+                            Hilbert curve over the tile grid (R44) */
   int32_t num_groups;    /* P */
   const int32_t* group_waves; /* [P] wave counts, sum == T = ceil(tiles / S); NULL => one group */
   const int32_t* row_dst;     /* All-to-All: [m] destination rank of each output row */

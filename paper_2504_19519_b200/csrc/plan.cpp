@@ -18,18 +18,80 @@ std::vector<int32_t> default_order(int Mt, int Nt, int s) {
   return o;
 }
 
-static long wave_footprint(int Mt, int Nt, int S, int s) {
-  // tile-rows + tile-columns touched by one wave of S consecutive positions
-  const long panel = (long)s * Nt;
-  long rows, cols;
-  if (S <= panel) {
-    cols = std::min<long>(Nt, (S + s - 1) / s);
-    rows = std::min<long>(s, S);
-  } else {
-    cols = Nt;
-    rows = std::min<long>(Mt, (long)s * ((S + panel - 1) / panel));
+// Generalized Hilbert curve over a w x h rectangle (any sizes; R44):
+// consecutive positions are neighbouring tiles, so any run of S positions —
+// a wave — covers a compact region and touches few tile-rows + tile-columns,
+// whatever S is (a panel order's waves straddle panel boundaries unless S is a
+// multiple of the panel size).  Recursive split of the longer side, as in
+// J. Cervený's "gilbert" construction.
+static int sgn(int v) { return (v > 0) - (v < 0); }
+static int floordiv2(int v) { return v >= 0 ? v / 2 : -((-v + 1) / 2); }
+
+static void gilbert(int x, int y, int ax, int ay, int bx, int by, int Nt, std::vector<int32_t>& out) {
+  const int w = std::abs(ax + ay), h = std::abs(bx + by);
+  const int dax = sgn(ax), day = sgn(ay), dbx = sgn(bx), dby = sgn(by);
+  if (h == 1) {
+    for (int i = 0; i < w; ++i, x += dax, y += day) out.push_back(y * Nt + x);
+    return;
   }
-  return rows + cols;
+  if (w == 1) {
+    for (int i = 0; i < h; ++i, x += dbx, y += dby) out.push_back(y * Nt + x);
+    return;
+  }
+  int ax2 = floordiv2(ax), ay2 = floordiv2(ay), bx2 = floordiv2(bx), by2 = floordiv2(by);
+  const int w2 = std::abs(ax2 + ay2), h2 = std::abs(bx2 + by2);
+  if (2 * w > 3 * h) {
+    if ((w2 & 1) && w > 2) {
+      ax2 += dax;
+      ay2 += day;
+    }
+    gilbert(x, y, ax2, ay2, bx, by, Nt, out);
+    gilbert(x + ax2, y + ay2, ax - ax2, ay - ay2, bx, by, Nt, out);
+  } else {
+    if ((h2 & 1) && h > 2) {
+      bx2 += dbx;
+      by2 += dby;
+    }
+    gilbert(x, y, bx2, by2, ax2, ay2, Nt, out);
+    gilbert(x + bx2, y + by2, ax, ay, bx - bx2, by - by2, Nt, out);
+    gilbert(x + (ax - dax) + (bx2 - dbx), y + (ay - day) + (by2 - dby), -bx2, -by2, -(ax - ax2), -(ay - ay2), Nt,
+            out);
+  }
+}
+
+std::vector<int32_t> hilbert_order(int Mt, int Nt) {
+  std::vector<int32_t> o;
+  o.reserve((size_t)Mt * Nt);
+  if (Nt >= Mt) gilbert(0, 0, Nt, 0, 0, Mt, Nt, o);   // x = tile-column, y = tile-row
+  else gilbert(0, 0, 0, Mt, Nt, 0, Nt, o);
+  return o;
+}
+
+// Tile-rows + tile-columns touched, summed over the waves of S positions.
+static long order_footprint(const std::vector<int32_t>& o, int Nt, int S) {
+  long total = 0;
+  std::vector<int> rseen, cseen;
+  for (size_t w0 = 0; w0 < o.size(); w0 += (size_t)S) {
+    rseen.clear();
+    cseen.clear();
+    for (size_t q = w0; q < std::min(o.size(), w0 + (size_t)S); ++q) {
+      rseen.push_back(o[q] / Nt);
+      cseen.push_back(o[q] % Nt);
+    }
+    std::sort(rseen.begin(), rseen.end());
+    std::sort(cseen.begin(), cseen.end());
+    total += std::unique(rseen.begin(), rseen.end()) - rseen.begin();
+    total += std::unique(cseen.begin(), cseen.end()) - cseen.begin();
+  }
+  return total;
+}
+
+// Footprint of the panel order of height s: tile-rows + tile-columns touched,
+// summed over all waves (each touched row / column is an operand panel the
+// wave streams from HBM; measured, the bench GEMM's DRAM reads follow it:
+// 82 / 75 / 71 panels -> 526 / 490 / 468 MB, profiles/r02_order_probe.txt).
+static long wave_footprint(int Mt, int Nt, int S, int s) {
+  return order_footprint(default_order(Mt, Nt, s), Nt, S);
 }
 
 int auto_swizzle(int Mt, int Nt, int S) {
@@ -126,9 +188,12 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
       if (t < 0 || t >= g.tiles || seen[t]) fail(FO_ERR_INVALID_ARG, "tile_order is not a permutation");
       seen[t] = 1;
     }
+  } else if (d.swizzle == -1) {
+    g.order = hilbert_order(g.Mt, g.Nt);  // DESIGN.md R44
   } else {
-    if (d.swizzle < 0) fail(FO_ERR_INVALID_ARG, "swizzle must be >= 0");
+    if (d.swizzle < 0) fail(FO_ERR_INVALID_ARG, "swizzle must be >= -1");
     int s = d.swizzle;
+    const bool autos = s == 0;
     if (s == 0) {
       // ROWBAND asked for: the best band-aligned panel height; AUTO (AR / RS):
       // band-aligned unless its footprint is much larger; otherwise (and
@@ -140,6 +205,20 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
               : auto_swizzle(g.Mt, g.Nt, d.workers);
     }
     g.order = default_order(g.Mt, g.Nt, s);
+    if (autos) {
+      // the generalized Hilbert order (R44) when it touches clearly fewer
+      // operand panels over all waves and no band layout depends on the
+      // panel order (one group is a band in any order; a panel height that is
+      // not aligned to the groups gives no bands either)
+      bool aligned = true;
+      for (size_t j = 1; j + 1 < g.gpos.size() && aligned; ++j) aligned = g.gpos[j] % ((long)s * g.Nt) == 0;
+      const bool band_pref = d.ar_layout != FO_LAYOUT_SLOT && d.coll != FO_NOCOMM;
+      if (!band_pref || g.P == 1 || !aligned) {
+        std::vector<int32_t> hil = hilbert_order(g.Mt, g.Nt);
+        if (20 * order_footprint(hil, g.Nt, d.workers) < 19 * order_footprint(g.order, g.Nt, d.workers))
+          g.order.swap(hil);
+      }
+    }
   }
   (void)world;
   return g;

@@ -81,6 +81,8 @@ struct PlanHost {
 
 // Default order of DESIGN.md R1: row-panels of s tile-rows, column-major inside.
 std::vector<int32_t> default_order(int Mt, int Nt, int s);
+// swizzle == -1 (R44): a generalized Hilbert curve over the tile grid.
+std::vector<int32_t> hilbert_order(int Mt, int Nt);
 // swizzle == 0: the panel height minimising the tile-rows + tile-columns one
 // wave of S touches (the operand panels that must be L2-resident together).
 int auto_swizzle(int Mt, int Nt, int S);
