@@ -67,21 +67,24 @@ std::vector<int32_t> hilbert_order(int Mt, int Nt) {
   return o;
 }
 
-// Tile-rows + tile-columns touched, summed over the waves of S positions.
+// Tile-rows + tile-columns touched, summed over the waves of S positions
+// (stamp arrays: linear in the number of tiles).
 static long order_footprint(const std::vector<int32_t>& o, int Nt, int S) {
+  int Mt = 0;
+  for (int32_t t : o) Mt = std::max(Mt, t / Nt + 1);
+  std::vector<int32_t> rstamp((size_t)Mt, -1), cstamp((size_t)Nt, -1);
   long total = 0;
-  std::vector<int> rseen, cseen;
-  for (size_t w0 = 0; w0 < o.size(); w0 += (size_t)S) {
-    rseen.clear();
-    cseen.clear();
-    for (size_t q = w0; q < std::min(o.size(), w0 + (size_t)S); ++q) {
-      rseen.push_back(o[q] / Nt);
-      cseen.push_back(o[q] % Nt);
+  for (size_t q = 0; q < o.size(); ++q) {
+    const int32_t w = (int32_t)(q / (size_t)S);
+    const int r = o[q] / Nt, c = o[q] % Nt;
+    if (rstamp[(size_t)r] != w) {
+      rstamp[(size_t)r] = w;
+      ++total;
     }
-    std::sort(rseen.begin(), rseen.end());
-    std::sort(cseen.begin(), cseen.end());
-    total += std::unique(rseen.begin(), rseen.end()) - rseen.begin();
-    total += std::unique(cseen.begin(), cseen.end()) - cseen.begin();
+    if (cstamp[(size_t)c] != w) {
+      cstamp[(size_t)c] = w;
+      ++total;
+    }
   }
   return total;
 }
