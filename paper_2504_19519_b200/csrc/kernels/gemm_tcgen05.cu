@@ -62,7 +62,7 @@ struct Cfg {
   static constexpr int BUDGET = 232448 - 1024 - EPI_BYTES - 256;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulator stages
-  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 5) + 16;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM alloc power of 2");
@@ -415,7 +415,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* lte_go = tempty + 2;  // shared last-tile epilogue: accumulator ready for warps 0-3
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4 * CG);  // one arrive per epilogue warp of each CTA of the group
     }
+    mbar_init(lte_go, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -472,6 +474,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int KB = (int)(p.K / BK);
+  constexpr int NC = BN / EPI_COLS;  // 64-column epilogue chunks per tile
+  // Shared last-tile epilogue: a worker's last unit has no successor whose
+  // MMAs hide its epilogue, and one warp per SM sub-partition stages its
+  // chunks serially (~0.5 us per 64-column chunk: TMEM load, bf16 pack,
+  // staging, store issue), so warps 0-3 — producer, MMA issuer, TMEM
+  // allocator, idle, all done by then — take the upper half of its chunks
+  // (measured: the last signal ~1 us earlier on one-wave shapes,
+  // profiles/r02_epilogue_ab.txt).  Whole tiles with the TMA-store epilogue
+  // only (split-tile parts/owners and SwiGLU keep the 4-warp path; so do
+  // multicast clusters: a partner's loads may still land in this CTA's
+  // stages, which warps 0-3 reuse as staging).  Whether the last unit is a
+  // whole tile is decided where it is needed (a split plan's segment table
+  // is cold here: reading it now would delay every warp's start).
+  const bool lte = MC == 1 && NC >= 2 && p.tma_store && p.mode != EPI_SWIGLU;
+  // one TMA box store of chunk c of rows [r0, r0 + RPW) of a tile staged in
+  // `s`: row-major C, AR slot or RS band (h >= RPW: consecutive buffer rows)
+  auto tma_chunk = [&](const uint8_t* s, int c, int pos, int ti, int tj, int r0, int2 rs) {
+    if (p.mode == EPI_SLOT) tma_store_2d(&tmC, s, c * EPI_COLS, pos * TM + r0);
+    else if (p.mode == EPI_RS_BAND)
+      tma_store_2d(&tmC, s, tj * BN + c * EPI_COLS, (int)rs_band_row<TM>(p, ti, r0, rs.x, rs.y));
+    else tma_store_2d(&tmC, s, tj * BN + c * EPI_COLS, ti * TM + r0);
+    bulk_commit();
+  };
 
   if (warp == 0) {
     // ======================= TMA producer (every CTA loads its own A rows and B rows)
@@ -667,6 +692,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                    nx_slot[it]) +
                    (lane & 7) * 8;
       mbar_wait(&tfull[acc], aphase);
+      const bool lte_tile = lte && k == nu - 1 && un.role == 0;
+      if (lte_tile && q == 0 && lane == 0) mbar_arrive(lte_go);  // accumulator ready: wake warps 0-3
       if (k + 1 < nu) prefetch_dst(my_unit(p, worker, nworkers, k + 1, KB).pos);
       tc_fence_after();
       if (p.dist_fold && p.mode != EPI_SWIGLU && (owner || part)) {
@@ -674,7 +701,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // worker's last unit, so slices may wait on each other): slice `me`
         // reduces and stores the 64-column chunks c with c % f == me and
         // publishes the fp32 partials of the others to its own slot
-        constexpr int NC = BN / EPI_COLS;
         const int f = un.nparts, me = un.idx;
         const int base = owner ? un.slot : un.slot - me + 1;  // the tile's first slot
         auto pslot = [&](int j) { return j == 0 ? base + f - 1 : base + j - 1; };
@@ -859,14 +885,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           continue;
         }
       }
+      const int c_end = lte_tile ? NC / 2 : NC;  // the shared last tile: chunks [NC/2, NC) go to warps 0-3
 #pragma unroll 1
-      for (int c = 0; c < BN / EPI_COLS; ++c) {
+      for (int c = 0; c < c_end; ++c) {
         uint32_t v[64];
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * EPI_COLS);
         tmem_ld32(taddr, v);
         tmem_ld32(taddr + 32, v + 32);
         tmem_wait_ld();
-        if (c == BN / EPI_COLS - 1) {
+        if (c == c_end - 1) {
           // accumulator fully read: hand the TMEM stage back to the MMA warp
           tc_fence_before();
           __syncwarp();
@@ -929,14 +956,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // writes made visible to the async proxy first)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) {
-            const int r0 = (int)half * RB + q * RPW;
-            if (p.mode == EPI_SLOT) tma_store_2d(&tmC, stg, c * EPI_COLS, pos * TM + r0);
-            else if (p.mode == EPI_RS_BAND)  // h >= RPW: the warp's rows are consecutive buffer rows
-              tma_store_2d(&tmC, stg, tj * BN + c * EPI_COLS, (int)rs_band_row<TM>(p, ti, r0, cur_rs.x, cur_rs.y));
-            else tma_store_2d(&tmC, stg, tj * BN + c * EPI_COLS, ti * TM + r0);
-            bulk_commit();
-          }
+          if (lane == 0) tma_chunk(stg, c, pos, ti, tj, (int)half * RB + q * RPW, cur_rs);
           continue;
         }
         __syncwarp();
@@ -964,11 +984,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // release add (a pair signals twice per tile: counters count half tiles);
       // TMA stores are complete (not just read out) and ordered before the
       // release by the async-proxy fence
-      if (p.tma_store && !owner && p.counters && lane == 0) {
+      if (p.tma_store && !owner && (p.counters || lte_tile) && lane == 0) {
         bulk_wait_all();
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // the shared last tile: warps 0-3's chunks are complete too (barrier 2)
+      if (lte_tile) asm volatile("bar.sync 2, 256;" ::: "memory");
+      else asm volatile("bar.sync 1, 128;" ::: "memory");
       if (q == 0 && lane == 0) {
         if (p.counters) red_release_add(&p.counters[p.group_of_pos[pos]], 1u);
         if (p.tile_ts && leader) p.tile_ts[pos] = globaltimer();
@@ -978,6 +1000,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         aphase ^= 1;
       }
     }
+  }
+  const int nu_all = (lte && warp < 4) ? unit_count(p, worker, nworkers) : 0;
+  const Unit last = nu_all > 0 ? my_unit(p, worker, nworkers, nu_all - 1, KB) : Unit{};
+  if (nu_all > 0 && last.role == 0) {
+    // ======================= shared last-tile epilogue, warps 0-3 (TMEM lane
+    // quarter = warp): chunks [NC/2, NC) of the worker's last tile, staged in
+    // the idle A stages — every MMA, hence every load, has completed once
+    // the accumulator is ready (lte_go: the epilogue warps saw tfull)
+    static_assert(ST * A_STAGE_BYTES >= 4 * EPI_WARP_BYTES, "staging for warps 0-3 fits the A stages");
+    __syncwarp();
+    const int q = warp;
+    const int k = nu_all - 1;
+    const int pos = last.pos;
+    const int t = p.order[pos];
+    const int ti = t / p.Nt, tj = t - ti * p.Nt;
+    const int2 rs = (p.mode == EPI_RS_BAND) ? p.rs_info[pos] : make_int2(0, 0);
+    uint8_t* hstg = sA + q * EPI_WARP_BYTES;
+    mbar_wait(lte_go, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = NC / 2; c < NC; ++c) {
+      uint32_t v[64];
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((k & 1) * BN + c * EPI_COLS);
+      tmem_ld32(taddr, v);
+      tmem_ld32(taddr + 32, v + 32);
+      tmem_wait_ld();
+      if (c > NC / 2) {
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
+      if (lane < RPW) {
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          uint4 w;
+          w.x = pack_bf16(v[8 * x + 0], v[8 * x + 1]);
+          w.y = pack_bf16(v[8 * x + 2], v[8 * x + 3]);
+          w.z = pack_bf16(v[8 * x + 4], v[8 * x + 5]);
+          w.w = pack_bf16(v[8 * x + 6], v[8 * x + 7]);
+          *stg_at(hstg, lane, x) = w;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tma_chunk(hstg, c, pos, ti, tj, (int)half * RB + q * RPW, rs);
+    }
+    if (lane == 0) {
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    tc_fence_before();
+    asm volatile("bar.sync 2, 256;" ::: "memory");
   }
   if (warp >= 4 && lane == 0 && p.tma_store) bulk_wait_all();  // the staging must outlive the stores
   tc_fence_before();

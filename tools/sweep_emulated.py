@@ -10,7 +10,7 @@ north_star asks the overlapped layer to beat the sequential one on every
 shape; this checks the schedule against that bar under the link model.
 Dev tool; prints one line per cell and a summary.
 
-    python tools/sweep_emulated.py [--ms 1024,2048,...] [--nk 4096,...] [--n 2,4,8] [--colls allreduce,reducescatter]
+    python tools/sweep_emulated.py [--ms 1024,2048,...] [--nk 4096,...] [--n 2,4,8] [--colls allreduce,reducescatter] [--tiles 256x256,128x256]
 """
 import argparse
 import json
@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--colls", default="allreduce,reducescatter")
     ap.add_argument("--gbps", type=float, default=770.0)
     ap.add_argument("--lat", type=float, default=6.0)
+    ap.add_argument("--tiles", default="256x256,128x256", help="tile shapes the tuner searches")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
@@ -44,6 +45,7 @@ def main():
     sms = fo.device_sm_count(0)
     print(f"# EMULATED link {args.gbps} GB/s per direction, {args.lat} us latency, 16 CTAs per call (R42); "
           f"GEMM peak {peak} TF/s (MEASURED_PEAKS.json)", flush=True)
+    shapes = [tuple(int(v) for v in t.split("x")) for t in args.tiles.split(",")]
     wins, ties, cells = 0, 0, 0
     fracs = []
     for n in [int(x) for x in args.n.split(",")]:
@@ -58,7 +60,7 @@ def main():
                     N = K = nk
                     A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.cell_seed(M, N, K), device="cuda")
                     ch = tuner.tune_layer(M, N, K, ctxs, coll, "none", device=0, iters=3, verify=4,
-                                          tile_shapes=[(256, 256), (128, 256)])
+                                          tile_shapes=shapes)
                     plan = fo.Plan(rank=0, world=n, **ch.spec(M, N, K, coll))
                     out = torch.empty(plan.info["out_rows"], N, dtype=torch.bfloat16, device="cuda")
                     tiles = (M // 256) * (N // 256)
