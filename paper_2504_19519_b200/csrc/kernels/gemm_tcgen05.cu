@@ -62,7 +62,7 @@ struct Cfg {
   static constexpr int BUDGET = 232448 - 1024 - EPI_BYTES - 256;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulator stages
-  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 5) + 16;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 6) + 16;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM alloc power of 2");
@@ -415,8 +415,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
-  uint64_t* lte_go = tempty + 2;  // shared last-tile epilogue: accumulator ready for warps 0-3
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
+  uint64_t* lte_go = tempty + 2;    // shared last-tile epilogue: accumulator ready for warps 0-3
+  uint64_t* lte_done = tempty + 3;  // ... and warps 0-3's stores complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -454,6 +455,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tempty[s], 4 * CG);  // one arrive per epilogue warp of each CTA of the group
     }
     mbar_init(lte_go, 1);
+    mbar_init(lte_done, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -984,14 +986,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // release add (a pair signals twice per tile: counters count half tiles);
       // TMA stores are complete (not just read out) and ordered before the
       // release by the async-proxy fence
-      if (p.tma_store && !owner && (p.counters || lte_tile) && lane == 0) {
+      if (p.tma_store && !owner && p.counters && lane == 0) {
         bulk_wait_all();
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
-      // the shared last tile: warps 0-3's chunks are complete too (barrier 2)
-      if (lte_tile) asm volatile("bar.sync 2, 256;" ::: "memory");
-      else asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       if (q == 0 && lane == 0) {
+        // the shared last tile: warps 0-3's stores are complete too (their
+        // release arrivals, acquired here, precede this thread's release)
+        if (lte_tile) mbar_wait(lte_done, 0);
         if (p.counters) red_release_add(&p.counters[p.group_of_pos[pos]], 1u);
         if (p.tile_ts && leader) p.tile_ts[pos] = globaltimer();
       }
@@ -1048,9 +1051,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       bulk_wait_all();
       asm volatile("fence.proxy.async.global;" ::: "memory");
+      mbar_arrive(lte_done);
     }
     tc_fence_before();
-    asm volatile("bar.sync 2, 256;" ::: "memory");
+    __syncwarp();
   }
   if (warp >= 4 && lane == 0 && p.tma_store) bulk_wait_all();  // the staging must outlive the stores
   tc_fence_before();
