@@ -439,6 +439,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
     }
   }
+  // Producer prologue (K-major, no multicast, a regular first unit, A
+  // resident): the first tile's row is read now and its first k-blocks are
+  // loaded right after the setup sync, in straight-line code — the main
+  // loop's first TMA otherwise issues ~1 us after the sync (the table load,
+  // then the loop's cold code path; profiles/r02_epilogue_ab.txt)
+  const bool pro = MJ == 0 && MC == 1 && p.tail_pos > worker && !p.a_ready;
+  int t_pro = 0;
+  if (pro && warp == 0 && lane == 0) t_pro = p.order[worker];  // consumed after the setup
   if (warp == 3 && lane == 0) {
     // warm L2 with the table entries the producer needs for its first TMA
     // (cold after an L2 flush) while the setup below runs; non-blocking
@@ -505,6 +513,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int kk_pro = 0;  // unit 0's k-blocks already issued by the prologue
+      if (pro) {
+        const int ti = t_pro / p.Nt, tj = t_pro - ti * p.Nt;
+        const int arow = ti * TM + (int)half * RB, brow = tj * BN + (int)half * C::B_ROWS;
+        kk_pro = min(ST, KB);
+        for (int s0 = 0; s0 < kk_pro; ++s0) {  // fresh stages: no empty wait
+          if (leader) mbar_arrive_expect_tx(&full[s0], CG * C::STAGE_BYTES);
+          if constexpr (CG == 1) {
+            tma_load_2d(sA + s0 * A_STAGE_BYTES, &tmA, s0 * BK, arow, &full[s0]);
+            tma_load_2d(sB + s0 * C::B_STAGE_BYTES, &tmB, s0 * BK, brow, &full[s0]);
+          } else {
+            const uint32_t fb = mapa_shared(&full[s0], lead_rank);
+            tma_load_2d_2sm(sA + s0 * A_STAGE_BYTES, &tmA, s0 * BK, arow, fb);
+            tma_load_2d_2sm(sB + s0 * C::B_STAGE_BYTES, &tmB, s0 * BK, brow, fb);
+          }
+        }
+        stage = kk_pro % ST;
+        phase = (kk_pro == ST) ? 1u : 0u;
+      }
       int ready_chunk = -1;
       // the first regular unit's tile is loaded independently of the segment
       // table, so the two loads overlap
@@ -547,7 +574,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           while ((int32_t)(ld_acquire(p.wave_ctr + wave - 1) - target) < 0) __nanosleep(64);
         }
         const bool rev = p.k_snake && (k & 1);
-        for (int kk = un.kb0; kk < un.kb1; ++kk) {
+        for (int kk = un.kb0 + (k == 0 ? kk_pro : 0); kk < un.kb1; ++kk) {
           const int kb = rev ? un.kb0 + un.kb1 - 1 - kk : kk;
           mbar_wait(&empty[stage], phase ^ 1);
           // K-major operand: one box [rows, 64 k]; MN-major operand: 64x64
