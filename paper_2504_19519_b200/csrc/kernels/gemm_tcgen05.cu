@@ -118,6 +118,15 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// setup barrier of a cluster: what other CTAs need from this one before
+// their first remote operation is its mbarrier initialisation, already
+// released to the cluster by fence.mbarrier_init; the TMEM address slot is
+// CTA-local (bar.sync orders it).  So the cluster arrive can be relaxed.
+__device__ __forceinline__ void cluster_setup_sync() {
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // shared::cluster address of the same object in CTA `rank` of the cluster
 __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
   uint32_t r;
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   tc_fence_before();
-  if constexpr (CG * MC == 1) __syncthreads(); else cluster_sync();
+  if constexpr (CG * MC == 1) __syncthreads(); else cluster_setup_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int KB = (int)(p.K / BK);

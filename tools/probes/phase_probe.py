@@ -1,6 +1,6 @@
-"""GEMM phase trace (dev probe; needs the instrumented build under
-tools/probes/phase/, whose kernel writes %globaltimer stamps after the
-per-tile area of the debug buffer): per stamp, the min / median / max over
+"""GEMM phase trace (dev probe; needs the instrumented build made by
+tools/probes/phase_patch.py, whose kernel writes %globaltimer stamps after
+the per-tile area of the debug buffer): per stamp, the min / median / max over
 CTAs of (stamp - first CTA's entry), median over runs, L2 flushed by a write.
 
     python tools/probes/phase_probe.py tools/probes/phase [M N K S ts]...
@@ -18,8 +18,8 @@ import paper_2504_19519_b200 as fo  # noqa: E402
 import synthetic  # noqa: E402
 
 NAMES = ["entry", "setup done", "1st TMA issued", "MMA 1st full", "MMA last commit", "epi last tfull",
-         "epi stores issued", "epi signalled", "epi bulk done", "exit barrier", "prod. tile known",
-         "epi c0 packed+STS", "epi c0 fenced", "epi chunk0 TMEM ld", "epi chunk0 store", "epi chunk1 read-wait"]
+         "epi stores issued", "epi signalled", "epi bulk done", "exit barrier", "barriers init'd",
+         "TMEM allocated", "thread 0 at sync"]
 
 
 def main():
@@ -44,7 +44,7 @@ def main():
             torch.cuda.synchronize()
             fo.gemm_stage_timed(p, A, Bt, C, buf)
             torch.cuda.synchronize()
-            st = buf[tiles:].view(grid, 16).cpu()
+            st = buf[tiles:].view(grid, 16)[:, :len(NAMES)].cpu()
             if it >= 2:
                 runs.append(st)
         print(f"== {M}x{N}x{K} S={S} ts={ts} tiles={tiles}" + (" (no L2 flush)" if noflush else ""))
