@@ -64,6 +64,11 @@ def patch(src):
     once("  tc_fence_before();\n  if constexpr (CG * MC == 1) __syncthreads(); else cluster_setup_sync();\n",
          "  if (threadIdx.x == 0) STAMP(12);\n"
          "  tc_fence_before();\n  if constexpr (CG * MC == 1) __syncthreads(); else cluster_setup_sync();\n")
+    # prologue: first expect_tx, first stage's loads issued
+    once("          if (leader) mbar_arrive_expect_tx(&full[s0], CG * C::STAGE_BYTES);\n",
+         "          if (s0 == 0) STAMP(13);\n          if (leader) mbar_arrive_expect_tx(&full[s0], CG * C::STAGE_BYTES);\n")
+    once("            tma_load_2d_2sm(sB + s0 * C::B_STAGE_BYTES, &tmB, s0 * BK, brow, fb);\n",
+         "            tma_load_2d_2sm(sB + s0 * C::B_STAGE_BYTES, &tmB, s0 * BK, brow, fb);\n            if (s0 == 0) STAMP(14);\n")
     return src
 
 

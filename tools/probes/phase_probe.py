@@ -19,7 +19,7 @@ import synthetic  # noqa: E402
 
 NAMES = ["entry", "setup done", "1st TMA issued", "MMA 1st full", "MMA last commit", "epi last tfull",
          "epi stores issued", "epi signalled", "epi bulk done", "exit barrier", "barriers init'd",
-         "TMEM allocated", "thread 0 at sync"]
+         "TMEM allocated", "thread 0 at sync", "prologue start", "1st stage issued"]
 
 
 def main():
