@@ -723,6 +723,158 @@ __global__ void __launch_bounds__(256) fo_combine_kernel(const CombineArgs p, in
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int CMB_SEG_COLS = SEG_CHUNKS * 8;  // columns per work unit (1024)
+constexpr int CMB_TBL_REGS = 4;               // table entries per lane: topk x tiles-per-segment <= 128
+constexpr int CMB_ASYNC_MAX_BUF = 3;          // more slots (+ residual) per unit: the register kernel
+
+// MoE combine, async-copy pipeline (R31b).  Same work unit, same
+// lane -> chunk map and the same fp32 accumulation order as fo_combine_kernel
+// (bit-identical results), but the gathers go through cp.async (LDGSTS) into a
+// per-warp, two-stage shared-memory buffer [stage][slot (+ residual)][2 KB]:
+// while unit u is accumulated from shared memory, unit u+1's k row segments
+// (and its residual) are in flight without holding registers, and unit u+2's
+// (row, weight) pairs are being loaded.  The slot -> source-row table entries a
+// unit needs (topk x tiles-per-segment) are loaded once per unit, one per lane,
+// and broadcast with shuffles, so no per-slot chain of dependent loads sits
+// on the issue path.  Each lane reads back exactly the chunks it copied, so
+// cp.async.wait_group alone orders the copy before the read.
+__global__ void __launch_bounds__(256) fo_combine_async_kernel(const CombineArgs p, int lbn, int nbuf) {
+  extern __shared__ uint4 cmb_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int64_t warps = (int64_t)gridDim.x * wpb;
+  const int64_t chunks = p.N >> 3;
+  const int64_t upr = (chunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
+  const int64_t units = p.tokens * upr;
+  const int bn_mask = p.BN - 1;
+  const int topk = p.topk;
+  const int tps = lbn >= 10 ? 1 : (CMB_SEG_COLS >> lbn);  // tile columns per unit
+  const int ents = topk * tps;
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(p.src);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(p.residual);
+  uint4* buf = cmb_smem + (int64_t)(threadIdx.x >> 5) * 2 * nbuf * SEG_CHUNKS;
+
+  // lane i < topk: slot i's receive row (-1 when dropped) and weight
+  auto load_meta = [&](int64_t uu, int& r, float& wt) {
+    r = -1;
+    wt = 0.f;
+    if (uu < units && lane < topk) {
+      const int64_t t = uu / upr;
+      r = __ldg(p.idx + t * topk + lane);
+      wt = __ldg(p.w + t * topk + lane);
+      if (r < 0 || r >= p.a2a_rows) r = -1;
+    }
+  };
+  // start unit uu's copies into stage `st` (always commits a group, possibly
+  // empty, so every lane's wait_group count stays uniform)
+  auto issue = [&](int64_t uu, int r_l, int st) {
+    if (uu < units) {
+      const int64_t t = uu / upr;
+      const int64_t c0 = (uu - t * upr) * SEG_CHUNKS;
+      const int64_t jt0 = (8 * c0) >> lbn;  // first tile column of the unit
+      int tv[CMB_TBL_REGS];
+#pragma unroll
+      for (int q = 0; q < CMB_TBL_REGS; ++q) {
+        const int e = lane + 32 * q;
+        const int slot = e / tps;
+        const int rr = __shfl_sync(0xffffffffu, r_l, slot < topk ? slot : 0);
+        const int64_t jc = jt0 + (e - slot * tps);
+        tv[q] = (e < ents && rr >= 0 && jc < p.Nt) ? __ldg(p.src_row + (int64_t)rr * p.Nt + jc) : 0;
+      }
+      uint4* sb = buf + st * nbuf * SEG_CHUNKS;
+      for (int i = 0; i < topk; ++i) {
+        const int rr = __shfl_sync(0xffffffffu, r_l, i);
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) {
+          const int64_t c = c0 + lane + 32 * k;
+          const int64_t col = 8 * c;
+          const int e = i * tps + (int)((col >> lbn) - jt0);
+          int tval = 0;
+#pragma unroll
+          for (int q = 0; q < CMB_TBL_REGS; ++q) {
+            const int v = __shfl_sync(0xffffffffu, tv[q], e & 31);
+            if (q == (e >> 5)) tval = v;
+          }
+          if (rr >= 0 && c < chunks)
+            cp_async16(sb + i * SEG_CHUNKS + lane + 32 * k, src + (int64_t)tval * p.BN + (col & bn_mask));
+        }
+      }
+      if (res) {
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) {
+          const int64_t c = c0 + lane + 32 * k;
+          if (c < chunks) cp_async16(sb + topk * SEG_CHUNKS + lane + 32 * k, res + t * p.N + 8 * c);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+  int64_t u = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+  int r_cur, r_nxt;
+  float w_cur, w_nxt;
+  load_meta(u, r_cur, w_cur);
+  issue(u, r_cur, 0);
+  load_meta(u + warps, r_nxt, w_nxt);
+  int st = 0;
+  for (; u < units; u += warps) {
+    issue(u + warps, r_nxt, st ^ 1);
+    int r_n2;
+    float w_n2;
+    load_meta(u + 2 * warps, r_n2, w_n2);
+    cp_async_wait<1>();  // this lane's copies of unit u have landed
+    const int64_t t = u / upr;
+    const int64_t c0 = (u - t * upr) * SEG_CHUNKS;
+    const uint4* sb = buf + st * nbuf * SEG_CHUNKS;
+    float acc[UNROLL][8];
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+    for (int i = 0; i < topk; ++i) {
+      const int rr = __shfl_sync(0xffffffffu, r_cur, i);
+      const float wt = __shfl_sync(0xffffffffu, w_cur, i);
+      if (rr < 0) continue;  // dropped slot
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        if (c0 + lane + 32 * k < chunks) {
+          float f[8];
+          unpack8(sb[i * SEG_CHUNKS + lane + 32 * k], f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[k][e] = fmaf(wt, f[e], acc[k][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      const int64_t c = c0 + lane + 32 * k;
+      if (c >= chunks) continue;
+      if (res) {
+        float f[8];
+        unpack8(sb[topk * SEG_CHUNKS + lane + 32 * k], f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[k][e] += f[e];
+      }
+      st_stream(out + t * p.N + 8 * c, pack8(acc[k]));
+    }
+    r_cur = r_nxt;
+    w_cur = w_nxt;
+    r_nxt = r_n2;
+    w_nxt = w_n2;
+    st ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
 }  // namespace
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
@@ -731,8 +883,27 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
   int lbn = 0;
   while ((1 << lbn) < a.BN) ++lbn;
   const int64_t units = a.tokens * ((a.N / 8 + SEG_CHUNKS - 1) / SEG_CHUNKS);
-  const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)num_sms() * 16);
-  fo_combine_kernel<<<grid, 256, 0, stream>>>(a, lbn);
+  const int tps = lbn >= 10 ? 1 : (CMB_SEG_COLS >> lbn);
+  const int nbuf = a.topk + (a.residual ? 1 : 0);
+  const int per_warp = 2 * nbuf * SEG_CHUNKS * 16;  // two stages of (topk [+1]) 2 KB segments
+  // the async pipeline needs 16 warps per SM (two 8-warp blocks) to beat the
+  // register kernel, i.e. at most three 2 KB buffers per stage: top-1/top-2
+  // (+ residual) (profiles/r02_combine_probe.txt)
+  if (nbuf <= CMB_ASYNC_MAX_BUF && a.topk * tps <= 32 * CMB_TBL_REGS) {
+    const int wpb = std::max(1, std::min(8, (112 * 1024) / per_warp));
+    const int smem = wpb * per_warp;
+    cudaError_t e = cudaFuncSetAttribute(fo_combine_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fo_combine_async_kernel, 32 * wpb, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (units + wpb - 1) / wpb;
+    const int grid = (int)std::min<int64_t>(blocks, (int64_t)num_sms() * std::max(1, occ));
+    fo_combine_async_kernel<<<grid, 32 * wpb, smem, stream>>>(a, lbn, nbuf);
+  } else {
+    const int grid = (int)std::min<int64_t>((units + 7) / 8, (int64_t)num_sms() * 16);
+    fo_combine_kernel<<<grid, 256, 0, stream>>>(a, lbn);
+  }
   count_launch();
   return cudaGetLastError();
 }

@@ -707,6 +707,43 @@ def test_moe_combine_stages(n, k, skew):
         assert _combine_close(_host(out), want2), r
 
 
+@pytest.mark.parametrize("BN,N,k", [(64, 1600, 2), (128, 1536, 3), (64, 1536, 1), (256, 4096, 2), (64, 512, 2), (128, 640, 8), (128, 640, 36)])
+def test_moe_combine_table_broadcast(BN, N, k):
+    """The combine's async-copy kernel (R31b) loads the unit's topk x
+    tiles-per-unit table entries once and broadcasts them: exercise the most
+    entries (BN=64: 16 tile columns per 1024-column unit, k=4 -> 64), a ragged
+    last unit (N % 1024), dropped slots, a residual, and k > 4 (the register
+    kernel) — each vs the oracle's combine of the A2A output at world 1."""
+    BM, K = 64, 64
+    tokens = 96
+    M = tokens * k
+    M += (-M) % BM
+    rd = np.zeros(M, np.int32)
+    A = synthetic.exact_int_A(M, K, 31, 16)
+    Bt = synthetic.exact_int_B(N, K, 32)
+    tiles = (M // BM) * (N // BN)
+    S = max(1, tiles // 3)
+    T = op.num_waves(tiles, S)
+    spec = dict(coll="alltoall", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=S, swizzle=1,
+                group_waves=[1, T - 1], row_dst=rd, ar_layout="slot")
+    plan = fo.Plan(peers=[spec], **spec)
+    ores = opl.run_alltoall([A], [Bt], [op.make_plan(M, N, BM, BN, S, [1, T - 1], swizzle=1)], [rd])
+    recv = np.concatenate([c.reshape(-1) for _, c in ores["recv"][0]])
+    rng = np.random.default_rng(BN + k)
+    idx = rng.permutation(M)[:tokens * k].astype(np.int32).reshape(tokens, k)
+    idx[::3, -1] = -1                      # dropped slots
+    idx[1::5, 0] = M + 7                   # out of range -> dropped
+    w = rng.random((tokens, k)).astype(np.float32)
+    res = synthetic.normal_bf16((tokens, N), 1.0, 11)
+    out = torch.empty(tokens, N, dtype=torch.bfloat16, device="cuda")
+    for r in (None, res):
+        args = (_dev_bf16(r),) if r is not None else ()
+        fo.combine_stage(plan, _dev_bf16(recv), out, torch.from_numpy(idx).cuda(), torch.from_numpy(w).cuda(), *args)
+        torch.cuda.synchronize()
+        want = opost.topk_combine(ores["out"][0], idx, w, residual=None if r is None else onum.to_f64(r))
+        assert _combine_close(_host(out), want), (BN, N, k, r is None)
+
+
 @pytest.mark.parametrize("layout", ["slot", "rowband"])
 def test_moe_combine_full_path_world1(ctx1, layout):
     """fo_run_combine at one rank (one expert, top-1): GEMM + A2A (local) +

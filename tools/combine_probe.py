@@ -10,6 +10,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if len(sys.argv) > 1:   # A/B: import the package from another build's root
+    sys.path.insert(0, sys.argv[1])
 
 import json  # noqa: E402
 
@@ -46,7 +48,7 @@ def main():
     fbuf = buf.view(torch.float32)
     flush_fn = lambda: fbuf.amax()  # noqa: E731
     print(f"# HBM peak {hbm:.0f} GB/s (MEASURED_PEAKS.json)", flush=True)
-    for tokens, N, k in ((4096, 4096, 2), (8192, 4096, 2), (16384, 4096, 2), (8192, 7168, 8)):
+    for tokens, N, k in ((4096, 4096, 2), (8192, 4096, 2), (16384, 4096, 2), (8192, 4096, 4), (8192, 7168, 8)):
         BM, BN = 256, 256
         rows = tokens * k                                  # one rank holding every slot's row
         rd = np.zeros(rows, np.int32)
