@@ -24,6 +24,25 @@ def main():
     res = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
     gam = torch.ones(N, dtype=torch.bfloat16, device="cuda")
     bad = 0
+    # the MoE combine (R31 / R31b): async-copy kernel (k <= 2 [+ residual]) and
+    # register kernel (k = 3 + residual, k = 5), dropped slots, ragged last unit
+    Mc, Nc = 768, 1600
+    kwc = dict(coll="alltoall", m=Mc, n=Nc, k=64, tile_m=128, tile_n=64, workers=8, swizzle=1,
+               ar_layout="slot", row_dst=np.zeros(Mc, np.int32))
+    pc = fo.Plan(rank=0, world=1, peers=[kwc], **kwc)
+    recv_c = torch.randn(Mc * Nc, device="cuda").to(torch.bfloat16)
+    for kc, with_res in ((1, False), (2, True), (2, False), (3, True), (5, False)):
+        tok = Mc // kc
+        idx_c = torch.randperm(Mc, device="cuda")[:tok * kc].to(torch.int32).view(tok, kc).contiguous()
+        idx_c[::3, -1] = -1
+        w_c = torch.rand(tok, kc, device="cuda")
+        out_c = torch.empty(tok, Nc, dtype=torch.bfloat16, device="cuda")
+        args_c = (torch.randn(tok, Nc, device="cuda").to(torch.bfloat16),) if with_res else ()
+        fo.combine_stage(pc, recv_c, out_c, idx_c, w_c, *args_c)
+    torch.cuda.synchronize()
+    if os.environ.get("SANITIZE_ONLY") == "combine":
+        print("sanitize cases done, mismatches:", bad)
+        return
     for BM in (128, 256):
         for coll in ("nocomm", "allreduce", "reducescatter", "alltoall"):
             for post in ("none", "add"):
