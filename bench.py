@@ -688,6 +688,15 @@ def main():
                                   f"GEMM alone at its best wave width (S={seqplan.info['workers']} CTA pairs"
                                   f"{', split tail' if K >= 3584 else ''}), then one NCCL AllReduce on a "
                                   "communicator with NCCL's default CTA count"),
+            # SURVEY ambiguity 17 / DESIGN R17: strict (incl. the post-communication
+            # reorder; the headline), the paper's (excl. it) and the fused op
+            "latency_conventions": {
+                "strict_us": round(ov_us, 2),
+                "paper_us": round(ov_us, 2) if plan.info["ar_layout"] == 1 else None,
+                "fused_us": round(m["ov_norm"], 2), "fused_sequential_us": round(m["seq_norm"], 2),
+                "note": ("ROWBAND plan: the AllReduce runs in place in C, no post-communication reorder exists, so "
+                         "the strict and the paper convention coincide" if plan.info["ar_layout"] == 1 else
+                         "slot plan: the per-group reorder overlaps the later groups; excluded time not separable")},
             "tflops": round(world * flops / (ov_us * 1e-6) / 1e12, 1),
             "layer_roofline_us": round(layer_roof_us, 2), "frac_of_layer_roofline": round(layer_roof_us / ov_us, 4),
             "layer_roofline": {"gemm_us": round(gemm_roof_us, 2),
