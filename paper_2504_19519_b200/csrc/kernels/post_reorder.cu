@@ -892,11 +892,21 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
   if (nbuf <= CMB_ASYNC_MAX_BUF && a.topk * tps <= 32 * CMB_TBL_REGS) {
     const int wpb = std::max(1, std::min(8, (112 * 1024) / per_warp));
     const int smem = wpb * per_warp;
-    cudaError_t e = cudaFuncSetAttribute(fo_combine_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static int attr_dev_mask = 0;  // per device bit: the dynamic-smem attribute is set (to the 112 KB cap)
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fo_combine_async_kernel, 32 * wpb, smem);
-    if (e != cudaSuccess) return e;
+    if (!(attr_dev_mask & (1 << (dev & 31)))) {
+      e = cudaFuncSetAttribute(fo_combine_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+      if (e != cudaSuccess) return e;
+      attr_dev_mask |= 1 << (dev & 31);
+    }
+    static int occ_cache[32][CMB_ASYNC_MAX_BUF + 1] = {};  // resident blocks per SM by (device, nbuf)
+    int& occ = occ_cache[dev & 31][nbuf];
+    if (occ == 0) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fo_combine_async_kernel, 32 * wpb, smem);
+      if (e != cudaSuccess) return e;
+    }
     const int64_t blocks = (units + wpb - 1) / wpb;
     const int grid = (int)std::min<int64_t>(blocks, (int64_t)num_sms() * std::max(1, occ));
     fo_combine_async_kernel<<<grid, 32 * wpb, smem, stream>>>(a, lbn, nbuf);
