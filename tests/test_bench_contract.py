@@ -51,6 +51,10 @@ def test_gpu_arm_contract():
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    lc = d["latency_conventions"]   # SURVEY ambiguity 17: strict headline, paper's, fused
+    assert lc["strict_us"] == d["value"] and lc["fused_us"] > 0
+    assert lc["paper_us"] is None or lc["paper_us"] <= lc["strict_us"]
+    assert d["perfect_overlap_bound_us"] > 0 and d["step_stats_us"]["ov"]["p10"] <= d["step_stats_us"]["ov"]["p90"]
 
 
 @pytest.mark.gpu
