@@ -303,6 +303,24 @@ def test_c2_bench_config_tp1_tail_split():
     ctx.close()
 
 
+def test_c2_bench_plan_exact():
+    """The plan bench.py's tuner picks at N=1 (profiles/r02_final_bench_n1.json:
+    256x256 CTA pairs, S=74, the auto order, one ROWBAND group — the AllReduce
+    in place in C — and the split tail), through fo_run: every element vs the
+    fp64 oracle product."""
+    M, N, K = 4096, 4096, 14336
+    A, Bt = synthetic.float_inputs(M, N, K, seed=synthetic.rank_seed(20000, 1, 0))
+    plan = fo.Plan(coll="allreduce", m=M, n=N, k=K, tile_m=BM, tile_n=BN, workers=74, group_waves=[4],
+                   swizzle=0, ar_layout="rowband", options={"tail_split": -1})
+    assert plan.info["ar_layout"] == 1
+    ctx = fo.Context.create(0, 0, 1, fo.unique_id())
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    fo.run(ctx, plan, A.cuda(), Bt.cuda(), out)
+    torch.cuda.synchronize()
+    _check_rows(out, _gemm_full(A, Bt))
+    ctx.close()
+
+
 def test_c0_two_ranks_four_groups():
     """configs[0] exactly as BASELINE.json states it: M=N=256, K=512 split over
     2 simulated ranks (K_loc=256), AllReduce, 64x64 tiles (tcgen05.mma M=64),
