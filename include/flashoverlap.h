@@ -100,7 +100,10 @@ typedef struct fo_plan_s* fo_plan;
 typedef struct {
   int32_t coll;          /* fo_coll */
   int32_t ar_layout;     /* fo_ar_layout (AllReduce, ReduceScatter, All-to-All; ignored for no-comm) */
-  int64_t m, n, k;       /* this rank's GEMM: A [m,k], Bt [n,k], C [m,n]; k = K/world for TP */
+  int64_t m, n, k;       /* this rank's GEMM: A [m,k], Bt [n,k], C [m,n]; k = K/world for TP;
+                            m = 0 only for an All-to-All source with no rows (an expert
+                            no token was routed to: no GEMM, P empty groups, whose
+                            group_waves are all 0; R45) */
   int32_t tile_m;        /* 64 or 128 (one CTA, tcgen05.mma M=64 / M=128; 64: K-major operands, no tail split)
                             or 256 (cta_group::2 CTA pair) */
   int32_t tile_n;        /* 64, 128 or 256 */
@@ -112,8 +115,9 @@ typedef struct {
                             order when that is 5% lower (and no band layout needs panels); -1 = a generalized
                             Hilbert curve over the tile grid (R44) */
   int32_t num_groups;    /* P */
-  const int32_t* group_waves; /* [P] wave counts, sum == T = ceil(tiles / S); NULL => one group */
-  const int32_t* row_dst;     /* All-to-All: [m] destination rank of each output row */
+  const int32_t* group_waves; /* [P] wave counts, sum == T = ceil(tiles / S); NULL => one group;
+                                 all 0 when m == 0 (All-to-All) */
+  const int32_t* row_dst;     /* All-to-All: [m] destination rank of each output row (may be NULL when m == 0) */
   int32_t post;          /* fo_post */
   float eps;             /* RMSNorm epsilon */
   int32_t a_mn_major;    /* 0: A is [m, k] row-major (K-major); 1: A is stored [k, m] row-major (M-major),

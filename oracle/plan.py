@@ -81,6 +81,11 @@ def group_ranges(partition, S: int, ntiles: int) -> list[tuple[int, int]]:
     [S*W_{j-1}, min(S*W_j, ntiles)) where W_j = g_1 + ... + g_j (in waves)."""
     T = num_waves(ntiles, S)
     part = [int(g) for g in partition]
+    if ntiles == 0 and part and all(g == 0 for g in part):
+        # an All-to-All source with no rows (an expert no token was routed
+        # to) still takes part in each of the P group exchanges, with empty
+        # groups (SURVEY §8(e): the same P on every rank; DESIGN.md R45)
+        return [(0, 0)] * len(part)
     if any(g < 1 for g in part) or sum(part) != T:
         raise OracleError(f"partition {part} is not a composition of T={T}")
     out = []

@@ -74,6 +74,8 @@ def rs_rowband_ok(plan: Plan) -> bool:
     (the receive buffer concatenates the groups' chunks in group order)."""
     nxt = 0
     for lo, hi in plan.ranges:
+        if lo == hi and plan.ntiles == 0:
+            continue   # an All-to-All source with no rows: empty groups, empty bands (DESIGN.md R45)
         band = rowband_of_group(plan, lo, hi)
         if band is None or band[0] != nxt:
             return False
@@ -235,7 +237,7 @@ def a2a_pre(Y: np.ndarray, plan: Plan, row_dst, n: int, layout: str = "slot") ->
     for gj, (ps, pe) in enumerate(plan.ranges):
         start = [len(s.pools[d]) for d in range(n)]
         if layout == "rowband":
-            r0, r1 = rowband_of_group(plan, ps, pe)
+            r0, r1 = rowband_of_group(plan, ps, pe) if pe > ps else (0, 0)
             for row in range(r0 * BM, r1 * BM):
                 d = int(row_dst[row])
                 for j in range(plan.Nt):

@@ -152,7 +152,11 @@ struct Grid {
 
 // O1-O3 for one descriptor (shared by self and A2A peers).
 static Grid make_grid(const fo_plan_desc& d, int world) {
-  if (d.m <= 0 || d.n <= 0 || d.k <= 0) fail(FO_ERR_SHAPE, "m, n, k must be positive");
+  // an All-to-All source with no rows (an expert rank no token was routed to)
+  // still takes part in every group's exchange: m = 0, T = 0, P empty groups
+  // (R45)
+  const bool empty_src = d.coll == FO_ALLTOALL && d.m == 0;
+  if ((d.m <= 0 && !empty_src) || d.n <= 0 || d.k <= 0) fail(FO_ERR_SHAPE, "m, n, k must be positive");
   check_tile_shape(d.tile_m, d.tile_n);
   if (d.m % d.tile_m || d.n % d.tile_n)
     fail(FO_ERR_SHAPE, "shape %lldx%lld not divisible by tile %dx%d", (long long)d.m, (long long)d.n,
@@ -173,7 +177,8 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
   g.P = (int)g.waves.size();
   long sum = 0;
   for (int w : g.waves) {
-    if (w < 1) fail(FO_ERR_INVALID_ARG, "group of %d waves (must be >= 1)", w);
+    if (g.tiles > 0 && w < 1) fail(FO_ERR_INVALID_ARG, "group of %d waves (must be >= 1)", w);
+    if (g.tiles == 0 && w != 0) fail(FO_ERR_INVALID_ARG, "a source with no rows has empty groups (0 waves each)");
     sum += w;
   }
   if (sum != g.T) fail(FO_ERR_INVALID_ARG, "group_waves sum to %ld but T=%d", sum, g.T);
@@ -184,7 +189,9 @@ static Grid make_grid(const fo_plan_desc& d, int world) {
     W += g.waves[j];
     g.gpos[j + 1] = (int32_t)std::min<long>((long)d.workers * W, g.tiles);
   }
-  if (d.tile_order) {
+  if (g.tiles == 0) {
+    g.order.clear();
+  } else if (d.tile_order) {
     g.order.assign(d.tile_order, d.tile_order + g.tiles);
     std::vector<char> seen(g.tiles, 0);
     for (int32_t t : g.order) {
@@ -357,10 +364,10 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
       break;
     }
     case FO_ALLTOALL: {
-      if (!d.row_dst) fail(FO_ERR_INVALID_ARG, "All-to-All needs row_dst");
+      if (!d.row_dst && p.M > 0) fail(FO_ERR_INVALID_ARG, "All-to-All needs row_dst");
       for (int64_t r = 0; r < p.M; ++r)
         if (d.row_dst[r] < 0 || d.row_dst[r] >= world) fail(FO_ERR_INVALID_ARG, "row_dst[%lld] out of range", (long long)r);
-      p.row_dst.assign(d.row_dst, d.row_dst + p.M);
+      if (p.M > 0) p.row_dst.assign(d.row_dst, d.row_dst + p.M);
       // ---- every source's grid (the census exchange: peers' descriptors)
       if (!peers) fail(FO_ERR_INVALID_ARG, "All-to-All needs the peers' descriptors");
       std::vector<Grid> pg(world);
@@ -369,7 +376,7 @@ PlanHost build_plan(const fo_plan_desc& d, int rank, int world, const fo_plan_de
         if (!ps) fail(FO_ERR_INVALID_ARG, "peer %d descriptor missing", s);
         if (ps->n != d.n || ps->tile_n != d.tile_n || ps->tile_m != d.tile_m)
           fail(FO_ERR_INVALID_ARG, "peer %d: n / tile shape differ", s);
-        if (!ps->row_dst) fail(FO_ERR_INVALID_ARG, "peer %d: row_dst missing", s);
+        if (!ps->row_dst && ps->m > 0) fail(FO_ERR_INVALID_ARG, "peer %d: row_dst missing", s);
         pg[s] = make_grid(*ps, world);
         if (pg[s].P != p.P) fail(FO_ERR_INVALID_ARG, "peer %d has %d groups, self %d", s, pg[s].P, p.P);
       }

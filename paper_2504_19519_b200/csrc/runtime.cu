@@ -463,6 +463,7 @@ static int epi_mode(const PlanHost& h) {
 
 static void run_gemm(fo_plan_s* p, const void* A, const void* Bt, void* dst, int mode, bool signal,
                      cudaStream_t s, unsigned long long* tile_ts = nullptr) {
+  if (p->host.tiles == 0) return;  // an All-to-All source with no rows (R45): nothing to compute or signal
   if (!A || !Bt || !dst) fail(FO_ERR_INVALID_ARG, "null device pointer");
   GemmArgs a = gemm_args(p, A, Bt, dst, mode, signal);
   if (p->swiglu && mode == EPI_ROWMAJOR) {  // FO_OPT_GEMM_SWIGLU: C is [m, n/2] = silu(gate) * up

@@ -143,57 +143,64 @@ def main(W):
                     check(f"{name}/run_host[{i}]/rank{r}", hosts[r][i], full if coll == "allreduce" else want[r])
         for p in plans:
             p.close()
-    # ---- All-to-All: imbalanced experts, random routing, same P on every rank
-    rng = np.random.default_rng(7 + W)
-    Ms = [256 * int(rng.integers(2, 5)) for _ in range(W)]   # >= 2 tile-rows: two one-row waves
-    rds = [rng.integers(0, W, size=Ms[s]).astype(np.int32) for s in range(W)]
-    inp = [synthetic.exact_inputs(Ms[s], N, K, seed=synthetic.rank_seed(71, W, s), nnz_per_row=128)
-           for s in range(W)]
-    As = [a.double().numpy() for a, _ in inp]
-    Bts = [b.double().numpy() for _, b in inp]
-    Ad = [a.cuda() for a, _ in inp]
-    Bd = [b.cuda() for _, b in inp]
-    want = opl.plain_alltoall(As, Bts, rds)
-    # the paper's subtoken pools (S = 2) and R41's rows received straight into
-    # the output (raster, one tile-row per wave)
-    for layout, S2, swz in (("slot", 2, 2), ("rowband", N // BN, 1)):
-        specs = []
-        for s in range(W):
-            T = -(-(Ms[s] // BM) * (N // BN) // S2)
-            specs.append(dict(coll="alltoall", m=Ms[s], n=N, k=K, tile_m=BM, tile_n=BN, workers=S2, swizzle=swz,
-                              group_waves=[1, T - 1], row_dst=rds[s], ar_layout=layout))
-        plans = [fo.Plan(rank=r, world=W, peers=specs, **specs[r]) for r in range(W)]
-        assert all(p.info["ar_layout"] == (1 if layout == "rowband" else 0) for p in plans)
-        print(f"[W={W}] alltoall/{layout} Ms={Ms}", flush=True)
-        for p in plans:
-            p.prepare(sequential=True)
-        outs = [torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda")
-                for p in plans]
-        torch.cuda.synchronize()
-        for _ in range(3):
-            each(lambda r: fo.run(ctxs[r], plans[r], Ad[r], Bd[r], outs[r], stream=streams[r]))
-        for r in range(W):
-            check(f"alltoall/{layout}/rank{r}", outs[r], want[r])
-        seq = [torch.full_like(o, float("nan")) for o in outs]
-        torch.cuda.synchronize()
-        each(lambda r: fo.run_sequential(ctxs[r], plans[r], Ad[r], Bd[r], seq[r], stream=streams[r]))
-        for r in range(W):
-            check(f"alltoall/{layout}/sequential/rank{r}", seq[r], want[r])
-        # the MoE combine as the post pass (R31): top-2 with weights 1 and 0
-        # over a permutation of the A2A output rows — the combined rows are the
-        # A2A rows in the permuted order, exactly (fp32 1*x + 0*y, one rounding)
-        perms = [np.random.default_rng(50 + r).permutation(p.info["out_rows"]).astype(np.int32) for r, p in
-                 enumerate(plans)]
-        idxs = [torch.from_numpy(np.stack([pm, pm[::-1].copy()], 1)).cuda() for pm in perms]
-        ws = [torch.tensor([[1.0, 0.0]], device="cuda").repeat(len(pm), 1).contiguous() for pm in perms]
-        comb = [torch.full((len(pm), N), float("nan"), dtype=torch.bfloat16, device="cuda") for pm in perms]
-        torch.cuda.synchronize()
-        for _ in range(2):
-            each(lambda r: fo.run_combine(ctxs[r], plans[r], Ad[r], Bd[r], comb[r], idxs[r], ws[r], stream=streams[r]))
-        for r in range(W):
-            check(f"alltoall/{layout}/combine/rank{r}", comb[r], want[r][perms[r]])
-        for p in plans:
-            p.close()
+    # ---- All-to-All: imbalanced experts, random routing, same P on every rank;
+    # then the same with the last expert receiving no tokens (m = 0: P empty
+    # groups, no GEMM; R45)
+    for empty in (False, True):
+        rng = np.random.default_rng(7 + W)
+        Ms = [256 * int(rng.integers(2, 5)) for _ in range(W)]   # >= 2 tile-rows: two one-row waves
+        if empty:
+            Ms[-1] = 0
+        rds = [rng.integers(0, W, size=Ms[s]).astype(np.int32) for s in range(W)]
+        inp = [synthetic.exact_inputs(max(Ms[s], 256), N, K, seed=synthetic.rank_seed(71, W, s), nnz_per_row=128)
+               for s in range(W)]
+        inp = [(a[:Ms[s]].contiguous(), b) for s, (a, b) in enumerate(inp)]
+        As = [a.double().numpy() for a, _ in inp]
+        Bts = [b.double().numpy() for _, b in inp]
+        Ad = [a.cuda() for a, _ in inp]
+        Bd = [b.cuda() for _, b in inp]
+        want = opl.plain_alltoall(As, Bts, rds)
+        # the paper's subtoken pools (S = 2) and R41's rows received straight into
+        # the output (raster, one tile-row per wave)
+        for layout, S2, swz in (("slot", 2, 2), ("rowband", N // BN, 1)):
+            specs = []
+            for s in range(W):
+                T = -(-(Ms[s] // BM) * (N // BN) // S2)
+                specs.append(dict(coll="alltoall", m=Ms[s], n=N, k=K, tile_m=BM, tile_n=BN, workers=S2, swizzle=swz,
+                                  group_waves=[1, T - 1] if T else [0, 0], row_dst=rds[s], ar_layout=layout))
+            plans = [fo.Plan(rank=r, world=W, peers=specs, **specs[r]) for r in range(W)]
+            assert all(p.info["ar_layout"] == (1 if layout == "rowband" else 0) for p in plans)
+            print(f"[W={W}] alltoall/{layout} Ms={Ms}", flush=True)
+            tag = "alltoall-empty" if empty else "alltoall"
+            for p in plans:
+                p.prepare(sequential=True)
+            outs = [torch.full((p.info["out_rows"], N), float("nan"), dtype=torch.bfloat16, device="cuda")
+                    for p in plans]
+            torch.cuda.synchronize()
+            for _ in range(3):
+                each(lambda r: fo.run(ctxs[r], plans[r], Ad[r], Bd[r], outs[r], stream=streams[r]))
+            for r in range(W):
+                check(f"{tag}/{layout}/rank{r}", outs[r], want[r])
+            seq = [torch.full_like(o, float("nan")) for o in outs]
+            torch.cuda.synchronize()
+            each(lambda r: fo.run_sequential(ctxs[r], plans[r], Ad[r], Bd[r], seq[r], stream=streams[r]))
+            for r in range(W):
+                check(f"{tag}/{layout}/sequential/rank{r}", seq[r], want[r])
+            # the MoE combine as the post pass (R31): top-2 with weights 1 and 0
+            # over a permutation of the A2A output rows — the combined rows are the
+            # A2A rows in the permuted order, exactly (fp32 1*x + 0*y, one rounding)
+            perms = [np.random.default_rng(50 + r).permutation(p.info["out_rows"]).astype(np.int32) for r, p in
+                     enumerate(plans)]
+            idxs = [torch.from_numpy(np.stack([pm, pm[::-1].copy()], 1)).cuda() for pm in perms]
+            ws = [torch.tensor([[1.0, 0.0]], device="cuda").repeat(len(pm), 1).contiguous() for pm in perms]
+            comb = [torch.full((len(pm), N), float("nan"), dtype=torch.bfloat16, device="cuda") for pm in perms]
+            torch.cuda.synchronize()
+            for _ in range(2):
+                each(lambda r: fo.run_combine(ctxs[r], plans[r], Ad[r], Bd[r], comb[r], idxs[r], ws[r], stream=streams[r]))
+            for r in range(W):
+                check(f"{tag}/{layout}/combine/rank{r}", comb[r], want[r][perms[r]])
+            for p in plans:
+                p.close()
     for c in ctxs:
         c.close()
     grp.close()

@@ -135,22 +135,34 @@ def test_reducescatter_schedule(world, layout):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("routing", ["random", "sorted", "skewed"])
+@pytest.mark.parametrize("routing", ["random", "sorted", "skewed", "empty_expert"])
 @pytest.mark.parametrize("layout", ["slot", "rowband"])
 def test_alltoall_schedule(world, routing, layout):
-    rng = np.random.default_rng(300 + world + {"random": 0, "sorted": 50, "skewed": 90}[routing])
+    """empty_expert: the last source (and the first, at world >= 3) has no rows
+    — an expert no token was routed to — and takes part with P empty groups
+    (R45)."""
+    if routing == "empty_expert" and world == 1:
+        pytest.skip("needs a peer")
+    rng = np.random.default_rng(300 + world + {"random": 0, "sorted": 50, "skewed": 90, "empty_expert": 130}[routing])
     for _ in range(6):
         BM = int(rng.choice([128, 256]))
         BN = int(rng.choice([64, 128]))
         N = BN * int(rng.integers(1, 4))
         Ms = [BM * int(rng.integers(1, 4)) for _ in range(world)]          # imbalanced experts
+        if routing == "empty_expert":
+            Ms[-1] = 0
+            if world >= 3:
+                Ms[0] = 0
         S = int(rng.integers(1, 3))
         if layout == "rowband":
             S = N // BN      # raster, one tile-row per wave: ascending bands on every source (R41)
         Ts = [-(-(m // BM) * (N // BN) // S) for m in Ms]
-        P = int(rng.integers(1, min(Ts) + 1))                             # a common number of groups
+        P = int(rng.integers(1, min(t for t in Ts if t) + 1))             # a common number of groups
         parts = []
         for T in Ts:
+            if T == 0:
+                parts.append([0] * P)
+                continue
             cuts = sorted(rng.choice(np.arange(1, T), size=P - 1, replace=False).tolist()) if P > 1 else []
             b = [0] + cuts + [T]
             parts.append([y - x for x, y in zip(b[:-1], b[1:])])
@@ -160,8 +172,10 @@ def test_alltoall_schedule(world, routing, layout):
                 rd = rng.integers(0, world, size=Ms[s])
             elif routing == "skewed":
                 rd = np.minimum(rng.geometric(0.6, size=Ms[s]) - 1, world - 1)
-            else:
+            elif routing == "sorted":
                 rd = np.sort(rng.integers(0, world, size=Ms[s]))
+            else:
+                rd = rng.integers(0, world, size=Ms[s])
             rds.append(rd.astype(np.int32))
         swz = [1 if layout == "rowband" else 1 + s % 2 for s in range(world)]
         specs = [dict(coll="alltoall", m=Ms[s], n=N, k=64, tile_m=BM, tile_n=BN, workers=S, swizzle=swz[s],

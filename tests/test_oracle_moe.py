@@ -64,3 +64,32 @@ def test_combine_gather_and_dropped_slots():
     # k = 1, w = 1: a pure row gather
     perm = np.array([[3], [1], [0], [2]])
     assert np.array_equal(post.topk_combine(x, perm, np.ones((4, 1))), x[perm[:, 0]])
+
+
+def test_a2a_with_a_source_without_rows():
+    """An expert rank no token was routed to (m = 0, R45): with P
+    empty groups the overlapped A2A delivers exactly the plain all-to-all-v
+    rows (the definition, oracle.pipeline.plain_alltoall) at every receiver;
+    a partition of empty groups is only legal when there are no tiles."""
+    n, N, K, BM, BN = 3, 256, 64, 128, 128
+    Ms = [256, 0, 384]
+    rng = np.random.default_rng(0)
+    As, Bts, plans, rds = [], [], [], []
+    for s in range(n):
+        A, Bt = synthetic.exact_inputs(max(Ms[s], 1), N, K, seed=5 + s, nnz_per_row=32)
+        A = A[:Ms[s]]
+        rd = rng.integers(0, n, Ms[s]).astype(np.int32)
+        tiles = (Ms[s] // BM) * (N // BN)
+        part = [0, 0] if tiles == 0 else [1, op.num_waves(tiles, 2) - 1]
+        plans.append(op.make_plan(Ms[s], N, BM, BN, 2, part))
+        As.append(A), Bts.append(Bt), rds.append(rd)
+    res = pipeline.run_alltoall(As, Bts, plans, rds)
+    plain = pipeline.plain_alltoall(As, Bts, rds)
+    for d in range(n):
+        assert res["out"][d].shape[0] == sum(int((rd == d).sum()) for rd in rds)
+        assert np.array_equal(res["out"][d], plain[d])
+    assert res["send"][1].ranges == [[(0, 0), (0, 0)]] * n
+    with pytest.raises(op.OracleError):
+        op.group_ranges([0, 1], 2, 4)          # empty groups beside tiles
+    with pytest.raises(op.OracleError):
+        op.group_ranges([1, 0], 2, 0)          # waves without tiles

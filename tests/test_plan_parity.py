@@ -343,3 +343,52 @@ def test_binding_enums_match_header():
     post = {"none": "FO_POST_NONE", "add": "FO_POST_ADD", "add_rmsnorm": "FO_POST_ADD_RMSNORM",
             "add_rmsnorm_res": "FO_POST_ADD_RMSNORM_RESIDUAL"}
     assert {post[k]: v for k, v in _lib.POST.items()} == enum("fo_post")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("layout", ["slot", "auto"])
+def test_alltoall_source_without_rows(world, layout):
+    """An expert rank no token was routed to (m = 0, R45) takes part
+    with P empty groups: its send side is empty, its receive map and the
+    per-(group, peer) counts of every rank match the oracle's."""
+    rng = np.random.default_rng(77 + world)
+    BN, N, P = 128, 256, 2
+    Ms = [256, 0, 384][:world]
+    specs, oplans, rds = [], [], []
+    for s in range(world):
+        tiles = (Ms[s] // 128) * (N // BN)
+        S = N // BN if layout == "auto" else 2
+        part = [0] * P if Ms[s] == 0 else [1, op.num_waves(tiles, S) - 1]
+        rd = rng.integers(0, world, Ms[s]).astype(np.int32)
+        specs.append(dict(coll="alltoall", m=Ms[s], n=N, k=64, tile_m=128, tile_n=BN, workers=S, swizzle=1,
+                          group_waves=part, row_dst=rd, ar_layout=layout))
+        oplans.append(op.make_plan(Ms[s], N, 128, BN, S, part, swizzle=1))
+        rds.append(rd)
+    lay = "rowband" if layout == "auto" and orr.a2a_rowband_ok(oplans) else "slot"
+    sends = [orr.a2a_pre(np.arange(oplans[s].M * N, dtype=float).reshape(-1, N), oplans[s], rds[s], world, lay)
+             for s in range(world)]
+    recv = oc.alltoall_groups(sends, P)
+    for me in range(world):
+        pl = fo.Plan(rank=me, world=world, peers=specs, **specs[me])
+        assert pl.info["ar_layout"] == (1 if lay == "rowband" else 0)
+        assert pl.info["waves"] == oplans[me].T and pl.info["num_groups"] == P
+        sc, rc = pl.export_a2a_counts()
+        for j in range(P):
+            for d in range(world):
+                a, b = sends[me].ranges[d][j]
+                assert sc[j, d] == b - a
+                a, b = sends[d].ranges[me][j]
+                assert rc[j, d] == b - a
+        if Ms[me] == 0:
+            assert pl.info["send_elems"] == 0 and sc.sum() == 0
+        rows = sum(int((rds[s] == me).sum()) for s in range(world))
+        assert pl.info["out_rows"] == rows
+        if lay == "rowband":
+            assert np.array_equal(pl.export_recv_map(), np.arange(rows * N))
+            continue
+        parts, idx = [], 0
+        for s, chunk in recv[me]:
+            parts.append((s, np.arange(idx * BN, (idx + len(chunk)) * BN, dtype=float).reshape(-1, BN)))
+            idx += len(chunk)
+        post = orr.a2a_post(parts, [sends[s].meta[me] for s in range(world)], rds, me, N, BN)
+        assert np.array_equal(pl.export_recv_map(), post.reshape(-1).astype(np.int64))
