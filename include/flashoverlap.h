@@ -364,7 +364,8 @@ fo_status fo_combine_stage(fo_plan plan, const void* recv, void* out, const int3
  *   out: device bf16 [info.out_rows, info.out_cols]:
  *     AR  -> [m, n] row-major, identical on every rank;
  *     RS  -> [m/world, n]: local row l = global row floor(l/h)*tile_m + rank*h + l%h (h = tile_m/world);
- *     A2A -> [sum_s cnt(s->rank), n]: rows grouped by source rank ascending, then source row ascending;
+ *     A2A -> [sum_s cnt(s->rank), n]: rows grouped by source rank ascending, then source row ascending
+ *       (may be NULL when no row is routed to this rank; A and Bt may be NULL when m == 0, R45);
  *     NOCOMM -> [m, n].
  *   residual (FO_POST_ADD*): device bf16, same shape as out; gamma (RMSNorm): device bf16 [n].
  * Internals: counters reset, GEMM on the caller stream, per group a

@@ -916,8 +916,12 @@ static void group_d2h(fo_ctx c, fo_plan p, int j, const void* out, cudaStream_t 
 fo_status fo_run(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
                  const void* gamma, void* stream) {
   return guard([&] {
-    if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (!c || !p) fail(FO_ERR_INVALID_ARG, "null argument");
     const PlanHost& h = p->host;
+    // an All-to-All rank that receives no rows (or a combine with no tokens)
+    // has an empty output and may pass NULL (R45)
+    if (!out && !(h.coll == FO_ALLTOALL && (p->combine ? p->combine->tokens == 0 : h.out_rows == 0)))
+      fail(FO_ERR_INVALID_ARG, "null argument");
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
     if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
     bind_ctx(c, p);
@@ -1168,7 +1172,8 @@ fo_status fo_run_host(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* 
 fo_status fo_run_sequential(fo_ctx c, fo_plan p, const void* A, const void* Bt, void* out, const void* residual,
                             const void* gamma, void* stream) {
   return guard([&] {
-    if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (!c || !p) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (!out && !(p->host.coll == FO_ALLTOALL && p->host.out_rows == 0)) fail(FO_ERR_INVALID_ARG, "null argument");
     if (c->aborted) fail(FO_ERR_STATE, "context aborted by the watchdog (fo_plan_sync timed out)");
     const PlanHost& h = p->host;
     if (h.world != c->world || h.rank != c->rank) fail(FO_ERR_STATE, "plan rank/world do not match the context");
@@ -1352,7 +1357,7 @@ fo_status fo_run_combine(fo_ctx c, fo_plan p, const void* A, const void* Bt, voi
     ~Transient() { p->combine = nullptr; }
   };
   return guard([&] {
-    if (!c || !p || !out) fail(FO_ERR_INVALID_ARG, "null argument");
+    if (!c || !p || (!out && tokens > 0)) fail(FO_ERR_INVALID_ARG, "null argument");
     ensure_device(p);
     const CombineArgs ca = combine_args(p, nullptr, out, idx, w, topk, tokens, residual);
     Transient t{p};

@@ -145,13 +145,14 @@ def main(W):
             p.close()
     # ---- All-to-All: imbalanced experts, random routing, same P on every rank;
     # then the same with the last expert receiving no tokens (m = 0: P empty
-    # groups, no GEMM; R45)
+    # groups, no GEMM) and rank 0 receiving no rows (R45)
     for empty in (False, True):
         rng = np.random.default_rng(7 + W)
         Ms = [256 * int(rng.integers(2, 5)) for _ in range(W)]   # >= 2 tile-rows: two one-row waves
         if empty:
             Ms[-1] = 0
-        rds = [rng.integers(0, W, size=Ms[s]).astype(np.int32) for s in range(W)]
+        # the empty variant also routes no row to rank 0: an empty output (NULL out)
+        rds = [rng.integers(1 if empty else 0, W, size=Ms[s]).astype(np.int32) for s in range(W)]
         inp = [synthetic.exact_inputs(max(Ms[s], 256), N, K, seed=synthetic.rank_seed(71, W, s), nnz_per_row=128)
                for s in range(W)]
         inp = [(a[:Ms[s]].contiguous(), b) for s, (a, b) in enumerate(inp)]
