@@ -195,20 +195,21 @@ def a2a_wave_bytes(specs: list, elem_bytes: int = 2):
 
     n = len(specs)
     out = []
-    Ts = set()
+
+    def waves(s):
+        return -(-(s["m"] // s["tile_m"]) * (s["n"] // s["tile_n"]) // s["workers"])
+    # experts with no rows (m = 0, R45) send nothing in every wave
+    Ts = {waves(s) for s in specs if s["m"] > 0}
+    if len(Ts) > 1:
+        raise ValueError("imbalance-aware search needs a common wave count (pad experts to a common tile count)")
+    Tc = Ts.pop() if Ts else 0
+    per_wave = [dict(s, group_waves=[1] * Tc if s["m"] > 0 else [0] * Tc) for s in specs]
     for r, sp in enumerate(specs):
-        tiles = (sp["m"] // sp["tile_m"]) * (sp["n"] // sp["tile_n"])
-        T = -(-tiles // sp["workers"])
-        Ts.add(T)
-        per_wave = [dict(s, group_waves=[1] * (-(-(s["m"] // s["tile_m"]) * (s["n"] // s["tile_n"]) // s["workers"])))
-                    for s in specs]
         plan = Plan(rank=r, world=n, peers=per_wave, **per_wave[r])
         sc, _ = plan.export_a2a_counts()          # [T, n] subtokens per (wave, destination)
         sc = sc.astype(np.float64)
         sc[:, r] = 0.0                            # the self part is a local copy
         out.append((sc.sum(axis=1) * sp["tile_n"] * elem_bytes).tolist())
-    if len(Ts) != 1:
-        raise ValueError("imbalance-aware search needs a common wave count (pad experts to a common tile count)")
     return out
 
 

@@ -93,3 +93,31 @@ def test_effective_curve_adds_post_cost():
         t = b / (bw * 1e9) * 1e6
         te = b / (ebw * 1e9) * 1e6
         assert te == pytest.approx(t + 2.0 + 1e-5 * b)
+
+
+def test_tune_alltoall_with_an_expert_without_rows():
+    """An expert with no rows (m = 0, R45) sends nothing in every
+    wave and takes duration 0; the common partition is the search over the
+    other experts' waves, equal to the oracle's multi-rank Alg. 1."""
+    import numpy as np
+
+    from oracle import alg1
+    from paper_2504_19519_b200 import build
+
+    build.build()
+    n, N = 3, 256
+    rng = np.random.default_rng(1)
+    specs = []
+    for r in range(n):
+        m = 0 if r == 1 else 512
+        specs.append(dict(coll="alltoall", m=m, n=N, k=64, tile_m=128, tile_n=128, workers=2,
+                          row_dst=rng.integers(0, n, size=m).astype(np.int32)))
+    wb = tuner.a2a_wave_bytes(specs)
+    assert [len(w) for w in wb] == [4, 4, 4] and sum(wb[1]) == 0
+    for r in (0, 2):
+        assert sum(wb[r]) == int((specs[r]["row_dst"] != r).sum()) * N * 2
+    curve = [(2 ** 12, 5.0), (2 ** 20, 100.0), (2 ** 26, 400.0)]
+    durs = [50.0, 0.0, 80.0]
+    G, t = tuner.tune_alltoall(specs, durs, curve)
+    lat = lambda b: alg1.interp_latency_us(curve, b)
+    assert t == pytest.approx(alg1.search_multi(4, durs, wb, lat)[1], rel=1e-12)
