@@ -12,6 +12,8 @@
 // Reads are 16-byte vector loads (consecutive lanes read consecutive chunks of
 // a BN-wide contiguous run), writes are fully coalesced row segments, so the
 // kernel is HBM-bound at 2 x bytes(out) (+ residual).
+#include <atomic>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -531,14 +533,18 @@ __global__ void fo_fill_u16_kernel(uint16_t* dst, int64_t n, uint16_t v) {
     dst[i] = v;
 }
 
+// Host-side per-device caches below are written by whichever thread gets
+// there first (the loopback backend issues every rank from its own thread);
+// each value is idempotent, so relaxed atomics suffice.
 int num_sms() {
-  static int cache[64] = {0};  // per device
+  static std::atomic<int> cache[64];  // per device
   int dev = 0;
   cudaGetDevice(&dev);
-  int& n = cache[dev & 63];
+  int n = cache[dev & 63].load(std::memory_order_relaxed);
   if (!n) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (!n) n = 148;
+    cache[dev & 63].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -549,18 +555,17 @@ int num_sms() {
 // current row instead of the block retiring after one row.
 template <int MAP, int MAXC, int THREADS, bool RES>
 int resident_grid(int smem) {
-  static int cache[64][2];  // [device][smem != 0] -> blocks per SM
+  static std::atomic<int> cache[64][2];  // [device][smem != 0] -> blocks per SM
   int dev = 0;
   cudaGetDevice(&dev);
-  int& v = cache[dev & 63][smem != 0];
+  int v = cache[dev & 63][smem != 0].load(std::memory_order_relaxed);
   if (!v) {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fo_post_rmsnorm_kernel<MAP, MAXC, THREADS, RES>, THREADS,
-                                                      smem) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fo_post_rmsnorm_kernel<MAP, MAXC, THREADS, RES>, THREADS,
+                                                      smem) != cudaSuccess || v < 1) {
       cudaGetLastError();
-      n = 1;
+      v = 1;
     }
-    v = n;
+    cache[dev & 63][smem != 0].store(v, std::memory_order_relaxed);
   }
   return v * num_sms();
 }
@@ -574,15 +579,15 @@ bool launch_rmsnorm_bulk_cpt(const PostArgs& a, int lbn, cudaStream_t stream) {
   const int stages = (int)std::max<size_t>(2, std::min<size_t>(4, (100u << 10) / slot));
   const int smem = (int)(stages * slot + stages * 8 + 2 * 8 * sizeof(float));
   auto kern = fo_post_rmsnorm_bulk_kernel<MAP, CPT, RES>;
-  static int attr_dev_mask = 0;  // per device bit: the dynamic-smem attribute is set
+  static std::atomic<int> attr_dev_mask{0};  // per device bit: the dynamic-smem attribute is set
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!(attr_dev_mask & (1 << (dev & 31)))) {
+  if (!(attr_dev_mask.load(std::memory_order_relaxed) & (1 << (dev & 31)))) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10) != cudaSuccess) {
       cudaGetLastError();
       return false;
     }
-    attr_dev_mask |= 1 << (dev & 31);
+    attr_dev_mask.fetch_or(1 << (dev & 31), std::memory_order_relaxed);
   }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BULK_THREADS, smem) != cudaSuccess || per_sm < 1) {
@@ -892,20 +897,21 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
   if (nbuf <= CMB_ASYNC_MAX_BUF && a.topk * tps <= 32 * CMB_TBL_REGS) {
     const int wpb = std::max(1, std::min(8, (112 * 1024) / per_warp));
     const int smem = wpb * per_warp;
-    static int attr_dev_mask = 0;  // per device bit: the dynamic-smem attribute is set (to the 112 KB cap)
+    static std::atomic<int> attr_dev_mask{0};  // per device bit: the dynamic-smem attribute is set (112 KB cap)
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (!(attr_dev_mask & (1 << (dev & 31)))) {
+    if (!(attr_dev_mask.load(std::memory_order_relaxed) & (1 << (dev & 31)))) {
       e = cudaFuncSetAttribute(fo_combine_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
       if (e != cudaSuccess) return e;
-      attr_dev_mask |= 1 << (dev & 31);
+      attr_dev_mask.fetch_or(1 << (dev & 31), std::memory_order_relaxed);
     }
-    static int occ_cache[32][CMB_ASYNC_MAX_BUF + 1] = {};  // resident blocks per SM by (device, nbuf)
-    int& occ = occ_cache[dev & 31][nbuf];
+    static std::atomic<int> occ_cache[32][CMB_ASYNC_MAX_BUF + 1];  // resident blocks per SM by (device, nbuf)
+    int occ = occ_cache[dev & 31][nbuf].load(std::memory_order_relaxed);
     if (occ == 0) {
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fo_combine_async_kernel, 32 * wpb, smem);
       if (e != cudaSuccess) return e;
+      occ_cache[dev & 31][nbuf].store(occ, std::memory_order_relaxed);
     }
     const int64_t blocks = (units + wpb - 1) / wpb;
     const int grid = (int)std::min<int64_t>(blocks, (int64_t)num_sms() * std::max(1, occ));
