@@ -21,6 +21,20 @@ def test_loopback_world(world):
     # eager module loading: a lazily loaded kernel's first launch may wait for
     # running kernels, i.e. for another in-process rank's call at its barrier
     env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "loopback_worker.py"), str(world)], cwd=ROOT,
-                       env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0 and f"loopback W={world}: OK" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
+    # W ranks on ONE GPU wait on each other's kernels: a rank's spinning
+    # barrier blocks can hold SMs that a peer rank's persistent GEMM (whose
+    # split-tail slices wait for each other) needs, so now and then a barrier
+    # times out with an arrival count short of its target although every rank
+    # issued the same calls (the loopback traps instead of hanging).  That
+    # scheduling artefact of the single-GPU stand-in is retried; a real
+    # schedule mismatch (wrong pairing, count or order) fails every attempt,
+    # and any numerical mismatch fails at once.
+    for attempt in range(3):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "loopback_worker.py"), str(world)],
+                           cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+        ok = r.returncode == 0 and f"loopback W={world}: OK" in r.stdout
+        co_residency = "barrier arrive counter" in r.stdout + r.stderr and "MISMATCH" not in r.stdout
+        if ok or not co_residency:
+            break
+        print(f"loopback W={world}: barrier timeout on attempt {attempt} (co-residency), retrying", flush=True)
+    assert ok, r.stdout[-4000:] + r.stderr[-4000:]
